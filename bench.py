@@ -1,0 +1,325 @@
+#!/usr/bin/env python
+"""Benchmark of the multigrid V-cycle hot path (BASELINE.json metric:
+"smoother grid-pt updates/s; V-cycle time to 1e-10 residual; % HBM roofline").
+
+Default workload (N=1): BASELINE config 3 -- 8193^2 nodes, tanh wall grid
+gamma=4, 16-Gaussian RHS (seed 2), tweed smoother, V(2,2), full weighting.
+A step is one V(2,2) cycle over the whole hierarchy (13 levels) with u and f
+resident in HBM.  value = smoother grid-point updates per second,
+(nu1 + nu2) * sum over levels of interior points per cycle / cycle time.
+
+Also reported: the dominant kernel's roofline (one finest-level tweed sweep =
+the block-solver launches of both colours, 24 B per interior point
+algorithmic), the end-to-end number through the public API with pinned host
+buffers copied in and out every step, and the CPU oracle (C restatement of
+the reference, 1 core) on one V-cycle of the same workload.
+
+`--impl reference` times the reference algorithm's CPU path (the oracle port,
+all host threads) on the same workload and metric.  Under torchrun (N>1) every
+rank runs an independent replica (weak scaling; the hot path is not sharded in
+this round), timed on the device and reduced with max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import csv
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0
+
+
+def _peak_hbm():
+    try:
+        with open(PEAKS) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        with open(self.path) as fh:
+            for r in csv.reader(fh):
+                if len(r) >= 9:
+                    rows.append([x.strip() for x in r])
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def _updates_per_cycle(h, nu):
+    return nu * sum((lv.nx - 1) * (lv.ny - 1) for lv in h.levels)
+
+
+def _workload_desc(w):
+    return (f"{w.name}: {w.n + 1}^2 nodes fp64, "
+            + {"config1": "tanh wall c=3, f~U[-1,1) seed 0",
+               "config2": "sinh centre gamma=3, f~U[-1,1) seed 1",
+               "config3": "tanh wall gamma=4, 16 Gaussians seed 2"}[w.name]
+            + f", {w.smoother} V({w.nu1},{w.nu2}), full weighting, bilinear")
+
+
+def cpu_oracle_cycle(w, f, nthreads):
+    """One V-cycle of the workload through the CPU oracle; returns seconds."""
+    from oracle import oracle as orc
+    H = orc.Hierarchy(w.x.values, w.x.values)
+    u = np.zeros_like(f)
+    t0 = time.perf_counter()
+    orc.v_cycle(H, u, f, smoother=w.smoother, nu1=w.nu1, nu2=w.nu2, nthreads=nthreads)
+    return time.perf_counter() - t0, u
+
+
+def run_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return
+    from oracle import oracle as orc
+    from paper_2110_08389_b200 import configs, grid
+    w = configs.workload(args.config, n=args.n, nu=args.nu)
+    h = grid.build_hierarchy(w.x, w.x)
+    f = w.rhs()
+    cores = orc.max_threads()
+    for _ in range(args.warmup):
+        cpu_oracle_cycle(w, f, cores)
+    times = [cpu_oracle_cycle(w, f, cores)[0] for _ in range(args.steps)]
+    per = float(np.mean(times))
+    value = _updates_per_cycle(h, w.nu1 + w.nu2) / per
+    sample = f"one V({w.nu1},{w.nu2}) cycle of {args.config} per step, {cores} OpenMP threads"
+    line = {
+        "impl": "reference", "metric": "smoother grid-pt updates/s", "value": value,
+        "unit": "grid-pt updates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": _workload_desc(w)},
+        "cpu_baseline": {"value": value, "unit": "grid-pt updates/s", "cores": cores,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "grid-pt updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+
+    from paper_2110_08389_b200 import _lib, configs, grid, mgcycle
+    from paper_2110_08389_b200.stencil import native_level
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    w = configs.workload(args.config, n=args.n, nu=args.nu)
+    h = grid.build_hierarchy(w.x, w.x)
+    cfg = mgcycle.CycleConfig(smoother=w.smoother, nu1=w.nu1, nu2=w.nu2)
+    f_host = w.rhs()
+    fd = torch.from_numpy(f_host).cuda()
+    u = torch.zeros_like(fd)
+    L = _lib.lib()
+    state = mgcycle._CycleState(h)
+    kind, full, nu1, nu2 = mgcycle._cfg_args(cfg)
+    stream = torch.cuda.current_stream()
+    import ctypes
+    sh = ctypes.c_void_p(stream.cuda_stream)
+    up = ctypes.c_void_p(u.data_ptr())
+    fp = ctypes.c_void_p(fd.data_ptr())
+
+    def cycles(k):
+        _lib.check(L.tmg_vcycle_graph(state.native, kind, full, nu1, nu2, up, fp, k, sh))
+
+    for _ in range(max(args.warmup, 3)):
+        cycles(1)
+    torch.cuda.synchronize()
+    for lv in h.levels:
+        _lib.check(L.tmg_level_check(native_level(lv.stencil), sh))
+    kernels_per_cycle = L.tmg_hier_graph_kernels(state.native)
+
+    clk = ClockSampler(local)
+    clk.start()
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < 1.0:  # clocks settle; sampler covers the timed region
+        cycles(20)
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    cycles(args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    t_ms = max_over_ranks(e0.elapsed_time(e1))
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < 0.4:
+        cycles(20)
+        torch.cuda.synchronize()
+    clocks = clk.stop()
+
+    upc = _updates_per_cycle(h, w.nu1 + w.nu2)
+    ms_per_step = t_ms / args.steps
+    value = world * upc * args.steps / (t_ms * 1e-3)
+
+    # dominant kernel: one finest-level sweep (both colour stages), timed alone
+    fine = native_level(h.finest.stencil)
+    reps = 20
+    for _ in range(3):
+        _lib.check(L.tmg_sweep(fine, kind, up, fp, sh))
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(reps):
+        _lib.check(L.tmg_sweep(fine, kind, up, fp, sh))
+    s1.record(stream)
+    torch.cuda.synchronize()
+    sweep_ms = s0.elapsed_time(s1) / reps
+    n_int = (h.finest.nx - 1) * (h.finest.ny - 1)
+    alg_bytes = 24.0 * n_int
+    peak, peak_kind = _peak_hbm()
+    achieved = alg_bytes / (sweep_ms * 1e-3) / 1e9
+
+    # end to end through the public API: pinned host u, f in; u out; every step
+    u_h = torch.zeros(fd.shape, dtype=torch.float64).pin_memory()
+    f_h = torch.from_numpy(f_host).pin_memory()
+    ue = torch.empty_like(fd)
+    fe = torch.empty_like(fd)
+    e2e_steps = max(1, min(args.steps, 5))
+    for phase in ("warm", "timed"):
+        if phase == "timed":
+            barrier()
+            torch.cuda.synchronize()
+            x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            x0.record(stream)
+        for _ in range(1 if phase == "warm" else e2e_steps):
+            fe.copy_(f_h, non_blocking=True)
+            ue.copy_(u_h, non_blocking=True)
+            mgcycle.v_cycle(h, cfg, ue, fe, _state=state, check=False)
+            u_h.copy_(ue, non_blocking=True)
+        if phase == "timed":
+            x1.record(stream)
+            torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(x0.elapsed_time(x1)) / e2e_steps
+    field_bytes = fd.numel() * 8
+    e2e = {"value": world * upc / (e2e_ms * 1e-3), "unit": "grid-pt updates/s",
+           "h2d_bytes_per_step": 2 * field_bytes, "d2h_bytes_per_step": field_bytes,
+           "ms_per_step": e2e_ms}
+
+    line = {
+        "metric": "smoother grid-pt updates/s", "value": value, "unit": "grid-pt updates/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": _workload_desc(w), "levels": len(h.levels),
+                   "updates_per_cycle": upc, "vcycle_ms": ms_per_step,
+                   "l2": "inputs larger than L2 (u, f = 2 x %.0f MB)" % (field_bytes / 1e6),
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "block_sweep_kernel (one finest-level sweep, both colours)",
+                     "alg_bytes": alg_bytes, "ms": sweep_ms, "peak_kind": peak_kind},
+        "sweep_updates_per_s": n_int / (sweep_ms * 1e-3),
+        "e2e": e2e,
+        "clocks": clocks,
+        "gpu_launches": kernels_per_cycle * args.steps,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        secs, _ = cpu_oracle_cycle(w, f_host, 1)
+        line["cpu_baseline"] = {
+            "value": upc / secs, "unit": "grid-pt updates/s", "cores": 1, "kind": "port",
+            "sample": f"one V({w.nu1},{w.nu2}) cycle of the same workload, C oracle, 1 thread "
+                      f"({secs:.1f} s)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--config", default="config3", choices=("config1", "config2", "config3"))
+    p.add_argument("--n", type=int, default=None, help="override grid intervals")
+    p.add_argument("--nu", type=int, default=2, help="config3: V(nu,nu)")
+    p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = p.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

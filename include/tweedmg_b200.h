@@ -1,0 +1,135 @@
+/*
+ * tweedmg_b200.h -- C ABI of the B200-native multigrid V-cycle hot path.
+ *
+ * Drop-in boundary for the reference `tweedmg` package (arXiv 2110.08389).
+ * Every entry point is extern "C", takes plain pointers and sizes (device
+ * pointers for fields, a cudaStream_t passed as void*), is stream-ordered
+ * unless it says "synchronizes", and returns an int status:
+ *
+ *   TMG_OK        0
+ *   TMG_SINGULAR  1  vanishing pivot |p| < 1e-300; the reference raises
+ *                    SingularSystemError(ValueError)  (tridiag.py:17-27,
+ *                    _ckernels.pyx:11-18)
+ *   TMG_BADARG    2  shape / kind / size error; the reference raises
+ *                    ValueError (smoothers.py:134-137, stencil.py:70-73,
+ *                    transfer.py:13-17, layout.py:50-52)
+ *   TMG_CUDA      3  CUDA runtime error
+ *
+ * tmg_last_error() returns the message of the last failure on the calling
+ * thread.  Fields are fp64, C-order (nx+1) x (ny+1), u[i*(ny+1)+j]
+ * (stencil.py:12-15).  Coefficients W, E (length nx+1) and S, N (ny+1) are
+ * the stencil.assemble arrays (stencil.py:48-67).  Handles are bound to the
+ * device current at creation and must not be shared across host threads.
+ */
+#ifndef TWEEDMG_B200_H
+#define TWEEDMG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TMG_OK 0
+#define TMG_SINGULAR 1
+#define TMG_BADARG 2
+#define TMG_CUDA 3
+
+/* smoother kinds, smoothers.py:18-22 order */
+#define TMG_CHECKERBOARD 0
+#define TMG_ZEBRA_X 1
+#define TMG_ZEBRA_Y 2
+#define TMG_ZEBRA_ALT 3
+#define TMG_TWEED 4
+#define TMG_WIREFRAME 5
+#define TMG_TWEED_WIRE_ALT 6
+
+typedef struct tmg_level tmg_level; /* grid level: coefficients, plans, workspace */
+typedef struct tmg_hier tmg_hier;   /* V-cycle hierarchy over levels */
+
+const char* tmg_last_error(void);
+int tmg_version(void);
+
+/* ---- levels: grid.Level + stencil.StencilCoeffs (grid.py:105-135,
+ *      stencil.py:25-67).  W, E, S, N are HOST arrays, copied to the device. */
+int tmg_level_create(int nx, int ny, const double* W, const double* E, const double* S,
+                     const double* N, tmg_level** out);
+int tmg_level_destroy(tmg_level* lv);
+/* bytes of device memory held by the level (coefficients + plans) */
+long long tmg_level_device_bytes(tmg_level* lv);
+/* read and clear the level's device error flags; synchronizes `stream` */
+int tmg_level_check(tmg_level* lv, void* stream);
+
+/* ---- smoother: smoothers.sweep (smoothers.py:121-150), in place on u */
+int tmg_sweep(tmg_level* lv, int kind, double* u, const double* f, void* stream);
+/* one colour stage (red = 1 first, black = 0), test_smoothers.py:27-39 */
+int tmg_sweep_colour(tmg_level* lv, int kind, int red, double* u, const double* f,
+                     void* stream);
+
+/* ---- stencil.apply / stencil.defect (stencil.py:76-96) */
+int tmg_apply(tmg_level* lv, const double* u, double* out, void* stream);
+int tmg_defect(tmg_level* lv, const double* u, const double* f, double* d, void* stream);
+/* max over the interior of |f - L u| (mgcycle.py:122,130); synchronizes */
+int tmg_defect_norm(tmg_level* lv, const double* u, const double* f, double* out_host,
+                    void* stream);
+
+/* ---- transfers (transfer.py:21-56); full = 1 full weighting, 0 half */
+int tmg_restrict(int nxf, int nyf, int full, const double* d, double* out, void* stream);
+int tmg_prolong(int nxc, int nyc, const double* uc, double* v, void* stream);
+/* fused: fc = R (f - L u)  (mgcycle.py:98-99) */
+int tmg_defect_restrict(tmg_level* fine, int full, const double* u, const double* f,
+                        double* fc, void* stream);
+/* fused: u += P uc  (mgcycle.py:102) */
+int tmg_prolong_correct(int nxc, int nyc, const double* uc, double* u, void* stream);
+
+/* ---- DirectSolver (stencil.py:129-155): factor once, then u_int = L^-1 (f -
+ *      boundary couplings of u's ring); u's boundary ring is kept */
+int tmg_direct_solve(tmg_level* lv, double* u, const double* f, void* stream);
+
+/* ---- V-cycle hierarchy (mgcycle.py:64-139).  levels[0] is the finest. */
+int tmg_hier_create(int nlevels, tmg_level* const* levels, tmg_hier** out);
+int tmg_hier_destroy(tmg_hier* h);
+/* one V-cycle in place on u (mgcycle.py:80-104) */
+int tmg_vcycle(tmg_hier* h, int kind, int full, int nu1, int nu2, double* u, const double* f,
+               void* stream);
+/* the solve loop from the given u (mgcycle.py:107-139); norms_out (host) gets
+ * max_cycles + 1 entries at most; synchronizes once per cycle */
+int tmg_solve(tmg_hier* h, int kind, int full, int nu1, int nu2, double tol, int max_cycles,
+              double* u, const double* f, double* norms_out, int* cycles_out,
+              int* converged_out, void* stream);
+/* capture one V-cycle for (u, f) into a CUDA graph and replay it `reps` times */
+int tmg_vcycle_graph(tmg_hier* h, int kind, int full, int nu1, int nu2, double* u,
+                     const double* f, int reps, void* stream);
+/* kernel nodes in the most recently replayed V-cycle graph (launches/cycle) */
+int tmg_hier_graph_kernels(tmg_hier* h);
+
+/* ---- block geometry (layout.py:61-168): per-member (i, j, block, flags) in
+ *      the reference's member order (legs tip -> branch then the branch; rings
+ *      counter-clockwise from the lower-left point).  flags: bit 0 red,
+ *      bits 1-3 leg index (7 = hub / branch / closing point), bits 4-5 block
+ *      kind (0 point, 1 line, 2 legged, 3 ring).  Returns the member count, or
+ *      -1 on bad dimensions.  Host only; no GPU needed. */
+long tmg_layout_dump(int kind, int nx, int ny, int* oi, int* oj, int* oblk, int* oflags,
+                     long cap);
+
+/* ---- per-block plugin shims (kernels.active().relax_*, _ckernels.pyx:42-185)
+ *      ii, jj, offs: DEVICE int64 arrays; W, E, S, N, u, f: DEVICE arrays */
+int tmg_relax_points(long n, const int64_t* ii, const int64_t* jj, int nx, int ny,
+                     const double* W, const double* E, const double* S, const double* N,
+                     double* u, const double* f, void* stream);
+int tmg_relax_chain(long n, const int64_t* ii, const int64_t* jj, int nx, int ny,
+                    const double* W, const double* E, const double* S, const double* N,
+                    double* u, const double* f, void* stream);
+int tmg_relax_ring(long n, const int64_t* ii, const int64_t* jj, int nx, int ny,
+                   const double* W, const double* E, const double* S, const double* N,
+                   double* u, const double* f, void* stream);
+int tmg_relax_legged(long n, const int64_t* ii, const int64_t* jj, long m, const int64_t* offs,
+                     long bi, long bj, int nx, int ny, const double* W, const double* E,
+                     const double* S, const double* N, double* u, const double* f,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TWEEDMG_B200_H */

@@ -1,0 +1,80 @@
+// Internal types shared by the host plan builder, the runtime and the kernels.
+// Not part of the C ABI (include/tweedmg_b200.h is).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tmg {
+
+// Direction codes: the neighbour of (i, j) in direction d.
+// Coupling coefficient toward d (stencil.py:12-15): W[i], E[i], S[j], N[j].
+enum Dir : int { DW = 0, DE = 1, DS = 2, DN = 3, DNONE = 7 };
+__host__ __device__ inline int dir_di(int d) { return d == DW ? -1 : d == DE ? 1 : 0; }
+__host__ __device__ inline int dir_dj(int d) { return d == DS ? -1 : d == DN ? 1 : 0; }
+__host__ __device__ inline int dir_opp(int d) { return d ^ 1; }
+
+enum Scheme : int {
+  SCHEME_CHECKERBOARD = 0,
+  SCHEME_ZEBRA_X = 1,
+  SCHEME_ZEBRA_Y = 2,
+  SCHEME_ZEBRA_ALT = 3,
+  SCHEME_TWEED = 4,
+  SCHEME_WIREFRAME = 5,
+  SCHEME_TWEED_WIRE_ALT = 6,
+};
+
+// One leg: a chain of grid points walked from (i0, j0) through up to four
+// straight segments.  Legs of tweed blocks run tip -> branch (layout.py:81-82);
+// a wireframe ring is one leg (the ring minus its closing point) whose two
+// ends couple to the closing point, which plays the hub (_ckernels.pyx:114-141).
+struct LegD {
+  int32_t i0, j0;
+  int32_t npts;
+  int32_t tbase;       // first virtual thread (chunk) of this leg within its bin
+  int32_t nchunk;      // chunks == threads
+  int32_t block;       // owning block (global index)
+  int32_t seg_len[4];  // steps per segment
+  uint8_t seg_dir[4];
+  uint8_t nseg;
+  uint8_t flags;       // 1: first point couples to the hub, 2: last point does
+  uint8_t hub_dir_first, hub_dir_last;  // direction from the end point to the hub
+};
+
+// One block: an optional hub (branch point / ring closing point / single
+// point) and 0..4 legs.  Same-colour blocks never touch.
+struct BlockD {
+  int32_t hi, hj;      // hub point; hi < 0 if the block has no hub
+  int32_t leg0, nleg;  // global leg indices
+  int32_t hub_thread;  // virtual thread (within bin) that solves the hub row
+  int32_t bin;
+  uint8_t hub_mask;    // bit d: hub neighbour in direction d is a block member
+  uint8_t red;
+  uint8_t pad[2];
+};
+
+// Per-thread table entry (one int32 per virtual thread): >= 0 is the global
+// index of the leg whose chunk (t - leg.tbase) the thread owns; -1 is idle;
+// <= -2 marks the hub-only block -(code + 2) (a point block).  The hub row of
+// a block with legs is solved by chunk 0 of its first leg.
+typedef int32_t ThreadD;
+
+struct BinD {
+  int32_t pcr_steps;  // ceil(log2(max chunks of any leg in the bin))
+  int32_t pad[3];
+};
+
+// One kernel launch worth of bins sharing (q, cluster size).
+struct LaunchClass {
+  int q;
+  int cs;          // CTAs per cluster (1, 2, 4, 8)
+  int nbins;
+  int red;
+  // device arrays
+  ThreadD* threads;  // nbins * cs * kThreads
+  BinD* bins;
+};
+
+constexpr int kThreads = 256;   // threads per CTA of the block-solver kernel
+constexpr int kQmax = 16;       // max points per thread chunk
+
+}  // namespace tmg

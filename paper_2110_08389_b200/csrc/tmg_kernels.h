@@ -1,0 +1,61 @@
+// Kernel launch entry points (internal).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "tmg_internal.h"
+#include "tmg_plan.h"
+
+namespace tmg {
+
+struct SweepArgs {
+  const LegD* legs;
+  const BlockD* blocks;
+  const double* W;
+  const double* E;
+  const double* S;
+  const double* N;
+  double* u;
+  const double* f;
+  int ld;    // row length ny + 1
+  int* err;  // device error flags (bit 0: vanishing pivot)
+};
+
+// Set kernel attributes once (host only, never inside stream capture).
+cudaError_t init_sweep_kernels();
+// One colour stage (red = 1 / black = 0) of a compiled plan.
+cudaError_t launch_colour(const Plan& P, int red, const SweepArgs& a, cudaStream_t stream);
+
+struct GridArgs {
+  int nx, ny;
+  const double* W;
+  const double* E;
+  const double* S;
+  const double* N;
+};
+
+// out = L u on the interior (0 on the boundary) if negate == 0, or
+// out = f - L u (defect) if f != nullptr.  stencil.py:76-96.
+cudaError_t launch_apply(const GridArgs& g, const double* u, const double* f, double* out,
+                         cudaStream_t s);
+// *dmax_bits = max over the interior of |f - L u| as IEEE bits (atomicMax on
+// non-negative doubles); caller zeroes it.  mgcycle.py:122,130.
+cudaError_t launch_defect_norm(const GridArgs& g, const double* u, const double* f,
+                               unsigned long long* dmax_bits, cudaStream_t s);
+// fc = R (f - L u), fused residual + restriction (full = 1 / half = 0).
+// stencil.py:91-96 + transfer.py:21-39 + mgcycle.py:98-99.
+cudaError_t launch_defect_restrict(const GridArgs& g, int full, const double* u,
+                                   const double* f, double* fc, cudaStream_t s);
+// out = R d (transfer.py:21-39)
+cudaError_t launch_restrict(int nxf, int nyf, int full, const double* d, double* out,
+                            cudaStream_t s);
+// v = P uc (transfer.py:42-56), fine shape (2 ncx - 1, 2 ncy - 1)
+cudaError_t launch_prolong(int nxc, int nyc, const double* uc, double* v, cudaStream_t s);
+// u += P uc on the fine interior (transfer.py:42-56 + mgcycle.py:102)
+cudaError_t launch_prolong_correct(int nxc, int nyc, const double* uc, double* u,
+                                   cudaStream_t s);
+// Coarse direct solve with a precomputed dense inverse of the interior
+// operator (j-outer ordering, stencil.py:111): u_int = Ainv (f - B u_bdry).
+cudaError_t launch_dense_solve(const GridArgs& g, const double* Ainv, double* u,
+                               const double* f, double* work, cudaStream_t s);
+
+}  // namespace tmg

@@ -1,0 +1,491 @@
+// Host-side block geometry (closed form) and bin packing for the block-solver
+// kernel.  Replaces the reference's Python-tuple plans (layout.py:61-168,
+// smoothers.py:42-118): a block here is a hub plus up to four legs described
+// by straight segments, O(#blocks) to build instead of O(#points) tuples.
+#include <algorithm>
+#include <cstring>
+
+#include "tmg_plan.h"
+
+namespace tmg {
+
+namespace {
+
+int parity_red(int k) { return (k % 2) != 0; }  // layout.py:22-23
+
+struct Builder {
+  Geometry& g;
+  explicit Builder(Geometry& gg) : g(gg) {}
+
+  int new_block(int red, int hi, int hj) {
+    BlockD b;
+    std::memset(&b, 0, sizeof(b));
+    b.hi = hi;
+    b.hj = hj;
+    b.leg0 = (int)g.legs.size();
+    b.nleg = 0;
+    b.hub_thread = -1;
+    b.bin = -1;
+    b.red = (uint8_t)red;
+    g.blocks.push_back(b);
+    return (int)g.blocks.size() - 1;
+  }
+
+  // Straight leg of npts points starting at (i0, j0) stepping in direction d.
+  // If to_hub, the point after the last one (same direction) is the hub.
+  void straight_leg(int blk, int i0, int j0, int d, int npts, bool to_hub) {
+    LegD L;
+    std::memset(&L, 0, sizeof(L));
+    L.i0 = i0;
+    L.j0 = j0;
+    L.npts = npts;
+    L.block = blk;
+    L.nseg = 1;
+    L.seg_dir[0] = (uint8_t)d;
+    L.seg_len[0] = npts - 1;
+    L.flags = to_hub ? 2 : 0;
+    L.hub_dir_first = DNONE;
+    L.hub_dir_last = to_hub ? (uint8_t)d : (uint8_t)DNONE;
+    g.legs.push_back(L);
+    BlockD& b = g.blocks[blk];
+    b.nleg++;
+    if (to_hub) b.hub_mask |= (uint8_t)(1u << dir_opp(d));
+  }
+};
+
+// layout.py:61-133
+void tweed(Builder& B, int nx, int ny) {
+  int mx = nx - 1, my = ny - 1, s = std::min(mx, my), c = (s + 1) / 2;
+  int corners[4][4] = {{1, 1, 1, 1}, {mx, 1, -1, 1}, {1, my, 1, -1}, {mx, my, -1, -1}};
+  for (auto& cr : corners) B.new_block(1, cr[0], cr[1]);
+  for (int k = 2; k < c; k++) {
+    int red = parity_red(k);
+    for (auto& cr : corners) {
+      int x0 = cr[0], y0 = cr[1], sx = cr[2], sy = cr[3];
+      int bi = x0 + sx * (k - 1), bj = y0 + sy * (k - 1);
+      int b = B.new_block(red, bi, bj);
+      B.straight_leg(b, x0, bj, sx > 0 ? DE : DW, k - 1, true);  // leg_x
+      B.straight_leg(b, bi, y0, sy > 0 ? DN : DS, k - 1, true);  // leg_y
+    }
+  }
+  int redc = parity_red(c);
+  if (mx == my) {
+    int b = B.new_block(redc, c, c);
+    B.straight_leg(b, 1, c, DE, c - 1, true);
+    B.straight_leg(b, mx, c, DW, mx - c, true);
+    B.straight_leg(b, c, 1, DN, c - 1, true);
+    B.straight_leg(b, c, my, DS, my - c, true);
+  } else if (mx > my) {
+    int b = B.new_block(redc, c, c);
+    B.straight_leg(b, 1, c, DE, c - 1, true);
+    B.straight_leg(b, c, 1, DN, c - 1, true);
+    B.straight_leg(b, c, my, DS, my - c, true);
+    int br = mx + 1 - c;
+    b = B.new_block(redc, br, c);
+    B.straight_leg(b, mx, c, DW, mx - br, true);
+    B.straight_leg(b, br, 1, DN, c - 1, true);
+    B.straight_leg(b, br, my, DS, my - c, true);
+    for (int i = c + 1; i < mx - c + 1; i++) {
+      int l = B.new_block(parity_red(i), -1, -1);
+      B.straight_leg(l, i, 1, DN, my, false);
+    }
+  } else {
+    int b = B.new_block(redc, c, c);
+    B.straight_leg(b, c, 1, DN, c - 1, true);
+    B.straight_leg(b, 1, c, DE, c - 1, true);
+    B.straight_leg(b, mx, c, DW, mx - c, true);
+    int br = my + 1 - c;
+    b = B.new_block(redc, c, br);
+    B.straight_leg(b, c, my, DS, my - br, true);
+    B.straight_leg(b, 1, br, DE, c - 1, true);
+    B.straight_leg(b, mx, br, DW, mx - c, true);
+    for (int j = c + 1; j < my - c + 1; j++) {
+      int l = B.new_block(parity_red(j), -1, -1);
+      B.straight_leg(l, 1, j, DE, mx, false);
+    }
+  }
+}
+
+// layout.py:136-168.  Ring r is the chain p_0..p_{m-2} (counter-clockwise
+// from (r, r), x increasing first) plus the closing point p_{m-1} = (r, r+1)
+// as the hub, coupled to both chain ends (_ckernels.pyx:114-118).
+void wireframe(Builder& B, int nx, int ny) {
+  int mx = nx - 1, my = ny - 1, s = std::min(mx, my), q = (s - 1) / 2;
+  for (int r = 1; r <= q; r++) {
+    int hi_i = mx + 1 - r, hi_j = my + 1 - r;
+    int b = B.new_block(parity_red(r), r, r + 1);
+    LegD L;
+    std::memset(&L, 0, sizeof(L));
+    L.i0 = r;
+    L.j0 = r;
+    L.block = b;
+    L.nseg = 4;
+    L.seg_dir[0] = DE; L.seg_len[0] = hi_i - r;
+    L.seg_dir[1] = DN; L.seg_len[1] = hi_j - r;
+    L.seg_dir[2] = DW; L.seg_len[2] = hi_i - r;
+    L.seg_dir[3] = DS; L.seg_len[3] = hi_j - r - 2;
+    L.npts = 1 + L.seg_len[0] + L.seg_len[1] + L.seg_len[2] + L.seg_len[3];
+    L.flags = 3;
+    L.hub_dir_first = DN;  // (r, r) -> (r, r+1)
+    L.hub_dir_last = DS;   // (r, r+2) -> (r, r+1)
+    B.g.legs.push_back(L);
+    BlockD& bb = B.g.blocks[b];
+    bb.nleg = 1;
+    bb.hub_mask = (uint8_t)((1u << DS) | (1u << DN));
+  }
+  int tred = parity_red(q + 1);
+  if (mx == my) {
+    B.new_block(tred, q + 1, q + 1);
+  } else if (mx > my) {
+    int l = B.new_block(tred, -1, -1);
+    B.straight_leg(l, q + 1, q + 1, DE, mx - 2 * q, false);
+  } else {
+    int l = B.new_block(tred, -1, -1);
+    B.straight_leg(l, q + 1, q + 1, DN, my - 2 * q, false);
+  }
+}
+
+// smoothers.py:77-89
+void zebra(Builder& B, int nx, int ny, bool axis_x) {
+  if (axis_x) {
+    for (int j = 1; j < ny; j++) {
+      int l = B.new_block(j % 2, -1, -1);
+      B.straight_leg(l, 1, j, DE, nx - 1, false);
+    }
+  } else {
+    for (int i = 1; i < nx; i++) {
+      int l = B.new_block(i % 2, -1, -1);
+      B.straight_leg(l, i, 1, DN, ny - 1, false);
+    }
+  }
+}
+
+int nchunks(const LegD& L, int q) {
+  if (L.flags & 1) return 1 + (L.npts - 1 + q - 1) / q;
+  return (L.npts + q - 1) / q;
+}
+
+}  // namespace
+
+std::string build_geometry(int scheme, int nx, int ny, Geometry& g) {
+  g = Geometry();
+  g.scheme = scheme;
+  g.nx = nx;
+  g.ny = ny;
+  Builder B(g);
+  switch (scheme) {
+    case SCHEME_ZEBRA_X:
+    case SCHEME_ZEBRA_Y:
+      if (nx < 2 || ny < 2) return "zebra needs nx, ny >= 2";
+      zebra(B, nx, ny, scheme == SCHEME_ZEBRA_X);
+      return "";
+    case SCHEME_TWEED:
+    case SCHEME_WIREFRAME:
+      if (nx < 4 || ny < 4 || nx % 2 || ny % 2)
+        return "block layouts need even nx, ny >= 4, got (" + std::to_string(nx) + ", " +
+               std::to_string(ny) + ")";
+      if (scheme == SCHEME_TWEED) tweed(B, nx, ny);
+      else wireframe(B, nx, ny);
+      return "";
+    default:
+      return "no block geometry for scheme " + std::to_string(scheme);
+  }
+}
+
+static void leg_point_host(const LegD& L, int p, int& i, int& j) {
+  i = L.i0;
+  j = L.j0;
+  int rem = p;
+  for (int s = 0; s < L.nseg && rem > 0; s++) {
+    int st = std::min(rem, L.seg_len[s]);
+    i += st * dir_di(L.seg_dir[s]);
+    j += st * dir_dj(L.seg_dir[s]);
+    rem -= st;
+  }
+}
+
+long dump_members(const Geometry& g, int* oi, int* oj, int* oblk, int* oflags, long cap) {
+  long p = 0;
+  auto put = [&](int i, int j, int b, int flags) {
+    if (p < cap) { oi[p] = i; oj[p] = j; oblk[p] = b; oflags[p] = flags; }
+    p++;
+  };
+  for (size_t b = 0; b < g.blocks.size(); b++) {
+    const BlockD& B = g.blocks[b];
+    // kind: 0 point, 1 line, 2 legged, 3 ring (layout.py:30)
+    int kind = B.nleg == 0 ? 0 : B.hi < 0 ? 1 : (g.legs[B.leg0].flags & 1) ? 3 : 2;
+    for (int l = 0; l < B.nleg; l++) {
+      const LegD& L = g.legs[B.leg0 + l];
+      for (int t = 0; t < L.npts; t++) {
+        int i, j;
+        leg_point_host(L, t, i, j);
+        put(i, j, (int)b, B.red | (l << 1) | (kind << 4));
+      }
+    }
+    if (B.hi >= 0) put(B.hi, B.hj, (int)b, B.red | (7 << 1) | (kind << 4));
+  }
+  return p;
+}
+
+template <class T>
+static T* upload(const std::vector<T>& v, size_t& bytes, std::string& err) {
+  if (v.empty()) return nullptr;
+  T* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, v.size() * sizeof(T));
+  if (e != cudaSuccess) { err = cudaGetErrorString(e); return nullptr; }
+  e = cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { err = cudaGetErrorString(e); return nullptr; }
+  bytes += v.size() * sizeof(T);
+  return d;
+}
+
+std::string build_plan(int scheme, int nx, int ny, int q, Plan& P) {
+  P = Plan();
+  if (q < 1 || q > kQmax) return "chunk size q out of range";
+  P.q = q;
+  if (scheme == SCHEME_CHECKERBOARD) {
+    if (nx < 2 || ny < 2) return "checkerboard needs nx, ny >= 2";
+    P.geo.scheme = scheme;
+    P.geo.nx = nx;
+    P.geo.ny = ny;
+    P.point_scheme = true;
+    return "";
+  }
+  Geometry g;
+  std::string err = build_geometry(scheme, nx, ny, g);
+  if (!err.empty()) return err;
+  return pack_plan(std::move(g), q, P);
+}
+
+std::string pack_plan(Geometry&& geo, int q, Plan& P) {
+  P = Plan();
+  if (q < 1 || q > kQmax) return "chunk size q out of range";
+  P.q = q;
+  P.geo = std::move(geo);
+  Geometry& g = P.geo;
+  std::string err;
+  const int T = kThreads;
+
+  // minimal cluster size per block
+  std::vector<int> need(g.blocks.size());
+  for (size_t b = 0; b < g.blocks.size(); b++) {
+    const BlockD& B = g.blocks[b];
+    int ctas = 1, off = 0;
+    if (B.nleg == 0) off = 1;
+    for (int l = 0; l < B.nleg; l++) {
+      int nch = nchunks(g.legs[B.leg0 + l], q);
+      if (nch > T)
+        return "leg of " + std::to_string(g.legs[B.leg0 + l].npts) +
+               " points exceeds the in-CTA solver capacity (" + std::to_string(T * q) + ")";
+      if (off + nch > T) { ctas++; off = 0; }
+      off += nch;
+    }
+    int cs = 1;
+    while (cs < ctas) cs *= 2;
+    if (cs > 8) return "block needs more than 8 CTAs";
+    need[b] = cs;
+  }
+
+  for (int red = 1; red >= 0; red--) {
+    for (int cs = 1; cs <= 8; cs *= 2) {
+      std::vector<int> blks;
+      for (size_t b = 0; b < g.blocks.size(); b++)
+        if (g.blocks[b].red == red && need[b] == cs) blks.push_back((int)b);
+      if (blks.empty()) continue;
+      std::vector<BinD> bins;
+      std::vector<int> maxch;
+      int bin = -1, rank = cs, off = 0;
+      auto new_bin = [&]() {
+        bin++;
+        rank = 0;
+        off = 0;
+        bins.push_back(BinD{0, {0, 0, 0}});
+        maxch.push_back(1);
+      };
+      for (int b : blks) {
+        BlockD& B = g.blocks[b];
+        for (int attempt = 0; attempt < 2; attempt++) {
+          int r = rank, o = off;
+          bool ok = bin >= 0;
+          std::vector<int> tb(B.nleg);
+          int hub_t = -1;
+          if (ok && B.nleg == 0) {
+            if (o + 1 > T) { r++; o = 0; }
+            if (r >= cs) ok = false;
+            else { hub_t = r * T + o; o += 1; }
+          }
+          for (int l = 0; ok && l < B.nleg; l++) {
+            int nch = nchunks(g.legs[B.leg0 + l], q);
+            if (o + nch > T) { r++; o = 0; }
+            if (r >= cs) { ok = false; break; }
+            tb[l] = r * T + o;
+            o += nch;
+          }
+          if (!ok) {
+            if (attempt == 1) return "internal: block does not fit an empty bin";
+            new_bin();
+            continue;
+          }
+          rank = r;
+          off = o;
+          B.bin = bin;
+          for (int l = 0; l < B.nleg; l++) {
+            LegD& L = g.legs[B.leg0 + l];
+            L.tbase = tb[l];
+            L.nchunk = nchunks(L, q);
+            maxch[bin] = std::max(maxch[bin], L.nchunk);
+          }
+          B.hub_thread = B.nleg ? tb[0] : hub_t;
+          break;
+        }
+      }
+      LaunchClass lc;
+      lc.q = q;
+      lc.cs = cs;
+      lc.red = red;
+      lc.nbins = (int)bins.size();
+      for (int k = 0; k < lc.nbins; k++) {
+        int st = 0;
+        while ((1 << st) < maxch[k]) st++;
+        bins[k].pcr_steps = st;
+      }
+      std::vector<ThreadD> th((size_t)lc.nbins * cs * T, -1);
+      for (int b : blks) {
+        const BlockD& B = g.blocks[b];
+        size_t base = (size_t)B.bin * cs * T;
+        if (B.nleg == 0) th[base + B.hub_thread] = -(b + 2);
+        for (int l = 0; l < B.nleg; l++) {
+          const LegD& L = g.legs[B.leg0 + l];
+          for (int c = 0; c < L.nchunk; c++) th[base + L.tbase + c] = B.leg0 + l;
+        }
+      }
+      lc.threads = upload(th, P.device_bytes, err);
+      lc.bins = upload(bins, P.device_bytes, err);
+      if (!err.empty()) return err;
+      P.classes.push_back(lc);
+    }
+  }
+  P.d_legs = upload(g.legs, P.device_bytes, err);
+  P.d_blocks = upload(g.blocks, P.device_bytes, err);
+  return err;
+}
+
+static int step_dir(long di, long dj) {
+  if (di == -1 && dj == 0) return DW;
+  if (di == 1 && dj == 0) return DE;
+  if (di == 0 && dj == -1) return DS;
+  if (di == 0 && dj == 1) return DN;
+  return -1;
+}
+
+// Path p_0..p_{n-1} of 4-neighbour steps -> leg with <= 4 straight segments.
+static std::string path_leg(int blk, const long long* ii, const long long* jj, long n, LegD& L) {
+  std::memset(&L, 0, sizeof(L));
+  if (n < 1) return "empty leg";
+  L.i0 = (int)ii[0];
+  L.j0 = (int)jj[0];
+  L.npts = (int)n;
+  L.block = blk;
+  L.hub_dir_first = DNONE;
+  L.hub_dir_last = DNONE;
+  L.nseg = 1;
+  L.seg_dir[0] = DE;
+  L.seg_len[0] = 0;
+  int ns = 0;
+  for (long k = 1; k < n; k++) {
+    int d = step_dir(ii[k] - ii[k - 1], jj[k] - jj[k - 1]);
+    if (d < 0) return "block members are not 4-neighbour adjacent";
+    if (ns > 0 && L.seg_dir[ns - 1] == d) {
+      L.seg_len[ns - 1]++;
+    } else {
+      if (ns == 4) return "block path has more than 4 straight segments";
+      L.seg_dir[ns] = (uint8_t)d;
+      L.seg_len[ns] = 1;
+      ns++;
+    }
+  }
+  L.nseg = (uint8_t)(ns > 0 ? ns : 1);
+  return "";
+}
+
+std::string add_explicit_block(Geometry& g, int kind, long n, const long long* ii,
+                               const long long* jj, long m, const long long* offs, long bi,
+                               long bj) {
+  auto new_block = [&](int hi, int hj) {
+    BlockD b;
+    std::memset(&b, 0, sizeof(b));
+    b.hi = hi;
+    b.hj = hj;
+    b.leg0 = (int)g.legs.size();
+    b.hub_thread = -1;
+    b.bin = -1;
+    b.red = 1;
+    g.blocks.push_back(b);
+    return (int)g.blocks.size() - 1;
+  };
+  std::string err;
+  if (kind == 0) {  // merged point blocks
+    for (long k = 0; k < n; k++) new_block((int)ii[k], (int)jj[k]);
+    return "";
+  }
+  if (kind == 1) {  // open chain (_ckernels.pyx:91-103); m == 1 is a point
+    if (n == 1) { new_block((int)ii[0], (int)jj[0]); return ""; }
+    int b = new_block(-1, -1);
+    LegD L;
+    err = path_leg(b, ii, jj, n, L);
+    if (!err.empty()) return err;
+    g.legs.push_back(L);
+    g.blocks[b].nleg = 1;
+    return "";
+  }
+  if (kind == 2) {  // ring: chain p_0..p_{n-2}, hub p_{n-1} (_ckernels.pyx:106-141)
+    if (n < 3) return "circulant system needs m >= 3";
+    int b = new_block((int)ii[n - 1], (int)jj[n - 1]);
+    LegD L;
+    err = path_leg(b, ii, jj, n - 1, L);
+    if (!err.empty()) return err;
+    int df = step_dir(ii[n - 1] - ii[0], jj[n - 1] - jj[0]);
+    int dl = step_dir(ii[n - 1] - ii[n - 2], jj[n - 1] - jj[n - 2]);
+    if (df < 0 || dl < 0) return "ring is not closed by 4-neighbour steps";
+    L.flags = 3;
+    L.hub_dir_first = (uint8_t)df;
+    L.hub_dir_last = (uint8_t)dl;
+    g.legs.push_back(L);
+    g.blocks[b].nleg = 1;
+    g.blocks[b].hub_mask = (uint8_t)((1u << dir_opp(df)) | (1u << dir_opp(dl)));
+    return "";
+  }
+  if (kind == 3) {  // legged (_ckernels.pyx:144-185)
+    if (m < 1) return "legged block needs legs";
+    int b = new_block((int)bi, (int)bj);
+    for (long k = 0; k < m; k++) {
+      long lo = (long)offs[k], hi = (long)offs[k + 1];
+      LegD L;
+      err = path_leg(b, ii + lo, jj + lo, hi - lo, L);
+      if (!err.empty()) return err;
+      int dl = step_dir(bi - ii[hi - 1], bj - jj[hi - 1]);
+      if (dl < 0) return "leg does not end next to the branch point";
+      L.flags = 2;
+      L.hub_dir_last = (uint8_t)dl;
+      g.legs.push_back(L);
+      g.blocks[b].nleg++;
+      g.blocks[b].hub_mask |= (uint8_t)(1u << dir_opp(dl));
+    }
+    return "";
+  }
+  return "bad block kind";
+}
+
+void free_plan(Plan& p) {
+  for (auto& c : p.classes) {
+    cudaFree(c.threads);
+    cudaFree(c.bins);
+  }
+  p.classes.clear();
+  cudaFree(p.d_legs);
+  cudaFree(p.d_blocks);
+  p.d_legs = nullptr;
+  p.d_blocks = nullptr;
+}
+
+}  // namespace tmg

@@ -1,0 +1,47 @@
+// Host-side block geometry and launch planning (native runtime).
+#pragma once
+#include <string>
+#include <vector>
+
+#include "tmg_internal.h"
+
+namespace tmg {
+
+// Closed-form block decomposition of one smoothing scheme on an nx x ny grid.
+// Blocks are emitted in the reference's construction order (layout.py:61-168,
+// smoothers.py:65-89) so that member dumps can be compared one to one.
+struct Geometry {
+  int scheme = 0, nx = 0, ny = 0;
+  std::vector<BlockD> blocks;
+  std::vector<LegD> legs;
+};
+
+// Returns "" on success, else an error message (bad dims / scheme).
+std::string build_geometry(int scheme, int nx, int ny, Geometry& g);
+
+// Per-point member dump in layout.py order (legs tip->branch, then branch;
+// rings in traversal order).  Returns the number of members.
+long dump_members(const Geometry& g, int* oi, int* oj, int* oblk, int* oflags, long cap);
+
+// Device-resident launch plan for one (scheme, grid): geometry + bins.
+struct Plan {
+  Geometry geo;
+  int q = kQmax;
+  LegD* d_legs = nullptr;
+  BlockD* d_blocks = nullptr;
+  std::vector<LaunchClass> classes;  // red classes first, then black
+  bool point_scheme = false;         // checkerboard: dedicated point kernel
+  size_t device_bytes = 0;
+};
+
+std::string build_plan(int scheme, int nx, int ny, int q, Plan& p);
+// Pack an explicit geometry (e.g. one block from the per-block shims).
+std::string pack_plan(Geometry&& g, int q, Plan& p);
+// Append a block made of explicit member paths (host index arrays).
+// kind: 0 points (each a hub-only block), 1 chain, 2 ring, 3 legged.
+std::string add_explicit_block(Geometry& g, int kind, long n, const long long* ii,
+                               const long long* jj, long m, const long long* offs, long bi,
+                               long bj);
+void free_plan(Plan& p);
+
+}  // namespace tmg

@@ -1,0 +1,657 @@
+// Native runtime behind the C ABI (include/tweedmg_b200.h): level handles
+// with lazily compiled device plans, the coarse direct solver, the V-cycle
+// driver (mgcycle.py:80-139) and the solve loop, CUDA-graph replay.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/tweedmg_b200.h"
+#include "tmg_kernels.h"
+#include "tmg_plan.h"
+
+using namespace tmg;
+
+namespace {
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(TMG_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define TMG_CUDA_TRY(expr)                                    \
+  do {                                                        \
+    cudaError_t _e = (expr);                                  \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr);       \
+  } while (0)
+
+int default_q() {
+  const char* s = std::getenv("TMG_CHUNK");
+  if (s) {
+    int q = std::atoi(s);
+    if (q >= 1 && q <= kQmax) return q;
+  }
+  return kQmax;
+}
+
+bool valid_kind(int k) { return k >= TMG_CHECKERBOARD && k <= TMG_TWEED_WIRE_ALT; }
+}  // namespace
+
+struct tmg_level {
+  int nx = 0, ny = 0, device = 0;
+  double *W = nullptr, *E = nullptr, *S = nullptr, *N = nullptr;
+  std::vector<double> hW, hE, hS, hN;
+  Plan* plans[7] = {};
+  int* d_err = nullptr;
+  unsigned long long* d_norm = nullptr;
+  int* h_err = nullptr;                 // pinned
+  unsigned long long* h_norm = nullptr; // pinned
+  double* d_ainv = nullptr;  // coarse dense inverse (or the 1x1 operator)
+  double* d_work = nullptr;
+  long long bytes = 0;
+
+  GridArgs grid() const { return GridArgs{nx, ny, W, E, S, N}; }
+};
+
+struct tmg_hier {
+  std::vector<tmg_level*> lv;
+  std::vector<double*> u, f;  // per-level work fields (index 0 unused)
+  std::map<std::tuple<int, int, int, int, const void*, const void*, void*>,
+           std::pair<cudaGraphExec_t, int>>
+      graphs;
+  int last_kernels = 0;
+};
+
+namespace {
+
+int get_plan(tmg_level* lv, int scheme, Plan** out) {
+  if (!lv->plans[scheme]) {
+    cudaError_t e = init_sweep_kernels();
+    if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");
+    Plan* p = new Plan();
+    std::string err = build_plan(scheme, lv->nx, lv->ny, default_q(), *p);
+    if (!err.empty()) {
+      free_plan(*p);
+      delete p;
+      return fail(TMG_BADARG, err);
+    }
+    lv->plans[scheme] = p;
+    lv->bytes += (long long)p->device_bytes;
+  }
+  *out = lv->plans[scheme];
+  return TMG_OK;
+}
+
+SweepArgs sweep_args(tmg_level* lv, const Plan* p, double* u, const double* f) {
+  SweepArgs a;
+  a.legs = p->d_legs;
+  a.blocks = p->d_blocks;
+  a.W = lv->W;
+  a.E = lv->E;
+  a.S = lv->S;
+  a.N = lv->N;
+  a.u = u;
+  a.f = f;
+  a.ld = lv->ny + 1;
+  a.err = lv->d_err;
+  return a;
+}
+
+int sweep_one(tmg_level* lv, int scheme, int colour_mask, double* u, const double* f,
+              cudaStream_t s) {
+  Plan* p = nullptr;
+  int st = get_plan(lv, scheme, &p);
+  if (st) return st;
+  SweepArgs a = sweep_args(lv, p, u, f);
+  for (int red = 1; red >= 0; red--) {
+    if (!(colour_mask & (red ? 1 : 2))) continue;
+    cudaError_t e = launch_colour(*p, red, a, s);
+    if (e != cudaSuccess) return cuda_fail(e, "sweep launch");
+  }
+  return TMG_OK;
+}
+
+int sweep_kind(tmg_level* lv, int kind, int colour_mask, double* u, const double* f,
+               cudaStream_t s) {
+  if (!valid_kind(kind)) return fail(TMG_BADARG, "unknown smoother kind " + std::to_string(kind));
+  if (kind == TMG_ZEBRA_ALT) {  // smoothers.py:126-129
+    int st = sweep_one(lv, TMG_ZEBRA_X, colour_mask, u, f, s);
+    return st ? st : sweep_one(lv, TMG_ZEBRA_Y, colour_mask, u, f, s);
+  }
+  if (kind == TMG_TWEED_WIRE_ALT) {  // smoothers.py:130-133
+    int st = sweep_one(lv, TMG_TWEED, colour_mask, u, f, s);
+    return st ? st : sweep_one(lv, TMG_WIREFRAME, colour_mask, u, f, s);
+  }
+  return sweep_one(lv, kind, colour_mask, u, f, s);
+}
+
+// Dense inverse of the interior operator in j-outer ordering (stencil.py:99-126),
+// Gauss-Jordan with partial pivoting, computed once per level on the host.
+int factor_coarse(tmg_level* lv) {
+  if (lv->d_ainv) return TMG_OK;
+  const int mi = lv->nx - 1, mj = lv->ny - 1;
+  const long n = (long)mi * mj;
+  if (n < 1) return fail(TMG_BADARG, "grid has no interior");
+  if (n > 4096)
+    return fail(TMG_BADARG, "direct solve supports at most 4096 interior unknowns, got " +
+                                std::to_string(n));
+  std::vector<double> A((size_t)n * n, 0.0), X((size_t)n * n, 0.0);
+  for (int i = 1; i <= mi; i++)
+    for (int j = 1; j <= mj; j++) {
+      const long k = (long)(j - 1) * mi + (i - 1);
+      A[k * n + k] = -(lv->hW[i] + lv->hE[i] + lv->hS[j] + lv->hN[j]);
+      if (i > 1) A[k * n + k - 1] = lv->hW[i];
+      if (i < mi) A[k * n + k + 1] = lv->hE[i];
+      if (j > 1) A[k * n + k - mi] = lv->hS[j];
+      if (j < mj) A[k * n + k + mi] = lv->hN[j];
+      X[k * n + k] = 1.0;
+    }
+  if (n == 1) {
+    X[0] = A[0];  // divided on the device, as SuperLU does for a 1x1 system
+    if (std::fabs(A[0]) < 1e-300) return fail(TMG_SINGULAR, "zero pivot in direct solve");
+  } else {
+    for (long c = 0; c < n; c++) {
+      long p = c;
+      for (long r = c + 1; r < n; r++)
+        if (std::fabs(A[r * n + c]) > std::fabs(A[p * n + c])) p = r;
+      if (std::fabs(A[p * n + c]) < 1e-300) return fail(TMG_SINGULAR, "zero pivot in direct solve");
+      if (p != c)
+        for (long k = 0; k < n; k++) {
+          std::swap(A[c * n + k], A[p * n + k]);
+          std::swap(X[c * n + k], X[p * n + k]);
+        }
+      const double inv = 1.0 / A[c * n + c];
+      for (long k = 0; k < n; k++) {
+        A[c * n + k] *= inv;
+        X[c * n + k] *= inv;
+      }
+      for (long r = 0; r < n; r++) {
+        if (r == c) continue;
+        const double l = A[r * n + c];
+        if (l == 0.0) continue;
+        for (long k = 0; k < n; k++) {
+          A[r * n + k] -= l * A[c * n + k];
+          X[r * n + k] -= l * X[c * n + k];
+        }
+      }
+    }
+  }
+  TMG_CUDA_TRY(cudaMalloc(&lv->d_ainv, sizeof(double) * (size_t)n * n));
+  TMG_CUDA_TRY(cudaMalloc(&lv->d_work, sizeof(double) * (size_t)n));
+  TMG_CUDA_TRY(cudaMemcpy(lv->d_ainv, X.data(), sizeof(double) * (size_t)n * n,
+                          cudaMemcpyHostToDevice));
+  lv->bytes += (long long)(sizeof(double) * (size_t)n * (n + 1));
+  return TMG_OK;
+}
+
+int fetch_flags_async(tmg_level* lv, cudaStream_t s) {
+  TMG_CUDA_TRY(cudaMemcpyAsync(lv->h_err, lv->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  TMG_CUDA_TRY(cudaMemsetAsync(lv->d_err, 0, sizeof(int), s));
+  return TMG_OK;
+}
+
+int check_fetched(tmg_level* lv) {
+  if (*lv->h_err & 1) return fail(TMG_SINGULAR, "zero pivot during block elimination");
+  return TMG_OK;
+}
+
+int read_flags(tmg_level* lv, cudaStream_t s) {
+  int st = fetch_flags_async(lv, s);
+  if (st) return st;
+  TMG_CUDA_TRY(cudaStreamSynchronize(s));
+  return check_fetched(lv);
+}
+
+int vcycle_launches(tmg_hier* h, int kind, int full, int nu1, int nu2, double* u,
+                    const double* f, cudaStream_t s) {
+  const int L = (int)h->lv.size();
+  std::vector<double*> U(L), F(L);
+  U[0] = u;
+  F[0] = const_cast<double*>(f);
+  for (int l = 1; l < L; l++) {
+    U[l] = h->u[l];
+    F[l] = h->f[l];
+  }
+  for (int l = 0; l < L - 1; l++) {  // mgcycle.py:96-101 on the way down
+    tmg_level* lv = h->lv[l];
+    for (int k = 0; k < nu1; k++) {
+      int st = sweep_kind(lv, kind, 3, U[l], F[l], s);
+      if (st) return st;
+    }
+    cudaError_t e = launch_defect_restrict(lv->grid(), full, U[l], F[l], F[l + 1], s);
+    if (e != cudaSuccess) return cuda_fail(e, "defect_restrict");
+    tmg_level* lc = h->lv[l + 1];
+    TMG_CUDA_TRY(cudaMemsetAsync(U[l + 1], 0,
+                                 sizeof(double) * (size_t)(lc->nx + 1) * (lc->ny + 1), s));
+  }
+  {  // mgcycle.py:93-95
+    tmg_level* lc = h->lv[L - 1];
+    int st = factor_coarse(lc);
+    if (st) return st;
+    cudaError_t e = launch_dense_solve(lc->grid(), lc->d_ainv, U[L - 1], F[L - 1], lc->d_work, s);
+    if (e != cudaSuccess) return cuda_fail(e, "coarse solve");
+  }
+  for (int l = L - 2; l >= 0; l--) {  // mgcycle.py:102-104 on the way up
+    tmg_level* lv = h->lv[l];
+    tmg_level* lc = h->lv[l + 1];
+    cudaError_t e = launch_prolong_correct(lc->nx, lc->ny, U[l + 1], U[l], s);
+    if (e != cudaSuccess) return cuda_fail(e, "prolong_correct");
+    for (int k = 0; k < nu2; k++) {
+      int st = sweep_kind(lv, kind, 3, U[l], F[l], s);
+      if (st) return st;
+    }
+  }
+  return TMG_OK;
+}
+
+int norm_async(tmg_level* lv, const double* u, const double* f, cudaStream_t s) {
+  TMG_CUDA_TRY(cudaMemsetAsync(lv->d_norm, 0, sizeof(unsigned long long), s));
+  cudaError_t e = launch_defect_norm(lv->grid(), u, f, lv->d_norm, s);
+  if (e != cudaSuccess) return cuda_fail(e, "defect_norm");
+  TMG_CUDA_TRY(cudaMemcpyAsync(lv->h_norm, lv->d_norm, sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s));
+  return TMG_OK;
+}
+
+double bits_to_double(unsigned long long b) {
+  double d;
+  std::memcpy(&d, &b, sizeof(d));
+  return d;
+}
+
+int check_hier_args(tmg_hier* h, int kind, int nu1, int nu2) {
+  if (!h || h->lv.empty()) return fail(TMG_BADARG, "null hierarchy");
+  if (!valid_kind(kind)) return fail(TMG_BADARG, "unknown smoother " + std::to_string(kind));
+  if (nu1 < 0 || nu2 < 0 || nu1 + nu2 < 1)
+    return fail(TMG_BADARG, "need nu1, nu2 >= 0 with nu1 + nu2 >= 1");
+  return TMG_OK;
+}
+
+template <class F>
+int guarded(F&& fn) {
+  try {
+    return fn();
+  } catch (const std::exception& ex) {
+    return fail(TMG_CUDA, ex.what());
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tmg_last_error(void) { return g_last_error.c_str(); }
+int tmg_version(void) { return 100; }
+
+int tmg_level_create(int nx, int ny, const double* W, const double* E, const double* S,
+                     const double* N, tmg_level** out) {
+  return guarded([&]() -> int {
+    if (!out) return fail(TMG_BADARG, "null output handle");
+    if (nx < 2 || ny < 2) return fail(TMG_BADARG, "grid needs nx, ny >= 2");
+    tmg_level* lv = new tmg_level();
+    lv->nx = nx;
+    lv->ny = ny;
+    cudaGetDevice(&lv->device);
+    lv->hW.assign(W, W + nx + 1);
+    lv->hE.assign(E, E + nx + 1);
+    lv->hS.assign(S, S + ny + 1);
+    lv->hN.assign(N, N + ny + 1);
+    size_t bx = sizeof(double) * (nx + 1), by = sizeof(double) * (ny + 1);
+    TMG_CUDA_TRY(cudaMalloc(&lv->W, 2 * bx + 2 * by));
+    lv->E = lv->W + (nx + 1);
+    lv->S = lv->E + (nx + 1);
+    lv->N = lv->S + (ny + 1);
+    TMG_CUDA_TRY(cudaMemcpy(lv->W, W, bx, cudaMemcpyHostToDevice));
+    TMG_CUDA_TRY(cudaMemcpy(lv->E, E, bx, cudaMemcpyHostToDevice));
+    TMG_CUDA_TRY(cudaMemcpy(lv->S, S, by, cudaMemcpyHostToDevice));
+    TMG_CUDA_TRY(cudaMemcpy(lv->N, N, by, cudaMemcpyHostToDevice));
+    TMG_CUDA_TRY(cudaMalloc(&lv->d_err, sizeof(int) + sizeof(unsigned long long) * 2));
+    lv->d_norm = reinterpret_cast<unsigned long long*>(lv->d_err + 2);
+    TMG_CUDA_TRY(cudaMemset(lv->d_err, 0, sizeof(int)));
+    TMG_CUDA_TRY(cudaMallocHost(&lv->h_err, sizeof(int) * 2 + sizeof(unsigned long long) * 2));
+    lv->h_norm = reinterpret_cast<unsigned long long*>(lv->h_err + 2);
+    lv->bytes = (long long)(2 * bx + 2 * by);
+    *out = lv;
+    return TMG_OK;
+  });
+}
+
+int tmg_level_destroy(tmg_level* lv) {
+  if (!lv) return TMG_OK;
+  for (auto& p : lv->plans)
+    if (p) {
+      free_plan(*p);
+      delete p;
+    }
+  cudaFree(lv->W);
+  cudaFree(lv->d_err);
+  cudaFreeHost(lv->h_err);
+  cudaFree(lv->d_ainv);
+  cudaFree(lv->d_work);
+  delete lv;
+  return TMG_OK;
+}
+
+long long tmg_level_device_bytes(tmg_level* lv) { return lv ? lv->bytes : 0; }
+
+int tmg_level_check(tmg_level* lv, void* stream) {
+  if (!lv) return fail(TMG_BADARG, "null level");
+  return read_flags(lv, (cudaStream_t)stream);
+}
+
+int tmg_sweep(tmg_level* lv, int kind, double* u, const double* f, void* stream) {
+  if (!lv) return fail(TMG_BADARG, "null level");
+  return guarded([&] { return sweep_kind(lv, kind, 3, u, f, (cudaStream_t)stream); });
+}
+
+int tmg_sweep_colour(tmg_level* lv, int kind, int red, double* u, const double* f,
+                     void* stream) {
+  if (!lv) return fail(TMG_BADARG, "null level");
+  return guarded([&] { return sweep_kind(lv, kind, red ? 1 : 2, u, f, (cudaStream_t)stream); });
+}
+
+int tmg_apply(tmg_level* lv, const double* u, double* out, void* stream) {
+  if (!lv) return fail(TMG_BADARG, "null level");
+  cudaError_t e = launch_apply(lv->grid(), u, nullptr, out, (cudaStream_t)stream);
+  return e == cudaSuccess ? TMG_OK : cuda_fail(e, "apply");
+}
+
+int tmg_defect(tmg_level* lv, const double* u, const double* f, double* d, void* stream) {
+  if (!lv) return fail(TMG_BADARG, "null level");
+  cudaError_t e = launch_apply(lv->grid(), u, f, d, (cudaStream_t)stream);
+  return e == cudaSuccess ? TMG_OK : cuda_fail(e, "defect");
+}
+
+int tmg_defect_norm(tmg_level* lv, const double* u, const double* f, double* out_host,
+                    void* stream) {
+  if (!lv) return fail(TMG_BADARG, "null level");
+  cudaStream_t s = (cudaStream_t)stream;
+  int st = norm_async(lv, u, f, s);
+  if (st) return st;
+  TMG_CUDA_TRY(cudaStreamSynchronize(s));
+  *out_host = bits_to_double(*lv->h_norm);
+  return TMG_OK;
+}
+
+int tmg_restrict(int nxf, int nyf, int full, const double* d, double* out, void* stream) {
+  if (nxf % 2 || nyf % 2 || nxf < 2 || nyf < 2) return fail(TMG_BADARG, "fine grid cannot be halved");
+  cudaError_t e = launch_restrict(nxf, nyf, full, d, out, (cudaStream_t)stream);
+  return e == cudaSuccess ? TMG_OK : cuda_fail(e, "restrict");
+}
+
+int tmg_prolong(int nxc, int nyc, const double* uc, double* v, void* stream) {
+  if (nxc < 2 || nyc < 2) return fail(TMG_BADARG, "coarse grid has no interior to interpolate");
+  cudaError_t e = launch_prolong(nxc, nyc, uc, v, (cudaStream_t)stream);
+  return e == cudaSuccess ? TMG_OK : cuda_fail(e, "prolong");
+}
+
+int tmg_defect_restrict(tmg_level* fine, int full, const double* u, const double* f, double* fc,
+                        void* stream) {
+  if (!fine) return fail(TMG_BADARG, "null level");
+  if (fine->nx % 2 || fine->ny % 2) return fail(TMG_BADARG, "fine grid cannot be halved");
+  cudaError_t e = launch_defect_restrict(fine->grid(), full, u, f, fc, (cudaStream_t)stream);
+  return e == cudaSuccess ? TMG_OK : cuda_fail(e, "defect_restrict");
+}
+
+int tmg_prolong_correct(int nxc, int nyc, const double* uc, double* u, void* stream) {
+  cudaError_t e = launch_prolong_correct(nxc, nyc, uc, u, (cudaStream_t)stream);
+  return e == cudaSuccess ? TMG_OK : cuda_fail(e, "prolong_correct");
+}
+
+int tmg_direct_solve(tmg_level* lv, double* u, const double* f, void* stream) {
+  if (!lv) return fail(TMG_BADARG, "null level");
+  return guarded([&]() -> int {
+    int st = factor_coarse(lv);
+    if (st) return st;
+    cudaError_t e = launch_dense_solve(lv->grid(), lv->d_ainv, u, f, lv->d_work,
+                                       (cudaStream_t)stream);
+    return e == cudaSuccess ? TMG_OK : cuda_fail(e, "direct solve");
+  });
+}
+
+int tmg_hier_create(int nlevels, tmg_level* const* levels, tmg_hier** out) {
+  return guarded([&]() -> int {
+    if (nlevels < 1 || !levels || !out) return fail(TMG_BADARG, "bad hierarchy arguments");
+    for (int l = 1; l < nlevels; l++)
+      if (levels[l]->nx * 2 != levels[l - 1]->nx || levels[l]->ny * 2 != levels[l - 1]->ny)
+        return fail(TMG_BADARG, "each level must halve the previous one");
+    tmg_hier* h = new tmg_hier();
+    h->lv.assign(levels, levels + nlevels);
+    h->u.assign(nlevels, nullptr);
+    h->f.assign(nlevels, nullptr);
+    for (int l = 1; l < nlevels; l++) {
+      size_t n = (size_t)(levels[l]->nx + 1) * (levels[l]->ny + 1);
+      TMG_CUDA_TRY(cudaMalloc(&h->u[l], 2 * n * sizeof(double)));
+      h->f[l] = h->u[l] + n;
+      TMG_CUDA_TRY(cudaMemset(h->u[l], 0, 2 * n * sizeof(double)));
+    }
+    *out = h;
+    return TMG_OK;
+  });
+}
+
+int tmg_hier_destroy(tmg_hier* h) {
+  if (!h) return TMG_OK;
+  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.first);
+  for (size_t l = 1; l < h->u.size(); l++) cudaFree(h->u[l]);
+  delete h;
+  return TMG_OK;
+}
+
+int tmg_vcycle(tmg_hier* h, int kind, int full, int nu1, int nu2, double* u, const double* f,
+               void* stream) {
+  int st = check_hier_args(h, kind, nu1, nu2);
+  if (st) return st;
+  return guarded([&] { return vcycle_launches(h, kind, full, nu1, nu2, u, f, (cudaStream_t)stream); });
+}
+
+int tmg_vcycle_graph(tmg_hier* h, int kind, int full, int nu1, int nu2, double* u,
+                     const double* f, int reps, void* stream) {
+  int st = check_hier_args(h, kind, nu1, nu2);
+  if (st) return st;
+  return guarded([&]() -> int {
+    cudaStream_t s = (cudaStream_t)stream;
+    auto key = std::make_tuple(kind, full, nu1, nu2, (const void*)u, (const void*)f, stream);
+    auto it = h->graphs.find(key);
+    if (it == h->graphs.end()) {
+      // build plans and coarse factors outside capture (they allocate)
+      for (size_t l = 0; l < h->lv.size(); l++) {
+        int sub[2] = {kind, -1};
+        if (kind == TMG_ZEBRA_ALT) { sub[0] = TMG_ZEBRA_X; sub[1] = TMG_ZEBRA_Y; }
+        if (kind == TMG_TWEED_WIRE_ALT) { sub[0] = TMG_TWEED; sub[1] = TMG_WIREFRAME; }
+        for (int k : sub) {
+          if (k < 0 || l + 1 == h->lv.size()) continue;
+          Plan* p;
+          int st2 = get_plan(h->lv[l], k, &p);
+          if (st2) return st2;
+        }
+      }
+      int st2 = factor_coarse(h->lv.back());
+      if (st2) return st2;
+      cudaStream_t cs;
+      TMG_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      cudaGraph_t g;
+      TMG_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      int st3 = vcycle_launches(h, kind, full, nu1, nu2, u, f, cs);
+      cudaError_t e = cudaStreamEndCapture(cs, &g);
+      cudaStreamDestroy(cs);
+      if (st3) return st3;
+      if (e != cudaSuccess) return cuda_fail(e, "graph capture");
+      size_t nn = 0;
+      TMG_CUDA_TRY(cudaGraphGetNodes(g, nullptr, &nn));
+      std::vector<cudaGraphNode_t> nodes(nn);
+      TMG_CUDA_TRY(cudaGraphGetNodes(g, nodes.data(), &nn));
+      int kernels = 0;
+      for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        TMG_CUDA_TRY(cudaGraphNodeGetType(nd, &t));
+        kernels += (t == cudaGraphNodeTypeKernel);
+      }
+      cudaGraphExec_t ge;
+      TMG_CUDA_TRY(cudaGraphInstantiate(&ge, g, 0));
+      cudaGraphDestroy(g);
+      if (h->graphs.size() >= 32) {  // bound the cache
+        for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.first);
+        h->graphs.clear();
+      }
+      it = h->graphs.emplace(key, std::make_pair(ge, kernels)).first;
+    }
+    h->last_kernels = it->second.second;
+    for (int r = 0; r < reps; r++) TMG_CUDA_TRY(cudaGraphLaunch(it->second.first, s));
+    return TMG_OK;
+  });
+}
+
+int tmg_hier_graph_kernels(tmg_hier* h) { return h ? h->last_kernels : 0; }
+
+int tmg_solve(tmg_hier* h, int kind, int full, int nu1, int nu2, double tol, int max_cycles,
+              double* u, const double* f, double* norms_out, int* cycles_out, int* converged_out,
+              void* stream) {
+  int st = check_hier_args(h, kind, nu1, nu2);
+  if (st) return st;
+  if (!(tol > 0)) return fail(TMG_BADARG, "tol must be positive");
+  return guarded([&]() -> int {
+    cudaStream_t s = (cudaStream_t)stream;
+    tmg_level* fine = h->lv[0];
+    *cycles_out = 0;
+    *converged_out = 0;
+    int st2 = norm_async(fine, u, f, s);
+    if (st2) return st2;
+    TMG_CUDA_TRY(cudaStreamSynchronize(s));
+    const double d0 = bits_to_double(*fine->h_norm);
+    norms_out[0] = d0;
+    if (d0 == 0.0) {  // mgcycle.py:124-126
+      *converged_out = 1;
+      return TMG_OK;
+    }
+    for (int cycle = 1; cycle <= max_cycles; cycle++) {  // mgcycle.py:128-138
+      st2 = tmg_vcycle_graph(h, kind, full, nu1, nu2, u, f, 1, stream);
+      if (st2) return st2;
+      st2 = norm_async(fine, u, f, s);
+      if (st2) return st2;
+      for (size_t l = 0; l < h->lv.size(); l++) {
+        st2 = fetch_flags_async(h->lv[l], s);
+        if (st2) return st2;
+      }
+      TMG_CUDA_TRY(cudaStreamSynchronize(s));
+      for (size_t l = 0; l < h->lv.size(); l++) {
+        st2 = check_fetched(h->lv[l]);
+        if (st2) return st2;
+      }
+      const double dn = bits_to_double(*fine->h_norm);
+      norms_out[cycle] = dn;
+      *cycles_out = cycle;
+      if (!std::isfinite(dn)) break;
+      if (dn <= tol * d0) {
+        *converged_out = 1;
+        break;
+      }
+    }
+    return TMG_OK;
+  });
+}
+
+long tmg_layout_dump(int kind, int nx, int ny, int* oi, int* oj, int* oblk, int* oflags, long cap) {
+  Geometry g;
+  std::string err = build_geometry(kind, nx, ny, g);
+  if (!err.empty()) {
+    g_last_error = err;
+    return -1;
+  }
+  return dump_members(g, oi, oj, oblk, oflags, cap);
+}
+
+}  // extern "C"
+
+// ---------------- per-block shims (test / plugin surface) -------------------
+namespace {
+
+int relax_explicit(int kind, long n, const int64_t* ii, const int64_t* jj, long m,
+                   const int64_t* offs, long bi, long bj, int nx, int ny, const double* W,
+                   const double* E, const double* S, const double* N, double* u, const double* f,
+                   cudaStream_t s) {
+  if (n < 1) return TMG_OK;
+  std::vector<long long> hi(n), hj(n), ho(m > 0 ? m + 1 : 1);
+  TMG_CUDA_TRY(cudaMemcpyAsync(hi.data(), ii, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
+  TMG_CUDA_TRY(cudaMemcpyAsync(hj.data(), jj, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
+  if (kind == 3)
+    TMG_CUDA_TRY(cudaMemcpyAsync(ho.data(), offs, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToHost, s));
+  TMG_CUDA_TRY(cudaStreamSynchronize(s));
+  for (long k = 0; k < n; k++)
+    if (hi[k] < 1 || hi[k] >= nx || hj[k] < 1 || hj[k] >= ny)
+      return fail(TMG_BADARG, "block member outside the grid interior");
+  Geometry g;
+  g.nx = nx;
+  g.ny = ny;
+  g.scheme = -1;
+  std::string err = add_explicit_block(g, kind, n, hi.data(), hj.data(), m, ho.data(), bi, bj);
+  if (!err.empty()) return fail(TMG_BADARG, err);
+  Plan p;
+  err = pack_plan(std::move(g), kQmax, p);
+  if (!err.empty()) {
+    free_plan(p);
+    return fail(TMG_BADARG, err);
+  }
+  int* d_err = nullptr;
+  TMG_CUDA_TRY(cudaMalloc(&d_err, sizeof(int)));
+  TMG_CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(int), s));
+  SweepArgs a{p.d_legs, p.d_blocks, W, E, S, N, u, f, ny + 1, d_err};
+  cudaError_t e = launch_colour(p, 1, a, s);
+  int herr = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(d_err);
+  free_plan(p);
+  if (e != cudaSuccess) return cuda_fail(e, "relax shim");
+  if (herr & 1) return fail(TMG_SINGULAR, "zero pivot");
+  return TMG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tmg_relax_points(long n, const int64_t* ii, const int64_t* jj, int nx, int ny, const double* W,
+                     const double* E, const double* S, const double* N, double* u, const double* f,
+                     void* stream) {
+  return guarded([&] {
+    return relax_explicit(0, n, ii, jj, 0, nullptr, 0, 0, nx, ny, W, E, S, N, u, f,
+                          (cudaStream_t)stream);
+  });
+}
+
+int tmg_relax_chain(long n, const int64_t* ii, const int64_t* jj, int nx, int ny, const double* W,
+                    const double* E, const double* S, const double* N, double* u, const double* f,
+                    void* stream) {
+  return guarded([&] {
+    return relax_explicit(1, n, ii, jj, 0, nullptr, 0, 0, nx, ny, W, E, S, N, u, f,
+                          (cudaStream_t)stream);
+  });
+}
+
+int tmg_relax_ring(long n, const int64_t* ii, const int64_t* jj, int nx, int ny, const double* W,
+                   const double* E, const double* S, const double* N, double* u, const double* f,
+                   void* stream) {
+  return guarded([&] {
+    return relax_explicit(2, n, ii, jj, 0, nullptr, 0, 0, nx, ny, W, E, S, N, u, f,
+                          (cudaStream_t)stream);
+  });
+}
+
+int tmg_relax_legged(long n, const int64_t* ii, const int64_t* jj, long m, const int64_t* offs,
+                     long bi, long bj, int nx, int ny, const double* W, const double* E,
+                     const double* S, const double* N, double* u, const double* f, void* stream) {
+  return guarded([&] {
+    return relax_explicit(3, n, ii, jj, m, offs, bi, bj, nx, ny, W, E, S, N, u, f,
+                          (cudaStream_t)stream);
+  });
+}
+
+}  // extern "C"

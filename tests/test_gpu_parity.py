@@ -1,0 +1,267 @@
+"""GPU parity: every device operator against the CPU oracle on the same seeded
+inputs (the oracle is itself pinned bit-exact to the reference by
+tests/test_oracle.py and tests/golden).
+
+Tolerances: the residual, transfers and max-norm evaluate in the reference's
+order and must be bit-identical; block solves use a different (partitioned)
+elimination order, so sweeps are compared at <= 1e-12 relative per sweep (the
+north-star gate is 1e-10)."""
+
+import numpy as np
+import pytest
+
+from paper_2110_08389_b200 import grid, kernels, mgcycle, smoothers, stencil, transfer
+from paper_2110_08389_b200.rng import Lcg64
+from paper_2110_08389_b200.tridiag import SingularSystemError
+
+pytestmark = pytest.mark.gpu
+
+SWEEP_TOL = 1e-12
+GRIDS = [("uniform", None), ("wall", 3.0), ("centre", 1.5)]
+SIZES = [(12, 10), (10, 10), (10, 8), (8, 14), (20, 8), (16, 16), (34, 34)]
+
+
+def _problem(stretch, c, nx, ny, seed=31):
+    x = grid.make_coords(stretch, nx, 1.0, c)
+    y = grid.make_coords(stretch, ny, 1.0, c)
+    st = stencil.assemble(x, y)
+    rng = Lcg64(seed)
+    f = np.zeros((nx + 1, ny + 1))
+    f[1:-1, 1:-1] = rng.fill((nx - 1, ny - 1)) - 0.5
+    u = np.zeros_like(f)
+    u[1:-1, 1:-1] = rng.fill((nx - 1, ny - 1)) - 0.5
+    return st, u, f
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(1.0, np.max(np.abs(b))))
+
+
+def _tens(cuda, a):
+    return cuda.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("kind", smoothers.KINDS)
+@pytest.mark.parametrize("stretch,c", GRIDS)
+@pytest.mark.parametrize("nx,ny", SIZES)
+def test_sweeps_match_oracle(cuda, orc, kind, stretch, c, nx, ny):
+    st, u0, f = _problem(stretch, c, nx, ny)
+    ud, fd = _tens(cuda, u0), _tens(cuda, f)
+    uo = u0.copy()
+    bundle = smoothers.PlanBundle(nx, ny)
+    for _ in range(3):
+        smoothers.sweep(kind, st, bundle, ud, fd)
+        orc.sweep(kind, (st.W, st.E, st.S, st.N), uo, f)
+        assert _rel(ud.cpu().numpy(), uo) <= SWEEP_TOL
+
+
+@pytest.mark.parametrize("kind", ("checkerboard", "zebra_x", "zebra_y", "tweed", "wireframe"))
+@pytest.mark.parametrize("stretch,c", GRIDS)
+def test_exactness_by_colour(cuda, kind, stretch, c):
+    """test_smoothers.py:54-66: after each colour stage the defect vanishes
+    on that colour's points."""
+    nx, ny = 10, 8
+    st, u0, f = _problem(stretch, c, nx, ny, seed=5)
+    ud, fd = _tens(cuda, u0), _tens(cuda, f)
+    lay = None
+    if kind in ("tweed", "wireframe"):
+        lay = grid.Level(grid.make_coords(stretch, nx, 1.0, c),
+                         grid.make_coords(stretch, ny, 1.0, c)).layout(kind)
+    for colour in ("red", "black"):
+        smoothers.sweep_colour(kind, st, ud, fd, colour)
+        d = stencil.defect(st, ud, fd).cpu().numpy()
+        if lay is not None:
+            pts = [p for b in lay.blocks if b.colour == colour for p in b.members]
+        elif kind == "checkerboard":
+            pts = [(i, j) for i in range(1, nx) for j in range(1, ny)
+                   if ((i + j) % 2 == 0) == (colour == "red")]
+        elif kind == "zebra_x":
+            pts = [(i, j) for i in range(1, nx) for j in range(1, ny)
+                   if (j % 2 == 1) == (colour == "red")]
+        else:
+            pts = [(i, j) for i in range(1, nx) for j in range(1, ny)
+                   if (i % 2 == 1) == (colour == "red")]
+        worst = max(abs(d[i, j]) for i, j in pts)
+        assert worst <= 1e-11 * np.max(np.abs(f)), (kind, colour, worst)
+
+
+@pytest.mark.parametrize("kind", smoothers.KINDS)
+def test_exact_solution_is_fixed_point(cuda, kind):
+    st, _, f = _problem("wall", 2.0, 10, 10)
+    u = stencil.direct_solve(st, f)
+    ref = np.array(u, copy=True)
+    smoothers.sweep(kind, st, smoothers.PlanBundle(10, 10), u, f)
+    assert np.max(np.abs(u - ref)) <= 1e-11 * max(1.0, np.max(np.abs(ref)))
+
+
+def test_per_block_shims_match_oracle(cuda, orc):
+    """test_kernels.py:58-79 pattern: each relax_* entry point on one block."""
+    import ctypes
+    nx = ny = 8
+    st, u0, f = _problem("wall", 3.0, nx, ny, seed=3)
+    W, E, S, N = st.W, st.E, st.S, st.N
+    lay = grid.Level(grid.make_coords("wall", nx, 1.0, 3.0),
+                     grid.make_coords("wall", ny, 1.0, 3.0))
+    lib = orc.lib()
+    dp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))  # noqa: E731
+    lp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_long))  # noqa: E731
+    tw = lay.layout("tweed")
+    legged = [b for b in tw.blocks if b.kind == "legged"]
+    for blk in legged:
+        flat = [p for leg in blk.legs for p in leg]
+        ii = np.array([p[0] for p in flat], dtype=np.int64)
+        jj = np.array([p[1] for p in flat], dtype=np.int64)
+        offs = np.cumsum([0] + [len(leg) for leg in blk.legs]).astype(np.int64)
+        u = u0.copy()
+        uo = u0.copy()
+        kernels.relax_legged(ii, jj, offs, blk.branch[0], blk.branch[1], W, E, S, N, u, f)
+        lib.orc_relax_legged(len(ii), lp(ii), lp(jj), len(offs) - 1, lp(offs), blk.branch[0],
+                             blk.branch[1], dp(W), dp(E), dp(S), dp(N), dp(uo), dp(f), ny + 1)
+        assert _rel(u, uo) <= SWEEP_TOL
+    wf = lay.layout("wireframe")
+    for blk in wf.blocks:
+        ii = np.array([p[0] for p in blk.members], dtype=np.int64)
+        jj = np.array([p[1] for p in blk.members], dtype=np.int64)
+        u = u0.copy()
+        uo = u0.copy()
+        if blk.kind == "ring":
+            kernels.relax_ring(ii, jj, W, E, S, N, u, f)
+            lib.orc_relax_ring(len(ii), lp(ii), lp(jj), dp(W), dp(E), dp(S), dp(N), dp(uo),
+                               dp(f), ny + 1)
+        else:
+            kernels.relax_points(ii, jj, W, E, S, N, u, f)
+            lib.orc_relax_points(len(ii), lp(ii), lp(jj), dp(W), dp(E), dp(S), dp(N), dp(uo),
+                                 dp(f), ny + 1)
+        assert _rel(u, uo) <= SWEEP_TOL
+    for j in range(1, ny):
+        ii = np.arange(1, nx, dtype=np.int64)
+        jj = np.full_like(ii, j)
+        u = u0.copy()
+        uo = u0.copy()
+        kernels.relax_chain(ii, jj, W, E, S, N, u, f)
+        lib.orc_relax_chain(len(ii), lp(ii), lp(jj), dp(W), dp(E), dp(S), dp(N), dp(uo),
+                            dp(f), ny + 1)
+        assert _rel(u, uo) <= SWEEP_TOL
+
+
+@pytest.mark.parametrize("stretch,c", GRIDS)
+@pytest.mark.parametrize("nx,ny", [(12, 10), (64, 64), (130, 66)])
+def test_residual_and_transfers_bit_exact(cuda, orc, stretch, c, nx, ny):
+    st, u, f = _problem(stretch, c, nx, ny, seed=9)
+    sto = (st.W, st.E, st.S, st.N)
+    d = stencil.defect(st, u, f)
+    assert np.array_equal(d, orc.defect(sto, u, f))
+    lu = stencil.apply(st, u)
+    assert np.array_equal(-lu + np.pad(f[1:-1, 1:-1], 1), d)
+    assert stencil.defect_norm(st, u, f) == orc.defect_max(sto, u, f)
+    for kind in ("half", "full"):
+        assert np.array_equal(transfer.restrict(kind, d), orc.restrict(kind, d))
+    fc = transfer.restrict("full", d)
+    assert np.array_equal(transfer.prolong(fc), orc.prolong(fc))
+
+
+def test_fused_transfers_equal_unfused(cuda, orc):
+    import ctypes
+
+    from paper_2110_08389_b200 import _lib
+    from paper_2110_08389_b200.stencil import native_level
+    for nx, ny in ((16, 16), (258, 130), (1026, 1024)):
+        st, u, f = _problem("wall", 3.0, nx, ny, seed=4)
+        ud, fd = _tens(cuda, u), _tens(cuda, f)
+        for full in (0, 1):
+            fc = cuda.zeros((nx // 2 + 1, ny // 2 + 1), dtype=cuda.float64, device="cuda")
+            _lib.check(_lib.lib().tmg_defect_restrict(
+                native_level(st), full, ctypes.c_void_p(ud.data_ptr()),
+                ctypes.c_void_p(fd.data_ptr()), ctypes.c_void_p(fc.data_ptr()), None))
+            want = orc.restrict("full" if full else "half", orc.defect((st.W, st.E, st.S, st.N), u, f))
+            assert np.array_equal(fc.cpu().numpy(), want)
+        uc = _problem("uniform", None, nx // 2, ny // 2, seed=6)[1]
+        ucd = _tens(cuda, uc)
+        _lib.check(_lib.lib().tmg_prolong_correct(nx // 2, ny // 2, ctypes.c_void_p(ucd.data_ptr()),
+                                                  ctypes.c_void_p(ud.data_ptr()), None))
+        uo = u.copy()
+        orc.prolong_add(uc, uo)
+        assert np.array_equal(ud.cpu().numpy(), uo)
+
+
+@pytest.mark.parametrize("nx,ny", [(8, 8), (16, 16), (12, 10), (32, 32)])
+def test_direct_solve_matches_oracle(cuda, orc, nx, ny):
+    st, u, f = _problem("centre", 1.5, nx, ny, seed=2)
+    g = np.zeros_like(u)
+    g[0, :], g[-1, :], g[:, 0], g[:, -1] = u[0, :] + 1, u[-1, :] - 2, 0.5, 0.25
+    got = stencil.direct_solve(st, f, g)
+    want = orc.dense_solve((st.W, st.E, st.S, st.N), f, g)
+    assert _rel(got, want) <= 1e-11
+    assert np.array_equal(got[0, :], want[0, :]) and np.array_equal(got[:, -1], want[:, -1])
+
+
+def test_singular_pivot_raises(cuda):
+    nx = ny = 8
+    z = np.zeros(nx + 1)
+    st = stencil.StencilCoeffs(z, z.copy(), z.copy(), z.copy())
+    u = np.zeros((nx + 1, ny + 1))
+    with pytest.raises(SingularSystemError):
+        smoothers.sweep("tweed", st, smoothers.PlanBundle(nx, ny), u, u.copy())
+    with pytest.raises(ValueError):
+        smoothers.sweep("zebra_y", st, smoothers.PlanBundle(nx, ny), u, u.copy())
+
+
+def test_sweep_rejects_bad_shapes(cuda):
+    st, u, f = _problem("uniform", None, 8, 8)
+    with pytest.raises(ValueError):
+        smoothers.sweep("tweed", st, smoothers.PlanBundle(8, 8), u[:-1], f[:-1])
+    with pytest.raises(ValueError):
+        smoothers.sweep("houndstooth", st, smoothers.PlanBundle(8, 8), u, f)
+
+
+@pytest.mark.parametrize("smoother,restriction,stretch,c,n",
+                         [("tweed", "full", "wall", 3.0, 64), ("wireframe", "full", "centre", 1.5, 64),
+                          ("zebra_alt", "half", "uniform", None, 32),
+                          ("checkerboard", "full", "wall", 2.0, 48),
+                          ("tweed_wire_alt", "full", "wall", 1.5, 40)])
+def test_solve_matches_oracle(cuda, orc, smoother, restriction, stretch, c, n):
+    x = grid.make_coords(stretch, n, 1.0, c)
+    h = grid.build_hierarchy(x, x)
+    cfg = mgcycle.CycleConfig(smoother=smoother, restriction=restriction)
+    f = mgcycle.random_rhs(n, n, 1)
+    u, rep = mgcycle.solve(h, cfg, f)
+    H = orc.Hierarchy(x.values, x.values)
+    uo, repo = orc.solve(H, f, smoother=smoother, restriction=restriction)
+    assert rep.cycles == repo.cycles and rep.converged == repo.converged
+    assert rep.defect_norms[0] == repo.defect_norms[0]
+    assert _rel(u, uo) <= 1e-10
+    for a, b in zip(rep.defect_norms[1:], repo.defect_norms[1:]):
+        assert abs(a - b) <= 1e-6 * b + 1e-13 * rep.defect_norms[0]
+
+
+def test_v_cycle_tensor_graph_path(cuda, orc):
+    n = 64
+    x = grid.make_tanh_wall(n, 1.0, 3.0)
+    h = grid.build_hierarchy(x, x)
+    cfg = mgcycle.CycleConfig(smoother="tweed")
+    f = mgcycle.random_rhs(n, n, 3)
+    u = cuda.zeros((n + 1, n + 1), dtype=cuda.float64, device="cuda")
+    fd = _tens(cuda, f)
+    H = orc.Hierarchy(x.values, x.values)
+    uo = np.zeros((n + 1, n + 1))
+    for _ in range(3):
+        mgcycle.v_cycle(h, cfg, u, fd)
+        orc.v_cycle(H, uo, f)
+        assert _rel(u.cpu().numpy(), uo) <= 1e-10
+
+
+def test_boundary_values_bitwise_preserved(cuda):
+    n = 16
+    x = grid.make_coords("centre", n, 1.0, 1.5)
+    h = grid.build_hierarchy(x, x)
+    f = mgcycle.random_rhs(n, n, seed=5)
+    rng = Lcg64(11)
+    g = np.zeros((n + 1, n + 1))
+    g[0, :] = rng.fill(n + 1)
+    g[-1, :] = rng.fill(n + 1)
+    g[:, 0] = rng.fill(n + 1)
+    g[:, -1] = rng.fill(n + 1)
+    u, rep = mgcycle.solve(h, mgcycle.CycleConfig(), f, g=g)
+    assert rep.converged
+    assert np.array_equal(u[0, :], g[0, :]) and np.array_equal(u[-1, :], g[-1, :])
+    assert np.array_equal(u[:, 0], g[:, 0]) and np.array_equal(u[:, -1], g[:, -1])
