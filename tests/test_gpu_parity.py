@@ -175,7 +175,8 @@ def test_fused_transfers_equal_unfused(cuda, orc):
                 ctypes.c_void_p(fd.data_ptr()), ctypes.c_void_p(fc.data_ptr()), None))
             want = orc.restrict("full" if full else "half", orc.defect((st.W, st.E, st.S, st.N), u, f))
             assert np.array_equal(fc.cpu().numpy(), want)
-        uc = _problem("uniform", None, nx // 2, ny // 2, seed=6)[1]
+        uc = np.zeros((nx // 2 + 1, ny // 2 + 1))
+        uc[1:-1, 1:-1] = Lcg64(6).fill((nx // 2 - 1, ny // 2 - 1)) - 0.5
         ucd = _tens(cuda, uc)
         _lib.check(_lib.lib().tmg_prolong_correct(nx // 2, ny // 2, ctypes.c_void_p(ucd.data_ptr()),
                                                   ctypes.c_void_p(ud.data_ptr()), None))
