@@ -52,15 +52,44 @@ struct BlockD {
   uint8_t pad[2];
 };
 
-// Per-thread table entry (one int32 per virtual thread): >= 0 is the global
-// index of the leg whose chunk (t - leg.tbase) the thread owns; -1 is idle;
-// <= -2 marks the hub-only block -(code + 2) (a point block).  The hub row of
-// a block with legs is solved by chunk 0 of its first leg.
-typedef int32_t ThreadD;
+// One thread's chunk: <= q consecutive points of a leg lying on one straight
+// run (chunks never turn a corner), so point k of the chunk is at element
+// offset off + k*stride and along-axis index a0 + k*da.
+struct ChunkD {
+  int32_t off;    // element offset of the first point
+  int16_t a0;     // along-axis index of the first point (i if axis 0, else j)
+  int16_t cidx;   // cross-axis index (j if axis 0, else i)
+  int16_t hub;    // virtual thread that owns the block's hub value, -1 if none
+  int16_t own;    // index of the hub this thread solves (within the bin), -1
+  uint8_t n;      // points in the chunk (0: no chunk)
+  uint8_t geo;    // bit 0: axis (0: i varies, 1: j varies); bit 1: decreasing
+  uint16_t link;  // bits 0-2 dfirst, 3-5 dlast (direction from the first /
+                  // last point to its in-block neighbour outside the chunk,
+                  // 7 = none); bit 6 left = previous thread, bit 7 left = hub,
+                  // bit 8 right = next thread, bit 9 right = hub
+};
+static_assert(sizeof(ChunkD) == 16, "ChunkD must stay 16 bytes");
+
+constexpr int kLinkLeftPrev = 1 << 6, kLinkLeftHub = 1 << 7;
+constexpr int kLinkRightNext = 1 << 8, kLinkRightHub = 1 << 9;
+
+// Hub row of one block (branch point, ring closing point or a point block).
+struct HubD {
+  int32_t off;
+  int16_t i, j;
+  uint8_t mask;       // bit d: the hub's neighbour in direction d is in-block
+  uint8_t nadj;       // adjacent chunk ends (0..4)
+  int16_t adj_t[4];   // virtual thread whose reduced unknown is that point
+  uint8_t adj_d[4];   // direction from the hub to that point
+  uint8_t pad[2];
+};
+static_assert(sizeof(HubD) == 24, "HubD layout");
 
 struct BinD {
   int32_t pcr_steps;  // ceil(log2(max chunks of any leg in the bin))
-  int32_t pad[3];
+  int32_t hub0;       // first hub of the bin in the class hub array
+  int32_t nhub;
+  int32_t warp_local;  // 1: every leg of the bin lies inside one warp
 };
 
 // One kernel launch worth of bins sharing (q, cluster size).
@@ -69,9 +98,9 @@ struct LaunchClass {
   int cs;          // CTAs per cluster (1, 2, 4, 8)
   int nbins;
   int red;
-  // device arrays
-  ThreadD* threads;  // nbins * cs * kThreads
+  ChunkD* chunks;  // nbins * cs * kThreads
   BinD* bins;
+  HubD* hubs;
 };
 
 constexpr int kThreads = 256;   // threads per CTA of the block-solver kernel

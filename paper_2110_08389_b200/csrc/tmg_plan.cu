@@ -160,9 +160,40 @@ void zebra(Builder& B, int nx, int ny, bool axis_x) {
   }
 }
 
-int nchunks(const LegD& L, int q) {
-  if (L.flags & 1) return 1 + (L.npts - 1 + q - 1) / q;
-  return (L.npts + q - 1) / q;
+// Direction of step p (the step arriving at point p >= 1) of a leg.
+int step_direction(const LegD& L, int p) {
+  int cum = 0;
+  for (int s = 0; s < L.nseg; s++) {
+    if (p > cum && p <= cum + L.seg_len[s]) return L.seg_dir[s];
+    cum += L.seg_len[s];
+  }
+  return L.seg_dir[L.nseg - 1];
+}
+
+// Split a leg into straight runs (pieces) and the pieces into chunks of at
+// most q points.  A leg whose first point couples to the hub starts with a
+// one-point chunk, so that every hub neighbour is a chunk end (a reduced
+// unknown).  Returns [first, last] point ranges.
+std::vector<std::pair<int, int>> leg_chunks(const LegD& L, int q) {
+  std::vector<std::pair<int, int>> pieces, out;
+  int start = 0;
+  if (L.flags & 1) {
+    pieces.push_back({0, 0});
+    start = 1;
+  }
+  int cum = 0;
+  for (int s = 0; s < L.nseg; s++) {
+    const int endp = cum + L.seg_len[s];
+    if (endp >= start) {
+      pieces.push_back({start, endp});
+      start = endp + 1;
+    }
+    cum = endp;
+  }
+  if (start <= L.npts - 1) pieces.push_back({start, L.npts - 1});
+  for (auto& pc : pieces)
+    for (int a = pc.first; a <= pc.second; a += q) out.push_back({a, std::min(a + q - 1, pc.second)});
+  return out;
 }
 
 }  // namespace
@@ -259,24 +290,30 @@ std::string build_plan(int scheme, int nx, int ny, int q, Plan& P) {
 
 std::string pack_plan(Geometry&& geo, int q, Plan& P) {
   P = Plan();
-  if (q < 1 || q > kQmax) return "chunk size q out of range";
+  if (q < 1 || q > kQmax || (q & (q - 1))) return "chunk size q must be a power of two <= 16";
   P.q = q;
   P.geo = std::move(geo);
   Geometry& g = P.geo;
   std::string err;
   const int T = kThreads;
+  const int ld = g.ny + 1;
 
-  // minimal cluster size per block
+  std::vector<std::vector<std::pair<int, int>>> lchunks(g.legs.size());
+  for (size_t l = 0; l < g.legs.size(); l++) {
+    lchunks[l] = leg_chunks(g.legs[l], q);
+    g.legs[l].nchunk = (int)lchunks[l].size();
+    if (g.legs[l].nchunk > T)
+      return "leg of " + std::to_string(g.legs[l].npts) +
+             " points exceeds the in-CTA solver capacity (" + std::to_string(T * q) + ")";
+  }
+  // minimal cluster size per block (legs never straddle CTAs)
   std::vector<int> need(g.blocks.size());
   for (size_t b = 0; b < g.blocks.size(); b++) {
     const BlockD& B = g.blocks[b];
-    int ctas = 1, off = 0;
-    if (B.nleg == 0) off = 1;
+    int ctas = 1, off = B.nleg == 0 ? 1 : 0;
     for (int l = 0; l < B.nleg; l++) {
-      int nch = nchunks(g.legs[B.leg0 + l], q);
-      if (nch > T)
-        return "leg of " + std::to_string(g.legs[B.leg0 + l].npts) +
-               " points exceeds the in-CTA solver capacity (" + std::to_string(T * q) + ")";
+      int nch = g.legs[B.leg0 + l].nchunk;
+      if (nch <= 32 && (off / 32) != ((off + nch - 1) / 32)) off = (off / 32 + 1) * 32;
       if (off + nch > T) { ctas++; off = 0; }
       off += nch;
     }
@@ -295,13 +332,6 @@ std::string pack_plan(Geometry&& geo, int q, Plan& P) {
       std::vector<BinD> bins;
       std::vector<int> maxch;
       int bin = -1, rank = cs, off = 0;
-      auto new_bin = [&]() {
-        bin++;
-        rank = 0;
-        off = 0;
-        bins.push_back(BinD{0, {0, 0, 0}});
-        maxch.push_back(1);
-      };
       for (int b : blks) {
         BlockD& B = g.blocks[b];
         for (int attempt = 0; attempt < 2; attempt++) {
@@ -315,7 +345,9 @@ std::string pack_plan(Geometry&& geo, int q, Plan& P) {
             else { hub_t = r * T + o; o += 1; }
           }
           for (int l = 0; ok && l < B.nleg; l++) {
-            int nch = nchunks(g.legs[B.leg0 + l], q);
+            int nch = g.legs[B.leg0 + l].nchunk;
+            // keep warp-sized legs inside one warp (shuffle-only reduction)
+            if (nch <= 32 && (o / 32) != ((o + nch - 1) / 32)) o = (o / 32 + 1) * 32;
             if (o + nch > T) { r++; o = 0; }
             if (r >= cs) { ok = false; break; }
             tb[l] = r * T + o;
@@ -323,7 +355,11 @@ std::string pack_plan(Geometry&& geo, int q, Plan& P) {
           }
           if (!ok) {
             if (attempt == 1) return "internal: block does not fit an empty bin";
-            new_bin();
+            bin++;
+            rank = 0;
+            off = 0;
+            bins.push_back(BinD{0, 0, 0, 0});
+            maxch.push_back(1);
             continue;
           }
           rank = r;
@@ -332,10 +368,9 @@ std::string pack_plan(Geometry&& geo, int q, Plan& P) {
           for (int l = 0; l < B.nleg; l++) {
             LegD& L = g.legs[B.leg0 + l];
             L.tbase = tb[l];
-            L.nchunk = nchunks(L, q);
             maxch[bin] = std::max(maxch[bin], L.nchunk);
           }
-          B.hub_thread = B.nleg ? tb[0] : hub_t;
+          B.hub_thread = B.nleg ? -1 : hub_t;
           break;
         }
       }
@@ -344,23 +379,92 @@ std::string pack_plan(Geometry&& geo, int q, Plan& P) {
       lc.cs = cs;
       lc.red = red;
       lc.nbins = (int)bins.size();
+      ChunkD idle;
+      std::memset(&idle, 0, sizeof(idle));
+      idle.hub = -1;
+      idle.own = -1;
+      idle.link = (uint16_t)(DNONE | (DNONE << 3));
+      std::vector<ChunkD> ch((size_t)lc.nbins * cs * T, idle);
+      std::vector<std::vector<HubD>> bhubs(lc.nbins);
+      for (int b : blks) {
+        BlockD& B = g.blocks[b];
+        const size_t base = (size_t)B.bin * cs * T;
+        // hub: owner = first adjacent chunk thread, or the reserved thread
+        int owner = -1, own_idx = -1;
+        if (B.hi >= 0) {
+          HubD H;
+          std::memset(&H, 0, sizeof(H));
+          H.off = B.hi * ld + B.hj;
+          H.i = (int16_t)B.hi;
+          H.j = (int16_t)B.hj;
+          H.mask = B.hub_mask;
+          for (int l = 0; l < B.nleg; l++) {
+            const LegD& L = g.legs[B.leg0 + l];
+            if (L.flags & 2) {
+              H.adj_t[H.nadj] = (int16_t)(L.tbase + L.nchunk - 1);
+              H.adj_d[H.nadj++] = (uint8_t)dir_opp(L.hub_dir_last);
+            }
+            if (L.flags & 1) {
+              H.adj_t[H.nadj] = (int16_t)L.tbase;
+              H.adj_d[H.nadj++] = (uint8_t)dir_opp(L.hub_dir_first);
+            }
+          }
+          owner = B.nleg ? (H.nadj ? H.adj_t[0] : g.legs[B.leg0].tbase) : B.hub_thread;
+          B.hub_thread = owner;
+          own_idx = (int)bhubs[B.bin].size();
+          bhubs[B.bin].push_back(H);
+          ch[base + owner].own = (int16_t)own_idx;
+          ch[base + owner].hub = (int16_t)owner;
+        }
+        for (int l = 0; l < B.nleg; l++) {
+          const LegD& L = g.legs[B.leg0 + l];
+          const auto& cks = lchunks[B.leg0 + l];
+          for (int c = 0; c < (int)cks.size(); c++) {
+            const int s = cks[c].first, e = cks[c].second;
+            int i, j;
+            leg_point_host(L, s, i, j);
+            // direction of the run containing the chunk
+            const int d = (e > s) ? step_direction(L, s + 1)
+                                  : (s > 0 ? step_direction(L, s) : L.seg_dir[0]);
+            const int axis = (d == DS || d == DN) ? 1 : 0;
+            const int neg = (d == DW || d == DS) ? 1 : 0;
+            int dfirst = DNONE, dlast = DNONE, link = 0;
+            if (s == 0) {
+              if (L.flags & 1) { dfirst = L.hub_dir_first; link |= kLinkLeftHub; }
+            } else {
+              dfirst = dir_opp(step_direction(L, s));
+              link |= kLinkLeftPrev;
+            }
+            if (e == L.npts - 1) {
+              if (L.flags & 2) { dlast = L.hub_dir_last; link |= kLinkRightHub; }
+            } else {
+              dlast = step_direction(L, e + 1);
+              link |= kLinkRightNext;
+            }
+            ChunkD& C = ch[base + L.tbase + c];
+            C.off = i * ld + j;
+            C.a0 = (int16_t)(axis ? j : i);
+            C.cidx = (int16_t)(axis ? i : j);
+            C.n = (uint8_t)(e - s + 1);
+            C.geo = (uint8_t)(axis | (neg << 1));
+            C.link = (uint16_t)(dfirst | (dlast << 3) | link);
+            C.hub = (int16_t)owner;
+          }
+        }
+      }
+      std::vector<HubD> hubs;
       for (int k = 0; k < lc.nbins; k++) {
         int st = 0;
         while ((1 << st) < maxch[k]) st++;
         bins[k].pcr_steps = st;
+        bins[k].warp_local = maxch[k] <= 32 ? 1 : 0;
+        bins[k].hub0 = (int)hubs.size();
+        bins[k].nhub = (int)bhubs[k].size();
+        hubs.insert(hubs.end(), bhubs[k].begin(), bhubs[k].end());
       }
-      std::vector<ThreadD> th((size_t)lc.nbins * cs * T, -1);
-      for (int b : blks) {
-        const BlockD& B = g.blocks[b];
-        size_t base = (size_t)B.bin * cs * T;
-        if (B.nleg == 0) th[base + B.hub_thread] = -(b + 2);
-        for (int l = 0; l < B.nleg; l++) {
-          const LegD& L = g.legs[B.leg0 + l];
-          for (int c = 0; c < L.nchunk; c++) th[base + L.tbase + c] = B.leg0 + l;
-        }
-      }
-      lc.threads = upload(th, P.device_bytes, err);
+      lc.chunks = upload(ch, P.device_bytes, err);
       lc.bins = upload(bins, P.device_bytes, err);
+      lc.hubs = upload(hubs, P.device_bytes, err);
       if (!err.empty()) return err;
       P.classes.push_back(lc);
     }
@@ -478,8 +582,9 @@ std::string add_explicit_block(Geometry& g, int kind, long n, const long long* i
 
 void free_plan(Plan& p) {
   for (auto& c : p.classes) {
-    cudaFree(c.threads);
+    cudaFree(c.chunks);
     cudaFree(c.bins);
+    cudaFree(c.hubs);
   }
   p.classes.clear();
   cudaFree(p.d_legs);

@@ -3,19 +3,22 @@
 // blocks.  Replaces relax_points / relax_chain / relax_ring / relax_legged
 // (_ckernels.pyx:42-185) driven by smoothers.sweep (smoothers.py:121-150).
 //
-// Algorithm per bin (all fp64):
-//  A  coalesced gather: each block point p gets r_p = f_p - sum of its
-//     out-of-block neighbours (the frozen-RHS of _ckernels.pyx:34-39 without
-//     the subtract/add-back of in-block neighbours, algebraically equal),
-//     staged in shared memory in a chunk-major padded layout.
-//  B  each thread owns a chunk of <= q consecutive leg points.  A down sweep
-//     (Thomas forward elimination) and an affine back pass express every
-//     chunk point as x = alpha + beta*x_{s-1} + gamma*x_e, leaving one reduced
-//     unknown per chunk (its last point).  The reduced system is tridiagonal
-//     per leg and is solved by parallel cyclic reduction across the CTA with
-//     two right-hand sides: the data and the hub-coupling column.  The hub
-//     (branch point / ring closing point) row then reduces to a scalar solve,
-//     exactly as m_legged_thomas / circulant_thomas do (tridiag.py:46-125).
+// Work decomposition (host side, tmg_plan.cu): every leg of a block is cut
+// into straight chunks of <= q points, one chunk per thread, described by a
+// 16-byte ChunkD (element offset, stride, along/cross indices, the couplings
+// of its two ends).  Per bin, all fp64:
+//  A  coalesced gather: lane-consecutive points of the bin's chunks read f and
+//     the out-of-block neighbours of u and stage the frozen right-hand side
+//     r_p = f_p - sum(out-of-block couplings) in shared memory (the frozen RHS
+//     of _ckernels.pyx:34-39 without the subtract / add-back of in-block
+//     neighbours, which is algebraically equal).
+//  B  per thread: a Thomas down sweep and an affine back pass over the chunk
+//     interior express every chunk point as x = alpha + beta*x_left + gamma*X,
+//     X being the chunk's last point; the chunk ends form a tridiagonal reduced
+//     system per leg, solved by parallel cyclic reduction (warp shuffles, then
+//     shared memory) with two right-hand sides: the data and the hub coupling.
+//     The hub row (branch point / ring closing point) is then a scalar solve,
+//     as in m_legged_thomas / circulant_thomas (tridiag.py:46-125).
 //  C  coalesced scatter of the new values.
 #include <cooperative_groups.h>
 
@@ -27,47 +30,20 @@ namespace tmg {
 
 namespace {
 
-struct PInfo {
-  int i, j, dprev, dnext;
-};
-
-__device__ __forceinline__ PInfo leg_point(const LegD& L, int p) {
-  PInfo r;
-  r.i = L.i0;
-  r.j = L.j0;
-  r.dprev = (p == 0) ? ((L.flags & 1) ? (int)L.hub_dir_first : (int)DNONE) : (int)DNONE;
-  r.dnext = (p == L.npts - 1) ? ((L.flags & 2) ? (int)L.hub_dir_last : (int)DNONE) : (int)DNONE;
-  int cum = 0;
-#pragma unroll
-  for (int s = 0; s < 4; s++) {
-    if (s < L.nseg) {
-      int len = L.seg_len[s], d = L.seg_dir[s];
-      int st = min(max(p - cum, 0), len);
-      r.i += st * dir_di(d);
-      r.j += st * dir_dj(d);
-      if (p >= 1 && p > cum && p <= cum + len) r.dprev = dir_opp(d);
-      if (p < L.npts - 1 && p + 1 > cum && p + 1 <= cum + len) r.dnext = d;
-      cum += len;
-    }
-  }
-  return r;
-}
-
-__device__ __forceinline__ void chunk_range(const LegD& L, int c, int q, int& s, int& e) {
-  if (L.flags & 1) {
-    if (c == 0) {
-      s = 0;
-      e = 0;
-      return;
-    }
-    s = 1 + (c - 1) * q;
-  } else {
-    s = c * q;
-  }
-  e = min(s + q - 1, L.npts - 1);
-}
-
 __device__ __forceinline__ bool bad_pivot(double v) { return v > -1e-300 && v < 1e-300; }
+
+// reciprocal: hardware approximation refined by three Newton steps (full
+// double precision; ~1 ulp from 1/x)
+__device__ __forceinline__ double drcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
 
 template <bool CLUSTER>
 __device__ __forceinline__ double* remote(double* p, int rank) {
@@ -87,23 +63,79 @@ __device__ __forceinline__ void bin_sync() {
   }
 }
 
+struct Coefs {
+  const double* __restrict__ W;
+  const double* __restrict__ E;
+  const double* __restrict__ S;
+  const double* __restrict__ N;
+  __device__ __forceinline__ double dir(int d, int i, int j) const {
+    switch (d) {
+      case DW: return __ldg(W + i);
+      case DE: return __ldg(E + i);
+      case DS: return __ldg(S + j);
+      case DN: return __ldg(N + j);
+      default: return 0.0;
+    }
+  }
+};
+
+// Geometry of one chunk, unpacked into registers.
+struct Chunk {
+  int off, stride, a0, da, cidx, cs, n, dfirst, dlast, link, hub, own, axis;
+  const double* __restrict__ pa;  // along coupling toward the previous point
+  const double* __restrict__ pc;  // along coupling toward the next point
+  const double* __restrict__ xl;  // cross coefficients (low / high side)
+  const double* __restrict__ xh;
+
+  __device__ __forceinline__ void unpack(const ChunkD& c, const Coefs& C, int ld) {
+    n = c.n;
+    off = c.off;
+    a0 = c.a0;
+    cidx = c.cidx;
+    axis = c.geo & 1;
+    const int neg = (c.geo >> 1) & 1;
+    da = neg ? -1 : 1;
+    stride = axis ? da : da * ld;
+    cs = axis ? ld : 1;
+    dfirst = c.link & 7;
+    dlast = (c.link >> 3) & 7;
+    link = c.link;
+    hub = c.hub;
+    own = c.own;
+    const double* lo = axis ? C.S : C.W;
+    const double* hi = axis ? C.N : C.E;
+    pa = neg ? hi : lo;
+    pc = neg ? lo : hi;
+    xl = axis ? C.W : C.S;
+    xh = axis ? C.E : C.N;
+  }
+  __device__ __forceinline__ void ij(int k, int& i, int& j) const {
+    const int a = a0 + k * da;
+    i = axis ? cidx : a;
+    j = axis ? a : cidx;
+  }
+};
+
 }  // namespace
 
-// Shared-memory carve-up (doubles):
-//   R   [T * QSMAX]   chunk-major point values (rhs -> rho -> alpha -> x)
-//   E5  [5 * T]       reduced equations (A, B, C, D, H); also UP triples
-//   XH  [T]           hub values of blocks whose hub thread lives here
-constexpr int QSMAX = kQmax | 1;
-constexpr size_t kSweepSmem = sizeof(double) * (size_t)(kThreads * QSMAX + 6 * kThreads);
+// Shared memory (doubles unless noted):
+//   R   [T * QS]  chunk-major point values (rhs -> rho -> alpha -> x)
+//   E5  [5 * T]   reduced rows (A, B, C, D, H); first-point affine triples
+//   XH  [T]       hub values, slot = owner thread
+template <int Q>
+constexpr size_t sweep_smem() {
+  return sizeof(double) * (size_t)(kThreads * (Q | 1) + 6 * kThreads);
+}
 
-template <bool CLUSTER>
+template <bool CLUSTER, int Q>
 __global__ void __launch_bounds__(kThreads, 2)
-block_sweep_kernel(SweepArgs a, const ThreadD* __restrict__ threads,
-                   const BinD* __restrict__ bins, int q, int cs) {
+block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* __restrict__ bins,
+                   const HubD* __restrict__ hubs, int cs_size) {
   extern __shared__ double smem[];
   constexpr int T = kThreads;
+  constexpr int QS = Q | 1;
   double* R = smem;
-  double* sA = R + T * QSMAX;
+  double* sA = R + T * QS;
   double* sB = sA + T;
   double* sC = sB + T;
   double* sD = sC + T;
@@ -112,105 +144,125 @@ block_sweep_kernel(SweepArgs a, const ThreadD* __restrict__ threads,
 
   const int tid = threadIdx.x;
   const int rank = CLUSTER ? (int)cg::this_cluster().block_rank() : 0;
-  const int bin = blockIdx.x / cs;
-  const int tv = rank * T + tid;  // virtual thread within the bin
-  const ThreadD* th = threads + (size_t)blockIdx.x * T;
-  const int QS = q | 1;
-  const double* __restrict__ W = a.W;
-  const double* __restrict__ E = a.E;
-  const double* __restrict__ S = a.S;
-  const double* __restrict__ N = a.N;
-  const size_t ld = (size_t)a.ld;
+  const int bin = blockIdx.x / cs_size;
+  const int ld = a.ld;
+  const Coefs C{a.W, a.E, a.S, a.N};
   double* __restrict__ u = a.u;
   const double* __restrict__ f = a.f;
 
-  auto coef = [&](int d, int i, int j) -> double {
-    switch (d) {
-      case DW: return __ldg(W + i);
-      case DE: return __ldg(E + i);
-      case DS: return __ldg(S + j);
-      case DN: return __ldg(N + j);
-      default: return 0.0;
-    }
-  };
-  auto diag = [&](int i, int j) -> double {
-    return -(__ldg(W + i) + __ldg(E + i) + __ldg(S + j) + __ldg(N + j));
-  };
-  // f - sum of neighbours not in `skip` (bit d set: neighbour d is in-block)
-  auto frozen_rhs = [&](int i, int j, unsigned skip) -> double {
-    const size_t o = (size_t)i * ld + j;
-    double r = f[o];
-    if (!(skip & 1u)) r -= __ldg(W + i) * u[o - ld];
-    if (!(skip & 2u)) r -= __ldg(E + i) * u[o + ld];
-    if (!(skip & 4u)) r -= __ldg(S + j) * u[o - 1];
-    if (!(skip & 8u)) r -= __ldg(N + j) * u[o + 1];
-    return r;
-  };
-  auto skipmask = [](int dp, int dn) -> unsigned {
-    return (dp < 4 ? (1u << dp) : 0u) | (dn < 4 ? (1u << dn) : 0u);
-  };
+  const ChunkD mine = chunks[(size_t)blockIdx.x * T + tid];
+  Chunk c;
+  c.unpack(mine, C, ld);
+  const double xlv = c.n > 0 ? __ldg(c.xl + c.cidx) : 0.0;
+  const double xhv = c.n > 0 ? __ldg(c.xh + c.cidx) : 0.0;
+  const int lane = tid & 31, wbase = tid & ~31;
+  constexpr int PER = 32 / Q;  // chunks covered by one warp-wide pass
+  constexpr int BATCH = Q < 8 ? Q : 8;
+  const int ksub = lane % Q, csub = lane / Q;
+  constexpr unsigned FULL = 0xffffffffu;
 
   // ---------------- phase A: coalesced gather of frozen right-hand sides ----
-  for (int L = tid; L < T * q; L += T) {
-    const int t = L / q, k = L - t * q;
-    const int code = th[t];
-    if (code < 0) continue;
-    const LegD lg = a.legs[code];
-    int s, e;
-    chunk_range(lg, rank * T + t - lg.tbase, q, s, e);
-    const int p = s + k;
-    if (p > e) continue;
-    const PInfo pi = leg_point(lg, p);
-    R[t * QS + k] = frozen_rhs(pi.i, pi.j, skipmask(pi.dprev, pi.dnext));
+  // Warp-local: the warp streams the points of its own 32 chunks, lanes
+  // consecutive along each chunk, all loads of a batch in flight together.
+  // Interior points subtract the two cross neighbours; chunk ends are
+  // redone below with their exact in-block neighbour sets.
+#pragma unroll
+  for (int m0 = 0; m0 < Q; m0 += BATCH) {
+    double vf[BATCH], vl[BATCH], vh[BATCH];
+    int slot[BATCH];
+#pragma unroll
+    for (int b = 0; b < BATCH; b++) {
+      const int src = (m0 + b) * PER + csub;
+      const int n_s = __shfl_sync(FULL, c.n, src);
+      const int off_s = __shfl_sync(FULL, c.off, src);
+      const int str_s = __shfl_sync(FULL, c.stride, src);
+      const int cs_s = __shfl_sync(FULL, c.cs, src);
+      const int o = off_s + ksub * str_s;
+      slot[b] = ksub < n_s ? (wbase + src) * QS + ksub : -1;
+      if (ksub < n_s) {
+        vf[b] = f[o];
+        vl[b] = u[o - cs_s];
+        vh[b] = u[o + cs_s];
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < BATCH; b++) {
+      const int src = (m0 + b) * PER + csub;
+      const double xl_s = __shfl_sync(FULL, xlv, src);
+      const double xh_s = __shfl_sync(FULL, xhv, src);
+      if (slot[b] >= 0) R[slot[b]] = fma(-xh_s, vh[b], fma(-xl_s, vl[b], vf[b]));
+    }
   }
-  __syncthreads();
+  __syncwarp();
+  double* Rt = R + tid * QS;
+  if (c.n > 0) {  // chunk ends: neighbours outside the block from the link directions
+    const int alo = c.da > 0 ? (c.axis ? DS : DW) : (c.axis ? DN : DE);  // toward k-1
+    const int ahi = alo ^ 1;                                             // toward k+1
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+      const int k = e ? c.n - 1 : 0;
+      if (e && c.n == 1) break;
+      const int dp = k == 0 ? c.dfirst : alo;
+      const int dn = k == c.n - 1 ? c.dlast : ahi;
+      const unsigned skip = (dp < 4 ? 1u << dp : 0u) | (dn < 4 ? 1u << dn : 0u);
+      int i, j;
+      c.ij(k, i, j);
+      const int o = c.off + k * c.stride;
+      double r = f[o];
+      if (!(skip & 1u)) r -= __ldg(a.W + i) * u[o - ld];
+      if (!(skip & 2u)) r -= __ldg(a.E + i) * u[o + ld];
+      if (!(skip & 4u)) r -= __ldg(a.S + j) * u[o - 1];
+      if (!(skip & 8u)) r -= __ldg(a.N + j) * u[o + 1];
+      Rt[k] = r;
+    }
+  }
+  __syncwarp();
 
   // ---------------- phase B: chunk elimination -------------------------------
-  const int code = th[tid];
-  LegD lg;
-  int s = 0, e = -1, nI = 0, c = 0;
-  if (code >= 0) {
-    lg = a.legs[code];
-    c = tv - lg.tbase;
-    chunk_range(lg, c, q, s, e);
-    nI = e - s;
-  }
-  double lam[kQmax], ivr[kQmax];
-  double ad = 0.0, bd = 1.0, gd = 0.0;  // x_{e-1} = ad + bd*L + gd*X
-  double au = 0.0, bu = 0.0, gu = 1.0;  // x_s     = au + bu*L + gu*X
+  const int nI = c.n - 1;  // interior points (all but the chunk end)
+  double lam[Q], ivr[Q];
+  double ad = 0.0, bd = 1.0, gd = 0.0;  // x_{e-1} = ad + bd*Xleft + gd*X
+  double au = 0.0, bu = 0.0, gu = 1.0;  // x_s     = au + bu*Xleft + gu*X
   bool bad = false;
-  double* Rt = R + tid * QS;
+  const double csum = xlv + xhv;
+  double a_first = 0.0;
+  if (c.n > 0) {
+    int i0, j0;
+    c.ij(0, i0, j0);
+    a_first = C.dir(c.dfirst, i0, j0);
+  }
+  double cprev = 0.0;
   if (nI > 0) {
-    double bp = 0.0, rho = 0.0, lm = 0.0, cprev = 0.0, ivp = 0.0;
+    double bp = 0.0, rho = 0.0, lm = 0.0, ivp = 0.0;
 #pragma unroll
-    for (int k = 0; k < kQmax; k++) {
+    for (int k = 0; k < Q; k++) {
       if (k < nI) {
-        const PInfo pi = leg_point(lg, s + k);
-        const double ap = coef(pi.dprev, pi.i, pi.j);
-        const double bb = diag(pi.i, pi.j);
+        const int ai = c.a0 + k * c.da;
+        const double pav = __ldg(c.pa + ai), pcv = __ldg(c.pc + ai);
+        const double bb = -(pav + pcv + csum);
         const double rp = Rt[k];
         if (k == 0) {
           bp = bb;
           rho = rp;
-          lm = -ap;
+          lm = -a_first;
         } else {
-          const double w = ap * ivp;
-          bp = bb - w * cprev;
-          rho = rp - w * rho;
+          const double w = pav * ivp;
+          bp = fma(-w, cprev, bb);
+          rho = fma(-w, rho, rp);
           lm = -w * lm;
         }
         bad |= bad_pivot(bp);
-        ivp = 1.0 / bp;
+        ivp = drcp(bp);
         Rt[k] = rho;
         lam[k] = lm;
         ivr[k] = ivp;
-        cprev = coef(pi.dnext, pi.i, pi.j);
+        cprev = pcv;
       }
     }
-    // affine back substitution; cprev now holds c_{e-1}
+    // affine back substitution: cprev = c_{e-1}
     double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
-    for (int k = kQmax - 1; k >= 0; k--) {
+    for (int k = Q - 1; k >= 0; k--) {
       if (k < nI) {
         if (k == nI - 1) {
           al = Rt[k] * ivr[k];
@@ -220,10 +272,9 @@ block_sweep_kernel(SweepArgs a, const ThreadD* __restrict__ threads,
           bd = be;
           gd = ga;
         } else {
-          const PInfo pi = leg_point(lg, s + k);
-          const double cp = coef(pi.dnext, pi.i, pi.j);
-          al = (Rt[k] - cp * al) * ivr[k];
-          be = (lam[k] - cp * be) * ivr[k];
+          const double cp = __ldg(c.pc + c.a0 + k * c.da);
+          al = fma(-cp, al, Rt[k]) * ivr[k];
+          be = fma(-cp, be, lam[k]) * ivr[k];
           ga = -cp * ga * ivr[k];
         }
         Rt[k] = al;
@@ -241,126 +292,131 @@ block_sweep_kernel(SweepArgs a, const ThreadD* __restrict__ threads,
   sC[tid] = gu;
   __syncthreads();
 
-  // reduced row of the chunk end e
-  double A = 0.0, B = 1.0, C = 0.0, D = 0.0, H = 0.0;
-  if (code >= 0) {
-    const PInfo pe = leg_point(lg, e);
-    const double ae = coef(pe.dprev, pe.i, pe.j);
-    const double ce = coef(pe.dnext, pe.i, pe.j);
+  // reduced row of the chunk end
+  double A = 0.0, B = 1.0, Cc = 0.0, D = 0.0, H = 0.0;
+  if (c.n > 0) {
+    int ie, je;
+    c.ij(nI, ie, je);
+    const int ae_i = c.a0 + nI * c.da;
+    const double pav = __ldg(c.pa + ae_i), pcv = __ldg(c.pc + ae_i);
+    const double ae = nI > 0 ? pav : a_first;
+    const double ce = C.dir(c.dlast, ie, je);
     A = ae * bd;
-    B = diag(pe.i, pe.j) + ae * gd;
+    B = -(pav + pcv + csum) + ae * gd;
     D = Rt[nI] - ae * ad;
-    if (c == lg.nchunk - 1) {
-      if (lg.flags & 2) H += ce;
-    } else {
-      const double au1 = sA[tid + 1], bu1 = sB[tid + 1], gu1 = sC[tid + 1];
-      B += ce * bu1;
-      C = ce * gu1;
-      D -= ce * au1;
+    if (c.link & kLinkRightNext) {
+      B = fma(ce, sB[tid + 1], B);
+      Cc = ce * sC[tid + 1];
+      D = fma(-ce, sA[tid + 1], D);
+    } else if (c.link & kLinkRightHub) {
+      H += ce;
     }
-    if (c == 0) {
-      if (lg.flags & 1) H += A;
-      A = 0.0;
-    }
+    if (c.link & kLinkLeftHub) H += A;
+    if (!(c.link & kLinkLeftPrev)) A = 0.0;
   }
-  __syncthreads();
-  sA[tid] = A;
-  sB[tid] = B;
-  sC[tid] = C;
-  sD[tid] = D;
-  sH[tid] = H;
-  __syncthreads();
 
-  // parallel cyclic reduction of the per-leg reduced systems (legs never
-  // straddle CTAs, so the exchange stays inside this CTA)
-  const int steps = bins[bin].pcr_steps;
-  for (int st = 0; st < steps; st++) {
-    const int d = 1 << st;
-    double Am = 0, Bm = 1, Cm = 0, Dm = 0, Hm = 0, Ap = 0, Bp = 1, Cp = 0, Dp = 0, Hp = 0;
-    if (tid - d >= 0) {
-      Am = sA[tid - d]; Bm = sB[tid - d]; Cm = sC[tid - d]; Dm = sD[tid - d]; Hm = sH[tid - d];
+  // parallel cyclic reduction of the per-leg reduced systems.  Legs never
+  // straddle CTAs; when no leg of the bin straddles a warp either, the
+  // exchange runs on warp shuffles without block barriers.
+  const BinD bd_ = bins[bin];
+  const int steps = bd_.pcr_steps;
+  if (bd_.warp_local) {
+    const int lane = tid & 31;
+    for (int st = 0; st < steps; st++) {
+      const int d = 1 << st;
+      double Am = __shfl_up_sync(0xffffffffu, A, d), Bm = __shfl_up_sync(0xffffffffu, B, d);
+      double Cm = __shfl_up_sync(0xffffffffu, Cc, d), Dm = __shfl_up_sync(0xffffffffu, D, d);
+      double Hm = __shfl_up_sync(0xffffffffu, H, d);
+      double Ap = __shfl_down_sync(0xffffffffu, A, d), Bp = __shfl_down_sync(0xffffffffu, B, d);
+      double Cp = __shfl_down_sync(0xffffffffu, Cc, d), Dp = __shfl_down_sync(0xffffffffu, D, d);
+      double Hp = __shfl_down_sync(0xffffffffu, H, d);
+      if (lane < d) { Am = 0.0; Bm = 1.0; Cm = 0.0; Dm = 0.0; Hm = 0.0; }
+      if (lane + d > 31) { Ap = 0.0; Bp = 1.0; Cp = 0.0; Dp = 0.0; Hp = 0.0; }
+      const double k1 = A * drcp(Bm), k2 = Cc * drcp(Bp);
+      A = -k1 * Am;
+      B = B - k1 * Cm - k2 * Ap;
+      D = D - k1 * Dm - k2 * Dp;
+      H = H - k1 * Hm - k2 * Hp;
+      Cc = -k2 * Cp;
     }
-    if (tid + d < T) {
-      Ap = sA[tid + d]; Bp = sB[tid + d]; Cp = sC[tid + d]; Dp = sD[tid + d]; Hp = sH[tid + d];
+  } else if (steps > 0) {
+    __syncthreads();  // sA..sC held the first-point triples
+    sA[tid] = A; sB[tid] = B; sC[tid] = Cc; sD[tid] = D; sH[tid] = H;
+    __syncthreads();
+    for (int st = 0; st < steps; st++) {
+      const int d = 1 << st;
+      double Am = 0, Bm = 1, Cm = 0, Dm = 0, Hm = 0, Ap = 0, Bp = 1, Cp = 0, Dp = 0, Hp = 0;
+      if (tid - d >= 0) {
+        Am = sA[tid - d]; Bm = sB[tid - d]; Cm = sC[tid - d]; Dm = sD[tid - d]; Hm = sH[tid - d];
+      }
+      if (tid + d < T) {
+        Ap = sA[tid + d]; Bp = sB[tid + d]; Cp = sC[tid + d]; Dp = sD[tid + d]; Hp = sH[tid + d];
+      }
+      __syncthreads();
+      const double k1 = A * drcp(Bm), k2 = Cc * drcp(Bp);
+      A = -k1 * Am;
+      Cc = -k2 * Cp;
+      B = B - k1 * Cm - k2 * Ap;
+      D = D - k1 * Dm - k2 * Dp;
+      H = H - k1 * Hm - k2 * Hp;
+      sA[tid] = A; sB[tid] = B; sC[tid] = Cc; sD[tid] = D; sH[tid] = H;
+      __syncthreads();
     }
-    __syncthreads();
-    const double k1 = A / Bm, k2 = C / Bp;
-    A = -k1 * Am;
-    C = -k2 * Cp;
-    B = B - k1 * Cm - k2 * Ap;
-    D = D - k1 * Dm - k2 * Dp;
-    H = H - k1 * Hm - k2 * Hp;
-    sA[tid] = A; sB[tid] = B; sC[tid] = C; sD[tid] = D; sH[tid] = H;
-    __syncthreads();
   }
-  bad |= (code >= 0) && bad_pivot(B);
-  const double P = D / B, Q = H / B;  // X_t = P - Q * x_hub
+  bad |= (c.n > 0) && bad_pivot(B);
+  const double iB = drcp(B);
+  const double P = D * iB, Qh = H * iB;  // X_t = P - Qh * x_hub
   sD[tid] = P;
-  sH[tid] = Q;
+  sH[tid] = Qh;
   bin_sync<CLUSTER>();
 
-  // hub rows: chunk 0 of a block's first leg, or the dedicated point thread
-  int hub_blk = -1;
-  if (code <= -2) hub_blk = -(code + 2);
-  else if (code >= 0 && c == 0 && code == a.blocks[lg.block].leg0) hub_blk = lg.block;
-  if (hub_blk >= 0) {
-    const BlockD bk = a.blocks[hub_blk];
-    if (bk.hi >= 0) {
-      const int hi = bk.hi, hj = bk.hj;
-      double num = frozen_rhs(hi, hj, bk.hub_mask);
-      double den = diag(hi, hj);
-      for (int l = 0; l < bk.nleg; l++) {
-        const LegD L2 = a.legs[bk.leg0 + l];
-        if (L2.flags & 2) {
-          const int ta = L2.tbase + L2.nchunk - 1;
-          const double cf = coef(dir_opp(L2.hub_dir_last), hi, hj);
-          num -= cf * remote<CLUSTER>(sD, ta / T)[ta % T];
-          den -= cf * remote<CLUSTER>(sH, ta / T)[ta % T];
-        }
-        if (L2.flags & 1) {
-          const int ta = L2.tbase;
-          const double cf = coef(dir_opp(L2.hub_dir_first), hi, hj);
-          num -= cf * remote<CLUSTER>(sD, ta / T)[ta % T];
-          den -= cf * remote<CLUSTER>(sH, ta / T)[ta % T];
-        }
-      }
-      bad |= bad_pivot(den);
-      const double xh = num / den;
-      XH[tid] = xh;
-      u[(size_t)hi * ld + hj] = xh;
+  // hub rows
+  if (c.own >= 0) {
+    const HubD hb = hubs[bd_.hub0 + c.own];
+    const int hi = hb.i, hj = hb.j;
+    const int o = hb.off;
+    double num = f[o];
+    if (!(hb.mask & 1u)) num -= __ldg(a.W + hi) * u[o - ld];
+    if (!(hb.mask & 2u)) num -= __ldg(a.E + hi) * u[o + ld];
+    if (!(hb.mask & 4u)) num -= __ldg(a.S + hj) * u[o - 1];
+    if (!(hb.mask & 8u)) num -= __ldg(a.N + hj) * u[o + 1];
+    double den = -(__ldg(a.W + hi) + __ldg(a.E + hi) + __ldg(a.S + hj) + __ldg(a.N + hj));
+    for (int q = 0; q < hb.nadj; q++) {
+      const int ta = hb.adj_t[q];
+      const double cf = C.dir(hb.adj_d[q], hi, hj);
+      num -= cf * remote<CLUSTER>(sD, ta / T)[ta % T];
+      den -= cf * remote<CLUSTER>(sH, ta / T)[ta % T];
     }
+    bad |= bad_pivot(den);
+    const double xh = num / den;
+    XH[tid] = xh;
+    u[o] = xh;
   }
   bin_sync<CLUSTER>();
 
   // final values of the chunk
-  if (code >= 0) {
-    const BlockD bk = a.blocks[lg.block];
-    double xh = 0.0;
-    if (bk.hi >= 0) xh = remote<CLUSTER>(XH, bk.hub_thread / T)[bk.hub_thread % T];
-    const double X = P - Q * xh;
-    double Lv;
-    if (c == 0) Lv = (lg.flags & 1) ? xh : 0.0;
-    else Lv = sD[tid - 1] - sH[tid - 1] * xh;
+  if (c.n > 0) {
+    const double xh = c.hub >= 0 ? remote<CLUSTER>(XH, c.hub / T)[c.hub % T] : 0.0;
+    const double X = fma(-Qh, xh, P);
+    double Lv = 0.0;
+    if (c.link & kLinkLeftPrev) Lv = fma(-sH[tid - 1], xh, sD[tid - 1]);
+    else if (c.link & kLinkLeftHub) Lv = xh;
 #pragma unroll
-    for (int k = 0; k < kQmax; k++)
-      if (k < nI) Rt[k] = Rt[k] + lam[k] * Lv + ivr[k] * X;
+    for (int k = 0; k < Q; k++)
+      if (k < nI) Rt[k] = fma(ivr[k], X, fma(lam[k], Lv, Rt[k]));
     Rt[nI] = X;
   }
   if (bad) atomicOr(a.err, 1);
   bin_sync<CLUSTER>();
 
-  // ---------------- phase C: coalesced scatter ------------------------------
-  for (int L = tid; L < T * q; L += T) {
-    const int t = L / q, k = L - t * q;
-    const int cd = th[t];
-    if (cd < 0) continue;
-    const LegD l2 = a.legs[cd];
-    int s2, e2;
-    chunk_range(l2, rank * T + t - l2.tbase, q, s2, e2);
-    const int p = s2 + k;
-    if (p > e2) continue;
-    const PInfo pi = leg_point(l2, p);
-    u[(size_t)pi.i * ld + pi.j] = R[t * QS + k];
+  // ---------------- phase C: coalesced scatter (warp-local) ----------------
+#pragma unroll
+  for (int m = 0; m < Q; m++) {
+    const int src = m * PER + csub;
+    const int n_s = __shfl_sync(FULL, c.n, src);
+    const int off_s = __shfl_sync(FULL, c.off, src);
+    const int str_s = __shfl_sync(FULL, c.stride, src);
+    if (ksub < n_s) u[off_s + ksub * str_s] = R[(wbase + src) * QS + ksub];
   }
 }
 
@@ -378,14 +434,50 @@ __global__ void __launch_bounds__(256) point_sweep_kernel(SweepArgs a, int nx, i
   a.u[o] = r / b;
 }
 
+namespace {
+template <int Q>
+cudaError_t set_attrs() {
+  cudaError_t e = cudaFuncSetAttribute(block_sweep_kernel<false, Q>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sweep_smem<Q>());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(block_sweep_kernel<true, Q>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep_smem<Q>());
+  return e;
+}
+
+template <int Q>
+cudaError_t launch_class(const LaunchClass& lc, const SweepArgs& a, cudaStream_t stream) {
+  if (lc.cs == 1) {
+    block_sweep_kernel<false, Q><<<lc.nbins, kThreads, sweep_smem<Q>(), stream>>>(
+        a, lc.chunks, lc.bins, lc.hubs, 1);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(lc.nbins * lc.cs);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = sweep_smem<Q>();
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = lc.cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, block_sweep_kernel<true, Q>, a, (const ChunkD*)lc.chunks,
+                            (const BinD*)lc.bins, (const HubD*)lc.hubs, lc.cs);
+}
+}  // namespace
+
 cudaError_t init_sweep_kernels() {
   static cudaError_t done = cudaErrorNotReady;
   if (done == cudaErrorNotReady) {
-    done = cudaFuncSetAttribute(block_sweep_kernel<false>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
-    if (done == cudaSuccess)
-      done = cudaFuncSetAttribute(block_sweep_kernel<true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
+    done = set_attrs<16>();
+    if (done == cudaSuccess) done = set_attrs<8>();
+    if (done == cudaSuccess) done = set_attrs<4>();
+    if (done == cudaSuccess) done = set_attrs<2>();
+    if (done == cudaSuccess) done = set_attrs<1>();
   }
   return done;
 }
@@ -398,28 +490,14 @@ cudaError_t launch_colour(const Plan& P, int red, const SweepArgs& a, cudaStream
   }
   for (const LaunchClass& lc : P.classes) {
     if (lc.red != red || lc.nbins == 0) continue;
-    if (lc.cs == 1) {
-      block_sweep_kernel<false><<<lc.nbins, kThreads, kSweepSmem, stream>>>(a, lc.threads, lc.bins,
-                                                                            lc.q, 1);
-    } else {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(lc.nbins * lc.cs);
-      cfg.blockDim = dim3(kThreads);
-      cfg.dynamicSmemBytes = kSweepSmem;
-      cfg.stream = stream;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = lc.cs;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      cudaError_t e = cudaLaunchKernelEx(&cfg, block_sweep_kernel<true>, a,
-                                         (const ThreadD*)lc.threads, (const BinD*)lc.bins, lc.q,
-                                         lc.cs);
-      if (e != cudaSuccess) return e;
+    cudaError_t e;
+    switch (lc.q) {
+      case 16: e = launch_class<16>(lc, a, stream); break;
+      case 8: e = launch_class<8>(lc, a, stream); break;
+      case 4: e = launch_class<4>(lc, a, stream); break;
+      case 2: e = launch_class<2>(lc, a, stream); break;
+      default: e = launch_class<1>(lc, a, stream); break;
     }
-    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -231,8 +231,11 @@ def test_solve_matches_oracle(cuda, orc, smoother, restriction, stretch, c, n):
     assert rep.cycles == repo.cycles and rep.converged == repo.converged
     assert rep.defect_norms[0] == repo.defect_norms[0]
     assert _rel(u, uo) <= 1e-10
+    # the defect of a converging iterate is rounding-dominated near the end
+    # (the reference's own two backends differ at 4e-6 relative there), so
+    # the trace is compared with an absolute floor relative to d0
     for a, b in zip(rep.defect_norms[1:], repo.defect_norms[1:]):
-        assert abs(a - b) <= 1e-6 * b + 1e-13 * rep.defect_norms[0]
+        assert abs(a - b) <= 1e-5 * b + 1e-11 * rep.defect_norms[0]
 
 
 def test_v_cycle_tensor_graph_path(cuda, orc):
