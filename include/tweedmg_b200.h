@@ -102,6 +102,22 @@ int tmg_vcycle_graph(tmg_hier* h, int kind, int full, int nu1, int nu2, double* 
                      const double* f, int reps, void* stream);
 /* kernel nodes in the most recently replayed V-cycle graph (launches/cycle) */
 int tmg_hier_graph_kernels(tmg_hier* h);
+/* bytes of device work fields held by the hierarchy */
+long long tmg_hier_device_bytes(tmg_hier* h);
+
+/* ---- solver sessions: the hierarchy keeps u and f of the finest level in
+ *      its working layout (the smoother's preferred hybrid N/T layout, see
+ *      DESIGN.md) across calls.  tmg_vcycle / tmg_solve are load + cycles +
+ *      store on the caller's C-order arrays. */
+int tmg_session_load(tmg_hier* h, int kind, const double* u, const double* f, void* stream);
+int tmg_session_cycles(tmg_hier* h, int kind, int full, int nu1, int nu2, int reps,
+                       void* stream);
+/* finest-level max |f - L u| of the session, plus the pivot flags; synchronizes */
+int tmg_session_norm(tmg_hier* h, double* out_host, void* stream);
+int tmg_session_store(tmg_hier* h, double* u, void* stream);
+/* `reps` finest-level sweeps on the session's fields (smoothers.sweep on the
+ * solver state; used to time the smoother alone) */
+int tmg_session_sweeps(tmg_hier* h, int kind, int reps, void* stream);
 
 /* ---- block geometry (layout.py:61-168): per-member (i, j, block, flags) in
  *      the reference's member order (legs tip -> branch then the branch; rings
@@ -127,6 +143,12 @@ int tmg_relax_legged(long n, const int64_t* ii, const int64_t* jj, long m, const
                      long bi, long bj, int nx, int ny, const double* W, const double* E,
                      const double* S, const double* N, double* u, const double* f,
                      void* stream);
+
+/* ---- profiling aid: average per-CTA cycles between the phase marks of the
+ *      block-solver kernel (gather, elimination, reduced solve, hub, finalize,
+ *      scatter) over the last launch; non-zero only in builds made with
+ *      EXTRA=-DTMG_PHASE_TIMING.  Returns the number of CTAs sampled. */
+int tmg_debug_phase_cycles(double* out6);
 
 #ifdef __cplusplus
 }

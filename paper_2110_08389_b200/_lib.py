@@ -56,6 +56,13 @@ def _declare(L):
         "tmg_vcycle": ([vp, ip, ip, ip, ip, vp, vp, vp], ip),
         "tmg_vcycle_graph": ([vp, ip, ip, ip, ip, vp, vp, ip, vp], ip),
         "tmg_hier_graph_kernels": ([vp], ip),
+        "tmg_hier_device_bytes": ([vp], ctypes.c_longlong),
+        "tmg_session_load": ([vp, ip, vp, vp, vp], ip),
+        "tmg_session_cycles": ([vp, ip, ip, ip, ip, ip, vp], ip),
+        "tmg_session_norm": ([vp, pd, vp], ip),
+        "tmg_session_store": ([vp, vp, vp], ip),
+        "tmg_session_sweeps": ([vp, ip, ip, vp], ip),
+        "tmg_debug_phase_cycles": ([pd], ip),
         "tmg_solve": ([vp, ip, ip, ip, ip, dp, ip, vp, vp, pd, pi, pi, vp], ip),
         "tmg_layout_dump": ([ip, ip, ip, pi, pi, pi, pi, lp], lp),
         "tmg_relax_points": ([lp, vp, vp, ip, ip, vp, vp, vp, vp, vp, vp, vp], ip),

@@ -62,7 +62,8 @@ struct ChunkD {
   int16_t hub;    // virtual thread that owns the block's hub value, -1 if none
   int16_t own;    // index of the hub this thread solves (within the bin), -1
   uint8_t n;      // points in the chunk (0: no chunk)
-  uint8_t geo;    // bit 0: axis (0: i varies, 1: j varies); bit 1: decreasing
+  uint8_t geo;    // bit 0: axis (0: i varies, 1: j varies); bit 1: decreasing;
+                  // bit 2: the chunk lives in the transposed buffer (tmg_layout.h)
   uint16_t link;  // bits 0-2 dfirst, 3-5 dlast (direction from the first /
                   // last point to its in-block neighbour outside the chunk,
                   // 7 = none); bit 6 left = previous thread, bit 7 left = hub,
@@ -81,7 +82,8 @@ struct HubD {
   uint8_t nadj;       // adjacent chunk ends (0..4)
   int16_t adj_t[4];   // virtual thread whose reduced unknown is that point
   uint8_t adj_d[4];   // direction from the hub to that point
-  uint8_t pad[2];
+  uint8_t tbuf;       // 1: the hub point lives in the transposed buffer
+  uint8_t pad;
 };
 static_assert(sizeof(HubD) == 24, "HubD layout");
 

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include "tmg_internal.h"
+#include "tmg_layout.h"
 #include "tmg_plan.h"
 
 namespace tmg {
@@ -14,10 +15,15 @@ struct SweepArgs {
   const double* E;
   const double* S;
   const double* N;
-  double* u;
+  double* u;         // N buffer (C order)
   const double* f;
-  int ld;    // row length ny + 1
-  int* err;  // device error flags (bit 0: vanishing pivot)
+  int ld;            // N row length ny + 1
+  int* err;          // device error flags (bit 0: vanishing pivot)
+  double* ut;        // T buffer (== u in LM_NATURAL)
+  const double* ft;
+  int ldt;           // T row length nx + 1
+  int mode;          // LayoutMode of u / f
+  int nx, ny;
 };
 
 // Set kernel attributes once (host only, never inside stream capture).
@@ -57,5 +63,18 @@ cudaError_t launch_prolong_correct(int nxc, int nyc, const double* uc, double* u
 // operator (j-outer ordering, stencil.py:111): u_int = Ainv (f - B u_bdry).
 cudaError_t launch_dense_solve(const GridArgs& g, const double* Ainv, double* u,
                                const double* f, double* work, cudaStream_t s);
+
+// ---- hybrid-layout (tmg_layout.h) versions used inside the V-cycle ----
+cudaError_t launch_hdefect_norm(const GridArgs& g, const FieldView& U, const FieldView& F,
+                                unsigned long long* dmax, cudaStream_t s);
+cudaError_t launch_hdefect_restrict(const GridArgs& g, int full, const FieldView& U,
+                                    const FieldView& F, const FieldView& FC, cudaStream_t s);
+// u += P uc on the fine interior; (nx, ny) are the FINE dimensions
+cudaError_t launch_hprolong_correct(int nx, int ny, const FieldView& C, const FieldView& U,
+                                    cudaStream_t s);
+cudaError_t launch_to_hybrid(const FieldView& V, const double* nat, cudaStream_t s);
+cudaError_t launch_from_hybrid(const FieldView& V, double* nat, cudaStream_t s);
+cudaError_t launch_hdense_solve(const GridArgs& g, const double* Ainv, const FieldView& U,
+                                const FieldView& F, double* work, cudaStream_t s);
 
 }  // namespace tmg

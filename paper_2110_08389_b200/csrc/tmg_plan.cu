@@ -13,6 +13,20 @@ namespace {
 
 int parity_red(int k) { return (k % 2) != 0; }  // layout.py:22-23
 
+void leg_point_host(const LegD& L, int p, int& i, int& j) {
+  i = L.i0;
+  j = L.j0;
+  int rem = p;
+  for (int s = 0; s < L.nseg && rem > 0; s++) {
+    int st = std::min(rem, L.seg_len[s]);
+    i += st * dir_di(L.seg_dir[s]);
+    j += st * dir_dj(L.seg_dir[s]);
+    rem -= st;
+  }
+}
+
+
+
 struct Builder {
   Geometry& g;
   explicit Builder(Geometry& gg) : g(gg) {}
@@ -173,9 +187,13 @@ int step_direction(const LegD& L, int p) {
 // Split a leg into straight runs (pieces) and the pieces into chunks of at
 // most q points.  A leg whose first point couples to the hub starts with a
 // one-point chunk, so that every hub neighbour is a chunk end (a reduced
-// unknown).  Returns [first, last] point ranges.
-std::vector<std::pair<int, int>> leg_chunks(const LegD& L, int q) {
-  std::vector<std::pair<int, int>> pieces, out;
+// unknown).  With a hybrid field layout a run is further cut wherever the
+// owning buffer changes, and a point whose cross neighbour lives in the other
+// buffer becomes a one-point chunk, so that inside every chunk the point and
+// its two cross neighbours are addressed through one buffer with fixed
+// strides.  Returns [first, last] point ranges.
+std::vector<std::pair<int, int>> leg_chunks(const LegD& L, int q, int mode, int nx, int ny) {
+  std::vector<std::pair<int, int>> pieces, runs, out;
   int start = 0;
   if (L.flags & 1) {
     pieces.push_back({0, 0});
@@ -191,8 +209,50 @@ std::vector<std::pair<int, int>> leg_chunks(const LegD& L, int q) {
     cum = endp;
   }
   if (start <= L.npts - 1) pieces.push_back({start, L.npts - 1});
-  for (auto& pc : pieces)
-    for (int a = pc.first; a <= pc.second; a += q) out.push_back({a, std::min(a + q - 1, pc.second)});
+  auto interior = [&](int i, int j) { return i > 0 && j > 0 && i < nx && j < ny; };
+  // A chunk's end points are addressed one by one (tmg_sweep.cu); only its
+  // inner points need their cross neighbours in the chunk's own buffer.
+  std::vector<char> bad;
+  for (auto& pc : pieces) {
+    if (mode == LM_NATURAL || pc.first == pc.second) {
+      for (int a = pc.first; a <= pc.second; a += q)
+        out.push_back({a, std::min(a + q - 1, pc.second)});
+      continue;
+    }
+    const int d = step_direction(L, pc.first + 1);
+    const bool axis_i = (d == DW || d == DE);
+    bad.assign(pc.second - pc.first + 1, 0);
+    runs.clear();
+    int rs = pc.first, rown = -1;
+    for (int p = pc.first; p <= pc.second; p++) {
+      int i, j;
+      leg_point_host(L, p, i, j);
+      const int o = owns_t(mode, nx, ny, i, j);
+      const int i1 = axis_i ? i : i - 1, j1 = axis_i ? j - 1 : j;
+      const int i2 = axis_i ? i : i + 1, j2 = axis_i ? j + 1 : j;
+      bad[p - pc.first] = (interior(i1, j1) && owns_t(mode, nx, ny, i1, j1) != (bool)o) ||
+                          (interior(i2, j2) && owns_t(mode, nx, ny, i2, j2) != (bool)o);
+      if (p > pc.first && o != rown) {  // the owning buffer changes
+        runs.push_back({rs, p - 1});
+        rs = p;
+      }
+      rown = o;
+    }
+    runs.push_back({rs, pc.second});
+    for (auto& r : runs) {
+      int a = r.first;
+      while (a <= r.second) {
+        int e = std::min(a + q - 1, r.second);
+        for (int p = a + 1; p < e; p++)  // a mismatching point may only be a chunk end
+          if (bad[p - pc.first]) {
+            e = p;
+            break;
+          }
+        out.push_back({a, e});
+        a = e + 1;
+      }
+    }
+  }
   return out;
 }
 
@@ -220,18 +280,6 @@ std::string build_geometry(int scheme, int nx, int ny, Geometry& g) {
       return "";
     default:
       return "no block geometry for scheme " + std::to_string(scheme);
-  }
-}
-
-static void leg_point_host(const LegD& L, int p, int& i, int& j) {
-  i = L.i0;
-  j = L.j0;
-  int rem = p;
-  for (int s = 0; s < L.nseg && rem > 0; s++) {
-    int st = std::min(rem, L.seg_len[s]);
-    i += st * dir_di(L.seg_dir[s]);
-    j += st * dir_dj(L.seg_dir[s]);
-    rem -= st;
   }
 }
 
@@ -270,7 +318,7 @@ static T* upload(const std::vector<T>& v, size_t& bytes, std::string& err) {
   return d;
 }
 
-std::string build_plan(int scheme, int nx, int ny, int q, Plan& P) {
+std::string build_plan(int scheme, int nx, int ny, int q, int mode, Plan& P) {
   P = Plan();
   if (q < 1 || q > kQmax) return "chunk size q out of range";
   P.q = q;
@@ -279,28 +327,30 @@ std::string build_plan(int scheme, int nx, int ny, int q, Plan& P) {
     P.geo.scheme = scheme;
     P.geo.nx = nx;
     P.geo.ny = ny;
+    P.mode = mode;
     P.point_scheme = true;
     return "";
   }
   Geometry g;
   std::string err = build_geometry(scheme, nx, ny, g);
   if (!err.empty()) return err;
-  return pack_plan(std::move(g), q, P);
+  return pack_plan(std::move(g), q, mode, P);
 }
 
-std::string pack_plan(Geometry&& geo, int q, Plan& P) {
+std::string pack_plan(Geometry&& geo, int q, int mode, Plan& P) {
   P = Plan();
   if (q < 1 || q > kQmax || (q & (q - 1))) return "chunk size q must be a power of two <= 16";
   P.q = q;
+  P.mode = mode;
   P.geo = std::move(geo);
   Geometry& g = P.geo;
   std::string err;
   const int T = kThreads;
-  const int ld = g.ny + 1;
+  const FieldView fv{nullptr, nullptr, g.nx, g.ny, mode};
 
   std::vector<std::vector<std::pair<int, int>>> lchunks(g.legs.size());
   for (size_t l = 0; l < g.legs.size(); l++) {
-    lchunks[l] = leg_chunks(g.legs[l], q);
+    lchunks[l] = leg_chunks(g.legs[l], q, mode, g.nx, g.ny);
     g.legs[l].nchunk = (int)lchunks[l].size();
     if (g.legs[l].nchunk > T)
       return "leg of " + std::to_string(g.legs[l].npts) +
@@ -394,7 +444,8 @@ std::string pack_plan(Geometry&& geo, int q, Plan& P) {
         if (B.hi >= 0) {
           HubD H;
           std::memset(&H, 0, sizeof(H));
-          H.off = B.hi * ld + B.hj;
+          H.tbuf = owns_t(mode, g.nx, g.ny, B.hi, B.hj) ? 1 : 0;
+          H.off = (int32_t)(H.tbuf ? fv.off_t(B.hi, B.hj) : fv.off_n(B.hi, B.hj));
           H.i = (int16_t)B.hi;
           H.j = (int16_t)B.hj;
           H.mask = B.hub_mask;
@@ -442,11 +493,12 @@ std::string pack_plan(Geometry&& geo, int q, Plan& P) {
               link |= kLinkRightNext;
             }
             ChunkD& C = ch[base + L.tbase + c];
-            C.off = i * ld + j;
+            const bool tb = owns_t(mode, g.nx, g.ny, i, j);
+            C.off = (int32_t)(tb ? fv.off_t(i, j) : fv.off_n(i, j));
             C.a0 = (int16_t)(axis ? j : i);
             C.cidx = (int16_t)(axis ? i : j);
             C.n = (uint8_t)(e - s + 1);
-            C.geo = (uint8_t)(axis | (neg << 1));
+            C.geo = (uint8_t)(axis | (neg << 1) | (tb ? 4 : 0));
             C.link = (uint16_t)(dfirst | (dlast << 3) | link);
             C.hub = (int16_t)owner;
           }

@@ -4,6 +4,7 @@
 #include <vector>
 
 #include "tmg_internal.h"
+#include "tmg_layout.h"
 
 namespace tmg {
 
@@ -27,6 +28,7 @@ long dump_members(const Geometry& g, int* oi, int* oj, int* oblk, int* oflags, l
 struct Plan {
   Geometry geo;
   int q = kQmax;
+  int mode = LM_NATURAL;  // field layout the chunk offsets address
   LegD* d_legs = nullptr;
   BlockD* d_blocks = nullptr;
   std::vector<LaunchClass> classes;  // red classes first, then black
@@ -34,9 +36,9 @@ struct Plan {
   size_t device_bytes = 0;
 };
 
-std::string build_plan(int scheme, int nx, int ny, int q, Plan& p);
+std::string build_plan(int scheme, int nx, int ny, int q, int mode, Plan& p);
 // Pack an explicit geometry (e.g. one block from the per-block shims).
-std::string pack_plan(Geometry&& g, int q, Plan& p);
+std::string pack_plan(Geometry&& g, int q, int mode, Plan& p);
 // Append a block made of explicit member paths (host index arrays).
 // kind: 0 points (each a hub-only block), 1 chain, 2 ring, 3 legged.
 std::string add_explicit_block(Geometry& g, int kind, long n, const long long* ii,

@@ -1,6 +1,7 @@
 // Native runtime behind the C ABI (include/tweedmg_b200.h): level handles
 // with lazily compiled device plans, the coarse direct solver, the V-cycle
-// driver (mgcycle.py:80-139) and the solve loop, CUDA-graph replay.
+// driver (mgcycle.py:80-139) on the hybrid field layout, solver sessions and
+// CUDA-graph replay of whole cycles.
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -26,34 +27,42 @@ int fail(int code, const std::string& msg) {
 int cuda_fail(cudaError_t e, const char* where) {
   return fail(TMG_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
-#define TMG_CUDA_TRY(expr)                                    \
-  do {                                                        \
-    cudaError_t _e = (expr);                                  \
-    if (_e != cudaSuccess) return cuda_fail(_e, #expr);       \
+#define TMG_CUDA_TRY(expr)                              \
+  do {                                                  \
+    cudaError_t _e = (expr);                            \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
   } while (0)
 
 int default_q() {
   const char* s = std::getenv("TMG_CHUNK");
   if (s) {
     int q = std::atoi(s);
-    if (q >= 1 && q <= kQmax) return q;
+    if (q >= 1 && q <= kQmax && !(q & (q - 1))) return q;
   }
   return kQmax;
 }
 
 bool valid_kind(int k) { return k >= TMG_CHECKERBOARD && k <= TMG_TWEED_WIRE_ALT; }
+
+// the hierarchy's working layout: the preferred one of the smoother unless
+// TMG_LAYOUT=natural forces plain C order (for A/B measurements)
+int session_mode(int kind) {
+  const char* s = std::getenv("TMG_LAYOUT");
+  if (s && std::strcmp(s, "natural") == 0) return LM_NATURAL;
+  return layout_for_kind(kind);
+}
 }  // namespace
 
 struct tmg_level {
   int nx = 0, ny = 0, device = 0;
   double *W = nullptr, *E = nullptr, *S = nullptr, *N = nullptr;
   std::vector<double> hW, hE, hS, hN;
-  Plan* plans[7] = {};
+  Plan* plans[7][4] = {};  // [scheme][layout mode]
   int* d_err = nullptr;
   unsigned long long* d_norm = nullptr;
-  int* h_err = nullptr;                 // pinned
-  unsigned long long* h_norm = nullptr; // pinned
-  double* d_ainv = nullptr;  // coarse dense inverse (or the 1x1 operator)
+  int* h_err = nullptr;                  // pinned
+  unsigned long long* h_norm = nullptr;  // pinned
+  double* d_ainv = nullptr;              // coarse dense inverse (or the 1x1 operator)
   double* d_work = nullptr;
   long long bytes = 0;
 
@@ -62,54 +71,66 @@ struct tmg_level {
 
 struct tmg_hier {
   std::vector<tmg_level*> lv;
-  std::vector<double*> u, f;  // per-level work fields (index 0 unused)
-  std::map<std::tuple<int, int, int, int, const void*, const void*, void*>,
-           std::pair<cudaGraphExec_t, int>>
-      graphs;
+  int mode = -1;                // layout of the work fields (-1: not allocated)
+  std::vector<FieldView> U, F;  // work fields of every level (level 0 included)
+  std::vector<double*> blocks;  // allocations
+  bool loaded = false;          // level 0 holds a session's u and f
+  std::map<std::tuple<int, int, int, int>, std::pair<cudaGraphExec_t, int>> graphs;
   int last_kernels = 0;
+  long long bytes = 0;
 };
 
 namespace {
 
-int get_plan(tmg_level* lv, int scheme, Plan** out) {
-  if (!lv->plans[scheme]) {
+int get_plan(tmg_level* lv, int scheme, int mode, Plan** out) {
+  if (!lv->plans[scheme][mode]) {
     cudaError_t e = init_sweep_kernels();
     if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");
     Plan* p = new Plan();
-    std::string err = build_plan(scheme, lv->nx, lv->ny, default_q(), *p);
+    std::string err = build_plan(scheme, lv->nx, lv->ny, default_q(), mode, *p);
     if (!err.empty()) {
       free_plan(*p);
       delete p;
       return fail(TMG_BADARG, err);
     }
-    lv->plans[scheme] = p;
+    lv->plans[scheme][mode] = p;
     lv->bytes += (long long)p->device_bytes;
   }
-  *out = lv->plans[scheme];
+  *out = lv->plans[scheme][mode];
   return TMG_OK;
 }
 
-SweepArgs sweep_args(tmg_level* lv, const Plan* p, double* u, const double* f) {
-  SweepArgs a;
+SweepArgs sweep_args(tmg_level* lv, const Plan* p, const FieldView& U, const FieldView& F) {
+  SweepArgs a{};
   a.legs = p->d_legs;
   a.blocks = p->d_blocks;
   a.W = lv->W;
   a.E = lv->E;
   a.S = lv->S;
   a.N = lv->N;
-  a.u = u;
-  a.f = f;
+  a.u = U.n;
+  a.f = F.n;
   a.ld = lv->ny + 1;
   a.err = lv->d_err;
+  a.ut = U.t;
+  a.ft = F.t;
+  a.ldt = lv->nx + 1;
+  a.mode = U.mode;
+  a.nx = lv->nx;
+  a.ny = lv->ny;
   return a;
 }
 
-int sweep_one(tmg_level* lv, int scheme, int colour_mask, double* u, const double* f,
+FieldView natural_view(tmg_level* lv, double* p) {
+  return FieldView{p, p, lv->nx, lv->ny, LM_NATURAL};
+}
+
+int sweep_one(tmg_level* lv, int scheme, int colour_mask, const FieldView& U, const FieldView& F,
               cudaStream_t s) {
   Plan* p = nullptr;
-  int st = get_plan(lv, scheme, &p);
+  int st = get_plan(lv, scheme, U.mode, &p);
   if (st) return st;
-  SweepArgs a = sweep_args(lv, p, u, f);
+  SweepArgs a = sweep_args(lv, p, U, F);
   for (int red = 1; red >= 0; red--) {
     if (!(colour_mask & (red ? 1 : 2))) continue;
     cudaError_t e = launch_colour(*p, red, a, s);
@@ -118,18 +139,18 @@ int sweep_one(tmg_level* lv, int scheme, int colour_mask, double* u, const doubl
   return TMG_OK;
 }
 
-int sweep_kind(tmg_level* lv, int kind, int colour_mask, double* u, const double* f,
+int sweep_kind(tmg_level* lv, int kind, int colour_mask, const FieldView& U, const FieldView& F,
                cudaStream_t s) {
   if (!valid_kind(kind)) return fail(TMG_BADARG, "unknown smoother kind " + std::to_string(kind));
   if (kind == TMG_ZEBRA_ALT) {  // smoothers.py:126-129
-    int st = sweep_one(lv, TMG_ZEBRA_X, colour_mask, u, f, s);
-    return st ? st : sweep_one(lv, TMG_ZEBRA_Y, colour_mask, u, f, s);
+    int st = sweep_one(lv, TMG_ZEBRA_X, colour_mask, U, F, s);
+    return st ? st : sweep_one(lv, TMG_ZEBRA_Y, colour_mask, U, F, s);
   }
   if (kind == TMG_TWEED_WIRE_ALT) {  // smoothers.py:130-133
-    int st = sweep_one(lv, TMG_TWEED, colour_mask, u, f, s);
-    return st ? st : sweep_one(lv, TMG_WIREFRAME, colour_mask, u, f, s);
+    int st = sweep_one(lv, TMG_TWEED, colour_mask, U, F, s);
+    return st ? st : sweep_one(lv, TMG_WIREFRAME, colour_mask, U, F, s);
   }
-  return sweep_one(lv, kind, colour_mask, u, f, s);
+  return sweep_one(lv, kind, colour_mask, U, F, s);
 }
 
 // Dense inverse of the interior operator in j-outer ordering (stencil.py:99-126),
@@ -209,61 +230,84 @@ int read_flags(tmg_level* lv, cudaStream_t s) {
   return check_fetched(lv);
 }
 
-int vcycle_launches(tmg_hier* h, int kind, int full, int nu1, int nu2, double* u,
-                    const double* f, cudaStream_t s) {
-  const int L = (int)h->lv.size();
-  std::vector<double*> U(L), F(L);
-  U[0] = u;
-  F[0] = const_cast<double*>(f);
-  for (int l = 1; l < L; l++) {
-    U[l] = h->u[l];
-    F[l] = h->f[l];
-  }
-  for (int l = 0; l < L - 1; l++) {  // mgcycle.py:96-101 on the way down
-    tmg_level* lv = h->lv[l];
-    for (int k = 0; k < nu1; k++) {
-      int st = sweep_kind(lv, kind, 3, U[l], F[l], s);
-      if (st) return st;
-    }
-    cudaError_t e = launch_defect_restrict(lv->grid(), full, U[l], F[l], F[l + 1], s);
-    if (e != cudaSuccess) return cuda_fail(e, "defect_restrict");
-    tmg_level* lc = h->lv[l + 1];
-    TMG_CUDA_TRY(cudaMemsetAsync(U[l + 1], 0,
-                                 sizeof(double) * (size_t)(lc->nx + 1) * (lc->ny + 1), s));
-  }
-  {  // mgcycle.py:93-95
-    tmg_level* lc = h->lv[L - 1];
-    int st = factor_coarse(lc);
-    if (st) return st;
-    cudaError_t e = launch_dense_solve(lc->grid(), lc->d_ainv, U[L - 1], F[L - 1], lc->d_work, s);
-    if (e != cudaSuccess) return cuda_fail(e, "coarse solve");
-  }
-  for (int l = L - 2; l >= 0; l--) {  // mgcycle.py:102-104 on the way up
-    tmg_level* lv = h->lv[l];
-    tmg_level* lc = h->lv[l + 1];
-    cudaError_t e = launch_prolong_correct(lc->nx, lc->ny, U[l + 1], U[l], s);
-    if (e != cudaSuccess) return cuda_fail(e, "prolong_correct");
-    for (int k = 0; k < nu2; k++) {
-      int st = sweep_kind(lv, kind, 3, U[l], F[l], s);
-      if (st) return st;
-    }
-  }
-  return TMG_OK;
-}
-
-int norm_async(tmg_level* lv, const double* u, const double* f, cudaStream_t s) {
-  TMG_CUDA_TRY(cudaMemsetAsync(lv->d_norm, 0, sizeof(unsigned long long), s));
-  cudaError_t e = launch_defect_norm(lv->grid(), u, f, lv->d_norm, s);
-  if (e != cudaSuccess) return cuda_fail(e, "defect_norm");
-  TMG_CUDA_TRY(cudaMemcpyAsync(lv->h_norm, lv->d_norm, sizeof(unsigned long long),
-                               cudaMemcpyDeviceToHost, s));
-  return TMG_OK;
-}
-
 double bits_to_double(unsigned long long b) {
   double d;
   std::memcpy(&d, &b, sizeof(d));
   return d;
+}
+
+// work fields of every level in layout `mode` (re-allocated on a mode change)
+int ensure_fields(tmg_hier* h, int mode) {
+  if (h->mode == mode) return TMG_OK;
+  for (double* p : h->blocks) cudaFree(p);
+  h->blocks.clear();
+  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.first);
+  h->graphs.clear();
+  h->bytes = 0;
+  const int L = (int)h->lv.size();
+  h->U.assign(L, FieldView{});
+  h->F.assign(L, FieldView{});
+  for (int l = 0; l < L; l++) {
+    const int nx = h->lv[l]->nx, ny = h->lv[l]->ny;
+    const size_t n = (size_t)(nx + 1) * (ny + 1);
+    const int nbuf = mode == LM_NATURAL ? 2 : 4;
+    double* p = nullptr;
+    TMG_CUDA_TRY(cudaMalloc(&p, nbuf * n * sizeof(double)));
+    TMG_CUDA_TRY(cudaMemset(p, 0, nbuf * n * sizeof(double)));
+    h->blocks.push_back(p);
+    h->bytes += (long long)(nbuf * n * sizeof(double));
+    double* un = p;
+    double* fn = p + n;
+    double* ut = mode == LM_NATURAL ? un : p + 2 * n;
+    double* ft = mode == LM_NATURAL ? fn : p + 3 * n;
+    h->U[l] = FieldView{un, ut, nx, ny, mode};
+    h->F[l] = FieldView{fn, ft, nx, ny, mode};
+  }
+  h->mode = mode;
+  h->loaded = false;
+  return TMG_OK;
+}
+
+size_t field_elems(const FieldView& v) { return (size_t)(v.nx + 1) * (v.ny + 1); }
+
+int zero_field(const FieldView& v, cudaStream_t s) {
+  TMG_CUDA_TRY(cudaMemsetAsync(v.n, 0, field_elems(v) * sizeof(double), s));
+  if (v.t != v.n) TMG_CUDA_TRY(cudaMemsetAsync(v.t, 0, field_elems(v) * sizeof(double), s));
+  return TMG_OK;
+}
+
+// one V-cycle on the hierarchy's work fields (mgcycle.py:89-104)
+int vcycle_launches(tmg_hier* h, int kind, int full, int nu1, int nu2, cudaStream_t s) {
+  const int L = (int)h->lv.size();
+  for (int l = 0; l < L - 1; l++) {  // down: smooth, residual + restriction, zero guess
+    tmg_level* lv = h->lv[l];
+    for (int k = 0; k < nu1; k++) {
+      int st = sweep_kind(lv, kind, 3, h->U[l], h->F[l], s);
+      if (st) return st;
+    }
+    cudaError_t e = launch_hdefect_restrict(lv->grid(), full, h->U[l], h->F[l], h->F[l + 1], s);
+    if (e != cudaSuccess) return cuda_fail(e, "defect_restrict");
+    int st = zero_field(h->U[l + 1], s);
+    if (st) return st;
+  }
+  {  // coarsest level: direct solve (mgcycle.py:93-95)
+    tmg_level* lc = h->lv[L - 1];
+    int st = factor_coarse(lc);
+    if (st) return st;
+    cudaError_t e = launch_hdense_solve(lc->grid(), lc->d_ainv, h->U[L - 1], h->F[L - 1],
+                                        lc->d_work, s);
+    if (e != cudaSuccess) return cuda_fail(e, "coarse solve");
+  }
+  for (int l = L - 2; l >= 0; l--) {  // up: prolongation + correction, smooth
+    tmg_level* lv = h->lv[l];
+    cudaError_t e = launch_hprolong_correct(lv->nx, lv->ny, h->U[l + 1], h->U[l], s);
+    if (e != cudaSuccess) return cuda_fail(e, "prolong_correct");
+    for (int k = 0; k < nu2; k++) {
+      int st = sweep_kind(lv, kind, 3, h->U[l], h->F[l], s);
+      if (st) return st;
+    }
+  }
+  return TMG_OK;
 }
 
 int check_hier_args(tmg_hier* h, int kind, int nu1, int nu2) {
@@ -274,8 +318,106 @@ int check_hier_args(tmg_hier* h, int kind, int nu1, int nu2) {
   return TMG_OK;
 }
 
-template <class F>
-int guarded(F&& fn) {
+// plans and coarse factors allocate: build them before any stream capture
+int prepare(tmg_hier* h, int kind) {
+  int sub[2] = {kind, -1};
+  if (kind == TMG_ZEBRA_ALT) {
+    sub[0] = TMG_ZEBRA_X;
+    sub[1] = TMG_ZEBRA_Y;
+  }
+  if (kind == TMG_TWEED_WIRE_ALT) {
+    sub[0] = TMG_TWEED;
+    sub[1] = TMG_WIREFRAME;
+  }
+  for (size_t l = 0; l + 1 < h->lv.size(); l++)
+    for (int k : sub) {
+      if (k < 0) continue;
+      Plan* p;
+      int st = get_plan(h->lv[l], k, h->mode, &p);
+      if (st) return st;
+    }
+  return factor_coarse(h->lv.back());
+}
+
+int session_load(tmg_hier* h, int kind, const double* u, const double* f, cudaStream_t s) {
+  int st = ensure_fields(h, session_mode(kind));
+  if (st) return st;
+  cudaError_t e = launch_to_hybrid(h->U[0], u, s);
+  if (e == cudaSuccess) e = launch_to_hybrid(h->F[0], f, s);
+  if (e != cudaSuccess) return cuda_fail(e, "layout conversion");
+  h->loaded = true;
+  return TMG_OK;
+}
+
+int session_store(tmg_hier* h, double* u, cudaStream_t s) {
+  if (!h->loaded) return fail(TMG_BADARG, "no solver session loaded");
+  cudaError_t e = launch_from_hybrid(h->U[0], u, s);
+  return e == cudaSuccess ? TMG_OK : cuda_fail(e, "layout conversion");
+}
+
+int session_cycles(tmg_hier* h, int kind, int full, int nu1, int nu2, int reps, cudaStream_t s) {
+  if (!h->loaded) return fail(TMG_BADARG, "no solver session loaded");
+  if (session_mode(kind) != h->mode)
+    return fail(TMG_BADARG, "smoother kind does not match the loaded session's layout");
+  auto key = std::make_tuple(kind, full, nu1, nu2);
+  auto it = h->graphs.find(key);
+  if (it == h->graphs.end()) {
+    int st = prepare(h, kind);
+    if (st) return st;
+    cudaStream_t cs;
+    TMG_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaGraph_t g;
+    TMG_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    int st3 = vcycle_launches(h, kind, full, nu1, nu2, cs);
+    cudaError_t e = cudaStreamEndCapture(cs, &g);
+    cudaStreamDestroy(cs);
+    if (st3) return st3;
+    if (e != cudaSuccess) return cuda_fail(e, "graph capture");
+    size_t nn = 0;
+    TMG_CUDA_TRY(cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    TMG_CUDA_TRY(cudaGraphGetNodes(g, nodes.data(), &nn));
+    int kernels = 0;
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      TMG_CUDA_TRY(cudaGraphNodeGetType(nd, &t));
+      kernels += (t == cudaGraphNodeTypeKernel);
+    }
+    cudaGraphExec_t ge;
+    TMG_CUDA_TRY(cudaGraphInstantiate(&ge, g, 0));
+    cudaGraphDestroy(g);
+    it = h->graphs.emplace(key, std::make_pair(ge, kernels)).first;
+  }
+  h->last_kernels = it->second.second;
+  for (int r = 0; r < reps; r++) TMG_CUDA_TRY(cudaGraphLaunch(it->second.first, s));
+  return TMG_OK;
+}
+
+int session_norm_async(tmg_hier* h, cudaStream_t s) {
+  tmg_level* fine = h->lv[0];
+  TMG_CUDA_TRY(cudaMemsetAsync(fine->d_norm, 0, sizeof(unsigned long long), s));
+  cudaError_t e = launch_hdefect_norm(fine->grid(), h->U[0], h->F[0], fine->d_norm, s);
+  if (e != cudaSuccess) return cuda_fail(e, "defect_norm");
+  TMG_CUDA_TRY(cudaMemcpyAsync(fine->h_norm, fine->d_norm, sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s));
+  return TMG_OK;
+}
+
+int flags_all(tmg_hier* h, cudaStream_t s) {
+  for (auto* lv : h->lv) {
+    int st = fetch_flags_async(lv, s);
+    if (st) return st;
+  }
+  TMG_CUDA_TRY(cudaStreamSynchronize(s));
+  for (auto* lv : h->lv) {
+    int st = check_fetched(lv);
+    if (st) return st;
+  }
+  return TMG_OK;
+}
+
+template <class Fn>
+int guarded(Fn&& fn) {
   try {
     return fn();
   } catch (const std::exception& ex) {
@@ -288,7 +430,7 @@ int guarded(F&& fn) {
 extern "C" {
 
 const char* tmg_last_error(void) { return g_last_error.c_str(); }
-int tmg_version(void) { return 100; }
+int tmg_version(void) { return 110; }
 
 int tmg_level_create(int nx, int ny, const double* W, const double* E, const double* S,
                      const double* N, tmg_level** out) {
@@ -325,11 +467,12 @@ int tmg_level_create(int nx, int ny, const double* W, const double* E, const dou
 
 int tmg_level_destroy(tmg_level* lv) {
   if (!lv) return TMG_OK;
-  for (auto& p : lv->plans)
-    if (p) {
-      free_plan(*p);
-      delete p;
-    }
+  for (auto& row : lv->plans)
+    for (auto& p : row)
+      if (p) {
+        free_plan(*p);
+        delete p;
+      }
   cudaFree(lv->W);
   cudaFree(lv->d_err);
   cudaFreeHost(lv->h_err);
@@ -348,13 +491,18 @@ int tmg_level_check(tmg_level* lv, void* stream) {
 
 int tmg_sweep(tmg_level* lv, int kind, double* u, const double* f, void* stream) {
   if (!lv) return fail(TMG_BADARG, "null level");
-  return guarded([&] { return sweep_kind(lv, kind, 3, u, f, (cudaStream_t)stream); });
+  return guarded([&] {
+    return sweep_kind(lv, kind, 3, natural_view(lv, u), natural_view(lv, const_cast<double*>(f)),
+                      (cudaStream_t)stream);
+  });
 }
 
-int tmg_sweep_colour(tmg_level* lv, int kind, int red, double* u, const double* f,
-                     void* stream) {
+int tmg_sweep_colour(tmg_level* lv, int kind, int red, double* u, const double* f, void* stream) {
   if (!lv) return fail(TMG_BADARG, "null level");
-  return guarded([&] { return sweep_kind(lv, kind, red ? 1 : 2, u, f, (cudaStream_t)stream); });
+  return guarded([&] {
+    return sweep_kind(lv, kind, red ? 1 : 2, natural_view(lv, u),
+                      natural_view(lv, const_cast<double*>(f)), (cudaStream_t)stream);
+  });
 }
 
 int tmg_apply(tmg_level* lv, const double* u, double* out, void* stream) {
@@ -373,15 +521,19 @@ int tmg_defect_norm(tmg_level* lv, const double* u, const double* f, double* out
                     void* stream) {
   if (!lv) return fail(TMG_BADARG, "null level");
   cudaStream_t s = (cudaStream_t)stream;
-  int st = norm_async(lv, u, f, s);
-  if (st) return st;
+  TMG_CUDA_TRY(cudaMemsetAsync(lv->d_norm, 0, sizeof(unsigned long long), s));
+  cudaError_t e = launch_defect_norm(lv->grid(), u, f, lv->d_norm, s);
+  if (e != cudaSuccess) return cuda_fail(e, "defect_norm");
+  TMG_CUDA_TRY(cudaMemcpyAsync(lv->h_norm, lv->d_norm, sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s));
   TMG_CUDA_TRY(cudaStreamSynchronize(s));
   *out_host = bits_to_double(*lv->h_norm);
   return TMG_OK;
 }
 
 int tmg_restrict(int nxf, int nyf, int full, const double* d, double* out, void* stream) {
-  if (nxf % 2 || nyf % 2 || nxf < 2 || nyf < 2) return fail(TMG_BADARG, "fine grid cannot be halved");
+  if (nxf % 2 || nyf % 2 || nxf < 2 || nyf < 2)
+    return fail(TMG_BADARG, "fine grid cannot be halved");
   cudaError_t e = launch_restrict(nxf, nyf, full, d, out, (cudaStream_t)stream);
   return e == cudaSuccess ? TMG_OK : cuda_fail(e, "restrict");
 }
@@ -410,8 +562,8 @@ int tmg_direct_solve(tmg_level* lv, double* u, const double* f, void* stream) {
   return guarded([&]() -> int {
     int st = factor_coarse(lv);
     if (st) return st;
-    cudaError_t e = launch_dense_solve(lv->grid(), lv->d_ainv, u, f, lv->d_work,
-                                       (cudaStream_t)stream);
+    cudaError_t e =
+        launch_dense_solve(lv->grid(), lv->d_ainv, u, f, lv->d_work, (cudaStream_t)stream);
     return e == cudaSuccess ? TMG_OK : cuda_fail(e, "direct solve");
   });
 }
@@ -424,14 +576,6 @@ int tmg_hier_create(int nlevels, tmg_level* const* levels, tmg_hier** out) {
         return fail(TMG_BADARG, "each level must halve the previous one");
     tmg_hier* h = new tmg_hier();
     h->lv.assign(levels, levels + nlevels);
-    h->u.assign(nlevels, nullptr);
-    h->f.assign(nlevels, nullptr);
-    for (int l = 1; l < nlevels; l++) {
-      size_t n = (size_t)(levels[l]->nx + 1) * (levels[l]->ny + 1);
-      TMG_CUDA_TRY(cudaMalloc(&h->u[l], 2 * n * sizeof(double)));
-      h->f[l] = h->u[l] + n;
-      TMG_CUDA_TRY(cudaMemset(h->u[l], 0, 2 * n * sizeof(double)));
-    }
     *out = h;
     return TMG_OK;
   });
@@ -440,16 +584,58 @@ int tmg_hier_create(int nlevels, tmg_level* const* levels, tmg_hier** out) {
 int tmg_hier_destroy(tmg_hier* h) {
   if (!h) return TMG_OK;
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.first);
-  for (size_t l = 1; l < h->u.size(); l++) cudaFree(h->u[l]);
+  for (double* p : h->blocks) cudaFree(p);
   delete h;
   return TMG_OK;
 }
 
-int tmg_vcycle(tmg_hier* h, int kind, int full, int nu1, int nu2, double* u, const double* f,
-               void* stream) {
+int tmg_hier_graph_kernels(tmg_hier* h) { return h ? h->last_kernels : 0; }
+
+long long tmg_hier_device_bytes(tmg_hier* h) { return h ? h->bytes : 0; }
+
+int tmg_session_load(tmg_hier* h, int kind, const double* u, const double* f, void* stream) {
+  if (!h || h->lv.empty()) return fail(TMG_BADARG, "null hierarchy");
+  if (!valid_kind(kind)) return fail(TMG_BADARG, "unknown smoother " + std::to_string(kind));
+  return guarded([&] { return session_load(h, kind, u, f, (cudaStream_t)stream); });
+}
+
+int tmg_session_cycles(tmg_hier* h, int kind, int full, int nu1, int nu2, int reps,
+                       void* stream) {
   int st = check_hier_args(h, kind, nu1, nu2);
   if (st) return st;
-  return guarded([&] { return vcycle_launches(h, kind, full, nu1, nu2, u, f, (cudaStream_t)stream); });
+  return guarded(
+      [&] { return session_cycles(h, kind, full, nu1, nu2, reps, (cudaStream_t)stream); });
+}
+
+int tmg_session_norm(tmg_hier* h, double* out_host, void* stream) {
+  if (!h || !h->loaded) return fail(TMG_BADARG, "no solver session loaded");
+  return guarded([&]() -> int {
+    cudaStream_t s = (cudaStream_t)stream;
+    int st = session_norm_async(h, s);
+    if (st) return st;
+    st = flags_all(h, s);
+    if (st) return st;
+    *out_host = bits_to_double(*h->lv[0]->h_norm);
+    return TMG_OK;
+  });
+}
+
+int tmg_session_store(tmg_hier* h, double* u, void* stream) {
+  if (!h) return fail(TMG_BADARG, "null hierarchy");
+  return guarded([&] { return session_store(h, u, (cudaStream_t)stream); });
+}
+
+int tmg_session_sweeps(tmg_hier* h, int kind, int reps, void* stream) {
+  if (!h || !h->loaded) return fail(TMG_BADARG, "no solver session loaded");
+  if (!valid_kind(kind) || session_mode(kind) != h->mode)
+    return fail(TMG_BADARG, "smoother kind does not match the loaded session's layout");
+  return guarded([&]() -> int {
+    for (int r = 0; r < reps; r++) {
+      int st = sweep_kind(h->lv[0], kind, 3, h->U[0], h->F[0], (cudaStream_t)stream);
+      if (st) return st;
+    }
+    return TMG_OK;
+  });
 }
 
 int tmg_vcycle_graph(tmg_hier* h, int kind, int full, int nu1, int nu2, double* u,
@@ -458,58 +644,17 @@ int tmg_vcycle_graph(tmg_hier* h, int kind, int full, int nu1, int nu2, double* 
   if (st) return st;
   return guarded([&]() -> int {
     cudaStream_t s = (cudaStream_t)stream;
-    auto key = std::make_tuple(kind, full, nu1, nu2, (const void*)u, (const void*)f, stream);
-    auto it = h->graphs.find(key);
-    if (it == h->graphs.end()) {
-      // build plans and coarse factors outside capture (they allocate)
-      for (size_t l = 0; l < h->lv.size(); l++) {
-        int sub[2] = {kind, -1};
-        if (kind == TMG_ZEBRA_ALT) { sub[0] = TMG_ZEBRA_X; sub[1] = TMG_ZEBRA_Y; }
-        if (kind == TMG_TWEED_WIRE_ALT) { sub[0] = TMG_TWEED; sub[1] = TMG_WIREFRAME; }
-        for (int k : sub) {
-          if (k < 0 || l + 1 == h->lv.size()) continue;
-          Plan* p;
-          int st2 = get_plan(h->lv[l], k, &p);
-          if (st2) return st2;
-        }
-      }
-      int st2 = factor_coarse(h->lv.back());
-      if (st2) return st2;
-      cudaStream_t cs;
-      TMG_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-      cudaGraph_t g;
-      TMG_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-      int st3 = vcycle_launches(h, kind, full, nu1, nu2, u, f, cs);
-      cudaError_t e = cudaStreamEndCapture(cs, &g);
-      cudaStreamDestroy(cs);
-      if (st3) return st3;
-      if (e != cudaSuccess) return cuda_fail(e, "graph capture");
-      size_t nn = 0;
-      TMG_CUDA_TRY(cudaGraphGetNodes(g, nullptr, &nn));
-      std::vector<cudaGraphNode_t> nodes(nn);
-      TMG_CUDA_TRY(cudaGraphGetNodes(g, nodes.data(), &nn));
-      int kernels = 0;
-      for (auto nd : nodes) {
-        cudaGraphNodeType t;
-        TMG_CUDA_TRY(cudaGraphNodeGetType(nd, &t));
-        kernels += (t == cudaGraphNodeTypeKernel);
-      }
-      cudaGraphExec_t ge;
-      TMG_CUDA_TRY(cudaGraphInstantiate(&ge, g, 0));
-      cudaGraphDestroy(g);
-      if (h->graphs.size() >= 32) {  // bound the cache
-        for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.first);
-        h->graphs.clear();
-      }
-      it = h->graphs.emplace(key, std::make_pair(ge, kernels)).first;
-    }
-    h->last_kernels = it->second.second;
-    for (int r = 0; r < reps; r++) TMG_CUDA_TRY(cudaGraphLaunch(it->second.first, s));
-    return TMG_OK;
+    int st2 = session_load(h, kind, u, f, s);
+    if (!st2) st2 = session_cycles(h, kind, full, nu1, nu2, reps, s);
+    if (!st2) st2 = session_store(h, u, s);
+    return st2;
   });
 }
 
-int tmg_hier_graph_kernels(tmg_hier* h) { return h ? h->last_kernels : 0; }
+int tmg_vcycle(tmg_hier* h, int kind, int full, int nu1, int nu2, double* u, const double* f,
+               void* stream) {
+  return tmg_vcycle_graph(h, kind, full, nu1, nu2, u, f, 1, stream);
+}
 
 int tmg_solve(tmg_hier* h, int kind, int full, int nu1, int nu2, double tol, int max_cycles,
               double* u, const double* f, double* norms_out, int* cycles_out, int* converged_out,
@@ -519,33 +664,24 @@ int tmg_solve(tmg_hier* h, int kind, int full, int nu1, int nu2, double tol, int
   if (!(tol > 0)) return fail(TMG_BADARG, "tol must be positive");
   return guarded([&]() -> int {
     cudaStream_t s = (cudaStream_t)stream;
-    tmg_level* fine = h->lv[0];
     *cycles_out = 0;
     *converged_out = 0;
-    int st2 = norm_async(fine, u, f, s);
+    int st2 = session_load(h, kind, u, f, s);
+    if (!st2) st2 = session_norm_async(h, s);
     if (st2) return st2;
     TMG_CUDA_TRY(cudaStreamSynchronize(s));
-    const double d0 = bits_to_double(*fine->h_norm);
+    const double d0 = bits_to_double(*h->lv[0]->h_norm);
     norms_out[0] = d0;
     if (d0 == 0.0) {  // mgcycle.py:124-126
       *converged_out = 1;
-      return TMG_OK;
+      return session_store(h, u, s);
     }
     for (int cycle = 1; cycle <= max_cycles; cycle++) {  // mgcycle.py:128-138
-      st2 = tmg_vcycle_graph(h, kind, full, nu1, nu2, u, f, 1, stream);
+      st2 = session_cycles(h, kind, full, nu1, nu2, 1, s);
+      if (!st2) st2 = session_norm_async(h, s);
+      if (!st2) st2 = flags_all(h, s);
       if (st2) return st2;
-      st2 = norm_async(fine, u, f, s);
-      if (st2) return st2;
-      for (size_t l = 0; l < h->lv.size(); l++) {
-        st2 = fetch_flags_async(h->lv[l], s);
-        if (st2) return st2;
-      }
-      TMG_CUDA_TRY(cudaStreamSynchronize(s));
-      for (size_t l = 0; l < h->lv.size(); l++) {
-        st2 = check_fetched(h->lv[l]);
-        if (st2) return st2;
-      }
-      const double dn = bits_to_double(*fine->h_norm);
+      const double dn = bits_to_double(*h->lv[0]->h_norm);
       norms_out[cycle] = dn;
       *cycles_out = cycle;
       if (!std::isfinite(dn)) break;
@@ -554,11 +690,12 @@ int tmg_solve(tmg_hier* h, int kind, int full, int nu1, int nu2, double tol, int
         break;
       }
     }
-    return TMG_OK;
+    return session_store(h, u, s);
   });
 }
 
-long tmg_layout_dump(int kind, int nx, int ny, int* oi, int* oj, int* oblk, int* oflags, long cap) {
+long tmg_layout_dump(int kind, int nx, int ny, int* oi, int* oj, int* oblk, int* oflags,
+                     long cap) {
   Geometry g;
   std::string err = build_geometry(kind, nx, ny, g);
   if (!err.empty()) {
@@ -582,7 +719,8 @@ int relax_explicit(int kind, long n, const int64_t* ii, const int64_t* jj, long 
   TMG_CUDA_TRY(cudaMemcpyAsync(hi.data(), ii, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
   TMG_CUDA_TRY(cudaMemcpyAsync(hj.data(), jj, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
   if (kind == 3)
-    TMG_CUDA_TRY(cudaMemcpyAsync(ho.data(), offs, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToHost, s));
+    TMG_CUDA_TRY(cudaMemcpyAsync(ho.data(), offs, sizeof(int64_t) * (m + 1),
+                                 cudaMemcpyDeviceToHost, s));
   TMG_CUDA_TRY(cudaStreamSynchronize(s));
   for (long k = 0; k < n; k++)
     if (hi[k] < 1 || hi[k] >= nx || hj[k] < 1 || hj[k] >= ny)
@@ -593,8 +731,10 @@ int relax_explicit(int kind, long n, const int64_t* ii, const int64_t* jj, long 
   g.scheme = -1;
   std::string err = add_explicit_block(g, kind, n, hi.data(), hj.data(), m, ho.data(), bi, bj);
   if (!err.empty()) return fail(TMG_BADARG, err);
+  cudaError_t e = init_sweep_kernels();
+  if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");
   Plan p;
-  err = pack_plan(std::move(g), kQmax, p);
+  err = pack_plan(std::move(g), kQmax, LM_NATURAL, p);
   if (!err.empty()) {
     free_plan(p);
     return fail(TMG_BADARG, err);
@@ -602,8 +742,24 @@ int relax_explicit(int kind, long n, const int64_t* ii, const int64_t* jj, long 
   int* d_err = nullptr;
   TMG_CUDA_TRY(cudaMalloc(&d_err, sizeof(int)));
   TMG_CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(int), s));
-  SweepArgs a{p.d_legs, p.d_blocks, W, E, S, N, u, f, ny + 1, d_err};
-  cudaError_t e = launch_colour(p, 1, a, s);
+  SweepArgs a{};
+  a.legs = p.d_legs;
+  a.blocks = p.d_blocks;
+  a.W = W;
+  a.E = E;
+  a.S = S;
+  a.N = N;
+  a.u = u;
+  a.f = f;
+  a.ld = ny + 1;
+  a.err = d_err;
+  a.ut = u;
+  a.ft = f;
+  a.ldt = nx + 1;
+  a.mode = LM_NATURAL;
+  a.nx = nx;
+  a.ny = ny;
+  e = launch_colour(p, 1, a, s);
   int herr = 0;
   if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);

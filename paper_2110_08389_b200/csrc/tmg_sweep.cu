@@ -22,9 +22,15 @@
 //  C  coalesced scatter of the new values.
 #include <cooperative_groups.h>
 
+#include <vector>
+
 #include "tmg_kernels.h"
 
 namespace cg = cooperative_groups;
+
+#ifndef TMG_MINB
+#define TMG_MINB 2  // resident CTAs per SM the register budget is sized for
+#endif
 
 namespace tmg {
 
@@ -81,22 +87,25 @@ struct Coefs {
 
 // Geometry of one chunk, unpacked into registers.
 struct Chunk {
-  int off, stride, a0, da, cidx, cs, n, dfirst, dlast, link, hub, own, axis;
+  int off, stride, a0, da, cidx, cs, n, dfirst, dlast, link, hub, own, axis, tb;
   const double* __restrict__ pa;  // along coupling toward the previous point
   const double* __restrict__ pc;  // along coupling toward the next point
   const double* __restrict__ xl;  // cross coefficients (low / high side)
   const double* __restrict__ xh;
 
-  __device__ __forceinline__ void unpack(const ChunkD& c, const Coefs& C, int ld) {
+  __device__ __forceinline__ void unpack(const ChunkD& c, const Coefs& C, int ld, int ldt) {
     n = c.n;
     off = c.off;
     a0 = c.a0;
     cidx = c.cidx;
     axis = c.geo & 1;
     const int neg = (c.geo >> 1) & 1;
+    tb = (c.geo >> 2) & 1;
     da = neg ? -1 : 1;
-    stride = axis ? da : da * ld;
-    cs = axis ? ld : 1;
+    // along / cross strides inside the owning buffer (tmg_layout.h)
+    const int si = tb ? 1 : ld, sj = tb ? ldt : 1;
+    stride = (axis ? sj : si) * da;
+    cs = axis ? si : sj;
     dfirst = c.link & 7;
     dlast = (c.link >> 3) & 7;
     link = c.link;
@@ -118,24 +127,51 @@ struct Chunk {
 
 }  // namespace
 
-// Shared memory (doubles unless noted):
-//   R   [T * QS]  chunk-major point values (rhs -> rho -> alpha -> x)
-//   E5  [5 * T]   reduced rows (A, B, C, D, H); first-point affine triples
-//   XH  [T]       hub values, slot = owner thread
+#ifdef TMG_PHASE_TIMING
+__device__ long long g_phase_t[8][1 << 16];
+__device__ int g_phase_n;
+#define TMG_T(slot)                                                        \
+  do {                                                                     \
+    if (threadIdx.x == 0 && blockIdx.x < (1 << 16)) {                      \
+      g_phase_t[slot][blockIdx.x] = clock64();                             \
+      if (slot == 0) atomicMax(&g_phase_n, (int)blockIdx.x + 1);           \
+    }                                                                      \
+  } while (0)
+#else
+#define TMG_T(slot) \
+  do {              \
+  } while (0)
+#endif
+
+// Shared memory (doubles):
+//   R, PA, PC [T * Q] chunk-major point values: the right-hand side (later
+//                     rho, alpha, x) and the along couplings toward the
+//                     previous / next point; row t slot k lives at
+//                     t*Q + (k ^ (t & (Q-1))) (XOR swizzle: conflict-free
+//                     for both the lane-along-chunk gather and the
+//                     lane-per-chunk elimination, no padding)
+//   E5        [5 * T] reduced rows (A, B, C, D, H); first-point triples
+//   XH        [T]     hub values, slot = owner thread
 template <int Q>
 constexpr size_t sweep_smem() {
-  return sizeof(double) * (size_t)(kThreads * (Q | 1) + 6 * kThreads);
+  return sizeof(double) * (size_t)(3 * kThreads * Q + 6 * kThreads);
+}
+
+template <int Q>
+__device__ __forceinline__ int sw(int t, int k) {
+  return t * Q + (k ^ (t & (Q - 1)));
 }
 
 template <bool CLUSTER, int Q>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, TMG_MINB)
 block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* __restrict__ bins,
                    const HubD* __restrict__ hubs, int cs_size) {
   extern __shared__ double smem[];
   constexpr int T = kThreads;
-  constexpr int QS = Q | 1;
   double* R = smem;
-  double* sA = R + T * QS;
+  double* PA = R + T * Q;
+  double* PC = PA + T * Q;
+  double* sA = PC + T * Q;
   double* sB = sA + T;
   double* sC = sB + T;
   double* sD = sC + T;
@@ -150,9 +186,12 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
   double* __restrict__ u = a.u;
   const double* __restrict__ f = a.f;
 
+  TMG_T(0);
   const ChunkD mine = chunks[(size_t)blockIdx.x * T + tid];
   Chunk c;
-  c.unpack(mine, C, ld);
+  c.unpack(mine, C, ld, a.ldt);
+  const FieldView U{u, a.ut, a.nx, a.ny, a.mode};
+  const FieldView F{const_cast<double*>(f), const_cast<double*>(a.ft), a.nx, a.ny, a.mode};
   const double xlv = c.n > 0 ? __ldg(c.xl + c.cidx) : 0.0;
   const double xhv = c.n > 0 ? __ldg(c.xh + c.cidx) : 0.0;
   const int lane = tid & 31, wbase = tid & ~31;
@@ -161,14 +200,15 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
   const int ksub = lane % Q, csub = lane / Q;
   constexpr unsigned FULL = 0xffffffffu;
 
-  // ---------------- phase A: coalesced gather of frozen right-hand sides ----
+  // ---------------- phase A: coalesced gather --------------------------------
   // Warp-local: the warp streams the points of its own 32 chunks, lanes
   // consecutive along each chunk, all loads of a batch in flight together.
-  // Interior points subtract the two cross neighbours; chunk ends are
-  // redone below with their exact in-block neighbour sets.
+  // Each point stages its frozen right-hand side (interior points subtract
+  // the two cross neighbours; chunk ends are redone below with their exact
+  // in-block neighbour sets) and its two along couplings.
 #pragma unroll
   for (int m0 = 0; m0 < Q; m0 += BATCH) {
-    double vf[BATCH], vl[BATCH], vh[BATCH];
+    double vf[BATCH], vl[BATCH], vh[BATCH], va[BATCH], vc[BATCH];
     int slot[BATCH];
 #pragma unroll
     for (int b = 0; b < BATCH; b++) {
@@ -177,12 +217,22 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
       const int off_s = __shfl_sync(FULL, c.off, src);
       const int str_s = __shfl_sync(FULL, c.stride, src);
       const int cs_s = __shfl_sync(FULL, c.cs, src);
+      const int tb_s = __shfl_sync(FULL, c.tb, src);
+      const double* ub = tb_s ? a.ut : u;
+      const double* fb = tb_s ? a.ft : f;
+      const int ai_s = __shfl_sync(FULL, c.a0, src) + ksub * __shfl_sync(FULL, c.da, src);
+      const double* pa_s = reinterpret_cast<const double*>(
+          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(c.pa), src));
+      const double* pc_s = reinterpret_cast<const double*>(
+          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(c.pc), src));
       const int o = off_s + ksub * str_s;
-      slot[b] = ksub < n_s ? (wbase + src) * QS + ksub : -1;
+      slot[b] = ksub < n_s ? sw<Q>(wbase + src, ksub) : -1;
       if (ksub < n_s) {
-        vf[b] = f[o];
-        vl[b] = u[o - cs_s];
-        vh[b] = u[o + cs_s];
+        vf[b] = fb[o];
+        vl[b] = ub[o - cs_s];
+        vh[b] = ub[o + cs_s];
+        va[b] = __ldg(pa_s + ai_s);
+        vc[b] = __ldg(pc_s + ai_s);
       }
     }
 #pragma unroll
@@ -190,11 +240,14 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
       const int src = (m0 + b) * PER + csub;
       const double xl_s = __shfl_sync(FULL, xlv, src);
       const double xh_s = __shfl_sync(FULL, xhv, src);
-      if (slot[b] >= 0) R[slot[b]] = fma(-xh_s, vh[b], fma(-xl_s, vl[b], vf[b]));
+      if (slot[b] >= 0) {
+        R[slot[b]] = fma(-xh_s, vh[b], fma(-xl_s, vl[b], vf[b]));
+        PA[slot[b]] = va[b];
+        PC[slot[b]] = vc[b];
+      }
     }
   }
   __syncwarp();
-  double* Rt = R + tid * QS;
   if (c.n > 0) {  // chunk ends: neighbours outside the block from the link directions
     const int alo = c.da > 0 ? (c.axis ? DS : DW) : (c.axis ? DN : DE);  // toward k-1
     const int ahi = alo ^ 1;                                             // toward k+1
@@ -207,18 +260,21 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
       const unsigned skip = (dp < 4 ? 1u << dp : 0u) | (dn < 4 ? 1u << dn : 0u);
       int i, j;
       c.ij(k, i, j);
-      const int o = c.off + k * c.stride;
-      double r = f[o];
-      if (!(skip & 1u)) r -= __ldg(a.W + i) * u[o - ld];
-      if (!(skip & 2u)) r -= __ldg(a.E + i) * u[o + ld];
-      if (!(skip & 4u)) r -= __ldg(a.S + j) * u[o - 1];
-      if (!(skip & 8u)) r -= __ldg(a.N + j) * u[o + 1];
-      Rt[k] = r;
+      double r = *F.at(i, j);
+      if (!(skip & 1u)) r -= __ldg(a.W + i) * *U.at(i - 1, j);
+      if (!(skip & 2u)) r -= __ldg(a.E + i) * *U.at(i + 1, j);
+      if (!(skip & 4u)) r -= __ldg(a.S + j) * *U.at(i, j - 1);
+      if (!(skip & 8u)) r -= __ldg(a.N + j) * *U.at(i, j + 1);
+      R[sw<Q>(tid, k)] = r;
     }
   }
   __syncwarp();
+  TMG_T(1);
 
   // ---------------- phase B: chunk elimination -------------------------------
+  // Down sweep (Thomas forward elimination over the chunk interior, the
+  // coupling to the previous chunk's end kept as a column) and an affine back
+  // pass: x_k = alpha_k + beta_k * Xleft + gamma_k * X.
   const int nI = c.n - 1;  // interior points (all but the chunk end)
   double lam[Q], ivr[Q];
   double ad = 0.0, bd = 1.0, gd = 0.0;  // x_{e-1} = ad + bd*Xleft + gd*X
@@ -231,16 +287,14 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
     c.ij(0, i0, j0);
     a_first = C.dir(c.dfirst, i0, j0);
   }
-  double cprev = 0.0;
   if (nI > 0) {
-    double bp = 0.0, rho = 0.0, lm = 0.0, ivp = 0.0;
+    double bp = 0.0, rho = 0.0, lm = 0.0, ivp = 0.0, cprev = 0.0;
 #pragma unroll
     for (int k = 0; k < Q; k++) {
       if (k < nI) {
-        const int ai = c.a0 + k * c.da;
-        const double pav = __ldg(c.pa + ai), pcv = __ldg(c.pc + ai);
+        const int sl = sw<Q>(tid, k);
+        const double pav = PA[sl], pcv = PC[sl], rp = R[sl];
         const double bb = -(pav + pcv + csum);
-        const double rp = Rt[k];
         if (k == 0) {
           bp = bb;
           rho = rp;
@@ -253,31 +307,32 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
         }
         bad |= bad_pivot(bp);
         ivp = drcp(bp);
-        Rt[k] = rho;
+        R[sl] = rho;
         lam[k] = lm;
         ivr[k] = ivp;
         cprev = pcv;
       }
     }
-    // affine back substitution: cprev = c_{e-1}
+    // affine back substitution; cprev = c_{e-1}
     double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
     for (int k = Q - 1; k >= 0; k--) {
       if (k < nI) {
+        const int sl = sw<Q>(tid, k);
         if (k == nI - 1) {
-          al = Rt[k] * ivr[k];
+          al = R[sl] * ivr[k];
           be = lam[k] * ivr[k];
           ga = -cprev * ivr[k];
           ad = al;
           bd = be;
           gd = ga;
         } else {
-          const double cp = __ldg(c.pc + c.a0 + k * c.da);
-          al = fma(-cp, al, Rt[k]) * ivr[k];
+          const double cp = PC[sl];
+          al = fma(-cp, al, R[sl]) * ivr[k];
           be = fma(-cp, be, lam[k]) * ivr[k];
           ga = -cp * ga * ivr[k];
         }
-        Rt[k] = al;
+        R[sl] = al;
         lam[k] = be;
         ivr[k] = ga;
       }
@@ -286,6 +341,7 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
     bu = be;
     gu = ga;
   }
+  TMG_T(2);
   // publish the first-point affine form for the left neighbour chunk
   sA[tid] = au;
   sB[tid] = bu;
@@ -297,13 +353,13 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
   if (c.n > 0) {
     int ie, je;
     c.ij(nI, ie, je);
-    const int ae_i = c.a0 + nI * c.da;
-    const double pav = __ldg(c.pa + ae_i), pcv = __ldg(c.pc + ae_i);
+    const int sl = sw<Q>(tid, nI);
+    const double pav = PA[sl], pcv = PC[sl];
     const double ae = nI > 0 ? pav : a_first;
     const double ce = C.dir(c.dlast, ie, je);
     A = ae * bd;
     B = -(pav + pcv + csum) + ae * gd;
-    D = Rt[nI] - ae * ad;
+    D = R[sl] - ae * ad;
     if (c.link & kLinkRightNext) {
       B = fma(ce, sB[tid + 1], B);
       Cc = ce * sC[tid + 1];
@@ -321,15 +377,14 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
   const BinD bd_ = bins[bin];
   const int steps = bd_.pcr_steps;
   if (bd_.warp_local) {
-    const int lane = tid & 31;
     for (int st = 0; st < steps; st++) {
       const int d = 1 << st;
-      double Am = __shfl_up_sync(0xffffffffu, A, d), Bm = __shfl_up_sync(0xffffffffu, B, d);
-      double Cm = __shfl_up_sync(0xffffffffu, Cc, d), Dm = __shfl_up_sync(0xffffffffu, D, d);
-      double Hm = __shfl_up_sync(0xffffffffu, H, d);
-      double Ap = __shfl_down_sync(0xffffffffu, A, d), Bp = __shfl_down_sync(0xffffffffu, B, d);
-      double Cp = __shfl_down_sync(0xffffffffu, Cc, d), Dp = __shfl_down_sync(0xffffffffu, D, d);
-      double Hp = __shfl_down_sync(0xffffffffu, H, d);
+      double Am = __shfl_up_sync(FULL, A, d), Bm = __shfl_up_sync(FULL, B, d);
+      double Cm = __shfl_up_sync(FULL, Cc, d), Dm = __shfl_up_sync(FULL, D, d);
+      double Hm = __shfl_up_sync(FULL, H, d);
+      double Ap = __shfl_down_sync(FULL, A, d), Bp = __shfl_down_sync(FULL, B, d);
+      double Cp = __shfl_down_sync(FULL, Cc, d), Dp = __shfl_down_sync(FULL, D, d);
+      double Hp = __shfl_down_sync(FULL, H, d);
       if (lane < d) { Am = 0.0; Bm = 1.0; Cm = 0.0; Dm = 0.0; Hm = 0.0; }
       if (lane + d > 31) { Ap = 0.0; Bp = 1.0; Cp = 0.0; Dp = 0.0; Hp = 0.0; }
       const double k1 = A * drcp(Bm), k2 = Cc * drcp(Bp);
@@ -368,6 +423,7 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
   const double P = D * iB, Qh = H * iB;  // X_t = P - Qh * x_hub
   sD[tid] = P;
   sH[tid] = Qh;
+  TMG_T(3);
   bin_sync<CLUSTER>();
 
   // hub rows
@@ -375,11 +431,11 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
     const HubD hb = hubs[bd_.hub0 + c.own];
     const int hi = hb.i, hj = hb.j;
     const int o = hb.off;
-    double num = f[o];
-    if (!(hb.mask & 1u)) num -= __ldg(a.W + hi) * u[o - ld];
-    if (!(hb.mask & 2u)) num -= __ldg(a.E + hi) * u[o + ld];
-    if (!(hb.mask & 4u)) num -= __ldg(a.S + hj) * u[o - 1];
-    if (!(hb.mask & 8u)) num -= __ldg(a.N + hj) * u[o + 1];
+    double num = (hb.tbuf ? a.ft : f)[o];
+    if (!(hb.mask & 1u)) num -= __ldg(a.W + hi) * *U.at(hi - 1, hj);
+    if (!(hb.mask & 2u)) num -= __ldg(a.E + hi) * *U.at(hi + 1, hj);
+    if (!(hb.mask & 4u)) num -= __ldg(a.S + hj) * *U.at(hi, hj - 1);
+    if (!(hb.mask & 8u)) num -= __ldg(a.N + hj) * *U.at(hi, hj + 1);
     double den = -(__ldg(a.W + hi) + __ldg(a.E + hi) + __ldg(a.S + hj) + __ldg(a.N + hj));
     for (int q = 0; q < hb.nadj; q++) {
       const int ta = hb.adj_t[q];
@@ -390,10 +446,11 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
     bad |= bad_pivot(den);
     const double xh = num / den;
     XH[tid] = xh;
-    u[o] = xh;
+    (hb.tbuf ? a.ut : u)[o] = xh;
   }
   bin_sync<CLUSTER>();
 
+  TMG_T(4);
   // final values of the chunk
   if (c.n > 0) {
     const double xh = c.hub >= 0 ? remote<CLUSTER>(XH, c.hub / T)[c.hub % T] : 0.0;
@@ -403,11 +460,19 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
     else if (c.link & kLinkLeftHub) Lv = xh;
 #pragma unroll
     for (int k = 0; k < Q; k++)
-      if (k < nI) Rt[k] = fma(ivr[k], X, fma(lam[k], Lv, Rt[k]));
-    Rt[nI] = X;
+      if (k < nI) {
+        const int sl = sw<Q>(tid, k);
+        R[sl] = fma(ivr[k], X, fma(lam[k], Lv, R[sl]));
+      }
+    R[sw<Q>(tid, nI)] = X;
   }
   if (bad) atomicOr(a.err, 1);
-  bin_sync<CLUSTER>();
+  TMG_T(5);
+  if constexpr (CLUSTER) {
+    cg::this_cluster().sync();  // remote XH / sD reads done before any CTA exits
+  } else {
+    __syncwarp();
+  }
 
   // ---------------- phase C: coalesced scatter (warp-local) ----------------
 #pragma unroll
@@ -416,8 +481,10 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
     const int n_s = __shfl_sync(FULL, c.n, src);
     const int off_s = __shfl_sync(FULL, c.off, src);
     const int str_s = __shfl_sync(FULL, c.stride, src);
-    if (ksub < n_s) u[off_s + ksub * str_s] = R[(wbase + src) * QS + ksub];
+    const int tb_s = __shfl_sync(FULL, c.tb, src);
+    if (ksub < n_s) (tb_s ? a.ut : u)[off_s + ksub * str_s] = R[sw<Q>(wbase + src, ksub)];
   }
+  TMG_T(6);
 }
 
 // Point Gauss-Seidel colour stage for checkerboard (smoothers.py:65-75,
@@ -469,6 +536,27 @@ cudaError_t launch_class(const LaunchClass& lc, const SweepArgs& a, cudaStream_t
                             (const BinD*)lc.bins, (const HubD*)lc.hubs, lc.cs);
 }
 }  // namespace
+
+// Average per-CTA cycles between the phase marks of the last launches
+// (debug builds with -DTMG_PHASE_TIMING; zeros otherwise).
+extern "C" int tmg_debug_phase_cycles(double* out6) {
+  for (int k = 0; k < 6; k++) out6[k] = 0.0;
+#ifdef TMG_PHASE_TIMING
+  int n = 0;
+  cudaMemcpyFromSymbol(&n, g_phase_n, sizeof(int));
+  if (n <= 0) return 0;
+  std::vector<long long> t(8 * (size_t)(1 << 16));
+  cudaMemcpyFromSymbol(t.data(), g_phase_t, t.size() * sizeof(long long));
+  for (int b = 0; b < n; b++)
+    for (int k = 0; k < 6; k++) out6[k] += (double)(t[(size_t)(k + 1) * (1 << 16) + b] - t[(size_t)k * (1 << 16) + b]);
+  for (int k = 0; k < 6; k++) out6[k] /= n;
+  int z = 0;
+  cudaMemcpyToSymbol(g_phase_n, &z, sizeof(int));
+  return n;
+#else
+  return 0;
+#endif
+}
 
 cudaError_t init_sweep_kernels() {
   static cudaError_t done = cudaErrorNotReady;

@@ -215,18 +215,26 @@ def test_sweep_rejects_bad_shapes(cuda):
         smoothers.sweep("houndstooth", st, smoothers.PlanBundle(8, 8), u, f)
 
 
-@pytest.mark.parametrize("smoother,restriction,stretch,c,n",
-                         [("tweed", "full", "wall", 3.0, 64), ("wireframe", "full", "centre", 1.5, 64),
-                          ("zebra_alt", "half", "uniform", None, 32),
-                          ("checkerboard", "full", "wall", 2.0, 48),
-                          ("tweed_wire_alt", "full", "wall", 1.5, 40)])
-def test_solve_matches_oracle(cuda, orc, smoother, restriction, stretch, c, n):
+@pytest.mark.parametrize("smoother,restriction,stretch,c,n,m",
+                         [("tweed", "full", "wall", 3.0, 64, 64),
+                          ("wireframe", "full", "centre", 1.5, 64, 64),
+                          ("tweed", "full", "wall", 2.0, 64, 48),
+                          ("tweed", "half", "wall", 2.0, 40, 72),
+                          ("wireframe", "full", "centre", 1.5, 48, 64),
+                          ("wireframe", "full", "centre", 1.5, 72, 40),
+                          ("zebra_x", "full", "wall", 2.0, 32, 48),
+                          ("zebra_y", "full", "wall", 2.0, 48, 32),
+                          ("zebra_alt", "half", "uniform", None, 32, 32),
+                          ("checkerboard", "full", "wall", 2.0, 48, 48),
+                          ("tweed_wire_alt", "full", "wall", 1.5, 40, 40)])
+def test_solve_matches_oracle(cuda, orc, smoother, restriction, stretch, c, n, m):
     x = grid.make_coords(stretch, n, 1.0, c)
-    h = grid.build_hierarchy(x, x)
+    y = grid.make_coords(stretch, m, 1.0, c)
+    h = grid.build_hierarchy(x, y)
     cfg = mgcycle.CycleConfig(smoother=smoother, restriction=restriction)
-    f = mgcycle.random_rhs(n, n, 1)
+    f = mgcycle.random_rhs(n, m, 1)
     u, rep = mgcycle.solve(h, cfg, f)
-    H = orc.Hierarchy(x.values, x.values)
+    H = orc.Hierarchy(x.values, y.values)
     uo, repo = orc.solve(H, f, smoother=smoother, restriction=restriction)
     assert rep.cycles == repo.cycles and rep.converged == repo.converged
     assert rep.defect_norms[0] == repo.defect_norms[0]
