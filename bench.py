@@ -247,6 +247,14 @@ def run_ours(args):
     alg_bytes = 24.0 * n_int
     peak, peak_kind = _peak_hbm()
     achieved = alg_bytes / (sweep_ms * 1e-3) / 1e9
+    traffic = None
+    try:  # DRAM bytes of one such sweep from the latest committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "latest_traffic.json")) as fh:
+            tj = json.load(fh)
+        if args.config == "config3" and args.n in (None, 8192):
+            traffic = float(tj["bytes_per_sweep"]) / 1e9
+    except Exception:
+        traffic = None
 
     # end to end through the public API: pinned host u, f in; u out; every step
     u_h = torch.zeros(fd.shape, dtype=torch.float64).pin_memory()
@@ -284,7 +292,7 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (u, f = 2 x %.0f MB)" % (field_bytes / 1e6),
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_unit": "GB per launch set",
                      "kernel": "block_sweep_kernel (one finest-level sweep, both colours)",
                      "alg_bytes": alg_bytes, "ms": sweep_ms, "peak_kind": peak_kind},
         "sweep_updates_per_s": n_int / (sweep_ms * 1e-3),

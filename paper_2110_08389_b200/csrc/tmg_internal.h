@@ -91,7 +91,7 @@ struct BinD {
   int32_t pcr_steps;  // ceil(log2(max chunks of any leg in the bin))
   int32_t hub0;       // first hub of the bin in the class hub array
   int32_t nhub;
-  int32_t warp_local;  // 1: every leg of the bin lies inside one warp
+  int32_t warp_local;  // 1: every leg lies inside one warp; 2: some leg spans CTAs
 };
 
 // One kernel launch worth of bins sharing (q, cluster size).

@@ -352,21 +352,30 @@ std::string pack_plan(Geometry&& geo, int q, int mode, Plan& P) {
   for (size_t l = 0; l < g.legs.size(); l++) {
     lchunks[l] = leg_chunks(g.legs[l], q, mode, g.nx, g.ny);
     g.legs[l].nchunk = (int)lchunks[l].size();
-    if (g.legs[l].nchunk > T)
+    if (g.legs[l].nchunk > 8 * T)
       return "leg of " + std::to_string(g.legs[l].npts) +
-             " points exceeds the in-CTA solver capacity (" + std::to_string(T * q) + ")";
+             " points exceeds the cluster solver capacity (" + std::to_string(8 * T * q) + ")";
   }
-  // minimal cluster size per block (legs never straddle CTAs)
+  // Virtual-thread placement of a leg of nch chunks at position v (rank * T
+  // + offset): a leg of <= 32 chunks stays inside one warp (shuffle-only
+  // reduction), a leg of <= T chunks inside one CTA; a longer leg runs on
+  // across CTA boundaries of its cluster (cross-CTA reduction via DSMEM).
+  auto place = [&](int v, int nch) {
+    const int o = v % T;
+    if (nch <= 32 && (o / 32) != ((o + nch - 1) / 32)) v += 32 - o % 32;
+    if (nch <= T && (v % T) + nch > T) v += T - v % T;
+    return v;
+  };
+  // minimal cluster size per block
   std::vector<int> need(g.blocks.size());
   for (size_t b = 0; b < g.blocks.size(); b++) {
     const BlockD& B = g.blocks[b];
-    int ctas = 1, off = B.nleg == 0 ? 1 : 0;
+    int v = B.nleg == 0 ? 1 : 0;
     for (int l = 0; l < B.nleg; l++) {
-      int nch = g.legs[B.leg0 + l].nchunk;
-      if (nch <= 32 && (off / 32) != ((off + nch - 1) / 32)) off = (off / 32 + 1) * 32;
-      if (off + nch > T) { ctas++; off = 0; }
-      off += nch;
+      const int nch = g.legs[B.leg0 + l].nchunk;
+      v = place(v, nch) + nch;
     }
+    const int ctas = (v + T - 1) / T;
     int cs = 1;
     while (cs < ctas) cs *= 2;
     if (cs > 8) return "block needs more than 8 CTAs";
@@ -380,45 +389,41 @@ std::string pack_plan(Geometry&& geo, int q, int mode, Plan& P) {
         if (g.blocks[b].red == red && need[b] == cs) blks.push_back((int)b);
       if (blks.empty()) continue;
       std::vector<BinD> bins;
-      std::vector<int> maxch;
-      int bin = -1, rank = cs, off = 0;
+      std::vector<int> maxch, xcta;
+      int bin = -1, vpos = 0;
       for (int b : blks) {
         BlockD& B = g.blocks[b];
         for (int attempt = 0; attempt < 2; attempt++) {
-          int r = rank, o = off;
+          int v = vpos;
           bool ok = bin >= 0;
           std::vector<int> tb(B.nleg);
           int hub_t = -1;
           if (ok && B.nleg == 0) {
-            if (o + 1 > T) { r++; o = 0; }
-            if (r >= cs) ok = false;
-            else { hub_t = r * T + o; o += 1; }
+            hub_t = v;
+            v += 1;
           }
           for (int l = 0; ok && l < B.nleg; l++) {
-            int nch = g.legs[B.leg0 + l].nchunk;
-            // keep warp-sized legs inside one warp (shuffle-only reduction)
-            if (nch <= 32 && (o / 32) != ((o + nch - 1) / 32)) o = (o / 32 + 1) * 32;
-            if (o + nch > T) { r++; o = 0; }
-            if (r >= cs) { ok = false; break; }
-            tb[l] = r * T + o;
-            o += nch;
+            const int nch = g.legs[B.leg0 + l].nchunk;
+            tb[l] = place(v, nch);
+            v = tb[l] + nch;
           }
+          if (ok && v > cs * T) ok = false;
           if (!ok) {
             if (attempt == 1) return "internal: block does not fit an empty bin";
             bin++;
-            rank = 0;
-            off = 0;
+            vpos = 0;
             bins.push_back(BinD{0, 0, 0, 0});
             maxch.push_back(1);
+            xcta.push_back(0);
             continue;
           }
-          rank = r;
-          off = o;
+          vpos = v;
           B.bin = bin;
           for (int l = 0; l < B.nleg; l++) {
             LegD& L = g.legs[B.leg0 + l];
             L.tbase = tb[l];
             maxch[bin] = std::max(maxch[bin], L.nchunk);
+            if (tb[l] / T != (tb[l] + L.nchunk - 1) / T) xcta[bin] = 1;
           }
           B.hub_thread = B.nleg ? -1 : hub_t;
           break;
@@ -509,7 +514,7 @@ std::string pack_plan(Geometry&& geo, int q, int mode, Plan& P) {
         int st = 0;
         while ((1 << st) < maxch[k]) st++;
         bins[k].pcr_steps = st;
-        bins[k].warp_local = maxch[k] <= 32 ? 1 : 0;
+        bins[k].warp_local = xcta[k] ? 2 : (maxch[k] <= 32 ? 1 : 0);
         bins[k].hub0 = (int)hubs.size();
         bins[k].nhub = (int)bhubs[k].size();
         hubs.insert(hubs.end(), bhubs[k].begin(), bhubs[k].end());

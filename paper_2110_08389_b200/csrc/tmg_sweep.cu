@@ -343,10 +343,13 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
   }
   TMG_T(2);
   // publish the first-point affine form for the left neighbour chunk
+  const BinD bd_ = bins[bin];
+  const bool xcta = bd_.warp_local == 2;  // some leg crosses a CTA boundary
   sA[tid] = au;
   sB[tid] = bu;
   sC[tid] = gu;
-  __syncthreads();
+  if (CLUSTER && xcta) bin_sync<CLUSTER>();
+  else __syncthreads();
 
   // reduced row of the chunk end
   double A = 0.0, B = 1.0, Cc = 0.0, D = 0.0, H = 0.0;
@@ -361,9 +364,19 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
     B = -(pav + pcv + csum) + ae * gd;
     D = R[sl] - ae * ad;
     if (c.link & kLinkRightNext) {
-      B = fma(ce, sB[tid + 1], B);
-      Cc = ce * sC[tid + 1];
-      D = fma(-ce, sA[tid + 1], D);
+      double an, bn, gn;
+      if (CLUSTER && tid == T - 1) {  // the next chunk opens the next CTA
+        an = remote<CLUSTER>(sA, rank + 1)[0];
+        bn = remote<CLUSTER>(sB, rank + 1)[0];
+        gn = remote<CLUSTER>(sC, rank + 1)[0];
+      } else {
+        an = sA[tid + 1];
+        bn = sB[tid + 1];
+        gn = sC[tid + 1];
+      }
+      B = fma(ce, bn, B);
+      Cc = ce * gn;
+      D = fma(-ce, an, D);
     } else if (c.link & kLinkRightHub) {
       H += ce;
     }
@@ -374,9 +387,8 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
   // parallel cyclic reduction of the per-leg reduced systems.  Legs never
   // straddle CTAs; when no leg of the bin straddles a warp either, the
   // exchange runs on warp shuffles without block barriers.
-  const BinD bd_ = bins[bin];
   const int steps = bd_.pcr_steps;
-  if (bd_.warp_local) {
+  if (bd_.warp_local == 1) {
     for (int st = 0; st < steps; st++) {
       const int d = 1 << st;
       double Am = __shfl_up_sync(FULL, A, d), Bm = __shfl_up_sync(FULL, B, d);
@@ -393,6 +405,38 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
       D = D - k1 * Dm - k2 * Dp;
       H = H - k1 * Hm - k2 * Hp;
       Cc = -k2 * Cp;
+    }
+  } else if (CLUSTER && xcta && steps > 0) {
+    // some leg runs across CTAs of the cluster: the same reduction over the
+    // cluster's virtual thread index, neighbours read through DSMEM
+    const int vt = rank * T + tid, vtot = cs_size * T;
+    bin_sync<CLUSTER>();
+    sA[tid] = A; sB[tid] = B; sC[tid] = Cc; sD[tid] = D; sH[tid] = H;
+    bin_sync<CLUSTER>();
+    for (int st = 0; st < steps; st++) {
+      const int d = 1 << st;
+      double Am = 0, Bm = 1, Cm = 0, Dm = 0, Hm = 0, Ap = 0, Bp = 1, Cp = 0, Dp = 0, Hp = 0;
+      if (vt - d >= 0) {
+        const int r = (vt - d) / T, l = (vt - d) % T;
+        Am = remote<CLUSTER>(sA, r)[l]; Bm = remote<CLUSTER>(sB, r)[l];
+        Cm = remote<CLUSTER>(sC, r)[l]; Dm = remote<CLUSTER>(sD, r)[l];
+        Hm = remote<CLUSTER>(sH, r)[l];
+      }
+      if (vt + d < vtot) {
+        const int r = (vt + d) / T, l = (vt + d) % T;
+        Ap = remote<CLUSTER>(sA, r)[l]; Bp = remote<CLUSTER>(sB, r)[l];
+        Cp = remote<CLUSTER>(sC, r)[l]; Dp = remote<CLUSTER>(sD, r)[l];
+        Hp = remote<CLUSTER>(sH, r)[l];
+      }
+      bin_sync<CLUSTER>();
+      const double k1 = A * drcp(Bm), k2 = Cc * drcp(Bp);
+      A = -k1 * Am;
+      Cc = -k2 * Cp;
+      B = B - k1 * Cm - k2 * Ap;
+      D = D - k1 * Dm - k2 * Dp;
+      H = H - k1 * Hm - k2 * Hp;
+      sA[tid] = A; sB[tid] = B; sC[tid] = Cc; sD[tid] = D; sH[tid] = H;
+      bin_sync<CLUSTER>();
     }
   } else if (steps > 0) {
     __syncthreads();  // sA..sC held the first-point triples
@@ -456,8 +500,15 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
     const double xh = c.hub >= 0 ? remote<CLUSTER>(XH, c.hub / T)[c.hub % T] : 0.0;
     const double X = fma(-Qh, xh, P);
     double Lv = 0.0;
-    if (c.link & kLinkLeftPrev) Lv = fma(-sH[tid - 1], xh, sD[tid - 1]);
-    else if (c.link & kLinkLeftHub) Lv = xh;
+    if (c.link & kLinkLeftPrev) {
+      if (CLUSTER && tid == 0) {  // the previous chunk ends the previous CTA
+        Lv = fma(-remote<CLUSTER>(sH, rank - 1)[T - 1], xh, remote<CLUSTER>(sD, rank - 1)[T - 1]);
+      } else {
+        Lv = fma(-sH[tid - 1], xh, sD[tid - 1]);
+      }
+    } else if (c.link & kLinkLeftHub) {
+      Lv = xh;
+    }
 #pragma unroll
     for (int k = 0; k < Q; k++)
       if (k < nI) {
