@@ -11,6 +11,8 @@ namespace tmg {
 struct SweepArgs {
   const LegD* legs;
   const BlockD* blocks;
+  // one allocation [W | E | S | N] (lengths nx+1, nx+1, ny+1, ny+1): the
+  // block solver addresses a chunk's couplings by element offsets from W
   const double* W;
   const double* E;
   const double* S;

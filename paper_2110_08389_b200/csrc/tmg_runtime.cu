@@ -739,16 +739,24 @@ int relax_explicit(int kind, long n, const int64_t* ii, const int64_t* jj, long 
     free_plan(p);
     return fail(TMG_BADARG, err);
   }
+  // the kernel addresses W, E, S, N as one allocation (tmg_kernels.h)
+  const size_t bx = (size_t)nx + 1, by = (size_t)ny + 1;
   int* d_err = nullptr;
+  double* cw = nullptr;
   TMG_CUDA_TRY(cudaMalloc(&d_err, sizeof(int)));
+  TMG_CUDA_TRY(cudaMalloc(&cw, sizeof(double) * (2 * bx + 2 * by)));
   TMG_CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(int), s));
+  TMG_CUDA_TRY(cudaMemcpyAsync(cw, W, sizeof(double) * bx, cudaMemcpyDeviceToDevice, s));
+  TMG_CUDA_TRY(cudaMemcpyAsync(cw + bx, E, sizeof(double) * bx, cudaMemcpyDeviceToDevice, s));
+  TMG_CUDA_TRY(cudaMemcpyAsync(cw + 2 * bx, S, sizeof(double) * by, cudaMemcpyDeviceToDevice, s));
+  TMG_CUDA_TRY(cudaMemcpyAsync(cw + 2 * bx + by, N, sizeof(double) * by, cudaMemcpyDeviceToDevice, s));
   SweepArgs a{};
   a.legs = p.d_legs;
   a.blocks = p.d_blocks;
-  a.W = W;
-  a.E = E;
-  a.S = S;
-  a.N = N;
+  a.W = cw;
+  a.E = cw + bx;
+  a.S = cw + 2 * bx;
+  a.N = cw + 2 * bx + by;
   a.u = u;
   a.f = f;
   a.ld = ny + 1;
@@ -764,6 +772,7 @@ int relax_explicit(int kind, long n, const int64_t* ii, const int64_t* jj, long 
   if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   cudaFree(d_err);
+  cudaFree(cw);
   free_plan(p);
   if (e != cudaSuccess) return cuda_fail(e, "relax shim");
   if (herr & 1) return fail(TMG_SINGULAR, "zero pivot");
