@@ -119,6 +119,46 @@ int tmg_session_store(tmg_hier* h, double* u, void* stream);
  * solver state; used to time the smoother alone) */
 int tmg_session_sweeps(tmg_hier* h, int kind, int reps, void* stream);
 
+/* ---- sharded V-cycle (one process per GPU).
+ *      The grid's blocks fall into a chain of sharding groups (tweed L-shells
+ *      max(i',j'), wireframe rings min(i',j'), zebra_x rows j, zebra_y and
+ *      checkerboard columns i; coarse group G = fine group 2G).  A rank owns a
+ *      contiguous group range, sweeps only its blocks and exchanges halo
+ *      groups with its neighbours; the replaced reference loop is
+ *      mgcycle.py:89-104 with smoothers.py:139-150 split by rank.
+ *      Pair kinds (zebra_alt, tweed_wire_alt) do not shard. */
+/* number of groups (numbered 1..G), 0 if the kind does not shard; host only */
+int tmg_group_count(int kind, int nx, int ny);
+/* sizes[g] = interior points of group g, g = 0..G; returns G + 1 (-1: bad kind) */
+long tmg_group_sizes(int kind, int nx, int ny, long long* sizes, long cap);
+/* encoded work-field positions (2 * element offset + 1 if in the transposed
+ * buffer) of the interior points of groups [g0, g1) in C order, in the
+ * session layout of `kind`; returns the count (entries beyond cap are not
+ * written).  Host only. */
+long tmg_group_offsets(int kind, int nx, int ny, int g0, int g1, long long* enc, long cap);
+/* one colour stage (red = 1 / black = 0) of the blocks in groups [g0, g1) */
+int tmg_session_sweep_part(tmg_hier* h, int level, int kind, int red, int g0, int g1,
+                           void* stream);
+/* f[level+1] = R (f - L u)[level] and u[level+1] = 0 (mgcycle.py:98-100) */
+int tmg_session_restrict(tmg_hier* h, int level, int full, void* stream);
+/* u[level] += P u[level+1] (mgcycle.py:101-102) */
+int tmg_session_prolong(tmg_hier* h, int level, void* stream);
+/* the V-cycle from `level` down to the coarsest and back (replicated tail) */
+int tmg_session_tail(tmg_hier* h, int level, int kind, int full, int nu1, int nu2,
+                     void* stream);
+/* out[k] = field at enc[k] / field at enc[k] = in[k]; which: 0 u, 1 f;
+ * enc, out, in: DEVICE arrays */
+int tmg_session_gather(tmg_hier* h, int level, int which, const long long* enc, long n,
+                       double* out, void* stream);
+int tmg_session_scatter(tmg_hier* h, int level, int which, const long long* enc, long n,
+                        const double* in, void* stream);
+/* finest-level max |f - L u| over groups [g0, g1) plus the pivot flags of
+ * every level; synchronizes */
+int tmg_session_norm_part(tmg_hier* h, int kind, int g0, int g1, double* out_host,
+                          void* stream);
+/* pivot flags of every level; synchronizes */
+int tmg_session_check(tmg_hier* h, void* stream);
+
 /* ---- block geometry (layout.py:61-168): per-member (i, j, block, flags) in
  *      the reference's member order (legs tip -> branch then the branch; rings
  *      counter-clockwise from the lower-left point).  flags: bit 0 red,

@@ -63,6 +63,10 @@ def lib():
         L.orc_relax_legged.argtypes = [c_long, lp, lp, c_long, lp, c_long, c_long,
                                        dp, dp, dp, dp, dp, dp, c_long]
         L.orc_max_threads.restype = c_int
+        L.orc_group.argtypes = [c_int, c_long, c_long, c_long, c_long]
+        L.orc_group.restype = c_long
+        L.orc_sweep_part.argtypes = [c_int, c_long, c_long, dp, dp, dp, dp, dp, dp, c_int,
+                                     c_long, c_long, c_int]
         _lib = L
     return _lib
 
@@ -164,6 +168,26 @@ def sweep(kind, st, u, f, nthreads=1):
         raise ValueError("field shapes do not match the stencil grid")
     _check(lib().orc_sweep(SCHEME_IDS[kind], nx, ny, _dp(W), _dp(E), _dp(S), _dp(N),
                            _dp(u), _dp(f), int(nthreads)))
+
+
+def sweep_part(kind, st, u, f, red, g0, g1, nthreads=1):
+    """One colour stage over the blocks of sharding groups [g0, g1) -- one
+    rank's share of smoothers.py:139-150 in a sharded V-cycle."""
+    W, E, S, N = st
+    nx, ny = len(W) - 1, len(S) - 1
+    _check(lib().orc_sweep_part(SCHEME_IDS[kind], nx, ny, _dp(W), _dp(E), _dp(S), _dp(N),
+                                _dp(u), _dp(f), int(red), int(g0), int(g1), int(nthreads)))
+
+
+def group_map(kind, nx, ny):
+    """(nx+1, ny+1) int array of every interior point's sharding group
+    (0 on the boundary), from the C restatement orc_group."""
+    g = np.zeros((nx + 1, ny + 1), dtype=np.int64)
+    L, sid = lib(), SCHEME_IDS[kind]
+    for i in range(1, nx):
+        for j in range(1, ny):
+            g[i, j] = L.orc_group(sid, nx, ny, i, j)
+    return g
 
 
 def defect(st, u, f, nthreads=1):

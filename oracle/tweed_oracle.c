@@ -385,9 +385,38 @@ static int build_layout(int scheme, long nx, long ny, OLayout *L) {
 /* One colour stage, blocks in construction order (smoothers.py:139-150).
  * Same-colour blocks are independent, so the OpenMP split over
  * blocks gives bit-identical results to the serial loop. */
+/* Sharding group of an interior point for the multi-GPU partition (test
+ * oracle for DESIGN.md §6 / SURVEY.md §8(e)): tweed L-shells by
+ * max(i', j') and wireframe rings by min(i', j') with the mirrored indices
+ * of SURVEY.md §8(a'); zebra_x lines by j; zebra_y lines and checkerboard
+ * points by i.  Every block lies in one group. */
+long orc_group(int scheme, long nx, long ny, long i, long j) {
+    long ip = i < nx - i ? i : nx - i, jp = j < ny - j ? j : ny - j;
+    if (scheme == SK_TWEED) return ip > jp ? ip : jp;
+    if (scheme == SK_WIRE) return ip < jp ? ip : jp;
+    if (scheme == SK_ZEBRA_X) return j;
+    return i;
+}
+
+static long block_group(int scheme, long nx, long ny, const OBlock *B) {
+    if (B->kind == BK_LEGGED) return orc_group(scheme, nx, ny, B->bi, B->bj);
+    return orc_group(scheme, nx, ny, B->ii[0], B->jj[0]);
+}
+
+static int run_stage_part(const OLayout *L, int red, const double *W, const double *E,
+                          const double *S, const double *N, double *u, const double *f,
+                          long ld, int nthreads, int scheme, long nx, long g0, long g1);
+
 static int run_stage(const OLayout *L, int red, const double *W, const double *E,
                      const double *S, const double *N, double *u, const double *f,
                      long ld, int nthreads) {
+    return run_stage_part(L, red, W, E, S, N, u, f, ld, nthreads, -1, 0, 0, 0);
+}
+
+/* one colour stage over the blocks of groups [g0, g1) (scheme < 0: all) */
+static int run_stage_part(const OLayout *L, int red, const double *W, const double *E,
+                          const double *S, const double *N, double *u, const double *f,
+                          long ld, int nthreads, int scheme, long nx, long g0, long g1) {
     int status = ORC_OK;
     /* points first (merged), then legged, lines, rings: order is irrelevant
      * for the result but kept for fidelity */
@@ -397,6 +426,10 @@ static int run_stage(const OLayout *L, int red, const double *W, const double *E
         for (long k = 0; k < L->n; k++) {
             const OBlock *B = &L->b[k];
             if (B->kind != kind || B->red != red) continue;
+            if (scheme >= 0) {
+                long grp = block_group(scheme, nx, ld - 1, B);
+                if (grp < g0 || grp >= g1) continue;
+            }
             int st = ORC_OK;
             if (kind == BK_POINT)
                 st = orc_relax_points(B->npts, B->ii, B->jj, W, E, S, N, u, f, ld);
@@ -438,6 +471,30 @@ int orc_sweep(int scheme, long nx, long ny, const double *W, const double *E,
     if (st != ORC_OK) return st;
     st = run_stage(&L, 1, W, E, S, N, u, f, ld, nthreads);
     if (st == ORC_OK) st = run_stage(&L, 0, W, E, S, N, u, f, ld, nthreads);
+    lay_free(&L);
+    return st;
+}
+
+/* One colour stage (red = 1 / black = 0) of one rank's share, the blocks of
+ * sharding groups [g0, g1) -- the CPU restatement of a sharded sweep. */
+int orc_sweep_part(int scheme, long nx, long ny, const double *W, const double *E,
+                   const double *S, const double *N, double *u, const double *f,
+                   int red, long g0, long g1, int nthreads) {
+    long ld = ny + 1;
+    if (scheme == SK_CHECKER) {
+#pragma omp parallel for schedule(static) num_threads(nthreads) if (nthreads > 1)
+        for (long i = (g0 > 1 ? g0 : 1); i < (g1 < nx ? g1 : nx); i++)
+            for (long j = 1; j < ny; j++) {
+                if ((((i + j) % 2) == 0) != red) continue;
+                long ii = i, jj = j;
+                orc_relax_points(1, &ii, &jj, W, E, S, N, u, f, ld);
+            }
+        return ORC_OK;
+    }
+    OLayout L;
+    int st = build_layout(scheme, nx, ny, &L);
+    if (st != ORC_OK) return st;
+    st = run_stage_part(&L, red, W, E, S, N, u, f, ld, nthreads, scheme, nx, g0, g1);
     lay_free(&L);
     return st;
 }

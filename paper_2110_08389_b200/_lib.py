@@ -63,6 +63,17 @@ def _declare(L):
         "tmg_session_store": ([vp, vp, vp], ip),
         "tmg_session_sweeps": ([vp, ip, ip, vp], ip),
         "tmg_debug_phase_cycles": ([pd], ip),
+        "tmg_group_count": ([ip, ip, ip], ip),
+        "tmg_group_sizes": ([ip, ip, ip, vp, lp], lp),
+        "tmg_group_offsets": ([ip, ip, ip, ip, ip, vp, lp], lp),
+        "tmg_session_sweep_part": ([vp, ip, ip, ip, ip, ip, vp], ip),
+        "tmg_session_restrict": ([vp, ip, ip, vp], ip),
+        "tmg_session_prolong": ([vp, ip, vp], ip),
+        "tmg_session_tail": ([vp, ip, ip, ip, ip, ip, vp], ip),
+        "tmg_session_gather": ([vp, ip, ip, vp, lp, vp, vp], ip),
+        "tmg_session_scatter": ([vp, ip, ip, vp, lp, vp, vp], ip),
+        "tmg_session_norm_part": ([vp, ip, ip, ip, pd, vp], ip),
+        "tmg_session_check": ([vp, vp], ip),
         "tmg_solve": ([vp, ip, ip, ip, ip, dp, ip, vp, vp, pd, pi, pi, vp], ip),
         "tmg_layout_dump": ([ip, ip, ip, pi, pi, pi, pi, lp], lp),
         "tmg_relax_points": ([lp, vp, vp, ip, ip, vp, vp, vp, vp, vp, vp, vp], ip),

@@ -75,8 +75,14 @@ __device__ __forceinline__ double lu_strided(const double* __restrict__ b, size_
 
 // Residual max-norm over the interior; one 32x32 tile per CTA (256 threads,
 // 4 points per thread), lanes along the owning buffer's contiguous axis.
+// With gsel.g0 > 0 only points of sharding groups [g0, g1) count (one rank's
+// share in a sharded solve; the ranks then all-reduce the maximum).
+struct GroupSel {
+  int scheme, g0, g1;
+};
+
 __global__ void __launch_bounds__(256) hdefect_norm_kernel(GridArgs g, FieldView U, FieldView F,
-                                                           unsigned long long* dmax) {
+                                                           unsigned long long* dmax, GroupSel gsel) {
   const int i0 = 1 + blockIdx.y * TILE, j0 = 1 + blockIdx.x * TILE;
   const int ni = min(TILE, g.nx - i0), nj = min(TILE, g.ny - j0);
   const int own = tile_owner_exact(U, i0 - 1, j0 - 1, ni + 2, nj + 2);
@@ -88,6 +94,10 @@ __global__ void __launch_bounds__(256) hdefect_norm_kernel(GridArgs g, FieldView
     const int i = own == 1 ? i0 + a : i0 + b;
     const int j = own == 1 ? j0 + b : j0 + a;
     if (i >= g.nx || j >= g.ny) continue;
+    if (gsel.g0 > 0) {
+      const int grp = point_group(gsel.scheme, g.nx, g.ny, i, j);
+      if (grp < gsel.g0 || grp >= gsel.g1) continue;
+    }
     const double Wi = __ldg(g.W + i), Ei = __ldg(g.E + i), Sj = __ldg(g.S + j), Nj = __ldg(g.N + j);
     double lu, fv;
     if (own == 1) {
@@ -275,10 +285,47 @@ __global__ void hdense_apply_kernel(GridArgs g, const double* __restrict__ Ainv,
 }  // namespace
 
 cudaError_t launch_hdefect_norm(const GridArgs& g, const FieldView& U, const FieldView& F,
-                                unsigned long long* dmax, cudaStream_t s) {
+                                unsigned long long* dmax, cudaStream_t s, int scheme, int g0,
+                                int g1) {
   if (g.nx < 2 || g.ny < 2) return cudaSuccess;
   dim3 grid((g.ny - 1 + TILE - 1) / TILE, (g.nx - 1 + TILE - 1) / TILE);
-  hdefect_norm_kernel<<<grid, 256, 0, s>>>(g, U, F, dmax);
+  hdefect_norm_kernel<<<grid, 256, 0, s>>>(g, U, F, dmax, GroupSel{scheme, g0, g1});
+  return cudaGetLastError();
+}
+
+namespace {
+// enc = 2 * element offset + (1 if the point lives in the T buffer)
+__global__ void gather_points_kernel(FieldView V, const long long* __restrict__ enc, long n,
+                                     double* __restrict__ out) {
+  for (long k = blockIdx.x * (long)blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
+    const long long e = enc[k];
+    out[k] = ((e & 1) ? V.t : V.n)[e >> 1];
+  }
+}
+__global__ void scatter_points_kernel(FieldView V, const long long* __restrict__ enc, long n,
+                                      const double* __restrict__ in) {
+  for (long k = blockIdx.x * (long)blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
+    const long long e = enc[k];
+    ((e & 1) ? V.t : V.n)[e >> 1] = in[k];
+  }
+}
+int point_blocks(long n) {
+  const long b = (n + 255) / 256;
+  return (int)(b < 148 * 8 ? (b > 0 ? b : 1) : 148 * 8);
+}
+}  // namespace
+
+cudaError_t launch_gather_points(const FieldView& V, const long long* enc, long n, double* out,
+                                 cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  gather_points_kernel<<<point_blocks(n), 256, 0, s>>>(V, enc, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_points(const FieldView& V, const long long* enc, long n,
+                                  const double* in, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  scatter_points_kernel<<<point_blocks(n), 256, 0, s>>>(V, enc, n, in);
   return cudaGetLastError();
 }
 

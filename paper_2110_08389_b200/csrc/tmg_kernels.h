@@ -67,8 +67,15 @@ cudaError_t launch_dense_solve(const GridArgs& g, const double* Ainv, double* u,
                                const double* f, double* work, cudaStream_t s);
 
 // ---- hybrid-layout (tmg_layout.h) versions used inside the V-cycle ----
+// scheme / [g0, g1): only points of those sharding groups count (g0 = 0: all)
 cudaError_t launch_hdefect_norm(const GridArgs& g, const FieldView& U, const FieldView& F,
-                                unsigned long long* dmax, cudaStream_t s);
+                                unsigned long long* dmax, cudaStream_t s, int scheme = 0,
+                                int g0 = 0, int g1 = 0);
+// out[k] = V at enc[k] / V at enc[k] = in[k]; enc = 2 * offset + (T buffer)
+cudaError_t launch_gather_points(const FieldView& V, const long long* enc, long n, double* out,
+                                 cudaStream_t s);
+cudaError_t launch_scatter_points(const FieldView& V, const long long* enc, long n,
+                                  const double* in, cudaStream_t s);
 cudaError_t launch_hdefect_restrict(const GridArgs& g, int full, const FieldView& U,
                                     const FieldView& F, const FieldView& FC, cudaStream_t s);
 // u += P uc on the fine interior; (nx, ny) are the FINE dimensions

@@ -38,6 +38,35 @@ __host__ __device__ inline int layout_for_kind(int kind) {
   }
 }
 
+// Sharding group of an interior point (multi-GPU unit): every
+// block of a scheme lies in one group, groups form a chain (a point's stencil
+// neighbours are in groups g-1..g+1), and coarse group G is fine group 2G.
+//   tweed        L-shell / cross / strip index max(i', j')   (layout.py:61-133)
+//   wireframe    ring index min(i', j'), the centre is q+1   (layout.py:136-168)
+//   zebra_x      row j;  zebra_y, checkerboard: column i     (smoothers.py:65-89)
+// Scheme codes as tmg_internal.h / include/tweedmg_b200.h.
+__host__ __device__ inline int point_group(int scheme, int nx, int ny, int i, int j) {
+  const int ip = i < nx - i ? i : nx - i;
+  const int jp = j < ny - j ? j : ny - j;
+  switch (scheme) {
+    case 4: return ip > jp ? ip : jp;
+    case 5: return ip < jp ? ip : jp;
+    case 1: return j;
+    default: return i;
+  }
+}
+// groups are numbered 1..group_count (0 if the scheme does not shard)
+__host__ __device__ inline int group_count(int scheme, int nx, int ny) {
+  switch (scheme) {
+    case 4: return (nx > ny ? nx : ny) / 2;
+    case 5: return (nx < ny ? nx : ny) / 2;
+    case 1: return ny - 1;
+    case 0:
+    case 2: return nx - 1;
+    default: return 0;
+  }
+}
+
 struct FieldView {
   double* n;
   double* t;

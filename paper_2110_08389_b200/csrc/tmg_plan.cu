@@ -337,6 +337,54 @@ std::string build_plan(int scheme, int nx, int ny, int q, int mode, Plan& P) {
   return pack_plan(std::move(g), q, mode, P);
 }
 
+void filter_groups(Geometry& g, int g0, int g1) {
+  Geometry out;
+  out.scheme = g.scheme;
+  out.nx = g.nx;
+  out.ny = g.ny;
+  for (const BlockD& B : g.blocks) {
+    int i = B.hi, j = B.hj;
+    if (i < 0) {
+      i = g.legs[B.leg0].i0;
+      j = g.legs[B.leg0].j0;
+    }
+    const int grp = point_group(g.scheme, g.nx, g.ny, i, j);
+    if (grp < g0 || grp >= g1) continue;
+    BlockD nb = B;
+    nb.leg0 = (int32_t)out.legs.size();
+    for (int l = 0; l < B.nleg; l++) {
+      LegD L = g.legs[B.leg0 + l];
+      L.block = (int32_t)out.blocks.size();
+      out.legs.push_back(L);
+    }
+    out.blocks.push_back(nb);
+  }
+  g = std::move(out);
+}
+
+std::string build_plan_part(int scheme, int nx, int ny, int q, int mode, int g0, int g1,
+                            Plan& P) {
+  const int G = group_count(scheme, nx, ny);
+  if (G < 1) return "smoother kind " + std::to_string(scheme) + " has no sharding groups";
+  if (g0 < 1 || g1 > G + 1 || g0 >= g1)
+    return "group range [" + std::to_string(g0) + ", " + std::to_string(g1) +
+           ") outside 1.." + std::to_string(G);
+  if (scheme == SCHEME_CHECKERBOARD) {
+    std::string err = build_plan(scheme, nx, ny, q, mode, P);
+    P.g0 = g0;  // rows i in [g0, g1)
+    P.g1 = g1;
+    return err;
+  }
+  Geometry g;
+  std::string err = build_geometry(scheme, nx, ny, g);
+  if (!err.empty()) return err;
+  filter_groups(g, g0, g1);
+  err = pack_plan(std::move(g), q, mode, P);
+  P.g0 = g0;
+  P.g1 = g1;
+  return err;
+}
+
 std::string pack_plan(Geometry&& geo, int q, int mode, Plan& P) {
   P = Plan();
   if (q < 1 || q > kQmax || (q & (q - 1))) return "chunk size q must be a power of two <= 16";

@@ -33,10 +33,16 @@ struct Plan {
   BlockD* d_blocks = nullptr;
   std::vector<LaunchClass> classes;  // red classes first, then black
   bool point_scheme = false;         // checkerboard: dedicated point kernel
+  int g0 = 0, g1 = 0;                // group range of a partial plan (0, 0: all)
   size_t device_bytes = 0;
 };
 
 std::string build_plan(int scheme, int nx, int ny, int q, int mode, Plan& p);
+// Plan restricted to the blocks of sharding groups [g0, g1) (point_group in
+// tmg_layout.h): one rank's share of a colour stage in a sharded V-cycle.
+std::string build_plan_part(int scheme, int nx, int ny, int q, int mode, int g0, int g1, Plan& p);
+// Keep only the blocks whose group lies in [g0, g1).
+void filter_groups(Geometry& g, int g0, int g1);
 // Pack an explicit geometry (e.g. one block from the per-block shims).
 std::string pack_plan(Geometry&& g, int q, int mode, Plan& p);
 // Append a block made of explicit member paths (host index arrays).

@@ -58,6 +58,7 @@ struct tmg_level {
   double *W = nullptr, *E = nullptr, *S = nullptr, *N = nullptr;
   std::vector<double> hW, hE, hS, hN;
   Plan* plans[7][4] = {};  // [scheme][layout mode]
+  std::map<std::tuple<int, int, int, int>, Plan*> part_plans;  // (scheme, mode, g0, g1)
   int* d_err = nullptr;
   unsigned long long* d_norm = nullptr;
   int* h_err = nullptr;                  // pinned
@@ -97,6 +98,27 @@ int get_plan(tmg_level* lv, int scheme, int mode, Plan** out) {
     lv->bytes += (long long)p->device_bytes;
   }
   *out = lv->plans[scheme][mode];
+  return TMG_OK;
+}
+
+// plan of one rank's sharding groups [g0, g1) (sharded V-cycle)
+int get_part_plan(tmg_level* lv, int scheme, int mode, int g0, int g1, Plan** out) {
+  auto key = std::make_tuple(scheme, mode, g0, g1);
+  auto it = lv->part_plans.find(key);
+  if (it == lv->part_plans.end()) {
+    cudaError_t e = init_sweep_kernels();
+    if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");
+    Plan* p = new Plan();
+    std::string err = build_plan_part(scheme, lv->nx, lv->ny, default_q(), mode, g0, g1, *p);
+    if (!err.empty()) {
+      free_plan(*p);
+      delete p;
+      return fail(TMG_BADARG, err);
+    }
+    lv->bytes += (long long)p->device_bytes;
+    it = lv->part_plans.emplace(key, p).first;
+  }
+  *out = it->second;
   return TMG_OK;
 }
 
@@ -276,10 +298,12 @@ int zero_field(const FieldView& v, cudaStream_t s) {
   return TMG_OK;
 }
 
-// one V-cycle on the hierarchy's work fields (mgcycle.py:89-104)
-int vcycle_launches(tmg_hier* h, int kind, int full, int nu1, int nu2, cudaStream_t s) {
+// one V-cycle on the hierarchy's work fields (mgcycle.py:89-104), entered at
+// level l0 (0: the whole cycle; > 0: the replicated tail of a sharded cycle)
+int vcycle_launches(tmg_hier* h, int kind, int full, int nu1, int nu2, cudaStream_t s,
+                    int l0 = 0) {
   const int L = (int)h->lv.size();
-  for (int l = 0; l < L - 1; l++) {  // down: smooth, residual + restriction, zero guess
+  for (int l = l0; l < L - 1; l++) {  // down: smooth, residual + restriction, zero guess
     tmg_level* lv = h->lv[l];
     for (int k = 0; k < nu1; k++) {
       int st = sweep_kind(lv, kind, 3, h->U[l], h->F[l], s);
@@ -298,7 +322,7 @@ int vcycle_launches(tmg_hier* h, int kind, int full, int nu1, int nu2, cudaStrea
                                         lc->d_work, s);
     if (e != cudaSuccess) return cuda_fail(e, "coarse solve");
   }
-  for (int l = L - 2; l >= 0; l--) {  // up: prolongation + correction, smooth
+  for (int l = L - 2; l >= l0; l--) {  // up: prolongation + correction, smooth
     tmg_level* lv = h->lv[l];
     cudaError_t e = launch_hprolong_correct(lv->nx, lv->ny, h->U[l + 1], h->U[l], s);
     if (e != cudaSuccess) return cuda_fail(e, "prolong_correct");
@@ -473,6 +497,10 @@ int tmg_level_destroy(tmg_level* lv) {
         free_plan(*p);
         delete p;
       }
+  for (auto& kv : lv->part_plans) {
+    free_plan(*kv.second);
+    delete kv.second;
+  }
   cudaFree(lv->W);
   cudaFree(lv->d_err);
   cudaFreeHost(lv->h_err);
@@ -692,6 +720,152 @@ int tmg_solve(tmg_hier* h, int kind, int full, int nu1, int nu2, double tol, int
     }
     return session_store(h, u, s);
   });
+}
+
+// ---- sharded V-cycle support (one rank's share) ----
+
+int tmg_group_count(int kind, int nx, int ny) {
+  if (!valid_kind(kind) || nx < 2 || ny < 2) return 0;
+  return group_count(kind, nx, ny);
+}
+
+long tmg_group_sizes(int kind, int nx, int ny, long long* sizes, long cap) {
+  const int G = tmg_group_count(kind, nx, ny);
+  if (G < 1) {
+    g_last_error = "smoother kind " + std::to_string(kind) + " does not shard";
+    return -1;
+  }
+  if (cap < G + 1) return G + 1;
+  for (int g = 0; g <= G; g++) sizes[g] = 0;
+  for (int i = 1; i < nx; i++)
+    for (int j = 1; j < ny; j++) sizes[point_group(kind, nx, ny, i, j)]++;
+  return G + 1;
+}
+
+long tmg_group_offsets(int kind, int nx, int ny, int g0, int g1, long long* enc, long cap) {
+  const int G = tmg_group_count(kind, nx, ny);
+  if (G < 1) {
+    g_last_error = "smoother kind " + std::to_string(kind) + " does not shard";
+    return -1;
+  }
+  const FieldView v{nullptr, nullptr, nx, ny, session_mode(kind)};
+  long n = 0;
+  for (int i = 1; i < nx; i++)
+    for (int j = 1; j < ny; j++) {
+      const int grp = point_group(kind, nx, ny, i, j);
+      if (grp < g0 || grp >= g1) continue;
+      if (n < cap) {
+        const bool t = owns_t(v.mode, nx, ny, i, j);
+        enc[n] = 2 * (long long)(t ? v.off_t(i, j) : v.off_n(i, j)) + (t ? 1 : 0);
+      }
+      n++;
+    }
+  return n;
+}
+
+}  // extern "C"
+
+namespace {
+int session_level(tmg_hier* h, int level, int need_coarser) {
+  if (!h || !h->loaded) return fail(TMG_BADARG, "no solver session loaded");
+  if (level < 0 || level >= (int)h->lv.size() - need_coarser)
+    return fail(TMG_BADARG, "level " + std::to_string(level) + " out of range");
+  return TMG_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int tmg_session_sweep_part(tmg_hier* h, int level, int kind, int red, int g0, int g1,
+                           void* stream) {
+  int st = session_level(h, level, 0);
+  if (st) return st;
+  if (!valid_kind(kind) || session_mode(kind) != h->mode)
+    return fail(TMG_BADARG, "smoother kind does not match the loaded session's layout");
+  return guarded([&]() -> int {
+    tmg_level* lv = h->lv[level];
+    Plan* p = nullptr;
+    int st2 = get_part_plan(lv, kind, h->mode, g0, g1, &p);
+    if (st2) return st2;
+    cudaError_t e = launch_colour(*p, red ? 1 : 0, sweep_args(lv, p, h->U[level], h->F[level]),
+                                  (cudaStream_t)stream);
+    return e == cudaSuccess ? TMG_OK : cuda_fail(e, "sweep launch");
+  });
+}
+
+int tmg_session_restrict(tmg_hier* h, int level, int full, void* stream) {
+  int st = session_level(h, level, 1);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = launch_hdefect_restrict(h->lv[level]->grid(), full, h->U[level], h->F[level],
+                                          h->F[level + 1], s);
+  if (e != cudaSuccess) return cuda_fail(e, "defect_restrict");
+  return zero_field(h->U[level + 1], s);
+}
+
+int tmg_session_prolong(tmg_hier* h, int level, void* stream) {
+  int st = session_level(h, level, 1);
+  if (st) return st;
+  tmg_level* lv = h->lv[level];
+  cudaError_t e = launch_hprolong_correct(lv->nx, lv->ny, h->U[level + 1], h->U[level],
+                                          (cudaStream_t)stream);
+  return e == cudaSuccess ? TMG_OK : cuda_fail(e, "prolong_correct");
+}
+
+int tmg_session_tail(tmg_hier* h, int level, int kind, int full, int nu1, int nu2, void* stream) {
+  int st = check_hier_args(h, kind, nu1, nu2);
+  if (!st) st = session_level(h, level, 0);
+  if (st) return st;
+  if (session_mode(kind) != h->mode)
+    return fail(TMG_BADARG, "smoother kind does not match the loaded session's layout");
+  return guarded([&]() -> int {
+    int st2 = prepare(h, kind);
+    return st2 ? st2 : vcycle_launches(h, kind, full, nu1, nu2, (cudaStream_t)stream, level);
+  });
+}
+
+int tmg_session_gather(tmg_hier* h, int level, int which, const long long* enc, long n,
+                       double* out, void* stream) {
+  int st = session_level(h, level, 0);
+  if (st) return st;
+  const FieldView& v = which ? h->F[level] : h->U[level];
+  cudaError_t e = launch_gather_points(v, enc, n, out, (cudaStream_t)stream);
+  return e == cudaSuccess ? TMG_OK : cuda_fail(e, "gather");
+}
+
+int tmg_session_scatter(tmg_hier* h, int level, int which, const long long* enc, long n,
+                        const double* in, void* stream) {
+  int st = session_level(h, level, 0);
+  if (st) return st;
+  const FieldView& v = which ? h->F[level] : h->U[level];
+  cudaError_t e = launch_scatter_points(v, enc, n, in, (cudaStream_t)stream);
+  return e == cudaSuccess ? TMG_OK : cuda_fail(e, "scatter");
+}
+
+int tmg_session_norm_part(tmg_hier* h, int kind, int g0, int g1, double* out_host, void* stream) {
+  int st = session_level(h, 0, 0);
+  if (st) return st;
+  if (tmg_group_count(kind, h->lv[0]->nx, h->lv[0]->ny) < 1)
+    return fail(TMG_BADARG, "smoother kind does not shard");
+  return guarded([&]() -> int {
+    cudaStream_t s = (cudaStream_t)stream;
+    tmg_level* fine = h->lv[0];
+    TMG_CUDA_TRY(cudaMemsetAsync(fine->d_norm, 0, sizeof(unsigned long long), s));
+    cudaError_t e = launch_hdefect_norm(fine->grid(), h->U[0], h->F[0], fine->d_norm, s, kind,
+                                        g0, g1);
+    if (e != cudaSuccess) return cuda_fail(e, "defect_norm");
+    TMG_CUDA_TRY(cudaMemcpyAsync(fine->h_norm, fine->d_norm, sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, s));
+    int st2 = flags_all(h, s);
+    if (st2) return st2;
+    *out_host = bits_to_double(*fine->h_norm);
+    return TMG_OK;
+  });
+}
+
+int tmg_session_check(tmg_hier* h, void* stream) {
+  if (!h) return fail(TMG_BADARG, "null hierarchy");
+  return guarded([&] { return flags_all(h, (cudaStream_t)stream); });
 }
 
 long tmg_layout_dump(int kind, int nx, int ny, int* oi, int* oj, int* oblk, int* oflags,

@@ -552,9 +552,11 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
 
 // Point Gauss-Seidel colour stage for checkerboard (smoothers.py:65-75,
 // _ckernels.pyx:42-51): red = (i + j) even.
-__global__ void __launch_bounds__(256) point_sweep_kernel(SweepArgs a, int nx, int ny, int red) {
+// Rows i in [i0, i0 + gridDim.y) (a partial plan covers its sharding groups).
+__global__ void __launch_bounds__(256) point_sweep_kernel(SweepArgs a, int nx, int ny, int red,
+                                                          int i0) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x + 1;
-  const int i = blockIdx.y + 1;
+  const int i = blockIdx.y + i0;
   if (j >= ny || i >= nx) return;
   if ((((i + j) & 1) == 0) != (red != 0)) return;
   const size_t ld = (size_t)a.ld, o = (size_t)i * ld + j;
@@ -652,8 +654,9 @@ cudaError_t init_sweep_kernels() {
 
 cudaError_t launch_colour(const Plan& P, int red, const SweepArgs& a, cudaStream_t stream) {
   if (P.point_scheme) {
-    dim3 grid((P.geo.ny - 1 + 255) / 256, P.geo.nx - 1);
-    point_sweep_kernel<<<grid, 256, 0, stream>>>(a, P.geo.nx, P.geo.ny, red);
+    const int i0 = P.g0 > 0 ? P.g0 : 1, i1 = P.g0 > 0 ? P.g1 : P.geo.nx;
+    dim3 grid((P.geo.ny - 1 + 255) / 256, i1 - i0);
+    point_sweep_kernel<<<grid, 256, 0, stream>>>(a, P.geo.nx, P.geo.ny, red, i0);
     return cudaGetLastError();
   }
   for (const LaunchClass& lc : P.classes) {
