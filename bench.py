@@ -15,9 +15,11 @@ buffers copied in and out every step, and the CPU oracle (C restatement of
 the reference, 1 core) on one V-cycle of the same workload.
 
 `--impl reference` times the reference algorithm's CPU path (the oracle port,
-all host threads) on the same workload and metric.  Under torchrun (N>1) every
-rank runs an independent replica (weak scaling; the hot path is not sharded in
-this round), timed on the device and reduced with max over ranks.
+all host threads) on the same workload and metric.  Under torchrun (N>1) the
+one problem is sharded over the ranks (paper_2110_08389_b200.sharded: group
+ranges per rank, NCCL halo swaps, replicated coarse tail; strong scaling),
+timed on the device and reduced with max over ranks; `--replicas` runs N
+independent copies instead (weak scaling).
 """
 
 from __future__ import annotations
@@ -206,6 +208,7 @@ def run_ours(args):
     for lv in h.levels:
         _lib.check(L.tmg_level_check(native_level(lv.stencil), sh))
     kernels_per_cycle = L.tmg_hier_graph_kernels(state.native)
+    launches0 = L.tmg_kernel_launches()
 
     clk = ClockSampler(local)
     clk.start()
@@ -221,6 +224,7 @@ def run_ours(args):
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
+    launches = L.tmg_kernel_launches() - launches0
     t_ms = max_over_ranks(e0.elapsed_time(e1))
     t_soak = time.perf_counter()
     while time.perf_counter() - t_soak < 0.4:
@@ -298,7 +302,8 @@ def run_ours(args):
         "sweep_updates_per_s": n_int / (sweep_ms * 1e-3),
         "e2e": e2e,
         "clocks": clocks,
-        "gpu_launches": kernels_per_cycle * args.steps,
+        "gpu_launches": launches,
+        "kernels_per_cycle": kernels_per_cycle,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         secs, _ = cpu_oracle_cycle(w, f_host, 1)
@@ -313,6 +318,116 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_sharded(args):
+    """N > 1: one problem, fine levels split between the ranks (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2110_08389_b200 import _lib, configs, grid, mgcycle, sharded
+
+    world, rank, local = _dist()
+    # TMG_DIST_BACKEND=gloo (halos staged through the host) lets the sharded
+    # path be exercised with several ranks on one GPU; timings need nccl
+    backend = os.environ.get("TMG_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    L = _lib.lib()
+    w = configs.workload(args.config, n=args.n, nu=args.nu)
+    h = grid.build_hierarchy(w.x, w.x)
+    cfg = mgcycle.CycleConfig(smoother=w.smoother, nu1=w.nu1, nu2=w.nu2)
+    f_host = w.rhs()
+    fd = torch.from_numpy(f_host).cuda()
+    u = torch.zeros_like(fd)
+    solver = sharded.ShardedSolver(h, cfg)
+    solver.load(u, fd)
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, k):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(args.warmup, 3)):
+        solver.v_cycle()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    launches0, swaps0 = L.tmg_kernel_launches(), solver.exchanges
+    t_ms = timed(solver.v_cycle, args.steps)
+    launches = L.tmg_kernel_launches() - launches0
+    swaps = (solver.exchanges - swaps0) // args.steps
+    clocks = clk.stop()
+    upc = _updates_per_cycle(h, w.nu1 + w.nu2)
+    value = upc * args.steps / (t_ms * 1e-3)
+
+    # dominant kernel: this rank's finest-level colour stages
+    g0, g1 = solver.plan.own(0, rank)
+    reps = 20
+
+    def rank_sweep():
+        for red in (1, 0):
+            solver.ops.sweep(0, red, g0, g1)
+    sweep_ms = timed(rank_sweep, reps) / reps
+    owned = int(sharded.group_sizes(w.smoother, h.finest.nx, h.finest.ny)[g0:g1].sum())
+    alg_bytes = 24.0 * owned
+    peak, peak_kind = _peak_hbm()
+    achieved = alg_bytes / (sweep_ms * 1e-3) / 1e9
+
+    # end to end: pinned host f and u in, sharded cycle, full u gathered and out
+    u_h = torch.zeros(fd.shape, dtype=torch.float64).pin_memory()
+    f_h = torch.from_numpy(f_host).pin_memory()
+    ue, fe = torch.empty_like(fd), torch.empty_like(fd)
+
+    def e2e_step():
+        fe.copy_(f_h, non_blocking=True)
+        ue.copy_(u_h, non_blocking=True)
+        solver.load(ue, fe)
+        solver.v_cycle()
+        solver.store(ue)
+        u_h.copy_(ue, non_blocking=True)
+    e2e_step()
+    e2e_steps = max(1, min(args.steps, 5))
+    e2e_ms = timed(e2e_step, e2e_steps) / e2e_steps
+    field_bytes = fd.numel() * 8
+    line = {
+        "metric": "smoother grid-pt updates/s", "value": value, "unit": "grid-pt updates/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": _workload_desc(w), "levels": len(h.levels),
+                   "updates_per_cycle": upc, "vcycle_ms": t_ms / args.steps,
+                   "sharded_levels": solver.plan.nshard,
+                   "l2": "inputs larger than L2 (u, f = 2 x %.0f MB)" % (field_bytes / 1e6),
+                   "parallelism": f"sharded x{world}: group ranges, {backend} halo swaps"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "block_sweep_kernel (rank's finest-level share, both colours)",
+                     "alg_bytes": alg_bytes, "ms": sweep_ms, "peak_kind": peak_kind},
+        "e2e": {"value": upc / (e2e_ms * 1e-3), "unit": "grid-pt updates/s",
+                "h2d_bytes_per_step": 2 * field_bytes, "d2h_bytes_per_step": field_bytes,
+                "ms_per_step": e2e_ms},
+        "clocks": clocks,
+        "gpu_launches": launches,
+        "halo_swaps_per_cycle": swaps, "dist_backend": backend,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -323,11 +438,15 @@ def main():
     p.add_argument("--n", type=int, default=None, help="override grid intervals")
     p.add_argument("--nu", type=int, default=2, help="config3: V(nu,nu)")
     p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    p.add_argument("--replicas", action="store_true",
+                   help="N > 1: independent replicas instead of one sharded problem")
     args = p.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif _dist()[0] > 1 and not args.replicas:
+        run_sharded(args)
     else:
         run_ours(args)
 

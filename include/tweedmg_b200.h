@@ -189,6 +189,9 @@ int tmg_relax_legged(long n, const int64_t* ii, const int64_t* jj, long m, const
  *      scatter) over the last launch; non-zero only in builds made with
  *      EXTRA=-DTMG_PHASE_TIMING.  Returns the number of CTAs sampled. */
 int tmg_debug_phase_cycles(double* out6);
+/* kernels this library has put on streams so far (host-side count; a graph
+ * replay adds its kernel nodes) */
+long long tmg_kernel_launches(void);
 
 #ifdef __cplusplus
 }

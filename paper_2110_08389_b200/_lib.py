@@ -63,6 +63,7 @@ def _declare(L):
         "tmg_session_store": ([vp, vp, vp], ip),
         "tmg_session_sweeps": ([vp, ip, ip, vp], ip),
         "tmg_debug_phase_cycles": ([pd], ip),
+        "tmg_kernel_launches": ([], ctypes.c_longlong),
         "tmg_group_count": ([ip, ip, ip], ip),
         "tmg_group_sizes": ([ip, ip, ip, vp, lp], lp),
         "tmg_group_offsets": ([ip, ip, ip, ip, ip, vp, lp], lp),

@@ -210,6 +210,7 @@ __global__ void dense_apply_kernel(GridArgs g, const double* __restrict__ Ainv,
 cudaError_t launch_apply(const GridArgs& g, const double* u, const double* f, double* out,
                          cudaStream_t s) {
   dim3 grid((g.ny + 1 + 255) / 256, g.nx + 1);
+  TMG_COUNT(1);
   apply_kernel<<<grid, 256, 0, s>>>(g, u, f, out);
   return cudaGetLastError();
 }
@@ -221,6 +222,7 @@ cudaError_t launch_defect_norm(const GridArgs& g, const double* u, const double*
   int by = g.nx - 1;
   const int cap = 148 * 16 / (bx > 0 ? bx : 1);
   if (by > cap) by = cap > 0 ? cap : 1;
+  TMG_COUNT(1);
   defect_norm_kernel<<<dim3(bx, by), 256, 0, s>>>(g, u, f, dmax_bits);
   return cudaGetLastError();
 }
@@ -230,6 +232,7 @@ cudaError_t launch_defect_restrict(const GridArgs& g, int full, const double* u,
   const int nxc = g.nx / 2, nyc = g.ny / 2;
   if (nxc < 2 || nyc < 2) return cudaSuccess;
   dim3 grid((nyc - 1 + RTJ - 1) / RTJ, (nxc - 1 + RTI - 1) / RTI);
+  TMG_COUNT(1);
   defect_restrict_kernel<<<grid, 256, 0, s>>>(g, full, u, f, fc);
   return cudaGetLastError();
 }
@@ -238,12 +241,14 @@ cudaError_t launch_restrict(int nxf, int nyf, int full, const double* d, double*
                             cudaStream_t s) {
   const int nxc = nxf / 2, nyc = nyf / 2;
   dim3 grid((nyc + 1 + 255) / 256, nxc + 1);
+  TMG_COUNT(1);
   restrict_kernel<<<grid, 256, 0, s>>>(nxf, nyf, full, d, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_prolong(int nxc, int nyc, const double* uc, double* v, cudaStream_t s) {
   dim3 grid((2 * nyc + 1 + 255) / 256, 2 * nxc + 1);
+  TMG_COUNT(1);
   prolong_kernel<<<grid, 256, 0, s>>>(nxc, nyc, uc, v);
   return cudaGetLastError();
 }
@@ -251,6 +256,7 @@ cudaError_t launch_prolong(int nxc, int nyc, const double* uc, double* v, cudaSt
 cudaError_t launch_prolong_correct(int nxc, int nyc, const double* uc, double* u, cudaStream_t s) {
   if (nxc < 1 || nyc < 1) return cudaSuccess;
   dim3 grid((2 * nyc - 1 + 255) / 256, 2 * nxc - 1);
+  TMG_COUNT(1);
   prolong_correct_kernel<<<grid, 256, 0, s>>>(nxc, nyc, uc, u);
   return cudaGetLastError();
 }
@@ -259,7 +265,9 @@ cudaError_t launch_dense_solve(const GridArgs& g, const double* Ainv, double* u,
                                double* work, cudaStream_t s) {
   const int n = (g.nx - 1) * (g.ny - 1);
   if (n <= 0) return cudaSuccess;
+  TMG_COUNT(1);
   dense_rhs_kernel<<<(n + 255) / 256, 256, 0, s>>>(g, u, f, work);
+  TMG_COUNT(1);
   dense_apply_kernel<<<(n * 32 + 255) / 256, 256, 0, s>>>(g, Ainv, work, u);
   return cudaGetLastError();
 }

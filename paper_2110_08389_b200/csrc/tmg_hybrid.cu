@@ -289,6 +289,7 @@ cudaError_t launch_hdefect_norm(const GridArgs& g, const FieldView& U, const Fie
                                 int g1) {
   if (g.nx < 2 || g.ny < 2) return cudaSuccess;
   dim3 grid((g.ny - 1 + TILE - 1) / TILE, (g.nx - 1 + TILE - 1) / TILE);
+  TMG_COUNT(1);
   hdefect_norm_kernel<<<grid, 256, 0, s>>>(g, U, F, dmax, GroupSel{scheme, g0, g1});
   return cudaGetLastError();
 }
@@ -318,6 +319,7 @@ int point_blocks(long n) {
 cudaError_t launch_gather_points(const FieldView& V, const long long* enc, long n, double* out,
                                  cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
+  TMG_COUNT(1);
   gather_points_kernel<<<point_blocks(n), 256, 0, s>>>(V, enc, n, out);
   return cudaGetLastError();
 }
@@ -325,6 +327,7 @@ cudaError_t launch_gather_points(const FieldView& V, const long long* enc, long 
 cudaError_t launch_scatter_points(const FieldView& V, const long long* enc, long n,
                                   const double* in, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
+  TMG_COUNT(1);
   scatter_points_kernel<<<point_blocks(n), 256, 0, s>>>(V, enc, n, in);
   return cudaGetLastError();
 }
@@ -334,6 +337,7 @@ cudaError_t launch_hdefect_restrict(const GridArgs& g, int full, const FieldView
   const int nxc = g.nx / 2, nyc = g.ny / 2;
   if (nxc < 2 || nyc < 2) return cudaSuccess;
   dim3 grid((nyc - 1 + CT - 1) / CT, (nxc - 1 + CT - 1) / CT);
+  TMG_COUNT(1);
   hdefect_restrict_kernel<<<grid, 256, 0, s>>>(g, full, U, F, FC);
   return cudaGetLastError();
 }
@@ -342,6 +346,7 @@ cudaError_t launch_hprolong_correct(int nx, int ny, const FieldView& C, const Fi
                                     cudaStream_t s) {
   if (nx < 2 || ny < 2) return cudaSuccess;
   dim3 grid((ny - 1 + TILE - 1) / TILE, (nx - 1 + TILE - 1) / TILE);
+  TMG_COUNT(1);
   hprolong_correct_kernel<<<grid, 256, 0, s>>>(nx, ny, C, U);
   return cudaGetLastError();
 }
@@ -351,6 +356,7 @@ cudaError_t launch_to_hybrid(const FieldView& V, const double* nat, cudaStream_t
   cudaError_t e = cudaMemcpyAsync(V.n, nat, n * sizeof(double), cudaMemcpyDeviceToDevice, s);
   if (e != cudaSuccess || V.mode == LM_NATURAL) return e;
   dim3 grid((V.ny + 1 + TILE - 1) / TILE, (V.nx + 1 + TILE - 1) / TILE);
+  TMG_COUNT(1);
   to_t_kernel<<<grid, 256, 0, s>>>(V.nx, V.ny, nat, V.t);
   return cudaGetLastError();
 }
@@ -362,6 +368,7 @@ cudaError_t launch_from_hybrid(const FieldView& V, double* nat, cudaStream_t s) 
     return cudaMemcpyAsync(nat, V.n, n * sizeof(double), cudaMemcpyDeviceToDevice, s);
   }
   dim3 grid((V.ny + 1 + TILE - 1) / TILE, (V.nx + 1 + TILE - 1) / TILE);
+  TMG_COUNT(1);
   from_hybrid_kernel<<<grid, 256, 0, s>>>(V, nat);
   return cudaGetLastError();
 }
@@ -370,7 +377,9 @@ cudaError_t launch_hdense_solve(const GridArgs& g, const double* Ainv, const Fie
                                 const FieldView& F, double* work, cudaStream_t s) {
   const int n = (g.nx - 1) * (g.ny - 1);
   if (n <= 0) return cudaSuccess;
+  TMG_COUNT(1);
   hdense_rhs_kernel<<<(n + 255) / 256, 256, 0, s>>>(g, U, F, work);
+  TMG_COUNT(1);
   hdense_apply_kernel<<<(n * 32 + 255) / 256, 256, 0, s>>>(g, Ainv, work, U);
   return cudaGetLastError();
 }

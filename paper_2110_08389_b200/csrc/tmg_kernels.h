@@ -8,6 +8,11 @@
 
 namespace tmg {
 
+// Host-side count of the kernels this library has put on streams (graph
+// replays add their kernel nodes); tmg_kernel_launches() reads it.
+long long& launch_counter();
+#define TMG_COUNT(n) (::tmg::launch_counter() += (n))
+
 struct SweepArgs {
   const LegD* legs;
   const BlockD* blocks;

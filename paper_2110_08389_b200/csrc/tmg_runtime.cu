@@ -391,9 +391,11 @@ int session_cycles(tmg_hier* h, int kind, int full, int nu1, int nu2, int reps, 
     cudaStream_t cs;
     TMG_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     cudaGraph_t g;
+    const long long counted = launch_counter();  // captured launches do not run
     TMG_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
     int st3 = vcycle_launches(h, kind, full, nu1, nu2, cs);
     cudaError_t e = cudaStreamEndCapture(cs, &g);
+    launch_counter() = counted;
     cudaStreamDestroy(cs);
     if (st3) return st3;
     if (e != cudaSuccess) return cuda_fail(e, "graph capture");
@@ -413,7 +415,10 @@ int session_cycles(tmg_hier* h, int kind, int full, int nu1, int nu2, int reps, 
     it = h->graphs.emplace(key, std::make_pair(ge, kernels)).first;
   }
   h->last_kernels = it->second.second;
-  for (int r = 0; r < reps; r++) TMG_CUDA_TRY(cudaGraphLaunch(it->second.first, s));
+  for (int r = 0; r < reps; r++) {
+    TMG_CUDA_TRY(cudaGraphLaunch(it->second.first, s));
+    TMG_COUNT(it->second.second);
+  }
   return TMG_OK;
 }
 
@@ -451,9 +456,17 @@ int guarded(Fn&& fn) {
 
 }  // namespace
 
+namespace tmg {
+long long& launch_counter() {
+  static long long n = 0;
+  return n;
+}
+}  // namespace tmg
+
 extern "C" {
 
 const char* tmg_last_error(void) { return g_last_error.c_str(); }
+long long tmg_kernel_launches(void) { return launch_counter(); }
 int tmg_version(void) { return 110; }
 
 int tmg_level_create(int nx, int ny, const double* W, const double* E, const double* S,

@@ -598,6 +598,7 @@ cudaError_t set_attrs() {
 template <int Q>
 cudaError_t launch_class(const LaunchClass& lc, const SweepArgs& a, cudaStream_t stream) {
   if (lc.cs == 1) {
+    TMG_COUNT(1);
     block_sweep_kernel<false, Q><<<lc.nbins, kThreads, smem_bytes<Q>(), stream>>>(
         a, lc.chunks, lc.bins, lc.hubs, 1);
     return cudaGetLastError();
@@ -614,6 +615,7 @@ cudaError_t launch_class(const LaunchClass& lc, const SweepArgs& a, cudaStream_t
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  TMG_COUNT(1);
   return cudaLaunchKernelEx(&cfg, block_sweep_kernel<true, Q>, a, (const ChunkD*)lc.chunks,
                             (const BinD*)lc.bins, (const HubD*)lc.hubs, lc.cs);
 }
@@ -656,6 +658,7 @@ cudaError_t launch_colour(const Plan& P, int red, const SweepArgs& a, cudaStream
   if (P.point_scheme) {
     const int i0 = P.g0 > 0 ? P.g0 : 1, i1 = P.g0 > 0 ? P.g1 : P.geo.nx;
     dim3 grid((P.geo.ny - 1 + 255) / 256, i1 - i0);
+    TMG_COUNT(1);
     point_sweep_kernel<<<grid, 256, 0, stream>>>(a, P.geo.nx, P.geo.ny, red, i0);
     return cudaGetLastError();
   }
