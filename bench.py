@@ -208,7 +208,6 @@ def run_ours(args):
     for lv in h.levels:
         _lib.check(L.tmg_level_check(native_level(lv.stencil), sh))
     kernels_per_cycle = L.tmg_hier_graph_kernels(state.native)
-    launches0 = L.tmg_kernel_launches()
 
     clk = ClockSampler(local)
     clk.start()
@@ -219,6 +218,7 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = L.tmg_kernel_launches()
     e0.record(stream)
     cycles(args.steps)
     e1.record(stream)
@@ -435,7 +435,8 @@ def main():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
     p.add_argument("--config", default="config3", choices=("config1", "config2", "config3"))
-    p.add_argument("--n", type=int, default=None, help="override grid intervals")
+    p.add_argument("--intervals", "--n", dest="n", type=int, default=None,
+                   help="override grid intervals (use --intervals under torchrun)")
     p.add_argument("--nu", type=int, default=2, help="config3: V(nu,nu)")
     p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     p.add_argument("--replicas", action="store_true",
