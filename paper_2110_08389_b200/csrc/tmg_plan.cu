@@ -3,6 +3,7 @@
 // smoothers.py:42-118): a block here is a hub plus up to four legs described
 // by straight segments, O(#blocks) to build instead of O(#points) tuples.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "tmg_plan.h"
@@ -306,9 +307,13 @@ long dump_members(const Geometry& g, int* oi, int* oj, int* oblk, int* oflags, l
   return p;
 }
 
+// plan statistics without a device (tmg_plan_stats): uploads are skipped
+static thread_local bool g_dry_run = false;
+static thread_local long long g_stats[8];
+
 template <class T>
 static T* upload(const std::vector<T>& v, size_t& bytes, std::string& err) {
-  if (v.empty()) return nullptr;
+  if (v.empty() || g_dry_run) return nullptr;
   T* d = nullptr;
   cudaError_t e = cudaMalloc(&d, v.size() * sizeof(T));
   if (e != cudaSuccess) { err = cudaGetErrorString(e); return nullptr; }
@@ -430,11 +435,242 @@ std::string pack_plan(Geometry&& geo, int q, int mode, Plan& P) {
     need[b] = cs;
   }
 
+  // Chunk descriptors, hub rows and bin records of one launch class whose
+  // blocks have been assigned to bins (B.bin, L.tbase, B.hub_thread).
+  auto emit = [&](int red, int cs, const std::vector<int>& blks, std::vector<BinD>& bins,
+                  const std::vector<int>& maxch, const std::vector<int>& xcta,
+                  bool warp_aligned) -> std::string {
+    LaunchClass lc;
+    lc.q = q;
+    lc.cs = cs;
+    lc.red = red;
+    lc.nbins = (int)bins.size();
+    ChunkD idle;
+    std::memset(&idle, 0, sizeof(idle));
+    idle.hub = -1;
+    idle.own = -1;
+    idle.link = (uint16_t)(DNONE | (DNONE << 3));
+    std::vector<ChunkD> ch((size_t)lc.nbins * cs * T, idle);
+    std::vector<std::vector<HubD>> bhubs(lc.nbins);
+    for (int b : blks) {
+      BlockD& B = g.blocks[b];
+      const size_t base = (size_t)B.bin * cs * T;
+      // hub: owner = first adjacent chunk thread, or the reserved thread
+      int owner = -1, own_idx = -1;
+      if (B.hi >= 0) {
+        HubD H;
+        std::memset(&H, 0, sizeof(H));
+        H.tbuf = owns_t(mode, g.nx, g.ny, B.hi, B.hj) ? 1 : 0;
+        H.off = (int32_t)(H.tbuf ? fv.off_t(B.hi, B.hj) : fv.off_n(B.hi, B.hj));
+        H.i = (int16_t)B.hi;
+        H.j = (int16_t)B.hj;
+        H.mask = B.hub_mask;
+        for (int l = 0; l < B.nleg; l++) {
+          const LegD& L = g.legs[B.leg0 + l];
+          if (L.flags & 2) {
+            H.adj_t[H.nadj] = (int16_t)(L.tbase + L.nchunk - 1);
+            H.adj_d[H.nadj++] = (uint8_t)dir_opp(L.hub_dir_last);
+          }
+          if (L.flags & 1) {
+            H.adj_t[H.nadj] = (int16_t)L.tbase;
+            H.adj_d[H.nadj++] = (uint8_t)dir_opp(L.hub_dir_first);
+          }
+        }
+        owner = B.nleg ? (H.nadj ? H.adj_t[0] : g.legs[B.leg0].tbase) : B.hub_thread;
+        B.hub_thread = owner;
+        own_idx = (int)bhubs[B.bin].size();
+        bhubs[B.bin].push_back(H);
+        ch[base + owner].own = (int16_t)own_idx;
+        ch[base + owner].hub = (int16_t)owner;
+      }
+      for (int l = 0; l < B.nleg; l++) {
+        const LegD& L = g.legs[B.leg0 + l];
+        const auto& cks = lchunks[B.leg0 + l];
+        for (int c = 0; c < (int)cks.size(); c++) {
+          const int s = cks[c].first, e = cks[c].second;
+          int i, j;
+          leg_point_host(L, s, i, j);
+          // direction of the run containing the chunk
+          const int d = (e > s) ? step_direction(L, s + 1)
+                                : (s > 0 ? step_direction(L, s) : L.seg_dir[0]);
+          const int axis = (d == DS || d == DN) ? 1 : 0;
+          const int neg = (d == DW || d == DS) ? 1 : 0;
+          int dfirst = DNONE, dlast = DNONE, link = 0;
+          if (s == 0) {
+            if (L.flags & 1) { dfirst = L.hub_dir_first; link |= kLinkLeftHub; }
+          } else {
+            dfirst = dir_opp(step_direction(L, s));
+            link |= kLinkLeftPrev;
+          }
+          if (e == L.npts - 1) {
+            if (L.flags & 2) { dlast = L.hub_dir_last; link |= kLinkRightHub; }
+          } else {
+            dlast = step_direction(L, e + 1);
+            link |= kLinkRightNext;
+          }
+          ChunkD& C = ch[base + L.tbase + c];
+          const bool tb = owns_t(mode, g.nx, g.ny, i, j);
+          C.off = (int32_t)(tb ? fv.off_t(i, j) : fv.off_n(i, j));
+          C.a0 = (int16_t)(axis ? j : i);
+          C.cidx = (int16_t)(axis ? i : j);
+          C.n = (uint8_t)(e - s + 1);
+          C.geo = (uint8_t)(axis | (neg << 1) | (tb ? 4 : 0));
+          C.link = (uint16_t)(dfirst | (dlast << 3) | link);
+          C.hub = (int16_t)owner;
+        }
+      }
+    }
+    std::vector<HubD> hubs;
+    for (int k = 0; k < lc.nbins; k++) {
+      int st = 0;
+      while ((1 << st) < maxch[k]) st++;
+      bins[k].pcr_steps = st;
+      bins[k].warp_local = xcta[k] ? 2 : (warp_aligned && maxch[k] <= 32 ? 1 : 0);
+      bins[k].hub0 = (int)hubs.size();
+      bins[k].nhub = (int)bhubs[k].size();
+      hubs.insert(hubs.end(), bhubs[k].begin(), bhubs[k].end());
+    }
+    if (g_dry_run) {  // [red|black] x (CTAs, threads with a chunk, points, hubs)
+      long long* st = g_stats + (red ? 0 : 4);
+      st[0] += (long long)lc.nbins * cs;
+      for (const ChunkD& c : ch) {
+        st[1] += c.n > 0;
+        st[2] += c.n;
+      }
+      for (const auto& bh : bhubs) st[3] += (long long)bh.size();
+    }
+    lc.chunks = upload(ch, P.device_bytes, err);
+    lc.bins = upload(bins, P.device_bytes, err);
+    lc.hubs = upload(hubs, P.device_bytes, err);
+    if (!err.empty()) return err;
+    P.classes.push_back(lc);
+    return std::string();
+  };
+
+  const char* pk = std::getenv("TMG_PACK");
+  const bool dense = !(pk && std::strcmp(pk, "sequential") == 0);
+  std::vector<char> taken(g.blocks.size(), 0);
+  auto block_size = [&](int b) {
+    const BlockD& B = g.blocks[b];
+    int n = B.nleg == 0 ? 1 : 0;
+    for (int l = 0; l < B.nleg; l++) n += g.legs[B.leg0 + l].nchunk;
+    return n;
+  };
   for (int red = 1; red >= 0; red--) {
+    // Dense packing (first-fit decreasing over blocks sorted by size): legs
+    // of <= 32 chunks go into any warp with room (never straddling a warp,
+    // so bins of short legs keep the shuffle-only reduction); longer legs
+    // start at the first free slot of a warp and run on through empty warps
+    // of one CTA (of the cluster if longer than a CTA); the legs of a block
+    // may sit in different CTAs of a cluster (hubs through DSMEM).  Clusters
+    // are opened by the blocks that need them and their spare warps filled
+    // with the colour's smaller blocks; the rest go to single-CTA bins packed
+    // the same way.  The sequential placement below (TMG_PACK=sequential)
+    // leaves 25-35 % of the thread slots idle on tweed and wireframe grids.
+    int csmax = 1;
+    std::vector<int> order;
+    for (size_t b = 0; b < g.blocks.size(); b++) {
+      if (g.blocks[b].red != red) continue;
+      order.push_back((int)b);
+      csmax = std::max(csmax, need[b]);
+    }
+    if (dense) {
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int x, int y) { return block_size(x) > block_size(y); });
+      constexpr int NW = T / 32;
+      for (int pass_cs : {csmax, 1}) {
+        std::vector<BinD> bins;
+        std::vector<int> maxch, xcta, blks;
+        std::vector<std::vector<int>> fill;  // per bin: per warp (cta * NW + w) slots used
+        size_t first_open = 0;
+        for (int b : order) {
+          if (taken[b]) continue;
+          if (pass_cs == 1 && need[b] > 1) continue;
+          BlockD& B = g.blocks[b];
+          std::vector<int> items;
+          for (int l = 0; l < B.nleg; l++) items.push_back(l);
+          std::stable_sort(items.begin(), items.end(), [&](int x, int y) {
+            return g.legs[B.leg0 + x].nchunk > g.legs[B.leg0 + y].nchunk;
+          });
+          auto try_bin = [&](size_t k, bool commit) {
+            std::vector<int> f = fill[k];
+            std::vector<int> tb(B.nleg, -1);
+            int hub_t = -1;
+            auto small = [&](int nch) {  // first warp with room
+              for (int w = 0; w < pass_cs * NW; w++)
+                if (f[w] + nch <= 32) {
+                  const int t = w * 32 + f[w];
+                  f[w] += nch;
+                  return t;
+                }
+              return -1;
+            };
+            if (B.nleg == 0 && (hub_t = small(1)) < 0) return false;
+            for (int l : items) {
+              const int nch = g.legs[B.leg0 + l].nchunk;
+              if (nch <= 32) {
+                if ((tb[l] = small(nch)) < 0) return false;
+                continue;
+              }
+              // a long leg starts at the first free slot of a warp and runs
+              // on through empty warps of the same CTA (of the whole cluster
+              // for a leg longer than a CTA: cross-CTA reduction)
+              const bool cross = nch > T;
+              for (int c = 0; c < (cross ? 1 : pass_cs) && tb[l] < 0; c++)
+                for (int w = c * NW; w < (cross ? pass_cs : c + 1) * NW && tb[l] < 0; w++) {
+                  if (f[w] >= 32) continue;
+                  const int start = w * 32 + f[w], end = start + nch - 1, we = end / 32;
+                  if (we >= (cross ? pass_cs : c + 1) * NW) break;
+                  bool empty = true;
+                  for (int x = w + 1; x <= we; x++) empty &= f[x] == 0;
+                  if (!empty) continue;
+                  tb[l] = start;
+                  for (int x = w; x < we; x++) f[x] = 32;
+                  f[we] = end % 32 + 1;
+                }
+              if (tb[l] < 0) return false;
+            }
+            if (!commit) return true;
+            fill[k] = f;
+            B.bin = (int)k;
+            for (int l = 0; l < B.nleg; l++) {
+              LegD& L = g.legs[B.leg0 + l];
+              L.tbase = tb[l];
+              maxch[k] = std::max(maxch[k], L.nchunk);
+              if (tb[l] / T != (tb[l] + L.nchunk - 1) / T) xcta[k] = 1;
+            }
+            B.hub_thread = B.nleg ? -1 : hub_t;
+            return true;
+          };
+          bool ok = false;
+          for (size_t k = first_open; k < bins.size() && !ok; k++)
+            if (try_bin(k, false)) ok = try_bin(k, true);
+          if (!ok && (pass_cs == 1 || need[b] > 1)) {
+            bins.push_back(BinD{0, 0, 0, 0});
+            maxch.push_back(1);
+            xcta.push_back(0);
+            fill.push_back(std::vector<int>(pass_cs * NW, 0));
+            ok = try_bin(bins.size() - 1, true);
+            if (!ok) return "internal: block does not fit an empty bin";
+          }
+          if (!ok) continue;
+          taken[b] = 1;
+          blks.push_back(b);
+          while (first_open < bins.size() &&
+                 *std::min_element(fill[first_open].begin(), fill[first_open].end()) >= 32)
+            first_open++;
+        }
+        if (!blks.empty()) {
+          err = emit(red, pass_cs, blks, bins, maxch, xcta, true);
+          if (!err.empty()) return err;
+        }
+        if (pass_cs == 1) break;
+      }
+    }
     for (int cs = 1; cs <= 8; cs *= 2) {
       std::vector<int> blks;
       for (size_t b = 0; b < g.blocks.size(); b++)
-        if (g.blocks[b].red == red && need[b] == cs) blks.push_back((int)b);
+        if (g.blocks[b].red == red && need[b] == cs && !taken[b]) blks.push_back((int)b);
       if (blks.empty()) continue;
       std::vector<BinD> bins;
       std::vector<int> maxch, xcta;
@@ -477,101 +713,8 @@ std::string pack_plan(Geometry&& geo, int q, int mode, Plan& P) {
           break;
         }
       }
-      LaunchClass lc;
-      lc.q = q;
-      lc.cs = cs;
-      lc.red = red;
-      lc.nbins = (int)bins.size();
-      ChunkD idle;
-      std::memset(&idle, 0, sizeof(idle));
-      idle.hub = -1;
-      idle.own = -1;
-      idle.link = (uint16_t)(DNONE | (DNONE << 3));
-      std::vector<ChunkD> ch((size_t)lc.nbins * cs * T, idle);
-      std::vector<std::vector<HubD>> bhubs(lc.nbins);
-      for (int b : blks) {
-        BlockD& B = g.blocks[b];
-        const size_t base = (size_t)B.bin * cs * T;
-        // hub: owner = first adjacent chunk thread, or the reserved thread
-        int owner = -1, own_idx = -1;
-        if (B.hi >= 0) {
-          HubD H;
-          std::memset(&H, 0, sizeof(H));
-          H.tbuf = owns_t(mode, g.nx, g.ny, B.hi, B.hj) ? 1 : 0;
-          H.off = (int32_t)(H.tbuf ? fv.off_t(B.hi, B.hj) : fv.off_n(B.hi, B.hj));
-          H.i = (int16_t)B.hi;
-          H.j = (int16_t)B.hj;
-          H.mask = B.hub_mask;
-          for (int l = 0; l < B.nleg; l++) {
-            const LegD& L = g.legs[B.leg0 + l];
-            if (L.flags & 2) {
-              H.adj_t[H.nadj] = (int16_t)(L.tbase + L.nchunk - 1);
-              H.adj_d[H.nadj++] = (uint8_t)dir_opp(L.hub_dir_last);
-            }
-            if (L.flags & 1) {
-              H.adj_t[H.nadj] = (int16_t)L.tbase;
-              H.adj_d[H.nadj++] = (uint8_t)dir_opp(L.hub_dir_first);
-            }
-          }
-          owner = B.nleg ? (H.nadj ? H.adj_t[0] : g.legs[B.leg0].tbase) : B.hub_thread;
-          B.hub_thread = owner;
-          own_idx = (int)bhubs[B.bin].size();
-          bhubs[B.bin].push_back(H);
-          ch[base + owner].own = (int16_t)own_idx;
-          ch[base + owner].hub = (int16_t)owner;
-        }
-        for (int l = 0; l < B.nleg; l++) {
-          const LegD& L = g.legs[B.leg0 + l];
-          const auto& cks = lchunks[B.leg0 + l];
-          for (int c = 0; c < (int)cks.size(); c++) {
-            const int s = cks[c].first, e = cks[c].second;
-            int i, j;
-            leg_point_host(L, s, i, j);
-            // direction of the run containing the chunk
-            const int d = (e > s) ? step_direction(L, s + 1)
-                                  : (s > 0 ? step_direction(L, s) : L.seg_dir[0]);
-            const int axis = (d == DS || d == DN) ? 1 : 0;
-            const int neg = (d == DW || d == DS) ? 1 : 0;
-            int dfirst = DNONE, dlast = DNONE, link = 0;
-            if (s == 0) {
-              if (L.flags & 1) { dfirst = L.hub_dir_first; link |= kLinkLeftHub; }
-            } else {
-              dfirst = dir_opp(step_direction(L, s));
-              link |= kLinkLeftPrev;
-            }
-            if (e == L.npts - 1) {
-              if (L.flags & 2) { dlast = L.hub_dir_last; link |= kLinkRightHub; }
-            } else {
-              dlast = step_direction(L, e + 1);
-              link |= kLinkRightNext;
-            }
-            ChunkD& C = ch[base + L.tbase + c];
-            const bool tb = owns_t(mode, g.nx, g.ny, i, j);
-            C.off = (int32_t)(tb ? fv.off_t(i, j) : fv.off_n(i, j));
-            C.a0 = (int16_t)(axis ? j : i);
-            C.cidx = (int16_t)(axis ? i : j);
-            C.n = (uint8_t)(e - s + 1);
-            C.geo = (uint8_t)(axis | (neg << 1) | (tb ? 4 : 0));
-            C.link = (uint16_t)(dfirst | (dlast << 3) | link);
-            C.hub = (int16_t)owner;
-          }
-        }
-      }
-      std::vector<HubD> hubs;
-      for (int k = 0; k < lc.nbins; k++) {
-        int st = 0;
-        while ((1 << st) < maxch[k]) st++;
-        bins[k].pcr_steps = st;
-        bins[k].warp_local = xcta[k] ? 2 : (maxch[k] <= 32 ? 1 : 0);
-        bins[k].hub0 = (int)hubs.size();
-        bins[k].nhub = (int)bhubs[k].size();
-        hubs.insert(hubs.end(), bhubs[k].begin(), bhubs[k].end());
-      }
-      lc.chunks = upload(ch, P.device_bytes, err);
-      lc.bins = upload(bins, P.device_bytes, err);
-      lc.hubs = upload(hubs, P.device_bytes, err);
+      err = emit(red, cs, blks, bins, maxch, xcta, true);
       if (!err.empty()) return err;
-      P.classes.push_back(lc);
     }
   }
   P.d_legs = upload(g.legs, P.device_bytes, err);
@@ -699,3 +842,20 @@ void free_plan(Plan& p) {
 }
 
 }  // namespace tmg
+
+// Packing statistics of a full plan, computed on the host without a device:
+// out[0..3] red (CTAs, threads holding a chunk, points in chunks, hubs),
+// out[4..7] the same for black.  Returns 0, or -1 with the error in stderr.
+extern "C" int tmg_plan_stats(int scheme, int nx, int ny, int q, int mode, long long* out) {
+  tmg::g_dry_run = true;
+  for (auto& v : tmg::g_stats) v = 0;
+  tmg::Plan P;
+  std::string err = tmg::build_plan(scheme, nx, ny, q, mode, P);
+  tmg::g_dry_run = false;
+  for (int k = 0; k < 8; k++) out[k] = tmg::g_stats[k];
+  if (!err.empty()) {
+    std::fprintf(stderr, "tmg_plan_stats: %s\n", err.c_str());
+    return -1;
+  }
+  return 0;
+}
