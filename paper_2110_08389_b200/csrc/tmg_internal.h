@@ -83,7 +83,7 @@ struct HubD {
   int16_t adj_t[4];   // virtual thread whose reduced unknown is that point
   uint8_t adj_d[4];   // direction from the hub to that point
   uint8_t tbuf;       // 1: the hub point lives in the transposed buffer
-  uint8_t pad;
+  uint8_t pad;        // bit 0: a CTA-local copy that does not store the hub
 };
 static_assert(sizeof(HubD) == 24, "HubD layout");
 

@@ -455,8 +455,12 @@ std::string pack_plan(Geometry&& geo, int q, int mode, Plan& P) {
     for (int b : blks) {
       BlockD& B = g.blocks[b];
       const size_t base = (size_t)B.bin * cs * T;
-      // hub: owner = first adjacent chunk thread, or the reserved thread
-      int owner = -1, own_idx = -1;
+      // hub: one copy per CTA holding chunks of the block (so that the hub
+      // value is read locally in the finalize step); owner = the first
+      // adjacent chunk thread in that CTA, else its first chunk thread, or
+      // the reserved thread of a point block.  Copies after the first only
+      // solve, they do not store the hub point (HubD.pad bit 0).
+      int owner_cta[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
       if (B.hi >= 0) {
         HubD H;
         std::memset(&H, 0, sizeof(H));
@@ -476,12 +480,29 @@ std::string pack_plan(Geometry&& geo, int q, int mode, Plan& P) {
             H.adj_d[H.nadj++] = (uint8_t)dir_opp(L.hub_dir_first);
           }
         }
-        owner = B.nleg ? (H.nadj ? H.adj_t[0] : g.legs[B.leg0].tbase) : B.hub_thread;
-        B.hub_thread = owner;
-        own_idx = (int)bhubs[B.bin].size();
-        bhubs[B.bin].push_back(H);
-        ch[base + owner].own = (int16_t)own_idx;
-        ch[base + owner].hub = (int16_t)owner;
+        if (B.nleg == 0) {
+          owner_cta[B.hub_thread / T] = B.hub_thread;
+        } else {
+          for (int q = 0; q < H.nadj; q++)
+            if (owner_cta[H.adj_t[q] / T] < 0) owner_cta[H.adj_t[q] / T] = H.adj_t[q];
+          for (int l = 0; l < B.nleg; l++) {
+            const LegD& L = g.legs[B.leg0 + l];
+            for (int c = 0; c < L.nchunk; c++)
+              if (owner_cta[(L.tbase + c) / T] < 0) owner_cta[(L.tbase + c) / T] = L.tbase + c;
+          }
+        }
+        bool primary = true;
+        for (int r = 0; r < cs; r++) {
+          const int ow = owner_cta[r];
+          if (ow < 0) continue;
+          HubD Hc = H;
+          Hc.pad = primary ? 0 : 1;
+          if (primary) B.hub_thread = ow;
+          primary = false;
+          ch[base + ow].own = (int16_t)bhubs[B.bin].size();
+          ch[base + ow].hub = (int16_t)ow;
+          bhubs[B.bin].push_back(Hc);
+        }
       }
       for (int l = 0; l < B.nleg; l++) {
         const LegD& L = g.legs[B.leg0 + l];
@@ -516,7 +537,7 @@ std::string pack_plan(Geometry&& geo, int q, int mode, Plan& P) {
           C.n = (uint8_t)(e - s + 1);
           C.geo = (uint8_t)(axis | (neg << 1) | (tb ? 4 : 0));
           C.link = (uint16_t)(dfirst | (dlast << 3) | link);
-          C.hub = (int16_t)owner;
+          C.hub = (int16_t)owner_cta[(L.tbase + c) / T];
         }
       }
     }

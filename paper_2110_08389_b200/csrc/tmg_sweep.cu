@@ -60,6 +60,15 @@ __device__ __forceinline__ double* remote(double* p, int rank) {
   }
 }
 
+// split cluster barrier: arrive once this CTA's DSMEM reads are done, wait
+// before exiting (no CTA may exit while a peer can still read its memory)
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 template <bool CLUSTER>
 __device__ __forceinline__ void bin_sync() {
   if constexpr (CLUSTER) {
@@ -502,14 +511,14 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
     bad |= bad_pivot(den);
     const double xh = num / den;
     XH[tid] = xh;
-    (hb.tbuf ? a.ut : u)[o] = xh;
+    if (!(hb.pad & 1)) (hb.tbuf ? a.ut : u)[o] = xh;  // one copy stores the hub
   }
-  bin_sync<CLUSTER>();
+  __syncthreads();  // every CTA holding chunks of a block solves its own hub copy
 
   TMG_T(4);
   // final values of the chunk
   if (c.n > 0) {
-    const double xh = c.hub >= 0 ? remote<CLUSTER>(XH, c.hub / T)[c.hub % T] : 0.0;
+    const double xh = c.hub >= 0 ? XH[c.hub % T] : 0.0;
     const double X = fma(-Qh, xh, P);
     double Lv = 0.0;
     if (c.link & kLinkLeftPrev) {
@@ -531,11 +540,8 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
   }
   if (bad) atomicOr(a.err, 1);
   TMG_T(5);
-  if constexpr (CLUSTER) {
-    cg::this_cluster().sync();  // remote XH / sD reads done before any CTA exits
-  } else {
-    __syncwarp();
-  }
+  if constexpr (CLUSTER) cluster_arrive();  // this CTA's DSMEM reads are done
+  __syncwarp();
 
   // ---------------- phase C: coalesced scatter (warp-local) ----------------
 #pragma unroll
@@ -547,6 +553,7 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
     const int tb_s = __shfl_sync(FULL, c.tb, src);
     if (ksub < n_s) (tb_s ? a.ut : u)[off_s + ksub * str_s] = R[sw<Q>(wbase + src, ksub)];
   }
+  if constexpr (CLUSTER) cluster_wait();
   TMG_T(6);
 }
 
