@@ -232,6 +232,34 @@ def run_ours(args):
         torch.cuda.synchronize()
     clocks = clk.stop()
 
+    # BASELINE metric part 2: the solve (tmg_solve from u = 0, one norm and
+    # pivot-flag read-back per cycle).  Configs 1-2: time to a 1e-10
+    # relative residual.  Config 3: 20 cycles at tol = 1e-300 and the
+    # convergence factor over them (BASELINE config 3; its relative defect
+    # floors near 3e-9 in fp64, so 1e-10 is not reachable)
+    solve = None
+    if not args.no_solve:
+        c3 = args.config == "config3"
+        tol_s, max_s = (1e-300, 20) if c3 else (1e-10, 50)
+        cfg_s = mgcycle.CycleConfig(smoother=w.smoother, nu1=w.nu1, nu2=w.nu2, tol=tol_s,
+                                    max_cycles=max_s)
+        fd_s = fd.clone()
+        mgcycle.solve(h, cfg_s, fd_s)  # warm (plans, graph)
+        barrier()
+        torch.cuda.synchronize()
+        z0, z1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        z0.record(stream)
+        _, rep = mgcycle.solve(h, cfg_s, fd_s)
+        z1.record(stream)
+        torch.cuda.synchronize()
+        r = rep.per_cycle_ratios
+        solve = {"tol": tol_s, "max_cycles": max_s, "cycles": rep.cycles,
+                 "converged": rep.converged,
+                 "ms": max_over_ranks(z0.elapsed_time(z1)),
+                 "final_rel_defect": rep.final_rel_defect,
+                 "mean_convergence_factor": float(np.exp(np.mean(np.log(r)))) if r else None}
+        _lib.check(L.tmg_session_load(state.native, kind, up, fp, sh))
+
     upc = _updates_per_cycle(h, w.nu1 + w.nu2)
     ms_per_step = t_ms / args.steps
     value = world * upc * args.steps / (t_ms * 1e-3)
@@ -300,6 +328,7 @@ def run_ours(args):
                      "kernel": "block_sweep_kernel (one finest-level sweep, both colours)",
                      "alg_bytes": alg_bytes, "ms": sweep_ms, "peak_kind": peak_kind},
         "sweep_updates_per_s": n_int / (sweep_ms * 1e-3),
+        "solve": solve,
         "e2e": e2e,
         "clocks": clocks,
         "gpu_launches": launches,
@@ -439,6 +468,7 @@ def main():
                    help="override grid intervals (use --intervals under torchrun)")
     p.add_argument("--nu", type=int, default=2, help="config3: V(nu,nu)")
     p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    p.add_argument("--no-solve", action="store_true", help="skip the time-to-1e-10 solve")
     p.add_argument("--replicas", action="store_true",
                    help="N > 1: independent replicas instead of one sharded problem")
     args = p.parse_args()

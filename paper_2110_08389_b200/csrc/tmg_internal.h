@@ -97,7 +97,7 @@ struct BinD {
 // One kernel launch worth of bins sharing (q, cluster size).
 struct LaunchClass {
   int q;
-  int cs;          // CTAs per cluster (1, 2, 4, 8)
+  int cs;          // CTAs per cluster (1, 2, 4, 8, 16)
   int nbins;
   int red;
   ChunkD* chunks;  // nbins * cs * kThreads
@@ -106,6 +106,7 @@ struct LaunchClass {
 };
 
 constexpr int kThreads = 256;   // threads per CTA of the block-solver kernel
+constexpr int kMaxCluster = 16;  // CTAs per cluster (16 is a non-portable size on B200)
 constexpr int kQmax = 16;       // max points per thread chunk
 
 }  // namespace tmg

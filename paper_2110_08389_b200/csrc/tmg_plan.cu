@@ -405,9 +405,9 @@ std::string pack_plan(Geometry&& geo, int q, int mode, Plan& P) {
   for (size_t l = 0; l < g.legs.size(); l++) {
     lchunks[l] = leg_chunks(g.legs[l], q, mode, g.nx, g.ny);
     g.legs[l].nchunk = (int)lchunks[l].size();
-    if (g.legs[l].nchunk > 8 * T)
+    if (g.legs[l].nchunk > kMaxCluster * T)
       return "leg of " + std::to_string(g.legs[l].npts) +
-             " points exceeds the cluster solver capacity (" + std::to_string(8 * T * q) + ")";
+             " points exceeds the cluster solver capacity (" + std::to_string(kMaxCluster * T * q) + ")";
   }
   // Virtual-thread placement of a leg of nch chunks at position v (rank * T
   // + offset): a leg of <= 32 chunks stays inside one warp (shuffle-only
@@ -431,7 +431,7 @@ std::string pack_plan(Geometry&& geo, int q, int mode, Plan& P) {
     const int ctas = (v + T - 1) / T;
     int cs = 1;
     while (cs < ctas) cs *= 2;
-    if (cs > 8) return "block needs more than 8 CTAs";
+    if (cs > kMaxCluster) return "block needs more than " + std::to_string(kMaxCluster) + " CTAs";
     need[b] = cs;
   }
 
@@ -460,7 +460,8 @@ std::string pack_plan(Geometry&& geo, int q, int mode, Plan& P) {
       // adjacent chunk thread in that CTA, else its first chunk thread, or
       // the reserved thread of a point block.  Copies after the first only
       // solve, they do not store the hub point (HubD.pad bit 0).
-      int owner_cta[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+      int owner_cta[kMaxCluster];
+      std::fill(owner_cta, owner_cta + kMaxCluster, -1);
       if (B.hi >= 0) {
         HubD H;
         std::memset(&H, 0, sizeof(H));
@@ -688,7 +689,7 @@ std::string pack_plan(Geometry&& geo, int q, int mode, Plan& P) {
         if (pass_cs == 1) break;
       }
     }
-    for (int cs = 1; cs <= 8; cs *= 2) {
+    for (int cs = 1; cs <= kMaxCluster; cs *= 2) {
       std::vector<int> blks;
       for (size_t b = 0; b < g.blocks.size(); b++)
         if (g.blocks[b].red == red && need[b] == cs && !taken[b]) blks.push_back((int)b);

@@ -599,6 +599,9 @@ cudaError_t set_attrs() {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(block_sweep_kernel<true, Q>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<Q>());
+  if (e == cudaSuccess)  // clusters of 16 CTAs (rings of wireframe grids >= 8193^2)
+    e = cudaFuncSetAttribute(block_sweep_kernel<true, Q>,
+                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return e;
 }
 

@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 from paper_2110_08389_b200 import configs, grid, mgcycle, smoothers, stencil, transfer
+from paper_2110_08389_b200.rng import Lcg64
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
@@ -131,6 +132,32 @@ def test_config3_sweep_and_cycles_match_oracle(cuda, orc, config3):
         mgcycle.v_cycle(h, cfg, ug, fd)
         orc.v_cycle(H, uo, f, nthreads=nthreads)
         assert _rel(ug.cpu().numpy(), uo) <= 1e-10
+
+
+def test_wireframe_8193_sweep_and_cycle(cuda, orc):
+    """Wireframe at 8193^2 (centre-clustered): the outer rings hold ~2050
+    chunks and run on 16-CTA clusters.  One sweep on the API layout and one
+    V(2,2) cycle (hybrid layout) against the oracle."""
+    n = 8192
+    x = grid.make_coords("centre", n, 1.0, 3.0)
+    h = grid.build_hierarchy(x, x)
+    st = h.finest.stencil
+    f = np.zeros((n + 1, n + 1))
+    f[1:-1, 1:-1] = Lcg64(4).fill((n - 1, n - 1)) * 2.0 - 1.0
+    nthreads = orc.max_threads()
+    fd = cuda.from_numpy(f).cuda()
+    u = cuda.zeros_like(fd)
+    smoothers.sweep("wireframe", st, smoothers.PlanBundle(n, n), u, fd)
+    uo = np.zeros_like(f)
+    orc.sweep("wireframe", (st.W, st.E, st.S, st.N), uo, f, nthreads)
+    assert _rel(u.cpu().numpy(), uo) <= 1e-10
+    del u
+    H = orc.Hierarchy(x.values, x.values)
+    ug = cuda.zeros_like(fd)
+    uo = np.zeros_like(f)
+    mgcycle.v_cycle(h, mgcycle.CycleConfig(smoother="wireframe"), ug, fd)
+    orc.v_cycle(H, uo, f, smoother="wireframe", nthreads=nthreads)
+    assert _rel(ug.cpu().numpy(), uo) <= 1e-10
 
 
 @pytest.mark.parametrize("nu", [1, 2])
