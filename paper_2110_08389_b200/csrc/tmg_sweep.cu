@@ -29,6 +29,18 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef TMG_FULL_PATH
+#define TMG_FULL_PATH 0  // 1: separate predicate-free elimination for full chunks
+#endif
+
+#ifndef TMG_ASYNC_GATHER
+#define TMG_ASYNC_GATHER 0  // 1: phase A stages f, u-, u+ with cp.async (no register round trip)
+#endif
+
+#ifndef TMG_SKIP
+#define TMG_SKIP 0  // profiling only: 1 skip elimination, 2 skip PCR, 4 skip hubs, 8 skip finalize, 16 skip chunk-end pass
+#endif
+
 #ifndef TMG_MINB
 #define TMG_MINB 2  // resident CTAs per SM the register budget is sized for
 #endif
@@ -58,6 +70,15 @@ __device__ __forceinline__ double* remote(double* p, int rank) {
   } else {
     return p;
   }
+}
+
+// 8-byte asynchronous global -> shared copy (LDGSTS) and its completion wait
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
 // split cluster barrier: arrive once this CTA's DSMEM reads are done, wait
@@ -171,6 +192,73 @@ __device__ __forceinline__ int sw(int t, int k) {
   return t * Q + (k ^ (t & (Q - 1)));
 }
 
+// Phase B of one chunk: Thomas down sweep over the chunk interior (the
+// coupling to the previous chunk's end kept as the column lam) and an affine
+// back pass leaving x_k = alpha_k + beta_k * Xleft + gamma_k * X in (R, lam,
+// ivr).  NI > 0: compile-time interior count (full chunks, no predicates);
+// NI == 0: runtime count nI.  (ad, bd, gd) = the form of the last interior
+// point, (au, bu, gu) = that of the first.
+template <int Q, int NI>
+__device__ __forceinline__ void chunk_eliminate(int tid, int nI, double* R, const double* PA,
+                                                const double* PC, double csum, double a_first,
+                                                double (&lam)[Q], double (&ivr)[Q], bool& bad,
+                                                double& ad, double& bd, double& gd, double& au,
+                                                double& bu, double& gu) {
+  const int n = NI > 0 ? NI : nI;
+  double bp = 0.0, rho = 0.0, lm = 0.0, ivp = 0.0, cprev = 0.0;
+#pragma unroll
+  for (int k = 0; k < Q; k++) {
+    if (k < n) {
+      const int sl = sw<Q>(tid, k);
+      const double pav = PA[sl], pcv = PC[sl], rp = R[sl];
+      const double bb = -(pav + pcv + csum);
+      if (k == 0) {
+        bp = bb;
+        rho = rp;
+        lm = -a_first;
+      } else {
+        const double w = pav * ivp;
+        bp = fma(-w, cprev, bb);
+        rho = fma(-w, rho, rp);
+        lm = -w * lm;
+      }
+      bad |= bad_pivot(bp);
+      ivp = drcp(bp);
+      R[sl] = rho;
+      lam[k] = lm;
+      ivr[k] = ivp;
+      cprev = pcv;
+    }
+  }
+  // affine back substitution; cprev = c_{e-1}
+  double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+  for (int k = Q - 1; k >= 0; k--) {
+    if (k < n) {
+      const int sl = sw<Q>(tid, k);
+      if (k == n - 1) {
+        al = R[sl] * ivr[k];
+        be = lam[k] * ivr[k];
+        ga = -cprev * ivr[k];
+        ad = al;
+        bd = be;
+        gd = ga;
+      } else {
+        const double cp = PC[sl];
+        al = fma(-cp, al, R[sl]) * ivr[k];
+        be = fma(-cp, be, lam[k]) * ivr[k];
+        ga = -cp * ga * ivr[k];
+      }
+      R[sl] = al;
+      lam[k] = be;
+      ivr[k] = ga;
+    }
+  }
+  au = al;
+  bu = be;
+  gu = ga;
+}
+
 template <bool CLUSTER, int Q>
 __global__ void __launch_bounds__(kThreads, TMG_MINB)
 block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* __restrict__ bins,
@@ -201,6 +289,21 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
   c.unpack(mine, C, ld, a.ldt);
   const FieldView U{u, a.ut, a.nx, a.ny, a.mode};
   const FieldView F{const_cast<double*>(f), const_cast<double*>(a.ft), a.nx, a.ny, a.mode};
+  const BinD bd_ = bins[bin];
+  // frozen part of this thread's hub row (its out-of-block neighbours are
+  // never written during this colour stage), loaded now so that the loads
+  // overlap the gather instead of sitting on the hub step's critical path
+  double hub_num = 0.0, hub_den = 1.0;
+  if (!(TMG_SKIP & 4) && c.own >= 0) {
+    const HubD hb = hubs[bd_.hub0 + c.own];
+    const int hi = hb.i, hj = hb.j;
+    hub_num = (hb.tbuf ? a.ft : f)[hb.off];
+    if (!(hb.mask & 1u)) hub_num -= __ldg(a.W + hi) * *U.at(hi - 1, hj);
+    if (!(hb.mask & 2u)) hub_num -= __ldg(a.E + hi) * *U.at(hi + 1, hj);
+    if (!(hb.mask & 4u)) hub_num -= __ldg(a.S + hj) * *U.at(hi, hj - 1);
+    if (!(hb.mask & 8u)) hub_num -= __ldg(a.N + hj) * *U.at(hi, hj + 1);
+    hub_den = -(__ldg(a.W + hi) + __ldg(a.E + hi) + __ldg(a.S + hj) + __ldg(a.N + hj));
+  }
   const double xlv = c.n > 0 ? __ldg(c.xl + c.cidx) : 0.0;
   const double xhv = c.n > 0 ? __ldg(c.xh + c.cidx) : 0.0;
   const int lane = tid & 31, wbase = tid & ~31;
@@ -220,16 +323,97 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
   // elimination is done) and are only read inside the owning warp.  The
   // coefficient arrays W, E, S, N are one allocation, so a chunk's along
   // couplings are addressed by element offsets from W.
+  // A warp whose chunks are one straight run of full chunks (the bulk of
+  // every long leg) addresses its points arithmetically: lane l of pass m
+  // takes point p = 32 m + l of the run, which is point l % Q of chunk
+  // m * 32/Q + l / Q -- the same slots as the record-driven path below.
+  const int pa_rel = (int)(c.pa - a.W) + c.a0, pc_rel = (int)(c.pc - a.W) + c.a0;
+  bool uniform;
   {
+    const int off_p = __shfl_up_sync(FULL, c.off, 1), str_p = __shfl_up_sync(FULL, c.stride, 1);
+    const int tb_p = __shfl_up_sync(FULL, c.tb, 1), cid_p = __shfl_up_sync(FULL, c.cidx, 1);
+    const bool contig = c.n == Q && (lane == 0 || (str_p == c.stride && off_p + Q * str_p == c.off &&
+                                                   tb_p == c.tb && cid_p == c.cidx));
+    uniform = __all_sync(FULL, contig);
+  }
+  if (uniform) {
+    const int off0 = __shfl_sync(FULL, c.off, 0), str0 = __shfl_sync(FULL, c.stride, 0);
+    const int cs0 = __shfl_sync(FULL, c.cs, 0), tb0 = __shfl_sync(FULL, c.tb, 0);
+    const int pa0 = __shfl_sync(FULL, pa_rel, 0), pc0 = __shfl_sync(FULL, pc_rel, 0);
+    const int da0 = __shfl_sync(FULL, c.da, 0);
+    const double xl0 = __shfl_sync(FULL, xlv, 0), xh0 = __shfl_sync(FULL, xhv, 0);
+    const double* ub = tb0 ? a.ut : u;
+    const double* fb = tb0 ? a.ft : f;
+#pragma unroll
+    for (int m0 = 0; m0 < Q; m0 += BATCH) {
+      double vf[BATCH], vl[BATCH], vh[BATCH], va[BATCH], vc[BATCH];
+#pragma unroll
+      for (int b = 0; b < BATCH; b++) {
+        const int p = 32 * (m0 + b) + lane;
+        const int o = off0 + p * str0;
+        vf[b] = fb[o];
+        vl[b] = ub[o - cs0];
+        vh[b] = ub[o + cs0];
+        va[b] = __ldg(a.W + pa0 + p * da0);
+        vc[b] = __ldg(a.W + pc0 + p * da0);
+      }
+#pragma unroll
+      for (int b = 0; b < BATCH; b++) {
+        const int sl = sw<Q>(wbase + (m0 + b) * PER + csub, ksub);
+        R[sl] = fma(-xh0, vh[b], fma(-xl0, vl[b], vf[b]));
+        PA[sl] = va[b];
+        PC[sl] = vc[b];
+      }
+    }
+  } else {
     int4* recI = reinterpret_cast<int4*>(sA);
     int4* recJ = recI + T;
     double2* recX = reinterpret_cast<double2*>(recJ + T);
     recI[tid] = make_int4(c.off, c.stride, c.cs, c.n | (c.tb << 8));
-    recJ[tid] = make_int4((int)(c.pa - a.W) + c.a0, (int)(c.pc - a.W) + c.a0, c.da, 0);
+    recJ[tid] = make_int4(pa_rel, pc_rel, c.da, 0);
     recX[tid] = make_double2(xlv, xhv);
-  }
   __syncwarp();
-  {
+  if constexpr (TMG_ASYNC_GATHER) {
+    // pass 1: every lane issues the asynchronous copies of all its points
+    // (f, u at the two cross neighbours into the R, PA, PC slots) back to
+    // back, so the whole bin's loads are in flight at once; pass 2 turns
+    // them into the frozen right-hand side and stages the along couplings
+    const int4* recI = reinterpret_cast<const int4*>(sA);
+    const int4* recJ = recI + T;
+    const double2* recX = reinterpret_cast<const double2*>(recJ + T);
+#pragma unroll
+    for (int m = 0; m < Q; m++) {
+      const int src = wbase + m * PER + csub;
+      const int4 ri = recI[src];
+      if (ksub < (ri.w & 255)) {
+        const bool tb_s = (ri.w >> 8) & 1;
+        const double* ub = tb_s ? a.ut : u;
+        const double* fb = tb_s ? a.ft : f;
+        const int o = ri.x + ksub * ri.y;
+        const int sl = sw<Q>(src, ksub);
+        cp_async8(R + sl, fb + o);
+        cp_async8(PA + sl, ub + o - ri.z);
+        cp_async8(PC + sl, ub + o + ri.z);
+      }
+    }
+    cp_async_wait_all();
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < Q; m++) {
+      const int src = wbase + m * PER + csub;
+      const int nn = recI[src].w & 255;
+      if (ksub < nn) {
+        const int4 rj = recJ[src];
+        const double2 rx = recX[src];
+        const int sl = sw<Q>(src, ksub);
+        const int ai = ksub * rj.z;
+        const double va = __ldg(a.W + rj.x + ai), vc = __ldg(a.W + rj.y + ai);
+        R[sl] = fma(-rx.y, PC[sl], fma(-rx.x, PA[sl], R[sl]));
+        PA[sl] = va;
+        PC[sl] = vc;
+      }
+    }
+  } else {
     const int4* recI = reinterpret_cast<const int4*>(sA);
     const int4* recJ = recI + T;
     const double2* recX = reinterpret_cast<const double2*>(recJ + T);
@@ -267,8 +451,9 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
       }
     }
   }
+  }  // record-driven gather
   __syncwarp();
-  if (c.n > 0) {  // chunk ends: neighbours outside the block from the link directions
+  if (!(TMG_SKIP & 16) && c.n > 0) {  // chunk ends: neighbours outside the block from the link directions
     const int alo = c.da > 0 ? (c.axis ? DS : DW) : (c.axis ? DN : DE);  // toward k-1
     const int ahi = alo ^ 1;                                             // toward k+1
 #pragma unroll
@@ -277,9 +462,21 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
       if (e && c.n == 1) break;
       const int dp = k == 0 ? c.dfirst : alo;
       const int dn = k == c.n - 1 ? c.dlast : ahi;
-      const unsigned skip = (dp < 4 ? 1u << dp : 0u) | (dn < 4 ? 1u << dn : 0u);
       int i, j;
       c.ij(k, i, j);
+      // The gather's value is already exact for an end whose in-block
+      // neighbours are the two along neighbours and whose cross neighbours
+      // live in the chunk's buffer (most chunk ends); recompute the others
+      // (leg tips, corners, points next to an ownership boundary).
+      bool fix = dp != alo || dn != ahi;
+      if (!fix && a.mode != LM_NATURAL) {
+        const int i1 = c.axis ? i - 1 : i, j1 = c.axis ? j : j - 1;
+        const int i2 = c.axis ? i + 1 : i, j2 = c.axis ? j : j + 1;
+        fix = owns_t(a.mode, a.nx, a.ny, i1, j1) != (c.tb != 0) && i1 > 0 && j1 > 0 ||
+              owns_t(a.mode, a.nx, a.ny, i2, j2) != (c.tb != 0) && i2 < a.nx && j2 < a.ny;
+      }
+      if (!fix) continue;
+      const unsigned skip = (dp < 4 ? 1u << dp : 0u) | (dn < 4 ? 1u << dn : 0u);
       double r = *F.at(i, j);
       if (!(skip & 1u)) r -= __ldg(a.W + i) * *U.at(i - 1, j);
       if (!(skip & 2u)) r -= __ldg(a.E + i) * *U.at(i + 1, j);
@@ -307,63 +504,17 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
     c.ij(0, i0, j0);
     a_first = C.dir(c.dfirst, i0, j0);
   }
-  if (nI > 0) {
-    double bp = 0.0, rho = 0.0, lm = 0.0, ivp = 0.0, cprev = 0.0;
-#pragma unroll
-    for (int k = 0; k < Q; k++) {
-      if (k < nI) {
-        const int sl = sw<Q>(tid, k);
-        const double pav = PA[sl], pcv = PC[sl], rp = R[sl];
-        const double bb = -(pav + pcv + csum);
-        if (k == 0) {
-          bp = bb;
-          rho = rp;
-          lm = -a_first;
-        } else {
-          const double w = pav * ivp;
-          bp = fma(-w, cprev, bb);
-          rho = fma(-w, rho, rp);
-          lm = -w * lm;
-        }
-        bad |= bad_pivot(bp);
-        ivp = drcp(bp);
-        R[sl] = rho;
-        lam[k] = lm;
-        ivr[k] = ivp;
-        cprev = pcv;
-      }
-    }
-    // affine back substitution; cprev = c_{e-1}
-    double al = 0.0, be = 0.0, ga = 0.0;
-#pragma unroll
-    for (int k = Q - 1; k >= 0; k--) {
-      if (k < nI) {
-        const int sl = sw<Q>(tid, k);
-        if (k == nI - 1) {
-          al = R[sl] * ivr[k];
-          be = lam[k] * ivr[k];
-          ga = -cprev * ivr[k];
-          ad = al;
-          bd = be;
-          gd = ga;
-        } else {
-          const double cp = PC[sl];
-          al = fma(-cp, al, R[sl]) * ivr[k];
-          be = fma(-cp, be, lam[k]) * ivr[k];
-          ga = -cp * ga * ivr[k];
-        }
-        R[sl] = al;
-        lam[k] = be;
-        ivr[k] = ga;
-      }
-    }
-    au = al;
-    bu = be;
-    gu = ga;
+  if constexpr (Q > 1 && !(TMG_SKIP & 1)) {
+    // full chunks (all but the last chunk of a leg) take the predicate-free path
+    if (TMG_FULL_PATH && nI == Q - 1)
+      chunk_eliminate<Q, Q - 1>(tid, nI, R, PA, PC, csum, a_first, lam, ivr, bad, ad, bd, gd, au,
+                                bu, gu);
+    else if (nI > 0)
+      chunk_eliminate<Q, 0>(tid, nI, R, PA, PC, csum, a_first, lam, ivr, bad, ad, bd, gd, au, bu,
+                            gu);
   }
   TMG_T(2);
   // publish the first-point affine form for the left neighbour chunk
-  const BinD bd_ = bins[bin];
   const bool xcta = bd_.warp_local == 2;  // some leg crosses a CTA boundary
   __syncthreads();  // every warp is done with its gather records (same region)
   sA[tid] = au;
@@ -408,7 +559,7 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
   // parallel cyclic reduction of the per-leg reduced systems.  Legs never
   // straddle CTAs; when no leg of the bin straddles a warp either, the
   // exchange runs on warp shuffles without block barriers.
-  const int steps = bd_.pcr_steps;
+  const int steps = (TMG_SKIP & 2) ? 0 : bd_.pcr_steps;
   if (bd_.warp_local == 1) {
     for (int st = 0; st < steps; st++) {
       const int d = 1 << st;
@@ -492,16 +643,11 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
   bin_sync<CLUSTER>();
 
   // hub rows
-  if (c.own >= 0) {
+  if (!(TMG_SKIP & 4) && c.own >= 0) {
     const HubD hb = hubs[bd_.hub0 + c.own];
     const int hi = hb.i, hj = hb.j;
     const int o = hb.off;
-    double num = (hb.tbuf ? a.ft : f)[o];
-    if (!(hb.mask & 1u)) num -= __ldg(a.W + hi) * *U.at(hi - 1, hj);
-    if (!(hb.mask & 2u)) num -= __ldg(a.E + hi) * *U.at(hi + 1, hj);
-    if (!(hb.mask & 4u)) num -= __ldg(a.S + hj) * *U.at(hi, hj - 1);
-    if (!(hb.mask & 8u)) num -= __ldg(a.N + hj) * *U.at(hi, hj + 1);
-    double den = -(__ldg(a.W + hi) + __ldg(a.E + hi) + __ldg(a.S + hj) + __ldg(a.N + hj));
+    double num = hub_num, den = hub_den;
     for (int q = 0; q < hb.nadj; q++) {
       const int ta = hb.adj_t[q];
       const double cf = C.dir(hb.adj_d[q], hi, hj);
@@ -517,7 +663,7 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
 
   TMG_T(4);
   // final values of the chunk
-  if (c.n > 0) {
+  if (!(TMG_SKIP & 8) && c.n > 0) {
     const double xh = c.hub >= 0 ? XH[c.hub % T] : 0.0;
     const double X = fma(-Qh, xh, P);
     double Lv = 0.0;
@@ -541,17 +687,31 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
   if (bad) atomicOr(a.err, 1);
   TMG_T(5);
   if constexpr (CLUSTER) cluster_arrive();  // this CTA's DSMEM reads are done
+  // scatter records (sA/sB are free after the reduced solve; the finalize of
+  // other warps reads only sD, sH and XH)
+  reinterpret_cast<int2*>(sA)[tid] = make_int2(c.off, c.stride);
+  reinterpret_cast<int*>(sC)[tid] = c.n | (c.tb << 8);
   __syncwarp();
 
   // ---------------- phase C: coalesced scatter (warp-local) ----------------
+  if (uniform) {
+    const int off0 = __shfl_sync(FULL, c.off, 0), str0 = __shfl_sync(FULL, c.stride, 0);
+    double* ub = __shfl_sync(FULL, c.tb, 0) ? a.ut : u;
 #pragma unroll
-  for (int m = 0; m < Q; m++) {
-    const int src = m * PER + csub;
-    const int n_s = __shfl_sync(FULL, c.n, src);
-    const int off_s = __shfl_sync(FULL, c.off, src);
-    const int str_s = __shfl_sync(FULL, c.stride, src);
-    const int tb_s = __shfl_sync(FULL, c.tb, src);
-    if (ksub < n_s) (tb_s ? a.ut : u)[off_s + ksub * str_s] = R[sw<Q>(wbase + src, ksub)];
+    for (int m = 0; m < Q; m++)
+      ub[off0 + (32 * m + lane) * str0] = R[sw<Q>(wbase + m * PER + csub, ksub)];
+  } else {
+    const int2* recO = reinterpret_cast<const int2*>(sA);
+    const int* recN = reinterpret_cast<const int*>(sC);
+#pragma unroll
+    for (int m = 0; m < Q; m++) {
+      const int src = wbase + m * PER + csub;
+      const int nt = recN[src];
+      if (ksub < (nt & 255)) {
+        const int2 ro = recO[src];
+        ((nt >> 8) ? a.ut : u)[ro.x + ksub * ro.y] = R[sw<Q>(src, ksub)];
+      }
+    }
   }
   if constexpr (CLUSTER) cluster_wait();
   TMG_T(6);
