@@ -22,6 +22,7 @@
 //  C  coalesced scatter of the new values.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <vector>
 
@@ -39,6 +40,10 @@ namespace cg = cooperative_groups;
 
 #ifndef TMG_SKIP
 #define TMG_SKIP 0  // profiling only: 1 skip elimination, 2 skip PCR, 4 skip hubs, 8 skip finalize, 16 skip chunk-end pass
+#endif
+
+#ifndef TMG_PREFETCH
+#define TMG_PREFETCH 0  // 1: prefetch the next bin's field rows into L2
 #endif
 
 #ifndef TMG_MINB
@@ -79,6 +84,10 @@ __device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) 
 }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void prefetch_l2(const double* p) {
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
 
 // split cluster barrier: arrive once this CTA's DSMEM reads are done, wait
@@ -259,11 +268,14 @@ __device__ __forceinline__ void chunk_eliminate(int tid, int nI, double* R, cons
   gu = ga;
 }
 
+// One bin (a cluster's worth of chunks) of a colour stage.  next_bin >= 0:
+// the bin this CTA handles next, whose field rows are prefetched into L2
+// once this bin's gather is done, so that its gather finds them there.
 template <bool CLUSTER, int Q>
-__global__ void __launch_bounds__(kThreads, TMG_MINB)
-block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* __restrict__ bins,
-                   const HubD* __restrict__ hubs, int cs_size) {
-  extern __shared__ double smem[];
+__device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __restrict__ chunks,
+                                          const BinD* __restrict__ bins,
+                                          const HubD* __restrict__ hubs, int cs_size, int bin,
+                                          int rank, int next_bin, double* smem) {
   constexpr int T = kThreads;
   double* R = smem;
   double* PA = R + T * Q;
@@ -276,15 +288,16 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
   double* XH = sH + T;
 
   const int tid = threadIdx.x;
-  const int rank = CLUSTER ? (int)cg::this_cluster().block_rank() : 0;
-  const int bin = blockIdx.x / cs_size;
   const int ld = a.ld;
   const Coefs C{a.W, a.E, a.S, a.N};
   double* __restrict__ u = a.u;
   const double* __restrict__ f = a.f;
 
   TMG_T(0);
-  const ChunkD mine = chunks[(size_t)blockIdx.x * T + tid];
+  const ChunkD mine = chunks[((size_t)bin * cs_size + rank) * T + tid];
+  ChunkD nxt;
+  nxt.n = 0;
+  if (TMG_PREFETCH && next_bin >= 0) nxt = chunks[((size_t)next_bin * cs_size + rank) * T + tid];
   Chunk c;
   c.unpack(mine, C, ld, a.ldt);
   const FieldView U{u, a.ut, a.nx, a.ny, a.mode};
@@ -486,6 +499,20 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
     }
   }
   __syncwarp();
+  if (TMG_PREFETCH && nxt.n > 0) {  // next bin's rows of f and u into L2
+    const int tb = (nxt.geo >> 2) & 1, axis = nxt.geo & 1, neg = (nxt.geo >> 1) & 1;
+    const int si = tb ? 1 : ld, sj = tb ? a.ldt : 1;
+    const int st = (axis ? sj : si) * (neg ? -1 : 1), cs = axis ? si : sj;
+    const double* ub = tb ? a.ut : u;
+    const double* fb = tb ? a.ft : f;
+    const int o0 = nxt.off, o1 = nxt.off + (nxt.n - 1) * st;
+    prefetch_l2(fb + o0);
+    prefetch_l2(fb + o1);
+    prefetch_l2(ub + o0 - cs);
+    prefetch_l2(ub + o1 - cs);
+    prefetch_l2(ub + o0 + cs);
+    prefetch_l2(ub + o1 + cs);
+  }
   TMG_T(1);
 
   // ---------------- phase B: chunk elimination -------------------------------
@@ -713,8 +740,21 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
       }
     }
   }
-  if constexpr (CLUSTER) cluster_wait();
   TMG_T(6);
+}
+
+// One CTA (cluster) per bin.  The bin `ahead` places later (ahead = the
+// number of co-resident clusters) starts about when this one retires, so its
+// field rows are prefetched into L2 while this bin computes.
+template <bool CLUSTER, int Q>
+__global__ void __launch_bounds__(kThreads, TMG_MINB)
+block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* __restrict__ bins,
+                   const HubD* __restrict__ hubs, int cs_size, int nbins, int ahead) {
+  extern __shared__ double smem[];
+  const int rank = CLUSTER ? (int)cg::this_cluster().block_rank() : 0;
+  const int bin = blockIdx.x / cs_size, nb = bin + ahead;
+  sweep_bin<CLUSTER, Q>(a, chunks, bins, hubs, cs_size, bin, rank, nb < nbins ? nb : -1, smem);
+  if constexpr (CLUSTER) cluster_wait();
 }
 
 // Point Gauss-Seidel colour stage for checkerboard (smoothers.py:65-75,
@@ -765,16 +805,62 @@ cudaError_t set_attrs() {
   return e;
 }
 
+// co-resident clusters of the block-solver kernel per (log2 Q, log2 cs),
+// measured once at init (before any stream capture)
+int g_resident[5][5];
+
+int qlog(int v) {
+  int l = 0;
+  while ((1 << l) < v) l++;
+  return l;
+}
+
+template <int Q>
+cudaError_t measure_resident() {
+  int dev = 0, sms = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
+  for (int cs = 1; cs <= kMaxCluster; cs *= 2) {
+    int n = 0;
+    if (cs == 1) {
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, block_sweep_kernel<false, Q>, kThreads,
+                                                        smem_bytes<Q>());
+      n *= sms;
+    } else {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(cs * 1024);
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = smem_bytes<Q>();
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = cs;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      e = cudaOccupancyMaxActiveClusters(&n, block_sweep_kernel<true, Q>, &cfg);
+    }
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    g_resident[qlog(Q)][qlog(cs)] = n > 0 ? n : 1;
+  }
+  return cudaSuccess;
+}
+
 template <int Q>
 cudaError_t launch_class(const LaunchClass& lc, const SweepArgs& a, cudaStream_t stream) {
+  const int grid = lc.nbins, ahead = g_resident[qlog(Q)][qlog(lc.cs)];
   if (lc.cs == 1) {
     TMG_COUNT(1);
-    block_sweep_kernel<false, Q><<<lc.nbins, kThreads, smem_bytes<Q>(), stream>>>(
-        a, lc.chunks, lc.bins, lc.hubs, 1);
+    block_sweep_kernel<false, Q><<<grid, kThreads, smem_bytes<Q>(), stream>>>(
+        a, lc.chunks, lc.bins, lc.hubs, 1, lc.nbins, ahead);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(lc.nbins * lc.cs);
+  cfg.gridDim = dim3(grid * lc.cs);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem_bytes<Q>();
   cfg.stream = stream;
@@ -787,7 +873,7 @@ cudaError_t launch_class(const LaunchClass& lc, const SweepArgs& a, cudaStream_t
   cfg.numAttrs = 1;
   TMG_COUNT(1);
   return cudaLaunchKernelEx(&cfg, block_sweep_kernel<true, Q>, a, (const ChunkD*)lc.chunks,
-                            (const BinD*)lc.bins, (const HubD*)lc.hubs, lc.cs);
+                            (const BinD*)lc.bins, (const HubD*)lc.hubs, lc.cs, lc.nbins, ahead);
 }
 }  // namespace
 
@@ -820,6 +906,11 @@ cudaError_t init_sweep_kernels() {
     if (done == cudaSuccess) done = set_attrs<4>();
     if (done == cudaSuccess) done = set_attrs<2>();
     if (done == cudaSuccess) done = set_attrs<1>();
+    if (done == cudaSuccess) done = measure_resident<16>();
+    if (done == cudaSuccess) done = measure_resident<8>();
+    if (done == cudaSuccess) done = measure_resident<4>();
+    if (done == cudaSuccess) done = measure_resident<2>();
+    if (done == cudaSuccess) done = measure_resident<1>();
   }
   return done;
 }
