@@ -33,13 +33,35 @@ int cuda_fail(cudaError_t e, const char* where) {
     if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
   } while (0)
 
-int default_q() {
+// Points per thread chunk.  TMG_CHUNK forces a value; otherwise a level
+// keeps q = 16 while one colour stage still fills about one wave of
+// resident CTAs (2 per SM), and smaller levels halve q (down to 2) so that
+// their launches spread over the GPU with shorter per-thread chains.
+int default_q(int nx = 0, int ny = 0) {
   const char* s = std::getenv("TMG_CHUNK");
   if (s) {
     int q = std::atoi(s);
     if (q >= 1 && q <= kQmax && !(q & (q - 1))) return q;
   }
-  return kQmax;
+  static int wave = 0;
+  if (!wave) {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
+    wave = sms / 2;  // a quarter of the resident CTAs (2 per SM): measured best
+    const char* w = std::getenv("TMG_QWAVES");  // tuning: waves a q = 16 launch must fill
+    if (w && std::atof(w) > 0) wave = (int)(wave * std::atof(w));
+  }
+  const double per_colour = 0.5 * (double)(nx - 1) * (double)(ny - 1);
+  static int qmin = 0;
+  if (!qmin) {
+    const char* m = std::getenv("TMG_QMIN");  // tuning: smallest adaptive q
+    qmin = m && std::atoi(m) >= 1 ? std::atoi(m) : 2;
+  }
+  int q = kQmax;
+  while (q > qmin && per_colour < (double)wave * kThreads * q) q /= 2;
+  return q;
 }
 
 bool valid_kind(int k) { return k >= TMG_CHECKERBOARD && k <= TMG_TWEED_WIRE_ALT; }
@@ -88,7 +110,7 @@ int get_plan(tmg_level* lv, int scheme, int mode, Plan** out) {
     cudaError_t e = init_sweep_kernels();
     if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");
     Plan* p = new Plan();
-    std::string err = build_plan(scheme, lv->nx, lv->ny, default_q(), mode, *p);
+    std::string err = build_plan(scheme, lv->nx, lv->ny, default_q(lv->nx, lv->ny), mode, *p);
     if (!err.empty()) {
       free_plan(*p);
       delete p;
@@ -109,7 +131,8 @@ int get_part_plan(tmg_level* lv, int scheme, int mode, int g0, int g1, Plan** ou
     cudaError_t e = init_sweep_kernels();
     if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");
     Plan* p = new Plan();
-    std::string err = build_plan_part(scheme, lv->nx, lv->ny, default_q(), mode, g0, g1, *p);
+    std::string err =
+        build_plan_part(scheme, lv->nx, lv->ny, default_q(lv->nx, lv->ny), mode, g0, g1, *p);
     if (!err.empty()) {
       free_plan(*p);
       delete p;
