@@ -9,6 +9,9 @@
 // boundary address point by point.  Arithmetic is the reference's order
 // (stencil.py:82-87, transfer.py:33-38, 51-53) with explicit round-to-nearest
 // intrinsics, so results are bit-identical to the natural-layout kernels.
+#include <cstdlib>
+#include <cstring>
+
 #include "tmg_kernels.h"
 
 namespace tmg {
@@ -284,10 +287,20 @@ __global__ void hdense_apply_kernel(GridArgs g, const double* __restrict__ Ainv,
 
 }  // namespace
 
+bool transfer_v1() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("TMG_TRANSFER");
+    v = (e && std::strcmp(e, "v1") == 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
 cudaError_t launch_hdefect_norm(const GridArgs& g, const FieldView& U, const FieldView& F,
                                 unsigned long long* dmax, cudaStream_t s, int scheme, int g0,
                                 int g1) {
   if (g.nx < 2 || g.ny < 2) return cudaSuccess;
+  if (!transfer_v1()) return launch_norm2(g, U, F, dmax, s, scheme, g0, g1);
   dim3 grid((g.ny - 1 + TILE - 1) / TILE, (g.nx - 1 + TILE - 1) / TILE);
   TMG_COUNT(1);
   hdefect_norm_kernel<<<grid, 256, 0, s>>>(g, U, F, dmax, GroupSel{scheme, g0, g1});
@@ -336,6 +349,7 @@ cudaError_t launch_hdefect_restrict(const GridArgs& g, int full, const FieldView
                                     const FieldView& F, const FieldView& FC, cudaStream_t s) {
   const int nxc = g.nx / 2, nyc = g.ny / 2;
   if (nxc < 2 || nyc < 2) return cudaSuccess;
+  if (!transfer_v1()) return launch_restrict2(g, full, U, F, FC, s);
   dim3 grid((nyc - 1 + CT - 1) / CT, (nxc - 1 + CT - 1) / CT);
   TMG_COUNT(1);
   hdefect_restrict_kernel<<<grid, 256, 0, s>>>(g, full, U, F, FC);
@@ -345,6 +359,7 @@ cudaError_t launch_hdefect_restrict(const GridArgs& g, int full, const FieldView
 cudaError_t launch_hprolong_correct(int nx, int ny, const FieldView& C, const FieldView& U,
                                     cudaStream_t s) {
   if (nx < 2 || ny < 2) return cudaSuccess;
+  if (!transfer_v1()) return launch_prolong2(nx, ny, C, U, s);
   dim3 grid((ny - 1 + TILE - 1) / TILE, (nx - 1 + TILE - 1) / TILE);
   TMG_COUNT(1);
   hprolong_correct_kernel<<<grid, 256, 0, s>>>(nx, ny, C, U);

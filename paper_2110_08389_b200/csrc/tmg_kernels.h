@@ -86,6 +86,14 @@ cudaError_t launch_hdefect_restrict(const GridArgs& g, int full, const FieldView
 // u += P uc on the fine interior; (nx, ny) are the FINE dimensions
 cudaError_t launch_hprolong_correct(int nx, int ny, const FieldView& C, const FieldView& U,
                                     cudaStream_t s);
+// second-generation versions (tmg_transfer.cu), used unless TMG_TRANSFER=v1
+cudaError_t launch_norm2(const GridArgs& g, const FieldView& U, const FieldView& F,
+                         unsigned long long* dmax, cudaStream_t s, int scheme, int g0, int g1);
+cudaError_t launch_restrict2(const GridArgs& g, int full, const FieldView& U, const FieldView& F,
+                             const FieldView& FC, cudaStream_t s);
+cudaError_t launch_prolong2(int nx, int ny, const FieldView& C, const FieldView& U,
+                            cudaStream_t s);
+bool transfer_v1();
 cudaError_t launch_to_hybrid(const FieldView& V, const double* nat, cudaStream_t s);
 cudaError_t launch_from_hybrid(const FieldView& V, double* nat, cudaStream_t s);
 cudaError_t launch_hdense_solve(const GridArgs& g, const double* Ainv, const FieldView& U,
