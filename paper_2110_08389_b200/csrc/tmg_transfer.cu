@@ -52,14 +52,26 @@ template <int E, int LDS>
 __device__ __forceinline__ void load_box(const FieldView& v, int own, int i0, int j0, double* s) {
   constexpr int N = E * E, PER = (N + 255) / 256;
   double val[PER];
+  if (own >= 0 && i0 >= 0 && j0 >= 0 && i0 + E - 1 <= v.nx && j0 + E - 1 <= v.ny) {
+    // uniform box inside the grid: one base pointer, row stride of the buffer
+    const double* base = own == 1 ? v.t + v.off_t(i0, j0) : v.n + v.off_n(i0, j0);
+    const int ldr = own == 1 ? v.nx + 1 : v.ny + 1;
 #pragma unroll
-  for (int k = 0; k < PER; k++) {
-    const int t = threadIdx.x + k * 256;
-    val[k] = 0.0;
-    if (t < N) {
+    for (int k = 0; k < PER; k++) {
+      const int t = threadIdx.x + k * 256;
       const int y = t / E, x = t - y * E;
-      const int i = own == 1 ? i0 + x : i0 + y, j = own == 1 ? j0 + y : j0 + x;
-      if (i >= 0 && j >= 0 && i <= v.nx && j <= v.ny) val[k] = ld_view(v, own, i, j);
+      val[k] = t < N ? __ldg(base + (size_t)y * ldr + x) : 0.0;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < PER; k++) {
+      const int t = threadIdx.x + k * 256;
+      val[k] = 0.0;
+      if (t < N) {
+        const int y = t / E, x = t - y * E;
+        const int i = own == 1 ? i0 + x : i0 + y, j = own == 1 ? j0 + y : j0 + x;
+        if (i >= 0 && j >= 0 && i <= v.nx && j <= v.ny) val[k] = ld_view(v, own, i, j);
+      }
     }
   }
 #pragma unroll
@@ -144,11 +156,22 @@ __global__ void __launch_bounds__(256) restrict2_kernel(GridArgs g, int full, Fi
   const int ui0 = 2 * I0 - 2, uj0 = 2 * J0 - 2;
   const int own = box_owner(U, ui0, uj0, RU, RU);
   double fv[RPER];
+  const bool inner = own >= 0 && ui0 + RD < g.nx && uj0 + RD < g.ny;  // every defect point interior
+  if (inner) {
+    const double* base = own == 1 ? F.t + F.off_t(ui0 + 1, uj0 + 1) : F.n + F.off_n(ui0 + 1, uj0 + 1);
+    const int ldr = own == 1 ? g.nx + 1 : g.ny + 1;
 #pragma unroll
-  for (int k = 0; k < RPER; k++) {
-    const int t = threadIdx.x + k * 256, y = t / RD, x = t - y * RD;
-    const int i = ui0 + 1 + (own == 1 ? x : y), j = uj0 + 1 + (own == 1 ? y : x);
-    fv[k] = (t < RD * RD && i < g.nx && j < g.ny) ? ld_view(F, own, i, j) : 0.0;
+    for (int k = 0; k < RPER; k++) {
+      const int t = threadIdx.x + k * 256, y = t / RD, x = t - y * RD;
+      fv[k] = t < RD * RD ? __ldg(base + (size_t)y * ldr + x) : 0.0;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < RPER; k++) {
+      const int t = threadIdx.x + k * 256, y = t / RD, x = t - y * RD;
+      const int i = ui0 + 1 + (own == 1 ? x : y), j = uj0 + 1 + (own == 1 ? y : x);
+      fv[k] = (t < RD * RD && i < g.nx && j < g.ny) ? ld_view(F, own, i, j) : 0.0;
+    }
   }
   load_box<RU, RLU>(U, own, ui0, uj0, su);
   __syncthreads();
