@@ -105,7 +105,10 @@ struct LaunchClass {
   HubD* hubs;
 };
 
-constexpr int kThreads = 256;   // threads per CTA of the block-solver kernel
+#ifndef TMG_THREADS
+#define TMG_THREADS 256
+#endif
+constexpr int kThreads = TMG_THREADS;  // threads per CTA of the block-solver kernel
 constexpr int kMaxCluster = 16;  // CTAs per cluster (16 is a non-portable size on B200)
 constexpr int kQmax = 16;       // max points per thread chunk
 

@@ -46,8 +46,15 @@ namespace cg = cooperative_groups;
 #define TMG_PREFETCH 0  // 1: prefetch the next bin's field rows into L2
 #endif
 
+#ifndef TMG_BATCH
+#define TMG_BATCH 8  // gather items in flight per lane
+#endif
+#ifndef TMG_MINB8
+#define TMG_MINB8 TMG_MINB  // resident CTAs per SM targeted by the q <= 8 kernels
+#endif
+
 #ifndef TMG_MINB
-#define TMG_MINB 2  // resident CTAs per SM the register budget is sized for
+#define TMG_MINB (TMG_THREADS >= 512 ? 1 : 2)  // resident CTAs per SM the register budget is sized for
 #endif
 
 namespace tmg {
@@ -62,6 +69,9 @@ __device__ __forceinline__ bool bad_pivot(double v) { return v > -1e-300 && v < 
 __device__ __forceinline__ double drcp(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+#ifdef TMG_FAKE_RCP
+  return r;  // timing experiment only: wrong results
+#endif
   double e = fma(-x, r, 1.0);
   r = fma(r, e, r);
   e = fma(-x, r, 1.0);
@@ -321,7 +331,7 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
   const double xhv = c.n > 0 ? __ldg(c.xh + c.cidx) : 0.0;
   const int lane = tid & 31, wbase = tid & ~31;
   constexpr int PER = 32 / Q;  // chunks covered by one warp-wide pass
-  constexpr int BATCH = Q < 8 ? Q : 8;
+  constexpr int BATCH = Q < TMG_BATCH ? Q : TMG_BATCH;
   const int ksub = lane % Q, csub = lane / Q;
   constexpr unsigned FULL = 0xffffffffu;
 
@@ -747,7 +757,7 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
 // number of co-resident clusters) starts about when this one retires, so its
 // field rows are prefetched into L2 while this bin computes.
 template <bool CLUSTER, int Q>
-__global__ void __launch_bounds__(kThreads, TMG_MINB)
+__global__ void __launch_bounds__(kThreads, Q <= 8 ? TMG_MINB8 : TMG_MINB)
 block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* __restrict__ bins,
                    const HubD* __restrict__ hubs, int cs_size, int nbins, int ahead) {
   extern __shared__ double smem[];
