@@ -95,6 +95,25 @@ __device__ __forceinline__ double lu_s(const double* s, int o, int si, int sj, d
   return __dadd_rn(acc, __dmul_rn(Cc, s[o]));
 }
 
+// W, E at i0 .. i0+E-1 and S, N at j0 .. j0+E-1 into shared memory (0
+// outside the grid), so that the stencil reads them with LDS
+template <int E>
+__device__ __forceinline__ void load_coefs(const GridArgs& g, int i0, int j0, double* cW,
+                                           double* cE, double* cS, double* cN) {
+  for (int t = threadIdx.x; t < 4 * E; t += blockDim.x) {
+    const int which = t / E, k = t - which * E;
+    if (which < 2) {
+      const int i = i0 + k;
+      const double v = (i >= 0 && i <= g.nx) ? __ldg((which ? g.E : g.W) + i) : 0.0;
+      (which ? cE : cW)[k] = v;
+    } else {
+      const int j = j0 + k;
+      const double v = (j >= 0 && j <= g.ny) ? __ldg((which == 3 ? g.N : g.S) + j) : 0.0;
+      (which == 3 ? cN : cS)[k] = v;
+    }
+  }
+}
+
 struct GroupSel2 {
   int scheme, g0, g1;
 };
@@ -116,7 +135,9 @@ __global__ void __launch_bounds__(256) norm2_kernel(GridArgs g, FieldView U, Fie
     pj[k] = own == 1 ? j0 + y : j0 + x;
     fv[k] = (pi[k] < g.nx && pj[k] < g.ny) ? ld_view(F, own, pi[k], pj[k]) : 0.0;
   }
+  __shared__ double cW[NT], cE[NT], cS[NT], cN[NT];
   load_box<NE, NLD>(U, own, i0 - 1, j0 - 1, su);
+  load_coefs<NT>(g, i0, j0, cW, cE, cS, cN);
   __syncthreads();
   const int si = own == 1 ? 1 : NLD, sj = own == 1 ? NLD : 1;
   unsigned long long m = 0ull;
@@ -129,8 +150,8 @@ __global__ void __launch_bounds__(256) norm2_kernel(GridArgs g, FieldView U, Fie
       if (grp < gsel.g0 || grp >= gsel.g1) continue;
     }
     const int t = threadIdx.x + k * 256, y = t >> 5, x = t & 31;
-    const double lu = lu_s(su, (y + 1) * NLD + (x + 1), si, sj, __ldg(g.W + i), __ldg(g.E + i),
-                           __ldg(g.S + j), __ldg(g.N + j));
+    const double lu = lu_s(su, (y + 1) * NLD + (x + 1), si, sj, cW[i - i0], cE[i - i0],
+                           cS[j - j0], cN[j - j0]);
     const double d = fabs(__dadd_rn(-lu, fv[k]));
     const unsigned long long bits = (unsigned long long)__double_as_longlong(d);
     m = bits > m ? bits : m;
@@ -140,7 +161,15 @@ __global__ void __launch_bounds__(256) norm2_kernel(GridArgs g, FieldView U, Fie
     const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, m, s);
     m = o2 > m ? o2 : m;
   }
-  if ((threadIdx.x & 31) == 0 && m) atomicMax(dmax, m);
+  // one atomic per CTA (per-warp atomics on one address serialise in L2)
+  __shared__ unsigned long long wm[8];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 1; k < 8; k++) m = wm[k] > m ? wm[k] : m;
+    if (m) atomicMax(dmax, m);
+  }
 }
 
 // ---- fused residual + restriction: 16 x 16 coarse points per CTA ----------
@@ -173,7 +202,9 @@ __global__ void __launch_bounds__(256) restrict2_kernel(GridArgs g, int full, Fi
       fv[k] = (t < RD * RD && i < g.nx && j < g.ny) ? ld_view(F, own, i, j) : 0.0;
     }
   }
+  __shared__ double cW[RD], cE[RD], cS[RD], cN[RD];
   load_box<RU, RLU>(U, own, ui0, uj0, su);
+  load_coefs<RD>(g, ui0 + 1, uj0 + 1, cW, cE, cS, cN);
   __syncthreads();
   const int si = own == 1 ? 1 : RLU, sj = own == 1 ? RLU : 1;
 #pragma unroll
@@ -183,8 +214,8 @@ __global__ void __launch_bounds__(256) restrict2_kernel(GridArgs g, int full, Fi
     const int i = ui0 + 1 + (own == 1 ? x : y), j = uj0 + 1 + (own == 1 ? y : x);
     double dv = 0.0;
     if (i < g.nx && j < g.ny) {
-      const double lu = lu_s(su, (y + 1) * RLU + (x + 1), si, sj, __ldg(g.W + i), __ldg(g.E + i),
-                             __ldg(g.S + j), __ldg(g.N + j));
+      const double lu = lu_s(su, (y + 1) * RLU + (x + 1), si, sj, cW[i - ui0 - 1],
+                             cE[i - ui0 - 1], cS[j - uj0 - 1], cN[j - uj0 - 1]);
       dv = __dadd_rn(-lu, fv[k]);
     }
     sd[y * RLD + x] = dv;
