@@ -82,6 +82,12 @@ int tmg_defect_restrict(tmg_level* fine, int full, const double* u, const double
 /* fused: u += P uc  (mgcycle.py:102) */
 int tmg_prolong_correct(int nxc, int nyc, const double* uc, double* u, void* stream);
 
+/* ---- vector helpers of the two-grid analyser (spectral.py:92-120):
+ *      out_host = sqrt(sum x^2) in a fixed summation order (work: DEVICE
+ *      scratch of >= 1024 doubles; synchronizes); x *= alpha */
+int tmg_vec_norm2(const double* x, long n, double* work, double* out_host, void* stream);
+int tmg_vec_scale(double* x, long n, double alpha, void* stream);
+
 /* ---- DirectSolver (stencil.py:129-155): factor once, then u_int = L^-1 (f -
  *      boundary couplings of u's ring); u's boundary ring is kept */
 int tmg_direct_solve(tmg_level* lv, double* u, const double* f, void* stream);

@@ -335,3 +335,54 @@ def solve(h, f, smoother="tweed", restriction="full", nu1=2, nu2=2, tol=1e-10,
 
 def max_threads():
     return int(lib().orc_max_threads())
+
+
+# --------------------------------------------------------------------------
+# two-grid analyser (spectral.py:60-120), test oracle for the device version
+
+def two_grid_apply(xf, yf, e, smoother="tweed", restriction="full", nu1=1, nu2=0):
+    """M e for the fine grid (xf, yf) and its injected coarse grid."""
+    st = assemble(xf, yf)
+    stc = assemble(xf[::2].copy(), yf[::2].copy())
+    nx, ny = len(xf) - 1, len(yf) - 1
+    u = np.zeros((nx + 1, ny + 1))
+    u[1:-1, 1:-1] = np.asarray(e, dtype=float).reshape(nx - 1, ny - 1)
+    f0 = np.zeros_like(u)
+    for _ in range(nu1):
+        sweep(smoother, st, u, f0)
+    d = defect(st, u, f0)
+    uc = dense_solve(stc, restrict(restriction, d))
+    prolong_add(uc, u)
+    for _ in range(nu2):
+        sweep(smoother, st, u, f0)
+    return u[1:-1, 1:-1].ravel()
+
+
+def spectral_radius(xf, yf, smoother="tweed", restriction="full", nu1=1, nu2=0,
+                    max_iters=3000, rel_tol=1e-4, tail_window=30, seed=1):
+    """Power iteration with the reference's stopping rules; returns
+    (rho, converged, oscillation, iters)."""
+    from paper_2110_08389_b200.rng import Lcg64
+    n = (len(xf) - 2) * (len(yf) - 2)
+    v = Lcg64(seed).fill(n) - 0.5
+    v /= np.linalg.norm(v)
+    est = []
+
+    def stable(a):
+        return a.max() > 0 and (a.max() - a.min()) <= rel_tol * a.max()
+
+    for it in range(1, max_iters + 1):
+        w = two_grid_apply(xf, yf, v, smoother, restriction, nu1, nu2)
+        r = float(np.linalg.norm(w))
+        est.append(r)
+        if r < 1e-300:
+            return 0.0, True, False, it
+        v = w / r
+        if len(est) >= tail_window:
+            tail = np.array(est[-tail_window:])
+            if stable(tail):
+                return float(tail[-1]), True, False, it
+            if stable(np.sqrt(tail[1:] * tail[:-1])):
+                return float(np.exp(np.mean(np.log(tail)))), True, True, it
+    tail = np.array(est[-tail_window:])
+    return float(np.exp(np.mean(np.log(tail)))), False, False, max_iters

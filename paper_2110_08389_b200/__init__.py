@@ -8,11 +8,11 @@ from ._lib import available as _available
 
 HAVE_EXT = _available()
 
-from . import kernels, mgcycle, smoothers  # noqa: E402,F401
+from . import kernels, mgcycle, sharded, smoothers, spectral  # noqa: E402,F401
 
 __all__ = [
     "grid", "layout", "mgcycle", "smoothers", "stencil", "transfer", "tridiag",
-    "kernels", "HAVE_EXT",
+    "kernels", "sharded", "spectral", "HAVE_EXT",
 ]
 
 __version__ = "0.1.0"

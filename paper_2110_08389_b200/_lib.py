@@ -64,6 +64,8 @@ def _declare(L):
         "tmg_session_sweeps": ([vp, ip, ip, vp], ip),
         "tmg_debug_phase_cycles": ([pd], ip),
         "tmg_kernel_launches": ([], ctypes.c_longlong),
+        "tmg_vec_norm2": ([vp, lp, vp, pd, vp], ip),
+        "tmg_vec_scale": ([vp, lp, dp, vp], ip),
         "tmg_group_count": ([ip, ip, ip], ip),
         "tmg_group_sizes": ([ip, ip, ip, vp, lp], lp),
         "tmg_group_offsets": ([ip, ip, ip, ip, ip, vp, lp], lp),

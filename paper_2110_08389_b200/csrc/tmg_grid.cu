@@ -272,4 +272,60 @@ cudaError_t launch_dense_solve(const GridArgs& g, const double* Ainv, double* u,
   return cudaGetLastError();
 }
 
+namespace {
+// deterministic sum of squares: fixed per-block partial sums, then one block
+// adds the partials in index order (the power iteration must be reproducible)
+constexpr int kNormBlocks = 1024;
+
+__global__ void __launch_bounds__(256) sumsq_partial_kernel(const double* __restrict__ x, long n,
+                                                            double* __restrict__ part) {
+  __shared__ double sh[256];
+  double acc = 0.0;
+  for (long k = blockIdx.x * 256L + threadIdx.x; k < n; k += (long)gridDim.x * 256)
+    acc = fma(x[k], x[k], acc);
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void __launch_bounds__(256) sumsq_final_kernel(double* __restrict__ part, int m) {
+  __shared__ double sh[256];
+  double acc = 0.0;
+  for (int k = threadIdx.x; k < m; k += 256) acc += part[k];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[0] = sqrt(sh[0]);
+}
+
+__global__ void scale_kernel(double* __restrict__ x, long n, double alpha) {
+  for (long k = blockIdx.x * (long)blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x)
+    x[k] *= alpha;
+}
+}  // namespace
+
+cudaError_t launch_vec_norm2(const double* x, long n, double* work, cudaStream_t s) {
+  const long nb = (n + 255) / 256;
+  const int blocks = (int)(nb < kNormBlocks ? (nb > 0 ? nb : 1) : kNormBlocks);
+  TMG_COUNT(2);
+  sumsq_partial_kernel<<<blocks, 256, 0, s>>>(x, n, work);
+  sumsq_final_kernel<<<1, 256, 0, s>>>(work, blocks);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_vec_scale(double* x, long n, double alpha, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const long nb = (n + 255) / 256;
+  TMG_COUNT(1);
+  scale_kernel<<<(int)(nb < 148 * 16 ? nb : 148 * 16), 256, 0, s>>>(x, n, alpha);
+  return cudaGetLastError();
+}
+
 }  // namespace tmg

@@ -71,6 +71,11 @@ cudaError_t launch_prolong_correct(int nxc, int nyc, const double* uc, double* u
 cudaError_t launch_dense_solve(const GridArgs& g, const double* Ainv, double* u,
                                const double* f, double* work, cudaStream_t s);
 
+// sqrt(sum x^2) into work[0] (work: >= 1024 doubles), deterministic order
+cudaError_t launch_vec_norm2(const double* x, long n, double* work, cudaStream_t s);
+// x *= alpha
+cudaError_t launch_vec_scale(double* x, long n, double alpha, cudaStream_t s);
+
 // ---- hybrid-layout (tmg_layout.h) versions used inside the V-cycle ----
 // scheme / [g0, g1): only points of those sharding groups count (g0 = 0: all)
 cudaError_t launch_hdefect_norm(const GridArgs& g, const FieldView& U, const FieldView& F,
