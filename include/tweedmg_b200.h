@@ -87,6 +87,10 @@ int tmg_prolong_correct(int nxc, int nyc, const double* uc, double* u, void* str
  *      scratch of >= 1024 doubles; synchronizes); x *= alpha */
 int tmg_vec_norm2(const double* x, long n, double* work, double* out_host, void* stream);
 int tmg_vec_scale(double* x, long n, double alpha, void* stream);
+/* the next n uniform [0, 1) values of the Lcg64 stream (rng.py:20-40) whose
+ * current state is `state`, into DEVICE out (per-element jump-ahead; the
+ * caller advances its host state by n) */
+int tmg_lcg_fill(unsigned long long state, long n, double* out, void* stream);
 
 /* ---- DirectSolver (stencil.py:129-155): factor once, then u_int = L^-1 (f -
  *      boundary couplings of u's ring); u's boundary ring is kept */

@@ -66,6 +66,7 @@ def _declare(L):
         "tmg_kernel_launches": ([], ctypes.c_longlong),
         "tmg_vec_norm2": ([vp, lp, vp, pd, vp], ip),
         "tmg_vec_scale": ([vp, lp, dp, vp], ip),
+        "tmg_lcg_fill": ([ctypes.c_ulonglong, lp, vp, vp], ip),
         "tmg_group_count": ([ip, ip, ip], ip),
         "tmg_group_sizes": ([ip, ip, ip, vp, lp], lp),
         "tmg_group_offsets": ([ip, ip, ip, ip, ip, vp, lp], lp),

@@ -328,4 +328,38 @@ cudaError_t launch_vec_scale(double* x, long n, double alpha, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+namespace {
+// Lcg64 stream on the device (rng.py:20-40): value k (0-based) comes from
+// state_{k+1} = A^{k+1} s + C_{k+1}; thread-wise jump-ahead by squaring of
+// the affine map x -> M x + I (mod 2^64), identical to the scalar recurrence.
+__global__ void lcg_fill_kernel(unsigned long long s0, long n, double* __restrict__ out) {
+  const unsigned long long M = 6364136223846793005ull, I = 1442695040888963407ull;
+  for (long k = blockIdx.x * (long)blockDim.x + threadIdx.x; k < n;
+       k += (long)gridDim.x * blockDim.x) {
+    unsigned long long e = (unsigned long long)k + 1ull;  // steps to take
+    unsigned long long a = 1ull, c = 0ull;                // accumulated map
+    unsigned long long pa = M, pc = I;                    // map^(2^bit)
+    while (e) {
+      if (e & 1ull) {  // acc = p o acc
+        a = pa * a;
+        c = pa * c + pc;
+      }
+      pc = pa * pc + pc;  // p = p o p
+      pa = pa * pa;
+      e >>= 1;
+    }
+    const unsigned long long st = a * s0 + c;
+    out[k] = (double)(st >> 11) * (1.0 / 9007199254740992.0);
+  }
+}
+}  // namespace
+
+cudaError_t launch_lcg_fill(unsigned long long state, long n, double* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const long nb = (n + 255) / 256;
+  TMG_COUNT(1);
+  lcg_fill_kernel<<<(int)(nb < 148 * 32 ? nb : 148 * 32), 256, 0, s>>>(state, n, out);
+  return cudaGetLastError();
+}
+
 }  // namespace tmg

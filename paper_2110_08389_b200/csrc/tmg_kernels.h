@@ -73,6 +73,8 @@ cudaError_t launch_dense_solve(const GridArgs& g, const double* Ainv, double* u,
 
 // sqrt(sum x^2) into work[0] (work: >= 1024 doubles), deterministic order
 cudaError_t launch_vec_norm2(const double* x, long n, double* work, cudaStream_t s);
+// out[k] = uniform [0, 1) value k of the Lcg64 stream after `state`
+cudaError_t launch_lcg_fill(unsigned long long state, long n, double* out, cudaStream_t s);
 // x *= alpha
 cudaError_t launch_vec_scale(double* x, long n, double alpha, cudaStream_t s);
 

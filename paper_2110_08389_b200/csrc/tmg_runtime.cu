@@ -638,6 +638,11 @@ int tmg_vec_norm2(const double* x, long n, double* work, double* out_host, void*
   return e == cudaSuccess ? TMG_OK : cuda_fail(e, "vec_norm2");
 }
 
+int tmg_lcg_fill(unsigned long long state, long n, double* out, void* stream) {
+  cudaError_t e = launch_lcg_fill(state, n, out, (cudaStream_t)stream);
+  return e == cudaSuccess ? TMG_OK : cuda_fail(e, "lcg_fill");
+}
+
 int tmg_vec_scale(double* x, long n, double alpha, void* stream) {
   cudaError_t e = launch_vec_scale(x, n, alpha, (cudaStream_t)stream);
   return e == cudaSuccess ? TMG_OK : cuda_fail(e, "vec_scale");

@@ -57,6 +57,31 @@ class Lcg64:
             self.state = int(out[-1])
         return out
 
+    def advance(self, n: int):
+        """Skip n states (jump-ahead by squaring the affine map)."""
+        a, c = 1, 0
+        pa, pc = MULT, INC
+        e = int(n)
+        while e:
+            if e & 1:
+                a, c = (pa * a) & _MASK, (pa * c + pc) & _MASK
+            pa, pc = (pa * pa) & _MASK, (pa * pc + pc) & _MASK
+            e >>= 1
+        self.state = (a * self.state + c) & _MASK
+
+    def fill_device(self, shape):
+        """`fill` generated on the GPU (same stream, bit for bit): a CUDA
+        float64 tensor; for 10^8 - 10^9-value inputs."""
+        from . import _device, _lib
+        import torch
+        _device.require_cuda()
+        n = int(np.prod(shape))
+        out = torch.empty(n, dtype=torch.float64, device="cuda")
+        _lib.check(_lib.lib().tmg_lcg_fill(self.state, n, _device.ptr(out),
+                                           _device.stream_handle()))
+        self.advance(n)
+        return out.reshape(tuple(shape))
+
     def fill(self, shape) -> np.ndarray:
         """Array of uniform [0, 1) samples in C order."""
         n = int(np.prod(shape))

@@ -110,3 +110,22 @@ def test_config_validation():
     assert smoothers.sweep_cost("wireframe", 5) == 409
     with pytest.raises(ValueError):
         smoothers.compile_plan("plaid", 8, 8)
+
+
+def test_lcg_jump_ahead_matches_stream():
+    from paper_2110_08389_b200.rng import Lcg64
+    for seed, n in ((0, 1), (7, 4096), (3, 12345), (11, 5000)):
+        a, b = Lcg64(seed), Lcg64(seed)
+        a.fill(n)
+        b.advance(n)
+        assert a.state == b.state
+
+
+@pytest.mark.gpu
+def test_lcg_device_fill_bit_identical(cuda):
+    from paper_2110_08389_b200.rng import Lcg64
+    for seed, shape in ((0, (7,)), (5, (129, 131)), (2, (1000, 1003))):
+        a, b = Lcg64(seed), Lcg64(seed)
+        host = a.fill(shape)
+        dev = b.fill_device(shape).cpu().numpy()
+        assert np.array_equal(host, dev) and a.state == b.state
