@@ -302,7 +302,7 @@ def run_ours(args):
     s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
     ev = lambda: torch.cuda.Event()  # noqa: E731
     in_done, cmp_done, out_done = [ev(), ev()], [ev(), ev()], [ev(), ev()]
-    e2e_steps = max(2, min(args.steps, 6))
+    e2e_steps = max(2, min(args.steps, 10))
 
     def pipelined(k_steps):
         start = torch.cuda.Event(enable_timing=True)
