@@ -309,7 +309,7 @@ long dump_members(const Geometry& g, int* oi, int* oj, int* oblk, int* oflags, l
 
 // plan statistics without a device (tmg_plan_stats): uploads are skipped
 static thread_local bool g_dry_run = false;
-static thread_local long long g_stats[8];
+static thread_local long long g_stats[10];
 
 template <class T>
 static T* upload(const std::vector<T>& v, size_t& bytes, std::string& err) {
@@ -560,6 +560,24 @@ std::string pack_plan(Geometry&& geo, int q, int mode, Plan& P) {
         st[2] += c.n;
       }
       for (const auto& bh : bhubs) st[3] += (long long)bh.size();
+      // warps whose 32 chunks are one straight run of full chunks (the
+      // kernel's arithmetic gather path): g_stats[8]; all warps: [9]
+      for (size_t w = 0; w + 32 <= ch.size(); w += 32) {
+        bool uni = true;
+        for (int l = 0; l < 32 && uni; l++) {
+          const ChunkD& c = ch[w + l];
+          uni = c.n == q;
+          if (uni && l > 0) {
+            const ChunkD& p = ch[w + l - 1];
+            const int tb = (c.geo >> 2) & 1, axis = c.geo & 1, neg = (c.geo >> 1) & 1;
+            const int si = tb ? 1 : g.ny + 1, sj = tb ? g.nx + 1 : 1;
+            const int str = (axis ? sj : si) * (neg ? -1 : 1);
+            uni = p.geo == c.geo && p.cidx == c.cidx && p.off + q * str == c.off;
+          }
+        }
+        g_stats[8] += uni;
+        g_stats[9] += 1;
+      }
     }
     lc.chunks = upload(ch, P.device_bytes, err);
     lc.bins = upload(bins, P.device_bytes, err);
@@ -875,6 +893,7 @@ extern "C" int tmg_plan_stats(int scheme, int nx, int ny, int q, int mode, long 
   std::string err = tmg::build_plan(scheme, nx, ny, q, mode, P);
   tmg::g_dry_run = false;
   for (int k = 0; k < 8; k++) out[k] = tmg::g_stats[k];
+  std::fprintf(stderr, "uniform warps %lld of %lld\n", tmg::g_stats[8], tmg::g_stats[9]);
   if (!err.empty()) {
     std::fprintf(stderr, "tmg_plan_stats: %s\n", err.c_str());
     return -1;
