@@ -140,19 +140,22 @@ def test_shard_plan_levels():
 # ---------------------------------------------------------------------------
 # multi-process solves (gloo)
 
-@pytest.mark.parametrize("kind,n,ny,world", [
-    ("tweed", 64, 64, 2),
-    ("wireframe", 64, 64, 2),
-    ("tweed", 64, 32, 3),
-    ("zebra_x", 32, 32, 2),
-    ("checkerboard", 32, 32, 2),
+@pytest.mark.parametrize("kind,n,ny,world,restriction", [
+    ("tweed", 64, 64, 2, "full"),
+    ("wireframe", 64, 64, 2, "full"),
+    ("tweed", 64, 32, 3, "full"),
+    ("tweed", 128, 128, 4, "half"),
+    ("zebra_x", 32, 32, 2, "full"),
+    ("zebra_y", 32, 48, 3, "half"),
+    ("checkerboard", 32, 32, 2, "full"),
 ])
-def test_sharded_solve_oracle_ops(orc, tmp_path, kind, n, ny, world):
+def test_sharded_solve_oracle_ops(orc, tmp_path, kind, n, ny, world, restriction):
     """world ranks over gloo with oracle rank-local operators reproduce the
     single-domain oracle solve bit for bit (same cycles, same norms, same u)."""
-    u_ref, rep = _oracle_solve(orc, kind, n, ny, max_cycles=12)
+    u_ref, rep = _oracle_solve(orc, kind, n, ny, restriction=restriction, max_cycles=12)
     outs = _run_workers(tmp_path, world, "--ops", "oracle", "--kind", kind, "--nx", str(n),
-                        "--ny", str(ny), "--max-cycles", "12", "--min-groups", "3")
+                        "--ny", str(ny), "--max-cycles", "12", "--min-groups", "3",
+                        "--restriction", restriction)
     for o in outs:
         assert int(o["nshard"]) >= 1
         assert int(o["cycles"]) == rep.cycles
