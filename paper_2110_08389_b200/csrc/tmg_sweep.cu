@@ -30,21 +30,12 @@
 
 namespace cg = cooperative_groups;
 
-#ifndef TMG_FULL_PATH
-#define TMG_FULL_PATH 0  // 1: separate predicate-free elimination for full chunks
-#endif
 
-#ifndef TMG_ASYNC_GATHER
-#define TMG_ASYNC_GATHER 0  // 1: phase A stages f, u-, u+ with cp.async (no register round trip)
-#endif
 
 #ifndef TMG_SKIP
 #define TMG_SKIP 0  // profiling only: 1 skip elimination, 2 skip PCR, 4 skip hubs, 8 skip finalize, 16 skip chunk-end pass
 #endif
 
-#ifndef TMG_PREFETCH
-#define TMG_PREFETCH 0  // 1: prefetch the next bin's field rows into L2
-#endif
 
 #ifndef TMG_BATCH
 #define TMG_BATCH 8  // gather items in flight per lane
@@ -85,19 +76,6 @@ __device__ __forceinline__ double* remote(double* p, int rank) {
   } else {
     return p;
   }
-}
-
-// 8-byte asynchronous global -> shared copy (LDGSTS) and its completion wait
-__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-}
-
-__device__ __forceinline__ void prefetch_l2(const double* p) {
-  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
 
 // split cluster barrier: arrive once this CTA's DSMEM reads are done, wait
@@ -278,14 +256,12 @@ __device__ __forceinline__ void chunk_eliminate(int tid, int nI, double* R, cons
   gu = ga;
 }
 
-// One bin (a cluster's worth of chunks) of a colour stage.  next_bin >= 0:
-// the bin this CTA handles next, whose field rows are prefetched into L2
-// once this bin's gather is done, so that its gather finds them there.
+// One bin (a cluster's worth of chunks) of a colour stage.
 template <bool CLUSTER, int Q>
 __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __restrict__ chunks,
                                           const BinD* __restrict__ bins,
                                           const HubD* __restrict__ hubs, int cs_size, int bin,
-                                          int rank, int next_bin, double* smem) {
+                                          int rank, double* smem) {
   constexpr int T = kThreads;
   double* R = smem;
   double* PA = R + T * Q;
@@ -305,9 +281,6 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
 
   TMG_T(0);
   const ChunkD mine = chunks[((size_t)bin * cs_size + rank) * T + tid];
-  ChunkD nxt;
-  nxt.n = 0;
-  if (TMG_PREFETCH && next_bin >= 0) nxt = chunks[((size_t)next_bin * cs_size + rank) * T + tid];
   Chunk c;
   c.unpack(mine, C, ld, a.ldt);
   const FieldView U{u, a.ut, a.nx, a.ny, a.mode};
@@ -396,47 +369,7 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
     recJ[tid] = make_int4(pa_rel, pc_rel, c.da, 0);
     recX[tid] = make_double2(xlv, xhv);
   __syncwarp();
-  if constexpr (TMG_ASYNC_GATHER) {
-    // pass 1: every lane issues the asynchronous copies of all its points
-    // (f, u at the two cross neighbours into the R, PA, PC slots) back to
-    // back, so the whole bin's loads are in flight at once; pass 2 turns
-    // them into the frozen right-hand side and stages the along couplings
-    const int4* recI = reinterpret_cast<const int4*>(sA);
-    const int4* recJ = recI + T;
-    const double2* recX = reinterpret_cast<const double2*>(recJ + T);
-#pragma unroll
-    for (int m = 0; m < Q; m++) {
-      const int src = wbase + m * PER + csub;
-      const int4 ri = recI[src];
-      if (ksub < (ri.w & 255)) {
-        const bool tb_s = (ri.w >> 8) & 1;
-        const double* ub = tb_s ? a.ut : u;
-        const double* fb = tb_s ? a.ft : f;
-        const int o = ri.x + ksub * ri.y;
-        const int sl = sw<Q>(src, ksub);
-        cp_async8(R + sl, fb + o);
-        cp_async8(PA + sl, ub + o - ri.z);
-        cp_async8(PC + sl, ub + o + ri.z);
-      }
-    }
-    cp_async_wait_all();
-    __syncwarp();
-#pragma unroll
-    for (int m = 0; m < Q; m++) {
-      const int src = wbase + m * PER + csub;
-      const int nn = recI[src].w & 255;
-      if (ksub < nn) {
-        const int4 rj = recJ[src];
-        const double2 rx = recX[src];
-        const int sl = sw<Q>(src, ksub);
-        const int ai = ksub * rj.z;
-        const double va = __ldg(a.W + rj.x + ai), vc = __ldg(a.W + rj.y + ai);
-        R[sl] = fma(-rx.y, PC[sl], fma(-rx.x, PA[sl], R[sl]));
-        PA[sl] = va;
-        PC[sl] = vc;
-      }
-    }
-  } else {
+  {
     const int4* recI = reinterpret_cast<const int4*>(sA);
     const int4* recJ = recI + T;
     const double2* recX = reinterpret_cast<const double2*>(recJ + T);
@@ -509,20 +442,6 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
     }
   }
   __syncwarp();
-  if (TMG_PREFETCH && nxt.n > 0) {  // next bin's rows of f and u into L2
-    const int tb = (nxt.geo >> 2) & 1, axis = nxt.geo & 1, neg = (nxt.geo >> 1) & 1;
-    const int si = tb ? 1 : ld, sj = tb ? a.ldt : 1;
-    const int st = (axis ? sj : si) * (neg ? -1 : 1), cs = axis ? si : sj;
-    const double* ub = tb ? a.ut : u;
-    const double* fb = tb ? a.ft : f;
-    const int o0 = nxt.off, o1 = nxt.off + (nxt.n - 1) * st;
-    prefetch_l2(fb + o0);
-    prefetch_l2(fb + o1);
-    prefetch_l2(ub + o0 - cs);
-    prefetch_l2(ub + o1 - cs);
-    prefetch_l2(ub + o0 + cs);
-    prefetch_l2(ub + o1 + cs);
-  }
   TMG_T(1);
 
   // ---------------- phase B: chunk elimination -------------------------------
@@ -543,10 +462,7 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
   }
   if constexpr (Q > 1 && !(TMG_SKIP & 1)) {
     // full chunks (all but the last chunk of a leg) take the predicate-free path
-    if (TMG_FULL_PATH && nI == Q - 1)
-      chunk_eliminate<Q, Q - 1>(tid, nI, R, PA, PC, csum, a_first, lam, ivr, bad, ad, bd, gd, au,
-                                bu, gu);
-    else if (nI > 0)
+    if (nI > 0)
       chunk_eliminate<Q, 0>(tid, nI, R, PA, PC, csum, a_first, lam, ivr, bad, ad, bd, gd, au, bu,
                             gu);
   }
@@ -753,17 +669,14 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
   TMG_T(6);
 }
 
-// One CTA (cluster) per bin.  The bin `ahead` places later (ahead = the
-// number of co-resident clusters) starts about when this one retires, so its
-// field rows are prefetched into L2 while this bin computes.
+// One CTA (cluster) per bin.
 template <bool CLUSTER, int Q>
 __global__ void __launch_bounds__(kThreads, Q <= 8 ? TMG_MINB8 : TMG_MINB)
 block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* __restrict__ bins,
-                   const HubD* __restrict__ hubs, int cs_size, int nbins, int ahead) {
+                   const HubD* __restrict__ hubs, int cs_size) {
   extern __shared__ double smem[];
   const int rank = CLUSTER ? (int)cg::this_cluster().block_rank() : 0;
-  const int bin = blockIdx.x / cs_size, nb = bin + ahead;
-  sweep_bin<CLUSTER, Q>(a, chunks, bins, hubs, cs_size, bin, rank, nb < nbins ? nb : -1, smem);
+  sweep_bin<CLUSTER, Q>(a, chunks, bins, hubs, cs_size, blockIdx.x / cs_size, rank, smem);
   if constexpr (CLUSTER) cluster_wait();
 }
 
@@ -815,58 +728,13 @@ cudaError_t set_attrs() {
   return e;
 }
 
-// co-resident clusters of the block-solver kernel per (log2 Q, log2 cs),
-// measured once at init (before any stream capture)
-int g_resident[5][5];
-
-int qlog(int v) {
-  int l = 0;
-  while ((1 << l) < v) l++;
-  return l;
-}
-
-template <int Q>
-cudaError_t measure_resident() {
-  int dev = 0, sms = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e != cudaSuccess) return e;
-  for (int cs = 1; cs <= kMaxCluster; cs *= 2) {
-    int n = 0;
-    if (cs == 1) {
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, block_sweep_kernel<false, Q>, kThreads,
-                                                        smem_bytes<Q>());
-      n *= sms;
-    } else {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(cs * 1024);
-      cfg.blockDim = dim3(kThreads);
-      cfg.dynamicSmemBytes = smem_bytes<Q>();
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = cs;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      e = cudaOccupancyMaxActiveClusters(&n, block_sweep_kernel<true, Q>, &cfg);
-    }
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      n = 0;
-    }
-    g_resident[qlog(Q)][qlog(cs)] = n > 0 ? n : 1;
-  }
-  return cudaSuccess;
-}
-
 template <int Q>
 cudaError_t launch_class(const LaunchClass& lc, const SweepArgs& a, cudaStream_t stream) {
-  const int grid = lc.nbins, ahead = g_resident[qlog(Q)][qlog(lc.cs)];
+  const int grid = lc.nbins;
   if (lc.cs == 1) {
     TMG_COUNT(1);
     block_sweep_kernel<false, Q><<<grid, kThreads, smem_bytes<Q>(), stream>>>(
-        a, lc.chunks, lc.bins, lc.hubs, 1, lc.nbins, ahead);
+        a, lc.chunks, lc.bins, lc.hubs, 1);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -883,7 +751,7 @@ cudaError_t launch_class(const LaunchClass& lc, const SweepArgs& a, cudaStream_t
   cfg.numAttrs = 1;
   TMG_COUNT(1);
   return cudaLaunchKernelEx(&cfg, block_sweep_kernel<true, Q>, a, (const ChunkD*)lc.chunks,
-                            (const BinD*)lc.bins, (const HubD*)lc.hubs, lc.cs, lc.nbins, ahead);
+                            (const BinD*)lc.bins, (const HubD*)lc.hubs, lc.cs);
 }
 }  // namespace
 
@@ -916,11 +784,6 @@ cudaError_t init_sweep_kernels() {
     if (done == cudaSuccess) done = set_attrs<4>();
     if (done == cudaSuccess) done = set_attrs<2>();
     if (done == cudaSuccess) done = set_attrs<1>();
-    if (done == cudaSuccess) done = measure_resident<16>();
-    if (done == cudaSuccess) done = measure_resident<8>();
-    if (done == cudaSuccess) done = measure_resident<4>();
-    if (done == cudaSuccess) done = measure_resident<2>();
-    if (done == cudaSuccess) done = measure_resident<1>();
   }
   return done;
 }
