@@ -277,3 +277,25 @@ def test_boundary_values_bitwise_preserved(cuda):
     assert rep.converged
     assert np.array_equal(u[0, :], g[0, :]) and np.array_equal(u[-1, :], g[-1, :])
     assert np.array_equal(u[:, 0], g[:, 0]) and np.array_equal(u[:, -1], g[:, -1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,n,q", [("zebra_x", 512, 1), ("zebra_y", 512, 2), ("wireframe", 512, 1),
+                                      ("wireframe", 256, 2), ("tweed", 512, 1)])
+def test_legs_spanning_ctas(cuda, orc, monkeypatch, kind, n, q):
+    """Small chunks (TMG_CHUNK) make legs longer than a CTA's 256 threads, so
+    the reduced systems span the CTAs of a cluster (the cross-CTA path that
+    8193^2 wireframe rings and zebra lines take)."""
+    monkeypatch.setenv("TMG_CHUNK", str(q))
+    from paper_2110_08389_b200 import grid as g, smoothers as sm, stencil as stc
+    x = g.make_tanh_wall(n, 1.0, 2.0)
+    st = stc.assemble(x, x)
+    rng = np.random.default_rng(11)
+    u0 = np.zeros((n + 1, n + 1))
+    u0[1:-1, 1:-1] = rng.standard_normal((n - 1, n - 1))
+    f = rng.standard_normal((n + 1, n + 1))
+    ud = cuda.from_numpy(u0.copy()).cuda()
+    sm.sweep(kind, st, sm.PlanBundle(n, n), ud, cuda.from_numpy(f).cuda())
+    uo = u0.copy()
+    orc.sweep(kind, (st.W, st.E, st.S, st.N), uo, f, orc.max_threads())
+    assert np.abs(ud.cpu().numpy() - uo).max() <= 1e-10 * np.abs(uo).max()
