@@ -100,6 +100,7 @@ struct LaunchClass {
   int cs;          // CTAs per cluster (1, 2, 4, 8, 16)
   int nbins;
   int red;
+  int xcta;        // 1: every bin has a leg crossing a CTA boundary of its cluster
   ChunkD* chunks;  // nbins * cs * kThreads
   BinD* bins;
   HubD* hubs;

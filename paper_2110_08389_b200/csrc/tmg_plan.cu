@@ -444,6 +444,7 @@ std::string pack_plan(Geometry&& geo, int q, int mode, Plan& P) {
     lc.q = q;
     lc.cs = cs;
     lc.red = red;
+    lc.xcta = 0;
     lc.nbins = (int)bins.size();
     ChunkD idle;
     std::memset(&idle, 0, sizeof(idle));
@@ -579,11 +580,32 @@ std::string pack_plan(Geometry&& geo, int q, int mode, Plan& P) {
         g_stats[9] += 1;
       }
     }
-    lc.chunks = upload(ch, P.device_bytes, err);
-    lc.bins = upload(bins, P.device_bytes, err);
-    lc.hubs = upload(hubs, P.device_bytes, err);
-    if (!err.empty()) return err;
-    P.classes.push_back(lc);
+    // bins with a leg across a CTA boundary run on their own kernel
+    // instantiation (the cross-CTA reduced solve), the others keep theirs
+    for (int want = 0; want <= 1; want++) {
+      std::vector<ChunkD> ch2;
+      std::vector<BinD> bins2;
+      std::vector<HubD> hubs2;
+      for (int k = 0; k < lc.nbins; k++) {
+        if ((xcta[k] != 0) != (want != 0)) continue;
+        const size_t per = (size_t)cs * T;
+        ch2.insert(ch2.end(), ch.begin() + (size_t)k * per, ch.begin() + (size_t)(k + 1) * per);
+        BinD b2 = bins[k];
+        b2.hub0 = (int)hubs2.size();
+        hubs2.insert(hubs2.end(), hubs.begin() + bins[k].hub0,
+                     hubs.begin() + bins[k].hub0 + bins[k].nhub);
+        bins2.push_back(b2);
+      }
+      if (bins2.empty()) continue;
+      LaunchClass l2 = lc;
+      l2.xcta = want;
+      l2.nbins = (int)bins2.size();
+      l2.chunks = upload(ch2, P.device_bytes, err);
+      l2.bins = upload(bins2, P.device_bytes, err);
+      l2.hubs = upload(hubs2, P.device_bytes, err);
+      if (!err.empty()) return err;
+      P.classes.push_back(l2);
+    }
     return std::string();
   };
 

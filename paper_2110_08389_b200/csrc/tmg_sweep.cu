@@ -257,7 +257,7 @@ __device__ __forceinline__ void chunk_eliminate(int tid, int nI, double* R, cons
 }
 
 // One bin (a cluster's worth of chunks) of a colour stage.
-template <bool CLUSTER, int Q>
+template <bool CLUSTER, bool XCTA, int Q>
 __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __restrict__ chunks,
                                           const BinD* __restrict__ bins,
                                           const HubD* __restrict__ hubs, int cs_size, int bin,
@@ -468,7 +468,7 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
   }
   TMG_T(2);
   // publish the first-point affine form for the left neighbour chunk
-  const bool xcta = bd_.warp_local == 2;  // some leg crosses a CTA boundary
+  constexpr bool xcta = XCTA;  // some leg of every bin of this launch crosses a CTA boundary
   __syncthreads();  // every warp is done with its gather records (same region)
   sA[tid] = au;
   sB[tid] = bu;
@@ -670,13 +670,13 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
 }
 
 // One CTA (cluster) per bin.
-template <bool CLUSTER, int Q>
+template <bool CLUSTER, bool XCTA, int Q>
 __global__ void __launch_bounds__(kThreads, Q <= 8 ? TMG_MINB8 : TMG_MINB)
 block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* __restrict__ bins,
                    const HubD* __restrict__ hubs, int cs_size) {
   extern __shared__ double smem[];
   const int rank = CLUSTER ? (int)cg::this_cluster().block_rank() : 0;
-  sweep_bin<CLUSTER, Q>(a, chunks, bins, hubs, cs_size, blockIdx.x / cs_size, rank, smem);
+  sweep_bin<CLUSTER, XCTA, Q>(a, chunks, bins, hubs, cs_size, blockIdx.x / cs_size, rank, smem);
   if constexpr (CLUSTER) cluster_wait();
 }
 
@@ -716,14 +716,20 @@ size_t smem_bytes() {
 
 template <int Q>
 cudaError_t set_attrs() {
-  cudaError_t e = cudaFuncSetAttribute(block_sweep_kernel<false, Q>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem_bytes<Q>());
+  const int sm = (int)smem_bytes<Q>();
+  cudaError_t e = cudaFuncSetAttribute(block_sweep_kernel<false, false, Q>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(block_sweep_kernel<true, Q>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<Q>());
+    e = cudaFuncSetAttribute(block_sweep_kernel<true, false, Q>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(block_sweep_kernel<true, true, Q>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   if (e == cudaSuccess)  // clusters of 16 CTAs (rings of wireframe grids >= 8193^2)
-    e = cudaFuncSetAttribute(block_sweep_kernel<true, Q>,
+    e = cudaFuncSetAttribute(block_sweep_kernel<true, false, Q>,
+                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(block_sweep_kernel<true, true, Q>,
                              cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return e;
 }
@@ -733,7 +739,7 @@ cudaError_t launch_class(const LaunchClass& lc, const SweepArgs& a, cudaStream_t
   const int grid = lc.nbins;
   if (lc.cs == 1) {
     TMG_COUNT(1);
-    block_sweep_kernel<false, Q><<<grid, kThreads, smem_bytes<Q>(), stream>>>(
+    block_sweep_kernel<false, false, Q><<<grid, kThreads, smem_bytes<Q>(), stream>>>(
         a, lc.chunks, lc.bins, lc.hubs, 1);
     return cudaGetLastError();
   }
@@ -750,7 +756,11 @@ cudaError_t launch_class(const LaunchClass& lc, const SweepArgs& a, cudaStream_t
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   TMG_COUNT(1);
-  return cudaLaunchKernelEx(&cfg, block_sweep_kernel<true, Q>, a, (const ChunkD*)lc.chunks,
+  if (lc.xcta)
+    return cudaLaunchKernelEx(&cfg, block_sweep_kernel<true, true, Q>, a,
+                              (const ChunkD*)lc.chunks, (const BinD*)lc.bins,
+                              (const HubD*)lc.hubs, lc.cs);
+  return cudaLaunchKernelEx(&cfg, block_sweep_kernel<true, false, Q>, a, (const ChunkD*)lc.chunks,
                             (const BinD*)lc.bins, (const HubD*)lc.hubs, lc.cs);
 }
 }  // namespace
