@@ -344,6 +344,10 @@ class ShardedSolver:
                               self.ops.buffer(ri.numel())))
             self._halo.append(sides)
         self._gathers = {}
+        if self.comm.world > 1:
+            # a collective before the first batched send/recv of the group
+            # (NCCL requires the first P2P batch to follow one)
+            self.comm.allreduce_max([0.0], self.ops.device)
 
     # -- plumbing ---------------------------------------------------------
     def _swap(self, level, which):
