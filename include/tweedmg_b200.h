@@ -194,6 +194,27 @@ int tmg_relax_legged(long n, const int64_t* ii, const int64_t* jj, long m, const
                      const double* S, const double* N, double* u, const double* f,
                      void* stream);
 
+/* ---- 3D tweed on cubes (BASELINE config 4; no reference counterpart: the
+ *      2D semantics of stencil.py / transfer.py / tridiag.py:84-125 extended
+ *      to a third axis on the survey's cube layout).  Fields
+ *      are DEVICE (n+1)^3 C-order arrays, k fastest.  x: HOST coordinates
+ *      (n+1), used on all three axes. */
+typedef struct tmg_cube tmg_cube;
+const char* tmg_cube_last_error(void);
+int tmg_cube_create(int n, const double* x, tmg_cube** out);
+int tmg_cube_destroy(tmg_cube* h);
+int tmg_cube_levels(tmg_cube* h);
+long tmg_cube_blocks(tmg_cube* h, int level, int red);
+/* one 3D tweed sweep (red blocks, then black) of the finest level */
+int tmg_cube_sweep(tmg_cube* h, double* u, const double* f, void* stream);
+int tmg_cube_defect(tmg_cube* h, const double* u, const double* f, double* d, void* stream);
+/* session: load u, f; replay V(nu1, nu2) cycles (CUDA graph); norm + pivot
+ * flag (synchronizes); store u */
+int tmg_cube_load(tmg_cube* h, const double* u, const double* f, void* stream);
+int tmg_cube_cycles(tmg_cube* h, int nu1, int nu2, int reps, void* stream);
+int tmg_cube_norm(tmg_cube* h, double* out_host, void* stream);
+int tmg_cube_store(tmg_cube* h, double* u, void* stream);
+
 /* ---- profiling aid: average per-CTA cycles between the phase marks of the
  *      block-solver kernel (gather, elimination, reduced solve, hub, finalize,
  *      scatter) over the last launch; non-zero only in builds made with

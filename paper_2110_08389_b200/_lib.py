@@ -67,6 +67,17 @@ def _declare(L):
         "tmg_vec_norm2": ([vp, lp, vp, pd, vp], ip),
         "tmg_vec_scale": ([vp, lp, dp, vp], ip),
         "tmg_lcg_fill": ([ctypes.c_ulonglong, lp, vp, vp], ip),
+        "tmg_cube_last_error": ([], ctypes.c_char_p),
+        "tmg_cube_create": ([ip, vp, ctypes.POINTER(vp)], ip),
+        "tmg_cube_destroy": ([vp], ip),
+        "tmg_cube_levels": ([vp], ip),
+        "tmg_cube_blocks": ([vp, ip, ip], lp),
+        "tmg_cube_sweep": ([vp, vp, vp, vp], ip),
+        "tmg_cube_defect": ([vp, vp, vp, vp, vp], ip),
+        "tmg_cube_load": ([vp, vp, vp, vp], ip),
+        "tmg_cube_cycles": ([vp, ip, ip, ip, vp], ip),
+        "tmg_cube_norm": ([vp, pd, vp], ip),
+        "tmg_cube_store": ([vp, vp, vp], ip),
         "tmg_group_count": ([ip, ip, ip], ip),
         "tmg_group_sizes": ([ip, ip, ip, vp, lp], lp),
         "tmg_group_offsets": ([ip, ip, ip, ip, ip, vp, lp], lp),

@@ -1,0 +1,508 @@
+// 3D tweed V-cycle on cubes (BASELINE config 4).
+//
+// The reference is 2D only; this path extends its semantics to a third axis
+// (stencil.py:43-96 with coefficients B, T along k; transfer.py:21-56 as
+// tensor products; the m-legged Thomas of tridiag.py:84-125 for blocks of up
+// to 6 legs) on the survey's cube layout: a point lies on the line along the
+// axis of its unique smallest mirrored coordinate, from the wall to the first
+// tie point (the branch); colour = parity(s1 + s3) of the branch's sorted
+// mirrored coordinates, red = even.  Its checker is the CPU restatement in
+// oracle/tweed3d_oracle.c.
+//
+// Fields are C-order (n+1)^3 with k fastest.  The block solver runs one
+// thread per block (blocks enumerated with k fastest, so neighbouring
+// threads walk neighbouring lines); each leg's forward-eliminated pivots and
+// right-hand sides go to two field-sized scratch arrays, read back by the
+// back substitution.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tweedmg_b200.h"
+#include "tmg_kernels.h"
+
+using namespace tmg;
+
+namespace {
+
+struct Block3 {
+  int32_t bi, bj, bk;
+  int16_t len;      // points per leg (all legs of a block have s1 - 1)
+  uint8_t nleg;
+  uint8_t red;
+  uint8_t leg[6];   // bits 0-1 axis, bit 2: step -1 (tip at n-1)
+  uint8_t pad[2];
+};
+static_assert(sizeof(Block3) == 24, "Block3 layout");
+
+__host__ __device__ inline long mirror(long x, long n) { return x < n - x ? x : n - x; }
+
+struct Coef3 {
+  const double *W, *E, *S, *N, *B, *T;
+};
+
+__device__ __forceinline__ size_t idx3(int n, int i, int j, int k) {
+  return ((size_t)i * (n + 1) + j) * (size_t)(n + 1) + k;
+}
+
+__device__ __forceinline__ double cpl3(const Coef3& c, int a, int s, int i, int j, int k) {
+  if (a == 0) return s < 0 ? __ldg(c.W + i) : __ldg(c.E + i);
+  if (a == 1) return s < 0 ? __ldg(c.S + j) : __ldg(c.N + j);
+  return s < 0 ? __ldg(c.B + k) : __ldg(c.T + k);
+}
+
+__device__ __forceinline__ double diag3(const Coef3& c, int i, int j, int k) {
+  return -(__ldg(c.W + i) + __ldg(c.E + i) + __ldg(c.S + j) + __ldg(c.N + j) + __ldg(c.B + k) +
+           __ldg(c.T + k));
+}
+
+__device__ __forceinline__ unsigned dbit(int a, int s) { return 1u << (2 * a + (s > 0 ? 1 : 0)); }
+
+__device__ __forceinline__ double rhs3(const Coef3& c, int n, const double* __restrict__ u,
+                                       const double* __restrict__ f, int i, int j, int k,
+                                       unsigned skip) {
+  double r = f[idx3(n, i, j, k)];
+  if (!(skip & 1u)) r -= __ldg(c.W + i) * u[idx3(n, i - 1, j, k)];
+  if (!(skip & 2u)) r -= __ldg(c.E + i) * u[idx3(n, i + 1, j, k)];
+  if (!(skip & 4u)) r -= __ldg(c.S + j) * u[idx3(n, i, j - 1, k)];
+  if (!(skip & 8u)) r -= __ldg(c.N + j) * u[idx3(n, i, j + 1, k)];
+  if (!(skip & 16u)) r -= __ldg(c.B + k) * u[idx3(n, i, j, k - 1)];
+  if (!(skip & 32u)) r -= __ldg(c.T + k) * u[idx3(n, i, j, k + 1)];
+  return r;
+}
+
+// one colour stage: thread b solves block b of the colour's list
+__global__ void __launch_bounds__(128) sweep3_kernel(int n, Coef3 c, const Block3* __restrict__ blocks,
+                                                     int nb, double* __restrict__ u,
+                                                     const double* __restrict__ f,
+                                                     double* __restrict__ sb,
+                                                     double* __restrict__ sr, int* err) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const Block3 B = blocks[b];
+  unsigned bskip = 0;
+  for (int l = 0; l < B.nleg; l++) {
+    const int a = B.leg[l] & 3, s = (B.leg[l] & 4) ? -1 : 1;
+    bskip |= dbit(a, -s);
+  }
+  double num = rhs3(c, n, u, f, B.bi, B.bj, B.bk, bskip);
+  double den = diag3(c, B.bi, B.bj, B.bk);
+  bool bad = false;
+  const int L = B.len;
+  for (int l = 0; l < B.nleg; l++) {
+    const int a = B.leg[l] & 3, s = (B.leg[l] & 4) ? -1 : 1;
+    const int tip = s > 0 ? 1 : n - 1;
+    double bp = 0.0, rp = 0.0, cprev = 0.0;
+    for (int t = 0; t < L; t++) {
+      const int i = a == 0 ? tip + s * t : B.bi;
+      const int j = a == 1 ? tip + s * t : B.bj;
+      const int k = a == 2 ? tip + s * t : B.bk;
+      unsigned skip = dbit(a, s);
+      if (t > 0) skip |= dbit(a, -s);
+      const double r = rhs3(c, n, u, f, i, j, k, skip);
+      const double bb = diag3(c, i, j, k);
+      if (t == 0) {
+        bp = bb;
+        rp = r;
+      } else {
+        bad |= bp > -1e-300 && bp < 1e-300;
+        const double w = cpl3(c, a, -s, i, j, k) / bp;
+        bp = bb - w * cprev;
+        rp = r - w * rp;
+      }
+      cprev = cpl3(c, a, s, i, j, k);
+      const size_t o = idx3(n, i, j, k);
+      sb[o] = bp;
+      sr[o] = rp;
+    }
+    if (L > 0) {
+      const double d = cpl3(c, a, -s, B.bi, B.bj, B.bk);
+      bad |= bp > -1e-300 && bp < 1e-300;
+      num -= d * rp / bp;
+      den -= d * cprev / bp;
+    }
+  }
+  bad |= den > -1e-300 && den < 1e-300;
+  const double xb = num / den;
+  u[idx3(n, B.bi, B.bj, B.bk)] = xb;
+  for (int l = 0; l < B.nleg; l++) {
+    const int a = B.leg[l] & 3, s = (B.leg[l] & 4) ? -1 : 1;
+    const int tip = s > 0 ? 1 : n - 1;
+    double x = xb;
+    for (int t = L - 1; t >= 0; t--) {
+      const int i = a == 0 ? tip + s * t : B.bi;
+      const int j = a == 1 ? tip + s * t : B.bj;
+      const int k = a == 2 ? tip + s * t : B.bk;
+      const size_t o = idx3(n, i, j, k);
+      x = (sr[o] - cpl3(c, a, s, i, j, k) * x) / sb[o];
+      u[o] = x;
+    }
+  }
+  if (bad) atomicOr(err, 1);
+}
+
+// d = f - L u (interior), 0 on the boundary; or the max |f - L u| into dmax
+__global__ void __launch_bounds__(256) defect3_kernel(int n, Coef3 c, const double* __restrict__ u,
+                                                      const double* __restrict__ f,
+                                                      double* __restrict__ d,
+                                                      unsigned long long* dmax) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y, i = blockIdx.z;
+  if (k > n) return;
+  const size_t o = idx3(n, i, j, k);
+  double v = 0.0;
+  if (i > 0 && j > 0 && k > 0 && i < n && j < n && k < n) {
+    const double cc = -(__ldg(c.W + i) + __ldg(c.E + i) + __ldg(c.S + j) + __ldg(c.N + j) +
+                        __ldg(c.B + k) + __ldg(c.T + k));
+    double acc = __dmul_rn(__ldg(c.W + i), u[idx3(n, i - 1, j, k)]);
+    acc = __dadd_rn(acc, __dmul_rn(__ldg(c.E + i), u[idx3(n, i + 1, j, k)]));
+    acc = __dadd_rn(acc, __dmul_rn(__ldg(c.S + j), u[idx3(n, i, j - 1, k)]));
+    acc = __dadd_rn(acc, __dmul_rn(__ldg(c.N + j), u[idx3(n, i, j + 1, k)]));
+    acc = __dadd_rn(acc, __dmul_rn(__ldg(c.B + k), u[o - 1]));
+    acc = __dadd_rn(acc, __dmul_rn(__ldg(c.T + k), u[o + 1]));
+    acc = __dadd_rn(acc, __dmul_rn(cc, u[o]));
+    v = __dadd_rn(f[o], -acc);
+  }
+  if (d) d[o] = v;
+  if (dmax) {
+    unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(v));
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, bits, s);
+      bits = o2 > bits ? o2 : bits;
+    }
+    if ((threadIdx.x & 31) == 0 && bits) atomicMax(dmax, bits);
+  }
+}
+
+// coarse = full weighting of d (tensor product of [1/4, 1/2, 1/4])
+__global__ void __launch_bounds__(256) restrict3_kernel(int nf, const double* __restrict__ d,
+                                                        double* __restrict__ out) {
+  const int nc = nf / 2;
+  const int K = blockIdx.x * blockDim.x + threadIdx.x;
+  const int J = blockIdx.y, I = blockIdx.z;
+  if (K > nc) return;
+  double acc = 0.0;
+  if (I > 0 && J > 0 && K > 0 && I < nc && J < nc && K < nc) {
+    const double w[3] = {0.25, 0.5, 0.25};
+    for (int a = 0; a < 3; a++)
+      for (int b = 0; b < 3; b++)
+        for (int e = 0; e < 3; e++)
+          acc += w[a] * w[b] * w[e] * d[idx3(nf, 2 * I - 1 + a, 2 * J - 1 + b, 2 * K - 1 + e)];
+  }
+  out[idx3(nc, I, J, K)] = acc;
+}
+
+// u += trilinear P uc on the fine interior
+__global__ void __launch_bounds__(256) prolong3_kernel(int nc, const double* __restrict__ uc,
+                                                       double* __restrict__ u) {
+  const int nf = 2 * nc;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y, i = blockIdx.z;
+  if (k <= 0 || k >= nf || j <= 0 || j >= nf || i <= 0 || i >= nf) return;
+  const int I = i / 2, J = j / 2, K = k / 2;
+  const int oi = i & 1, oj = j & 1, ok = k & 1;
+  double acc = 0.0;
+  for (int a = 0; a <= oi; a++)
+    for (int b = 0; b <= oj; b++)
+      for (int e = 0; e <= ok; e++) acc += uc[idx3(nc, I + a, J + b, K + e)];
+  const double wgt = 1.0 / (double)((1 + oi) * (1 + oj) * (1 + ok));
+  u[idx3(nf, i, j, k)] += acc * wgt;
+}
+
+__global__ void coarse3_kernel(Coef3 c, double* u, const double* f) {
+  const int n = 2;
+  const double cc = -(c.W[1] + c.E[1] + c.S[1] + c.N[1] + c.B[1] + c.T[1]);
+  const double r = f[idx3(n, 1, 1, 1)] - c.W[1] * u[idx3(n, 0, 1, 1)] - c.E[1] * u[idx3(n, 2, 1, 1)] -
+                   c.S[1] * u[idx3(n, 1, 0, 1)] - c.N[1] * u[idx3(n, 1, 2, 1)] -
+                   c.B[1] * u[idx3(n, 1, 1, 0)] - c.T[1] * u[idx3(n, 1, 1, 2)];
+  u[idx3(n, 1, 1, 1)] = r / cc;
+}
+
+std::string g_err3;
+int fail3(int code, const std::string& m) {
+  g_err3 = m;
+  return code;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host side
+
+struct tmg_cube {
+  std::vector<int> n;                 // per level
+  std::vector<double*> coef;          // per level: W E S N B T (6 (n+1))
+  std::vector<Block3*> blocks[2];     // per level: black, red lists
+  std::vector<int> nblocks[2];
+  std::vector<double*> U, F;          // per level work fields (level 0: session)
+  double *sb = nullptr, *sr = nullptr, *d = nullptr;  // finest-size scratch
+  int* err = nullptr;
+  unsigned long long* dmax = nullptr;
+  int* h_err = nullptr;
+  unsigned long long* h_dmax = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  int gnu1 = -1, gnu2 = -1;
+};
+
+namespace {
+
+int cuda3(cudaError_t e, const char* w) {
+  return e == cudaSuccess ? TMG_OK : fail3(TMG_CUDA, std::string(w) + ": " + cudaGetErrorString(e));
+}
+#define T3(x)                                   \
+  do {                                          \
+    int _s = cuda3((x), #x);                    \
+    if (_s) return _s;                          \
+  } while (0)
+
+void build_blocks(int n, std::vector<Block3> out[2]) {
+  const int c = n / 2;
+  for (int i = 1; i < n; i++)
+    for (int j = 1; j < n; j++)
+      for (int k = 1; k < n; k++) {
+        const long m[3] = {mirror(i, n), mirror(j, n), mirror(k, n)};
+        long s1 = m[0], s2 = m[1], s3 = m[2], t;
+        if (s1 > s2) { t = s1; s1 = s2; s2 = t; }
+        if (s2 > s3) { t = s2; s2 = s3; s3 = t; }
+        if (s1 > s2) { t = s1; s1 = s2; s2 = t; }
+        if (s1 != s2) continue;
+        Block3 B;
+        std::memset(&B, 0, sizeof(B));
+        B.bi = i; B.bj = j; B.bk = k;
+        B.red = ((s1 + s3) % 2) == 0;
+        B.len = (int16_t)(s1 >= 2 ? s1 - 1 : 0);
+        const int x[3] = {i, j, k};
+        if (s1 >= 2)
+          for (int a = 0; a < 3; a++) {
+            if (m[a] != s1) continue;
+            if (x[a] <= c) B.leg[B.nleg++] = (uint8_t)a;        // tip at 1
+            if (x[a] >= c) B.leg[B.nleg++] = (uint8_t)(a | 4);  // tip at n-1
+          }
+        out[B.red].push_back(B);
+      }
+}
+
+Coef3 coefs(const tmg_cube* h, int l) {
+  const int n1 = h->n[l] + 1;
+  double* p = h->coef[l];
+  return Coef3{p, p + n1, p + 2 * n1, p + 3 * n1, p + 4 * n1, p + 5 * n1};
+}
+
+int sweep3(tmg_cube* h, int l, double* u, const double* f, cudaStream_t s) {
+  const int n = h->n[l];
+  for (int red = 1; red >= 0; red--) {
+    const int nb = h->nblocks[red][l];
+    if (!nb) continue;
+    TMG_COUNT(1);
+    sweep3_kernel<<<(nb + 127) / 128, 128, 0, s>>>(n, coefs(h, l), h->blocks[red][l], nb, u, f,
+                                                   h->sb, h->sr, h->err);
+    T3(cudaGetLastError());
+  }
+  return TMG_OK;
+}
+
+dim3 grid3(int n) { return dim3((n + 1 + 255) / 256, n + 1, n + 1); }
+
+int cycle3(tmg_cube* h, int nu1, int nu2, cudaStream_t s) {
+  const int L = (int)h->n.size();
+  for (int l = 0; l < L - 1; l++) {
+    for (int k = 0; k < nu1; k++) {
+      int st = sweep3(h, l, h->U[l], h->F[l], s);
+      if (st) return st;
+    }
+    TMG_COUNT(2);
+    defect3_kernel<<<grid3(h->n[l]), 256, 0, s>>>(h->n[l], coefs(h, l), h->U[l], h->F[l], h->d,
+                                                  nullptr);
+    restrict3_kernel<<<grid3(h->n[l + 1]), 256, 0, s>>>(h->n[l], h->d, h->F[l + 1]);
+    const size_t nc = (size_t)(h->n[l + 1] + 1) * (h->n[l + 1] + 1) * (h->n[l + 1] + 1);
+    T3(cudaMemsetAsync(h->U[l + 1], 0, nc * sizeof(double), s));
+  }
+  TMG_COUNT(1);
+  coarse3_kernel<<<1, 1, 0, s>>>(coefs(h, L - 1), h->U[L - 1], h->F[L - 1]);
+  for (int l = L - 2; l >= 0; l--) {
+    TMG_COUNT(1);
+    prolong3_kernel<<<grid3(h->n[l]), 256, 0, s>>>(h->n[l + 1], h->U[l + 1], h->U[l]);
+    for (int k = 0; k < nu2; k++) {
+      int st = sweep3(h, l, h->U[l], h->F[l], s);
+      if (st) return st;
+    }
+  }
+  return cuda3(cudaGetLastError(), "cycle3");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tmg_cube_last_error(void) { return g_err3.c_str(); }
+
+// Hierarchy of cube levels from the finest 1D coordinates (n+1 values);
+// coefficients W/E, S/N, B/T from the same coordinates on every axis
+int tmg_cube_create(int n, const double* x, tmg_cube** out) {
+  if (!out || !x || n < 2 || n % 2) return fail3(TMG_BADARG, "cube needs even n >= 2");
+  tmg_cube* h = new tmg_cube();
+  std::vector<double> xs(x, x + n + 1);
+  while (true) {
+    const int m = (int)xs.size() - 1;
+    h->n.push_back(m);
+    // stencil.py:48-67 per axis
+    std::vector<double> lo(m + 1, 0.0), hi(m + 1, 0.0);
+    for (int i = 1; i < m; i++) {
+      const double dc = (xs[i + 1] - xs[i - 1]) / 2.0;
+      lo[i] = 1.0 / (dc * (xs[i] - xs[i - 1]));
+      hi[i] = 1.0 / (dc * (xs[i + 1] - xs[i]));
+    }
+    std::vector<double> all;
+    for (int rep = 0; rep < 3; rep++) {
+      all.insert(all.end(), lo.begin(), lo.end());
+      all.insert(all.end(), hi.begin(), hi.end());
+    }
+    double* dc = nullptr;
+    T3(cudaMalloc(&dc, all.size() * sizeof(double)));
+    T3(cudaMemcpy(dc, all.data(), all.size() * sizeof(double), cudaMemcpyHostToDevice));
+    h->coef.push_back(dc);
+    std::vector<Block3> bl[2];
+    build_blocks(m, bl);
+    for (int r = 0; r < 2; r++) {
+      Block3* db = nullptr;
+      if (!bl[r].empty()) {
+        T3(cudaMalloc(&db, bl[r].size() * sizeof(Block3)));
+        T3(cudaMemcpy(db, bl[r].data(), bl[r].size() * sizeof(Block3), cudaMemcpyHostToDevice));
+      }
+      h->blocks[r].push_back(db);
+      h->nblocks[r].push_back((int)bl[r].size());
+    }
+    const size_t tot = (size_t)(m + 1) * (m + 1) * (m + 1);
+    double *pu = nullptr, *pf = nullptr;
+    T3(cudaMalloc(&pu, tot * sizeof(double)));
+    T3(cudaMalloc(&pf, tot * sizeof(double)));
+    T3(cudaMemset(pu, 0, tot * sizeof(double)));
+    T3(cudaMemset(pf, 0, tot * sizeof(double)));
+    h->U.push_back(pu);
+    h->F.push_back(pf);
+    if (m % 2 || m / 2 < 2) break;
+    std::vector<double> c;
+    for (int i = 0; i <= m; i += 2) c.push_back(xs[i]);
+    xs.swap(c);
+  }
+  const size_t tot = (size_t)(n + 1) * (n + 1) * (n + 1);
+  T3(cudaMalloc(&h->sb, tot * sizeof(double)));
+  T3(cudaMalloc(&h->sr, tot * sizeof(double)));
+  T3(cudaMalloc(&h->d, tot * sizeof(double)));
+  T3(cudaMalloc(&h->err, sizeof(int) + sizeof(unsigned long long) * 2));
+  h->dmax = reinterpret_cast<unsigned long long*>(h->err + 2);
+  T3(cudaMemset(h->err, 0, sizeof(int)));
+  T3(cudaMallocHost(&h->h_err, sizeof(int) * 2 + sizeof(unsigned long long) * 2));
+  h->h_dmax = reinterpret_cast<unsigned long long*>(h->h_err + 2);
+  *out = h;
+  return TMG_OK;
+}
+
+int tmg_cube_destroy(tmg_cube* h) {
+  if (!h) return TMG_OK;
+  if (h->graph) cudaGraphExecDestroy(h->graph);
+  for (double* p : h->coef) cudaFree(p);
+  for (int r = 0; r < 2; r++)
+    for (Block3* p : h->blocks[r]) cudaFree(p);
+  for (double* p : h->U) cudaFree(p);
+  for (double* p : h->F) cudaFree(p);
+  cudaFree(h->sb);
+  cudaFree(h->sr);
+  cudaFree(h->d);
+  cudaFree(h->err);
+  cudaFreeHost(h->h_err);
+  delete h;
+  return TMG_OK;
+}
+
+int tmg_cube_levels(tmg_cube* h) { return h ? (int)h->n.size() : 0; }
+
+long tmg_cube_blocks(tmg_cube* h, int level, int red) {
+  if (!h || level < 0 || level >= (int)h->n.size()) return -1;
+  return h->nblocks[red ? 1 : 0][level];
+}
+
+// one sweep of the finest level on caller arrays u, f (device, (n+1)^3)
+int tmg_cube_sweep(tmg_cube* h, double* u, const double* f, void* stream) {
+  if (!h) return fail3(TMG_BADARG, "null cube");
+  return sweep3(h, 0, u, f, (cudaStream_t)stream);
+}
+
+// d = f - L u on the finest level (device arrays)
+int tmg_cube_defect(tmg_cube* h, const double* u, const double* f, double* d, void* stream) {
+  if (!h) return fail3(TMG_BADARG, "null cube");
+  TMG_COUNT(1);
+  defect3_kernel<<<grid3(h->n[0]), 256, 0, (cudaStream_t)stream>>>(h->n[0], coefs(h, 0), u, f, d,
+                                                                   nullptr);
+  return cuda3(cudaGetLastError(), "defect3");
+}
+
+// session: copy u, f (device, finest) in; cycles; norm; copy u out
+int tmg_cube_load(tmg_cube* h, const double* u, const double* f, void* stream) {
+  if (!h) return fail3(TMG_BADARG, "null cube");
+  const size_t tot = (size_t)(h->n[0] + 1) * (h->n[0] + 1) * (h->n[0] + 1);
+  cudaStream_t s = (cudaStream_t)stream;
+  T3(cudaMemcpyAsync(h->U[0], u, tot * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  T3(cudaMemcpyAsync(h->F[0], f, tot * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  return TMG_OK;
+}
+
+int tmg_cube_store(tmg_cube* h, double* u, void* stream) {
+  if (!h) return fail3(TMG_BADARG, "null cube");
+  const size_t tot = (size_t)(h->n[0] + 1) * (h->n[0] + 1) * (h->n[0] + 1);
+  T3(cudaMemcpyAsync(u, h->U[0], tot * sizeof(double), cudaMemcpyDeviceToDevice,
+                     (cudaStream_t)stream));
+  return TMG_OK;
+}
+
+// `reps` V(nu1, nu2) cycles on the session (CUDA graph replay)
+int tmg_cube_cycles(tmg_cube* h, int nu1, int nu2, int reps, void* stream) {
+  if (!h) return fail3(TMG_BADARG, "null cube");
+  if (nu1 < 0 || nu2 < 0 || nu1 + nu2 < 1) return fail3(TMG_BADARG, "need nu1 + nu2 >= 1");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!h->graph || h->gnu1 != nu1 || h->gnu2 != nu2) {
+    if (h->graph) cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+    cudaStream_t cs;
+    T3(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaGraph_t g;
+    const long long counted = launch_counter();
+    T3(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    int st = cycle3(h, nu1, nu2, cs);
+    cudaError_t e = cudaStreamEndCapture(cs, &g);
+    launch_counter() = counted;
+    cudaStreamDestroy(cs);
+    if (st) return st;
+    T3(e);
+    T3(cudaGraphInstantiate(&h->graph, g, 0));
+    cudaGraphDestroy(g);
+    h->gnu1 = nu1;
+    h->gnu2 = nu2;
+  }
+  for (int r = 0; r < reps; r++) T3(cudaGraphLaunch(h->graph, s));
+  return TMG_OK;
+}
+
+// finest-level max |f - L u| of the session plus the pivot flag; synchronizes
+int tmg_cube_norm(tmg_cube* h, double* out_host, void* stream) {
+  if (!h) return fail3(TMG_BADARG, "null cube");
+  cudaStream_t s = (cudaStream_t)stream;
+  T3(cudaMemsetAsync(h->dmax, 0, sizeof(unsigned long long), s));
+  TMG_COUNT(1);
+  defect3_kernel<<<grid3(h->n[0]), 256, 0, s>>>(h->n[0], coefs(h, 0), h->U[0], h->F[0], nullptr,
+                                                h->dmax);
+  T3(cudaGetLastError());
+  T3(cudaMemcpyAsync(h->h_dmax, h->dmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  T3(cudaMemcpyAsync(h->h_err, h->err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  T3(cudaMemsetAsync(h->err, 0, sizeof(int), s));
+  T3(cudaStreamSynchronize(s));
+  double v;
+  std::memcpy(&v, h->h_dmax, sizeof(v));
+  *out_host = v;
+  if (*h->h_err & 1) return fail3(TMG_SINGULAR, "zero pivot during 3D block elimination");
+  return TMG_OK;
+}
+
+}  // extern "C"
