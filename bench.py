@@ -504,13 +504,184 @@ def run_sharded(args):
     dist.destroy_process_group()
 
 
+def _cube_workload(args):
+    from paper_2110_08389_b200 import grid
+    n = args.n or 256
+    return n, grid.make_tanh_wall(n, 1.0, 3.0)
+
+
+def _cube_desc(n):
+    return (f"config4: {n + 1}^3 nodes fp64, tanh wall gamma=3 on all axes, "
+            f"f = 2 Lcg64(3) - 1, 3D tweed V(2,2), full weighting, trilinear")
+
+
+def run_cube(args):
+    """BASELINE config 4 (3D tweed, 257^3) on one GPU (replicas under torchrun)."""
+    import ctypes
+
+    import torch
+
+    from paper_2110_08389_b200 import _lib, cube, mgcycle
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local % torch.cuda.device_count())
+    n, x = _cube_workload(args)
+    h = cube.CubeHierarchy(x)
+    f = cube.config4_rhs(n)
+    u = torch.zeros_like(f)
+    L = _lib.lib()
+    stream = torch.cuda.current_stream()
+    sh = ctypes.c_void_p(stream.cuda_stream)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    cube._check(L.tmg_cube_load(h._h, P(u), P(f), sh))
+    for _ in range(max(args.warmup, 3)):
+        cube._check(L.tmg_cube_cycles(h._h, args.nu, args.nu, 1, sh))
+    torch.cuda.synchronize()
+    clk = ClockSampler(local % torch.cuda.device_count())
+    clk.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = L.tmg_kernel_launches()
+    e0.record(stream)
+    cube._check(L.tmg_cube_cycles(h._h, args.nu, args.nu, args.steps, sh))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = L.tmg_kernel_launches() - launches0
+    clocks = clk.stop()
+    t_ms = e0.elapsed_time(e1)
+    upc = 2 * args.nu * h.interior_points()
+    value = world * upc * args.steps / (t_ms * 1e-3)
+    # dominant kernel: one finest-level 3D sweep
+    ws = torch.zeros_like(f)
+    for _ in range(2):
+        cube._check(L.tmg_cube_sweep(h._h, P(ws), P(f), sh))
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(10):
+        cube._check(L.tmg_cube_sweep(h._h, P(ws), P(f), sh))
+    s1.record(stream)
+    torch.cuda.synchronize()
+    sweep_ms = s0.elapsed_time(s1) / 10
+    alg = 24.0 * (n - 1) ** 3
+    peak, peak_kind = _peak_hbm()
+    # end to end: pinned host u, f in; u out; every step (serial)
+    u_h = torch.zeros(f.shape, dtype=torch.float64).pin_memory()
+    f_h = f.cpu().pin_memory()
+    ue, fe = torch.empty_like(f), torch.empty_like(f)
+    cfg = mgcycle.CycleConfig(smoother="tweed", nu1=args.nu, nu2=args.nu)
+
+    def e2e_step():
+        fe.copy_(f_h, non_blocking=True)
+        ue.copy_(u_h, non_blocking=True)
+        cube.v_cycle(h, cfg, ue, fe)
+        u_h.copy_(ue, non_blocking=True)
+    e2e_step()
+    torch.cuda.synchronize()
+    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ke = max(1, min(args.steps, 5))
+    x0.record(stream)
+    for _ in range(ke):
+        e2e_step()
+    x1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = x0.elapsed_time(x1) / ke
+    fb = f.numel() * 8
+    solve = None
+    if not args.no_solve:
+        cfg_s = mgcycle.CycleConfig(smoother="tweed", nu1=args.nu, nu2=args.nu, tol=1e-10)
+        torch.cuda.synchronize()
+        z0, z1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        z0.record(stream)
+        _, rep = cube.solve(h, cfg_s, f)
+        z1.record(stream)
+        torch.cuda.synchronize()
+        solve = {"tol": 1e-10, "cycles": rep.cycles, "converged": rep.converged,
+                 "ms": z0.elapsed_time(z1), "final_rel_defect": rep.final_rel_defect}
+    line = {
+        "metric": "smoother grid-pt updates/s", "value": value, "unit": "grid-pt updates/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": _cube_desc(n), "levels": h.levels, "updates_per_cycle": upc,
+                   "vcycle_ms": t_ms / args.steps,
+                   "l2": "inputs larger than L2 (u, f = 2 x %.0f MB)" % (fb / 1e6),
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": alg / (sweep_ms * 1e-3) / 1e9, "peak": peak,
+                     "unit": "GB/s", "frac": alg / (sweep_ms * 1e-3) / 1e9 / peak,
+                     "traffic": None, "kernel": "sweep3_kernel (one finest-level 3D sweep)",
+                     "alg_bytes": alg, "ms": sweep_ms, "peak_kind": peak_kind},
+        "solve": solve,
+        "e2e": {"value": world * upc / (e2e_ms * 1e-3), "unit": "grid-pt updates/s",
+                "h2d_bytes_per_step": 2 * fb, "d2h_bytes_per_step": fb, "ms_per_step": e2e_ms},
+        "clocks": clocks,
+        "gpu_launches": launches,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import oracle3d as o3
+        H = o3.Hierarchy3(x.values)
+        fh = f.cpu().numpy()
+        uo = np.zeros_like(fh)
+        t0 = time.perf_counter()
+        o3.v_cycle(H, uo, fh, args.nu, args.nu, 1)
+        secs = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": upc / secs, "unit": "grid-pt updates/s", "cores": 1,
+                                "kind": "port",
+                                "sample": f"one V({args.nu},{args.nu}) cycle of the same workload, "
+                                          f"3D C oracle, 1 thread ({secs:.1f} s)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_cube_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return
+    from oracle import oracle as orc
+    from oracle import oracle3d as o3
+    from paper_2110_08389_b200 import cube
+    n, x = _cube_workload(args)
+    H = o3.Hierarchy3(x.values)
+    f = cube.config4_rhs(n, device=False)
+    cores = orc.max_threads()
+    times = []
+    for k in range(args.warmup + args.steps):
+        u = np.zeros_like(f)
+        t0 = time.perf_counter()
+        o3.v_cycle(H, u, f, args.nu, args.nu, cores)
+        if k >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    per = float(np.mean(times))
+    pts, m = 0, n
+    while True:
+        pts += (m - 1) ** 3
+        if m % 2 or m // 2 < 2:
+            break
+        m //= 2
+    value = 2 * args.nu * pts / per
+    line = {
+        "impl": "reference", "metric": "smoother grid-pt updates/s", "value": value,
+        "unit": "grid-pt updates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": _cube_desc(n)},
+        "cpu_baseline": {"value": value, "unit": "grid-pt updates/s", "cores": cores,
+                         "kind": "port",
+                         "sample": f"one V({args.nu},{args.nu}) cycle per step, 3D C oracle, "
+                                   f"{cores} OpenMP threads"},
+        "e2e": {"value": value, "unit": "grid-pt updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    p.add_argument("--config", default="config3", choices=("config1", "config2", "config3"))
+    p.add_argument("--config", default="config3",
+                   choices=("config1", "config2", "config3", "config4"))
     p.add_argument("--intervals", "--n", dest="n", type=int, default=None,
                    help="override grid intervals (use --intervals under torchrun)")
     p.add_argument("--nu", type=int, default=2, help="config3: V(nu,nu)")
@@ -521,7 +692,12 @@ def main():
     args = p.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.config == "config4":
+        if args.impl == "reference":
+            run_cube_reference(args)
+        else:
+            run_cube(args)
+    elif args.impl == "reference":
         run_reference(args)
     elif _dist()[0] > 1 and not args.replicas:
         run_sharded(args)

@@ -9,11 +9,12 @@
 // mirrored coordinates, red = even.  Its checker is the CPU restatement in
 // oracle/tweed3d_oracle.c.
 //
-// Fields are C-order (n+1)^3 with k fastest.  The block solver runs one
-// thread per block (blocks enumerated with k fastest, so neighbouring
-// threads walk neighbouring lines); each leg's forward-eliminated pivots and
-// right-hand sides go to two field-sized scratch arrays, read back by the
-// back substitution.
+// Fields are C-order (n+1)^3 with k fastest.  A colour stage is leg
+// parallel: one thread per leg eliminates it toward its branch (pivots and
+// right-hand sides to two field-sized scratch arrays), one thread per block
+// solves the branch row, one thread per leg back-substitutes.  Blocks and
+// legs are enumerated with k fastest, so neighbouring threads walk
+// neighbouring lines.
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -35,6 +36,16 @@ struct Block3 {
   uint8_t pad[2];
 };
 static_assert(sizeof(Block3) == 24, "Block3 layout");
+
+// one leg of a block (the leg-parallel sweep: one thread per leg)
+struct Leg3 {
+  int32_t block;    // index in the colour's block list
+  int32_t bi, bj, bk;
+  int16_t len;
+  uint8_t code;     // bits 0-1 axis, bit 2: step -1
+  uint8_t slot;     // leg index within the block
+};
+static_assert(sizeof(Leg3) == 20, "Leg3 layout");
 
 __host__ __device__ inline long mirror(long x, long n) { return x < n - x ? x : n - x; }
 
@@ -72,12 +83,56 @@ __device__ __forceinline__ double rhs3(const Coef3& c, int n, const double* __re
   return r;
 }
 
-// one colour stage: thread b solves block b of the colour's list
-__global__ void __launch_bounds__(128) sweep3_kernel(int n, Coef3 c, const Block3* __restrict__ blocks,
-                                                     int nb, double* __restrict__ u,
+// Leg-parallel colour stage, three launches: (1) every leg's forward
+// elimination (pivots / rhs to the scratch arrays, its contribution to the
+// branch row into contrib), (2) every branch: num / den in leg order, the
+// branch value, (3) every leg's back substitution from its branch.
+__global__ void __launch_bounds__(128) legs_forward_kernel(int n, Coef3 c, const Leg3* __restrict__ legs,
+                                                           int nl, const double* __restrict__ u,
+                                                           const double* __restrict__ f,
+                                                           double* __restrict__ sb,
+                                                           double* __restrict__ sr,
+                                                           double2* __restrict__ contrib, int* err) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= nl) return;
+  const Leg3 G = legs[l];
+  const int a = G.code & 3, s = (G.code & 4) ? -1 : 1;
+  const int tip = s > 0 ? 1 : n - 1;
+  double bp = 0.0, rp = 0.0, cprev = 0.0;
+  bool bad = false;
+  for (int t = 0; t < G.len; t++) {
+    const int i = a == 0 ? tip + s * t : G.bi;
+    const int j = a == 1 ? tip + s * t : G.bj;
+    const int k = a == 2 ? tip + s * t : G.bk;
+    unsigned skip = dbit(a, s);
+    if (t > 0) skip |= dbit(a, -s);
+    const double r = rhs3(c, n, u, f, i, j, k, skip);
+    const double bb = diag3(c, i, j, k);
+    if (t == 0) {
+      bp = bb;
+      rp = r;
+    } else {
+      bad |= bp > -1e-300 && bp < 1e-300;
+      const double w = cpl3(c, a, -s, i, j, k) / bp;
+      bp = bb - w * cprev;
+      rp = r - w * rp;
+    }
+    cprev = cpl3(c, a, s, i, j, k);
+    const size_t o = idx3(n, i, j, k);
+    sb[o] = bp;
+    sr[o] = rp;
+  }
+  const double d = cpl3(c, a, -s, G.bi, G.bj, G.bk);
+  bad |= bp > -1e-300 && bp < 1e-300;
+  contrib[l] = make_double2(d * rp / bp, d * cprev / bp);
+  if (bad) atomicOr(err, 1);
+}
+
+__global__ void __launch_bounds__(128) branch_kernel(int n, Coef3 c, const Block3* __restrict__ blocks,
+                                                     const int* __restrict__ leg0, int nb,
+                                                     double* __restrict__ u,
                                                      const double* __restrict__ f,
-                                                     double* __restrict__ sb,
-                                                     double* __restrict__ sr, int* err) {
+                                                     const double2* __restrict__ contrib, int* err) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= nb) return;
   const Block3 B = blocks[b];
@@ -88,58 +143,34 @@ __global__ void __launch_bounds__(128) sweep3_kernel(int n, Coef3 c, const Block
   }
   double num = rhs3(c, n, u, f, B.bi, B.bj, B.bk, bskip);
   double den = diag3(c, B.bi, B.bj, B.bk);
-  bool bad = false;
-  const int L = B.len;
-  for (int l = 0; l < B.nleg; l++) {
-    const int a = B.leg[l] & 3, s = (B.leg[l] & 4) ? -1 : 1;
-    const int tip = s > 0 ? 1 : n - 1;
-    double bp = 0.0, rp = 0.0, cprev = 0.0;
-    for (int t = 0; t < L; t++) {
-      const int i = a == 0 ? tip + s * t : B.bi;
-      const int j = a == 1 ? tip + s * t : B.bj;
-      const int k = a == 2 ? tip + s * t : B.bk;
-      unsigned skip = dbit(a, s);
-      if (t > 0) skip |= dbit(a, -s);
-      const double r = rhs3(c, n, u, f, i, j, k, skip);
-      const double bb = diag3(c, i, j, k);
-      if (t == 0) {
-        bp = bb;
-        rp = r;
-      } else {
-        bad |= bp > -1e-300 && bp < 1e-300;
-        const double w = cpl3(c, a, -s, i, j, k) / bp;
-        bp = bb - w * cprev;
-        rp = r - w * rp;
-      }
-      cprev = cpl3(c, a, s, i, j, k);
-      const size_t o = idx3(n, i, j, k);
-      sb[o] = bp;
-      sr[o] = rp;
+  if (B.len > 0)
+    for (int l = 0; l < B.nleg; l++) {
+      const double2 q = contrib[leg0[b] + l];
+      num -= q.x;
+      den -= q.y;
     }
-    if (L > 0) {
-      const double d = cpl3(c, a, -s, B.bi, B.bj, B.bk);
-      bad |= bp > -1e-300 && bp < 1e-300;
-      num -= d * rp / bp;
-      den -= d * cprev / bp;
-    }
+  if (den > -1e-300 && den < 1e-300) atomicOr(err, 1);
+  u[idx3(n, B.bi, B.bj, B.bk)] = num / den;
+}
+
+__global__ void __launch_bounds__(128) legs_back_kernel(int n, Coef3 c, const Leg3* __restrict__ legs,
+                                                        int nl, double* __restrict__ u,
+                                                        const double* __restrict__ sb,
+                                                        const double* __restrict__ sr) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= nl) return;
+  const Leg3 G = legs[l];
+  const int a = G.code & 3, s = (G.code & 4) ? -1 : 1;
+  const int tip = s > 0 ? 1 : n - 1;
+  double x = u[idx3(n, G.bi, G.bj, G.bk)];
+  for (int t = G.len - 1; t >= 0; t--) {
+    const int i = a == 0 ? tip + s * t : G.bi;
+    const int j = a == 1 ? tip + s * t : G.bj;
+    const int k = a == 2 ? tip + s * t : G.bk;
+    const size_t o = idx3(n, i, j, k);
+    x = (sr[o] - cpl3(c, a, s, i, j, k) * x) / sb[o];
+    u[o] = x;
   }
-  bad |= den > -1e-300 && den < 1e-300;
-  const double xb = num / den;
-  u[idx3(n, B.bi, B.bj, B.bk)] = xb;
-  for (int l = 0; l < B.nleg; l++) {
-    const int a = B.leg[l] & 3, s = (B.leg[l] & 4) ? -1 : 1;
-    const int tip = s > 0 ? 1 : n - 1;
-    double x = xb;
-    for (int t = L - 1; t >= 0; t--) {
-      const int i = a == 0 ? tip + s * t : B.bi;
-      const int j = a == 1 ? tip + s * t : B.bj;
-      const int k = a == 2 ? tip + s * t : B.bk;
-      const size_t o = idx3(n, i, j, k);
-      x = (sr[o] - cpl3(c, a, s, i, j, k) * x) / sb[o];
-      u[o] = x;
-    }
-  }
-  if (bad) atomicOr(err, 1);
 }
 
 // d = f - L u (interior), 0 on the boundary; or the max |f - L u| into dmax
@@ -236,6 +267,10 @@ struct tmg_cube {
   std::vector<double*> coef;          // per level: W E S N B T (6 (n+1))
   std::vector<Block3*> blocks[2];     // per level: black, red lists
   std::vector<int> nblocks[2];
+  std::vector<Leg3*> legs[2];         // per level and colour: legs of the blocks
+  std::vector<int*> leg0[2];          // first leg of every block
+  std::vector<int> nlegs[2];
+  double2* contrib = nullptr;         // per leg (sized for the finest level)
   std::vector<double*> U, F;          // per level work fields (level 0: session)
   double *sb = nullptr, *sr = nullptr, *d = nullptr;  // finest-size scratch
   int* err = nullptr;
@@ -244,6 +279,7 @@ struct tmg_cube {
   unsigned long long* h_dmax = nullptr;
   cudaGraphExec_t graph = nullptr;
   int gnu1 = -1, gnu2 = -1;
+  int graph_kernels = 0;
 };
 
 namespace {
@@ -293,11 +329,21 @@ Coef3 coefs(const tmg_cube* h, int l) {
 int sweep3(tmg_cube* h, int l, double* u, const double* f, cudaStream_t s) {
   const int n = h->n[l];
   for (int red = 1; red >= 0; red--) {
-    const int nb = h->nblocks[red][l];
+    const int nb = h->nblocks[red][l], nl = h->nlegs[red][l];
     if (!nb) continue;
+    if (nl) {
+      TMG_COUNT(1);
+      legs_forward_kernel<<<(nl + 127) / 128, 128, 0, s>>>(n, coefs(h, l), h->legs[red][l], nl,
+                                                           u, f, h->sb, h->sr, h->contrib, h->err);
+    }
     TMG_COUNT(1);
-    sweep3_kernel<<<(nb + 127) / 128, 128, 0, s>>>(n, coefs(h, l), h->blocks[red][l], nb, u, f,
-                                                   h->sb, h->sr, h->err);
+    branch_kernel<<<(nb + 127) / 128, 128, 0, s>>>(n, coefs(h, l), h->blocks[red][l],
+                                                   h->leg0[red][l], nb, u, f, h->contrib, h->err);
+    if (nl) {
+      TMG_COUNT(1);
+      legs_back_kernel<<<(nl + 127) / 128, 128, 0, s>>>(n, coefs(h, l), h->legs[red][l], nl, u,
+                                                        h->sb, h->sr);
+    }
     T3(cudaGetLastError());
   }
   return TMG_OK;
@@ -373,6 +419,28 @@ int tmg_cube_create(int n, const double* x, tmg_cube** out) {
       }
       h->blocks[r].push_back(db);
       h->nblocks[r].push_back((int)bl[r].size());
+      std::vector<Leg3> lg;
+      std::vector<int> l0;
+      for (size_t b = 0; b < bl[r].size(); b++) {
+        const Block3& B = bl[r][b];
+        l0.push_back((int)lg.size());
+        if (B.len == 0) continue;
+        for (int q = 0; q < B.nleg; q++)
+          lg.push_back(Leg3{(int32_t)b, B.bi, B.bj, B.bk, B.len, B.leg[q], (uint8_t)q});
+      }
+      Leg3* dl = nullptr;
+      int* d0 = nullptr;
+      if (!lg.empty()) {
+        T3(cudaMalloc(&dl, lg.size() * sizeof(Leg3)));
+        T3(cudaMemcpy(dl, lg.data(), lg.size() * sizeof(Leg3), cudaMemcpyHostToDevice));
+      }
+      if (!l0.empty()) {
+        T3(cudaMalloc(&d0, l0.size() * sizeof(int)));
+        T3(cudaMemcpy(d0, l0.data(), l0.size() * sizeof(int), cudaMemcpyHostToDevice));
+      }
+      h->legs[r].push_back(dl);
+      h->leg0[r].push_back(d0);
+      h->nlegs[r].push_back((int)lg.size());
     }
     const size_t tot = (size_t)(m + 1) * (m + 1) * (m + 1);
     double *pu = nullptr, *pf = nullptr;
@@ -388,6 +456,10 @@ int tmg_cube_create(int n, const double* x, tmg_cube** out) {
     xs.swap(c);
   }
   const size_t tot = (size_t)(n + 1) * (n + 1) * (n + 1);
+  int maxlegs = 1;
+  for (int r = 0; r < 2; r++)
+    for (int v : h->nlegs[r]) maxlegs = v > maxlegs ? v : maxlegs;
+  T3(cudaMalloc(&h->contrib, maxlegs * sizeof(double2)));
   T3(cudaMalloc(&h->sb, tot * sizeof(double)));
   T3(cudaMalloc(&h->sr, tot * sizeof(double)));
   T3(cudaMalloc(&h->d, tot * sizeof(double)));
@@ -404,8 +476,12 @@ int tmg_cube_destroy(tmg_cube* h) {
   if (!h) return TMG_OK;
   if (h->graph) cudaGraphExecDestroy(h->graph);
   for (double* p : h->coef) cudaFree(p);
-  for (int r = 0; r < 2; r++)
+  for (int r = 0; r < 2; r++) {
     for (Block3* p : h->blocks[r]) cudaFree(p);
+    for (Leg3* p : h->legs[r]) cudaFree(p);
+    for (int* p : h->leg0[r]) cudaFree(p);
+  }
+  cudaFree(h->contrib);
   for (double* p : h->U) cudaFree(p);
   for (double* p : h->F) cudaFree(p);
   cudaFree(h->sb);
@@ -476,12 +552,25 @@ int tmg_cube_cycles(tmg_cube* h, int nu1, int nu2, int reps, void* stream) {
     cudaStreamDestroy(cs);
     if (st) return st;
     T3(e);
+    size_t nn = 0;
+    T3(cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    T3(cudaGraphGetNodes(g, nodes.data(), &nn));
+    h->graph_kernels = 0;
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      T3(cudaGraphNodeGetType(nd, &t));
+      h->graph_kernels += t == cudaGraphNodeTypeKernel;
+    }
     T3(cudaGraphInstantiate(&h->graph, g, 0));
     cudaGraphDestroy(g);
     h->gnu1 = nu1;
     h->gnu2 = nu2;
   }
-  for (int r = 0; r < reps; r++) T3(cudaGraphLaunch(h->graph, s));
+  for (int r = 0; r < reps; r++) {
+    T3(cudaGraphLaunch(h->graph, s));
+    TMG_COUNT(h->graph_kernels);
+  }
   return TMG_OK;
 }
 
