@@ -160,17 +160,31 @@ void wireframe(Builder& B, int nx, int ny) {
   }
 }
 
-// smoothers.py:77-89
+// smoothers.py:77-89.  A line longer than one CTA holds at q = 16 (kThreads
+// * kQmax points) is solved as a two-legged block around its middle point
+// (legs from both walls toward it): the same exact line solve, eliminated
+// from both ends, so its two halves sit in different CTAs of a cluster
+// without a reduced system spanning them.
 void zebra(Builder& B, int nx, int ny, bool axis_x) {
-  if (axis_x) {
-    for (int j = 1; j < ny; j++) {
-      int l = B.new_block(j % 2, -1, -1);
-      B.straight_leg(l, 1, j, DE, nx - 1, false);
+  const int len = axis_x ? nx - 1 : ny - 1;
+  const bool split = len > kThreads * kQmax;
+  const int h = (len + 1) / 2;  // hub: point h of the line (1-based)
+  for (int t = 1; t < (axis_x ? ny : nx); t++) {
+    const int red = t % 2;
+    if (!split) {
+      int l = B.new_block(red, -1, -1);
+      if (axis_x) B.straight_leg(l, 1, t, DE, len, false);
+      else B.straight_leg(l, t, 1, DN, len, false);
+      continue;
     }
-  } else {
-    for (int i = 1; i < nx; i++) {
-      int l = B.new_block(i % 2, -1, -1);
-      B.straight_leg(l, i, 1, DN, ny - 1, false);
+    if (axis_x) {
+      int b = B.new_block(red, h, t);
+      B.straight_leg(b, 1, t, DE, h - 1, true);
+      B.straight_leg(b, len, t, DW, len - h, true);
+    } else {
+      int b = B.new_block(red, t, h);
+      B.straight_leg(b, t, 1, DN, h - 1, true);
+      B.straight_leg(b, t, len, DS, len - h, true);
     }
   }
 }

@@ -160,6 +160,23 @@ def test_wireframe_8193_sweep_and_cycle(cuda, orc):
     assert _rel(ug.cpu().numpy(), uo) <= 1e-10
 
 
+@pytest.mark.parametrize("kind", ["zebra_x", "zebra_y"])
+def test_zebra_8193_sweep(cuda, orc, kind):
+    """Lines of 8191 points exceed one CTA: each runs as a two-legged block
+    around its middle point; one sweep against the oracle's line Thomas."""
+    n = 8192
+    x = grid.make_coords("wall", n, 1.0, 4.0)
+    st = stencil.assemble(x, x)
+    f = np.zeros((n + 1, n + 1))
+    f[1:-1, 1:-1] = Lcg64(9).fill((n - 1, n - 1)) - 0.5
+    fd = cuda.from_numpy(f).cuda()
+    u = cuda.zeros_like(fd)
+    smoothers.sweep(kind, st, smoothers.PlanBundle(n, n), u, fd)
+    uo = np.zeros_like(f)
+    orc.sweep(kind, (st.W, st.E, st.S, st.N), uo, f, orc.max_threads())
+    assert _rel(u.cpu().numpy(), uo) <= 1e-10
+
+
 @pytest.mark.parametrize("nu", [1, 2])
 def test_config3_convergence_factors(cuda, orc, config3, nu):
     """20 cycles at tol=1e-300 (cli.py:120): the per-cycle ratios of the first
