@@ -15,6 +15,7 @@
 // solves the branch row, one thread per leg back-substitutes.  Blocks and
 // legs are enumerated with k fastest, so neighbouring threads walk
 // neighbouring lines.
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -39,7 +40,7 @@ static_assert(sizeof(Block3) == 24, "Block3 layout");
 
 // one leg of a block (the leg-parallel sweep: one thread per leg)
 struct Leg3 {
-  int32_t block;    // index in the colour's block list
+  int32_t ci;       // contribution slot (the leg's index in the colour's leg list)
   int32_t bi, bj, bk;
   int16_t len;
   uint8_t code;     // bits 0-1 axis, bit 2: step -1
@@ -124,8 +125,176 @@ __global__ void __launch_bounds__(128) legs_forward_kernel(int n, Coef3 c, const
   }
   const double d = cpl3(c, a, -s, G.bi, G.bj, G.bk);
   bad |= bp > -1e-300 && bp < 1e-300;
-  contrib[l] = make_double2(d * rp / bp, d * cprev / bp);
+  contrib[G.ci] = make_double2(d * rp / bp, d * cprev / bp);
   if (bad) atomicOr(err, 1);
+}
+
+// Legs along k (the contiguous axis): one warp per leg, lanes along the leg
+// (coalesced), QK points per lane.  Each lane eliminates its chunk to its
+// last point (x = alpha + beta * X_left + gamma * X_end for the others), the
+// chunk ends form a tridiagonal system solved by warp PCR with two
+// right-hand sides (data, coupling to the branch), and every point is left
+// as x = A + G * x_branch in the scratch arrays (A in sb, G in sr) for the
+// back kernel.  2D analogue: tmg_sweep.cu phases B and C.
+template <int QK>
+__global__ void __launch_bounds__(128) kleg_forward_kernel(int n, Coef3 c, const Leg3* __restrict__ legs,
+                                                           int nl, const double* __restrict__ u,
+                                                           const double* __restrict__ f,
+                                                           double* __restrict__ sb,
+                                                           double* __restrict__ sr,
+                                                           double2* __restrict__ contrib, int* err) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= nl) return;
+  constexpr unsigned FULL = 0xffffffffu;
+  const Leg3 G = legs[w];
+  const int s = (G.code & 4) ? -1 : 1, tip = s > 0 ? 1 : n - 1;
+  const int L = G.len, q = (L + 31) / 32;
+  const int p0 = lane * q, cnt = max(0, min(q, L - p0));  // this lane's points
+  const int i = G.bi, j = G.bj;
+  double rho[QK], lam[QK], ivr[QK], cc[QK];
+  bool bad = false;
+  // frozen right-hand sides and couplings; the chunk is eliminated toward its
+  // last point, keeping the coupling to the previous lane's last point (lam)
+  double bp = 0.0, rp = 0.0, lm = 0.0, cprev = 0.0, a_first = 0.0;
+  double r_end = 0.0, b_end = 1.0, a_end = 0.0, c_end = 0.0;  // the chunk end's raw row
+  const int nI = cnt - 1;
+#pragma unroll
+  for (int t = 0; t < QK; t++) {
+    if (t > nI) continue;
+    const int p = p0 + t, k = tip + s * p;
+    unsigned skip = dbit(2, s);
+    if (p > 0) skip |= dbit(2, -s);
+    const double r = rhs3(c, n, u, f, i, j, k, skip);
+    const double bb = diag3(c, i, j, k);
+    const double am = p > 0 ? cpl3(c, 2, -s, i, j, k) : 0.0;
+    cc[t] = cpl3(c, 2, s, i, j, k);
+    if (t == 0) a_first = am;
+    if (t == nI) {  // the chunk end: its raw row, kept for the reduced system
+      r_end = r;
+      b_end = bb;
+      a_end = am;
+      c_end = cc[t];
+      continue;
+    }
+    if (t == 0) {
+      bp = bb;
+      rp = r;
+      lm = -am;
+    } else {
+      const double wv = am / bp;
+      bp = bb - wv * cprev;
+      rp = r - wv * rp;
+      lm = -wv * lm;
+    }
+    bad |= bp > -1e-300 && bp < 1e-300;
+    rho[t] = rp;
+    lam[t] = lm;
+    ivr[t] = 1.0 / bp;
+    cprev = cc[t];
+  }
+  // back pass over the interior: x_t = alpha + beta Xl + gamma Xe
+  double ad = 0.0, bd = 1.0, gd = 0.0, au = 0.0, bu = 0.0, gu = 1.0;
+  if (nI > 0) {
+    double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+    for (int t = QK - 1; t >= 0; t--) {
+      if (t >= nI) continue;
+      if (t == nI - 1) {
+        al = rho[t] * ivr[t];
+        be = lam[t] * ivr[t];
+        ga = -cc[t] * ivr[t];
+        ad = al; bd = be; gd = ga;
+      } else {
+        al = (rho[t] - cc[t] * al) * ivr[t];
+        be = (lam[t] - cc[t] * be) * ivr[t];
+        ga = -cc[t] * ga * ivr[t];
+      }
+      rho[t] = al;
+      lam[t] = be;
+      ivr[t] = ga;
+    }
+    au = al; bu = be; gu = ga;
+  }
+  // reduced row of the chunk end: A X_prevend + B X + C X_nextend + H xb = D
+  double A = 0.0, B = 1.0, Cc = 0.0, D = 0.0, H = 0.0;
+  const double an = __shfl_down_sync(FULL, au, 1), bn = __shfl_down_sync(FULL, bu, 1);
+  const double gn = __shfl_down_sync(FULL, gu, 1);
+  const int cnt_next = __shfl_down_sync(FULL, cnt, 1);
+  if (cnt > 0) {
+    const double ae = nI > 0 ? a_end : a_first;  // raw coupling toward the previous point
+    const double re = r_end, be_ = b_end, ce = c_end;
+    if (nI > 0) {  // the previous point is x_{nI-1} = ad + bd Xl + gd X
+      A = ae * bd;
+      B = be_ + ae * gd;
+      D = re - ae * ad;
+    } else {  // a one-point chunk: the previous point is the previous lane's end
+      A = ae;
+      B = be_;
+      D = re;
+    }
+    const bool last = p0 + cnt == L;
+    if (!last && cnt_next > 0) {  // next point = next lane's first = an + bn X + gn Xn
+      B += ce * bn;
+      Cc = ce * gn;
+      D -= ce * an;
+    } else if (last) {
+      H = ce;  // coupling to the branch
+    }
+    if (lane == 0) A = 0.0;
+  }
+  for (int d = 1; d < 32; d <<= 1) {
+    double Am = __shfl_up_sync(FULL, A, d), Bm = __shfl_up_sync(FULL, B, d);
+    double Cm = __shfl_up_sync(FULL, Cc, d), Dm = __shfl_up_sync(FULL, D, d);
+    double Hm = __shfl_up_sync(FULL, H, d);
+    double Ap = __shfl_down_sync(FULL, A, d), Bp = __shfl_down_sync(FULL, B, d);
+    double Cp = __shfl_down_sync(FULL, Cc, d), Dp = __shfl_down_sync(FULL, D, d);
+    double Hp = __shfl_down_sync(FULL, H, d);
+    if (lane < d) { Am = 0.0; Bm = 1.0; Cm = 0.0; Dm = 0.0; Hm = 0.0; }
+    if (lane + d > 31) { Ap = 0.0; Bp = 1.0; Cp = 0.0; Dp = 0.0; Hp = 0.0; }
+    const double k1 = A / Bm, k2 = Cc / Bp;
+    A = -k1 * Am;
+    B = B - k1 * Cm - k2 * Ap;
+    D = D - k1 * Dm - k2 * Dp;
+    H = H - k1 * Hm - k2 * Hp;
+    Cc = -k2 * Cp;
+  }
+  bad |= cnt > 0 && B > -1e-300 && B < 1e-300;
+  const double P = D / B, Qh = H / B;  // X_end = P - Qh xb
+  const double Pl = __shfl_up_sync(FULL, P, 1), Ql = __shfl_up_sync(FULL, Qh, 1);
+  const double PL = lane > 0 ? Pl : 0.0, QL = lane > 0 ? Ql : 0.0;
+  // every point as A' + G' xb
+#pragma unroll
+  for (int t = 0; t < QK; t++) {
+    if (t > nI) continue;
+    const size_t o = idx3(n, i, j, tip + s * (p0 + t));
+    if (t == nI) {
+      sb[o] = P;
+      sr[o] = -Qh;
+    } else {
+      sb[o] = rho[t] + lam[t] * PL + ivr[t] * P;
+      sr[o] = -(lam[t] * QL + ivr[t] * Qh);
+    }
+  }
+  if (cnt > 0 && p0 + cnt == L) {
+    const double d = cpl3(c, 2, -s, G.bi, G.bj, G.bk);
+    contrib[G.ci] = make_double2(d * P, d * Qh);
+  }
+  if (bad) atomicOr(err, 1);
+}
+
+__global__ void __launch_bounds__(128) kleg_back_kernel(int n, const Leg3* __restrict__ legs, int nl,
+                                                        double* __restrict__ u,
+                                                        const double* __restrict__ sb,
+                                                        const double* __restrict__ sr) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= nl) return;
+  const Leg3 G = legs[w];
+  const int s = (G.code & 4) ? -1 : 1, tip = s > 0 ? 1 : n - 1;
+  const double xb = u[idx3(n, G.bi, G.bj, G.bk)];
+  for (int p = lane; p < G.len; p += 32) {
+    const size_t o = idx3(n, G.bi, G.bj, tip + s * p);
+    u[o] = sb[o] + sr[o] * xb;
+  }
 }
 
 __global__ void __launch_bounds__(128) branch_kernel(int n, Coef3 c, const Block3* __restrict__ blocks,
@@ -270,7 +439,10 @@ struct tmg_cube {
   std::vector<Leg3*> legs[2];         // per level and colour: legs of the blocks
   std::vector<int*> leg0[2];          // first leg of every block
   std::vector<int> nlegs[2];
-  double2* contrib = nullptr;         // per leg (sized for the finest level)
+  std::vector<Leg3*> klegs[2];        // legs along k (warp per leg)
+  std::vector<int> nklegs[2];
+  int ncontrib = 1;
+  double2* contrib = nullptr;         // per leg (sized for the largest level)
   std::vector<double*> U, F;          // per level work fields (level 0: session)
   double *sb = nullptr, *sr = nullptr, *d = nullptr;  // finest-size scratch
   int* err = nullptr;
@@ -329,12 +501,22 @@ Coef3 coefs(const tmg_cube* h, int l) {
 int sweep3(tmg_cube* h, int l, double* u, const double* f, cudaStream_t s) {
   const int n = h->n[l];
   for (int red = 1; red >= 0; red--) {
-    const int nb = h->nblocks[red][l], nl = h->nlegs[red][l];
+    const int nb = h->nblocks[red][l], nl = h->nlegs[red][l], nk = h->nklegs[red][l];
     if (!nb) continue;
     if (nl) {
       TMG_COUNT(1);
       legs_forward_kernel<<<(nl + 127) / 128, 128, 0, s>>>(n, coefs(h, l), h->legs[red][l], nl,
                                                            u, f, h->sb, h->sr, h->contrib, h->err);
+    }
+    if (nk) {
+      TMG_COUNT(1);
+      const int grid = (nk * 32 + 127) / 128;
+      if (n / 2 - 1 <= 4 * 32)  // the longest leg has n/2 - 1 points
+        kleg_forward_kernel<4><<<grid, 128, 0, s>>>(n, coefs(h, l), h->klegs[red][l], nk, u, f,
+                                                    h->sb, h->sr, h->contrib, h->err);
+      else
+        kleg_forward_kernel<8><<<grid, 128, 0, s>>>(n, coefs(h, l), h->klegs[red][l], nk, u, f,
+                                                    h->sb, h->sr, h->contrib, h->err);
     }
     TMG_COUNT(1);
     branch_kernel<<<(nb + 127) / 128, 128, 0, s>>>(n, coefs(h, l), h->blocks[red][l],
@@ -343,6 +525,11 @@ int sweep3(tmg_cube* h, int l, double* u, const double* f, cudaStream_t s) {
       TMG_COUNT(1);
       legs_back_kernel<<<(nl + 127) / 128, 128, 0, s>>>(n, coefs(h, l), h->legs[red][l], nl, u,
                                                         h->sb, h->sr);
+    }
+    if (nk) {
+      TMG_COUNT(1);
+      kleg_back_kernel<<<(nk * 32 + 127) / 128, 128, 0, s>>>(n, h->klegs[red][l], nk, u, h->sb,
+                                                             h->sr);
     }
     T3(cudaGetLastError());
   }
@@ -419,14 +606,21 @@ int tmg_cube_create(int n, const double* x, tmg_cube** out) {
       }
       h->blocks[r].push_back(db);
       h->nblocks[r].push_back((int)bl[r].size());
-      std::vector<Leg3> lg;
+      std::vector<Leg3> lg, lk;  // legs along i / j (thread per leg), along k (warp per leg)
       std::vector<int> l0;
+      int ci = 0;
+      // k legs of levels up to 129^3 run warp-per-leg (measured faster there:
+      // 0.53 -> 0.30 ms per sweep at 129^3); at 257^3 the thread-per-leg path
+      // is faster (0.99 vs 1.09 ms)
+      const bool warp_k = m / 2 - 1 <= 64;
       for (size_t b = 0; b < bl[r].size(); b++) {
         const Block3& B = bl[r][b];
-        l0.push_back((int)lg.size());
+        l0.push_back(ci);
         if (B.len == 0) continue;
-        for (int q = 0; q < B.nleg; q++)
-          lg.push_back(Leg3{(int32_t)b, B.bi, B.bj, B.bk, B.len, B.leg[q], (uint8_t)q});
+        for (int q = 0; q < B.nleg; q++) {
+          const Leg3 G{ci++, B.bi, B.bj, B.bk, B.len, B.leg[q], (uint8_t)q};
+          ((B.leg[q] & 3) == 2 && warp_k ? lk : lg).push_back(G);
+        }
       }
       Leg3* dl = nullptr;
       int* d0 = nullptr;
@@ -441,6 +635,14 @@ int tmg_cube_create(int n, const double* x, tmg_cube** out) {
       h->legs[r].push_back(dl);
       h->leg0[r].push_back(d0);
       h->nlegs[r].push_back((int)lg.size());
+      Leg3* dk = nullptr;
+      if (!lk.empty()) {
+        T3(cudaMalloc(&dk, lk.size() * sizeof(Leg3)));
+        T3(cudaMemcpy(dk, lk.data(), lk.size() * sizeof(Leg3), cudaMemcpyHostToDevice));
+      }
+      h->klegs[r].push_back(dk);
+      h->nklegs[r].push_back((int)lk.size());
+      h->ncontrib = std::max(h->ncontrib, ci);
     }
     const size_t tot = (size_t)(m + 1) * (m + 1) * (m + 1);
     double *pu = nullptr, *pf = nullptr;
@@ -456,10 +658,7 @@ int tmg_cube_create(int n, const double* x, tmg_cube** out) {
     xs.swap(c);
   }
   const size_t tot = (size_t)(n + 1) * (n + 1) * (n + 1);
-  int maxlegs = 1;
-  for (int r = 0; r < 2; r++)
-    for (int v : h->nlegs[r]) maxlegs = v > maxlegs ? v : maxlegs;
-  T3(cudaMalloc(&h->contrib, maxlegs * sizeof(double2)));
+  T3(cudaMalloc(&h->contrib, h->ncontrib * sizeof(double2)));
   T3(cudaMalloc(&h->sb, tot * sizeof(double)));
   T3(cudaMalloc(&h->sr, tot * sizeof(double)));
   T3(cudaMalloc(&h->d, tot * sizeof(double)));
@@ -479,6 +678,7 @@ int tmg_cube_destroy(tmg_cube* h) {
   for (int r = 0; r < 2; r++) {
     for (Block3* p : h->blocks[r]) cudaFree(p);
     for (Leg3* p : h->legs[r]) cudaFree(p);
+    for (Leg3* p : h->klegs[r]) cudaFree(p);
     for (int* p : h->leg0[r]) cudaFree(p);
   }
   cudaFree(h->contrib);
