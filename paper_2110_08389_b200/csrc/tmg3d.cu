@@ -88,6 +88,43 @@ __device__ __forceinline__ double rhs3(const Coef3& c, int n, const double* __re
 // elimination (pivots / rhs to the scratch arrays, its contribution to the
 // branch row into contrib), (2) every branch: num / den in leg order, the
 // branch value, (3) every leg's back substitution from its branch.
+// Per-leg constants: the along-axis coefficient arrays and the four
+// transverse couplings (constant along a straight leg), so a point costs f,
+// four transverse neighbours and two along-axis coefficients.
+struct LegFrame {
+  const double* lo;  // coupling toward decreasing index along the axis
+  const double* hi;
+  double t0, t1, t2, t3, tsum;  // transverse couplings (-b, +b, -c, +c) and their sum
+  long sa, sb_, sc_;             // element strides: along (signed by step), transverse b, c
+  size_t o_tip;
+  int x_tip, step;
+};
+
+__device__ __forceinline__ LegFrame leg_frame(const Coef3& c, int n, const Leg3& G) {
+  LegFrame F;
+  const int a = G.code & 3, s = (G.code & 4) ? -1 : 1;
+  const long n1 = n + 1, str[3] = {n1 * n1, n1, 1};
+  const double* lo3[3] = {c.W, c.S, c.B};
+  const double* hi3[3] = {c.E, c.N, c.T};
+  const int x[3] = {G.bi, G.bj, G.bk};
+  const int b = a == 0 ? 1 : 0, cc = a == 2 ? 1 : 2;  // the transverse axes, in order
+  F.lo = lo3[a];
+  F.hi = hi3[a];
+  F.t0 = __ldg(lo3[b] + x[b]);
+  F.t1 = __ldg(hi3[b] + x[b]);
+  F.t2 = __ldg(lo3[cc] + x[cc]);
+  F.t3 = __ldg(hi3[cc] + x[cc]);
+  F.tsum = F.t0 + F.t1 + F.t2 + F.t3;
+  F.sa = str[a] * s;
+  F.sb_ = str[b];
+  F.sc_ = str[cc];
+  F.x_tip = s > 0 ? 1 : n - 1;
+  F.step = s;
+  const int xt[3] = {a == 0 ? F.x_tip : G.bi, a == 1 ? F.x_tip : G.bj, a == 2 ? F.x_tip : G.bk};
+  F.o_tip = ((size_t)xt[0] * n1 + xt[1]) * (size_t)n1 + xt[2];
+  return F;
+}
+
 __global__ void __launch_bounds__(128) legs_forward_kernel(int n, Coef3 c, const Leg3* __restrict__ legs,
                                                            int nl, const double* __restrict__ u,
                                                            const double* __restrict__ f,
@@ -97,33 +134,33 @@ __global__ void __launch_bounds__(128) legs_forward_kernel(int n, Coef3 c, const
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= nl) return;
   const Leg3 G = legs[l];
-  const int a = G.code & 3, s = (G.code & 4) ? -1 : 1;
-  const int tip = s > 0 ? 1 : n - 1;
+  const LegFrame F = leg_frame(c, n, G);
+  const int s = F.step;
   double bp = 0.0, rp = 0.0, cprev = 0.0;
   bool bad = false;
   for (int t = 0; t < G.len; t++) {
-    const int i = a == 0 ? tip + s * t : G.bi;
-    const int j = a == 1 ? tip + s * t : G.bj;
-    const int k = a == 2 ? tip + s * t : G.bk;
-    unsigned skip = dbit(a, s);
-    if (t > 0) skip |= dbit(a, -s);
-    const double r = rhs3(c, n, u, f, i, j, k, skip);
-    const double bb = diag3(c, i, j, k);
+    const int x = F.x_tip + s * t;
+    const size_t o = F.o_tip + (long)t * F.sa;
+    const double lo = __ldg(F.lo + x), hi = __ldg(F.hi + x);
+    const double am = s > 0 ? lo : hi, cn = s > 0 ? hi : lo;  // toward t-1 / t+1
+    double r = f[o] - F.t0 * u[o - F.sb_] - F.t1 * u[o + F.sb_] - F.t2 * u[o - F.sc_] -
+               F.t3 * u[o + F.sc_];
+    const double bb = -(lo + hi + F.tsum);
     if (t == 0) {
+      r -= am * u[o - F.sa];  // the wall-side neighbour (Dirichlet)
       bp = bb;
       rp = r;
     } else {
       bad |= bp > -1e-300 && bp < 1e-300;
-      const double w = cpl3(c, a, -s, i, j, k) / bp;
+      const double w = am / bp;
       bp = bb - w * cprev;
       rp = r - w * rp;
     }
-    cprev = cpl3(c, a, s, i, j, k);
-    const size_t o = idx3(n, i, j, k);
+    cprev = cn;
     sb[o] = bp;
     sr[o] = rp;
   }
-  const double d = cpl3(c, a, -s, G.bi, G.bj, G.bk);
+  const double d = cpl3(c, G.code & 3, -s, G.bi, G.bj, G.bk);
   bad |= bp > -1e-300 && bp < 1e-300;
   contrib[G.ci] = make_double2(d * rp / bp, d * cprev / bp);
   if (bad) atomicOr(err, 1);
@@ -329,15 +366,14 @@ __global__ void __launch_bounds__(128) legs_back_kernel(int n, Coef3 c, const Le
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= nl) return;
   const Leg3 G = legs[l];
-  const int a = G.code & 3, s = (G.code & 4) ? -1 : 1;
-  const int tip = s > 0 ? 1 : n - 1;
+  const LegFrame F = leg_frame(c, n, G);
+  const int s = F.step;
   double x = u[idx3(n, G.bi, G.bj, G.bk)];
   for (int t = G.len - 1; t >= 0; t--) {
-    const int i = a == 0 ? tip + s * t : G.bi;
-    const int j = a == 1 ? tip + s * t : G.bj;
-    const int k = a == 2 ? tip + s * t : G.bk;
-    const size_t o = idx3(n, i, j, k);
-    x = (sr[o] - cpl3(c, a, s, i, j, k) * x) / sb[o];
+    const int xa = F.x_tip + s * t;
+    const size_t o = F.o_tip + (long)t * F.sa;
+    const double cn = s > 0 ? __ldg(F.hi + xa) : __ldg(F.lo + xa);
+    x = (sr[o] - cn * x) / sb[o];
     u[o] = x;
   }
 }
