@@ -362,4 +362,22 @@ cudaError_t launch_lcg_fill(unsigned long long state, long n, double* out, cudaS
   return cudaGetLastError();
 }
 
+namespace {
+__global__ void zero_kernel(double* __restrict__ p, size_t n) {
+  pdl_trigger();
+  pdl_wait();
+  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
+       k += (size_t)gridDim.x * blockDim.x)
+    p[k] = 0.0;
+}
+}  // namespace
+
+cudaError_t launch_zero(double* p, size_t n, cudaStream_t s) {
+  if (!n) return cudaSuccess;
+  const size_t nb = (n + 255) / 256;
+  TMG_COUNT(1);
+  return launch_pdl(zero_kernel, dim3((unsigned)(nb < 148 * 16 ? nb : 148 * 16)), dim3(256), 0, s,
+                    p, n);
+}
+
 }  // namespace tmg

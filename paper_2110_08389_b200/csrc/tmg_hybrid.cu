@@ -256,6 +256,8 @@ __global__ void __launch_bounds__(256) from_hybrid_kernel(FieldView V, double* _
 }
 
 __global__ void hdense_rhs_kernel(GridArgs g, FieldView U, FieldView F, double* __restrict__ rhs) {
+  pdl_trigger();
+  pdl_wait();
   const int mi = g.nx - 1, n = mi * (g.ny - 1);
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int i = k % mi + 1, j = k / mi + 1;
@@ -271,6 +273,8 @@ __global__ void hdense_rhs_kernel(GridArgs g, FieldView U, FieldView F, double* 
 
 __global__ void hdense_apply_kernel(GridArgs g, const double* __restrict__ Ainv,
                                     const double* __restrict__ rhs, FieldView U) {
+  pdl_trigger();
+  pdl_wait();
   const int mi = g.nx - 1, n = mi * (g.ny - 1);
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= n) return;
@@ -393,9 +397,13 @@ cudaError_t launch_hdense_solve(const GridArgs& g, const double* Ainv, const Fie
   const int n = (g.nx - 1) * (g.ny - 1);
   if (n <= 0) return cudaSuccess;
   TMG_COUNT(1);
-  hdense_rhs_kernel<<<(n + 255) / 256, 256, 0, s>>>(g, U, F, work);
+  cudaError_t e = launch_pdl(hdense_rhs_kernel, dim3((n + 255) / 256), dim3(256), 0, s, g, U, F,
+                             work);
+  if (e != cudaSuccess) return e;
   TMG_COUNT(1);
-  hdense_apply_kernel<<<(n * 32 + 255) / 256, 256, 0, s>>>(g, Ainv, work, U);
+  e = launch_pdl(hdense_apply_kernel, dim3((n * 32 + 255) / 256), dim3(256), 0, s, g, Ainv,
+                 (const double*)work, U);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -8,6 +8,33 @@
 
 namespace tmg {
 
+// Programmatic dependent launch inside the V-cycle: a kernel launched with
+// launch_pdl() may start while its predecessor finishes; it calls
+// pdl_trigger() early (its own successor may then launch) and pdl_wait()
+// before it touches field data (the predecessor has completed and its
+// writes are visible).  Every kernel launched this way waits exactly once.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+bool pdl_enabled();  // TMG_PDL=0 launches without the attribute
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // Host-side count of the kernels this library has put on streams (graph
 // replays add their kernel nodes); tmg_kernel_launches() reads it.
 long long& launch_counter();
@@ -71,6 +98,8 @@ cudaError_t launch_prolong_correct(int nxc, int nyc, const double* uc, double* u
 cudaError_t launch_dense_solve(const GridArgs& g, const double* Ainv, double* u,
                                const double* f, double* work, cudaStream_t s);
 
+// p[0 .. n) = 0 (a PDL-aware kernel, so the V-cycle graph stays a kernel chain)
+cudaError_t launch_zero(double* p, size_t n, cudaStream_t s);
 // sqrt(sum x^2) into work[0] (work: >= 1024 doubles), deterministic order
 cudaError_t launch_vec_norm2(const double* x, long n, double* work, cudaStream_t s);
 // out[k] = uniform [0, 1) value k of the Lcg64 stream after `state`

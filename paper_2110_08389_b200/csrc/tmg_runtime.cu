@@ -350,8 +350,8 @@ int ensure_fields(tmg_hier* h, int mode) {
 size_t field_elems(const FieldView& v) { return (size_t)(v.nx + 1) * (v.ny + 1); }
 
 int zero_field(const FieldView& v, cudaStream_t s) {
-  TMG_CUDA_TRY(cudaMemsetAsync(v.n, 0, field_elems(v) * sizeof(double), s));
-  if (v.t != v.n) TMG_CUDA_TRY(cudaMemsetAsync(v.t, 0, field_elems(v) * sizeof(double), s));
+  TMG_CUDA_TRY(launch_zero(v.n, field_elems(v), s));
+  if (v.t != v.n) TMG_CUDA_TRY(launch_zero(v.t, field_elems(v), s));
   return TMG_OK;
 }
 
@@ -514,6 +514,15 @@ int guarded(Fn&& fn) {
 }  // namespace
 
 namespace tmg {
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("TMG_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 long long& launch_counter() {
   static long long n = 0;
   return n;

@@ -40,6 +40,10 @@ namespace cg = cooperative_groups;
 #ifndef TMG_BATCH
 #define TMG_BATCH 8  // gather items in flight per lane
 #endif
+#ifndef TMG_PDL_LATE
+#define TMG_PDL_LATE 1  // 0: signal the dependent launch at entry instead of after the solve
+#endif
+
 #ifndef TMG_MINB8
 #define TMG_MINB8 TMG_MINB  // resident CTAs per SM targeted by the q <= 8 kernels
 #endif
@@ -280,9 +284,11 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
   const double* __restrict__ f = a.f;
 
   TMG_T(0);
+  if (!TMG_PDL_LATE) pdl_trigger();
   const ChunkD mine = chunks[((size_t)bin * cs_size + rank) * T + tid];
   Chunk c;
   c.unpack(mine, C, ld, a.ldt);
+  pdl_wait();  // the field data of the previous kernel are complete from here on
   const FieldView U{u, a.ut, a.nx, a.ny, a.mode};
   const FieldView F{const_cast<double*>(f), const_cast<double*>(a.ft), a.nx, a.ny, a.mode};
   const BinD bd_ = bins[bin];
@@ -639,6 +645,7 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
   }
   if (bad) atomicOr(a.err, 1);
   TMG_T(5);
+  if (TMG_PDL_LATE) pdl_trigger();  // the successor may launch while this CTA scatters
   if constexpr (CLUSTER) cluster_arrive();  // this CTA's DSMEM reads are done
   // scatter records (sA/sB are free after the reduced solve; the finalize of
   // other warps reads only sD, sH and XH)
@@ -687,6 +694,8 @@ __global__ void __launch_bounds__(256) point_sweep_kernel(SweepArgs a, int nx, i
                                                           int i0) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x + 1;
   const int i = blockIdx.y + i0;
+  pdl_trigger();
+  pdl_wait();
   if (j >= ny || i >= nx) return;
   if ((((i + j) & 1) == 0) != (red != 0)) return;
   const size_t ld = (size_t)a.ld, o = (size_t)i * ld + j;
@@ -739,22 +748,24 @@ cudaError_t launch_class(const LaunchClass& lc, const SweepArgs& a, cudaStream_t
   const int grid = lc.nbins;
   if (lc.cs == 1) {
     TMG_COUNT(1);
-    block_sweep_kernel<false, false, Q><<<grid, kThreads, smem_bytes<Q>(), stream>>>(
-        a, lc.chunks, lc.bins, lc.hubs, 1);
-    return cudaGetLastError();
+    return launch_pdl(block_sweep_kernel<false, false, Q>, dim3(grid), dim3(kThreads),
+                      smem_bytes<Q>(), stream, a, (const ChunkD*)lc.chunks, (const BinD*)lc.bins,
+                      (const HubD*)lc.hubs, 1);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid * lc.cs);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem_bytes<Q>();
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = lc.cs;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   TMG_COUNT(1);
   if (lc.xcta)
     return cudaLaunchKernelEx(&cfg, block_sweep_kernel<true, true, Q>, a,
@@ -803,8 +814,8 @@ cudaError_t launch_colour(const Plan& P, int red, const SweepArgs& a, cudaStream
     const int i0 = P.g0 > 0 ? P.g0 : 1, i1 = P.g0 > 0 ? P.g1 : P.geo.nx;
     dim3 grid((P.geo.ny - 1 + 255) / 256, i1 - i0);
     TMG_COUNT(1);
-    point_sweep_kernel<<<grid, 256, 0, stream>>>(a, P.geo.nx, P.geo.ny, red, i0);
-    return cudaGetLastError();
+    return launch_pdl(point_sweep_kernel, grid, dim3(256), 0, stream, a, P.geo.nx, P.geo.ny, red,
+                      i0);
   }
   for (const LaunchClass& lc : P.classes) {
     if (lc.red != red || lc.nbins == 0) continue;

@@ -124,8 +124,10 @@ constexpr int NT = 32, NE = NT + 2, NLD = NE + 1;
 __global__ void __launch_bounds__(256) norm2_kernel(GridArgs g, FieldView U, FieldView F,
                                                     unsigned long long* dmax, GroupSel2 gsel) {
   __shared__ double su[NE * NLD];
+  pdl_trigger();
   const int i0 = 1 + blockIdx.y * NT, j0 = 1 + blockIdx.x * NT;
   const int own = box_owner(U, i0 - 1, j0 - 1, NE, NE);
+  pdl_wait();
   double fv[4];
   int pi[4], pj[4];
 #pragma unroll
@@ -183,7 +185,9 @@ __global__ void __launch_bounds__(256) restrict2_kernel(GridArgs g, int full, Fi
   const int nxc = g.nx / 2, nyc = g.ny / 2;
   const int I0 = 1 + blockIdx.y * RC, J0 = 1 + blockIdx.x * RC;
   const int ui0 = 2 * I0 - 2, uj0 = 2 * J0 - 2;
+  pdl_trigger();
   const int own = box_owner(U, ui0, uj0, RU, RU);
+  pdl_wait();
   double fv[RPER];
   const bool inner = own >= 0 && ui0 + RD < g.nx && uj0 + RD < g.ny;  // every defect point interior
   if (inner) {
@@ -256,7 +260,9 @@ __global__ void __launch_bounds__(256) prolong2_kernel(int nx, int ny, FieldView
   const int i0 = 1 + blockIdx.y * NT, j0 = 1 + blockIdx.x * NT;
   const int own = box_owner(U, i0, j0, NT, NT);
   const int Ic0 = i0 >> 1, Jc0 = j0 >> 1;
+  pdl_trigger();
   const int cown = box_owner(C, Ic0, Jc0, PC_E, PC_E);
+  pdl_wait();
   double uv[4];
   int pi[4], pj[4];
 #pragma unroll
@@ -296,8 +302,8 @@ cudaError_t launch_norm2(const GridArgs& g, const FieldView& U, const FieldView&
   if (g.nx < 2 || g.ny < 2) return cudaSuccess;
   dim3 grid((g.ny - 1 + NT - 1) / NT, (g.nx - 1 + NT - 1) / NT);
   TMG_COUNT(1);
-  norm2_kernel<<<grid, 256, 0, s>>>(g, U, F, dmax, GroupSel2{scheme, g0, g1});
-  return cudaGetLastError();
+  return launch_pdl(norm2_kernel, grid, dim3(256), 0, s, g, U, F, dmax,
+                    GroupSel2{scheme, g0, g1});
 }
 
 cudaError_t launch_restrict2(const GridArgs& g, int full, const FieldView& U, const FieldView& F,
@@ -306,8 +312,7 @@ cudaError_t launch_restrict2(const GridArgs& g, int full, const FieldView& U, co
   if (nxc < 2 || nyc < 2) return cudaSuccess;
   dim3 grid((nyc - 1 + RC - 1) / RC, (nxc - 1 + RC - 1) / RC);
   TMG_COUNT(1);
-  restrict2_kernel<<<grid, 256, 0, s>>>(g, full, U, F, FC);
-  return cudaGetLastError();
+  return launch_pdl(restrict2_kernel, grid, dim3(256), 0, s, g, full, U, F, FC);
 }
 
 cudaError_t launch_prolong2(int nx, int ny, const FieldView& C, const FieldView& U,
@@ -315,8 +320,7 @@ cudaError_t launch_prolong2(int nx, int ny, const FieldView& C, const FieldView&
   if (nx < 2 || ny < 2) return cudaSuccess;
   dim3 grid((ny - 1 + NT - 1) / NT, (nx - 1 + NT - 1) / NT);
   TMG_COUNT(1);
-  prolong2_kernel<<<grid, 256, 0, s>>>(nx, ny, C, U);
-  return cudaGetLastError();
+  return launch_pdl(prolong2_kernel, grid, dim3(256), 0, s, nx, ny, C, U);
 }
 
 }  // namespace tmg
