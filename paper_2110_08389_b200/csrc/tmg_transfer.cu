@@ -175,13 +175,18 @@ __global__ void __launch_bounds__(256) norm2_kernel(GridArgs g, FieldView U, Fie
 }
 
 // ---- fused residual + restriction: 16 x 16 coarse points per CTA ----------
-constexpr int RC = 16, RD = 2 * RC + 1, RU = 2 * RC + 3, RLU = RU + 1, RLD = RD + 1;
+#ifndef TMG_RC
+#define TMG_RC 16
+#endif
+constexpr int RC = TMG_RC, RD = 2 * RC + 1, RU = 2 * RC + 3, RLU = RU + 1, RLD = RD + 1;
+constexpr size_t kRestrictSmem = sizeof(double) * (size_t)(RU * RLU + RD * RLD);
 constexpr int RPER = (RD * RD + 255) / 256;
 
 __global__ void __launch_bounds__(256) restrict2_kernel(GridArgs g, int full, FieldView U,
                                                         FieldView F, FieldView FC) {
-  __shared__ double su[RU * RLU];
-  __shared__ double sd[RD * RLD];
+  extern __shared__ double rsm[];
+  double* su = rsm;
+  double* sd = rsm + RU * RLU;
   const int nxc = g.nx / 2, nyc = g.ny / 2;
   const int I0 = 1 + blockIdx.y * RC, J0 = 1 + blockIdx.x * RC;
   const int ui0 = 2 * I0 - 2, uj0 = 2 * J0 - 2;
@@ -227,7 +232,8 @@ __global__ void __launch_bounds__(256) restrict2_kernel(GridArgs g, int full, Fi
   __syncthreads();
   // coarse point, lanes along the coarse owner's contiguous axis
   const int cown = box_owner(FC, I0, J0, RC, RC);
-  const int p = threadIdx.x / RC, q = threadIdx.x - p * RC;
+  for (int cpt = threadIdx.x; cpt < RC * RC; cpt += 256) {
+  const int p = cpt / RC, q = cpt - p * RC;
   const int ca = cown == 1 ? q : p, cb = cown == 1 ? p : q;  // I offset, J offset
   const int I = I0 + ca, J = J0 + cb;
   if (I < nxc && J < nyc) {
@@ -249,6 +255,7 @@ __global__ void __launch_bounds__(256) restrict2_kernel(GridArgs g, int full, Fi
     if (cown == 1) FC.t[FC.off_t(I, J)] = v;
     else if (cown == 0) FC.n[FC.off_n(I, J)] = v;
     else *FC.at(I, J) = v;
+  }
   }
 }
 
@@ -312,7 +319,15 @@ cudaError_t launch_restrict2(const GridArgs& g, int full, const FieldView& U, co
   if (nxc < 2 || nyc < 2) return cudaSuccess;
   dim3 grid((nyc - 1 + RC - 1) / RC, (nxc - 1 + RC - 1) / RC);
   TMG_COUNT(1);
-  return launch_pdl(restrict2_kernel, grid, dim3(256), 0, s, g, full, U, F, FC);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(restrict2_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kRestrictSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  return launch_pdl(restrict2_kernel, grid, dim3(256), kRestrictSmem, s, g, full, U, F, FC);
 }
 
 cudaError_t launch_prolong2(int nx, int ny, const FieldView& C, const FieldView& U,
