@@ -201,11 +201,15 @@ int tmg_relax_legged(long n, const int64_t* ii, const int64_t* jj, long m, const
  *      (n+1), used on all three axes. */
 typedef struct tmg_cube tmg_cube;
 const char* tmg_cube_last_error(void);
-int tmg_cube_create(int n, const double* x, tmg_cube** out);
+int tmg_cube_create(int n, const double* x, tmg_cube** out); /* = scheme 0 */
+/* scheme 0: 3D tweed (config 4); 1: 3D wireframe (config 5: shell frames of
+ * 12 edges / 8 corners and closed face rings, SURVEY.md §8(c) "Candidate 3D
+ * layouts"; the ring solve restates _ckernels.pyx:106-141 per face) */
+int tmg_cube_create_scheme(int n, const double* x, int scheme, tmg_cube** out);
 int tmg_cube_destroy(tmg_cube* h);
 int tmg_cube_levels(tmg_cube* h);
 long tmg_cube_blocks(tmg_cube* h, int level, int red);
-/* one 3D tweed sweep (red blocks, then black) of the finest level */
+/* one 3D sweep (red blocks, then black) of the finest level */
 int tmg_cube_sweep(tmg_cube* h, double* u, const double* f, void* stream);
 int tmg_cube_defect(tmg_cube* h, const double* u, const double* f, double* d, void* stream);
 /* session: load u, f; replay V(nu1, nu2) cycles (CUDA graph); norm + pivot

@@ -1,5 +1,5 @@
-"""CPU ORACLE of the 3D tweed V-cycle (test infrastructure only): ctypes
-wrapper of tweed3d_oracle.c plus the V-cycle driver of mgcycle.py:89-139
+"""CPU ORACLE of the 3D tweed and wireframe V-cycles (test infrastructure
+only): ctypes wrapper of tweed3d_oracle.c / wire3d_oracle.c plus the V-cycle driver of mgcycle.py:89-139
 restated for cubes.  The reference is 2D only, so this restatement is the
 checker of the device 3D path (parity unpinned by the reference; pinned by
 property tests in tests/test_3d.py)."""
@@ -27,6 +27,9 @@ def _decl():
     L.orc3_coarse_solve.argtypes = [dp] * 8
     L.orc3_layout_dump.argtypes = [cl, lp, lp, lp, lp, lp, cl]
     L.orc3_layout_dump.restype = cl
+    L.orcw3_sweep.argtypes = [cl] + [dp] * 8 + [ci]
+    L.orcw3_layout_dump.argtypes = [cl, lp, lp, lp, lp, lp, cl]
+    L.orcw3_layout_dump.restype = cl
     L._o3 = True
     return L
 
@@ -61,9 +64,15 @@ def assemble3(x, y, z):
     return W, E, S, N, B, T
 
 
-def sweep(st, u, f, nthreads=1):
+SCHEMES = ("tweed", "wireframe")
+
+
+def sweep(st, u, f, nthreads=1, scheme="tweed"):
     n = len(st[0]) - 1
-    _check(_decl().orc3_sweep(n, *[_dp(a) for a in st], _dp(u), _dp(f), int(nthreads)))
+    fn = _decl().orc3_sweep if scheme == "tweed" else _decl().orcw3_sweep
+    if scheme not in SCHEMES:
+        raise ValueError(scheme)
+    _check(fn(n, *[_dp(a) for a in st], _dp(u), _dp(f), int(nthreads)))
 
 
 def defect(st, u, f, nthreads=1):
@@ -84,16 +93,20 @@ def prolong_add(uc, u):
     _decl().orc3_prolong_add(uc.shape[0] - 1, _dp(np.ascontiguousarray(uc)), _dp(u))
 
 
-def layout_dump(n):
+def layout_dump(n, scheme="tweed"):
     m = (n - 1) ** 3
     arrs = [np.empty(m, dtype=np.int64) for _ in range(5)]
-    got = _decl().orc3_layout_dump(n, *[a.ctypes.data_as(ctypes.POINTER(ctypes.c_long))
+    fn = _decl().orc3_layout_dump if scheme == "tweed" else _decl().orcw3_layout_dump
+    got = fn(n, *[a.ctypes.data_as(ctypes.POINTER(ctypes.c_long))
                                         for a in arrs], m)
     return tuple(a[:got] for a in arrs)
 
 
 class Hierarchy3:
-    def __init__(self, x):
+    def __init__(self, x, scheme="tweed"):
+        if scheme not in SCHEMES:
+            raise ValueError(scheme)
+        self.scheme = scheme
         levels = [np.asarray(x, float)]
         while True:
             n = len(levels[-1]) - 1
@@ -110,13 +123,13 @@ def _v_cycle(h, nu1, nu2, lvl, u, f, nthreads):
         _check(_decl().orc3_coarse_solve(*[_dp(a) for a in st], _dp(u), _dp(f)))
         return
     for _ in range(nu1):
-        sweep(st, u, f, nthreads)
+        sweep(st, u, f, nthreads, h.scheme)
     fc = restrict(defect(st, u, f, nthreads))
     uc = np.zeros_like(fc)
     _v_cycle(h, nu1, nu2, lvl + 1, uc, fc, nthreads)
     prolong_add(uc, u)
     for _ in range(nu2):
-        sweep(st, u, f, nthreads)
+        sweep(st, u, f, nthreads, h.scheme)
 
 
 def v_cycle(h, u, f, nu1=2, nu2=2, nthreads=1):

@@ -69,6 +69,7 @@ def _declare(L):
         "tmg_lcg_fill": ([ctypes.c_ulonglong, lp, vp, vp], ip),
         "tmg_cube_last_error": ([], ctypes.c_char_p),
         "tmg_cube_create": ([ip, vp, ctypes.POINTER(vp)], ip),
+        "tmg_cube_create_scheme": ([ip, vp, ip, ctypes.POINTER(vp)], ip),
         "tmg_cube_destroy": ([vp], ip),
         "tmg_cube_levels": ([vp], ip),
         "tmg_cube_blocks": ([vp, ip, ip], lp),

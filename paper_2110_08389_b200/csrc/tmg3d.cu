@@ -22,9 +22,13 @@
 #include <vector>
 
 #include "../../include/tweedmg_b200.h"
+#include "tmg3d.h"
 #include "tmg_kernels.h"
 
 using namespace tmg;
+using tmg3::Coef3;
+using tmg3::idx3;
+using tmg3::mirror;
 
 namespace {
 
@@ -47,16 +51,6 @@ struct Leg3 {
   uint8_t slot;     // leg index within the block
 };
 static_assert(sizeof(Leg3) == 20, "Leg3 layout");
-
-__host__ __device__ inline long mirror(long x, long n) { return x < n - x ? x : n - x; }
-
-struct Coef3 {
-  const double *W, *E, *S, *N, *B, *T;
-};
-
-__device__ __forceinline__ size_t idx3(int n, int i, int j, int k) {
-  return ((size_t)i * (n + 1) + j) * (size_t)(n + 1) + k;
-}
 
 __device__ __forceinline__ double cpl3(const Coef3& c, int a, int s, int i, int j, int k) {
   if (a == 0) return s < 0 ? __ldg(c.W + i) : __ldg(c.E + i);
@@ -468,6 +462,8 @@ int fail3(int code, const std::string& m) {
 // host side
 
 struct tmg_cube {
+  int scheme = 0;                     // 0 tweed, 1 wireframe
+  std::vector<tmg3::WLevel> wl;       // wireframe blocks per level
   std::vector<int> n;                 // per level
   std::vector<double*> coef;          // per level: W E S N B T (6 (n+1))
   std::vector<Block3*> blocks[2];     // per level: black, red lists
@@ -536,6 +532,12 @@ Coef3 coefs(const tmg_cube* h, int l) {
 
 int sweep3(tmg_cube* h, int l, double* u, const double* f, cudaStream_t s) {
   const int n = h->n[l];
+  if (h->scheme == 1) {
+    for (int red = 1; red >= 0; red--)
+      if (tmg3::wire_stage(h->wl[l], n, coefs(h, l), red, u, f, h->err, s))
+        return cuda3(cudaGetLastError(), "wireframe stage");
+    return TMG_OK;
+  }
   for (int red = 1; red >= 0; red--) {
     const int nb = h->nblocks[red][l], nl = h->nlegs[red][l], nk = h->nklegs[red][l];
     if (!nb) continue;
@@ -610,8 +612,15 @@ const char* tmg_cube_last_error(void) { return g_err3.c_str(); }
 // Hierarchy of cube levels from the finest 1D coordinates (n+1 values);
 // coefficients W/E, S/N, B/T from the same coordinates on every axis
 int tmg_cube_create(int n, const double* x, tmg_cube** out) {
+  return tmg_cube_create_scheme(n, x, 0, out);
+}
+
+// scheme 0: 3D tweed (config 4), 1: 3D wireframe (config 5)
+int tmg_cube_create_scheme(int n, const double* x, int scheme, tmg_cube** out) {
   if (!out || !x || n < 2 || n % 2) return fail3(TMG_BADARG, "cube needs even n >= 2");
+  if (scheme != 0 && scheme != 1) return fail3(TMG_BADARG, "cube scheme must be 0 (tweed) or 1 (wireframe)");
   tmg_cube* h = new tmg_cube();
+  h->scheme = scheme;
   std::vector<double> xs(x, x + n + 1);
   while (true) {
     const int m = (int)xs.size() - 1;
@@ -632,8 +641,17 @@ int tmg_cube_create(int n, const double* x, tmg_cube** out) {
     T3(cudaMalloc(&dc, all.size() * sizeof(double)));
     T3(cudaMemcpy(dc, all.data(), all.size() * sizeof(double), cudaMemcpyHostToDevice));
     h->coef.push_back(dc);
+    if (scheme == 1) {
+      h->wl.emplace_back();
+      std::string err;
+      const int st = tmg3::wire_build_level(m, h->wl.back(), err);
+      if (st) {
+        tmg_cube_destroy(h);
+        return fail3(st == 2 ? TMG_BADARG : TMG_CUDA, err);
+      }
+    }
     std::vector<Block3> bl[2];
-    build_blocks(m, bl);
+    if (scheme == 0) build_blocks(m, bl);
     for (int r = 0; r < 2; r++) {
       Block3* db = nullptr;
       if (!bl[r].empty()) {
@@ -695,8 +713,10 @@ int tmg_cube_create(int n, const double* x, tmg_cube** out) {
   }
   const size_t tot = (size_t)(n + 1) * (n + 1) * (n + 1);
   T3(cudaMalloc(&h->contrib, h->ncontrib * sizeof(double2)));
-  T3(cudaMalloc(&h->sb, tot * sizeof(double)));
-  T3(cudaMalloc(&h->sr, tot * sizeof(double)));
+  if (scheme == 0) {  // the tweed legs' elimination scratch
+    T3(cudaMalloc(&h->sb, tot * sizeof(double)));
+    T3(cudaMalloc(&h->sr, tot * sizeof(double)));
+  }
   T3(cudaMalloc(&h->d, tot * sizeof(double)));
   T3(cudaMalloc(&h->err, sizeof(int) + sizeof(unsigned long long) * 2));
   h->dmax = reinterpret_cast<unsigned long long*>(h->err + 2);
@@ -718,6 +738,7 @@ int tmg_cube_destroy(tmg_cube* h) {
     for (int* p : h->leg0[r]) cudaFree(p);
   }
   cudaFree(h->contrib);
+  for (auto& w : h->wl) tmg3::wire_free_level(w);
   for (double* p : h->U) cudaFree(p);
   for (double* p : h->F) cudaFree(p);
   cudaFree(h->sb);
@@ -733,6 +754,7 @@ int tmg_cube_levels(tmg_cube* h) { return h ? (int)h->n.size() : 0; }
 
 long tmg_cube_blocks(tmg_cube* h, int level, int red) {
   if (!h || level < 0 || level >= (int)h->n.size()) return -1;
+  if (h->scheme == 1) return tmg3::wire_blocks(h->wl[level], red ? 1 : 0);
   return h->nblocks[red ? 1 : 0][level];
 }
 

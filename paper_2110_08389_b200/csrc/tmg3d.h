@@ -1,0 +1,65 @@
+// Shared pieces of the 3D cube paths (tmg3d.cu: tweed and the V-cycle;
+// tmg3dw.cu: wireframe blocks).  Fields are C-order (n+1)^3, k fastest.
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+namespace tmg3 {
+
+struct Coef3 {
+  const double *W, *E, *S, *N, *B, *T;
+};
+
+__host__ __device__ inline long mirror(long x, long n) { return x < n - x ? x : n - x; }
+
+__device__ __forceinline__ size_t idx3(int n, int i, int j, int k) {
+  return ((size_t)i * (n + 1) + j) * (size_t)(n + 1) + k;
+}
+
+// ---------------------------------------------------------------------------
+// 3D wireframe (tmg3dw.cu).  Blocks of one level and colour:
+//   rings  closed square rings of a shell face, one CTA slice of TR threads
+//          per ring, grouped in classes by TR (kRingClasses);
+//   frames the 12-edge / 8-corner frame of a shell (red only): per-edge
+//          elimination, an 8x8 corner solve, per-edge back substitution;
+//   points face centres and the cube centre.
+constexpr int kRingClasses = 5;  // TR = 32, 64, 128, 256, 512 threads per ring
+
+struct Ring3 {
+  int16_t a;   // axis normal to the face
+  int16_t t;   // ring level in the face
+  int32_t xa;  // coordinate of the face along a
+};
+
+struct WEdge {
+  int32_t r;      // shell
+  int32_t off;    // first scratch slot of the edge (e = n - 2r - 1 points)
+  int32_t frame;  // index of the frame in the level's frame list
+  uint8_t ax, k0, k1, slot;  // axis; start / end corner (bit a: coordinate n - r); edge 0..11
+};
+
+struct WLevel {
+  Ring3* rings[2][kRingClasses] = {};
+  int nrings[2][kRingClasses] = {};
+  WEdge* edges = nullptr;  // red frames only
+  int nedges = 0;
+  int* frames = nullptr;   // shell r of each frame
+  int nframes = 0;
+  int4* points[2] = {};
+  int npoints[2] = {};
+  double* scratch = nullptr;   // 4 doubles per frame edge point
+  double* ends = nullptr;      // per edge: first and last point forms (6 doubles)
+};
+
+int wire_build_level(int n, WLevel& L, std::string& err);
+void wire_free_level(WLevel& L);
+// one colour stage (red = 1 / black = 0) of the wireframe sweep
+int wire_stage(const WLevel& L, int n, const Coef3& c, int red, double* u, const double* f,
+               int* err, cudaStream_t s);
+// blocks of a colour (for tmg_cube_blocks)
+long wire_blocks(const WLevel& L, int red);
+
+}  // namespace tmg3

@@ -1,4 +1,4 @@
-"""3D tweed multigrid on cubes (BASELINE config 4).
+"""3D tweed and wireframe multigrid on cubes (BASELINE configs 4 and 5).
 
 The reference is 2D only; this module carries its
 semantics to a third axis -- the 7-point operator of stencil.py:43-96 with
@@ -8,9 +8,13 @@ tridiag.py:84-125 for blocks of up to 6 legs -- on the survey's cube layout
 (a point lies on the line along the axis of its unique smallest mirrored
 coordinate, from the wall to the first tie point, the branch).  The API
 mirrors mgcycle: a hierarchy, ``sweep``, ``defect``, ``v_cycle`` and
-``solve`` returning a CycleReport.  Fields are (n+1)^3 float64 arrays, C
+``solve`` returning a CycleReport.  ``scheme="wireframe"`` selects the
+survey's 3D wireframe layout instead (shell frames of 12 edges and 8
+corners, closed rings on the shell faces solved as in _ckernels.pyx:106-141,
+face and cube centres as points).  Fields are (n+1)^3 float64 arrays, C
 order with k fastest; CUDA tensors stay on the device, numpy arrays come
-back as numpy.  The checker is oracle/tweed3d_oracle.c.
+back as numpy.  The checkers are oracle/tweed3d_oracle.c and
+oracle/wire3d_oracle.c.
 """
 
 from __future__ import annotations
@@ -37,20 +41,28 @@ def _check(st):
     raise RuntimeError(f"CUDA error: {msg}")
 
 
+SCHEMES = ("tweed", "wireframe")
+
+
 class CubeHierarchy:
     """Levels n, n/2, ... down to 2 of a cube whose three axes use the 1D
-    coordinates x (grid.Coords1D or an array of n+1 increasing values)."""
+    coordinates x (grid.Coords1D or an array of n+1 increasing values);
+    ``scheme`` is the block layout the sweeps relax ("tweed" or
+    "wireframe")."""
 
-    def __init__(self, x):
+    def __init__(self, x, scheme: str = "tweed"):
+        if scheme not in SCHEMES:
+            raise ValueError(f"unknown 3D scheme {scheme!r}; expected one of {SCHEMES}")
         _device.require_cuda()
+        self.scheme = scheme
         v = np.ascontiguousarray(getattr(x, "values", x), dtype=np.float64)
         self.n = len(v) - 1
         if self.n < 2 or self.n % 2:
             raise ValueError(f"cube needs an even n >= 2, got {self.n}")
         self.x = v
         h = ctypes.c_void_p()
-        _check(_lib.lib().tmg_cube_create(self.n, v.ctypes.data_as(ctypes.c_void_p),
-                                          ctypes.byref(h)))
+        _check(_lib.lib().tmg_cube_create_scheme(self.n, v.ctypes.data_as(ctypes.c_void_p),
+                                                 SCHEMES.index(scheme), ctypes.byref(h)))
         self._h = h
         weakref.finalize(self, _lib.lib().tmg_cube_destroy, h)
 
@@ -83,7 +95,8 @@ def _fields(h: CubeHierarchy, *arrs):
 
 
 def sweep(h: CubeHierarchy, u, f):
-    """One 3D tweed sweep (red blocks, then black) in place on u."""
+    """One 3D sweep of the hierarchy's scheme (red blocks, then black) in
+    place on u."""
     ud, fd = _fields(h, u, f)
     s = _device.stream_handle()
     _check(_lib.lib().tmg_cube_sweep(h._h, _device.ptr(ud), _device.ptr(fd), s))
@@ -100,10 +113,15 @@ def defect(h: CubeHierarchy, u, f):
     return _device.back(d, u)
 
 
+def _check_cfg(h: CubeHierarchy, cfg: CycleConfig):
+    if cfg.smoother != h.scheme or cfg.restriction != "full":
+        raise ValueError(f"this hierarchy smooths with {h.scheme!r} and full weighting; got "
+                         f"smoother={cfg.smoother!r}, restriction={cfg.restriction!r}")
+
+
 def v_cycle(h: CubeHierarchy, cfg: CycleConfig, u, f):
     """One V(nu1, nu2) cycle in place on u (mgcycle.py:80-104 in 3D)."""
-    if cfg.smoother != "tweed" or cfg.restriction != "full":
-        raise ValueError("the 3D path implements tweed smoothing with full weighting")
+    _check_cfg(h, cfg)
     ud, fd = _fields(h, u, f)
     L, s = _lib.lib(), _device.stream_handle()
     _check(L.tmg_cube_load(h._h, _device.ptr(ud), _device.ptr(fd), s))
@@ -117,8 +135,7 @@ def v_cycle(h: CubeHierarchy, cfg: CycleConfig, u, f):
 def solve(h: CubeHierarchy, cfg: CycleConfig, f):
     """V-cycles from u = 0 until max|f - Lu| <= tol * d0, a non-finite
     defect or max_cycles (mgcycle.py:107-139 in 3D)."""
-    if cfg.smoother != "tweed" or cfg.restriction != "full":
-        raise ValueError("the 3D path implements tweed smoothing with full weighting")
+    _check_cfg(h, cfg)
     (fd,) = _fields(h, f)
     u = _device.zeros(fd.shape)
     L, s = _lib.lib(), _device.stream_handle()
@@ -147,10 +164,10 @@ def solve(h: CubeHierarchy, cfg: CycleConfig, f):
     return _device.back(u, f), rep
 
 
-def config4_rhs(n: int, device: bool = True):
+def config4_rhs(n: int, device: bool = True, seed: int = 3):
     """BASELINE config 4 right-hand side: 2 * Lcg64(3).fill((n-1)^3) - 1 on the
     interior, 0 on the boundary."""
-    g = Lcg64(3)
+    g = Lcg64(seed)
     if device:
         import torch
         f = torch.zeros((n + 1,) * 3, dtype=torch.float64, device="cuda")
@@ -159,3 +176,10 @@ def config4_rhs(n: int, device: bool = True):
     f = np.zeros((n + 1,) * 3)
     f[1:-1, 1:-1, 1:-1] = 2.0 * g.fill((n - 1,) * 3) - 1.0
     return f
+
+
+def config5_rhs(n: int, device: bool = True):
+    """BASELINE config 5 right-hand side: 2 * Lcg64(4).fill((n-1)^3) - 1 on the
+    interior, 0 on the boundary (the device fill is the
+    jump-ahead generator checked bit-equal against Lcg64)."""
+    return config4_rhs(n, device, seed=4)

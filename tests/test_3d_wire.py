@@ -1,0 +1,163 @@
+"""3D wireframe on cubes (BASELINE config 5).  There is no 3D reference
+(SURVEY.md §8(c)); the CPU restatement oracle/wire3d_oracle.c is pinned by
+property tests here (partition, block shapes, same-colour independence,
+agreement with a dense block Gauss-Seidel, convergence), and the device path
+is checked against it."""
+
+import numpy as np
+import pytest
+
+from paper_2110_08389_b200 import configs, grid
+
+from test_3d import _dense
+
+
+def _o3():
+    from oracle import oracle3d
+    return oracle3d
+
+
+@pytest.mark.parametrize("n", [4, 6, 8, 12, 16])
+def test_layout_partition_and_colouring(orc, n):
+    o3 = _o3()
+    ii, jj, kk, blk, red = o3.layout_dump(n, "wireframe")
+    pts = list(zip(ii.tolist(), jj.tolist(), kk.tolist()))
+    assert len(set(pts)) == len(pts) == (n - 1) ** 3
+    owner = {p: (b, r) for p, b, r in zip(pts, blk.tolist(), red.tolist())}
+    for p, (bl, r) in owner.items():
+        for d in ((1, 0, 0), (0, 1, 0), (0, 0, 1)):
+            q = (p[0] + d[0], p[1] + d[1], p[2] + d[2])
+            if q in owner and owner[q][0] != bl:
+                assert owner[q][1] != r, (p, q)
+    # the corners and every frame are red
+    assert owner[(1, 1, 1)][1] == 1
+
+
+@pytest.mark.parametrize("n", [6, 8, 12])
+def test_block_shapes(orc, n):
+    """Every block is a frame (8 corners of degree 3, 12 paths), a closed
+    ring (every member has exactly two in-block neighbours) or a point."""
+    o3 = _o3()
+    ii, jj, kk, blk, red = o3.layout_dump(n, "wireframe")
+    members = {}
+    for p, b in zip(zip(ii.tolist(), jj.tolist(), kk.tolist()), blk.tolist()):
+        members.setdefault(b, set()).add(p)
+    c = n // 2
+    kinds = {"frame": 0, "ring": 0, "point": 0}
+    for b, pts in members.items():
+        deg = {}
+        for p in pts:
+            deg[p] = sum((p[0] + d0, p[1] + d1, p[2] + d2) in pts
+                         for d0, d1, d2 in ((1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0),
+                                            (0, 0, 1), (0, 0, -1)))
+        if len(pts) == 1:
+            kinds["point"] += 1
+        elif sorted(deg.values()).count(3) == 8:
+            assert set(deg.values()) == {2, 3}
+            r = min(min(p) for p in pts)
+            assert len(pts) == 8 + 12 * (n - 2 * r - 1)
+            kinds["frame"] += 1
+        else:
+            assert set(deg.values()) == {2}, b
+            kinds["ring"] += 1
+    assert kinds["frame"] == c - 1
+    assert kinds["ring"] == 6 * sum(c - 1 - s for s in range(1, c))
+    assert kinds["point"] == 1 + 6 * (c - 1)
+
+
+@pytest.mark.parametrize("n", [4, 6, 8])
+def test_sweep_equals_dense_block_gauss_seidel(orc, n):
+    o3 = _o3()
+    x = configs.sinh_centre(n, 1.0, 3.0).values
+    st = o3.assemble3(x, x, x)
+    rng = np.random.default_rng(7)
+    u = np.zeros((n + 1,) * 3)
+    u[1:-1, 1:-1, 1:-1] = rng.standard_normal((n - 1,) * 3)
+    f = rng.standard_normal((n + 1,) * 3)
+    uo = u.copy()
+    o3.sweep(st, uo, f, scheme="wireframe")
+    A, idx = _dense(st, n)
+    ii, jj, kk, blk, red = o3.layout_dump(n, "wireframe")
+    v = u[1:-1, 1:-1, 1:-1].reshape(-1).copy()
+    fv = f[1:-1, 1:-1, 1:-1].reshape(-1)
+    for colour in (1, 0):
+        for b in np.unique(blk[red == colour]):
+            sel = blk == b
+            I = np.array([idx(a, bb, c) for a, bb, c in zip(ii[sel], jj[sel], kk[sel])])
+            mask = np.ones(len(v), bool)
+            mask[I] = False
+            v[I] = np.linalg.solve(A[np.ix_(I, I)], fv[I] - A[np.ix_(I, mask)] @ v[mask])
+    assert np.abs(uo[1:-1, 1:-1, 1:-1].reshape(-1) - v).max() <= 1e-12 * np.abs(v).max()
+
+
+def test_oracle_vcycle_converges(orc):
+    o3 = _o3()
+    n = 16
+    h = o3.Hierarchy3(configs.sinh_centre(n, 1.0, 3.0).values, scheme="wireframe")
+    f = np.zeros((n + 1,) * 3)
+    f[1:-1, 1:-1, 1:-1] = np.random.default_rng(4).uniform(-1, 1, (n - 1,) * 3)
+    _, rep = o3.solve(h, f, max_cycles=40)
+    assert rep.converged
+    assert max(rep.per_cycle_ratios[2:]) < 0.5
+
+
+# ----------------------------------------------------------------------------
+# device path against the oracle
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [4, 6, 8, 16, 32, 66, 130])
+def test_device_sweep_matches_oracle(cuda, orc, n):
+    from paper_2110_08389_b200 import cube
+    o3 = _o3()
+    x = configs.sinh_centre(n, 1.0, 3.0)
+    h = cube.CubeHierarchy(x, scheme="wireframe")
+    rng = np.random.default_rng(5)
+    u = np.zeros((n + 1,) * 3)
+    u[1:-1, 1:-1, 1:-1] = rng.standard_normal((n - 1,) * 3)
+    f = rng.standard_normal((n + 1,) * 3)
+    ug = u.copy()
+    cube.sweep(h, ug, f)
+    uo = u.copy()
+    o3.sweep(o3.assemble3(x.values, x.values, x.values), uo, f, scheme="wireframe")
+    assert np.abs(ug - uo).max() <= 1e-12 * np.abs(uo).max()
+    assert np.all(ug[0] == 0) and np.all(ug[:, :, -1] == 0)
+
+
+@pytest.mark.gpu
+def test_device_vcycle_and_solve_match_oracle(cuda, orc):
+    from paper_2110_08389_b200 import cube, mgcycle
+    o3 = _o3()
+    n = 32
+    x = configs.sinh_centre(n, 1.0, 3.0)
+    h = cube.CubeHierarchy(x, scheme="wireframe")
+    H = o3.Hierarchy3(x.values, scheme="wireframe")
+    f = cube.config5_rhs(n, device=False)
+    cfg = mgcycle.CycleConfig(smoother="wireframe", nu1=2, nu2=2)
+    ug, uo = np.zeros_like(f), np.zeros_like(f)
+    for _ in range(2):
+        cube.v_cycle(h, cfg, ug, f)
+        o3.v_cycle(H, uo, f)
+        assert np.abs(ug - uo).max() <= 1e-10 * np.abs(uo).max()
+    _, rep = cube.solve(h, cfg, f)
+    _, repo = o3.solve(H, f)
+    assert rep.cycles == repo.cycles and rep.converged == repo.converged
+    for a, b in zip(rep.defect_norms, repo.defect_norms):
+        assert abs(a - b) <= 1e-6 * b + 1e-11 * repo.defect_norms[0]
+
+
+@pytest.mark.gpu
+def test_config5_scale_sweep(cuda, orc):
+    """513^3 (half the config-5 grid, so the oracle finishes in seconds): one
+    device sweep against the oracle."""
+    from paper_2110_08389_b200 import cube
+    o3 = _o3()
+    n = 512
+    x = configs.sinh_centre(n, 1.0, 3.0)
+    h = cube.CubeHierarchy(x, scheme="wireframe")
+    f = cube.config5_rhs(n)
+    u = cube.config5_rhs(n) * 0.5
+    uo = u.cpu().numpy()
+    cube.sweep(h, u, f)
+    o3.sweep(o3.assemble3(x.values, x.values, x.values), uo, f.cpu().numpy(), orc.max_threads(),
+             scheme="wireframe")
+    assert np.abs(u.cpu().numpy() - uo).max() <= 1e-10 * np.abs(uo).max()

@@ -1,4 +1,5 @@
-"""Time the 3D tweed sweep and V(2,2) cycle on a cube (default 257^3)."""
+"""Time the 3D sweep and V(2,2) cycle on a cube: cube_time.py [n] [tweed|wireframe]
+(default 257^3 tweed; wireframe uses the config-5 sinh-centre grid)."""
 import ctypes
 import os
 import sys
@@ -6,11 +7,16 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from paper_2110_08389_b200 import _lib, cube, grid  # noqa: E402
+from paper_2110_08389_b200 import _lib, configs, cube, grid  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 256
-h = cube.CubeHierarchy(grid.make_tanh_wall(n, 1.0, 3.0))
-f = cube.config4_rhs(n)
+scheme = sys.argv[2] if len(sys.argv) > 2 else "tweed"
+if scheme == "tweed":
+    h = cube.CubeHierarchy(grid.make_tanh_wall(n, 1.0, 3.0))
+    f = cube.config4_rhs(n)
+else:
+    h = cube.CubeHierarchy(configs.sinh_centre(n, 1.0, 3.0), scheme="wireframe")
+    f = cube.config5_rhs(n)
 u = torch.zeros_like(f)
 L = _lib.lib()
 s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -33,5 +39,5 @@ tsw = ev(lambda: L.tmg_cube_sweep(h._h, ctypes.c_void_p(u.data_ptr()), ctypes.c_
 L.tmg_cube_load(h._h, ctypes.c_void_p(u.data_ptr()), ctypes.c_void_p(f.data_ptr()), s)
 tcy = ev(lambda: L.tmg_cube_cycles(h._h, 2, 2, 1, s), 5)
 npts = (n - 1) ** 3
-print(f"n={n} blocks {h.blocks(0)} sweep {tsw:.3f} ms ({24 * npts / tsw / 1e6:.0f} GB/s alg) "
+print(f"{scheme} n={n} blocks {h.blocks(0)} sweep {tsw:.3f} ms ({24 * npts / tsw / 1e6:.0f} GB/s alg) "
       f"V(2,2) {tcy:.3f} ms ({4 * h.interior_points() / tcy / 1e6:.3e} updates/s)")
