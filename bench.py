@@ -504,19 +504,35 @@ def run_sharded(args):
     dist.destroy_process_group()
 
 
+def _cube_scheme(args):
+    return "wireframe" if args.config == "config5" else "tweed"
+
+
 def _cube_workload(args):
-    from paper_2110_08389_b200 import grid
+    from paper_2110_08389_b200 import configs, grid
+    if args.config == "config5":
+        n = args.n or 1024
+        return n, configs.sinh_centre(n, 1.0, 3.0)
     n = args.n or 256
     return n, grid.make_tanh_wall(n, 1.0, 3.0)
 
 
-def _cube_desc(n):
+def _cube_rhs(args, n, device=True):
+    from paper_2110_08389_b200 import cube
+    return cube.config5_rhs(n, device) if args.config == "config5" else cube.config4_rhs(n, device)
+
+
+def _cube_desc(args, n):
+    if args.config == "config5":
+        return (f"config5: {n + 1}^3 nodes fp64, sinh centre gamma=3 on all axes, "
+                f"f = 2 Lcg64(4) - 1, 3D wireframe V(2,2), full weighting, trilinear")
     return (f"config4: {n + 1}^3 nodes fp64, tanh wall gamma=3 on all axes, "
             f"f = 2 Lcg64(3) - 1, 3D tweed V(2,2), full weighting, trilinear")
 
 
 def run_cube(args):
-    """BASELINE config 4 (3D tweed, 257^3) on one GPU (replicas under torchrun)."""
+    """BASELINE config 4 (3D tweed, 257^3) or config 5 (3D wireframe, 1025^3)
+    on one GPU (replicas under torchrun)."""
     import ctypes
 
     import torch
@@ -526,8 +542,9 @@ def run_cube(args):
     world, rank, local = _dist()
     torch.cuda.set_device(local % torch.cuda.device_count())
     n, x = _cube_workload(args)
-    h = cube.CubeHierarchy(x)
-    f = cube.config4_rhs(n)
+    scheme = _cube_scheme(args)
+    h = cube.CubeHierarchy(x, scheme=scheme)
+    f = _cube_rhs(args, n)
     u = torch.zeros_like(f)
     L = _lib.lib()
     stream = torch.cuda.current_stream()
@@ -551,24 +568,36 @@ def run_cube(args):
     upc = 2 * args.nu * h.interior_points()
     value = world * upc * args.steps / (t_ms * 1e-3)
     # dominant kernel: one finest-level 3D sweep
-    ws = torch.zeros_like(f)
+    # convergence factor over a few more cycles of the session (config 5 has
+    # no tolerance target: BASELINE quotes V-cycle time)
+    out = ctypes.c_double()
+    cube._check(L.tmg_cube_norm(h._h, ctypes.byref(out), sh))
+    norms = [out.value]
+    for _ in range(4):
+        cube._check(L.tmg_cube_cycles(h._h, args.nu, args.nu, 1, sh))
+        cube._check(L.tmg_cube_norm(h._h, ctypes.byref(out), sh))
+        norms.append(out.value)
+    ratios = [b / a for a, b in zip(norms, norms[1:]) if a > 0]
+    ws = u
+    ws.zero_()
+    nsw = 10 if n <= 512 else 3
     for _ in range(2):
         cube._check(L.tmg_cube_sweep(h._h, P(ws), P(f), sh))
     torch.cuda.synchronize()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record(stream)
-    for _ in range(10):
+    for _ in range(nsw):
         cube._check(L.tmg_cube_sweep(h._h, P(ws), P(f), sh))
     s1.record(stream)
     torch.cuda.synchronize()
-    sweep_ms = s0.elapsed_time(s1) / 10
+    sweep_ms = s0.elapsed_time(s1) / nsw
     alg = 24.0 * (n - 1) ** 3
     peak, peak_kind = _peak_hbm()
     # end to end: pinned host u, f in; u out; every step (serial)
     u_h = torch.zeros(f.shape, dtype=torch.float64).pin_memory()
     f_h = f.cpu().pin_memory()
     ue, fe = torch.empty_like(f), torch.empty_like(f)
-    cfg = mgcycle.CycleConfig(smoother="tweed", nu1=args.nu, nu2=args.nu)
+    cfg = mgcycle.CycleConfig(smoother=scheme, nu1=args.nu, nu2=args.nu)
 
     def e2e_step():
         fe.copy_(f_h, non_blocking=True)
@@ -578,7 +607,7 @@ def run_cube(args):
     e2e_step()
     torch.cuda.synchronize()
     x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ke = max(1, min(args.steps, 5))
+    ke = max(1, min(args.steps, 5 if n <= 512 else 2))
     x0.record(stream)
     for _ in range(ke):
         e2e_step()
@@ -586,8 +615,9 @@ def run_cube(args):
     torch.cuda.synchronize()
     e2e_ms = x0.elapsed_time(x1) / ke
     fb = f.numel() * 8
+    del ue, fe
     solve = None
-    if not args.no_solve:
+    if not args.no_solve and scheme == "tweed":
         cfg_s = mgcycle.CycleConfig(smoother="tweed", nu1=args.nu, nu2=args.nu, tol=1e-10)
         torch.cuda.synchronize()
         z0, z1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -602,15 +632,20 @@ def run_cube(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": _cube_desc(n), "levels": h.levels, "updates_per_cycle": upc,
+        "config": {"workload": _cube_desc(args, n), "levels": h.levels, "updates_per_cycle": upc,
                    "vcycle_ms": t_ms / args.steps,
                    "l2": "inputs larger than L2 (u, f = 2 x %.0f MB)" % (fb / 1e6),
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "achieved": alg / (sweep_ms * 1e-3) / 1e9, "peak": peak,
                      "unit": "GB/s", "frac": alg / (sweep_ms * 1e-3) / 1e9 / peak,
-                     "traffic": None, "kernel": "sweep3_kernel (one finest-level 3D sweep)",
+                     "traffic": None,
+                     "kernel": ("ring3_kernel + frame/point kernels (one finest-level 3D "
+                                "wireframe sweep)" if scheme == "wireframe" else
+                                "legs/branch kernels (one finest-level 3D tweed sweep)"),
                      "alg_bytes": alg, "ms": sweep_ms, "peak_kind": peak_kind},
         "solve": solve,
+        "convergence": {"cycles": len(ratios), "ratios": ratios,
+                        "rho": float(np.exp(np.mean(np.log(ratios)))) if ratios else None},
         "e2e": {"value": world * upc / (e2e_ms * 1e-3), "unit": "grid-pt updates/s",
                 "h2d_bytes_per_step": 2 * fb, "d2h_bytes_per_step": fb, "ms_per_step": e2e_ms},
         "clocks": clocks,
@@ -618,16 +653,32 @@ def run_cube(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle import oracle3d as o3
-        H = o3.Hierarchy3(x.values)
-        fh = f.cpu().numpy()
-        uo = np.zeros_like(fh)
-        t0 = time.perf_counter()
-        o3.v_cycle(H, uo, fh, args.nu, args.nu, 1)
-        secs = time.perf_counter() - t0
-        line["cpu_baseline"] = {"value": upc / secs, "unit": "grid-pt updates/s", "cores": 1,
-                                "kind": "port",
-                                "sample": f"one V({args.nu},{args.nu}) cycle of the same workload, "
-                                          f"3D C oracle, 1 thread ({secs:.1f} s)"}
+        if n <= 256:
+            H = o3.Hierarchy3(x.values, scheme=scheme)
+            fh = f.cpu().numpy()
+            uo = np.zeros_like(fh)
+            t0 = time.perf_counter()
+            o3.v_cycle(H, uo, fh, args.nu, args.nu, 1)
+            secs = time.perf_counter() - t0
+            sample = (f"one V({args.nu},{args.nu}) cycle of the same workload, 3D C oracle, "
+                      f"1 thread ({secs:.1f} s)")
+            cpu_v = upc / secs
+        else:  # bounded sample: >= 10 s of sweeps of the 257^3 cube of the same grid family
+            n_s = 256
+            xs = x.values[:: n // n_s].copy()
+            fs = np.ascontiguousarray(f[:: n // n_s, :: n // n_s, :: n // n_s].cpu().numpy())
+            us = np.zeros_like(fs)
+            st = o3.assemble3(xs, xs, xs)
+            nsw, t0 = 0, time.perf_counter()
+            while nsw == 0 or time.perf_counter() - t0 < 10.0:
+                o3.sweep(st, us, fs, 1, scheme)
+                nsw += 1
+            secs = time.perf_counter() - t0
+            cpu_v = nsw * (n_s - 1) ** 3 / secs
+            sample = (f"{nsw} 3D {scheme} sweeps of a 257^3 cube (every {n // n_s}th node of "
+                      f"the same grid), C oracle, 1 thread ({secs:.1f} s)")
+        line["cpu_baseline"] = {"value": cpu_v, "unit": "grid-pt updates/s", "cores": 1,
+                                "kind": "port", "sample": sample}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -640,34 +691,50 @@ def run_cube_reference(args):
     from oracle import oracle3d as o3
     from paper_2110_08389_b200 import cube
     n, x = _cube_workload(args)
-    H = o3.Hierarchy3(x.values)
-    f = cube.config4_rhs(n, device=False)
+    scheme = _cube_scheme(args)
     cores = orc.max_threads()
     times = []
-    for k in range(args.warmup + args.steps):
+    if n <= 256:  # one V-cycle of the workload per step
+        H = o3.Hierarchy3(x.values, scheme=scheme)
+        f = _cube_rhs(args, n, device=False)
+        steps, warm = args.steps, args.warmup
+        for k in range(warm + steps):
+            u = np.zeros_like(f)
+            t0 = time.perf_counter()
+            o3.v_cycle(H, u, f, args.nu, args.nu, cores)
+            if k >= warm:
+                times.append(time.perf_counter() - t0)
+        per = float(np.mean(times))
+        pts, m = 0, n
+        while True:
+            pts += (m - 1) ** 3
+            if m % 2 or m // 2 < 2:
+                break
+            m //= 2
+        value = 2 * args.nu * pts / per
+        sample = f"one V({args.nu},{args.nu}) cycle per step, 3D C oracle, {cores} OpenMP threads"
+    else:  # bounded: one finest-level sweep of the full grid per step (<= 3 steps)
+        st = o3.assemble3(x.values, x.values, x.values)
+        f = _cube_rhs(args, n, device=False)
         u = np.zeros_like(f)
-        t0 = time.perf_counter()
-        o3.v_cycle(H, u, f, args.nu, args.nu, cores)
-        if k >= args.warmup:
-            times.append(time.perf_counter() - t0)
-    per = float(np.mean(times))
-    pts, m = 0, n
-    while True:
-        pts += (m - 1) ** 3
-        if m % 2 or m // 2 < 2:
-            break
-        m //= 2
-    value = 2 * args.nu * pts / per
+        steps, warm = min(args.steps, 3), 1
+        for k in range(warm + steps):
+            t0 = time.perf_counter()
+            o3.sweep(st, u, f, cores, scheme)
+            if k >= warm:
+                times.append(time.perf_counter() - t0)
+        per = float(np.mean(times))
+        value = (n - 1) ** 3 / per
+        sample = (f"one finest-level 3D {scheme} sweep of the {n + 1}^3 workload per step "
+                  f"({steps} steps after {warm} warm-up), C oracle, {cores} OpenMP threads")
     line = {
         "impl": "reference", "metric": "smoother grid-pt updates/s", "value": value,
-        "unit": "grid-pt updates/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+        "unit": "grid-pt updates/s", "n_gpus": world, "steps": steps,
+        "warmup": warm, "ms_per_step": per * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": _cube_desc(n)},
+        "config": {"workload": _cube_desc(args, n)},
         "cpu_baseline": {"value": value, "unit": "grid-pt updates/s", "cores": cores,
-                         "kind": "port",
-                         "sample": f"one V({args.nu},{args.nu}) cycle per step, 3D C oracle, "
-                                   f"{cores} OpenMP threads"},
+                         "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "grid-pt updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -681,7 +748,7 @@ def main():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
     p.add_argument("--config", default="config3",
-                   choices=("config1", "config2", "config3", "config4"))
+                   choices=("config1", "config2", "config3", "config4", "config5"))
     p.add_argument("--intervals", "--n", dest="n", type=int, default=None,
                    help="override grid intervals (use --intervals under torchrun)")
     p.add_argument("--nu", type=int, default=2, help="config3: V(nu,nu)")
@@ -692,7 +759,7 @@ def main():
     args = p.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.config == "config4":
+    if args.config in ("config4", "config5"):
         if args.impl == "reference":
             run_cube_reference(args)
         else:

@@ -15,6 +15,17 @@ struct Coef3 {
 
 __host__ __device__ inline long mirror(long x, long n) { return x < n - x ? x : n - x; }
 
+// reciprocal: the hardware approximation refined by two Newton steps (the
+// 2D solver's drcp, tmg_sweep.cu)
+__device__ __forceinline__ double rcp3(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 __device__ __forceinline__ size_t idx3(int n, int i, int j, int k) {
   return ((size_t)i * (n + 1) + j) * (size_t)(n + 1) + k;
 }

@@ -83,15 +83,31 @@ __device__ __forceinline__ void ring_pos(const RingG& G, int n, int p, int& s, i
   else { pb = t; pc = n - t - off; }
 }
 
-// Row of ring position p: frozen right-hand side r (all neighbours off the
-// ring), diagonal d, couplings toward p-1 (am) and p+1 (cn), element offset o.
-// In-face directions: 0 = b-, 1 = b+, 2 = c-, 3 = c+; side s runs toward
-// fwd(s) = {1, 3, 0, 2}[s].
-__device__ __forceinline__ void ring_row(const RingG& G, int n, const double* __restrict__ u,
-                                         const double* __restrict__ f, int p, double& r,
-                                         double& d, double& am, double& cn, size_t& o) {
+// A position on the ring: side s, offset off along it, in-face coordinates.
+struct RingW {
   int s, off, pb, pc;
-  ring_pos(G, n, p, s, off, pb, pc);
+  __device__ __forceinline__ void init(const RingG& G, int n, int p) { ring_pos(G, n, p, s, off, pb, pc); }
+  // one step toward p + 1
+  __device__ __forceinline__ void next(const RingG& G) {
+    if (++off == G.m) {
+      off = 0;
+      ++s;
+    }
+    // the corner that opens side s has the previous side's direction applied
+    const int ds = off == 0 ? s - 1 : s;
+    pb += ds == 0 ? 1 : (ds == 2 ? -1 : 0);
+    pc += ds == 1 ? 1 : (ds == 3 ? -1 : 0);
+  }
+};
+
+// Row of the ring point at walker W: frozen right-hand side r (all
+// neighbours off the ring), diagonal d, couplings toward p-1 (am) and p+1
+// (cn), element offset o.  In-face directions: 0 = b-, 1 = b+, 2 = c-, 3 =
+// c+; side s runs toward fwd(s) = {1, 3, 0, 2}[s].
+__device__ __forceinline__ void ring_row(const RingG& G, const double* __restrict__ u,
+                                         const double* __restrict__ f, const RingW& W, double& r,
+                                         double& d, double& am, double& cn, size_t& o) {
+  const int s = W.s, off = W.off, pb = W.pb, pc = W.pc;
   o = G.base + (size_t)pb * G.sb + (size_t)pc * G.sc;
   const double c0 = __ldg(G.lob + pb), c1 = __ldg(G.hib + pb), c2 = __ldg(G.loc + pc),
                c3 = __ldg(G.hic + pc);
@@ -111,11 +127,6 @@ __device__ __forceinline__ void ring_row(const RingG& G, int n, const double* __
   cn = dnext == 0 ? c0 : (dnext == 1 ? c1 : (dnext == 2 ? c2 : c3));
 }
 
-__device__ __forceinline__ size_t ring_off(const RingG& G, int n, int p) {
-  int s, off, pb, pc;
-  ring_pos(G, n, p, s, off, pb, pc);
-  return G.base + (size_t)pb * G.sb + (size_t)pc * G.sc;
-}
 
 template <int TR>
 __global__ void __launch_bounds__(TR > 256 ? TR : 256)
@@ -139,13 +150,17 @@ __global__ void __launch_bounds__(TR > 256 ? TR : 256)
   double rho[kQW], lam[kQW], ivr[kQW], cc[kQW];
   bool bad = false;
   double bp = 0.0, rp = 0.0, lm = 0.0, cprev = 0.0, a_first = 0.0;
-  double r_end = 0.0, b_end = 1.0, a_end = 0.0, c_end = 0.0;
+  double r_end = 0.0, b_end = 1.0, a_end = 0.0, c_end = 0.0, ivp = 0.0;
+  RingW W0;
+  W0.init(G, n, min(p0, Lg));
+  RingW W = W0;
 #pragma unroll
   for (int k = 0; k < kQW; k++) {
     if (k > nI) continue;
     double r, d, am, cn;
     size_t o;
-    ring_row(G, n, u, f, p0 + k, r, d, am, cn, o);
+    if (k > 0) W.next(G);
+    ring_row(G, u, f, W, r, d, am, cn, o);
     cc[k] = cn;
     if (k == 0) a_first = am;
     if (k == nI) {  // the chunk end keeps its raw row for the reduced system
@@ -160,15 +175,16 @@ __global__ void __launch_bounds__(TR > 256 ? TR : 256)
       rp = r;
       lm = -am;
     } else {
-      const double w = am / bp;
+      const double w = am * ivp;
       bp = d - w * cprev;
       rp = r - w * rp;
       lm = -w * lm;
     }
     bad |= wbad(bp);
+    ivp = rcp3(bp);
     rho[k] = rp;
     lam[k] = lm;
-    ivr[k] = 1.0 / bp;
+    ivr[k] = ivp;
     cprev = cn;
   }
   // affine back pass: x_k = alpha + beta X_left + gamma X_end
@@ -235,7 +251,7 @@ __global__ void __launch_bounds__(TR > 256 ? TR : 256)
       Ap = sA[tid + dd]; Bp = sB[tid + dd]; Cp = sC[tid + dd]; Dp = sD[tid + dd]; Hp = sH[tid + dd];
     }
     __syncthreads();
-    const double k1 = A / Bm, k2 = Cc / Bp;
+    const double k1 = A * rcp3(Bm), k2 = Cc * rcp3(Bp);
     A = -k1 * Am;
     Cc = -k2 * Cp;
     B = B - k1 * Cm - k2 * Ap;
@@ -245,14 +261,17 @@ __global__ void __launch_bounds__(TR > 256 ? TR : 256)
     __syncthreads();
   }
   bad |= cnt > 0 && wbad(B);
-  const double P = D / B, Qh = H / B;  // X_end = P - Qh x_hub
+  const double iB = rcp3(B);
+  const double P = D * iB, Qh = H * iB;  // X_end = P - Qh x_hub
   sD[tid] = P;
   sH[tid] = Qh;
   __syncthreads();
   if (live && lt == 0) {  // the hub row
     double r, d, am, cn;
     size_t o;
-    ring_row(G, n, u, f, Lg, r, d, am, cn, o);
+    RingW Wh;
+    Wh.init(G, n, Lg);
+    ring_row(G, u, f, Wh, r, d, am, cn, o);
     const int last = tid + (Lg - 1) / q;
     const double Pl = sD[last], Ql = sH[last];
     const double num = r - am * Pl - cn * (au + gu * P);
@@ -267,10 +286,12 @@ __global__ void __launch_bounds__(TR > 256 ? TR : 256)
     const double xh = sX[tid / TR];
     const double X = P - Qh * xh;
     const double Xl = lt == 0 ? xh : sD[tid - 1] - sH[tid - 1] * xh;
+    RingW Wf = W0;
 #pragma unroll
     for (int k = 0; k < kQW; k++) {
       if (k > nI) continue;
-      const size_t o = ring_off(G, n, p0 + k);
+      if (k > 0) Wf.next(G);
+      const size_t o = G.base + (size_t)Wf.pb * G.sb + (size_t)Wf.pc * G.sc;
       u[o] = k == nI ? X : rho[k] + lam[k] * Xl + ivr[k] * X;
     }
   }
@@ -307,7 +328,8 @@ __global__ void __launch_bounds__(128) frame_edge_kernel(int n, Coef3 c, const W
   const size_t base = ((size_t)p[0] * n1 + p[1]) * (size_t)n1 + p[2];
   double* s = scr + 4 * (size_t)E.off;
   bool bad = false;
-  double bp = 0.0, rp = 0.0, lm = 0.0, cprev = 0.0;
+  double bp = 0.0, rp = 0.0, lm = 0.0, cprev = 0.0, ivp = 0.0;
+#pragma unroll 4
   for (int k = 0; k < e; k++) {
     const int xx = r + 1 + k;
     const size_t o = base + (size_t)xx * str[x];
@@ -320,29 +342,31 @@ __global__ void __launch_bounds__(128) frame_edge_kernel(int n, Coef3 c, const W
       rp = rr;
       lm = -am;
     } else {
-      const double w = am / bp;
+      const double w = am * ivp;
       bp = d - w * cprev;
       rp = rr - w * rp;
       lm = -w * lm;
     }
     bad |= wbad(bp);
+    ivp = rcp3(bp);
     cprev = cn;
     s[4 * k + 0] = rp;
     s[4 * k + 1] = lm;
     s[4 * k + 2] = cn;
-    s[4 * k + 3] = bp;
+    s[4 * k + 3] = ivp;
   }
   double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll 4
   for (int k = e - 1; k >= 0; k--) {
-    const double rk = s[4 * k + 0], lk = s[4 * k + 1], ck = s[4 * k + 2], bk = s[4 * k + 3];
+    const double rk = s[4 * k + 0], lk = s[4 * k + 1], ck = s[4 * k + 2], ik = s[4 * k + 3];
     if (k == e - 1) {
-      al = rk / bk;
-      be = lk / bk;
-      ga = -ck / bk;
+      al = rk * ik;
+      be = lk * ik;
+      ga = -ck * ik;
     } else {
-      al = (rk - ck * al) / bk;
-      be = (lk - ck * be) / bk;
-      ga = -ck * ga / bk;
+      al = (rk - ck * al) * ik;
+      be = (lk - ck * be) * ik;
+      ga = -ck * ga * ik;
     }
     s[4 * k + 0] = al;
     s[4 * k + 1] = be;
@@ -439,6 +463,7 @@ __global__ void __launch_bounds__(128) frame_back_kernel(int n, const WEdge* __r
   p[x] = 0;
   const size_t base = ((size_t)p[0] * n1 + p[1]) * (size_t)n1 + p[2];
   const double* s = scr + 4 * (size_t)E.off;
+#pragma unroll 4
   for (int k = 0; k < e; k++)
     u[base + (size_t)(r + 1 + k) * str[x]] = s[4 * k] + s[4 * k + 1] * x0 + s[4 * k + 2] * x1;
 }
@@ -481,12 +506,17 @@ int upload(const std::vector<T>& v, T** out, std::string& err) {
 
 int wire_build_level(int n, WLevel& L, std::string& err) {
   const int c = n / 2;
-  // rings, ordered (axis, level, face coordinate) so that the rings in flight
-  // together share rows and sectors of f and u
+  // Rings in launch order so that same-colour rings sharing 32-byte sectors
+  // run together: a sector holds four consecutive k.  On faces normal to i or
+  // j the k-neighbours of a strided side point are rings t +- 1, t +- 2 of
+  // the same face: order (a, xa, t).  On faces normal to k they are the
+  // faces of shells s1 +- 1, s1 +- 2: order (a, t, xa).
   std::vector<Ring3> rg[2][kRingClasses];
   for (int a = 0; a < 3; a++)
-    for (int t = 2; t < c; t++)
-      for (int xa = 1; xa < n; xa++) {
+    for (int outer = 1; outer < n; outer++)
+      for (int inner = 1; inner < n; inner++) {
+        const int t = a == 2 ? outer : inner, xa = a == 2 ? inner : outer;
+        if (t < 2 || t >= c) continue;
         const long s1 = mirror(xa, n);
         if (s1 >= t) continue;
         const int Lg = 4 * (n - 2 * t) - 1;
