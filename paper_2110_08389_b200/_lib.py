@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtmg_b200.so")
+LIB_PATH = os.environ.get("TMG_LIB_PATH") or os.path.join(_HERE, "libtmg_b200.so")  # override: A/B runs
 
 TMG_OK, TMG_SINGULAR, TMG_BADARG, TMG_CUDA = 0, 1, 2, 3
 

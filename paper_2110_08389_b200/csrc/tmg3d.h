@@ -32,12 +32,11 @@ __device__ __forceinline__ size_t idx3(int n, int i, int j, int k) {
 
 // ---------------------------------------------------------------------------
 // 3D wireframe (tmg3dw.cu).  Blocks of one level and colour:
-//   rings  closed square rings of a shell face, one CTA slice of TR threads
-//          per ring, grouped in classes by TR (kRingClasses);
-//   frames the 12-edge / 8-corner frame of a shell (red only): per-edge
-//          elimination, an 8x8 corner solve, per-edge back substitution;
+//   rings  closed square rings of a shell face: 4 edges between 4 corners,
+//          grouped in classes by the threads per edge (kRingClasses);
+//   frames the 12-edge / 8-corner frame of a shell (red only);
 //   points face centres and the cube centre.
-constexpr int kRingClasses = 5;  // TR = 32, 64, 128, 256, 512 threads per ring
+constexpr int kRingClasses = 7;  // TE = 1 .. 64 threads per ring side
 
 struct Ring3 {
   int16_t a;   // axis normal to the face
@@ -45,24 +44,13 @@ struct Ring3 {
   int32_t xa;  // coordinate of the face along a
 };
 
-struct WEdge {
-  int32_t r;      // shell
-  int32_t off;    // first scratch slot of the edge (e = n - 2r - 1 points)
-  int32_t frame;  // index of the frame in the level's frame list
-  uint8_t ax, k0, k1, slot;  // axis; start / end corner (bit a: coordinate n - r); edge 0..11
-};
-
 struct WLevel {
   Ring3* rings[2][kRingClasses] = {};
   int nrings[2][kRingClasses] = {};
-  WEdge* edges = nullptr;  // red frames only
-  int nedges = 0;
   int* frames = nullptr;   // shell r of each frame
   int nframes = 0;
   int4* points[2] = {};
   int npoints[2] = {};
-  double* scratch = nullptr;   // 4 doubles per frame edge point
-  double* ends = nullptr;      // per edge: first and last point forms (6 doubles)
 };
 
 int wire_build_level(int n, WLevel& L, std::string& err);

@@ -10,17 +10,25 @@
 //             red = even.
 // The checker is oracle/wire3d_oracle.c (same layout, same ring order).
 //
-// Rings hold ~all the points.  One slice of TR threads per ring (TR = 32 ..
-// 512 by ring length, several rings per 256-thread CTA for the short ones):
-// the ring minus its closing point (the hub, the last point of the 2D ring
-// order) is cut into chunks of <= 8 points, one per thread; each thread
-// eliminates its chunk in registers to x = alpha + beta * X_left + gamma *
-// X_end, the chunk ends form a tridiagonal system with a hub column (PCR in
-// shared memory), one thread per ring solves the hub row, every thread
-// finalises its chunk.  The 2D analogue is tmg_sweep.cu phases B-C.
-// Frames (0.3 % of the points at 1025^3) are eliminated per edge with the two
-// corner values as columns, the 8 corner rows are solved densely, and the
-// edges are back-substituted.
+// Device design: rings and frames are the same kind of block, straight
+// edges between corners — a ring is 4 edges and 4 corners, a frame 12 edges
+// and 8 corners — so every edge point is addressed as corner + q * stride
+// and its row needs two 1D couplings and a per-edge constant.  One slice of
+// TE threads per edge, <= kQW points per thread:
+//  1. gather (one point per lane, coalesced along k): the frozen right-hand
+//     side of every edge point into shared memory, and the corner rows;
+//  2. per thread, backward elimination of its chunk and the affine forms of
+//     its first and last interior points (chunk_eliminate);
+//  3. per edge, the chunk ends' tridiagonal system with the two corner
+//     values as columns, PCR in shared memory: every chunk end is
+//     X = P - Q0 x_K0 - Q1 x_K1;
+//  4. the corner rows with the edges' end points substituted: a dense 4 x 4
+//     (ring) or 8 x 8 (frame, the survey's reduction to the corner unknowns)
+//     system, one thread per block, partial pivoting;
+//  5. every chunk finalised with both ends known (chunk_finalise), and a
+//     coalesced scatter.
+// The solve is exact for the block (the reference's block Gauss-Seidel
+// step); only the elimination order differs from the circulant Thomas.
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -31,441 +39,438 @@
 namespace tmg3 {
 namespace {
 
-constexpr int kQW = 8;  // ring points per thread
+constexpr int kQW = 16;      // edge points per thread (one chunk)
+constexpr int kRBD = 256;    // threads per ring CTA
+constexpr int kMaxN = 1028;  // edges of <= 64 * kQW points
 
 __device__ __forceinline__ bool wbad(double v) { return v > -1e-300 && v < 1e-300; }
 
-__device__ __forceinline__ const double* lo_of(const Coef3& c, int a) {
-  return a == 0 ? c.W : (a == 1 ? c.S : c.B);
-}
-__device__ __forceinline__ const double* hi_of(const Coef3& c, int a) {
-  return a == 0 ? c.E : (a == 1 ? c.N : c.T);
-}
+// padded index into the shared-memory coupling tables: chunk-per-thread
+// accesses (lane stride kQW points) land in distinct banks
+__device__ __forceinline__ int tix(int x) { return x + (x >> 4); }
+__host__ __device__ constexpr int tab_len(int n) { return n + 1 + (n + 1) / 16 + 1; }
 
-// hoisted geometry of one ring: face normal a at xa, in-face axes b < c
-struct RingG {
-  const double *lob, *hib, *loc, *hic;
-  double kal, kah;  // couplings across the face (constant on the ring)
-  long sa, sb, sc;
-  size_t base;
-  int t, m;
+// shared-memory slot of edge point q: chunk rows of kQW, XOR swizzled so
+// that both the chunk-per-thread and the point-per-lane accesses are
+// conflict free
+__device__ __forceinline__ int rsw(int p) { return (p & ~(kQW - 1)) | ((p ^ (p >> 4)) & (kQW - 1)); }
+
+// A block: a ring (NE = 4: face normal a at xa, level t) or a frame
+// (NE = 12: shell t).  Corners: ring K = 0..3 at in-face (b, c) = (t, t),
+// (n-t, t), (n-t, n-t), (t, n-t) (layout.py:136-143's ring order: side 0
+// runs K0 -> K1, side 1 K1 -> K2, side 2 K2 -> K3, side 3 K3 -> K0); frame K
+// = 0..7 with bit a set for coordinate n - t on axis a.
+struct WBlk {
+  int a, xa, t;
 };
 
-__device__ __forceinline__ RingG ring_geom(const Coef3& c, int n, const Ring3& R) {
-  RingG G;
-  const int a = R.a, b = a == 0 ? 1 : 0, cc = a == 2 ? 1 : 2;
-  const long n1 = n + 1;
-  auto str = [n1](int x) { return x == 0 ? n1 * n1 : (x == 1 ? n1 : 1L); };
-  G.lob = lo_of(c, b);
-  G.hib = hi_of(c, b);
-  G.loc = lo_of(c, cc);
-  G.hic = hi_of(c, cc);
-  G.kal = __ldg(lo_of(c, a) + R.xa);
-  G.kah = __ldg(hi_of(c, a) + R.xa);
-  G.sa = str(a);
-  G.sb = str(b);
-  G.sc = str(cc);
-  G.base = (size_t)R.xa * G.sa;
-  G.t = R.t;
-  G.m = n - 2 * R.t;
+template <int NE>
+__device__ __forceinline__ void corner_pos(const WBlk& B, int n, int K, int P[3]) {
+  if (NE == 12) {
+    P[0] = K & 1 ? n - B.t : B.t;
+    P[1] = K & 2 ? n - B.t : B.t;
+    P[2] = K & 4 ? n - B.t : B.t;
+  } else {
+    const int pb = (K == 1 || K == 2) ? n - B.t : B.t, pc = K >= 2 ? n - B.t : B.t;
+    P[0] = B.a == 0 ? B.xa : pb;
+    P[1] = B.a == 1 ? B.xa : (B.a == 0 ? pb : pc);
+    P[2] = B.a == 2 ? B.xa : pc;
+  }
+}
+
+// edge e: axis x, from corner K0 (lower coordinate) to K1
+template <int NE>
+__device__ __forceinline__ void edge_def(const WBlk& B, int e, int& x, int& K0, int& K1) {
+  if (NE == 12) {
+    x = e >> 2;
+    const int h = e & 3, o1 = x == 0 ? 1 : 0, o2 = x == 2 ? 1 : 2;
+    K0 = ((h & 1) << o1) | (((h >> 1) & 1) << o2);
+    K1 = K0 | (1 << x);
+  } else {
+    const int b = B.a == 0 ? 1 : 0, c = B.a == 2 ? 1 : 2;
+    x = (e & 1) ? c : b;
+    K0 = e == 0 ? 0 : (e == 1 ? 1 : (e == 2 ? 3 : 0));
+    K1 = e == 0 ? 1 : (e == 1 ? 2 : (e == 2 ? 2 : 3));
+  }
+}
+
+// One edge's hoisted geometry: point q (0 .. L-1) at offset o0 + (q+1) sx,
+// coordinate x0 + 1 + q along the axis; the four transverse couplings are
+// constant along the edge.
+struct EdgeG {
+  double t0, t1, t2, t3, tsum;
+  long sx, so1, so2;
+  size_t o0;
+  int x0, L;
+};
+
+// The cube API builds every axis from one coordinate array
+// (tmg_cube_create), so W = S = B and E = N = T: c.W / c.E serve every axis.
+template <int NE>
+__device__ __forceinline__ EdgeG edge_geom(const Coef3& c, int n, const WBlk& B, int e) {
+  int x, K0, K1, P0[3], P1[3];
+  edge_def<NE>(B, e, x, K0, K1);
+  corner_pos<NE>(B, n, K0, P0);
+  corner_pos<NE>(B, n, K1, P1);
+  const int o1 = x == 0 ? 1 : 0, o2 = x == 2 ? 1 : 2;
+  const long n1 = n + 1, str[3] = {n1 * n1, n1, 1};
+  EdgeG G;
+  const int p1 = o1 == 0 ? P0[0] : P0[1], p2 = o2 == 1 ? P0[1] : P0[2];
+  G.t0 = __ldg(c.W + p1);
+  G.t1 = __ldg(c.E + p1);
+  G.t2 = __ldg(c.W + p2);
+  G.t3 = __ldg(c.E + p2);
+  G.tsum = G.t0 + G.t1 + G.t2 + G.t3;
+  G.sx = str[x];
+  G.so1 = str[o1];
+  G.so2 = str[o2];
+  G.o0 = ((size_t)P0[0] * n1 + P0[1]) * (size_t)n1 + P0[2];
+  G.x0 = x == 0 ? P0[0] : (x == 1 ? P0[1] : P0[2]);
+  const int x1 = x == 0 ? P1[0] : (x == 1 ? P1[1] : P1[2]);
+  G.L = x1 - G.x0 - 1;
   return G;
 }
 
-// in-face coordinates of ring position p (layout.py:136-143 in the face)
-__device__ __forceinline__ void ring_pos(const RingG& G, int n, int p, int& s, int& off, int& pb,
-                                         int& pc) {
-  s = p / G.m;
-  off = p - s * G.m;
-  const int t = G.t;
-  if (s == 0) { pb = t + off; pc = t; }
-  else if (s == 1) { pb = n - t; pc = t + off; }
-  else if (s == 2) { pb = n - t - off; pc = n - t; }
-  else { pb = t; pc = n - t - off; }
-}
-
-// A position on the ring: side s, offset off along it, in-face coordinates.
-struct RingW {
-  int s, off, pb, pc;
-  __device__ __forceinline__ void init(const RingG& G, int n, int p) { ring_pos(G, n, p, s, off, pb, pc); }
-  // one step toward p + 1
-  __device__ __forceinline__ void next(const RingG& G) {
-    if (++off == G.m) {
-      off = 0;
-      ++s;
-    }
-    // the corner that opens side s has the previous side's direction applied
-    const int ds = off == 0 ? s - 1 : s;
-    pb += ds == 0 ? 1 : (ds == 2 ? -1 : 0);
-    pc += ds == 1 ? 1 : (ds == 3 ? -1 : 0);
+// Row of edge point q from the shared-memory coupling tables: the along
+// couplings toward q-1 (am) and q+1 (cn), the diagonal d.
+struct EdgeCpl {
+  const EdgeG& G;
+  const double *tlo, *thi;
+  __device__ __forceinline__ void operator()(int q, double& am, double& d, double& cn) const {
+    const int xx = tix(G.x0 + 1 + q);
+    am = tlo[xx];
+    cn = thi[xx];
+    d = -(am + cn + G.tsum);
   }
 };
 
-// Row of the ring point at walker W: frozen right-hand side r (all
-// neighbours off the ring), diagonal d, couplings toward p-1 (am) and p+1
-// (cn), element offset o.  In-face directions: 0 = b-, 1 = b+, 2 = c-, 3 =
-// c+; side s runs toward fwd(s) = {1, 3, 0, 2}[s].
-__device__ __forceinline__ void ring_row(const RingG& G, const double* __restrict__ u,
-                                         const double* __restrict__ f, const RingW& W, double& r,
-                                         double& d, double& am, double& cn, size_t& o) {
-  const int s = W.s, off = W.off, pb = W.pb, pc = W.pc;
-  o = G.base + (size_t)pb * G.sb + (size_t)pc * G.sc;
-  const double c0 = __ldg(G.lob + pb), c1 = __ldg(G.hib + pb), c2 = __ldg(G.loc + pc),
-               c3 = __ldg(G.hic + pc);
-  const int fwd_s = s == 0 ? 1 : (s == 1 ? 3 : (s == 2 ? 0 : 2));
-  const int sp = off > 0 ? s : (s + 3) & 3;
-  const int fwd_p = sp == 0 ? 1 : (sp == 1 ? 3 : (sp == 2 ? 0 : 2));
-  const int dnext = fwd_s, dprev = fwd_p ^ 1;
-  const unsigned in = (1u << dnext) | (1u << dprev);  // the two ring directions
-  d = -(c0 + c1 + c2 + c3 + G.kal + G.kah);
-  double rr = f[o] - G.kal * u[o - G.sa] - G.kah * u[o + G.sa];
-  if (!(in & 1u)) rr -= c0 * u[o - G.sb];
-  if (!(in & 2u)) rr -= c1 * u[o + G.sb];
-  if (!(in & 4u)) rr -= c2 * u[o - G.sc];
-  if (!(in & 8u)) rr -= c3 * u[o + G.sc];
-  r = rr;
-  am = dprev == 0 ? c0 : (dprev == 1 ? c1 : (dprev == 2 ? c2 : c3));
-  cn = dnext == 0 ? c0 : (dnext == 1 ? c1 : (dnext == 2 ? c2 : c3));
+// Chunk passes.  A thread owns the chunk points p0 .. p0+e (e <= kQW-1); the
+// interior 0 .. e-1 couples to X_left (the previous chunk's end, or a
+// corner) and X_end (point e).  Backward elimination from e-1 down to 0
+// leaves every interior row as
+//   x_k = Rq_k + Mu_k X_end - Am_k x_{k-1}        (x_{-1} = X_left),
+// Rq in shared memory (over r), Mu / Am in registers; a forward pass over
+// those gives the affine forms of the first and last interior points, and the
+// same recurrence finalises the chunk once X_left / X_end are known.
+struct ChunkForms {
+  double au = 0.0, bu = 0.0, gu = 1.0;  // x_0     = au + bu X_left + gu X_end
+  double ad = 0.0, bd = 0.0, gd = 0.0;  // x_{e-1} = ad + bd X_left + gd X_end
+};
+
+template <class CPL>
+__device__ __forceinline__ ChunkForms chunk_eliminate(const CPL& cpl, double* rr, int p0, int e,
+                                                      double (&mu)[kQW - 1], double (&amq)[kQW - 1],
+                                                      bool& bad) {
+  ChunkForms F;
+  if (e <= 0) return F;
+  double bq = 0.0, rq = 0.0, m = 0.0, anext = 0.0, ivq = 0.0;
+#pragma unroll
+  for (int k = kQW - 2; k >= 0; k--) {
+    if (k < e) {
+      double am, d, cn;
+      cpl(p0 + k, am, d, cn);
+      const int sl = rsw(p0 + k);
+      const double r = rr[sl];
+      if (k == e - 1) {
+        bq = d;
+        rq = r;
+        m = -cn;
+      } else {
+        const double w = cn * ivq;
+        bq = d - w * anext;
+        rq = r - w * rq;
+        m = -w * m;
+      }
+      bad |= wbad(bq);
+      ivq = rcp3(bq);
+      anext = am;
+      rr[sl] = rq * ivq;
+      mu[k] = m * ivq;
+      amq[k] = am * ivq;
+    }
+  }
+  double al = 0.0, be = 1.0, ga = 0.0;
+#pragma unroll
+  for (int k = 0; k < kQW - 1; k++) {
+    if (k < e) {
+      const double rq_k = rr[rsw(p0 + k)];
+      al = rq_k - amq[k] * al;
+      be = -amq[k] * be;
+      ga = mu[k] - amq[k] * ga;
+      if (k == 0) {
+        F.au = al;
+        F.bu = be;
+        F.gu = ga;
+      }
+    }
+  }
+  F.ad = al;
+  F.bd = be;
+  F.gd = ga;
+  return F;
 }
 
+__device__ __forceinline__ void chunk_finalise(double* rr, int p0, int e, double XL, double XE,
+                                               const double (&mu)[kQW - 1],
+                                               const double (&amq)[kQW - 1]) {
+  double x = XL;
+#pragma unroll
+  for (int k = 0; k < kQW - 1; k++) {
+    if (k < e) {
+      const int sl = rsw(p0 + k);
+      x = rr[sl] + mu[k] * XE - amq[k] * x;
+      rr[sl] = x;
+    }
+  }
+  rr[rsw(p0 + e)] = XE;
+}
 
-template <int TR>
-__global__ void __launch_bounds__(TR > 256 ? TR : 256)
-    ring3_kernel(int n, Coef3 c, const Ring3* __restrict__ rings, int nr, double* __restrict__ u,
-                 const double* __restrict__ f, int* err) {
-  constexpr int BD = TR > 256 ? TR : 256;
-  __shared__ double sA[BD], sB[BD], sC[BD], sD[BD], sH[BD];
-  __shared__ double sX[BD / TR];
-  const int tid = threadIdx.x, lt = tid % TR;
-  const int rid = blockIdx.x * (BD / TR) + tid / TR;
-  const bool live = rid < nr;
-  Ring3 R;
-  if (live) R = rings[rid];
-  else { R.a = 0; R.t = 1; R.xa = 1; }
-  const RingG G = ring_geom(c, n, R);
-  const int Lg = 4 * G.m - 1;  // open chain: every ring point but the hub
-  const int q = (Lg + TR - 1) / TR;
-  const int p0 = lt * q;
-  const int cnt = live ? max(0, min(q, Lg - p0)) : 0;
-  const int nI = cnt - 1;
-  double rho[kQW], lam[kQW], ivr[kQW], cc[kQW];
-  bool bad = false;
-  double bp = 0.0, rp = 0.0, lm = 0.0, cprev = 0.0, a_first = 0.0;
-  double r_end = 0.0, b_end = 1.0, a_end = 0.0, c_end = 0.0, ivp = 0.0;
-  RingW W0;
-  W0.init(G, n, min(p0, Lg));
-  RingW W = W0;
-#pragma unroll
-  for (int k = 0; k < kQW; k++) {
-    if (k > nI) continue;
-    double r, d, am, cn;
-    size_t o;
-    if (k > 0) W.next(G);
-    ring_row(G, u, f, W, r, d, am, cn, o);
-    cc[k] = cn;
-    if (k == 0) a_first = am;
-    if (k == nI) {  // the chunk end keeps its raw row for the reduced system
-      r_end = r;
-      b_end = d;
-      a_end = am;
-      c_end = cn;
-      continue;
-    }
-    if (k == 0) {
-      bp = d;
-      rp = r;
-      lm = -am;
-    } else {
-      const double w = am * ivp;
-      bp = d - w * cprev;
-      rp = r - w * rp;
-      lm = -w * lm;
-    }
-    bad |= wbad(bp);
-    ivp = rcp3(bp);
-    rho[k] = rp;
-    lam[k] = lm;
-    ivr[k] = ivp;
-    cprev = cn;
+template <int NE, int TE, int BD>
+constexpr size_t wblock_smem() {
+  return ((size_t)BD * (kQW + 6) + 2 * (size_t)tab_len(kMaxN)) * sizeof(double);
+}
+
+// Blocks of one kind and class: BD / (NE TE) blocks per CTA, TE threads per
+// edge.  Blocks come from `rings` (NE = 4) or `frames` (NE = 12, the shell
+// index).
+template <int NE, int TE, int BD>
+__global__ void __launch_bounds__(BD, BD == kRBD ? 2 : 1)
+    wblock_kernel(int n, Coef3 c, const Ring3* __restrict__ rings, const int* __restrict__ frames,
+                  int nb, double* __restrict__ u, const double* __restrict__ f, int* err) {
+  constexpr int NK = NE == 4 ? 4 : 8;
+  constexpr int SL = NE * TE;  // threads per block
+  constexpr int BPC = BD / SL;
+  static_assert(BPC >= 1 && SL >= NK, "block slice");
+  extern __shared__ double wsm[];
+  double* sR = wsm;  // BD * kQW
+  double *sA = sR + BD * kQW, *sB = sA + BD, *sC = sB + BD, *sD = sC + BD, *sH0 = sD + BD,
+         *sH1 = sH0 + BD;
+  double *tlo = sH1 + BD, *thi = tlo + tab_len(n);
+  __shared__ double sEnd[BPC][NE][6];  // per edge: first / last point as al + be x_K0 + ga x_K1
+  __shared__ double sKr[BPC][NK], sKd[BPC][NK], sXc[BPC][NK];
+  const int tid = threadIdx.x, g = tid / SL, ed = (tid % SL) / TE, lt = tid % TE;
+  const int bid = blockIdx.x * BPC + g;
+  const bool live = bid < nb;
+  WBlk B;
+  if (NE == 4) {
+    Ring3 R;
+    if (live) R = rings[bid];
+    else { R.a = 0; R.t = 1; R.xa = 1; }
+    B.a = R.a; B.xa = R.xa; B.t = R.t;
+  } else {
+    B.a = 0; B.xa = 0; B.t = live ? frames[bid] : 1;
   }
-  // affine back pass: x_k = alpha + beta X_left + gamma X_end
-  double ad = 0.0, bd = 1.0, gd = 0.0, au = 0.0, bu = 0.0, gu = 1.0;
-  if (nI > 0) {
-    double al = 0.0, be = 0.0, ga = 0.0;
+  for (int x = tid; x <= n; x += BD) {
+    tlo[tix(x)] = __ldg(c.W + x);
+    thi[tix(x)] = __ldg(c.E + x);
+  }
+  const EdgeG G = edge_geom<NE>(c, n, B, ed);
+  const int L = live ? G.L : 0;
+  double* rr = sR + (g * NE + ed) * TE * kQW;
+  // 1. gather: edge points (four transverse neighbours), and the corner rows
+  {
+    constexpr int NB = 4;  // points whose loads are in flight together
+#pragma unroll 1
+    for (int i0 = 0; i0 < kQW; i0 += NB) {
+      if (lt + i0 * TE >= L) break;
+      double f0[NB], v0[NB], v1[NB], v2[NB], v3[NB];
 #pragma unroll
-    for (int k = kQW - 1; k >= 0; k--) {
-      if (k >= nI) continue;
-      if (k == nI - 1) {
-        al = rho[k] * ivr[k];
-        be = lam[k] * ivr[k];
-        ga = -cc[k] * ivr[k];
-        ad = al; bd = be; gd = ga;
-      } else {
-        al = (rho[k] - cc[k] * al) * ivr[k];
-        be = (lam[k] - cc[k] * be) * ivr[k];
-        ga = -cc[k] * ga * ivr[k];
+      for (int b = 0; b < NB; b++) {
+        const int q = min(lt + (i0 + b) * TE, L - 1);  // clamped: loads stay unconditional
+        const size_t o = G.o0 + (size_t)(q + 1) * G.sx;
+        f0[b] = f[o];
+        v0[b] = u[o - G.so1];
+        v1[b] = u[o + G.so1];
+        v2[b] = u[o - G.so2];
+        v3[b] = u[o + G.so2];
       }
-      rho[k] = al;
-      lam[k] = be;
-      ivr[k] = ga;
+#pragma unroll
+      for (int b = 0; b < NB; b++) {
+        const int q = lt + (i0 + b) * TE;
+        if (q < L)
+          rr[rsw(q)] = f0[b] - G.t0 * v0[b] - G.t1 * v1[b] - G.t2 * v2[b] - G.t3 * v3[b];
+      }
     }
-    au = al; bu = be; gu = ga;
   }
-  sA[tid] = au;
-  sB[tid] = bu;
-  sC[tid] = gu;
+  if (live && tid % SL < NK) {
+    const int K = tid % SL;
+    int P[3];
+    corner_pos<NE>(B, n, K, P);
+    unsigned in = 0;  // in-block directions: bit 2a (toward -), 2a+1 (toward +)
+    for (int e = 0; e < NE; e++) {
+      int x, K0, K1;
+      edge_def<NE>(B, e, x, K0, K1);
+      if (K0 == K) in |= 2u << (2 * x);
+      if (K1 == K) in |= 1u << (2 * x);
+    }
+    const long n1 = n + 1, str[3] = {n1 * n1, n1, 1};
+    const size_t o = ((size_t)P[0] * n1 + P[1]) * (size_t)n1 + P[2];
+    double d = 0.0, rk = f[o];
+    for (int a = 0; a < 3; a++) {
+      const double lo = __ldg(c.W + P[a]), hi = __ldg(c.E + P[a]);
+      d -= lo + hi;
+      if (!(in & (1u << (2 * a)))) rk -= lo * u[o - str[a]];
+      if (!(in & (2u << (2 * a)))) rk -= hi * u[o + str[a]];
+    }
+    sKr[g][K] = rk;
+    sKd[g][K] = d;
+  }
   __syncthreads();
-  // reduced row of the chunk end: A X_prev + B X + C X_next + H x_hub = D
-  double A = 0.0, B = 1.0, Cc = 0.0, D = 0.0, H = 0.0;
+  // 2. chunk eliminations
+  const EdgeCpl cpl{G, tlo, thi};
+  const int p0 = lt * kQW;
+  const int cnt = max(0, min(kQW, L - p0));
+  const int e = cnt - 1;
+  bool bad = false;
+  double mu[kQW - 1], amq[kQW - 1];
+  const ChunkForms Fm = chunk_eliminate(cpl, rr, p0, e, mu, amq, bad);
+  sA[tid] = Fm.au;
+  sB[tid] = Fm.bu;
+  sC[tid] = Fm.gu;
+  __syncthreads();
+  // 3. reduced row of the chunk end: A X_prev + B X + C X_next + H0 x_K0 + H1 x_K1 = D
+  double A = 0.0, Bv = 1.0, Cc = 0.0, D = 0.0, H0 = 0.0, H1 = 0.0;
   if (cnt > 0) {
-    const double ae = nI > 0 ? a_end : a_first;
-    if (nI > 0) {
-      A = ae * bd;
-      B = b_end + ae * gd;
-      D = r_end - ae * ad;
+    double ae, be, ce;
+    cpl(p0 + e, ae, be, ce);
+    const double re = rr[rsw(p0 + e)];
+    if (e > 0) {
+      A = ae * Fm.bd;
+      Bv = be + ae * Fm.gd;
+      D = re - ae * Fm.ad;
     } else {
       A = ae;
-      B = b_end;
-      D = r_end;
+      Bv = be;
+      D = re;
     }
-    if (p0 + cnt < Lg) {  // the next chunk's first point: an + bn X + gn X_next
-      B += c_end * sB[tid + 1];
-      Cc = c_end * sC[tid + 1];
-      D -= c_end * sA[tid + 1];
+    if (p0 + cnt < L) {  // the next chunk's first point: an + bn X + gn X_next
+      Bv += ce * sB[tid + 1];
+      Cc = ce * sC[tid + 1];
+      D -= ce * sA[tid + 1];
     } else {
-      H += c_end;  // the last leg point's successor is the hub
+      H1 = ce;  // the last edge point's successor is the end corner
     }
-    if (lt == 0) {  // the first point's predecessor is the hub
-      H += A;
+    if (lt == 0) {  // the first edge point's predecessor is the start corner
+      H0 = A;
       A = 0.0;
     }
   }
   __syncthreads();
-  sA[tid] = A; sB[tid] = B; sC[tid] = Cc; sD[tid] = D; sH[tid] = H;
+  sA[tid] = A; sB[tid] = Bv; sC[tid] = Cc; sD[tid] = D; sH0[tid] = H0; sH1[tid] = H1;
   __syncthreads();
-  for (int dd = 1; dd < TR; dd <<= 1) {
-    double Am = 0, Bm = 1, Cm = 0, Dm = 0, Hm = 0, Ap = 0, Bp = 1, Cp = 0, Dp = 0, Hp = 0;
+#pragma unroll
+  for (int dd = 1; dd < TE; dd <<= 1) {
+    double Am = 0, Bm = 1, Cm = 0, Dm = 0, Gm = 0, Hm = 0, Ap = 0, Bp = 1, Cp = 0, Dp = 0, Gp = 0,
+           Hp = 0;
     if (lt - dd >= 0) {
-      Am = sA[tid - dd]; Bm = sB[tid - dd]; Cm = sC[tid - dd]; Dm = sD[tid - dd]; Hm = sH[tid - dd];
+      Am = sA[tid - dd]; Bm = sB[tid - dd]; Cm = sC[tid - dd]; Dm = sD[tid - dd];
+      Gm = sH0[tid - dd]; Hm = sH1[tid - dd];
     }
-    if (lt + dd < TR) {
-      Ap = sA[tid + dd]; Bp = sB[tid + dd]; Cp = sC[tid + dd]; Dp = sD[tid + dd]; Hp = sH[tid + dd];
+    if (lt + dd < TE) {
+      Ap = sA[tid + dd]; Bp = sB[tid + dd]; Cp = sC[tid + dd]; Dp = sD[tid + dd];
+      Gp = sH0[tid + dd]; Hp = sH1[tid + dd];
     }
     __syncthreads();
     const double k1 = A * rcp3(Bm), k2 = Cc * rcp3(Bp);
     A = -k1 * Am;
     Cc = -k2 * Cp;
-    B = B - k1 * Cm - k2 * Ap;
+    Bv = Bv - k1 * Cm - k2 * Ap;
     D = D - k1 * Dm - k2 * Dp;
-    H = H - k1 * Hm - k2 * Hp;
-    sA[tid] = A; sB[tid] = B; sC[tid] = Cc; sD[tid] = D; sH[tid] = H;
+    H0 = H0 - k1 * Gm - k2 * Gp;
+    H1 = H1 - k1 * Hm - k2 * Hp;
+    sA[tid] = A; sB[tid] = Bv; sC[tid] = Cc; sD[tid] = D; sH0[tid] = H0; sH1[tid] = H1;
     __syncthreads();
   }
-  bad |= cnt > 0 && wbad(B);
-  const double iB = rcp3(B);
-  const double P = D * iB, Qh = H * iB;  // X_end = P - Qh x_hub
+  bad |= cnt > 0 && wbad(Bv);
+  const double iB = rcp3(Bv);
+  const double P = D * iB, Q0 = H0 * iB, Q1 = H1 * iB;  // X_end = P - Q0 x_K0 - Q1 x_K1
   sD[tid] = P;
-  sH[tid] = Qh;
-  __syncthreads();
-  if (live && lt == 0) {  // the hub row
-    double r, d, am, cn;
-    size_t o;
-    RingW Wh;
-    Wh.init(G, n, Lg);
-    ring_row(G, u, f, Wh, r, d, am, cn, o);
-    const int last = tid + (Lg - 1) / q;
-    const double Pl = sD[last], Ql = sH[last];
-    const double num = r - am * Pl - cn * (au + gu * P);
-    const double den = d - am * Ql + cn * (bu - gu * Qh);
-    bad |= wbad(den);
-    const double xh = num / den;
-    u[o] = xh;
-    sX[tid / TR] = xh;
-  }
-  __syncthreads();
-  if (cnt > 0) {
-    const double xh = sX[tid / TR];
-    const double X = P - Qh * xh;
-    const double Xl = lt == 0 ? xh : sD[tid - 1] - sH[tid - 1] * xh;
-    RingW Wf = W0;
-#pragma unroll
-    for (int k = 0; k < kQW; k++) {
-      if (k > nI) continue;
-      if (k > 0) Wf.next(G);
-      const size_t o = G.base + (size_t)Wf.pb * G.sb + (size_t)Wf.pc * G.sc;
-      u[o] = k == nI ? X : rho[k] + lam[k] * Xl + ivr[k] * X;
-    }
-  }
-  if (bad) atomicOr(err, 1);
-}
-
-// corner K of shell r: bit a set -> coordinate n - r on axis a
-__device__ __forceinline__ size_t corner_off(int n, int r, int K) {
-  const int i = K & 1 ? n - r : r, j = K & 2 ? n - r : r, k = K & 4 ? n - r : r;
-  return idx3(n, i, j, k);
-}
-
-// Per frame edge: Thomas from the start corner with the two corner values as
-// columns; scratch (4 per point) ends as alpha, beta, gamma; the first and
-// last point forms go to ends.
-__global__ void __launch_bounds__(128) frame_edge_kernel(int n, Coef3 c, const WEdge* __restrict__ edges,
-                                                         int ne, const double* __restrict__ u,
-                                                         const double* __restrict__ f,
-                                                         double* __restrict__ scr,
-                                                         double* __restrict__ ends, int* err) {
-  const int id = blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= ne) return;
-  const WEdge E = edges[id];
-  const int r = E.r, x = E.ax, e = n - 2 * r - 1;
-  const int o1 = x == 0 ? 1 : 0, o2 = x == 2 ? 1 : 2;
-  const long n1 = n + 1, str[3] = {n1 * n1, n1, 1};
-  int p[3];
-  for (int a = 0; a < 3; a++) p[a] = (E.k0 >> a) & 1 ? n - r : r;
-  const double t0 = __ldg(lo_of(c, o1) + p[o1]), t1 = __ldg(hi_of(c, o1) + p[o1]);
-  const double t2 = __ldg(lo_of(c, o2) + p[o2]), t3 = __ldg(hi_of(c, o2) + p[o2]);
-  const double tsum = t0 + t1 + t2 + t3;
-  const double *lox = lo_of(c, x), *hix = hi_of(c, x);
-  p[x] = 0;
-  const size_t base = ((size_t)p[0] * n1 + p[1]) * (size_t)n1 + p[2];
-  double* s = scr + 4 * (size_t)E.off;
-  bool bad = false;
-  double bp = 0.0, rp = 0.0, lm = 0.0, cprev = 0.0, ivp = 0.0;
-#pragma unroll 4
-  for (int k = 0; k < e; k++) {
-    const int xx = r + 1 + k;
-    const size_t o = base + (size_t)xx * str[x];
-    const double am = __ldg(lox + xx), cn = __ldg(hix + xx);
-    const double d = -(am + cn + tsum);
-    const double rr = f[o] - t0 * u[o - str[o1]] - t1 * u[o + str[o1]] - t2 * u[o - str[o2]] -
-                      t3 * u[o + str[o2]];
-    if (k == 0) {
-      bp = d;
-      rp = rr;
-      lm = -am;
+  sH0[tid] = Q0;
+  sH1[tid] = Q1;
+  if (cnt > 0 && lt == 0) {  // the first edge point
+    if (e > 0) {
+      sEnd[g][ed][0] = Fm.au + Fm.gu * P;
+      sEnd[g][ed][1] = Fm.bu - Fm.gu * Q0;
+      sEnd[g][ed][2] = -Fm.gu * Q1;
     } else {
-      const double w = am * ivp;
-      bp = d - w * cprev;
-      rp = rr - w * rp;
-      lm = -w * lm;
-    }
-    bad |= wbad(bp);
-    ivp = rcp3(bp);
-    cprev = cn;
-    s[4 * k + 0] = rp;
-    s[4 * k + 1] = lm;
-    s[4 * k + 2] = cn;
-    s[4 * k + 3] = ivp;
-  }
-  double al = 0.0, be = 0.0, ga = 0.0;
-#pragma unroll 4
-  for (int k = e - 1; k >= 0; k--) {
-    const double rk = s[4 * k + 0], lk = s[4 * k + 1], ck = s[4 * k + 2], ik = s[4 * k + 3];
-    if (k == e - 1) {
-      al = rk * ik;
-      be = lk * ik;
-      ga = -ck * ik;
-    } else {
-      al = (rk - ck * al) * ik;
-      be = (lk - ck * be) * ik;
-      ga = -ck * ga * ik;
-    }
-    s[4 * k + 0] = al;
-    s[4 * k + 1] = be;
-    s[4 * k + 2] = ga;
-    if (k == e - 1) {
-      ends[6 * (size_t)id + 3] = al;
-      ends[6 * (size_t)id + 4] = be;
-      ends[6 * (size_t)id + 5] = ga;
+      sEnd[g][ed][0] = P;
+      sEnd[g][ed][1] = -Q0;
+      sEnd[g][ed][2] = -Q1;
     }
   }
-  ends[6 * (size_t)id + 0] = al;
-  ends[6 * (size_t)id + 1] = be;
-  ends[6 * (size_t)id + 2] = ga;
-  if (bad) atomicOr(err, 1);
-}
-
-// Per frame: the 8 corner rows with the edge end forms substituted, solved by
-// Gaussian elimination with partial pivoting (as the oracle).
-__global__ void __launch_bounds__(64) frame_corner_kernel(int n, Coef3 c, const int* __restrict__ frames,
-                                                          int nf, const WEdge* __restrict__ edges,
-                                                          const double* __restrict__ ends,
-                                                          double* __restrict__ u,
-                                                          const double* __restrict__ f, int* err) {
-  const int fi = blockIdx.x * blockDim.x + threadIdx.x;
-  if (fi >= nf) return;
-  const int r = frames[fi];
-  double M[8][9];
-  for (int K = 0; K < 8; K++) {
-    const int p[3] = {K & 1 ? n - r : r, K & 2 ? n - r : r, K & 4 ? n - r : r};
-    const size_t o = idx3(n, p[0], p[1], p[2]);
-    const long n1 = n + 1, str[3] = {n1 * n1, n1, 1};
-    double d = 0.0, rr = f[o];
-    for (int a = 0; a < 3; a++) {
-      const double lo = __ldg(lo_of(c, a) + p[a]), hi = __ldg(hi_of(c, a) + p[a]);
-      d -= lo + hi;
-      // the in-frame neighbour lies toward the shell's inside
-      if (K >> a & 1) rr -= hi * u[o + str[a]];
-      else rr -= lo * u[o - str[a]];
+  if (cnt > 0 && p0 + cnt == L) {  // the last edge point
+    sEnd[g][ed][3] = P;
+    sEnd[g][ed][4] = -Q0;
+    sEnd[g][ed][5] = -Q1;
+  }
+  __syncthreads();
+  // 4. the corner rows with the edge end points substituted
+  if (live && tid % SL == 0) {
+    double M[NK][NK + 1];
+    for (int K = 0; K < NK; K++) {
+      for (int q = 0; q < NK; q++) M[K][q] = 0.0;
+      M[K][K] = sKd[g][K];
+      M[K][NK] = sKr[g][K];
     }
-    for (int q = 0; q < 8; q++) M[K][q] = 0.0;
-    M[K][K] = d;
-    M[K][8] = rr;
-  }
-  for (int ed = 0; ed < 12; ed++) {
-    const WEdge E = edges[12 * fi + ed];
-    const double* en = ends + 6 * (size_t)(12 * fi + ed);
-    const int x = E.ax, K0 = E.k0, K1 = E.k1;
-    const double c0 = __ldg(hi_of(c, x) + r), c1 = __ldg(lo_of(c, x) + (n - r));
-    M[K0][K0] += c0 * en[1];
-    M[K0][K1] += c0 * en[2];
-    M[K0][8] -= c0 * en[0];
-    M[K1][K0] += c1 * en[4];
-    M[K1][K1] += c1 * en[5];
-    M[K1][8] -= c1 * en[3];
-  }
-  bool bad = false;
-  for (int col = 0; col < 8; col++) {
-    int piv = col;
-    for (int rr = col + 1; rr < 8; rr++)
-      if (fabs(M[rr][col]) > fabs(M[piv][col])) piv = rr;
-    bad |= wbad(M[piv][col]);
-    if (piv != col)
-      for (int q = 0; q < 9; q++) {
-        const double tmp = M[col][q];
-        M[col][q] = M[piv][q];
-        M[piv][q] = tmp;
+    for (int eg = 0; eg < NE; eg++) {
+      int x, K0, K1, P0[3], P1[3];
+      edge_def<NE>(B, eg, x, K0, K1);
+      corner_pos<NE>(B, n, K0, P0);
+      corner_pos<NE>(B, n, K1, P1);
+      const int x0 = x == 0 ? P0[0] : (x == 1 ? P0[1] : P0[2]);
+      const int x1 = x == 0 ? P1[0] : (x == 1 ? P1[1] : P1[2]);
+      const double c0 = __ldg(c.E + x0), c1 = __ldg(c.W + x1);
+      M[K0][K0] += c0 * sEnd[g][eg][1];
+      M[K0][K1] += c0 * sEnd[g][eg][2];
+      M[K0][NK] -= c0 * sEnd[g][eg][0];
+      M[K1][K0] += c1 * sEnd[g][eg][4];
+      M[K1][K1] += c1 * sEnd[g][eg][5];
+      M[K1][NK] -= c1 * sEnd[g][eg][3];
+    }
+    for (int col = 0; col < NK; col++) {
+      int piv = col;
+      for (int q = col + 1; q < NK; q++)
+        if (fabs(M[q][col]) > fabs(M[piv][col])) piv = q;
+      bad |= wbad(M[piv][col]);
+      if (piv != col)
+        for (int q = 0; q <= NK; q++) {
+          const double tmp = M[col][q];
+          M[col][q] = M[piv][q];
+          M[piv][q] = tmp;
+        }
+      for (int q = col + 1; q < NK; q++) {
+        const double w = M[q][col] / M[col][col];
+        for (int v = col; v <= NK; v++) M[q][v] -= w * M[col][v];
       }
-    for (int rr = col + 1; rr < 8; rr++) {
-      const double w = M[rr][col] / M[col][col];
-      for (int q = col; q < 9; q++) M[rr][q] -= w * M[col][q];
+    }
+    for (int q = NK - 1; q >= 0; q--) {
+      double sum = M[q][NK];
+      for (int v = q + 1; v < NK; v++) sum -= M[q][v] * sXc[g][v];
+      sXc[g][q] = sum / M[q][q];
     }
   }
-  double xc[8];
-  for (int rr = 7; rr >= 0; rr--) {
-    double s = M[rr][8];
-    for (int q = rr + 1; q < 8; q++) s -= M[rr][q] * xc[q];
-    xc[rr] = s / M[rr][rr];
+  __syncthreads();
+  if (live && tid % SL < NK) {
+    int P3[3];
+    corner_pos<NE>(B, n, tid % SL, P3);
+    u[idx3(n, P3[0], P3[1], P3[2])] = sXc[g][tid % SL];
   }
-  for (int K = 0; K < 8; K++) u[corner_off(n, r, K)] = xc[K];
-  if (bad) atomicOr(err, 1);
-}
-
-__global__ void __launch_bounds__(128) frame_back_kernel(int n, const WEdge* __restrict__ edges, int ne,
-                                                         const double* __restrict__ scr,
-                                                         double* __restrict__ u) {
-  const int id = blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= ne) return;
-  const WEdge E = edges[id];
-  const int r = E.r, x = E.ax, e = n - 2 * r - 1;
-  const double x0 = u[corner_off(n, r, E.k0)], x1 = u[corner_off(n, r, E.k1)];
-  const long n1 = n + 1, str[3] = {n1 * n1, n1, 1};
-  int p[3];
-  for (int a = 0; a < 3; a++) p[a] = (E.k0 >> a) & 1 ? n - r : r;
-  p[x] = 0;
-  const size_t base = ((size_t)p[0] * n1 + p[1]) * (size_t)n1 + p[2];
-  const double* s = scr + 4 * (size_t)E.off;
+  // 5. finalise every chunk with both ends known, then scatter
+  if (cnt > 0) {
+    int x, K0, K1;
+    edge_def<NE>(B, ed, x, K0, K1);
+    const double xa = sXc[g][K0], xb = sXc[g][K1];
+    const double XE = P - Q0 * xa - Q1 * xb;
+    const double XL = lt == 0 ? xa : sD[tid - 1] - sH0[tid - 1] * xa - sH1[tid - 1] * xb;
+    chunk_finalise(rr, p0, e, XL, XE, mu, amq);
+  }
+  __syncthreads();
 #pragma unroll 4
-  for (int k = 0; k < e; k++)
-    u[base + (size_t)(r + 1 + k) * str[x]] = s[4 * k] + s[4 * k + 1] * x0 + s[4 * k + 2] * x1;
+  for (int it = 0; it < kQW; it++) {
+    const int q = lt + it * TE;
+    if (q < L) u[G.o0 + (size_t)(q + 1) * G.sx] = rr[rsw(q)];
+  }
+  if (bad) atomicOr(err, 1);
 }
 
 __global__ void __launch_bounds__(128) wpoint_kernel(int n, Coef3 c, const int4* __restrict__ pts,
@@ -487,7 +492,8 @@ __global__ void __launch_bounds__(128) wpoint_kernel(int n, Coef3 c, const int4*
   u[o] = r / d;
 }
 
-constexpr int kTR[kRingClasses] = {32, 64, 128, 256, 512};
+// ring classes: TE = 1 .. 64 threads per side (edges of m - 1 <= TE kQW points)
+constexpr int kTE[kRingClasses] = {1, 2, 4, 8, 16, 32, 64};
 
 template <typename T>
 int upload(const std::vector<T>& v, T** out, std::string& err) {
@@ -502,9 +508,38 @@ int upload(const std::vector<T>& v, T** out, std::string& err) {
   return 0;
 }
 
+template <int NE, int TE, int BD>
+cudaError_t allow_smem() {
+  return cudaFuncSetAttribute(wblock_kernel<NE, TE, BD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)wblock_smem<NE, TE, BD>());
+}
+
+template <int TE>
+void launch_rings(const WLevel& L, int n, const Coef3& c, int red, int k, double* u, const double* f,
+                  int* err, cudaStream_t s) {
+  constexpr int BPC = kRBD / (4 * TE);
+  const int nr = L.nrings[red][k];
+  if (!nr) return;
+  TMG_COUNT(1);
+  wblock_kernel<4, TE, kRBD><<<(nr + BPC - 1) / BPC, kRBD, wblock_smem<4, TE, kRBD>(), s>>>(
+      n, c, L.rings[red][k], nullptr, nr, u, f, err);
+}
+
+template <int TE>
+void launch_frames(const WLevel& L, int n, const Coef3& c, double* u, const double* f, int* err,
+                   cudaStream_t s) {
+  TMG_COUNT(1);
+  wblock_kernel<12, TE, 12 * TE><<<L.nframes, 12 * TE, wblock_smem<12, TE, 12 * TE>(), s>>>(
+      n, c, nullptr, L.frames, L.nframes, u, f, err);
+}
+
 }  // namespace
 
 int wire_build_level(int n, WLevel& L, std::string& err) {
+  if (n > kMaxN) {
+    err = "3D wireframe cubes above " + std::to_string(kMaxN) + " intervals are not supported";
+    return 2;
+  }
   const int c = n / 2;
   // Rings in launch order so that same-colour rings sharing 32-byte sectors
   // run together: a sector holds four consecutive k.  On faces normal to i or
@@ -519,33 +554,14 @@ int wire_build_level(int n, WLevel& L, std::string& err) {
         if (t < 2 || t >= c) continue;
         const long s1 = mirror(xa, n);
         if (s1 >= t) continue;
-        const int Lg = 4 * (n - 2 * t) - 1;
+        const int side = n - 2 * t - 1;  // points between two corners
         int cls = 0;
-        while (cls < kRingClasses && kTR[cls] * kQW < Lg) cls++;
-        if (cls == kRingClasses) {
-          err = "3D wireframe rings longer than " + std::to_string(kTR[kRingClasses - 1] * kQW + 1) +
-                " points (n > 1026) are not supported";
-          return 2;
-        }
+        while (cls < kRingClasses - 1 && kTE[cls] * kQW < side) cls++;
         const int red = ((s1 + t) % 2) == 0;
         rg[red][cls].push_back(Ring3{(int16_t)a, (int16_t)t, xa});
       }
-  // frames (red) and their edges; scratch slots per edge point
-  std::vector<int> fr;
-  std::vector<WEdge> eg;
-  int off = 0;
-  for (int r = 1; r < c; r++) {
-    const int e = n - 2 * r - 1;
-    for (int ed = 0; ed < 12; ed++) {
-      const int x = ed / 4, h = ed % 4;
-      const int o1 = x == 0 ? 1 : 0, o2 = x == 2 ? 1 : 2;
-      const int base = ((h & 1) << o1) | (((h >> 1) & 1) << o2);
-      eg.push_back(WEdge{r, off, (int)fr.size(), (uint8_t)x, (uint8_t)base,
-                         (uint8_t)(base | (1 << x)), (uint8_t)ed});
-      off += e;
-    }
-    fr.push_back(r);
-  }
+  std::vector<int> fr;  // frames (red): shells 1 .. c-1
+  for (int r = 1; r < c; r++) fr.push_back(r);
   // points: the centre (red) and the face centres
   std::vector<int4> pt[2];
   pt[1].push_back(make_int4(c, c, c, 0));
@@ -564,16 +580,22 @@ int wire_build_level(int n, WLevel& L, std::string& err) {
     if (upload(pt[red], &L.points[red], err)) return 3;
     L.npoints[red] = (int)pt[red].size();
   }
-  if (upload(eg, &L.edges, err) || upload(fr, &L.frames, err)) return 3;
-  L.nedges = (int)eg.size();
+  if (upload(fr, &L.frames, err)) return 3;
   L.nframes = (int)fr.size();
-  if (off > 0) {
-    cudaError_t e = cudaMalloc(&L.scratch, 4 * (size_t)off * sizeof(double));
-    if (e == cudaSuccess) e = cudaMalloc(&L.ends, 6 * (size_t)L.nedges * sizeof(double));
-    if (e != cudaSuccess) {
-      err = std::string("wireframe scratch: ") + cudaGetErrorString(e);
-      return 3;
-    }
+  // dynamic shared memory above 48 KB (per function: sized for the largest n)
+  cudaError_t e = allow_smem<4, 1, kRBD>();
+  if (e == cudaSuccess) e = allow_smem<4, 2, kRBD>();
+  if (e == cudaSuccess) e = allow_smem<4, 4, kRBD>();
+  if (e == cudaSuccess) e = allow_smem<4, 8, kRBD>();
+  if (e == cudaSuccess) e = allow_smem<4, 16, kRBD>();
+  if (e == cudaSuccess) e = allow_smem<4, 32, kRBD>();
+  if (e == cudaSuccess) e = allow_smem<4, 64, kRBD>();
+  if (e == cudaSuccess) e = allow_smem<12, 4, 48>();
+  if (e == cudaSuccess) e = allow_smem<12, 16, 192>();
+  if (e == cudaSuccess) e = allow_smem<12, 64, 768>();
+  if (e != cudaSuccess) {
+    err = std::string("wireframe kernel shared memory: ") + cudaGetErrorString(e);
+    return 3;
   }
   return 0;
 }
@@ -583,10 +605,7 @@ void wire_free_level(WLevel& L) {
     for (int k = 0; k < kRingClasses; k++) cudaFree(L.rings[red][k]);
     cudaFree(L.points[red]);
   }
-  cudaFree(L.edges);
   cudaFree(L.frames);
-  cudaFree(L.scratch);
-  cudaFree(L.ends);
   L = WLevel();
 }
 
@@ -596,31 +615,20 @@ long wire_blocks(const WLevel& L, int red) {
   return nb;
 }
 
-template <int TR>
-static void launch_rings(const WLevel& L, int n, const Coef3& c, int red, int k, double* u,
-                         const double* f, int* err, cudaStream_t s) {
-  constexpr int BD = TR > 256 ? TR : 256;
-  const int nr = L.nrings[red][k];
-  if (!nr) return;
-  TMG_COUNT(1);
-  ring3_kernel<TR><<<(nr + BD / TR - 1) / (BD / TR), BD, 0, s>>>(n, c, L.rings[red][k], nr, u, f,
-                                                                  err);
-}
-
 int wire_stage(const WLevel& L, int n, const Coef3& c, int red, double* u, const double* f,
                int* err, cudaStream_t s) {
-  launch_rings<32>(L, n, c, red, 0, u, f, err, s);
-  launch_rings<64>(L, n, c, red, 1, u, f, err, s);
-  launch_rings<128>(L, n, c, red, 2, u, f, err, s);
-  launch_rings<256>(L, n, c, red, 3, u, f, err, s);
-  launch_rings<512>(L, n, c, red, 4, u, f, err, s);
-  if (red && L.nedges) {
-    TMG_COUNT(3);
-    frame_edge_kernel<<<(L.nedges + 127) / 128, 128, 0, s>>>(n, c, L.edges, L.nedges, u, f,
-                                                             L.scratch, L.ends, err);
-    frame_corner_kernel<<<(L.nframes + 63) / 64, 64, 0, s>>>(n, c, L.frames, L.nframes, L.edges,
-                                                             L.ends, u, f, err);
-    frame_back_kernel<<<(L.nedges + 127) / 128, 128, 0, s>>>(n, L.edges, L.nedges, L.scratch, u);
+  launch_rings<1>(L, n, c, red, 0, u, f, err, s);
+  launch_rings<2>(L, n, c, red, 1, u, f, err, s);
+  launch_rings<4>(L, n, c, red, 2, u, f, err, s);
+  launch_rings<8>(L, n, c, red, 3, u, f, err, s);
+  launch_rings<16>(L, n, c, red, 4, u, f, err, s);
+  launch_rings<32>(L, n, c, red, 5, u, f, err, s);
+  launch_rings<64>(L, n, c, red, 6, u, f, err, s);
+  if (red && L.nframes) {
+    const int emax = n - 3;  // the outermost frame's edges
+    if (emax <= 4 * kQW) launch_frames<4>(L, n, c, u, f, err, s);
+    else if (emax <= 16 * kQW) launch_frames<16>(L, n, c, u, f, err, s);
+    else launch_frames<64>(L, n, c, u, f, err, s);
   }
   if (L.npoints[red]) {
     TMG_COUNT(1);
