@@ -639,7 +639,7 @@ def run_cube(args):
         "roofline": {"bound": "hbm", "achieved": alg / (sweep_ms * 1e-3) / 1e9, "peak": peak,
                      "unit": "GB/s", "frac": alg / (sweep_ms * 1e-3) / 1e9 / peak,
                      "traffic": None,
-                     "kernel": ("ring3_kernel + frame/point kernels (one finest-level 3D "
+                     "kernel": ("wblock_kernel rings + frames, wpoint_kernel (one finest-level 3D "
                                 "wireframe sweep)" if scheme == "wireframe" else
                                 "legs/branch kernels (one finest-level 3D tweed sweep)"),
                      "alg_bytes": alg, "ms": sweep_ms, "peak_kind": peak_kind},

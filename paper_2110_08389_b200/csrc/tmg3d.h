@@ -36,7 +36,7 @@ __device__ __forceinline__ size_t idx3(int n, int i, int j, int k) {
 //          grouped in classes by the threads per edge (kRingClasses);
 //   frames the 12-edge / 8-corner frame of a shell (red only);
 //   points face centres and the cube centre.
-constexpr int kRingClasses = 7;  // TE = 1 .. 64 threads per ring side
+constexpr int kRingClasses = 8;  // TE = 1 .. 128 threads per ring side
 
 struct Ring3 {
   int16_t a;   // axis normal to the face

@@ -39,21 +39,27 @@
 namespace tmg3 {
 namespace {
 
-constexpr int kQW = 16;      // edge points per thread (one chunk)
-constexpr int kRBD = 256;    // threads per ring CTA
-constexpr int kMaxN = 1028;  // edges of <= 64 * kQW points
+#ifndef TMG_WQ
+#define TMG_WQ 16
+#endif
+constexpr int kQW = 16;      // frame edge points per thread (one chunk)
+constexpr int kRQ = TMG_WQ;  // ring side points per thread
+constexpr int kRBD = 256;    // threads per ring CTA (at least)
+constexpr int kMaxN = 1028;  // edges of <= 64 * 16 points
 
 __device__ __forceinline__ bool wbad(double v) { return v > -1e-300 && v < 1e-300; }
 
 // padded index into the shared-memory coupling tables: chunk-per-thread
 // accesses (lane stride kQW points) land in distinct banks
-__device__ __forceinline__ int tix(int x) { return x + (x >> 4); }
-__host__ __device__ constexpr int tab_len(int n) { return n + 1 + (n + 1) / 16 + 1; }
+template <int Q>
+__device__ __forceinline__ int tix(int x) { return x + x / Q; }
+__host__ __device__ constexpr int tab_len(int n) { return n + 1 + (n + 1) / 8 + 2; }
 
 // shared-memory slot of edge point q: chunk rows of kQW, XOR swizzled so
 // that both the chunk-per-thread and the point-per-lane accesses are
 // conflict free
-__device__ __forceinline__ int rsw(int p) { return (p & ~(kQW - 1)) | ((p ^ (p >> 4)) & (kQW - 1)); }
+template <int Q>
+__device__ __forceinline__ int rsw(int p) { return (p & ~(Q - 1)) | ((p ^ (p / Q)) & (Q - 1)); }
 
 // A block: a ring (NE = 4: face normal a at xa, level t) or a frame
 // (NE = 12: shell t).  Corners: ring K = 0..3 at in-face (b, c) = (t, t),
@@ -133,11 +139,12 @@ __device__ __forceinline__ EdgeG edge_geom(const Coef3& c, int n, const WBlk& B,
 
 // Row of edge point q from the shared-memory coupling tables: the along
 // couplings toward q-1 (am) and q+1 (cn), the diagonal d.
+template <int Q>
 struct EdgeCpl {
   const EdgeG& G;
   const double *tlo, *thi;
   __device__ __forceinline__ void operator()(int q, double& am, double& d, double& cn) const {
-    const int xx = tix(G.x0 + 1 + q);
+    const int xx = tix<Q>(G.x0 + 1 + q);
     am = tlo[xx];
     cn = thi[xx];
     d = -(am + cn + G.tsum);
@@ -157,19 +164,19 @@ struct ChunkForms {
   double ad = 0.0, bd = 0.0, gd = 0.0;  // x_{e-1} = ad + bd X_left + gd X_end
 };
 
-template <class CPL>
+template <int Q, class CPL>
 __device__ __forceinline__ ChunkForms chunk_eliminate(const CPL& cpl, double* rr, int p0, int e,
-                                                      double (&mu)[kQW - 1], double (&amq)[kQW - 1],
+                                                      double (&mu)[Q - 1], double (&amq)[Q - 1],
                                                       bool& bad) {
   ChunkForms F;
   if (e <= 0) return F;
   double bq = 0.0, rq = 0.0, m = 0.0, anext = 0.0, ivq = 0.0;
 #pragma unroll
-  for (int k = kQW - 2; k >= 0; k--) {
+  for (int k = Q - 2; k >= 0; k--) {
     if (k < e) {
       double am, d, cn;
       cpl(p0 + k, am, d, cn);
-      const int sl = rsw(p0 + k);
+      const int sl = rsw<Q>(p0 + k);
       const double r = rr[sl];
       if (k == e - 1) {
         bq = d;
@@ -191,9 +198,9 @@ __device__ __forceinline__ ChunkForms chunk_eliminate(const CPL& cpl, double* rr
   }
   double al = 0.0, be = 1.0, ga = 0.0;
 #pragma unroll
-  for (int k = 0; k < kQW - 1; k++) {
+  for (int k = 0; k < Q - 1; k++) {
     if (k < e) {
-      const double rq_k = rr[rsw(p0 + k)];
+      const double rq_k = rr[rsw<Q>(p0 + k)];
       al = rq_k - amq[k] * al;
       be = -amq[k] * be;
       ga = mu[k] - amq[k] * ga;
@@ -210,31 +217,32 @@ __device__ __forceinline__ ChunkForms chunk_eliminate(const CPL& cpl, double* rr
   return F;
 }
 
+template <int Q>
 __device__ __forceinline__ void chunk_finalise(double* rr, int p0, int e, double XL, double XE,
-                                               const double (&mu)[kQW - 1],
-                                               const double (&amq)[kQW - 1]) {
+                                               const double (&mu)[Q - 1],
+                                               const double (&amq)[Q - 1]) {
   double x = XL;
 #pragma unroll
-  for (int k = 0; k < kQW - 1; k++) {
+  for (int k = 0; k < Q - 1; k++) {
     if (k < e) {
-      const int sl = rsw(p0 + k);
+      const int sl = rsw<Q>(p0 + k);
       x = rr[sl] + mu[k] * XE - amq[k] * x;
       rr[sl] = x;
     }
   }
-  rr[rsw(p0 + e)] = XE;
+  rr[rsw<Q>(p0 + e)] = XE;
 }
 
-template <int NE, int TE, int BD>
+template <int NE, int TE, int BD, int Q>
 constexpr size_t wblock_smem() {
-  return ((size_t)BD * (kQW + 6) + 2 * (size_t)tab_len(kMaxN)) * sizeof(double);
+  return ((size_t)BD * (Q + 6) + 2 * (size_t)tab_len(kMaxN)) * sizeof(double);
 }
 
 // Blocks of one kind and class: BD / (NE TE) blocks per CTA, TE threads per
 // edge.  Blocks come from `rings` (NE = 4) or `frames` (NE = 12, the shell
 // index).
-template <int NE, int TE, int BD>
-__global__ void __launch_bounds__(BD, BD == kRBD ? 2 : 1)
+template <int NE, int TE, int BD, int Q>
+__global__ void __launch_bounds__(BD, NE == 4 ? (Q <= 8 ? (BD > 256 ? 2 : 3) : 2) : 1)
     wblock_kernel(int n, Coef3 c, const Ring3* __restrict__ rings, const int* __restrict__ frames,
                   int nb, double* __restrict__ u, const double* __restrict__ f, int* err) {
   constexpr int NK = NE == 4 ? 4 : 8;
@@ -242,8 +250,8 @@ __global__ void __launch_bounds__(BD, BD == kRBD ? 2 : 1)
   constexpr int BPC = BD / SL;
   static_assert(BPC >= 1 && SL >= NK, "block slice");
   extern __shared__ double wsm[];
-  double* sR = wsm;  // BD * kQW
-  double *sA = sR + BD * kQW, *sB = sA + BD, *sC = sB + BD, *sD = sC + BD, *sH0 = sD + BD,
+  double* sR = wsm;  // BD * Q
+  double *sA = sR + BD * Q, *sB = sA + BD, *sC = sB + BD, *sD = sC + BD, *sH0 = sD + BD,
          *sH1 = sH0 + BD;
   double *tlo = sH1 + BD, *thi = tlo + tab_len(n);
   __shared__ double sEnd[BPC][NE][6];  // per edge: first / last point as al + be x_K0 + ga x_K1
@@ -261,17 +269,17 @@ __global__ void __launch_bounds__(BD, BD == kRBD ? 2 : 1)
     B.a = 0; B.xa = 0; B.t = live ? frames[bid] : 1;
   }
   for (int x = tid; x <= n; x += BD) {
-    tlo[tix(x)] = __ldg(c.W + x);
-    thi[tix(x)] = __ldg(c.E + x);
+    tlo[tix<Q>(x)] = __ldg(c.W + x);
+    thi[tix<Q>(x)] = __ldg(c.E + x);
   }
   const EdgeG G = edge_geom<NE>(c, n, B, ed);
   const int L = live ? G.L : 0;
-  double* rr = sR + (g * NE + ed) * TE * kQW;
+  double* rr = sR + (g * NE + ed) * TE * Q;
   // 1. gather: edge points (four transverse neighbours), and the corner rows
   {
     constexpr int NB = 4;  // points whose loads are in flight together
 #pragma unroll 1
-    for (int i0 = 0; i0 < kQW; i0 += NB) {
+    for (int i0 = 0; i0 < Q; i0 += NB) {
       if (lt + i0 * TE >= L) break;
       double f0[NB], v0[NB], v1[NB], v2[NB], v3[NB];
 #pragma unroll
@@ -288,7 +296,7 @@ __global__ void __launch_bounds__(BD, BD == kRBD ? 2 : 1)
       for (int b = 0; b < NB; b++) {
         const int q = lt + (i0 + b) * TE;
         if (q < L)
-          rr[rsw(q)] = f0[b] - G.t0 * v0[b] - G.t1 * v1[b] - G.t2 * v2[b] - G.t3 * v3[b];
+          rr[rsw<Q>(q)] = f0[b] - G.t0 * v0[b] - G.t1 * v1[b] - G.t2 * v2[b] - G.t3 * v3[b];
       }
     }
   }
@@ -317,13 +325,13 @@ __global__ void __launch_bounds__(BD, BD == kRBD ? 2 : 1)
   }
   __syncthreads();
   // 2. chunk eliminations
-  const EdgeCpl cpl{G, tlo, thi};
-  const int p0 = lt * kQW;
-  const int cnt = max(0, min(kQW, L - p0));
+  const EdgeCpl<Q> cpl{G, tlo, thi};
+  const int p0 = lt * Q;
+  const int cnt = max(0, min(Q, L - p0));
   const int e = cnt - 1;
   bool bad = false;
-  double mu[kQW - 1], amq[kQW - 1];
-  const ChunkForms Fm = chunk_eliminate(cpl, rr, p0, e, mu, amq, bad);
+  double mu[Q - 1], amq[Q - 1];
+  const ChunkForms Fm = chunk_eliminate<Q>(cpl, rr, p0, e, mu, amq, bad);
   sA[tid] = Fm.au;
   sB[tid] = Fm.bu;
   sC[tid] = Fm.gu;
@@ -333,7 +341,7 @@ __global__ void __launch_bounds__(BD, BD == kRBD ? 2 : 1)
   if (cnt > 0) {
     double ae, be, ce;
     cpl(p0 + e, ae, be, ce);
-    const double re = rr[rsw(p0 + e)];
+    const double re = rr[rsw<Q>(p0 + e)];
     if (e > 0) {
       A = ae * Fm.bd;
       Bv = be + ae * Fm.gd;
@@ -462,13 +470,13 @@ __global__ void __launch_bounds__(BD, BD == kRBD ? 2 : 1)
     const double xa = sXc[g][K0], xb = sXc[g][K1];
     const double XE = P - Q0 * xa - Q1 * xb;
     const double XL = lt == 0 ? xa : sD[tid - 1] - sH0[tid - 1] * xa - sH1[tid - 1] * xb;
-    chunk_finalise(rr, p0, e, XL, XE, mu, amq);
+    chunk_finalise<Q>(rr, p0, e, XL, XE, mu, amq);
   }
   __syncthreads();
 #pragma unroll 4
-  for (int it = 0; it < kQW; it++) {
+  for (int it = 0; it < Q; it++) {
     const int q = lt + it * TE;
-    if (q < L) u[G.o0 + (size_t)(q + 1) * G.sx] = rr[rsw(q)];
+    if (q < L) u[G.o0 + (size_t)(q + 1) * G.sx] = rr[rsw<Q>(q)];
   }
   if (bad) atomicOr(err, 1);
 }
@@ -493,7 +501,8 @@ __global__ void __launch_bounds__(128) wpoint_kernel(int n, Coef3 c, const int4*
 }
 
 // ring classes: TE = 1 .. 64 threads per side (edges of m - 1 <= TE kQW points)
-constexpr int kTE[kRingClasses] = {1, 2, 4, 8, 16, 32, 64};
+constexpr int kTE[kRingClasses] = {1, 2, 4, 8, 16, 32, 64, 128};
+constexpr int ring_bd(int te) { return 4 * te > kRBD ? 4 * te : kRBD; }
 
 template <typename T>
 int upload(const std::vector<T>& v, T** out, std::string& err) {
@@ -508,20 +517,20 @@ int upload(const std::vector<T>& v, T** out, std::string& err) {
   return 0;
 }
 
-template <int NE, int TE, int BD>
+template <int NE, int TE, int BD, int Q>
 cudaError_t allow_smem() {
-  return cudaFuncSetAttribute(wblock_kernel<NE, TE, BD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)wblock_smem<NE, TE, BD>());
+  return cudaFuncSetAttribute(wblock_kernel<NE, TE, BD, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)wblock_smem<NE, TE, BD, Q>());
 }
 
 template <int TE>
 void launch_rings(const WLevel& L, int n, const Coef3& c, int red, int k, double* u, const double* f,
                   int* err, cudaStream_t s) {
-  constexpr int BPC = kRBD / (4 * TE);
+  constexpr int BD = ring_bd(TE), BPC = BD / (4 * TE);
   const int nr = L.nrings[red][k];
   if (!nr) return;
   TMG_COUNT(1);
-  wblock_kernel<4, TE, kRBD><<<(nr + BPC - 1) / BPC, kRBD, wblock_smem<4, TE, kRBD>(), s>>>(
+  wblock_kernel<4, TE, BD, kRQ><<<(nr + BPC - 1) / BPC, BD, wblock_smem<4, TE, BD, kRQ>(), s>>>(
       n, c, L.rings[red][k], nullptr, nr, u, f, err);
 }
 
@@ -529,7 +538,7 @@ template <int TE>
 void launch_frames(const WLevel& L, int n, const Coef3& c, double* u, const double* f, int* err,
                    cudaStream_t s) {
   TMG_COUNT(1);
-  wblock_kernel<12, TE, 12 * TE><<<L.nframes, 12 * TE, wblock_smem<12, TE, 12 * TE>(), s>>>(
+  wblock_kernel<12, TE, 12 * TE, kQW><<<L.nframes, 12 * TE, wblock_smem<12, TE, 12 * TE, kQW>(), s>>>(
       n, c, nullptr, L.frames, L.nframes, u, f, err);
 }
 
@@ -556,7 +565,7 @@ int wire_build_level(int n, WLevel& L, std::string& err) {
         if (s1 >= t) continue;
         const int side = n - 2 * t - 1;  // points between two corners
         int cls = 0;
-        while (cls < kRingClasses - 1 && kTE[cls] * kQW < side) cls++;
+        while (cls < kRingClasses - 1 && kTE[cls] * kRQ < side) cls++;
         const int red = ((s1 + t) % 2) == 0;
         rg[red][cls].push_back(Ring3{(int16_t)a, (int16_t)t, xa});
       }
@@ -583,16 +592,17 @@ int wire_build_level(int n, WLevel& L, std::string& err) {
   if (upload(fr, &L.frames, err)) return 3;
   L.nframes = (int)fr.size();
   // dynamic shared memory above 48 KB (per function: sized for the largest n)
-  cudaError_t e = allow_smem<4, 1, kRBD>();
-  if (e == cudaSuccess) e = allow_smem<4, 2, kRBD>();
-  if (e == cudaSuccess) e = allow_smem<4, 4, kRBD>();
-  if (e == cudaSuccess) e = allow_smem<4, 8, kRBD>();
-  if (e == cudaSuccess) e = allow_smem<4, 16, kRBD>();
-  if (e == cudaSuccess) e = allow_smem<4, 32, kRBD>();
-  if (e == cudaSuccess) e = allow_smem<4, 64, kRBD>();
-  if (e == cudaSuccess) e = allow_smem<12, 4, 48>();
-  if (e == cudaSuccess) e = allow_smem<12, 16, 192>();
-  if (e == cudaSuccess) e = allow_smem<12, 64, 768>();
+  cudaError_t e = allow_smem<4, 1, ring_bd(1), kRQ>();
+  if (e == cudaSuccess) e = allow_smem<4, 2, ring_bd(2), kRQ>();
+  if (e == cudaSuccess) e = allow_smem<4, 4, ring_bd(4), kRQ>();
+  if (e == cudaSuccess) e = allow_smem<4, 8, ring_bd(8), kRQ>();
+  if (e == cudaSuccess) e = allow_smem<4, 16, ring_bd(16), kRQ>();
+  if (e == cudaSuccess) e = allow_smem<4, 32, ring_bd(32), kRQ>();
+  if (e == cudaSuccess) e = allow_smem<4, 64, ring_bd(64), kRQ>();
+  if (kRQ < 16 && e == cudaSuccess) e = allow_smem<4, 128, ring_bd(128), kRQ>();
+  if (e == cudaSuccess) e = allow_smem<12, 4, 48, kQW>();
+  if (e == cudaSuccess) e = allow_smem<12, 16, 192, kQW>();
+  if (e == cudaSuccess) e = allow_smem<12, 64, 768, kQW>();
   if (e != cudaSuccess) {
     err = std::string("wireframe kernel shared memory: ") + cudaGetErrorString(e);
     return 3;
@@ -624,6 +634,7 @@ int wire_stage(const WLevel& L, int n, const Coef3& c, int red, double* u, const
   launch_rings<16>(L, n, c, red, 4, u, f, err, s);
   launch_rings<32>(L, n, c, red, 5, u, f, err, s);
   launch_rings<64>(L, n, c, red, 6, u, f, err, s);
+  if (kRQ < 16) launch_rings<128>(L, n, c, red, 7, u, f, err, s);
   if (red && L.nframes) {
     const int emax = n - 3;  // the outermost frame's edges
     if (emax <= 4 * kQW) launch_frames<4>(L, n, c, u, f, err, s);
