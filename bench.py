@@ -504,6 +504,109 @@ def run_sharded(args):
     dist.destroy_process_group()
 
 
+def run_cube_sharded(args):
+    """config 5 with N > 1: one 1025^3 problem, fine levels split between the
+    ranks by shells (cube_sharded; strong scaling)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2110_08389_b200 import _lib, cube, cube_sharded, mgcycle
+
+    world, rank, local = _dist()
+    backend = os.environ.get("TMG_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    L = _lib.lib()
+    n, x = _cube_workload(args)
+    h = cube.CubeHierarchy(x, scheme="wireframe")
+    cfg = mgcycle.CycleConfig(smoother="wireframe", nu1=2, nu2=2)
+    fd = _cube_rhs(args, n)
+    u = torch.zeros_like(fd)
+    solver = cube_sharded.CubeShardedSolver(h, cfg)
+    solver.load(u, fd)
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, k):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(args.warmup, 3)):
+        solver.v_cycle()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    launches0, swaps0 = L.tmg_kernel_launches(), solver.exchanges
+    t_ms = timed(solver.v_cycle, args.steps)
+    launches = L.tmg_kernel_launches() - launches0
+    swaps = (solver.exchanges - swaps0) // args.steps
+    clocks = clk.stop()
+    upc = 4 * h.interior_points()
+    value = upc * args.steps / (t_ms * 1e-3)
+    g0, g1 = solver.plan.own(0, rank)
+    reps = 3
+
+    def rank_sweep():
+        for red in (1, 0):
+            solver.ops.sweep(0, red, g0, g1)
+    sweep_ms = timed(rank_sweep, reps) / reps
+    owned = int(cube_sharded.group_sizes("wireframe", n)[g0:g1].sum())
+    alg_bytes = 24.0 * owned
+    peak, peak_kind = _peak_hbm()
+    achieved = alg_bytes / (sweep_ms * 1e-3) / 1e9
+    u_h = torch.zeros(fd.shape, dtype=torch.float64).pin_memory()
+    f_h = fd.cpu().pin_memory()
+    ue, fe = torch.empty_like(fd), torch.empty_like(fd)
+
+    def e2e_step():
+        fe.copy_(f_h, non_blocking=True)
+        ue.copy_(u_h, non_blocking=True)
+        solver.load(ue, fe)
+        solver.v_cycle()
+        solver.store(ue)
+        u_h.copy_(ue, non_blocking=True)
+    e2e_step()
+    e2e_ms = timed(e2e_step, 1)
+    field_bytes = fd.numel() * 8
+    line = {
+        "metric": "smoother grid-pt updates/s", "value": value, "unit": "grid-pt updates/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": _cube_desc(args, n), "levels": h.levels,
+                   "updates_per_cycle": upc, "vcycle_ms": t_ms / args.steps,
+                   "sharded_levels": solver.plan.nshard,
+                   "l2": "inputs larger than L2 (u, f = 2 x %.0f MB)" % (field_bytes / 1e6),
+                   "parallelism": f"sharded x{world}: shell ranges, {backend} halo swaps"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "wblock_kernel (rank's finest-level shells, both colours)",
+                     "alg_bytes": alg_bytes, "ms": sweep_ms, "peak_kind": peak_kind},
+        "e2e": {"value": upc / (e2e_ms * 1e-3), "unit": "grid-pt updates/s",
+                "h2d_bytes_per_step": 2 * field_bytes, "d2h_bytes_per_step": field_bytes,
+                "ms_per_step": e2e_ms},
+        "clocks": clocks,
+        "gpu_launches": launches,
+        "halo_swaps_per_cycle": swaps, "dist_backend": backend,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def _cube_scheme(args):
     return "wireframe" if args.config == "config5" else "tweed"
 
@@ -762,6 +865,8 @@ def main():
     if args.config in ("config4", "config5"):
         if args.impl == "reference":
             run_cube_reference(args)
+        elif args.config == "config5" and _dist()[0] > 1 and not args.replicas:
+            run_cube_sharded(args)
         else:
             run_cube(args)
     elif args.impl == "reference":

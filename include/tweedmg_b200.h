@@ -219,6 +219,37 @@ int tmg_cube_cycles(tmg_cube* h, int nu1, int nu2, int reps, void* stream);
 int tmg_cube_norm(tmg_cube* h, double* out_host, void* stream);
 int tmg_cube_store(tmg_cube* h, double* u, void* stream);
 
+/* ---- sharded cube V-cycle (BASELINE config 5 across GPUs).
+ *      Sharding groups 1 .. n/2: 3D wireframe min(i',j',k') (a shell: its
+ *      frame, face rings and face centres), 3D tweed max(i',j',k'); a block
+ *      never spans two groups, a point's neighbours lie in groups g-1 .. g+1,
+ *      coarse group G is fine group 2G.  Same protocol as the 2D
+ *      tmg_session_* entry points above (mgcycle.py:89-104 split by rank). */
+/* number of groups, 0 for a bad scheme / n; host only */
+int tmg_cube_group_count(int scheme, int n);
+/* sizes[g] = interior points of group g, g = 0..G; returns G + 1 (-1: bad args) */
+long tmg_cube_group_sizes(int scheme, int n, long long* sizes, long cap);
+/* element offsets (C order, (n+1)^3 field) of the interior points of groups
+ * [g0, g1), increasing; returns the count (entries beyond cap not written) */
+long tmg_cube_group_offsets(int scheme, int n, int g0, int g1, long long* off, long cap);
+/* one colour stage (red = 1 / black = 0) of the session's level blocks in
+ * groups [g0, g1) (3D wireframe only) */
+int tmg_cube_sweep_part(tmg_cube* h, int level, int red, int g0, int g1, void* stream);
+/* F[level+1] = R (f - L u)[level], U[level+1] = 0 */
+int tmg_cube_restrict(tmg_cube* h, int level, void* stream);
+/* U[level] += P U[level+1] */
+int tmg_cube_prolong(tmg_cube* h, int level, void* stream);
+/* the V(nu1, nu2) cycle from `level` down and back (replicated tail) */
+int tmg_cube_tail(tmg_cube* h, int level, int nu1, int nu2, void* stream);
+/* out[q] = field[off[q]] / field[off[q]] = in[q]; which: 0 u, 1 f;
+ * off, out, in: DEVICE arrays */
+int tmg_cube_gather(tmg_cube* h, int level, int which, const long long* off, long m, double* out,
+                    void* stream);
+int tmg_cube_scatter(tmg_cube* h, int level, int which, const long long* off, long m,
+                     const double* in, void* stream);
+/* finest-level max |f - L u| over groups [g0, g1) + pivot flag; synchronizes */
+int tmg_cube_norm_part(tmg_cube* h, int g0, int g1, double* out_host, void* stream);
+
 /* ---- profiling aid: average per-CTA cycles between the phase marks of the
  *      block-solver kernel (gather, elimination, reduced solve, hub, finalize,
  *      scatter) over the last launch; non-zero only in builds made with

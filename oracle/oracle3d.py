@@ -28,6 +28,7 @@ def _decl():
     L.orc3_layout_dump.argtypes = [cl, lp, lp, lp, lp, lp, cl]
     L.orc3_layout_dump.restype = cl
     L.orcw3_sweep.argtypes = [cl] + [dp] * 8 + [ci]
+    L.orcw3_sweep_part.argtypes = [cl] + [dp] * 8 + [ci, cl, cl]
     L.orcw3_layout_dump.argtypes = [cl, lp, lp, lp, lp, lp, cl]
     L.orcw3_layout_dump.restype = cl
     L._o3 = True
@@ -73,6 +74,24 @@ def sweep(st, u, f, nthreads=1, scheme="tweed"):
     if scheme not in SCHEMES:
         raise ValueError(scheme)
     _check(fn(n, *[_dp(a) for a in st], _dp(u), _dp(f), int(nthreads)))
+
+
+def sweep_part(st, u, f, red, g0, g1):
+    """One colour stage of the 3D wireframe blocks of sharding groups
+    [g0, g1) (group = min(i', j', k'))."""
+    n = len(st[0]) - 1
+    _check(_decl().orcw3_sweep_part(n, *[_dp(a) for a in st], _dp(u), _dp(f), int(red), int(g0),
+                                    int(g1)))
+
+
+def group_map(n, scheme="wireframe"):
+    """Sharding group of every node (0 on the boundary): min(i', j', k') for
+    the wireframe, max for the tweed."""
+    m = np.minimum(np.arange(n + 1), n - np.arange(n + 1))
+    a, b, c = np.meshgrid(m, m, m, indexing="ij")
+    g = np.minimum(np.minimum(a, b), c) if scheme == "wireframe" else np.maximum(np.maximum(a, b), c)
+    g[0, :, :] = g[-1, :, :] = g[:, 0, :] = g[:, -1, :] = g[:, :, 0] = g[:, :, -1] = 0
+    return g
 
 
 def defect(st, u, f, nthreads=1):

@@ -371,6 +371,39 @@ int orcw3_sweep(long n, const double *W, const double *E, const double *S, const
     return status;
 }
 
+/* One colour stage (red = 1 / black = 0) of the blocks whose sharding group
+ * lies in [g0, g1): group = min(i', j', k') of the block's points (the
+ * shell: frame r, the rings and face centres of shell s1, the centre c).
+ * The rank-local sweep of the sharded V-cycle. */
+int orcw3_sweep_part(long n, const double *W, const double *E, const double *S, const double *N,
+                     const double *Bc, const double *Tc, double *u, const double *f, int red,
+                     long g0, long g1) {
+    if (n < 2 || n % 2) return W3_BADARG;
+    const WG g = {n, {W, S, Bc}, {E, N, Tc}};
+    const long nb = orcw3_blocks(n, NULL, 0);
+    WBlock *blocks = (WBlock *)malloc(sizeof(WBlock) * (size_t)(nb > 0 ? nb : 1));
+    orcw3_blocks(n, blocks, nb);
+    double *wk = (double *)malloc(sizeof(double) * 48 * (size_t)(n + 1));
+    int status = W3_OK;
+    for (long b = 0; b < nb; b++) {
+        const WBlock *B = &blocks[b];
+        if (B->red != red) continue;
+        long grp;
+        if (B->kind == 0) grp = B->x0;                 /* frame r */
+        else if (B->kind == 1) grp = B->x2;            /* ring of shell s1 */
+        else {                                         /* point: min mirrored coordinate */
+            const long m0 = wmir(B->x0, n), m1 = wmir(B->x1, n), m2 = wmir(B->x2, n);
+            grp = m0 < m1 ? (m0 < m2 ? m0 : m2) : (m1 < m2 ? m1 : m2);
+        }
+        if (grp < g0 || grp >= g1) continue;
+        const int st = solve_wblock(&g, B, u, f, wk);
+        if (st != W3_OK) status = st;
+    }
+    free(wk);
+    free(blocks);
+    return status;
+}
+
 /* Block export for tests: per member point (i, j, k, block, red); frames list
  * their corners then edges, rings in ring order.  Returns the member count. */
 long orcw3_layout_dump(long n, long *oi, long *oj, long *ok, long *oblk, long *ored, long cap) {

@@ -79,6 +79,16 @@ def _declare(L):
         "tmg_cube_cycles": ([vp, ip, ip, ip, vp], ip),
         "tmg_cube_norm": ([vp, pd, vp], ip),
         "tmg_cube_store": ([vp, vp, vp], ip),
+        "tmg_cube_group_count": ([ip, ip], ip),
+        "tmg_cube_group_sizes": ([ip, ip, vp, lp], lp),
+        "tmg_cube_group_offsets": ([ip, ip, ip, ip, vp, lp], lp),
+        "tmg_cube_sweep_part": ([vp, ip, ip, ip, ip, vp], ip),
+        "tmg_cube_restrict": ([vp, ip, vp], ip),
+        "tmg_cube_prolong": ([vp, ip, vp], ip),
+        "tmg_cube_tail": ([vp, ip, ip, ip, vp], ip),
+        "tmg_cube_gather": ([vp, ip, ip, vp, lp, vp, vp], ip),
+        "tmg_cube_scatter": ([vp, ip, ip, vp, lp, vp, vp], ip),
+        "tmg_cube_norm_part": ([vp, ip, ip, pd, vp], ip),
         "tmg_group_count": ([ip, ip, ip], ip),
         "tmg_group_sizes": ([ip, ip, ip, vp, lp], lp),
         "tmg_group_offsets": ([ip, ip, ip, ip, ip, vp, lp], lp),

@@ -16,7 +16,10 @@
 // legs are enumerated with k fastest, so neighbouring threads walk
 // neighbouring lines.
 #include <algorithm>
+#include <climits>
 #include <cstdio>
+#include <map>
+#include <tuple>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -372,11 +375,20 @@ __global__ void __launch_bounds__(128) legs_back_kernel(int n, Coef3 c, const Le
   }
 }
 
-// d = f - L u (interior), 0 on the boundary; or the max |f - L u| into dmax
+// sharding group of an interior point: 3D tweed blocks lie in
+// one max(i', j', k') shell, 3D wireframe blocks in one min(i', j', k') shell
+__device__ __forceinline__ int cube_group(int scheme, int n, int i, int j, int k) {
+  const int a = (int)mirror(i, n), b = (int)mirror(j, n), c = (int)mirror(k, n);
+  return scheme == 1 ? min(a, min(b, c)) : max(a, max(b, c));
+}
+
+// d = f - L u (interior), 0 on the boundary; or the max |f - L u| over the
+// points of groups [g0, g1) into dmax
 __global__ void __launch_bounds__(256) defect3_kernel(int n, Coef3 c, const double* __restrict__ u,
                                                       const double* __restrict__ f,
                                                       double* __restrict__ d,
-                                                      unsigned long long* dmax) {
+                                                      unsigned long long* dmax, int gscheme = 0,
+                                                      int g0 = 0, int g1 = 1 << 30) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y, i = blockIdx.z;
   if (k > n) return;
@@ -396,6 +408,10 @@ __global__ void __launch_bounds__(256) defect3_kernel(int n, Coef3 c, const doub
   }
   if (d) d[o] = v;
   if (dmax) {
+    if (g0 > 0 || g1 < (1 << 30)) {
+      const int grp = v != 0.0 ? cube_group(gscheme, n, i, j, k) : g0;
+      if (grp < g0 || grp >= g1) v = 0.0;
+    }
     unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(v));
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) {
@@ -450,6 +466,18 @@ __global__ void coarse3_kernel(Coef3 c, double* u, const double* f) {
   u[idx3(n, 1, 1, 1)] = r / cc;
 }
 
+__global__ void cube_gather_kernel(const double* __restrict__ fld, const long long* __restrict__ off,
+                                   long m, double* __restrict__ out) {
+  const long q = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < m) out[q] = fld[off[q]];
+}
+
+__global__ void cube_scatter_kernel(double* __restrict__ fld, const long long* __restrict__ off,
+                                    long m, const double* __restrict__ in) {
+  const long q = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < m) fld[off[q]] = in[q];
+}
+
 std::string g_err3;
 int fail3(int code, const std::string& m) {
   g_err3 = m;
@@ -464,6 +492,7 @@ int fail3(int code, const std::string& m) {
 struct tmg_cube {
   int scheme = 0;                     // 0 tweed, 1 wireframe
   std::vector<tmg3::WLevel> wl;       // wireframe blocks per level
+  std::map<std::tuple<int, int, int>, tmg3::WLevel> wparts;  // (level, g0, g1): a rank's blocks
   std::vector<int> n;                 // per level
   std::vector<double*> coef;          // per level: W E S N B T (6 (n+1))
   std::vector<Block3*> blocks[2];     // per level: black, red lists
@@ -576,9 +605,9 @@ int sweep3(tmg_cube* h, int l, double* u, const double* f, cudaStream_t s) {
 
 dim3 grid3(int n) { return dim3((n + 1 + 255) / 256, n + 1, n + 1); }
 
-int cycle3(tmg_cube* h, int nu1, int nu2, cudaStream_t s) {
+int cycle3(tmg_cube* h, int nu1, int nu2, cudaStream_t s, int l0 = 0) {
   const int L = (int)h->n.size();
-  for (int l = 0; l < L - 1; l++) {
+  for (int l = l0; l < L - 1; l++) {
     for (int k = 0; k < nu1; k++) {
       int st = sweep3(h, l, h->U[l], h->F[l], s);
       if (st) return st;
@@ -592,7 +621,7 @@ int cycle3(tmg_cube* h, int nu1, int nu2, cudaStream_t s) {
   }
   TMG_COUNT(1);
   coarse3_kernel<<<1, 1, 0, s>>>(coefs(h, L - 1), h->U[L - 1], h->F[L - 1]);
-  for (int l = L - 2; l >= 0; l--) {
+  for (int l = L - 2; l >= l0; l--) {
     TMG_COUNT(1);
     prolong3_kernel<<<grid3(h->n[l]), 256, 0, s>>>(h->n[l + 1], h->U[l + 1], h->U[l]);
     for (int k = 0; k < nu2; k++) {
@@ -739,6 +768,7 @@ int tmg_cube_destroy(tmg_cube* h) {
   }
   cudaFree(h->contrib);
   for (auto& w : h->wl) tmg3::wire_free_level(w);
+  for (auto& kv : h->wparts) tmg3::wire_free_level(kv.second);
   for (double* p : h->U) cudaFree(p);
   for (double* p : h->F) cudaFree(p);
   cudaFree(h->sb);
@@ -840,6 +870,198 @@ int tmg_cube_norm(tmg_cube* h, double* out_host, void* stream) {
   TMG_COUNT(1);
   defect3_kernel<<<grid3(h->n[0]), 256, 0, s>>>(h->n[0], coefs(h, 0), h->U[0], h->F[0], nullptr,
                                                 h->dmax);
+  T3(cudaGetLastError());
+  T3(cudaMemcpyAsync(h->h_dmax, h->dmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  T3(cudaMemcpyAsync(h->h_err, h->err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  T3(cudaMemsetAsync(h->err, 0, sizeof(int), s));
+  T3(cudaStreamSynchronize(s));
+  double v;
+  std::memcpy(&v, h->h_dmax, sizeof(v));
+  *out_host = v;
+  if (*h->h_err & 1) return fail3(TMG_SINGULAR, "zero pivot during 3D block elimination");
+  return TMG_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// sharded cube V-cycle (one rank's share, DESIGN.md §7/§11).
+// Groups: 3D wireframe min(i', j', k') (the shell: its frame, the rings of its
+// faces, its face centres), 3D tweed max(i', j', k') (the blocks whose branch
+// has that largest mirrored coordinate); groups 1 .. n/2, neighbours of a
+// point lie in groups g-1 .. g+1 and coarse group G is fine group 2G.
+
+namespace {
+
+// k' in [a, b] (inclusive, 1 <= a): k in [a, b] or [n-b, n-a], merged when
+// they touch; visits the interior k in increasing order
+template <class F>
+void for_k_mirror_range(int n, int a, int b, F&& fn) {
+  if (a > b) return;
+  const int lo1 = a, hi1 = std::min(b, n - 1), lo2 = std::max(n - b, 1), hi2 = n - a;
+  if (lo2 <= hi1 + 1) {
+    for (int k = lo1; k <= std::max(hi1, hi2); k++) fn(k);
+  } else {
+    for (int k = lo1; k <= hi1; k++) fn(k);
+    for (int k = lo2; k <= hi2; k++) fn(k);
+  }
+}
+
+int cube_session_level(tmg_cube* h, int level, int need_coarser) {
+  if (!h) return fail3(TMG_BADARG, "null cube");
+  if (level < 0 || level >= (int)h->n.size() - need_coarser)
+    return fail3(TMG_BADARG, "level " + std::to_string(level) + " out of range");
+  return TMG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tmg_cube_group_count(int scheme, int n) {
+  if ((scheme != 0 && scheme != 1) || n < 2 || n % 2) return 0;
+  return n / 2;
+}
+
+long tmg_cube_group_sizes(int scheme, int n, long long* sizes, long cap) {
+  const int G = tmg_cube_group_count(scheme, n);
+  if (G < 1) {
+    g_err3 = "cube groups need scheme 0/1 and an even n >= 2";
+    return -1;
+  }
+  if (cap < G + 1) return G + 1;
+  // per axis: interior indices with mirrored coordinate >= g (n - 2g + 1) or <= g
+  auto ge = [n](long g) -> long long { return g > n / 2 ? 0 : (long long)(n - 2 * g + 1); };
+  auto le = [n](long g) -> long long { return g >= n / 2 ? (long long)(n - 1) : 2 * g; };
+  sizes[0] = 0;
+  for (int g = 1; g <= G; g++) {
+    if (scheme == 1)
+      sizes[g] = ge(g) * ge(g) * ge(g) - ge(g + 1) * ge(g + 1) * ge(g + 1);
+    else
+      sizes[g] = le(g) * le(g) * le(g) - le(g - 1) * le(g - 1) * le(g - 1);
+  }
+  return G + 1;
+}
+
+long tmg_cube_group_offsets(int scheme, int n, int g0, int g1, long long* off, long cap) {
+  const int G = tmg_cube_group_count(scheme, n);
+  if (G < 1) {
+    g_err3 = "cube groups need scheme 0/1 and an even n >= 2";
+    return -1;
+  }
+  g0 = std::max(g0, 1);
+  g1 = std::min(g1, G + 1);
+  long m = 0;
+  const long long n1 = n + 1;
+  for (int i = 1; i < n; i++)
+    for (int j = 1; j < n; j++) {
+      const int a = (int)mirror(i, n), b = (int)mirror(j, n);
+      int lo, hi;  // allowed k' range
+      if (scheme == 1) {  // min(a, b, k') in [g0, g1)
+        const int m2 = std::min(a, b);
+        if (m2 < g0) continue;
+        lo = g0;
+        hi = m2 >= g1 ? g1 - 1 : G;
+      } else {  // max(a, b, k') in [g0, g1)
+        const int m2 = std::max(a, b);
+        if (m2 >= g1) continue;
+        lo = m2 < g0 ? g0 : 1;
+        hi = g1 - 1;
+      }
+      for_k_mirror_range(n, lo, std::min(hi, G), [&](int k) {
+        if (m < cap) off[m] = (i * n1 + j) * n1 + k;
+        m++;
+      });
+    }
+  return m;
+}
+
+// one colour stage (red = 1 / black = 0) of the session's level-`level`
+// blocks in groups [g0, g1)
+int tmg_cube_sweep_part(tmg_cube* h, int level, int red, int g0, int g1, void* stream) {
+  int st = cube_session_level(h, level, 0);
+  if (st) return st;
+  if (h->scheme != 1)
+    return fail3(TMG_BADARG, "only the 3D wireframe shards (config 5); 3D tweed runs on one GPU");
+  const auto key = std::make_tuple(level, g0, g1);
+  auto it = h->wparts.find(key);
+  if (it == h->wparts.end()) {
+    std::string err;
+    tmg3::WLevel w;
+    const int b = tmg3::wire_build_level(h->n[level], w, err, g0, g1);
+    if (b) return fail3(b == 2 ? TMG_BADARG : TMG_CUDA, err);
+    it = h->wparts.emplace(key, w).first;
+  }
+  if (tmg3::wire_stage(it->second, h->n[level], coefs(h, level), red ? 1 : 0, h->U[level],
+                       h->F[level], h->err, (cudaStream_t)stream))
+    return cuda3(cudaGetLastError(), "wireframe part stage");
+  return TMG_OK;
+}
+
+// F[level+1] = R (f - L u)[level], U[level+1] = 0 (mgcycle.py:98-100)
+int tmg_cube_restrict(tmg_cube* h, int level, void* stream) {
+  int st = cube_session_level(h, level, 1);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  TMG_COUNT(2);
+  defect3_kernel<<<grid3(h->n[level]), 256, 0, s>>>(h->n[level], coefs(h, level), h->U[level],
+                                                     h->F[level], h->d, nullptr);
+  restrict3_kernel<<<grid3(h->n[level + 1]), 256, 0, s>>>(h->n[level], h->d, h->F[level + 1]);
+  const size_t nc = (size_t)(h->n[level + 1] + 1) * (h->n[level + 1] + 1) * (h->n[level + 1] + 1);
+  T3(cudaMemsetAsync(h->U[level + 1], 0, nc * sizeof(double), s));
+  return cuda3(cudaGetLastError(), "cube restrict");
+}
+
+// U[level] += P U[level+1] (mgcycle.py:101-102)
+int tmg_cube_prolong(tmg_cube* h, int level, void* stream) {
+  int st = cube_session_level(h, level, 1);
+  if (st) return st;
+  TMG_COUNT(1);
+  prolong3_kernel<<<grid3(h->n[level]), 256, 0, (cudaStream_t)stream>>>(
+      h->n[level + 1], h->U[level + 1], h->U[level]);
+  return cuda3(cudaGetLastError(), "cube prolong");
+}
+
+// the V-cycle from `level` down to the coarsest and back (replicated tail)
+int tmg_cube_tail(tmg_cube* h, int level, int nu1, int nu2, void* stream) {
+  int st = cube_session_level(h, level, 0);
+  if (st) return st;
+  if (nu1 < 0 || nu2 < 0 || nu1 + nu2 < 1) return fail3(TMG_BADARG, "need nu1 + nu2 >= 1");
+  return cycle3(h, nu1, nu2, (cudaStream_t)stream, level);
+}
+
+// out[q] = field[off[q]] / field[off[q]] = in[q]; which: 0 u, 1 f; off, out,
+// in: DEVICE arrays (element offsets in the (n+1)^3 C-order level field)
+int tmg_cube_gather(tmg_cube* h, int level, int which, const long long* off, long m, double* out,
+                    void* stream) {
+  int st = cube_session_level(h, level, 0);
+  if (st || m <= 0) return st;
+  TMG_COUNT(1);
+  cube_gather_kernel<<<(unsigned)((m + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      which ? h->F[level] : h->U[level], off, m, out);
+  return cuda3(cudaGetLastError(), "cube gather");
+}
+
+int tmg_cube_scatter(tmg_cube* h, int level, int which, const long long* off, long m,
+                     const double* in, void* stream) {
+  int st = cube_session_level(h, level, 0);
+  if (st || m <= 0) return st;
+  TMG_COUNT(1);
+  cube_scatter_kernel<<<(unsigned)((m + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      which ? h->F[level] : h->U[level], off, m, in);
+  return cuda3(cudaGetLastError(), "cube scatter");
+}
+
+// finest-level max |f - L u| over groups [g0, g1) plus the pivot flag;
+// synchronizes
+int tmg_cube_norm_part(tmg_cube* h, int g0, int g1, double* out_host, void* stream) {
+  int st = cube_session_level(h, 0, 0);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  T3(cudaMemsetAsync(h->dmax, 0, sizeof(unsigned long long), s));
+  TMG_COUNT(1);
+  defect3_kernel<<<grid3(h->n[0]), 256, 0, s>>>(h->n[0], coefs(h, 0), h->U[0], h->F[0], nullptr,
+                                                h->dmax, h->scheme, g0, g1);
   T3(cudaGetLastError());
   T3(cudaMemcpyAsync(h->h_dmax, h->dmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   T3(cudaMemcpyAsync(h->h_err, h->err, sizeof(int), cudaMemcpyDeviceToHost, s));

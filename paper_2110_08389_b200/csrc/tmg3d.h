@@ -53,7 +53,8 @@ struct WLevel {
   int npoints[2] = {};
 };
 
-int wire_build_level(int n, WLevel& L, std::string& err);
+// blocks of sharding groups [g0, g1) only (group = min(i', j', k'): the shell)
+int wire_build_level(int n, WLevel& L, std::string& err, int g0 = 0, int g1 = 1 << 30);
 void wire_free_level(WLevel& L);
 // one colour stage (red = 1 / black = 0) of the wireframe sweep
 int wire_stage(const WLevel& L, int n, const Coef3& c, int red, double* u, const double* f,

@@ -544,7 +544,7 @@ void launch_frames(const WLevel& L, int n, const Coef3& c, double* u, const doub
 
 }  // namespace
 
-int wire_build_level(int n, WLevel& L, std::string& err) {
+int wire_build_level(int n, WLevel& L, std::string& err, int g0, int g1) {
   if (n > kMaxN) {
     err = "3D wireframe cubes above " + std::to_string(kMaxN) + " intervals are not supported";
     return 2;
@@ -562,7 +562,7 @@ int wire_build_level(int n, WLevel& L, std::string& err) {
         const int t = a == 2 ? outer : inner, xa = a == 2 ? inner : outer;
         if (t < 2 || t >= c) continue;
         const long s1 = mirror(xa, n);
-        if (s1 >= t) continue;
+        if (s1 >= t || s1 < g0 || s1 >= g1) continue;  // the ring's sharding group is s1
         const int side = n - 2 * t - 1;  // points between two corners
         int cls = 0;
         while (cls < kRingClasses - 1 && kTE[cls] * kRQ < side) cls++;
@@ -570,13 +570,13 @@ int wire_build_level(int n, WLevel& L, std::string& err) {
         rg[red][cls].push_back(Ring3{(int16_t)a, (int16_t)t, xa});
       }
   std::vector<int> fr;  // frames (red): shells 1 .. c-1
-  for (int r = 1; r < c; r++) fr.push_back(r);
-  // points: the centre (red) and the face centres
+  for (int r = std::max(1, g0); r < std::min(c, g1); r++) fr.push_back(r);
+  // points: the centre (red, group c) and the face centres (group s1)
   std::vector<int4> pt[2];
-  pt[1].push_back(make_int4(c, c, c, 0));
+  if (c >= g0 && c < g1) pt[1].push_back(make_int4(c, c, c, 0));
   for (int a = 0; a < 3; a++)
     for (int side = 0; side < 2; side++)
-      for (int s1 = 1; s1 < c; s1++) {
+      for (int s1 = std::max(1, g0); s1 < std::min(c, g1); s1++) {
         int p[3] = {c, c, c};
         p[a] = side ? n - s1 : s1;
         pt[((s1 + c) % 2) == 0].push_back(make_int4(p[0], p[1], p[2], 0));

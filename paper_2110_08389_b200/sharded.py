@@ -330,7 +330,7 @@ class ShardedSolver:
         self.h, self.cfg = h, cfg
         self.comm = comm or Comm()
         self.ops = ops or NativeShardOps(h, cfg.smoother, cfg.restriction, cfg.nu1, cfg.nu2)
-        self.dims = [(lv.nx, lv.ny) for lv in h.levels]
+        self.dims = list(self.ops.dims)  # per level (nx, ny); (n, n) for cubes
         self.plan = ShardPlan.build(cfg.smoother, self.dims, self.comm.world,
                                     sizes_fn=self.ops.group_sizes, min_groups=min_groups)
         r = self.comm.rank
