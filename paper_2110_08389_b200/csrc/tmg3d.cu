@@ -9,12 +9,13 @@
 // mirrored coordinates, red = even.  Its checker is the CPU restatement in
 // oracle/tweed3d_oracle.c.
 //
-// Fields are C-order (n+1)^3 with k fastest.  A colour stage is leg
-// parallel: one thread per leg eliminates it toward its branch (pivots and
-// right-hand sides to two field-sized scratch arrays), one thread per block
-// solves the branch row, one thread per leg back-substitutes.  Blocks and
-// legs are enumerated with k fastest, so neighbouring threads walk
-// neighbouring lines.
+// Fields are C-order (n+1)^3 with k fastest.  A colour stage runs the block
+// kernel of tmg3dw.cu on hub blocks (a branch with 2, 3 or 6 legs from the
+// walls): per leg a coalesced gather, chunked elimination and PCR with the
+// branch and the wall as end columns, then the branch row, then finalise;
+// blocks are enumerated with k fastest, so neighbouring blocks are
+// neighbouring lines.  This file holds the block enumeration, the 7-point
+// residual, the transfers, the V-cycle (one CUDA graph) and the C ABI.
 #include <algorithm>
 #include <climits>
 #include <cstdio>
@@ -35,345 +36,7 @@ using tmg3::mirror;
 
 namespace {
 
-struct Block3 {
-  int32_t bi, bj, bk;
-  int16_t len;      // points per leg (all legs of a block have s1 - 1)
-  uint8_t nleg;
-  uint8_t red;
-  uint8_t leg[6];   // bits 0-1 axis, bit 2: step -1 (tip at n-1)
-  uint8_t pad[2];
-};
-static_assert(sizeof(Block3) == 24, "Block3 layout");
-
-// one leg of a block (the leg-parallel sweep: one thread per leg)
-struct Leg3 {
-  int32_t ci;       // contribution slot (the leg's index in the colour's leg list)
-  int32_t bi, bj, bk;
-  int16_t len;
-  uint8_t code;     // bits 0-1 axis, bit 2: step -1
-  uint8_t slot;     // leg index within the block
-};
-static_assert(sizeof(Leg3) == 20, "Leg3 layout");
-
-__device__ __forceinline__ double cpl3(const Coef3& c, int a, int s, int i, int j, int k) {
-  if (a == 0) return s < 0 ? __ldg(c.W + i) : __ldg(c.E + i);
-  if (a == 1) return s < 0 ? __ldg(c.S + j) : __ldg(c.N + j);
-  return s < 0 ? __ldg(c.B + k) : __ldg(c.T + k);
-}
-
-__device__ __forceinline__ double diag3(const Coef3& c, int i, int j, int k) {
-  return -(__ldg(c.W + i) + __ldg(c.E + i) + __ldg(c.S + j) + __ldg(c.N + j) + __ldg(c.B + k) +
-           __ldg(c.T + k));
-}
-
-__device__ __forceinline__ unsigned dbit(int a, int s) { return 1u << (2 * a + (s > 0 ? 1 : 0)); }
-
-__device__ __forceinline__ double rhs3(const Coef3& c, int n, const double* __restrict__ u,
-                                       const double* __restrict__ f, int i, int j, int k,
-                                       unsigned skip) {
-  double r = f[idx3(n, i, j, k)];
-  if (!(skip & 1u)) r -= __ldg(c.W + i) * u[idx3(n, i - 1, j, k)];
-  if (!(skip & 2u)) r -= __ldg(c.E + i) * u[idx3(n, i + 1, j, k)];
-  if (!(skip & 4u)) r -= __ldg(c.S + j) * u[idx3(n, i, j - 1, k)];
-  if (!(skip & 8u)) r -= __ldg(c.N + j) * u[idx3(n, i, j + 1, k)];
-  if (!(skip & 16u)) r -= __ldg(c.B + k) * u[idx3(n, i, j, k - 1)];
-  if (!(skip & 32u)) r -= __ldg(c.T + k) * u[idx3(n, i, j, k + 1)];
-  return r;
-}
-
-// Leg-parallel colour stage, three launches: (1) every leg's forward
-// elimination (pivots / rhs to the scratch arrays, its contribution to the
-// branch row into contrib), (2) every branch: num / den in leg order, the
-// branch value, (3) every leg's back substitution from its branch.
-// Per-leg constants: the along-axis coefficient arrays and the four
-// transverse couplings (constant along a straight leg), so a point costs f,
-// four transverse neighbours and two along-axis coefficients.
-struct LegFrame {
-  const double* lo;  // coupling toward decreasing index along the axis
-  const double* hi;
-  double t0, t1, t2, t3, tsum;  // transverse couplings (-b, +b, -c, +c) and their sum
-  long sa, sb_, sc_;             // element strides: along (signed by step), transverse b, c
-  size_t o_tip;
-  int x_tip, step;
-};
-
-__device__ __forceinline__ LegFrame leg_frame(const Coef3& c, int n, const Leg3& G) {
-  LegFrame F;
-  const int a = G.code & 3, s = (G.code & 4) ? -1 : 1;
-  const long n1 = n + 1, str[3] = {n1 * n1, n1, 1};
-  const double* lo3[3] = {c.W, c.S, c.B};
-  const double* hi3[3] = {c.E, c.N, c.T};
-  const int x[3] = {G.bi, G.bj, G.bk};
-  const int b = a == 0 ? 1 : 0, cc = a == 2 ? 1 : 2;  // the transverse axes, in order
-  F.lo = lo3[a];
-  F.hi = hi3[a];
-  F.t0 = __ldg(lo3[b] + x[b]);
-  F.t1 = __ldg(hi3[b] + x[b]);
-  F.t2 = __ldg(lo3[cc] + x[cc]);
-  F.t3 = __ldg(hi3[cc] + x[cc]);
-  F.tsum = F.t0 + F.t1 + F.t2 + F.t3;
-  F.sa = str[a] * s;
-  F.sb_ = str[b];
-  F.sc_ = str[cc];
-  F.x_tip = s > 0 ? 1 : n - 1;
-  F.step = s;
-  const int xt[3] = {a == 0 ? F.x_tip : G.bi, a == 1 ? F.x_tip : G.bj, a == 2 ? F.x_tip : G.bk};
-  F.o_tip = ((size_t)xt[0] * n1 + xt[1]) * (size_t)n1 + xt[2];
-  return F;
-}
-
-__global__ void __launch_bounds__(128) legs_forward_kernel(int n, Coef3 c, const Leg3* __restrict__ legs,
-                                                           int nl, const double* __restrict__ u,
-                                                           const double* __restrict__ f,
-                                                           double* __restrict__ sb,
-                                                           double* __restrict__ sr,
-                                                           double2* __restrict__ contrib, int* err) {
-  const int l = blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= nl) return;
-  const Leg3 G = legs[l];
-  const LegFrame F = leg_frame(c, n, G);
-  const int s = F.step;
-  double bp = 0.0, rp = 0.0, cprev = 0.0;
-  bool bad = false;
-  for (int t = 0; t < G.len; t++) {
-    const int x = F.x_tip + s * t;
-    const size_t o = F.o_tip + (long)t * F.sa;
-    const double lo = __ldg(F.lo + x), hi = __ldg(F.hi + x);
-    const double am = s > 0 ? lo : hi, cn = s > 0 ? hi : lo;  // toward t-1 / t+1
-    double r = f[o] - F.t0 * u[o - F.sb_] - F.t1 * u[o + F.sb_] - F.t2 * u[o - F.sc_] -
-               F.t3 * u[o + F.sc_];
-    const double bb = -(lo + hi + F.tsum);
-    if (t == 0) {
-      r -= am * u[o - F.sa];  // the wall-side neighbour (Dirichlet)
-      bp = bb;
-      rp = r;
-    } else {
-      bad |= bp > -1e-300 && bp < 1e-300;
-      const double w = am / bp;
-      bp = bb - w * cprev;
-      rp = r - w * rp;
-    }
-    cprev = cn;
-    sb[o] = bp;
-    sr[o] = rp;
-  }
-  const double d = cpl3(c, G.code & 3, -s, G.bi, G.bj, G.bk);
-  bad |= bp > -1e-300 && bp < 1e-300;
-  contrib[G.ci] = make_double2(d * rp / bp, d * cprev / bp);
-  if (bad) atomicOr(err, 1);
-}
-
-// Legs along k (the contiguous axis): one warp per leg, lanes along the leg
-// (coalesced), QK points per lane.  Each lane eliminates its chunk to its
-// last point (x = alpha + beta * X_left + gamma * X_end for the others), the
-// chunk ends form a tridiagonal system solved by warp PCR with two
-// right-hand sides (data, coupling to the branch), and every point is left
-// as x = A + G * x_branch in the scratch arrays (A in sb, G in sr) for the
-// back kernel.  2D analogue: tmg_sweep.cu phases B and C.
-template <int QK>
-__global__ void __launch_bounds__(128) kleg_forward_kernel(int n, Coef3 c, const Leg3* __restrict__ legs,
-                                                           int nl, const double* __restrict__ u,
-                                                           const double* __restrict__ f,
-                                                           double* __restrict__ sb,
-                                                           double* __restrict__ sr,
-                                                           double2* __restrict__ contrib, int* err) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (w >= nl) return;
-  constexpr unsigned FULL = 0xffffffffu;
-  const Leg3 G = legs[w];
-  const int s = (G.code & 4) ? -1 : 1, tip = s > 0 ? 1 : n - 1;
-  const int L = G.len, q = (L + 31) / 32;
-  const int p0 = lane * q, cnt = max(0, min(q, L - p0));  // this lane's points
-  const int i = G.bi, j = G.bj;
-  double rho[QK], lam[QK], ivr[QK], cc[QK];
-  bool bad = false;
-  // frozen right-hand sides and couplings; the chunk is eliminated toward its
-  // last point, keeping the coupling to the previous lane's last point (lam)
-  double bp = 0.0, rp = 0.0, lm = 0.0, cprev = 0.0, a_first = 0.0;
-  double r_end = 0.0, b_end = 1.0, a_end = 0.0, c_end = 0.0;  // the chunk end's raw row
-  const int nI = cnt - 1;
-#pragma unroll
-  for (int t = 0; t < QK; t++) {
-    if (t > nI) continue;
-    const int p = p0 + t, k = tip + s * p;
-    unsigned skip = dbit(2, s);
-    if (p > 0) skip |= dbit(2, -s);
-    const double r = rhs3(c, n, u, f, i, j, k, skip);
-    const double bb = diag3(c, i, j, k);
-    const double am = p > 0 ? cpl3(c, 2, -s, i, j, k) : 0.0;
-    cc[t] = cpl3(c, 2, s, i, j, k);
-    if (t == 0) a_first = am;
-    if (t == nI) {  // the chunk end: its raw row, kept for the reduced system
-      r_end = r;
-      b_end = bb;
-      a_end = am;
-      c_end = cc[t];
-      continue;
-    }
-    if (t == 0) {
-      bp = bb;
-      rp = r;
-      lm = -am;
-    } else {
-      const double wv = am / bp;
-      bp = bb - wv * cprev;
-      rp = r - wv * rp;
-      lm = -wv * lm;
-    }
-    bad |= bp > -1e-300 && bp < 1e-300;
-    rho[t] = rp;
-    lam[t] = lm;
-    ivr[t] = 1.0 / bp;
-    cprev = cc[t];
-  }
-  // back pass over the interior: x_t = alpha + beta Xl + gamma Xe
-  double ad = 0.0, bd = 1.0, gd = 0.0, au = 0.0, bu = 0.0, gu = 1.0;
-  if (nI > 0) {
-    double al = 0.0, be = 0.0, ga = 0.0;
-#pragma unroll
-    for (int t = QK - 1; t >= 0; t--) {
-      if (t >= nI) continue;
-      if (t == nI - 1) {
-        al = rho[t] * ivr[t];
-        be = lam[t] * ivr[t];
-        ga = -cc[t] * ivr[t];
-        ad = al; bd = be; gd = ga;
-      } else {
-        al = (rho[t] - cc[t] * al) * ivr[t];
-        be = (lam[t] - cc[t] * be) * ivr[t];
-        ga = -cc[t] * ga * ivr[t];
-      }
-      rho[t] = al;
-      lam[t] = be;
-      ivr[t] = ga;
-    }
-    au = al; bu = be; gu = ga;
-  }
-  // reduced row of the chunk end: A X_prevend + B X + C X_nextend + H xb = D
-  double A = 0.0, B = 1.0, Cc = 0.0, D = 0.0, H = 0.0;
-  const double an = __shfl_down_sync(FULL, au, 1), bn = __shfl_down_sync(FULL, bu, 1);
-  const double gn = __shfl_down_sync(FULL, gu, 1);
-  const int cnt_next = __shfl_down_sync(FULL, cnt, 1);
-  if (cnt > 0) {
-    const double ae = nI > 0 ? a_end : a_first;  // raw coupling toward the previous point
-    const double re = r_end, be_ = b_end, ce = c_end;
-    if (nI > 0) {  // the previous point is x_{nI-1} = ad + bd Xl + gd X
-      A = ae * bd;
-      B = be_ + ae * gd;
-      D = re - ae * ad;
-    } else {  // a one-point chunk: the previous point is the previous lane's end
-      A = ae;
-      B = be_;
-      D = re;
-    }
-    const bool last = p0 + cnt == L;
-    if (!last && cnt_next > 0) {  // next point = next lane's first = an + bn X + gn Xn
-      B += ce * bn;
-      Cc = ce * gn;
-      D -= ce * an;
-    } else if (last) {
-      H = ce;  // coupling to the branch
-    }
-    if (lane == 0) A = 0.0;
-  }
-  for (int d = 1; d < 32; d <<= 1) {
-    double Am = __shfl_up_sync(FULL, A, d), Bm = __shfl_up_sync(FULL, B, d);
-    double Cm = __shfl_up_sync(FULL, Cc, d), Dm = __shfl_up_sync(FULL, D, d);
-    double Hm = __shfl_up_sync(FULL, H, d);
-    double Ap = __shfl_down_sync(FULL, A, d), Bp = __shfl_down_sync(FULL, B, d);
-    double Cp = __shfl_down_sync(FULL, Cc, d), Dp = __shfl_down_sync(FULL, D, d);
-    double Hp = __shfl_down_sync(FULL, H, d);
-    if (lane < d) { Am = 0.0; Bm = 1.0; Cm = 0.0; Dm = 0.0; Hm = 0.0; }
-    if (lane + d > 31) { Ap = 0.0; Bp = 1.0; Cp = 0.0; Dp = 0.0; Hp = 0.0; }
-    const double k1 = A / Bm, k2 = Cc / Bp;
-    A = -k1 * Am;
-    B = B - k1 * Cm - k2 * Ap;
-    D = D - k1 * Dm - k2 * Dp;
-    H = H - k1 * Hm - k2 * Hp;
-    Cc = -k2 * Cp;
-  }
-  bad |= cnt > 0 && B > -1e-300 && B < 1e-300;
-  const double P = D / B, Qh = H / B;  // X_end = P - Qh xb
-  const double Pl = __shfl_up_sync(FULL, P, 1), Ql = __shfl_up_sync(FULL, Qh, 1);
-  const double PL = lane > 0 ? Pl : 0.0, QL = lane > 0 ? Ql : 0.0;
-  // every point as A' + G' xb
-#pragma unroll
-  for (int t = 0; t < QK; t++) {
-    if (t > nI) continue;
-    const size_t o = idx3(n, i, j, tip + s * (p0 + t));
-    if (t == nI) {
-      sb[o] = P;
-      sr[o] = -Qh;
-    } else {
-      sb[o] = rho[t] + lam[t] * PL + ivr[t] * P;
-      sr[o] = -(lam[t] * QL + ivr[t] * Qh);
-    }
-  }
-  if (cnt > 0 && p0 + cnt == L) {
-    const double d = cpl3(c, 2, -s, G.bi, G.bj, G.bk);
-    contrib[G.ci] = make_double2(d * P, d * Qh);
-  }
-  if (bad) atomicOr(err, 1);
-}
-
-__global__ void __launch_bounds__(128) kleg_back_kernel(int n, const Leg3* __restrict__ legs, int nl,
-                                                        double* __restrict__ u,
-                                                        const double* __restrict__ sb,
-                                                        const double* __restrict__ sr) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (w >= nl) return;
-  const Leg3 G = legs[w];
-  const int s = (G.code & 4) ? -1 : 1, tip = s > 0 ? 1 : n - 1;
-  const double xb = u[idx3(n, G.bi, G.bj, G.bk)];
-  for (int p = lane; p < G.len; p += 32) {
-    const size_t o = idx3(n, G.bi, G.bj, tip + s * p);
-    u[o] = sb[o] + sr[o] * xb;
-  }
-}
-
-__global__ void __launch_bounds__(128) branch_kernel(int n, Coef3 c, const Block3* __restrict__ blocks,
-                                                     const int* __restrict__ leg0, int nb,
-                                                     double* __restrict__ u,
-                                                     const double* __restrict__ f,
-                                                     const double2* __restrict__ contrib, int* err) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= nb) return;
-  const Block3 B = blocks[b];
-  unsigned bskip = 0;
-  for (int l = 0; l < B.nleg; l++) {
-    const int a = B.leg[l] & 3, s = (B.leg[l] & 4) ? -1 : 1;
-    bskip |= dbit(a, -s);
-  }
-  double num = rhs3(c, n, u, f, B.bi, B.bj, B.bk, bskip);
-  double den = diag3(c, B.bi, B.bj, B.bk);
-  if (B.len > 0)
-    for (int l = 0; l < B.nleg; l++) {
-      const double2 q = contrib[leg0[b] + l];
-      num -= q.x;
-      den -= q.y;
-    }
-  if (den > -1e-300 && den < 1e-300) atomicOr(err, 1);
-  u[idx3(n, B.bi, B.bj, B.bk)] = num / den;
-}
-
-__global__ void __launch_bounds__(128) legs_back_kernel(int n, Coef3 c, const Leg3* __restrict__ legs,
-                                                        int nl, double* __restrict__ u,
-                                                        const double* __restrict__ sb,
-                                                        const double* __restrict__ sr) {
-  const int l = blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= nl) return;
-  const Leg3 G = legs[l];
-  const LegFrame F = leg_frame(c, n, G);
-  const int s = F.step;
-  double x = u[idx3(n, G.bi, G.bj, G.bk)];
-  for (int t = G.len - 1; t >= 0; t--) {
-    const int xa = F.x_tip + s * t;
-    const size_t o = F.o_tip + (long)t * F.sa;
-    const double cn = s > 0 ? __ldg(F.hi + xa) : __ldg(F.lo + xa);
-    x = (sr[o] - cn * x) / sb[o];
-    u[o] = x;
-  }
-}
+using Block3 = tmg3::HubB;  // branch, legs (s1 - 1 points each), colour
 
 // sharding group of an interior point: 3D tweed blocks lie in
 // one max(i', j', k') shell, 3D wireframe blocks in one min(i', j', k') shell
@@ -389,6 +52,8 @@ __global__ void __launch_bounds__(256) defect3_kernel(int n, Coef3 c, const doub
                                                       double* __restrict__ d,
                                                       unsigned long long* dmax, int gscheme = 0,
                                                       int g0 = 0, int g1 = 1 << 30) {
+  pdl_trigger();
+  pdl_wait();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y, i = blockIdx.z;
   if (k > n) return;
@@ -425,6 +90,8 @@ __global__ void __launch_bounds__(256) defect3_kernel(int n, Coef3 c, const doub
 // coarse = full weighting of d (tensor product of [1/4, 1/2, 1/4])
 __global__ void __launch_bounds__(256) restrict3_kernel(int nf, const double* __restrict__ d,
                                                         double* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int nc = nf / 2;
   const int K = blockIdx.x * blockDim.x + threadIdx.x;
   const int J = blockIdx.y, I = blockIdx.z;
@@ -443,6 +110,8 @@ __global__ void __launch_bounds__(256) restrict3_kernel(int nf, const double* __
 // u += trilinear P uc on the fine interior
 __global__ void __launch_bounds__(256) prolong3_kernel(int nc, const double* __restrict__ uc,
                                                        double* __restrict__ u) {
+  pdl_trigger();
+  pdl_wait();
   const int nf = 2 * nc;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y, i = blockIdx.z;
@@ -458,12 +127,21 @@ __global__ void __launch_bounds__(256) prolong3_kernel(int nc, const double* __r
 }
 
 __global__ void coarse3_kernel(Coef3 c, double* u, const double* f) {
+  pdl_trigger();
+  pdl_wait();
   const int n = 2;
   const double cc = -(c.W[1] + c.E[1] + c.S[1] + c.N[1] + c.B[1] + c.T[1]);
   const double r = f[idx3(n, 1, 1, 1)] - c.W[1] * u[idx3(n, 0, 1, 1)] - c.E[1] * u[idx3(n, 2, 1, 1)] -
                    c.S[1] * u[idx3(n, 1, 0, 1)] - c.N[1] * u[idx3(n, 1, 2, 1)] -
                    c.B[1] * u[idx3(n, 1, 1, 0)] - c.T[1] * u[idx3(n, 1, 1, 2)];
   u[idx3(n, 1, 1, 1)] = r / cc;
+}
+
+__global__ void __launch_bounds__(256) zero3_kernel(double* __restrict__ p, size_t m) {
+  pdl_trigger();
+  pdl_wait();
+  for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (size_t)gridDim.x * blockDim.x)
+    p[q] = 0.0;
 }
 
 __global__ void cube_gather_kernel(const double* __restrict__ fld, const long long* __restrict__ off,
@@ -492,20 +170,13 @@ int fail3(int code, const std::string& m) {
 struct tmg_cube {
   int scheme = 0;                     // 0 tweed, 1 wireframe
   std::vector<tmg3::WLevel> wl;       // wireframe blocks per level
+  std::vector<tmg3::HubLevel> hl;     // 3D tweed blocks per level (the block kernel)
   std::map<std::tuple<int, int, int>, tmg3::WLevel> wparts;  // (level, g0, g1): a rank's blocks
   std::vector<int> n;                 // per level
   std::vector<double*> coef;          // per level: W E S N B T (6 (n+1))
-  std::vector<Block3*> blocks[2];     // per level: black, red lists
-  std::vector<int> nblocks[2];
-  std::vector<Leg3*> legs[2];         // per level and colour: legs of the blocks
-  std::vector<int*> leg0[2];          // first leg of every block
-  std::vector<int> nlegs[2];
-  std::vector<Leg3*> klegs[2];        // legs along k (warp per leg)
-  std::vector<int> nklegs[2];
-  int ncontrib = 1;
-  double2* contrib = nullptr;         // per leg (sized for the largest level)
+  std::vector<int> nblocks[2];        // per level: black, red 3D tweed block counts
   std::vector<double*> U, F;          // per level work fields (level 0: session)
-  double *sb = nullptr, *sr = nullptr, *d = nullptr;  // finest-size scratch
+  double* d = nullptr;                // finest-size defect scratch
   int* err = nullptr;
   unsigned long long* dmax = nullptr;
   int* h_err = nullptr;
@@ -567,39 +238,9 @@ int sweep3(tmg_cube* h, int l, double* u, const double* f, cudaStream_t s) {
         return cuda3(cudaGetLastError(), "wireframe stage");
     return TMG_OK;
   }
-  for (int red = 1; red >= 0; red--) {
-    const int nb = h->nblocks[red][l], nl = h->nlegs[red][l], nk = h->nklegs[red][l];
-    if (!nb) continue;
-    if (nl) {
-      TMG_COUNT(1);
-      legs_forward_kernel<<<(nl + 127) / 128, 128, 0, s>>>(n, coefs(h, l), h->legs[red][l], nl,
-                                                           u, f, h->sb, h->sr, h->contrib, h->err);
-    }
-    if (nk) {
-      TMG_COUNT(1);
-      const int grid = (nk * 32 + 127) / 128;
-      if (n / 2 - 1 <= 4 * 32)  // the longest leg has n/2 - 1 points
-        kleg_forward_kernel<4><<<grid, 128, 0, s>>>(n, coefs(h, l), h->klegs[red][l], nk, u, f,
-                                                    h->sb, h->sr, h->contrib, h->err);
-      else
-        kleg_forward_kernel<8><<<grid, 128, 0, s>>>(n, coefs(h, l), h->klegs[red][l], nk, u, f,
-                                                    h->sb, h->sr, h->contrib, h->err);
-    }
-    TMG_COUNT(1);
-    branch_kernel<<<(nb + 127) / 128, 128, 0, s>>>(n, coefs(h, l), h->blocks[red][l],
-                                                   h->leg0[red][l], nb, u, f, h->contrib, h->err);
-    if (nl) {
-      TMG_COUNT(1);
-      legs_back_kernel<<<(nl + 127) / 128, 128, 0, s>>>(n, coefs(h, l), h->legs[red][l], nl, u,
-                                                        h->sb, h->sr);
-    }
-    if (nk) {
-      TMG_COUNT(1);
-      kleg_back_kernel<<<(nk * 32 + 127) / 128, 128, 0, s>>>(n, h->klegs[red][l], nk, u, h->sb,
-                                                             h->sr);
-    }
-    T3(cudaGetLastError());
-  }
+  for (int red = 1; red >= 0; red--)
+    if (tmg3::hub_stage(h->hl[l], n, coefs(h, l), red, u, f, h->err, s))
+      return cuda3(cudaGetLastError(), "tweed stage");
   return TMG_OK;
 }
 
@@ -612,18 +253,21 @@ int cycle3(tmg_cube* h, int nu1, int nu2, cudaStream_t s, int l0 = 0) {
       int st = sweep3(h, l, h->U[l], h->F[l], s);
       if (st) return st;
     }
-    TMG_COUNT(2);
-    defect3_kernel<<<grid3(h->n[l]), 256, 0, s>>>(h->n[l], coefs(h, l), h->U[l], h->F[l], h->d,
-                                                  nullptr);
-    restrict3_kernel<<<grid3(h->n[l + 1]), 256, 0, s>>>(h->n[l], h->d, h->F[l + 1]);
+    TMG_COUNT(3);
+    T3(launch_pdl(defect3_kernel, grid3(h->n[l]), dim3(256), 0, s, h->n[l], coefs(h, l), h->U[l],
+                  h->F[l], h->d, (unsigned long long*)nullptr, 0, 0, 1 << 30));
+    T3(launch_pdl(restrict3_kernel, grid3(h->n[l + 1]), dim3(256), 0, s, h->n[l], h->d,
+                  h->F[l + 1]));
     const size_t nc = (size_t)(h->n[l + 1] + 1) * (h->n[l + 1] + 1) * (h->n[l + 1] + 1);
-    T3(cudaMemsetAsync(h->U[l + 1], 0, nc * sizeof(double), s));
+    T3(launch_pdl(zero3_kernel, dim3((unsigned)std::min<size_t>((nc + 255) / 256, 148 * 16)),
+                  dim3(256), 0, s, h->U[l + 1], nc));
   }
   TMG_COUNT(1);
-  coarse3_kernel<<<1, 1, 0, s>>>(coefs(h, L - 1), h->U[L - 1], h->F[L - 1]);
+  T3(launch_pdl(coarse3_kernel, dim3(1), dim3(1), 0, s, coefs(h, L - 1), h->U[L - 1], h->F[L - 1]));
   for (int l = L - 2; l >= l0; l--) {
     TMG_COUNT(1);
-    prolong3_kernel<<<grid3(h->n[l]), 256, 0, s>>>(h->n[l + 1], h->U[l + 1], h->U[l]);
+    T3(launch_pdl(prolong3_kernel, grid3(h->n[l]), dim3(256), 0, s, h->n[l + 1], h->U[l + 1],
+                  h->U[l]));
     for (int k = 0; k < nu2; k++) {
       int st = sweep3(h, l, h->U[l], h->F[l], s);
       if (st) return st;
@@ -680,53 +324,17 @@ int tmg_cube_create_scheme(int n, const double* x, int scheme, tmg_cube** out) {
       }
     }
     std::vector<Block3> bl[2];
-    if (scheme == 0) build_blocks(m, bl);
-    for (int r = 0; r < 2; r++) {
-      Block3* db = nullptr;
-      if (!bl[r].empty()) {
-        T3(cudaMalloc(&db, bl[r].size() * sizeof(Block3)));
-        T3(cudaMemcpy(db, bl[r].data(), bl[r].size() * sizeof(Block3), cudaMemcpyHostToDevice));
+    if (scheme == 0) {
+      build_blocks(m, bl);
+      h->hl.emplace_back();
+      std::string err;
+      const int st = tmg3::hub_build_level(m, bl, h->hl.back(), err);
+      if (st) {
+        tmg_cube_destroy(h);
+        return fail3(st == 2 ? TMG_BADARG : TMG_CUDA, err);
       }
-      h->blocks[r].push_back(db);
-      h->nblocks[r].push_back((int)bl[r].size());
-      std::vector<Leg3> lg, lk;  // legs along i / j (thread per leg), along k (warp per leg)
-      std::vector<int> l0;
-      int ci = 0;
-      // k legs of levels up to 129^3 run warp-per-leg (measured faster there:
-      // 0.53 -> 0.30 ms per sweep at 129^3); at 257^3 the thread-per-leg path
-      // is faster (0.99 vs 1.09 ms)
-      const bool warp_k = m / 2 - 1 <= 64;
-      for (size_t b = 0; b < bl[r].size(); b++) {
-        const Block3& B = bl[r][b];
-        l0.push_back(ci);
-        if (B.len == 0) continue;
-        for (int q = 0; q < B.nleg; q++) {
-          const Leg3 G{ci++, B.bi, B.bj, B.bk, B.len, B.leg[q], (uint8_t)q};
-          ((B.leg[q] & 3) == 2 && warp_k ? lk : lg).push_back(G);
-        }
-      }
-      Leg3* dl = nullptr;
-      int* d0 = nullptr;
-      if (!lg.empty()) {
-        T3(cudaMalloc(&dl, lg.size() * sizeof(Leg3)));
-        T3(cudaMemcpy(dl, lg.data(), lg.size() * sizeof(Leg3), cudaMemcpyHostToDevice));
-      }
-      if (!l0.empty()) {
-        T3(cudaMalloc(&d0, l0.size() * sizeof(int)));
-        T3(cudaMemcpy(d0, l0.data(), l0.size() * sizeof(int), cudaMemcpyHostToDevice));
-      }
-      h->legs[r].push_back(dl);
-      h->leg0[r].push_back(d0);
-      h->nlegs[r].push_back((int)lg.size());
-      Leg3* dk = nullptr;
-      if (!lk.empty()) {
-        T3(cudaMalloc(&dk, lk.size() * sizeof(Leg3)));
-        T3(cudaMemcpy(dk, lk.data(), lk.size() * sizeof(Leg3), cudaMemcpyHostToDevice));
-      }
-      h->klegs[r].push_back(dk);
-      h->nklegs[r].push_back((int)lk.size());
-      h->ncontrib = std::max(h->ncontrib, ci);
     }
+    for (int r = 0; r < 2; r++) h->nblocks[r].push_back((int)bl[r].size());
     const size_t tot = (size_t)(m + 1) * (m + 1) * (m + 1);
     double *pu = nullptr, *pf = nullptr;
     T3(cudaMalloc(&pu, tot * sizeof(double)));
@@ -741,11 +349,6 @@ int tmg_cube_create_scheme(int n, const double* x, int scheme, tmg_cube** out) {
     xs.swap(c);
   }
   const size_t tot = (size_t)(n + 1) * (n + 1) * (n + 1);
-  T3(cudaMalloc(&h->contrib, h->ncontrib * sizeof(double2)));
-  if (scheme == 0) {  // the tweed legs' elimination scratch
-    T3(cudaMalloc(&h->sb, tot * sizeof(double)));
-    T3(cudaMalloc(&h->sr, tot * sizeof(double)));
-  }
   T3(cudaMalloc(&h->d, tot * sizeof(double)));
   T3(cudaMalloc(&h->err, sizeof(int) + sizeof(unsigned long long) * 2));
   h->dmax = reinterpret_cast<unsigned long long*>(h->err + 2);
@@ -760,19 +363,11 @@ int tmg_cube_destroy(tmg_cube* h) {
   if (!h) return TMG_OK;
   if (h->graph) cudaGraphExecDestroy(h->graph);
   for (double* p : h->coef) cudaFree(p);
-  for (int r = 0; r < 2; r++) {
-    for (Block3* p : h->blocks[r]) cudaFree(p);
-    for (Leg3* p : h->legs[r]) cudaFree(p);
-    for (Leg3* p : h->klegs[r]) cudaFree(p);
-    for (int* p : h->leg0[r]) cudaFree(p);
-  }
-  cudaFree(h->contrib);
   for (auto& w : h->wl) tmg3::wire_free_level(w);
   for (auto& kv : h->wparts) tmg3::wire_free_level(kv.second);
+  for (auto& w : h->hl) tmg3::hub_free_level(w);
   for (double* p : h->U) cudaFree(p);
   for (double* p : h->F) cudaFree(p);
-  cudaFree(h->sb);
-  cudaFree(h->sr);
   cudaFree(h->d);
   cudaFree(h->err);
   cudaFreeHost(h->h_err);

@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -54,6 +55,34 @@ struct WLevel {
 };
 
 // blocks of sharding groups [g0, g1) only (group = min(i', j', k'): the shell)
+// ---------------------------------------------------------------------------
+// 3D tweed hub blocks (tmg3dw.cu, the same block kernel): a branch with 2, 3
+// or 6 legs running from the walls (tmg3d.cu build_blocks)
+struct HubB {
+  int32_t bi, bj, bk;  // the branch
+  int16_t len;         // points per leg (s1 - 1)
+  uint8_t nleg;
+  uint8_t red;
+  uint8_t leg[6];      // bits 0-1 axis, bit 2: step -1 (tip at n-1)
+  uint8_t pad[2];
+};
+static_assert(sizeof(HubB) == 24, "HubB layout");
+
+constexpr int kHubKinds = 2;    // 2 legs; 3 or 6 legs
+constexpr int kHubClasses = 6;  // TE = 1 .. 32 threads per leg
+
+struct HubLevel {
+  HubB* blocks[2][kHubKinds][kHubClasses] = {};
+  int nblocks[2][kHubKinds][kHubClasses] = {};
+  int4* points[2] = {};  // legless branches
+  int npoints[2] = {};
+};
+
+int hub_build_level(int n, const std::vector<HubB> blocks[2], HubLevel& L, std::string& err);
+void hub_free_level(HubLevel& L);
+int hub_stage(const HubLevel& L, int n, const Coef3& c, int red, double* u, const double* f,
+              int* err, cudaStream_t s);
+
 int wire_build_level(int n, WLevel& L, std::string& err, int g0 = 0, int g1 = 1 << 30);
 void wire_free_level(WLevel& L);
 // one colour stage (red = 1 / black = 0) of the wireframe sweep

@@ -61,42 +61,69 @@ __host__ __device__ constexpr int tab_len(int n) { return n + 1 + (n + 1) / 8 + 
 template <int Q>
 __device__ __forceinline__ int rsw(int p) { return (p & ~(Q - 1)) | ((p ^ (p / Q)) & (Q - 1)); }
 
-// A block: a ring (NE = 4: face normal a at xa, level t) or a frame
-// (NE = 12: shell t).  Corners: ring K = 0..3 at in-face (b, c) = (t, t),
+// Block kinds.  A ring (NE = 4 edges: face normal a at xa, level t), a frame
+// (NE = 12: shell t) or a 3D tweed hub block (NE = 2, 3 or 6 legs meeting at
+// a branch; tmg3d.cu).  Corners: ring K = 0..3 at in-face (b, c) = (t, t),
 // (n-t, t), (n-t, n-t), (t, n-t) (layout.py:136-143's ring order: side 0
 // runs K0 -> K1, side 1 K1 -> K2, side 2 K2 -> K3, side 3 K3 -> K0); frame K
-// = 0..7 with bit a set for coordinate n - t on axis a.
+// = 0..7 with bit a set for coordinate n - t on axis a; hub K = 0 the branch
+// (the only unknown corner), K = 1 + e the wall point at the tip end of leg
+// e (a Dirichlet value).
+constexpr int kRing = 0, kFrame = 1, kHub = 2;
+
+template <int KIND, int NE>
+constexpr int ncorners() { return KIND == kRing ? 4 : (KIND == kFrame ? 8 : 1 + NE); }
+
 struct WBlk {
-  int a, xa, t;
+  int a, xa, t;    // ring / frame
+  int p[3];        // hub: the branch
+  unsigned codes;  // hub: leg e in bits 3e .. 3e+2 (axis; bit 2: tip at n-1)
+  int nleg;        // hub: legs in use (NE = 6 kernels also take 3-leg blocks)
 };
 
-template <int NE>
+template <int KIND, int NE>
 __device__ __forceinline__ void corner_pos(const WBlk& B, int n, int K, int P[3]) {
-  if (NE == 12) {
+  if (KIND == kFrame) {
     P[0] = K & 1 ? n - B.t : B.t;
     P[1] = K & 2 ? n - B.t : B.t;
     P[2] = K & 4 ? n - B.t : B.t;
-  } else {
+  } else if (KIND == kRing) {
     const int pb = (K == 1 || K == 2) ? n - B.t : B.t, pc = K >= 2 ? n - B.t : B.t;
     P[0] = B.a == 0 ? B.xa : pb;
     P[1] = B.a == 1 ? B.xa : (B.a == 0 ? pb : pc);
     P[2] = B.a == 2 ? B.xa : pc;
+  } else {
+    P[0] = B.p[0];
+    P[1] = B.p[1];
+    P[2] = B.p[2];
+    if (K > 0) {
+      const unsigned code = (B.codes >> (3 * (K - 1))) & 7u;
+      const int a = code & 3, w = (code & 4) ? n : 0;
+      P[0] = a == 0 ? w : P[0];
+      P[1] = a == 1 ? w : P[1];
+      P[2] = a == 2 ? w : P[2];
+    }
   }
 }
 
 // edge e: axis x, from corner K0 (lower coordinate) to K1
-template <int NE>
+template <int KIND, int NE>
 __device__ __forceinline__ void edge_def(const WBlk& B, int e, int& x, int& K0, int& K1) {
-  if (NE == 12) {
+  if (KIND == kFrame) {
     x = e >> 2;
     const int h = e & 3, o1 = x == 0 ? 1 : 0, o2 = x == 2 ? 1 : 2;
     K0 = ((h & 1) << o1) | (((h >> 1) & 1) << o2);
     K1 = K0 | (1 << x);
-  } else {
+  } else if (KIND == kRing) {
     const int b = B.a == 0 ? 1 : 0, c = B.a == 2 ? 1 : 2;
     x = (e & 1) ? c : b;
     K0 = e == 0 ? 0 : (e == 1 ? 1 : (e == 2 ? 3 : 0));
     K1 = e == 0 ? 1 : (e == 1 ? 2 : (e == 2 ? 2 : 3));
+  } else {
+    const unsigned code = (B.codes >> (3 * e)) & 7u;
+    x = code & 3;
+    K0 = (code & 4) ? 0 : 1 + e;  // tip at n-1: the branch is the lower end
+    K1 = (code & 4) ? 1 + e : 0;
   }
 }
 
@@ -112,12 +139,12 @@ struct EdgeG {
 
 // The cube API builds every axis from one coordinate array
 // (tmg_cube_create), so W = S = B and E = N = T: c.W / c.E serve every axis.
-template <int NE>
+template <int KIND, int NE>
 __device__ __forceinline__ EdgeG edge_geom(const Coef3& c, int n, const WBlk& B, int e) {
   int x, K0, K1, P0[3], P1[3];
-  edge_def<NE>(B, e, x, K0, K1);
-  corner_pos<NE>(B, n, K0, P0);
-  corner_pos<NE>(B, n, K1, P1);
+  edge_def<KIND, NE>(B, e, x, K0, K1);
+  corner_pos<KIND, NE>(B, n, K0, P0);
+  corner_pos<KIND, NE>(B, n, K1, P1);
   const int o1 = x == 0 ? 1 : 0, o2 = x == 2 ? 1 : 2;
   const long n1 = n + 1, str[3] = {n1 * n1, n1, 1};
   EdgeG G;
@@ -233,22 +260,27 @@ __device__ __forceinline__ void chunk_finalise(double* rr, int p0, int e, double
   rr[rsw<Q>(p0 + e)] = XE;
 }
 
-template <int NE, int TE, int BD, int Q>
+// threads of a CTA: whole blocks of NE * TE threads, at most BDMAX
+template <int NE, int TE, int BDMAX>
+constexpr int wblock_bd() { return (BDMAX / (NE * TE)) * NE * TE; }
+
+template <int NE, int TE, int BDMAX, int Q>
 constexpr size_t wblock_smem() {
-  return ((size_t)BD * (Q + 6) + 2 * (size_t)tab_len(kMaxN)) * sizeof(double);
+  return ((size_t)wblock_bd<NE, TE, BDMAX>() * (Q + 6) + 2 * (size_t)tab_len(kMaxN)) * sizeof(double);
 }
 
-// Blocks of one kind and class: BD / (NE TE) blocks per CTA, TE threads per
-// edge.  Blocks come from `rings` (NE = 4) or `frames` (NE = 12, the shell
-// index).
-template <int NE, int TE, int BD, int Q>
-__global__ void __launch_bounds__(BD, NE == 4 ? (Q <= 8 ? (BD > 256 ? 2 : 3) : 2) : 1)
-    wblock_kernel(int n, Coef3 c, const Ring3* __restrict__ rings, const int* __restrict__ frames,
-                  int nb, double* __restrict__ u, const double* __restrict__ f, int* err) {
-  constexpr int NK = NE == 4 ? 4 : 8;
+// Blocks of one kind and class: whole blocks of NE * TE threads per CTA, TE
+// threads per edge.  `blocks`: Ring3 (rings), int shell (frames) or HubB
+// (3D tweed hub blocks).
+template <int KIND, int NE, int TE, int BDMAX, int Q>
+__global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1 : 2)
+    wblock_kernel(int n, Coef3 c, const void* __restrict__ blocks, int nb, double* __restrict__ u,
+                  const double* __restrict__ f, int* err) {
+  constexpr int NK = ncorners<KIND, NE>();
   constexpr int SL = NE * TE;  // threads per block
+  constexpr int BD = wblock_bd<NE, TE, BDMAX>();
   constexpr int BPC = BD / SL;
-  static_assert(BPC >= 1 && SL >= NK, "block slice");
+  static_assert(BPC >= 1 && (SL >= NK || KIND == kHub), "block slice");
   extern __shared__ double wsm[];
   double* sR = wsm;  // BD * Q
   double *sA = sR + BD * Q, *sB = sA + BD, *sC = sB + BD, *sD = sC + BD, *sH0 = sD + BD,
@@ -260,21 +292,28 @@ __global__ void __launch_bounds__(BD, NE == 4 ? (Q <= 8 ? (BD > 256 ? 2 : 3) : 2
   const int bid = blockIdx.x * BPC + g;
   const bool live = bid < nb;
   WBlk B;
-  if (NE == 4) {
-    Ring3 R;
-    if (live) R = rings[bid];
-    else { R.a = 0; R.t = 1; R.xa = 1; }
-    B.a = R.a; B.xa = R.xa; B.t = R.t;
-  } else {
-    B.a = 0; B.xa = 0; B.t = live ? frames[bid] : 1;
+  B.a = 0; B.xa = 0; B.t = 1; B.p[0] = B.p[1] = B.p[2] = 1; B.codes = 0; B.nleg = NE;
+  if (KIND == kRing) {
+    if (live) {
+      const Ring3 R = static_cast<const Ring3*>(blocks)[bid];
+      B.a = R.a; B.xa = R.xa; B.t = R.t;
+    }
+  } else if (KIND == kFrame) {
+    if (live) B.t = static_cast<const int*>(blocks)[bid];
+  } else if (live) {
+    const HubB H = static_cast<const HubB*>(blocks)[bid];
+    B.p[0] = H.bi; B.p[1] = H.bj; B.p[2] = H.bk;
+    B.nleg = H.nleg;
+    for (int e = 0; e < NE; e++) B.codes |= (unsigned)(e < H.nleg ? H.leg[e] : 0) << (3 * e);
   }
   for (int x = tid; x <= n; x += BD) {
     tlo[tix<Q>(x)] = __ldg(c.W + x);
     thi[tix<Q>(x)] = __ldg(c.E + x);
   }
-  const EdgeG G = edge_geom<NE>(c, n, B, ed);
-  const int L = live ? G.L : 0;
+  const EdgeG G = edge_geom<KIND, NE>(c, n, B, ed);
+  const int L = live && (KIND != kHub || ed < B.nleg) ? G.L : 0;  // unused hub legs: empty
   double* rr = sR + (g * NE + ed) * TE * Q;
+  tmg::pdl_wait();  // the previous kernel's fields are complete from here on
   // 1. gather: edge points (four transverse neighbours), and the corner rows
   {
     constexpr int NB = 4;  // points whose loads are in flight together
@@ -300,28 +339,31 @@ __global__ void __launch_bounds__(BD, NE == 4 ? (Q <= 8 ? (BD > 256 ? 2 : 3) : 2
       }
     }
   }
-  if (live && tid % SL < NK) {
-    const int K = tid % SL;
+  for (int K = tid % SL; live && K < NK; K += SL) {
     int P[3];
-    corner_pos<NE>(B, n, K, P);
-    unsigned in = 0;  // in-block directions: bit 2a (toward -), 2a+1 (toward +)
-    for (int e = 0; e < NE; e++) {
-      int x, K0, K1;
-      edge_def<NE>(B, e, x, K0, K1);
-      if (K0 == K) in |= 2u << (2 * x);
-      if (K1 == K) in |= 1u << (2 * x);
-    }
+    corner_pos<KIND, NE>(B, n, K, P);
     const long n1 = n + 1, str[3] = {n1 * n1, n1, 1};
     const size_t o = ((size_t)P[0] * n1 + P[1]) * (size_t)n1 + P[2];
-    double d = 0.0, rk = f[o];
-    for (int a = 0; a < 3; a++) {
-      const double lo = __ldg(c.W + P[a]), hi = __ldg(c.E + P[a]);
-      d -= lo + hi;
-      if (!(in & (1u << (2 * a)))) rk -= lo * u[o - str[a]];
-      if (!(in & (2u << (2 * a)))) rk -= hi * u[o + str[a]];
+    if (KIND == kHub && K > 0) {
+      sXc[g][K] = u[o];  // a wall point: its Dirichlet value
+    } else {
+      unsigned in = 0;  // in-block directions: bit 2a (toward -), 2a+1 (toward +)
+      for (int e = 0; e < (KIND == kHub ? B.nleg : NE); e++) {
+        int x, K0, K1;
+        edge_def<KIND, NE>(B, e, x, K0, K1);
+        if (K0 == K) in |= 2u << (2 * x);
+        if (K1 == K) in |= 1u << (2 * x);
+      }
+      double d = 0.0, rk = f[o];
+      for (int a = 0; a < 3; a++) {
+        const double lo = __ldg(c.W + P[a]), hi = __ldg(c.E + P[a]);
+        d -= lo + hi;
+        if (!(in & (1u << (2 * a)))) rk -= lo * u[o - str[a]];
+        if (!(in & (2u << (2 * a)))) rk -= hi * u[o + str[a]];
+      }
+      sKr[g][K] = rk;
+      sKd[g][K] = d;
     }
-    sKr[g][K] = rk;
-    sKd[g][K] = d;
   }
   __syncthreads();
   // 2. chunk eliminations
@@ -413,7 +455,29 @@ __global__ void __launch_bounds__(BD, NE == 4 ? (Q <= 8 ? (BD > 256 ? 2 : 3) : 2
   }
   __syncthreads();
   // 4. the corner rows with the edge end points substituted
-  if (live && tid % SL == 0) {
+  if (KIND == kHub && live && tid % SL == 0) {
+    // the branch row (m_legged_thomas's closing row, tridiag.py:84-125) with
+    // every leg's end point next to it substituted; the walls are known
+    double m = sKd[g][0], rhs = sKr[g][0];
+    for (int eg = 0; eg < B.nleg; eg++) {
+      int x, K0, K1, P0[3];
+      edge_def<KIND, NE>(B, eg, x, K0, K1);
+      corner_pos<KIND, NE>(B, n, 0, P0);
+      const int xb = x == 0 ? P0[0] : (x == 1 ? P0[1] : P0[2]);
+      if (K1 == 0) {  // tip at the low wall: the branch follows the leg's last point
+        const double cw = __ldg(c.W + xb);
+        m += cw * sEnd[g][eg][5];
+        rhs -= cw * (sEnd[g][eg][3] + sEnd[g][eg][4] * sXc[g][K0]);
+      } else {
+        const double ce = __ldg(c.E + xb);
+        m += ce * sEnd[g][eg][1];
+        rhs -= ce * (sEnd[g][eg][0] + sEnd[g][eg][2] * sXc[g][K1]);
+      }
+    }
+    bad |= wbad(m);
+    sXc[g][0] = rhs / m;
+  }
+  if (KIND != kHub && live && tid % SL == 0) {
     double M[NK][NK + 1];
     for (int K = 0; K < NK; K++) {
       for (int q = 0; q < NK; q++) M[K][q] = 0.0;
@@ -422,9 +486,9 @@ __global__ void __launch_bounds__(BD, NE == 4 ? (Q <= 8 ? (BD > 256 ? 2 : 3) : 2
     }
     for (int eg = 0; eg < NE; eg++) {
       int x, K0, K1, P0[3], P1[3];
-      edge_def<NE>(B, eg, x, K0, K1);
-      corner_pos<NE>(B, n, K0, P0);
-      corner_pos<NE>(B, n, K1, P1);
+      edge_def<KIND, NE>(B, eg, x, K0, K1);
+      corner_pos<KIND, NE>(B, n, K0, P0);
+      corner_pos<KIND, NE>(B, n, K1, P1);
       const int x0 = x == 0 ? P0[0] : (x == 1 ? P0[1] : P0[2]);
       const int x1 = x == 0 ? P1[0] : (x == 1 ? P1[1] : P1[2]);
       const double c0 = __ldg(c.E + x0), c1 = __ldg(c.W + x1);
@@ -458,21 +522,22 @@ __global__ void __launch_bounds__(BD, NE == 4 ? (Q <= 8 ? (BD > 256 ? 2 : 3) : 2
     }
   }
   __syncthreads();
-  if (live && tid % SL < NK) {
+  if (live && tid % SL < (KIND == kHub ? 1 : NK)) {  // hubs: the walls stay
     int P3[3];
-    corner_pos<NE>(B, n, tid % SL, P3);
+    corner_pos<KIND, NE>(B, n, tid % SL, P3);
     u[idx3(n, P3[0], P3[1], P3[2])] = sXc[g][tid % SL];
   }
   // 5. finalise every chunk with both ends known, then scatter
   if (cnt > 0) {
     int x, K0, K1;
-    edge_def<NE>(B, ed, x, K0, K1);
+    edge_def<KIND, NE>(B, ed, x, K0, K1);
     const double xa = sXc[g][K0], xb = sXc[g][K1];
     const double XE = P - Q0 * xa - Q1 * xb;
     const double XL = lt == 0 ? xa : sD[tid - 1] - sH0[tid - 1] * xa - sH1[tid - 1] * xb;
     chunk_finalise<Q>(rr, p0, e, XL, XE, mu, amq);
   }
   __syncthreads();
+  tmg::pdl_trigger();  // the successor may launch while this CTA scatters
 #pragma unroll 4
   for (int it = 0; it < Q; it++) {
     const int q = lt + it * TE;
@@ -484,6 +549,8 @@ __global__ void __launch_bounds__(BD, NE == 4 ? (Q <= 8 ? (BD > 256 ? 2 : 3) : 2
 __global__ void __launch_bounds__(128) wpoint_kernel(int n, Coef3 c, const int4* __restrict__ pts,
                                                      int np, double* __restrict__ u,
                                                      const double* __restrict__ f, int* err) {
+  tmg::pdl_trigger();
+  tmg::pdl_wait();
   const int id = blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= np) return;
   const int4 P = pts[id];
@@ -517,29 +584,77 @@ int upload(const std::vector<T>& v, T** out, std::string& err) {
   return 0;
 }
 
-template <int NE, int TE, int BD, int Q>
+template <int KIND, int NE, int TE, int BDMAX, int Q>
 cudaError_t allow_smem() {
-  return cudaFuncSetAttribute(wblock_kernel<NE, TE, BD, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)wblock_smem<NE, TE, BD, Q>());
+  return cudaFuncSetAttribute(wblock_kernel<KIND, NE, TE, BDMAX, Q>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)wblock_smem<NE, TE, BDMAX, Q>());
+}
+
+template <int KIND, int NE, int TE, int BDMAX, int Q>
+void launch_blocks(const void* blocks, int nb, int n, const Coef3& c, double* u, const double* f,
+                   int* err, cudaStream_t s) {
+  if (!nb) return;
+  constexpr int BD = wblock_bd<NE, TE, BDMAX>(), BPC = BD / (NE * TE);
+  TMG_COUNT(1);
+  tmg::launch_pdl(wblock_kernel<KIND, NE, TE, BDMAX, Q>, dim3((nb + BPC - 1) / BPC), dim3(BD),
+                  wblock_smem<NE, TE, BDMAX, Q>(), s, n, c, blocks, nb, u, f, err);
 }
 
 template <int TE>
 void launch_rings(const WLevel& L, int n, const Coef3& c, int red, int k, double* u, const double* f,
                   int* err, cudaStream_t s) {
-  constexpr int BD = ring_bd(TE), BPC = BD / (4 * TE);
-  const int nr = L.nrings[red][k];
-  if (!nr) return;
-  TMG_COUNT(1);
-  wblock_kernel<4, TE, BD, kRQ><<<(nr + BPC - 1) / BPC, BD, wblock_smem<4, TE, BD, kRQ>(), s>>>(
-      n, c, L.rings[red][k], nullptr, nr, u, f, err);
+  launch_blocks<kRing, 4, TE, ring_bd(TE), kRQ>(L.rings[red][k], L.nrings[red][k], n, c, u, f, err, s);
 }
 
 template <int TE>
 void launch_frames(const WLevel& L, int n, const Coef3& c, double* u, const double* f, int* err,
                    cudaStream_t s) {
-  TMG_COUNT(1);
-  wblock_kernel<12, TE, 12 * TE, kQW><<<L.nframes, 12 * TE, wblock_smem<12, TE, 12 * TE, kQW>(), s>>>(
-      n, c, nullptr, L.frames, L.nframes, u, f, err);
+  launch_blocks<kFrame, 12, TE, 12 * TE, kQW>(L.frames, L.nframes, n, c, u, f, err, s);
+}
+
+// 3D tweed hub blocks: classes by legs (2, 3, 6) and threads per leg
+constexpr int kHubLegs[kHubKinds] = {2, 6};  // 3-leg blocks run in the 6-leg kernels
+constexpr int kHubTE[kHubClasses] = {1, 2, 4, 8, 16, 32};
+
+// A launch class with less than two waves of CTAs is folded into the next
+// larger class (its blocks then run with idle threads): the small classes of
+// the coarse levels cost a launch latency each and little work.
+template <class T>
+void merge_small_classes(std::vector<T>* cls, int nc, int ne, const int* te) {
+  for (int q = 0; q + 1 < nc; q++) {
+    const size_t per_cta = std::max(1, kRBD / (ne * te[q]));
+    if (cls[q].empty() || cls[q].size() >= 2 * 148 * per_cta) continue;
+    int nxt = q + 1;
+    while (nxt + 1 < nc && cls[nxt].empty()) nxt++;
+    if (cls[nxt].empty()) continue;  // the largest non-empty class stays
+    cls[nxt].insert(cls[nxt].begin(), cls[q].begin(), cls[q].end());
+    cls[q].clear();
+  }
+}
+
+template <int NL>
+void launch_hubs(const HubLevel& L, int kind, int n, const Coef3& c, int red, double* u,
+                 const double* f, int* err, cudaStream_t s) {
+  const HubB* const* b = L.blocks[red][kind];
+  const int* nb = L.nblocks[red][kind];
+  launch_blocks<kHub, NL, 1, kRBD, kQW>(b[0], nb[0], n, c, u, f, err, s);
+  launch_blocks<kHub, NL, 2, kRBD, kQW>(b[1], nb[1], n, c, u, f, err, s);
+  launch_blocks<kHub, NL, 4, kRBD, kQW>(b[2], nb[2], n, c, u, f, err, s);
+  launch_blocks<kHub, NL, 8, kRBD, kQW>(b[3], nb[3], n, c, u, f, err, s);
+  launch_blocks<kHub, NL, 16, kRBD, kQW>(b[4], nb[4], n, c, u, f, err, s);
+  launch_blocks<kHub, NL, 32, kRBD, kQW>(b[5], nb[5], n, c, u, f, err, s);
+}
+
+template <int NL>
+cudaError_t allow_hub_smem() {
+  cudaError_t e = allow_smem<kHub, NL, 1, kRBD, kQW>();
+  if (e == cudaSuccess) e = allow_smem<kHub, NL, 2, kRBD, kQW>();
+  if (e == cudaSuccess) e = allow_smem<kHub, NL, 4, kRBD, kQW>();
+  if (e == cudaSuccess) e = allow_smem<kHub, NL, 8, kRBD, kQW>();
+  if (e == cudaSuccess) e = allow_smem<kHub, NL, 16, kRBD, kQW>();
+  if (e == cudaSuccess) e = allow_smem<kHub, NL, 32, kRBD, kQW>();
+  return e;
 }
 
 }  // namespace
@@ -569,6 +684,7 @@ int wire_build_level(int n, WLevel& L, std::string& err, int g0, int g1) {
         const int red = ((s1 + t) % 2) == 0;
         rg[red][cls].push_back(Ring3{(int16_t)a, (int16_t)t, xa});
       }
+  for (int red = 0; red < 2; red++) merge_small_classes(rg[red], kRingClasses, 4, kTE);
   std::vector<int> fr;  // frames (red): shells 1 .. c-1
   for (int r = std::max(1, g0); r < std::min(c, g1); r++) fr.push_back(r);
   // points: the centre (red, group c) and the face centres (group s1)
@@ -592,17 +708,17 @@ int wire_build_level(int n, WLevel& L, std::string& err, int g0, int g1) {
   if (upload(fr, &L.frames, err)) return 3;
   L.nframes = (int)fr.size();
   // dynamic shared memory above 48 KB (per function: sized for the largest n)
-  cudaError_t e = allow_smem<4, 1, ring_bd(1), kRQ>();
-  if (e == cudaSuccess) e = allow_smem<4, 2, ring_bd(2), kRQ>();
-  if (e == cudaSuccess) e = allow_smem<4, 4, ring_bd(4), kRQ>();
-  if (e == cudaSuccess) e = allow_smem<4, 8, ring_bd(8), kRQ>();
-  if (e == cudaSuccess) e = allow_smem<4, 16, ring_bd(16), kRQ>();
-  if (e == cudaSuccess) e = allow_smem<4, 32, ring_bd(32), kRQ>();
-  if (e == cudaSuccess) e = allow_smem<4, 64, ring_bd(64), kRQ>();
-  if (kRQ < 16 && e == cudaSuccess) e = allow_smem<4, 128, ring_bd(128), kRQ>();
-  if (e == cudaSuccess) e = allow_smem<12, 4, 48, kQW>();
-  if (e == cudaSuccess) e = allow_smem<12, 16, 192, kQW>();
-  if (e == cudaSuccess) e = allow_smem<12, 64, 768, kQW>();
+  cudaError_t e = allow_smem<kRing, 4, 1, ring_bd(1), kRQ>();
+  if (e == cudaSuccess) e = allow_smem<kRing, 4, 2, ring_bd(2), kRQ>();
+  if (e == cudaSuccess) e = allow_smem<kRing, 4, 4, ring_bd(4), kRQ>();
+  if (e == cudaSuccess) e = allow_smem<kRing, 4, 8, ring_bd(8), kRQ>();
+  if (e == cudaSuccess) e = allow_smem<kRing, 4, 16, ring_bd(16), kRQ>();
+  if (e == cudaSuccess) e = allow_smem<kRing, 4, 32, ring_bd(32), kRQ>();
+  if (e == cudaSuccess) e = allow_smem<kRing, 4, 64, ring_bd(64), kRQ>();
+  if (kRQ < 16 && e == cudaSuccess) e = allow_smem<kRing, 4, 128, ring_bd(128), kRQ>();
+  if (e == cudaSuccess) e = allow_smem<kFrame, 12, 4, 48, kQW>();
+  if (e == cudaSuccess) e = allow_smem<kFrame, 12, 16, 192, kQW>();
+  if (e == cudaSuccess) e = allow_smem<kFrame, 12, 64, 768, kQW>();
   if (e != cudaSuccess) {
     err = std::string("wireframe kernel shared memory: ") + cudaGetErrorString(e);
     return 3;
@@ -643,8 +759,70 @@ int wire_stage(const WLevel& L, int n, const Coef3& c, int red, double* u, const
   }
   if (L.npoints[red]) {
     TMG_COUNT(1);
-    wpoint_kernel<<<(L.npoints[red] + 127) / 128, 128, 0, s>>>(n, c, L.points[red],
-                                                               L.npoints[red], u, f, err);
+    tmg::launch_pdl(wpoint_kernel, dim3((L.npoints[red] + 127) / 128), dim3(128), 0, s, n, c,
+                    L.points[red], L.npoints[red], u, f, err);
+  }
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : 3;
+}
+
+int hub_build_level(int n, const std::vector<HubB> blocks[2], HubLevel& L, std::string& err) {
+  if (n > kMaxN) {
+    err = "3D tweed cubes above " + std::to_string(kMaxN) + " intervals are not supported";
+    return 2;
+  }
+  for (int red = 0; red < 2; red++) {
+    std::vector<HubB> cls[kHubKinds][kHubClasses];
+    std::vector<int4> pts;
+    for (const HubB& B : blocks[red]) {
+      if (B.len == 0) {  // a branch without legs: a point block
+        pts.push_back(make_int4(B.bi, B.bj, B.bk, 0));
+        continue;
+      }
+      if (B.nleg != 2 && B.nleg != 3 && B.nleg != 6) {
+        err = "3D tweed block with " + std::to_string(B.nleg) + " legs";
+        return 2;
+      }
+      const int kind = B.nleg == 2 ? 0 : 1;
+      int q = 0;
+      while (q < kHubClasses - 1 && kHubTE[q] * kQW < B.len) q++;
+      cls[kind][q].push_back(B);
+    }
+    for (int k = 0; k < kHubKinds; k++) merge_small_classes(cls[k], kHubClasses, kHubLegs[k], kHubTE);
+    for (int k = 0; k < kHubKinds; k++)
+      for (int q = 0; q < kHubClasses; q++) {
+        if (upload(cls[k][q], &L.blocks[red][k][q], err)) return 3;
+        L.nblocks[red][k][q] = (int)cls[k][q].size();
+      }
+    if (upload(pts, &L.points[red], err)) return 3;
+    L.npoints[red] = (int)pts.size();
+  }
+  cudaError_t e = allow_hub_smem<2>();
+  if (e == cudaSuccess) e = allow_hub_smem<6>();
+  if (e != cudaSuccess) {
+    err = std::string("tweed kernel shared memory: ") + cudaGetErrorString(e);
+    return 3;
+  }
+  return 0;
+}
+
+void hub_free_level(HubLevel& L) {
+  for (int red = 0; red < 2; red++) {
+    for (int k = 0; k < kHubKinds; k++)
+      for (int q = 0; q < kHubClasses; q++) cudaFree(L.blocks[red][k][q]);
+    cudaFree(L.points[red]);
+  }
+  L = HubLevel();
+}
+
+int hub_stage(const HubLevel& L, int n, const Coef3& c, int red, double* u, const double* f,
+              int* err, cudaStream_t s) {
+  launch_hubs<2>(L, 0, n, c, red, u, f, err, s);
+  launch_hubs<6>(L, 1, n, c, red, u, f, err, s);
+  if (L.npoints[red]) {
+    TMG_COUNT(1);
+    tmg::launch_pdl(wpoint_kernel, dim3((L.npoints[red] + 127) / 128), dim3(128), 0, s, n, c,
+                    L.points[red], L.npoints[red], u, f, err);
   }
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : 3;
