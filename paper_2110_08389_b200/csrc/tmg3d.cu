@@ -87,43 +87,199 @@ __global__ void __launch_bounds__(256) defect3_kernel(int n, Coef3 c, const doub
   }
 }
 
-// coarse = full weighting of d (tensor product of [1/4, 1/2, 1/4])
-__global__ void __launch_bounds__(256) restrict3_kernel(int nf, const double* __restrict__ d,
-                                                        double* __restrict__ out) {
+// Fused residual + full weighting (mgcycle.py:98-99 in 3D), marching along
+// i: a CTA owns a coarse (J, K) tile of 8 x 32 points and a run of coarse
+// planes; per fine plane it stages the u plane in a three-plane shared ring
+// buffer (rows along k, coalesced), computes the fine defects of its tile
+// (defect3_kernel's arithmetic) into shared memory and folds them into the
+// coarse points in the oracle's order (orc3_restrict: a, b, e nested), while
+// u and f are read once (16 B per fine point, no defect field in HBM).
+constexpr int kRTJ = 8, kRTK = 32;                          // coarse tile
+constexpr int kRDJ = 2 * kRTJ + 1, kRDK = 2 * kRTK + 1;     // fine defects
+constexpr int kRUJ = kRDJ + 2, kRUK = kRDK + 2;             // u with halo
+
+// 8-byte asynchronous global -> shared copy; src_bytes = 0 zero-fills
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
+               "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+constexpr int kRU = kRUJ * kRUK, kRD = kRDJ * kRDK;
+constexpr size_t kRestrictSmem3 = (4 * kRU + 3 * kRD + 2 * kRDJ + 2 * kRDK) * sizeof(double);
+
+// Coarse planes [I0, I0 + ti) per CTA.  u planes stream through a 4-slot
+// shared ring and f planes through 2 slots by cp.async, two fine planes
+// ahead of the defect computation, so HBM latency overlaps the stencil.
+__global__ void __launch_bounds__(256, 3) defect_restrict3_kernel(int nf, Coef3 c,
+                                                                  const double* __restrict__ u,
+                                                                  const double* __restrict__ f,
+                                                                  double* __restrict__ out,
+                                                                  int ti) {
+  extern __shared__ double rsm[];
+  double* su = rsm;              // 4 x kRU
+  double* sf = su + 4 * kRU;     // 2 x kRD
+  double* sd = sf + 2 * kRD;     // kRD defects
+  double* cS = sd + kRD;         // S, N along the tile's rows; B, T along its columns
+  double* cN = cS + kRDJ;
+  double* cB = cN + kRDJ;
+  double* cT = cB + kRDK;
   pdl_trigger();
-  pdl_wait();
   const int nc = nf / 2;
-  const int K = blockIdx.x * blockDim.x + threadIdx.x;
-  const int J = blockIdx.y, I = blockIdx.z;
-  if (K > nc) return;
-  double acc = 0.0;
-  if (I > 0 && J > 0 && K > 0 && I < nc && J < nc && K < nc) {
-    const double w[3] = {0.25, 0.5, 0.25};
-    for (int a = 0; a < 3; a++)
-      for (int b = 0; b < 3; b++)
-        for (int e = 0; e < 3; e++)
-          acc += w[a] * w[b] * w[e] * d[idx3(nf, 2 * I - 1 + a, 2 * J - 1 + b, 2 * K - 1 + e)];
+  const int J0 = 1 + blockIdx.y * kRTJ, K0 = 1 + blockIdx.x * kRTK;
+  const int I0 = 1 + blockIdx.z * ti, I1 = min(I0 + ti, nc);
+  const int jd0 = 2 * J0 - 1, kd0 = 2 * K0 - 1;  // fine origin of the defect tile
+  const int tid = threadIdx.x;
+  const size_t n1 = (size_t)nf + 1;
+  for (int t = tid; t < kRDJ; t += 256) {
+    const int j = min(jd0 + t, nf);
+    cS[t] = __ldg(c.S + j);
+    cN[t] = __ldg(c.N + j);
   }
-  out[idx3(nc, I, J, K)] = acc;
+  for (int t = tid; t < kRDK; t += 256) {
+    const int k = min(kd0 + t, nf);
+    cB[t] = __ldg(c.B + k);
+    cT[t] = __ldg(c.T + k);
+  }
+  // per-thread element offsets within a plane (fixed for every plane): u
+  // tile elements t = tid + 256 m, f / defect elements likewise; -1 = outside
+  constexpr int PU = (kRU + 255) / 256, PD = (kRD + 255) / 256;
+  int uo[PU], fo[PD], so[PD];
+#pragma unroll
+  for (int m = 0; m < PU; m++) {
+    const int t = tid + 256 * m, r = t / kRUK, q = t - r * kRUK;
+    const int j = jd0 - 1 + r, k = kd0 - 1 + q;
+    uo[m] = (t < kRU && j <= nf && k <= nf) ? j * (nf + 1) + k : -1;
+  }
+#pragma unroll
+  for (int m = 0; m < PD; m++) {
+    const int t = tid + 256 * m, r = t / kRDK, q = t - r * kRDK;
+    const int j = jd0 + r, k = kd0 + q;
+    const bool in = t < kRD && j < nf && k < nf;
+    fo[m] = in ? j * (nf + 1) + k : -1;
+    so[m] = t < kRD ? (r + 1) * kRUK + (q + 1) : 0;
+  }
+  const size_t plane = n1 * n1;
+  auto issue_u = [&](int i) {  // plane i (0 .. nf) into slot i % 4
+    double* dst = su + (i & 3) * kRU;
+    const double* base = u + (size_t)i * plane;
+    const bool pin = i <= nf;
+#pragma unroll
+    for (int m = 0; m < PU; m++) {
+      const int t = tid + 256 * m;
+      if (t < kRU) {
+        const bool ok = pin && uo[m] >= 0;
+        cp_async8(dst + t, ok ? base + uo[m] : u, ok);
+      }
+    }
+  };
+  auto issue_f = [&](int i) {  // plane i into slot i % 2
+    double* dst = sf + (i & 1) * kRD;
+    const double* base = f + (size_t)i * plane;
+    const bool pin = i < nf;
+#pragma unroll
+    for (int m = 0; m < PD; m++) {
+      const int t = tid + 256 * m;
+      if (t < kRD) {
+        const bool ok = pin && fo[m] >= 0;
+        cp_async8(dst + t, ok ? base + fo[m] : f, ok);
+      }
+    }
+  };
+  pdl_wait();
+  issue_u(2 * I0 - 2);
+  issue_u(2 * I0 - 1);
+  issue_u(2 * I0);
+  issue_f(2 * I0 - 1);
+  cp_async_commit();
+  issue_u(2 * I0 + 1);
+  issue_f(2 * I0);
+  cp_async_commit();
+  const int tj = tid / kRTK, tk = tid % kRTK, J = J0 + tj, K = K0 + tk;
+  const bool own = J < nc && K < nc;
+  double acc = 0.0;
+  for (int i = 2 * I0 - 1; i <= 2 * I1 - 1; i++) {
+    cp_async_wait1();  // u planes up to i + 1 and f plane i have landed
+    __syncthreads();
+    const double* um = su + ((i - 1) & 3) * kRU;
+    const double* uc = su + (i & 3) * kRU;
+    const double* up = su + ((i + 1) & 3) * kRU;
+    const double* fc = sf + (i & 1) * kRD;
+    const double Wi = __ldg(c.W + i), Ei = __ldg(c.E + i);
+#pragma unroll
+    for (int m = 0; m < PD; m++) {
+      const int t = tid + 256 * m;
+      if (t >= kRD) continue;
+      double v = 0.0;
+      if (fo[m] >= 0) {
+        const int o = so[m], r = o / kRUK - 1, q = o - (r + 1) * kRUK - 1;
+        const double Sj = cS[r], Nj = cN[r], Bk = cB[q], Tk = cT[q];
+        const double cc = -(Wi + Ei + Sj + Nj + Bk + Tk);
+        double a = __dmul_rn(Wi, um[o]);
+        a = __dadd_rn(a, __dmul_rn(Ei, up[o]));
+        a = __dadd_rn(a, __dmul_rn(Sj, uc[o - kRUK]));
+        a = __dadd_rn(a, __dmul_rn(Nj, uc[o + kRUK]));
+        a = __dadd_rn(a, __dmul_rn(Bk, uc[o - 1]));
+        a = __dadd_rn(a, __dmul_rn(Tk, uc[o + 1]));
+        a = __dadd_rn(a, __dmul_rn(cc, uc[o]));
+        v = __dadd_rn(fc[t], -a);
+      }
+      sd[t] = v;
+    }
+    __syncthreads();  // defects complete; u plane i-1 and f plane i are free
+    if (i + 3 <= 2 * I1) issue_u(i + 3);
+    if (i + 2 <= 2 * I1 - 1) issue_f(i + 2);
+    cp_async_commit();  // (possibly empty) keeps the group count per plane fixed
+    // plane i is a = 2 of coarse plane (i - 1) / 2 and a = 0 of (i + 1) / 2
+    // (odd i), or a = 1 of i / 2 (even i)
+    const int a_lo = (i & 1) ? 2 : 1, I_lo = (i & 1) ? (i - 1) / 2 : i / 2;
+    for (int pass = 0; pass < ((i & 1) ? 2 : 1); pass++) {
+      const int a = pass == 0 ? a_lo : 0, I = pass == 0 ? I_lo : (i + 1) / 2;
+      if (I < I0 || I >= I1) continue;
+      if (a == 0) acc = 0.0;
+      if (own) {
+        const double wa = a == 1 ? 0.5 : 0.25;
+#pragma unroll
+        for (int b = 0; b < 3; b++)
+#pragma unroll
+          for (int e = 0; e < 3; e++)
+            acc += wa * (b == 1 ? 0.5 : 0.25) * (e == 1 ? 0.5 : 0.25) *
+                   sd[(2 * tj + b) * kRDK + 2 * tk + e];
+      }
+      if (a == 2 && own) out[((size_t)I * (nc + 1) + J) * (nc + 1) + K] = acc;
+    }
+  }
 }
 
-// u += trilinear P uc on the fine interior
-__global__ void __launch_bounds__(256) prolong3_kernel(int nc, const double* __restrict__ uc,
-                                                       double* __restrict__ u) {
+// u += trilinear P uc on the fine interior: a thread per fine (i, j) and
+// coarse column K, writing fine k = 2K-1 and 2K; sums in orc3_prolong_add's
+// order (a, b, e nested), consecutive lanes on consecutive fine k pairs
+__global__ void __launch_bounds__(256) prolong3v2_kernel(int nc, const double* __restrict__ uc,
+                                                         double* __restrict__ u) {
   pdl_trigger();
   pdl_wait();
   const int nf = 2 * nc;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y, i = blockIdx.z;
-  if (k <= 0 || k >= nf || j <= 0 || j >= nf || i <= 0 || i >= nf) return;
-  const int I = i / 2, J = j / 2, K = k / 2;
-  const int oi = i & 1, oj = j & 1, ok = k & 1;
-  double acc = 0.0;
+  const int K = 1 + blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = 1 + blockIdx.y, i = 1 + blockIdx.z;
+  if (K > nc) return;
+  const int I = i / 2, J = j / 2, oi = i & 1, oj = j & 1;
+  const size_t c1 = (size_t)nc + 1;
+  double ao = 0.0, ae = 0.0;
   for (int a = 0; a <= oi; a++)
-    for (int b = 0; b <= oj; b++)
-      for (int e = 0; e <= ok; e++) acc += uc[idx3(nc, I + a, J + b, K + e)];
-  const double wgt = 1.0 / (double)((1 + oi) * (1 + oj) * (1 + ok));
-  u[idx3(nf, i, j, k)] += acc * wgt;
+    for (int b = 0; b <= oj; b++) {
+      const size_t o = ((size_t)(I + a) * c1 + (J + b)) * c1;
+      const double v0 = __ldg(uc + o + K - 1), v1 = __ldg(uc + o + K);
+      ao += v0;
+      ao += v1;
+      ae += v1;
+    }
+  const double wo = 1.0 / (double)((1 + oi) * (1 + oj) * 2), we = 1.0 / (double)((1 + oi) * (1 + oj));
+  const size_t of = ((size_t)i * (nf + 1) + j) * (nf + 1);
+  u[of + 2 * K - 1] += ao * wo;
+  if (2 * K < nf) u[of + 2 * K] += ae * we;
 }
 
 __global__ void coarse3_kernel(Coef3 c, double* u, const double* f) {
@@ -176,7 +332,6 @@ struct tmg_cube {
   std::vector<double*> coef;          // per level: W E S N B T (6 (n+1))
   std::vector<int> nblocks[2];        // per level: black, red 3D tweed block counts
   std::vector<double*> U, F;          // per level work fields (level 0: session)
-  double* d = nullptr;                // finest-size defect scratch
   int* err = nullptr;
   unsigned long long* dmax = nullptr;
   int* h_err = nullptr;
@@ -245,6 +400,19 @@ int sweep3(tmg_cube* h, int l, double* u, const double* f, cudaStream_t s) {
 }
 
 dim3 grid3(int n) { return dim3((n + 1 + 255) / 256, n + 1, n + 1); }
+// coarse planes per CTA: enough CTAs for ~4 waves of 148 SMs x 4
+int restrict_ti(int nf) {
+  const int m = nf / 2 - 1;
+  const long tiles = (long)((m + kRTK - 1) / kRTK) * ((m + kRTJ - 1) / kRTJ);
+  int ti = 16;
+  while (ti > 1 && tiles * ((m + ti - 1) / ti) < 4L * 148 * 4) ti /= 2;
+  return ti;
+}
+dim3 grid_restrict(int nf) {
+  const int m = nf / 2 - 1, ti = restrict_ti(nf);  // interior coarse points per axis
+  return dim3((m + kRTK - 1) / kRTK, (m + kRTJ - 1) / kRTJ, (m + ti - 1) / ti);
+}
+dim3 grid_prolong(int nc) { return dim3((nc + 255) / 256, 2 * nc - 1, 2 * nc - 1); }
 
 int cycle3(tmg_cube* h, int nu1, int nu2, cudaStream_t s, int l0 = 0) {
   const int L = (int)h->n.size();
@@ -253,11 +421,10 @@ int cycle3(tmg_cube* h, int nu1, int nu2, cudaStream_t s, int l0 = 0) {
       int st = sweep3(h, l, h->U[l], h->F[l], s);
       if (st) return st;
     }
-    TMG_COUNT(3);
-    T3(launch_pdl(defect3_kernel, grid3(h->n[l]), dim3(256), 0, s, h->n[l], coefs(h, l), h->U[l],
-                  h->F[l], h->d, (unsigned long long*)nullptr, 0, 0, 1 << 30));
-    T3(launch_pdl(restrict3_kernel, grid3(h->n[l + 1]), dim3(256), 0, s, h->n[l], h->d,
-                  h->F[l + 1]));
+    TMG_COUNT(2);
+    T3(launch_pdl(defect_restrict3_kernel, grid_restrict(h->n[l]), dim3(256), kRestrictSmem3, s,
+                  h->n[l],
+                  coefs(h, l), h->U[l], h->F[l], h->F[l + 1], restrict_ti(h->n[l])));
     const size_t nc = (size_t)(h->n[l + 1] + 1) * (h->n[l + 1] + 1) * (h->n[l + 1] + 1);
     T3(launch_pdl(zero3_kernel, dim3((unsigned)std::min<size_t>((nc + 255) / 256, 148 * 16)),
                   dim3(256), 0, s, h->U[l + 1], nc));
@@ -266,8 +433,8 @@ int cycle3(tmg_cube* h, int nu1, int nu2, cudaStream_t s, int l0 = 0) {
   T3(launch_pdl(coarse3_kernel, dim3(1), dim3(1), 0, s, coefs(h, L - 1), h->U[L - 1], h->F[L - 1]));
   for (int l = L - 2; l >= l0; l--) {
     TMG_COUNT(1);
-    T3(launch_pdl(prolong3_kernel, grid3(h->n[l]), dim3(256), 0, s, h->n[l + 1], h->U[l + 1],
-                  h->U[l]));
+    T3(launch_pdl(prolong3v2_kernel, grid_prolong(h->n[l + 1]), dim3(256), 0, s, h->n[l + 1],
+                  h->U[l + 1], h->U[l]));
     for (int k = 0; k < nu2; k++) {
       int st = sweep3(h, l, h->U[l], h->F[l], s);
       if (st) return st;
@@ -292,6 +459,8 @@ int tmg_cube_create(int n, const double* x, tmg_cube** out) {
 int tmg_cube_create_scheme(int n, const double* x, int scheme, tmg_cube** out) {
   if (!out || !x || n < 2 || n % 2) return fail3(TMG_BADARG, "cube needs even n >= 2");
   if (scheme != 0 && scheme != 1) return fail3(TMG_BADARG, "cube scheme must be 0 (tweed) or 1 (wireframe)");
+  T3(cudaFuncSetAttribute(defect_restrict3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)kRestrictSmem3));
   tmg_cube* h = new tmg_cube();
   h->scheme = scheme;
   std::vector<double> xs(x, x + n + 1);
@@ -349,7 +518,6 @@ int tmg_cube_create_scheme(int n, const double* x, int scheme, tmg_cube** out) {
     xs.swap(c);
   }
   const size_t tot = (size_t)(n + 1) * (n + 1) * (n + 1);
-  T3(cudaMalloc(&h->d, tot * sizeof(double)));
   T3(cudaMalloc(&h->err, sizeof(int) + sizeof(unsigned long long) * 2));
   h->dmax = reinterpret_cast<unsigned long long*>(h->err + 2);
   T3(cudaMemset(h->err, 0, sizeof(int)));
@@ -368,7 +536,6 @@ int tmg_cube_destroy(tmg_cube* h) {
   for (auto& w : h->hl) tmg3::hub_free_level(w);
   for (double* p : h->U) cudaFree(p);
   for (double* p : h->F) cudaFree(p);
-  cudaFree(h->d);
   cudaFree(h->err);
   cudaFreeHost(h->h_err);
   delete h;
@@ -598,10 +765,10 @@ int tmg_cube_restrict(tmg_cube* h, int level, void* stream) {
   int st = cube_session_level(h, level, 1);
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  TMG_COUNT(2);
-  defect3_kernel<<<grid3(h->n[level]), 256, 0, s>>>(h->n[level], coefs(h, level), h->U[level],
-                                                     h->F[level], h->d, nullptr);
-  restrict3_kernel<<<grid3(h->n[level + 1]), 256, 0, s>>>(h->n[level], h->d, h->F[level + 1]);
+  TMG_COUNT(1);
+  defect_restrict3_kernel<<<grid_restrict(h->n[level]), 256, kRestrictSmem3, s>>>(
+      h->n[level], coefs(h, level), h->U[level], h->F[level], h->F[level + 1],
+      restrict_ti(h->n[level]));
   const size_t nc = (size_t)(h->n[level + 1] + 1) * (h->n[level + 1] + 1) * (h->n[level + 1] + 1);
   T3(cudaMemsetAsync(h->U[level + 1], 0, nc * sizeof(double), s));
   return cuda3(cudaGetLastError(), "cube restrict");
@@ -612,7 +779,7 @@ int tmg_cube_prolong(tmg_cube* h, int level, void* stream) {
   int st = cube_session_level(h, level, 1);
   if (st) return st;
   TMG_COUNT(1);
-  prolong3_kernel<<<grid3(h->n[level]), 256, 0, (cudaStream_t)stream>>>(
+  prolong3v2_kernel<<<grid_prolong(h->n[level + 1]), 256, 0, (cudaStream_t)stream>>>(
       h->n[level + 1], h->U[level + 1], h->U[level]);
   return cuda3(cudaGetLastError(), "cube prolong");
 }

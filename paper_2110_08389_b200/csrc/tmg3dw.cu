@@ -39,6 +39,9 @@
 namespace tmg3 {
 namespace {
 
+#ifndef TMG_WNB
+#define TMG_WNB 4
+#endif
 #ifndef TMG_WQ
 #define TMG_WQ 16
 #endif
@@ -316,7 +319,7 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
   tmg::pdl_wait();  // the previous kernel's fields are complete from here on
   // 1. gather: edge points (four transverse neighbours), and the corner rows
   {
-    constexpr int NB = 4;  // points whose loads are in flight together
+    constexpr int NB = TMG_WNB;  // points whose loads are in flight together
 #pragma unroll 1
     for (int i0 = 0; i0 < Q; i0 += NB) {
       if (lt + i0 * TE >= L) break;
