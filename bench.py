@@ -744,7 +744,7 @@ def run_cube(args):
                      "traffic": None,
                      "kernel": ("wblock_kernel rings + frames, wpoint_kernel (one finest-level 3D "
                                 "wireframe sweep)" if scheme == "wireframe" else
-                                "legs/branch kernels (one finest-level 3D tweed sweep)"),
+                                "wblock_kernel hub blocks + wpoint_kernel (one finest-level 3D tweed sweep)"),
                      "alg_bytes": alg, "ms": sweep_ms, "peak_kind": peak_kind},
         "solve": solve,
         "convergence": {"cycles": len(ratios), "ratios": ratios,
