@@ -263,9 +263,13 @@ __device__ __forceinline__ void chunk_finalise(double* rr, int p0, int e, double
   rr[rsw<Q>(p0 + e)] = XE;
 }
 
-// threads of a CTA: whole blocks of NE * TE threads, at most BDMAX
+// blocks of NE * TE threads per CTA (at most BDMAX threads), and the CTA
+// size rounded up to whole warps (the extra threads idle: the PCR shuffles
+// need full warps)
 template <int NE, int TE, int BDMAX>
-constexpr int wblock_bd() { return (BDMAX / (NE * TE)) * NE * TE; }
+constexpr int wblock_bpc() { return BDMAX / (NE * TE); }
+template <int NE, int TE, int BDMAX>
+constexpr int wblock_bd() { return (wblock_bpc<NE, TE, BDMAX>() * NE * TE + 31) / 32 * 32; }
 
 template <int NE, int TE, int BDMAX, int Q>
 constexpr size_t wblock_smem() {
@@ -282,7 +286,7 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
   constexpr int NK = ncorners<KIND, NE>();
   constexpr int SL = NE * TE;  // threads per block
   constexpr int BD = wblock_bd<NE, TE, BDMAX>();
-  constexpr int BPC = BD / SL;
+  constexpr int BPC = wblock_bpc<NE, TE, BDMAX>();
   static_assert(BPC >= 1 && (SL >= NK || KIND == kHub), "block slice");
   extern __shared__ double wsm[];
   double* sR = wsm;  // BD * Q
@@ -293,7 +297,7 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
   __shared__ double sKr[BPC][NK], sKd[BPC][NK], sXc[BPC][NK];
   const int tid = threadIdx.x, g = tid / SL, ed = (tid % SL) / TE, lt = tid % TE;
   const int bid = blockIdx.x * BPC + g;
-  const bool live = bid < nb;
+  const bool live = g < BPC && bid < nb;  // threads past BPC blocks only fill the last warp
   WBlk B;
   B.a = 0; B.xa = 0; B.t = 1; B.p[0] = B.p[1] = B.p[2] = 1; B.codes = 0; B.nleg = NE;
   if (KIND == kRing) {
@@ -408,22 +412,37 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
       A = 0.0;
     }
   }
-  __syncthreads();
-  sA[tid] = A; sB[tid] = Bv; sC[tid] = Cc; sD[tid] = D; sH0[tid] = H0; sH1[tid] = H1;
-  __syncthreads();
+  // PCR over the edge's TE chunk ends: steps within a warp by shuffles
+  // (an edge of TE <= 32 threads is one aligned lane segment), the step
+  // across the two warps of a 64-thread edge through shared memory
+  constexpr int WS = TE < 32 ? TE : 32;
+  constexpr unsigned FULL = 0xffffffffu;
 #pragma unroll
   for (int dd = 1; dd < TE; dd <<= 1) {
     double Am = 0, Bm = 1, Cm = 0, Dm = 0, Gm = 0, Hm = 0, Ap = 0, Bp = 1, Cp = 0, Dp = 0, Gp = 0,
            Hp = 0;
-    if (lt - dd >= 0) {
-      Am = sA[tid - dd]; Bm = sB[tid - dd]; Cm = sC[tid - dd]; Dm = sD[tid - dd];
-      Gm = sH0[tid - dd]; Hm = sH1[tid - dd];
+    if (dd < 32) {
+      const double a1 = __shfl_up_sync(FULL, A, dd, WS), b1 = __shfl_up_sync(FULL, Bv, dd, WS);
+      const double c1 = __shfl_up_sync(FULL, Cc, dd, WS), d1 = __shfl_up_sync(FULL, D, dd, WS);
+      const double g1 = __shfl_up_sync(FULL, H0, dd, WS), h1 = __shfl_up_sync(FULL, H1, dd, WS);
+      const double a2 = __shfl_down_sync(FULL, A, dd, WS), b2 = __shfl_down_sync(FULL, Bv, dd, WS);
+      const double c2 = __shfl_down_sync(FULL, Cc, dd, WS), d2 = __shfl_down_sync(FULL, D, dd, WS);
+      const double g2 = __shfl_down_sync(FULL, H0, dd, WS), h2 = __shfl_down_sync(FULL, H1, dd, WS);
+      if (lt - dd >= 0) { Am = a1; Bm = b1; Cm = c1; Dm = d1; Gm = g1; Hm = h1; }
+      if (lt + dd < TE) { Ap = a2; Bp = b2; Cp = c2; Dp = d2; Gp = g2; Hp = h2; }
+    } else {
+      __syncthreads();  // the previous phase's readers of the row arrays are done
+      sA[tid] = A; sB[tid] = Bv; sC[tid] = Cc; sD[tid] = D; sH0[tid] = H0; sH1[tid] = H1;
+      __syncthreads();
+      if (lt - dd >= 0) {
+        Am = sA[tid - dd]; Bm = sB[tid - dd]; Cm = sC[tid - dd]; Dm = sD[tid - dd];
+        Gm = sH0[tid - dd]; Hm = sH1[tid - dd];
+      }
+      if (lt + dd < TE) {
+        Ap = sA[tid + dd]; Bp = sB[tid + dd]; Cp = sC[tid + dd]; Dp = sD[tid + dd];
+        Gp = sH0[tid + dd]; Hp = sH1[tid + dd];
+      }
     }
-    if (lt + dd < TE) {
-      Ap = sA[tid + dd]; Bp = sB[tid + dd]; Cp = sC[tid + dd]; Dp = sD[tid + dd];
-      Gp = sH0[tid + dd]; Hp = sH1[tid + dd];
-    }
-    __syncthreads();
     const double k1 = A * rcp3(Bm), k2 = Cc * rcp3(Bp);
     A = -k1 * Am;
     Cc = -k2 * Cp;
@@ -431,9 +450,8 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
     D = D - k1 * Dm - k2 * Dp;
     H0 = H0 - k1 * Gm - k2 * Gp;
     H1 = H1 - k1 * Hm - k2 * Hp;
-    sA[tid] = A; sB[tid] = Bv; sC[tid] = Cc; sD[tid] = D; sH0[tid] = H0; sH1[tid] = H1;
-    __syncthreads();
   }
+  __syncthreads();  // every read of the row arrays is done before they are reused
   bad |= cnt > 0 && wbad(Bv);
   const double iB = rcp3(Bv);
   const double P = D * iB, Q0 = H0 * iB, Q1 = H1 * iB;  // X_end = P - Q0 x_K0 - Q1 x_K1
@@ -480,7 +498,54 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
     bad |= wbad(m);
     sXc[g][0] = rhs / m;
   }
-  if (KIND != kHub && live && tid % SL == 0) {
+  if (KIND == kRing && live && tid % SL == 0) {
+    // 4 x 4 corner system in registers (static indices): the Schur
+    // complement of the diagonally dominant ring, eliminated without pivoting
+    double M[4][5];
+#pragma unroll
+    for (int K = 0; K < 4; K++) {
+#pragma unroll
+      for (int q = 0; q < 4; q++) M[K][q] = 0.0;
+      M[K][K] = sKd[g][K];
+      M[K][4] = sKr[g][K];
+    }
+#pragma unroll
+    for (int eg = 0; eg < 4; eg++) {
+      const int K0 = eg == 0 ? 0 : (eg == 1 ? 1 : (eg == 2 ? 3 : 0));
+      const int K1 = eg == 0 ? 1 : (eg == 1 ? 2 : (eg == 2 ? 2 : 3));
+      const int x0 = (K0 == 1 || K0 == 2) ? n - B.t : B.t;  // corner coordinates along the edge
+      const int x1 = (eg & 1) ? ((K1 >= 2) ? n - B.t : B.t) : ((K1 == 1 || K1 == 2) ? n - B.t : B.t);
+      const int y0 = (eg & 1) ? ((K0 >= 2) ? n - B.t : B.t) : x0;
+      const double c0 = __ldg(c.E + y0), c1 = __ldg(c.W + x1);
+      M[K0][K0] += c0 * sEnd[g][eg][1];
+      M[K0][K1] += c0 * sEnd[g][eg][2];
+      M[K0][4] -= c0 * sEnd[g][eg][0];
+      M[K1][K0] += c1 * sEnd[g][eg][4];
+      M[K1][K1] += c1 * sEnd[g][eg][5];
+      M[K1][4] -= c1 * sEnd[g][eg][3];
+    }
+#pragma unroll
+    for (int col = 0; col < 4; col++) {
+      bad |= wbad(M[col][col]);
+      const double iv = 1.0 / M[col][col];
+#pragma unroll
+      for (int q = col + 1; q < 4; q++) {
+        const double w = M[q][col] * iv;
+#pragma unroll
+        for (int v = col; v <= 4; v++) M[q][v] -= w * M[col][v];
+      }
+    }
+    double xr[4];
+#pragma unroll
+    for (int q = 3; q >= 0; q--) {
+      double sum = M[q][4];
+#pragma unroll
+      for (int v = q + 1; v < 4; v++) sum -= M[q][v] * xr[v];
+      xr[q] = sum / M[q][q];
+      sXc[g][q] = xr[q];
+    }
+  }
+  if (KIND == kFrame && live && tid % SL == 0) {
     double M[NK][NK + 1];
     for (int K = 0; K < NK; K++) {
       for (int q = 0; q < NK; q++) M[K][q] = 0.0;
@@ -598,7 +663,7 @@ template <int KIND, int NE, int TE, int BDMAX, int Q>
 void launch_blocks(const void* blocks, int nb, int n, const Coef3& c, double* u, const double* f,
                    int* err, cudaStream_t s) {
   if (!nb) return;
-  constexpr int BD = wblock_bd<NE, TE, BDMAX>(), BPC = BD / (NE * TE);
+  constexpr int BD = wblock_bd<NE, TE, BDMAX>(), BPC = wblock_bpc<NE, TE, BDMAX>();
   TMG_COUNT(1);
   tmg::launch_pdl(wblock_kernel<KIND, NE, TE, BDMAX, Q>, dim3((nb + BPC - 1) / BPC), dim3(BD),
                   wblock_smem<NE, TE, BDMAX, Q>(), s, n, c, blocks, nb, u, f, err);
