@@ -218,6 +218,9 @@ int tmg_cube_load(tmg_cube* h, const double* u, const double* f, void* stream);
 int tmg_cube_cycles(tmg_cube* h, int nu1, int nu2, int reps, void* stream);
 int tmg_cube_norm(tmg_cube* h, double* out_host, void* stream);
 int tmg_cube_store(tmg_cube* h, double* u, void* stream);
+/* `reps` finest-level sweeps on the session (the smoother alone, on the
+ * layout the V-cycle uses: i- / j-contiguous views for the 3D wireframe) */
+int tmg_cube_sweeps(tmg_cube* h, int reps, void* stream);
 
 /* ---- sharded cube V-cycle (BASELINE config 5 across GPUs).
  *      Sharding groups 1 .. n/2: 3D wireframe min(i',j',k') (a shell: its

@@ -79,6 +79,7 @@ def _declare(L):
         "tmg_cube_cycles": ([vp, ip, ip, ip, vp], ip),
         "tmg_cube_norm": ([vp, pd, vp], ip),
         "tmg_cube_store": ([vp, vp, vp], ip),
+        "tmg_cube_sweeps": ([vp, ip, vp], ip),
         "tmg_cube_group_count": ([ip, ip], ip),
         "tmg_cube_group_sizes": ([ip, ip, vp, lp], lp),
         "tmg_cube_group_offsets": ([ip, ip, ip, ip, vp, lp], lp),

@@ -282,6 +282,78 @@ __global__ void __launch_bounds__(256) prolong3v2_kernel(int nc, const double* _
   if (2 * K < nf) u[of + 2 * K] += ae * we;
 }
 
+// ---- hybrid layout of the 3D wireframe V-cycle ------------
+// View V (0: i-contiguous [j][k][i], 1: j-contiguous [i][k][j]) owns the
+// points whose strictly largest mirrored coordinate is on axis V; ties and
+// the boundary live in every view; the natural array is view 2.  A tile of
+// 32 (axis V) x 32 (k) points at a fixed third index moves through shared
+// memory so that both sides are read and written along a contiguous axis;
+// CTAs walk (k tile, fixed index) fastest and the axis-V tile slowest, so a
+// wave touches 32 planes of the natural array (TLB reach, DRAM rows).
+__device__ __forceinline__ int owner_h(int n, int i, int j, int k) {
+  if (i <= 0 || j <= 0 || k <= 0 || i >= n || j >= n || k >= n) return -1;
+  const int a = (int)mirror(i, n), b = (int)mirror(j, n), c = (int)mirror(k, n);
+  return (a > b && a > c) ? 0 : ((b > a && b > c) ? 1 : ((c > a && c > b) ? 2 : -1));
+}
+
+// TO_VIEW: natural -> view V for the points `mask` selects (1, u: every
+// point whose mirrored axis-V coordinate is not below the other two -- the
+// owned points, the ties and boundary points next to them, all a view-V edge
+// reads; 2, f: the owned points); else view V -> natural for the owned
+// points.  Tiles without such points are skipped (a view covers ~1/3 of the
+// cube).
+template <int V, bool TO_VIEW>
+__global__ void __launch_bounds__(256) hybrid_kernel(int n, double* __restrict__ nat,
+                                                     double* __restrict__ view, int mask) {
+  __shared__ double t[32][33];
+  pdl_trigger();
+  const int kt = blockIdx.x * 32, fx = blockIdx.y, at = blockIdx.z * 32;  // fx: j (V = 0) or i (V = 1)
+  const size_t n1 = (size_t)n + 1;
+  const int lane = threadIdx.x & 31, row = threadIdx.x >> 5;
+  // tile test: the largest mirrored axis-V coordinate of the tile against
+  // the fixed index's and the smallest k's
+  const int a1 = min(at + 31, n), k1 = min(kt + 31, n);
+  const int ma = (at <= n / 2 && n / 2 <= a1) ? n / 2 : max((int)mirror(at, n), (int)mirror(a1, n));
+  const int mk = min((int)mirror(kt, n), (int)mirror(k1, n));
+  const int mf = (int)mirror(fx, n);
+  const bool strict = !(TO_VIEW && mask == 1);
+  if (strict ? (ma <= mf || ma <= mk) : (ma < mf || ma < mk)) return;
+  pdl_wait();
+  auto nat_off = [&](int a, int k) {
+    return V == 0 ? ((size_t)a * n1 + fx) * n1 + k : ((size_t)fx * n1 + a) * n1 + k;
+  };
+  auto view_off = [&](int a, int k) { return ((size_t)fx * n1 + k) * n1 + a; };
+  auto sel = [&](int a, int k) {
+    const int i = V == 0 ? a : fx, j = V == 0 ? fx : a;
+    if (!strict) {
+      const int mv = (int)mirror(a, n), mo = max((int)mirror(fx, n), (int)mirror(k, n));
+      return mv >= mo;
+    }
+    return owner_h(n, i, j, k) == V;
+  };
+  if (TO_VIEW) {
+    for (int r = row; r < 32; r += 8) {
+      const int a = at + r, k = kt + lane;
+      if (a <= n && k <= n) t[r][lane] = nat[nat_off(a, k)];
+    }
+    __syncthreads();
+    for (int r = row; r < 32; r += 8) {
+      const int k = kt + r, a = at + lane;
+      if (a <= n && k <= n && sel(a, k)) view[view_off(a, k)] = t[lane][r];
+    }
+  } else {
+    for (int r = row; r < 32; r += 8) {
+      const int k = kt + r, a = at + lane;
+      if (a <= n && k <= n) t[lane][r] = view[view_off(a, k)];
+    }
+    __syncthreads();
+    for (int r = row; r < 32; r += 8) {
+      const int a = at + r, k = kt + lane;
+      if (a <= n && k <= n && sel(a, k)) nat[nat_off(a, k)] = t[r][lane];
+    }
+  }
+}
+
 __global__ void coarse3_kernel(Coef3 c, double* u, const double* f) {
   pdl_trigger();
   pdl_wait();
@@ -332,6 +404,10 @@ struct tmg_cube {
   std::vector<double*> coef;          // per level: W E S N B T (6 (n+1))
   std::vector<int> nblocks[2];        // per level: black, red 3D tweed block counts
   std::vector<double*> U, F;          // per level work fields (level 0: session)
+  // 3D wireframe hybrid views (i- and j-contiguous copies) of the levels with
+  // n >= hyb_min; null elsewhere
+  std::vector<double*> UI, UJ, FI, FJ;
+  int hyb_min = 256;
   int* err = nullptr;
   unsigned long long* dmax = nullptr;
   int* h_err = nullptr;
@@ -385,11 +461,37 @@ Coef3 coefs(const tmg_cube* h, int l) {
   return Coef3{p, p + n1, p + 2 * n1, p + 3 * n1, p + 4 * n1, p + 5 * n1};
 }
 
-int sweep3(tmg_cube* h, int l, double* u, const double* f, cudaStream_t s) {
+bool hyb(const tmg_cube* h, int l) { return h->scheme == 1 && l < (int)h->UI.size() && h->UI[l]; }
+
+// hybrid <-> natural for level l: which = 0 u, 1 f
+int convert3(tmg_cube* h, int l, int which, bool to_view, cudaStream_t s) {
+  const int n = h->n[l];
+  const dim3 grid((n + 32) / 32, n + 1, (n + 32) / 32);
+  double* nat = which ? h->F[l] : h->U[l];
+  double* v0 = which ? h->FI[l] : h->UI[l];
+  double* v1 = which ? h->FJ[l] : h->UJ[l];
+  const int mask = which ? 2 : 1;
+  TMG_COUNT(2);
+  if (to_view) {
+    T3(launch_pdl(hybrid_kernel<0, true>, grid, dim3(256), 0, s, n, nat, v0, mask));
+    T3(launch_pdl(hybrid_kernel<1, true>, grid, dim3(256), 0, s, n, nat, v1, mask));
+  } else {
+    T3(launch_pdl(hybrid_kernel<0, false>, grid, dim3(256), 0, s, n, nat, v0, mask));
+    T3(launch_pdl(hybrid_kernel<1, false>, grid, dim3(256), 0, s, n, nat, v1, mask));
+  }
+  return TMG_OK;
+}
+
+// one sweep of level l: on the caller's natural arrays (u, f), or on the
+// session's hybrid views when use_views
+int sweep3(tmg_cube* h, int l, double* u, const double* f, cudaStream_t s, bool use_views = false) {
   const int n = h->n[l];
   if (h->scheme == 1) {
+    const tmg3::Fields3 F = use_views && hyb(h, l)
+                                ? tmg3::Fields3{{h->UI[l], h->UJ[l], u}, {h->FI[l], h->FJ[l], f}, 1}
+                                : tmg3::Fields3{{u, u, u}, {f, f, f}, 0};
     for (int red = 1; red >= 0; red--)
-      if (tmg3::wire_stage(h->wl[l], n, coefs(h, l), red, u, f, h->err, s))
+      if (tmg3::wire_stage(h->wl[l], n, coefs(h, l), red, F, h->err, s))
         return cuda3(cudaGetLastError(), "wireframe stage");
     return TMG_OK;
   }
@@ -414,20 +516,40 @@ dim3 grid_restrict(int nf) {
 }
 dim3 grid_prolong(int nc) { return dim3((nc + 255) / 256, 2 * nc - 1, 2 * nc - 1); }
 
-int cycle3(tmg_cube* h, int nu1, int nu2, cudaStream_t s, int l0 = 0) {
+// The V-cycle from level l0.  Hybrid levels keep u in the views during the
+// sweeps and in the natural array for the transfers; on return both forms of
+// u[l0] are current.  entry: the views of l0 are to be filled first (the
+// replicated tail of the sharded cycle; a session keeps them current).
+int cycle3(tmg_cube* h, int nu1, int nu2, cudaStream_t s, int l0 = 0, bool entry = false) {
   const int L = (int)h->n.size();
+  if (entry && l0 < L - 1 && hyb(h, l0)) {
+    int st = convert3(h, l0, 0, true, s);
+    if (!st) st = convert3(h, l0, 1, true, s);
+    if (st) return st;
+  }
   for (int l = l0; l < L - 1; l++) {
     for (int k = 0; k < nu1; k++) {
-      int st = sweep3(h, l, h->U[l], h->F[l], s);
+      int st = sweep3(h, l, h->U[l], h->F[l], s, true);
       if (st) return st;
     }
-    TMG_COUNT(2);
+    if (hyb(h, l) && nu1 > 0) {
+      int st = convert3(h, l, 0, false, s);
+      if (st) return st;
+    }
+    TMG_COUNT(1);
     T3(launch_pdl(defect_restrict3_kernel, grid_restrict(h->n[l]), dim3(256), kRestrictSmem3, s,
-                  h->n[l],
-                  coefs(h, l), h->U[l], h->F[l], h->F[l + 1], restrict_ti(h->n[l])));
+                  h->n[l], coefs(h, l), h->U[l], h->F[l], h->F[l + 1], restrict_ti(h->n[l])));
     const size_t nc = (size_t)(h->n[l + 1] + 1) * (h->n[l + 1] + 1) * (h->n[l + 1] + 1);
-    T3(launch_pdl(zero3_kernel, dim3((unsigned)std::min<size_t>((nc + 255) / 256, 148 * 16)),
-                  dim3(256), 0, s, h->U[l + 1], nc));
+    const dim3 zg((unsigned)std::min<size_t>((nc + 255) / 256, 148 * 16));
+    TMG_COUNT(1);
+    T3(launch_pdl(zero3_kernel, zg, dim3(256), 0, s, h->U[l + 1], nc));
+    if (hyb(h, l + 1)) {
+      TMG_COUNT(2);
+      T3(launch_pdl(zero3_kernel, zg, dim3(256), 0, s, h->UI[l + 1], nc));
+      T3(launch_pdl(zero3_kernel, zg, dim3(256), 0, s, h->UJ[l + 1], nc));
+      int st = convert3(h, l + 1, 1, true, s);
+      if (st) return st;
+    }
   }
   TMG_COUNT(1);
   T3(launch_pdl(coarse3_kernel, dim3(1), dim3(1), 0, s, coefs(h, L - 1), h->U[L - 1], h->F[L - 1]));
@@ -435,8 +557,16 @@ int cycle3(tmg_cube* h, int nu1, int nu2, cudaStream_t s, int l0 = 0) {
     TMG_COUNT(1);
     T3(launch_pdl(prolong3v2_kernel, grid_prolong(h->n[l + 1]), dim3(256), 0, s, h->n[l + 1],
                   h->U[l + 1], h->U[l]));
+    if (hyb(h, l)) {
+      int st = convert3(h, l, 0, true, s);
+      if (st) return st;
+    }
     for (int k = 0; k < nu2; k++) {
-      int st = sweep3(h, l, h->U[l], h->F[l], s);
+      int st = sweep3(h, l, h->U[l], h->F[l], s, true);
+      if (st) return st;
+    }
+    if (hyb(h, l) && nu2 > 0) {  // natural u current for the transfers / the caller
+      int st = convert3(h, l, 0, false, s);
       if (st) return st;
     }
   }
@@ -463,6 +593,7 @@ int tmg_cube_create_scheme(int n, const double* x, int scheme, tmg_cube** out) {
                           (int)kRestrictSmem3));
   tmg_cube* h = new tmg_cube();
   h->scheme = scheme;
+  if (const char* e = getenv("TMG_HYB_MIN")) h->hyb_min = atoi(e);  // A/B: a large value disables
   std::vector<double> xs(x, x + n + 1);
   while (true) {
     const int m = (int)xs.size() - 1;
@@ -512,6 +643,16 @@ int tmg_cube_create_scheme(int n, const double* x, int scheme, tmg_cube** out) {
     T3(cudaMemset(pf, 0, tot * sizeof(double)));
     h->U.push_back(pu);
     h->F.push_back(pf);
+    double* views[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (scheme == 1 && m >= h->hyb_min)
+      for (double*& v : views) {
+        T3(cudaMalloc(&v, tot * sizeof(double)));
+        T3(cudaMemset(v, 0, tot * sizeof(double)));
+      }
+    h->UI.push_back(views[0]);
+    h->UJ.push_back(views[1]);
+    h->FI.push_back(views[2]);
+    h->FJ.push_back(views[3]);
     if (m % 2 || m / 2 < 2) break;
     std::vector<double> c;
     for (int i = 0; i <= m; i += 2) c.push_back(xs[i]);
@@ -536,6 +677,8 @@ int tmg_cube_destroy(tmg_cube* h) {
   for (auto& w : h->hl) tmg3::hub_free_level(w);
   for (double* p : h->U) cudaFree(p);
   for (double* p : h->F) cudaFree(p);
+  for (auto* vv : {&h->UI, &h->UJ, &h->FI, &h->FJ})
+    for (double* p : *vv) cudaFree(p);
   cudaFree(h->err);
   cudaFreeHost(h->h_err);
   delete h;
@@ -572,6 +715,11 @@ int tmg_cube_load(tmg_cube* h, const double* u, const double* f, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   T3(cudaMemcpyAsync(h->U[0], u, tot * sizeof(double), cudaMemcpyDeviceToDevice, s));
   T3(cudaMemcpyAsync(h->F[0], f, tot * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (hyb(h, 0)) {
+    int st = convert3(h, 0, 0, true, s);
+    if (!st) st = convert3(h, 0, 1, true, s);
+    if (st) return st;
+  }
   return TMG_OK;
 }
 
@@ -621,6 +769,20 @@ int tmg_cube_cycles(tmg_cube* h, int nu1, int nu2, int reps, void* stream) {
     T3(cudaGraphLaunch(h->graph, s));
     TMG_COUNT(h->graph_kernels);
   }
+  return TMG_OK;
+}
+
+// `reps` finest-level sweeps on the session's fields (the hybrid views when
+// the level has them; both forms of u current on return): the smoother
+// alone, as the V-cycle runs it
+int tmg_cube_sweeps(tmg_cube* h, int reps, void* stream) {
+  if (!h) return fail3(TMG_BADARG, "null cube");
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int r = 0; r < reps; r++) {
+    int st = sweep3(h, 0, h->U[0], h->F[0], s, true);
+    if (st) return st;
+  }
+  if (hyb(h, 0)) return convert3(h, 0, 0, false, s);
   return TMG_OK;
 }
 
@@ -789,7 +951,7 @@ int tmg_cube_tail(tmg_cube* h, int level, int nu1, int nu2, void* stream) {
   int st = cube_session_level(h, level, 0);
   if (st) return st;
   if (nu1 < 0 || nu2 < 0 || nu1 + nu2 < 1) return fail3(TMG_BADARG, "need nu1 + nu2 >= 1");
-  return cycle3(h, nu1, nu2, (cudaStream_t)stream, level);
+  return cycle3(h, nu1, nu2, (cudaStream_t)stream, level, true);
 }
 
 // out[q] = field[off[q]] / field[off[q]] = in[q]; which: 0 u, 1 f; off, out,

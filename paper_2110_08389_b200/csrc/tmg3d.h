@@ -14,6 +14,15 @@ struct Coef3 {
   const double *W, *E, *S, *N, *B, *T;
 };
 
+// Field views of the 3D block kernels (tmg3dw.cu): natural mode (hybrid = 0)
+// aliases the C-order arrays; hybrid mode adds i- and j-contiguous copies
+// (views 0, 1) next to the natural array (view 2), DESIGN.md §12.
+struct Fields3 {
+  double* u[3];
+  const double* f[3];
+  int hybrid;
+};
+
 __host__ __device__ inline long mirror(long x, long n) { return x < n - x ? x : n - x; }
 
 // reciprocal: the hardware approximation refined by two Newton steps (the
@@ -88,6 +97,8 @@ void wire_free_level(WLevel& L);
 // one colour stage (red = 1 / black = 0) of the wireframe sweep
 int wire_stage(const WLevel& L, int n, const Coef3& c, int red, double* u, const double* f,
                int* err, cudaStream_t s);
+int wire_stage(const WLevel& L, int n, const Coef3& c, int red, const Fields3& F, int* err,
+               cudaStream_t s);
 // blocks of a colour (for tmg_cube_blocks)
 long wire_blocks(const WLevel& L, int red);
 

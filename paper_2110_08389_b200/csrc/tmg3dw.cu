@@ -64,6 +64,45 @@ __host__ __device__ constexpr int tab_len(int n) { return n + 1 + (n + 1) / 8 + 
 template <int Q>
 __device__ __forceinline__ int rsw(int p) { return (p & ~(Q - 1)) | ((p ^ (p / Q)) & (Q - 1)); }
 
+// Field views of a colour stage.  Natural mode: the three
+// views alias the C-order arrays.  Hybrid mode (3D wireframe V-cycle): view
+// 0 is an i-contiguous copy ([j][k][i]) owning the points whose largest
+// mirrored coordinate is strictly i' (the i-edges), view 1 a j-contiguous
+// copy ([i][k][j]) owning the j-edges, view 2 the natural array owning the
+// k-edges; ties (ring and frame corners, face and cube centres) and the
+// boundary are valid in all three.
+__device__ __forceinline__ size_t off3(int lay, int n, int i, int j, int k) {
+  const size_t n1 = (size_t)n + 1;
+  return lay == 0 ? ((size_t)j * n1 + k) * n1 + i
+                  : (lay == 1 ? ((size_t)i * n1 + k) * n1 + j : ((size_t)i * n1 + j) * n1 + k);
+}
+__device__ __forceinline__ long str3(int lay, int n, int axis) {
+  const long n1 = n + 1;
+  if (lay == 0) return axis == 0 ? 1 : (axis == 1 ? n1 * n1 : n1);
+  if (lay == 1) return axis == 1 ? 1 : (axis == 0 ? n1 * n1 : n1);
+  return axis == 0 ? n1 * n1 : (axis == 1 ? n1 : 1);
+}
+// owner view of a point in hybrid mode: the axis of the strictly largest
+// mirrored coordinate; -1 for ties and the boundary (valid everywhere)
+__device__ __forceinline__ int owner3(int n, int i, int j, int k) {
+  if (i <= 0 || j <= 0 || k <= 0 || i >= n || j >= n || k >= n) return -1;
+  const int a = (int)mirror(i, n), b = (int)mirror(j, n), c = (int)mirror(k, n);
+  return (a > b && a > c) ? 0 : ((b > a && b > c) ? 1 : ((c > a && c > b) ? 2 : -1));
+}
+__device__ __forceinline__ double u_at(const Fields3& F, int n, int i, int j, int k) {
+  if (!F.hybrid) return F.u[2][off3(2, n, i, j, k)];
+  const int o = owner3(n, i, j, k), v = o < 0 ? 2 : o;
+  return F.u[v][off3(v, n, i, j, k)];
+}
+// a tie (or any point in natural mode): every view
+__device__ __forceinline__ void u_put_all(const Fields3& F, int n, int i, int j, int k, double x) {
+  F.u[2][off3(2, n, i, j, k)] = x;
+  if (F.hybrid) {
+    F.u[0][off3(0, n, i, j, k)] = x;
+    F.u[1][off3(1, n, i, j, k)] = x;
+  }
+}
+
 // Block kinds.  A ring (NE = 4 edges: face normal a at xa, level t), a frame
 // (NE = 12: shell t) or a 3D tweed hub block (NE = 2, 3 or 6 legs meeting at
 // a branch; tmg3d.cu).  Corners: ring K = 0..3 at in-face (b, c) = (t, t),
@@ -138,18 +177,20 @@ struct EdgeG {
   long sx, so1, so2;
   size_t o0;
   int x0, L;
+  double* u;        // the view owning the edge (natural mode: the C-order array)
+  const double* f;
 };
 
 // The cube API builds every axis from one coordinate array
 // (tmg_cube_create), so W = S = B and E = N = T: c.W / c.E serve every axis.
 template <int KIND, int NE>
-__device__ __forceinline__ EdgeG edge_geom(const Coef3& c, int n, const WBlk& B, int e) {
+__device__ __forceinline__ EdgeG edge_geom(const Coef3& c, int n, const WBlk& B, int e,
+                                           const Fields3& F) {
   int x, K0, K1, P0[3], P1[3];
   edge_def<KIND, NE>(B, e, x, K0, K1);
   corner_pos<KIND, NE>(B, n, K0, P0);
   corner_pos<KIND, NE>(B, n, K1, P1);
   const int o1 = x == 0 ? 1 : 0, o2 = x == 2 ? 1 : 2;
-  const long n1 = n + 1, str[3] = {n1 * n1, n1, 1};
   EdgeG G;
   const int p1 = o1 == 0 ? P0[0] : P0[1], p2 = o2 == 1 ? P0[1] : P0[2];
   G.t0 = __ldg(c.W + p1);
@@ -157,10 +198,13 @@ __device__ __forceinline__ EdgeG edge_geom(const Coef3& c, int n, const WBlk& B,
   G.t2 = __ldg(c.W + p2);
   G.t3 = __ldg(c.E + p2);
   G.tsum = G.t0 + G.t1 + G.t2 + G.t3;
-  G.sx = str[x];
-  G.so1 = str[o1];
-  G.so2 = str[o2];
-  G.o0 = ((size_t)P0[0] * n1 + P0[1]) * (size_t)n1 + P0[2];
+  const int lay = F.hybrid ? x : 2;
+  G.sx = str3(lay, n, x);
+  G.so1 = str3(lay, n, o1);
+  G.so2 = str3(lay, n, o2);
+  G.o0 = off3(lay, n, P0[0], P0[1], P0[2]);
+  G.u = F.u[lay];
+  G.f = F.f[lay];
   G.x0 = x == 0 ? P0[0] : (x == 1 ? P0[1] : P0[2]);
   const int x1 = x == 0 ? P1[0] : (x == 1 ? P1[1] : P1[2]);
   G.L = x1 - G.x0 - 1;
@@ -281,8 +325,7 @@ constexpr size_t wblock_smem() {
 // (3D tweed hub blocks).
 template <int KIND, int NE, int TE, int BDMAX, int Q>
 __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1 : 2)
-    wblock_kernel(int n, Coef3 c, const void* __restrict__ blocks, int nb, double* __restrict__ u,
-                  const double* __restrict__ f, int* err) {
+    wblock_kernel(int n, Coef3 c, const void* __restrict__ blocks, int nb, Fields3 F, int* err) {
   constexpr int NK = ncorners<KIND, NE>();
   constexpr int SL = NE * TE;  // threads per block
   constexpr int BD = wblock_bd<NE, TE, BDMAX>();
@@ -317,7 +360,7 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
     tlo[tix<Q>(x)] = __ldg(c.W + x);
     thi[tix<Q>(x)] = __ldg(c.E + x);
   }
-  const EdgeG G = edge_geom<KIND, NE>(c, n, B, ed);
+  const EdgeG G = edge_geom<KIND, NE>(c, n, B, ed, F);
   const int L = live && (KIND != kHub || ed < B.nleg) ? G.L : 0;  // unused hub legs: empty
   double* rr = sR + (g * NE + ed) * TE * Q;
   tmg::pdl_wait();  // the previous kernel's fields are complete from here on
@@ -332,11 +375,11 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
       for (int b = 0; b < NB; b++) {
         const int q = min(lt + (i0 + b) * TE, L - 1);  // clamped: loads stay unconditional
         const size_t o = G.o0 + (size_t)(q + 1) * G.sx;
-        f0[b] = f[o];
-        v0[b] = u[o - G.so1];
-        v1[b] = u[o + G.so1];
-        v2[b] = u[o - G.so2];
-        v3[b] = u[o + G.so2];
+        f0[b] = G.f[o];
+        v0[b] = G.u[o - G.so1];
+        v1[b] = G.u[o + G.so1];
+        v2[b] = G.u[o - G.so2];
+        v3[b] = G.u[o + G.so2];
       }
 #pragma unroll
       for (int b = 0; b < NB; b++) {
@@ -349,10 +392,8 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
   for (int K = tid % SL; live && K < NK; K += SL) {
     int P[3];
     corner_pos<KIND, NE>(B, n, K, P);
-    const long n1 = n + 1, str[3] = {n1 * n1, n1, 1};
-    const size_t o = ((size_t)P[0] * n1 + P[1]) * (size_t)n1 + P[2];
     if (KIND == kHub && K > 0) {
-      sXc[g][K] = u[o];  // a wall point: its Dirichlet value
+      sXc[g][K] = u_at(F, n, P[0], P[1], P[2]);  // a wall point: its Dirichlet value
     } else {
       unsigned in = 0;  // in-block directions: bit 2a (toward -), 2a+1 (toward +)
       for (int e = 0; e < (KIND == kHub ? B.nleg : NE); e++) {
@@ -361,12 +402,14 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
         if (K0 == K) in |= 2u << (2 * x);
         if (K1 == K) in |= 1u << (2 * x);
       }
-      double d = 0.0, rk = f[o];
+      double d = 0.0, rk = F.f[2][off3(2, n, P[0], P[1], P[2])];
       for (int a = 0; a < 3; a++) {
         const double lo = __ldg(c.W + P[a]), hi = __ldg(c.E + P[a]);
         d -= lo + hi;
-        if (!(in & (1u << (2 * a)))) rk -= lo * u[o - str[a]];
-        if (!(in & (2u << (2 * a)))) rk -= hi * u[o + str[a]];
+        const int i0 = P[0] - (a == 0), j0 = P[1] - (a == 1), k0 = P[2] - (a == 2);
+        const int i1 = P[0] + (a == 0), j1 = P[1] + (a == 1), k1 = P[2] + (a == 2);
+        if (!(in & (1u << (2 * a)))) rk -= lo * u_at(F, n, i0, j0, k0);
+        if (!(in & (2u << (2 * a)))) rk -= hi * u_at(F, n, i1, j1, k1);
       }
       sKr[g][K] = rk;
       sKd[g][K] = d;
@@ -593,7 +636,7 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
   if (live && tid % SL < (KIND == kHub ? 1 : NK)) {  // hubs: the walls stay
     int P3[3];
     corner_pos<KIND, NE>(B, n, tid % SL, P3);
-    u[idx3(n, P3[0], P3[1], P3[2])] = sXc[g][tid % SL];
+    u_put_all(F, n, P3[0], P3[1], P3[2], sXc[g][tid % SL]);
   }
   // 5. finalise every chunk with both ends known, then scatter
   if (cnt > 0) {
@@ -609,30 +652,28 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
 #pragma unroll 4
   for (int it = 0; it < Q; it++) {
     const int q = lt + it * TE;
-    if (q < L) u[G.o0 + (size_t)(q + 1) * G.sx] = rr[rsw<Q>(q)];
+    if (q < L) G.u[G.o0 + (size_t)(q + 1) * G.sx] = rr[rsw<Q>(q)];
   }
   if (bad) atomicOr(err, 1);
 }
 
 __global__ void __launch_bounds__(128) wpoint_kernel(int n, Coef3 c, const int4* __restrict__ pts,
-                                                     int np, double* __restrict__ u,
-                                                     const double* __restrict__ f, int* err) {
+                                                     int np, Fields3 F, int* err) {
   tmg::pdl_trigger();
   tmg::pdl_wait();
   const int id = blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= np) return;
   const int4 P = pts[id];
   const int i = P.x, j = P.y, k = P.z;
-  const size_t o = idx3(n, i, j, k);
   const double d = -(__ldg(c.W + i) + __ldg(c.E + i) + __ldg(c.S + j) + __ldg(c.N + j) +
                      __ldg(c.B + k) + __ldg(c.T + k));
-  const double r = f[o] - __ldg(c.W + i) * u[idx3(n, i - 1, j, k)] -
-                   __ldg(c.E + i) * u[idx3(n, i + 1, j, k)] -
-                   __ldg(c.S + j) * u[idx3(n, i, j - 1, k)] -
-                   __ldg(c.N + j) * u[idx3(n, i, j + 1, k)] - __ldg(c.B + k) * u[o - 1] -
-                   __ldg(c.T + k) * u[o + 1];
+  const double r = F.f[2][off3(2, n, i, j, k)] - __ldg(c.W + i) * u_at(F, n, i - 1, j, k) -
+                   __ldg(c.E + i) * u_at(F, n, i + 1, j, k) -
+                   __ldg(c.S + j) * u_at(F, n, i, j - 1, k) -
+                   __ldg(c.N + j) * u_at(F, n, i, j + 1, k) - __ldg(c.B + k) * u_at(F, n, i, j, k - 1) -
+                   __ldg(c.T + k) * u_at(F, n, i, j, k + 1);
   if (wbad(d)) atomicOr(err, 1);
-  u[o] = r / d;
+  u_put_all(F, n, i, j, k, r / d);
 }
 
 // ring classes: TE = 1 .. 64 threads per side (edges of m - 1 <= TE kQW points)
@@ -660,25 +701,25 @@ cudaError_t allow_smem() {
 }
 
 template <int KIND, int NE, int TE, int BDMAX, int Q>
-void launch_blocks(const void* blocks, int nb, int n, const Coef3& c, double* u, const double* f,
-                   int* err, cudaStream_t s) {
+void launch_blocks(const void* blocks, int nb, int n, const Coef3& c, const Fields3& F, int* err,
+                   cudaStream_t s) {
   if (!nb) return;
   constexpr int BD = wblock_bd<NE, TE, BDMAX>(), BPC = wblock_bpc<NE, TE, BDMAX>();
   TMG_COUNT(1);
   tmg::launch_pdl(wblock_kernel<KIND, NE, TE, BDMAX, Q>, dim3((nb + BPC - 1) / BPC), dim3(BD),
-                  wblock_smem<NE, TE, BDMAX, Q>(), s, n, c, blocks, nb, u, f, err);
+                  wblock_smem<NE, TE, BDMAX, Q>(), s, n, c, blocks, nb, F, err);
 }
 
 template <int TE>
-void launch_rings(const WLevel& L, int n, const Coef3& c, int red, int k, double* u, const double* f,
-                  int* err, cudaStream_t s) {
-  launch_blocks<kRing, 4, TE, ring_bd(TE), kRQ>(L.rings[red][k], L.nrings[red][k], n, c, u, f, err, s);
+void launch_rings(const WLevel& L, int n, const Coef3& c, int red, int k, const Fields3& F, int* err,
+                  cudaStream_t s) {
+  launch_blocks<kRing, 4, TE, ring_bd(TE), kRQ>(L.rings[red][k], L.nrings[red][k], n, c, F, err, s);
 }
 
 template <int TE>
-void launch_frames(const WLevel& L, int n, const Coef3& c, double* u, const double* f, int* err,
+void launch_frames(const WLevel& L, int n, const Coef3& c, const Fields3& F, int* err,
                    cudaStream_t s) {
-  launch_blocks<kFrame, 12, TE, 12 * TE, kQW>(L.frames, L.nframes, n, c, u, f, err, s);
+  launch_blocks<kFrame, 12, TE, 12 * TE, kQW>(L.frames, L.nframes, n, c, F, err, s);
 }
 
 // 3D tweed hub blocks: classes by legs (2, 3, 6) and threads per leg
@@ -702,16 +743,16 @@ void merge_small_classes(std::vector<T>* cls, int nc, int ne, const int* te) {
 }
 
 template <int NL>
-void launch_hubs(const HubLevel& L, int kind, int n, const Coef3& c, int red, double* u,
-                 const double* f, int* err, cudaStream_t s) {
+void launch_hubs(const HubLevel& L, int kind, int n, const Coef3& c, int red, const Fields3& F,
+                 int* err, cudaStream_t s) {
   const HubB* const* b = L.blocks[red][kind];
   const int* nb = L.nblocks[red][kind];
-  launch_blocks<kHub, NL, 1, kRBD, kQW>(b[0], nb[0], n, c, u, f, err, s);
-  launch_blocks<kHub, NL, 2, kRBD, kQW>(b[1], nb[1], n, c, u, f, err, s);
-  launch_blocks<kHub, NL, 4, kRBD, kQW>(b[2], nb[2], n, c, u, f, err, s);
-  launch_blocks<kHub, NL, 8, kRBD, kQW>(b[3], nb[3], n, c, u, f, err, s);
-  launch_blocks<kHub, NL, 16, kRBD, kQW>(b[4], nb[4], n, c, u, f, err, s);
-  launch_blocks<kHub, NL, 32, kRBD, kQW>(b[5], nb[5], n, c, u, f, err, s);
+  launch_blocks<kHub, NL, 1, kRBD, kQW>(b[0], nb[0], n, c, F, err, s);
+  launch_blocks<kHub, NL, 2, kRBD, kQW>(b[1], nb[1], n, c, F, err, s);
+  launch_blocks<kHub, NL, 4, kRBD, kQW>(b[2], nb[2], n, c, F, err, s);
+  launch_blocks<kHub, NL, 8, kRBD, kQW>(b[3], nb[3], n, c, F, err, s);
+  launch_blocks<kHub, NL, 16, kRBD, kQW>(b[4], nb[4], n, c, F, err, s);
+  launch_blocks<kHub, NL, 32, kRBD, kQW>(b[5], nb[5], n, c, F, err, s);
 }
 
 template <int NL>
@@ -809,29 +850,34 @@ long wire_blocks(const WLevel& L, int red) {
   return nb;
 }
 
-int wire_stage(const WLevel& L, int n, const Coef3& c, int red, double* u, const double* f,
-               int* err, cudaStream_t s) {
-  launch_rings<1>(L, n, c, red, 0, u, f, err, s);
-  launch_rings<2>(L, n, c, red, 1, u, f, err, s);
-  launch_rings<4>(L, n, c, red, 2, u, f, err, s);
-  launch_rings<8>(L, n, c, red, 3, u, f, err, s);
-  launch_rings<16>(L, n, c, red, 4, u, f, err, s);
-  launch_rings<32>(L, n, c, red, 5, u, f, err, s);
-  launch_rings<64>(L, n, c, red, 6, u, f, err, s);
-  if (kRQ < 16) launch_rings<128>(L, n, c, red, 7, u, f, err, s);
+int wire_stage(const WLevel& L, int n, const Coef3& c, int red, const Fields3& F, int* err,
+               cudaStream_t s) {
+  launch_rings<1>(L, n, c, red, 0, F, err, s);
+  launch_rings<2>(L, n, c, red, 1, F, err, s);
+  launch_rings<4>(L, n, c, red, 2, F, err, s);
+  launch_rings<8>(L, n, c, red, 3, F, err, s);
+  launch_rings<16>(L, n, c, red, 4, F, err, s);
+  launch_rings<32>(L, n, c, red, 5, F, err, s);
+  launch_rings<64>(L, n, c, red, 6, F, err, s);
+  if (kRQ < 16) launch_rings<128>(L, n, c, red, 7, F, err, s);
   if (red && L.nframes) {
     const int emax = n - 3;  // the outermost frame's edges
-    if (emax <= 4 * kQW) launch_frames<4>(L, n, c, u, f, err, s);
-    else if (emax <= 16 * kQW) launch_frames<16>(L, n, c, u, f, err, s);
-    else launch_frames<64>(L, n, c, u, f, err, s);
+    if (emax <= 4 * kQW) launch_frames<4>(L, n, c, F, err, s);
+    else if (emax <= 16 * kQW) launch_frames<16>(L, n, c, F, err, s);
+    else launch_frames<64>(L, n, c, F, err, s);
   }
   if (L.npoints[red]) {
     TMG_COUNT(1);
     tmg::launch_pdl(wpoint_kernel, dim3((L.npoints[red] + 127) / 128), dim3(128), 0, s, n, c,
-                    L.points[red], L.npoints[red], u, f, err);
+                    L.points[red], L.npoints[red], F, err);
   }
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : 3;
+}
+
+int wire_stage(const WLevel& L, int n, const Coef3& c, int red, double* u, const double* f,
+               int* err, cudaStream_t s) {
+  return wire_stage(L, n, c, red, Fields3{{u, u, u}, {f, f, f}, 0}, err, s);
 }
 
 int hub_build_level(int n, const std::vector<HubB> blocks[2], HubLevel& L, std::string& err) {
@@ -885,12 +931,13 @@ void hub_free_level(HubLevel& L) {
 
 int hub_stage(const HubLevel& L, int n, const Coef3& c, int red, double* u, const double* f,
               int* err, cudaStream_t s) {
-  launch_hubs<2>(L, 0, n, c, red, u, f, err, s);
-  launch_hubs<6>(L, 1, n, c, red, u, f, err, s);
+  const Fields3 F{{u, u, u}, {f, f, f}, 0};
+  launch_hubs<2>(L, 0, n, c, red, F, err, s);
+  launch_hubs<6>(L, 1, n, c, red, F, err, s);
   if (L.npoints[red]) {
     TMG_COUNT(1);
     tmg::launch_pdl(wpoint_kernel, dim3((L.npoints[red] + 127) / 128), dim3(128), 0, s, n, c,
-                    L.points[red], L.npoints[red], u, f, err);
+                    L.points[red], L.npoints[red], F, err);
   }
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : 3;

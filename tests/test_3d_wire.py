@@ -161,3 +161,27 @@ def test_config5_scale_sweep(cuda, orc):
     o3.sweep(o3.assemble3(x.values, x.values, x.values), uo, f.cpu().numpy(), orc.max_threads(),
              scheme="wireframe")
     assert np.abs(u.cpu().numpy() - uo).max() <= 1e-10 * np.abs(uo).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [16, 32])
+def test_hybrid_vcycle_matches_oracle(cuda, orc, monkeypatch, n):
+    """The V-cycle on the hybrid layout (i- and j-contiguous views of every
+    level, forced down to n = 4) against the oracle, per cycle and in the
+    solve's cycle count."""
+    from paper_2110_08389_b200 import cube, mgcycle
+    monkeypatch.setenv("TMG_HYB_MIN", "4")
+    o3 = _o3()
+    x = configs.sinh_centre(n, 1.0, 3.0)
+    h = cube.CubeHierarchy(x, scheme="wireframe")
+    H = o3.Hierarchy3(x.values, scheme="wireframe")
+    f = cube.config5_rhs(n, device=False)
+    cfg = mgcycle.CycleConfig(smoother="wireframe", nu1=2, nu2=2)
+    ug, uo = np.zeros_like(f), np.zeros_like(f)
+    for _ in range(3):
+        cube.v_cycle(h, cfg, ug, f)
+        o3.v_cycle(H, uo, f)
+        assert np.abs(ug - uo).max() <= 1e-10 * np.abs(uo).max()
+    _, rep = cube.solve(h, cfg, f)
+    _, repo = o3.solve(H, f)
+    assert rep.cycles == repo.cycles and rep.converged == repo.converged

@@ -1,5 +1,6 @@
 """One (or a few) 3D sweeps on a cube, for ncu captures:
-cube_sweep_once.py n tweed|wireframe [reps]."""
+cube_sweep_once.py n tweed|wireframe [reps] [session]  (session: the loaded
+session's sweeps, on the hybrid views of the 3D wireframe)."""
 import ctypes
 import os
 import sys
@@ -21,7 +22,11 @@ else:
 u = torch.zeros_like(f)
 L = _lib.lib()
 s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-for _ in range(reps):
-    L.tmg_cube_sweep(h._h, ctypes.c_void_p(u.data_ptr()), ctypes.c_void_p(f.data_ptr()), s)
+if len(sys.argv) > 4 and sys.argv[4] == "session":
+    L.tmg_cube_load(h._h, ctypes.c_void_p(u.data_ptr()), ctypes.c_void_p(f.data_ptr()), s)
+    L.tmg_cube_sweeps(h._h, reps, s)
+else:
+    for _ in range(reps):
+        L.tmg_cube_sweep(h._h, ctypes.c_void_p(u.data_ptr()), ctypes.c_void_p(f.data_ptr()), s)
 torch.cuda.synchronize()
 print("done", n, scheme, reps)

@@ -37,7 +37,9 @@ def ev(fn, reps):
 
 tsw = ev(lambda: L.tmg_cube_sweep(h._h, ctypes.c_void_p(u.data_ptr()), ctypes.c_void_p(f.data_ptr()), s), 10)
 L.tmg_cube_load(h._h, ctypes.c_void_p(u.data_ptr()), ctypes.c_void_p(f.data_ptr()), s)
+tss = ev(lambda: L.tmg_cube_sweeps(h._h, 1, s), 10)
 tcy = ev(lambda: L.tmg_cube_cycles(h._h, 2, 2, 1, s), 5)
 npts = (n - 1) ** 3
 print(f"{scheme} n={n} blocks {h.blocks(0)} sweep {tsw:.3f} ms ({24 * npts / tsw / 1e6:.0f} GB/s alg) "
+      f"session sweep {tss:.3f} ms ({24 * npts / tss / 1e6:.0f} GB/s alg) "
       f"V(2,2) {tcy:.3f} ms ({4 * h.interior_points() / tcy / 1e6:.3e} updates/s)")
