@@ -290,9 +290,10 @@ __global__ void __launch_bounds__(256) prolong3v2_kernel(int nc, const double* _
 // memory so that both sides are read and written along a contiguous axis;
 // CTAs walk (k tile, fixed index) fastest and the axis-V tile slowest, so a
 // wave touches 32 planes of the natural array (TLB reach, DRAM rows).
-__device__ __forceinline__ int owner_h(int n, int i, int j, int k) {
+__device__ __forceinline__ int owner_h(int n, int i, int j, int k, bool smallest) {
   if (i <= 0 || j <= 0 || k <= 0 || i >= n || j >= n || k >= n) return -1;
-  const int a = (int)mirror(i, n), b = (int)mirror(j, n), c = (int)mirror(k, n);
+  int a = (int)mirror(i, n), b = (int)mirror(j, n), c = (int)mirror(k, n);
+  if (smallest) { a = -a; b = -b; c = -c; }
   return (a > b && a > c) ? 0 : ((b > a && b > c) ? 1 : ((c > a && c > b) ? 2 : -1));
 }
 
@@ -302,7 +303,7 @@ __device__ __forceinline__ int owner_h(int n, int i, int j, int k) {
 // reads; 2, f: the owned points); else view V -> natural for the owned
 // points.  Tiles without such points are skipped (a view covers ~1/3 of the
 // cube).
-template <int V, bool TO_VIEW>
+template <int V, bool TO_VIEW, bool SMALL>
 __global__ void __launch_bounds__(256) hybrid_kernel(int n, double* __restrict__ nat,
                                                      double* __restrict__ view, int mask) {
   __shared__ double t[32][33];
@@ -310,12 +311,17 @@ __global__ void __launch_bounds__(256) hybrid_kernel(int n, double* __restrict__
   const int kt = blockIdx.x * 32, fx = blockIdx.y, at = blockIdx.z * 32;  // fx: j (V = 0) or i (V = 1)
   const size_t n1 = (size_t)n + 1;
   const int lane = threadIdx.x & 31, row = threadIdx.x >> 5;
-  // tile test: the largest mirrored axis-V coordinate of the tile against
-  // the fixed index's and the smallest k's
+  // tile test on the mirrored coordinates (negated for SMALL, the 3D tweed):
+  // the tile's best axis-V value against the fixed index's and the k range's
   const int a1 = min(at + 31, n), k1 = min(kt + 31, n);
-  const int ma = (at <= n / 2 && n / 2 <= a1) ? n / 2 : max((int)mirror(at, n), (int)mirror(a1, n));
-  const int mk = min((int)mirror(kt, n), (int)mirror(k1, n));
-  const int mf = (int)mirror(fx, n);
+  const int sg = SMALL ? -1 : 1;
+  const int ma = SMALL ? -min((int)mirror(at, n), (int)mirror(a1, n))
+                       : ((at <= n / 2 && n / 2 <= a1) ? n / 2
+                                                        : max((int)mirror(at, n), (int)mirror(a1, n)));
+  const int mk = SMALL ? -((kt <= n / 2 && n / 2 <= k1) ? n / 2
+                                                        : max((int)mirror(kt, n), (int)mirror(k1, n)))
+                       : min((int)mirror(kt, n), (int)mirror(k1, n));
+  const int mf = sg * (int)mirror(fx, n);
   const bool strict = !(TO_VIEW && mask == 1);
   if (strict ? (ma <= mf || ma <= mk) : (ma < mf || ma < mk)) return;
   pdl_wait();
@@ -326,10 +332,10 @@ __global__ void __launch_bounds__(256) hybrid_kernel(int n, double* __restrict__
   auto sel = [&](int a, int k) {
     const int i = V == 0 ? a : fx, j = V == 0 ? fx : a;
     if (!strict) {
-      const int mv = (int)mirror(a, n), mo = max((int)mirror(fx, n), (int)mirror(k, n));
+      const int mv = sg * (int)mirror(a, n), mo = max(sg * (int)mirror(fx, n), sg * (int)mirror(k, n));
       return mv >= mo;
     }
-    return owner_h(n, i, j, k) == V;
+    return owner_h(n, i, j, k, SMALL) == V;
   };
   if (TO_VIEW) {
     for (int r = row; r < 32; r += 8) {
@@ -407,7 +413,7 @@ struct tmg_cube {
   // 3D wireframe hybrid views (i- and j-contiguous copies) of the levels with
   // n >= hyb_min; null elsewhere
   std::vector<double*> UI, UJ, FI, FJ;
-  int hyb_min = 256;
+  int hyb_min = 256;                  // levels with n >= hyb_min get the views
   int* err = nullptr;
   unsigned long long* dmax = nullptr;
   int* h_err = nullptr;
@@ -461,7 +467,7 @@ Coef3 coefs(const tmg_cube* h, int l) {
   return Coef3{p, p + n1, p + 2 * n1, p + 3 * n1, p + 4 * n1, p + 5 * n1};
 }
 
-bool hyb(const tmg_cube* h, int l) { return h->scheme == 1 && l < (int)h->UI.size() && h->UI[l]; }
+bool hyb(const tmg_cube* h, int l) { return l < (int)h->UI.size() && h->UI[l]; }
 
 // hybrid <-> natural for level l: which = 0 u, 1 f
 int convert3(tmg_cube* h, int l, int which, bool to_view, cudaStream_t s) {
@@ -472,12 +478,20 @@ int convert3(tmg_cube* h, int l, int which, bool to_view, cudaStream_t s) {
   double* v1 = which ? h->FJ[l] : h->UJ[l];
   const int mask = which ? 2 : 1;
   TMG_COUNT(2);
-  if (to_view) {
-    T3(launch_pdl(hybrid_kernel<0, true>, grid, dim3(256), 0, s, n, nat, v0, mask));
-    T3(launch_pdl(hybrid_kernel<1, true>, grid, dim3(256), 0, s, n, nat, v1, mask));
+  if (h->scheme == 1) {
+    if (to_view) {
+      T3(launch_pdl(hybrid_kernel<0, true, false>, grid, dim3(256), 0, s, n, nat, v0, mask));
+      T3(launch_pdl(hybrid_kernel<1, true, false>, grid, dim3(256), 0, s, n, nat, v1, mask));
+    } else {
+      T3(launch_pdl(hybrid_kernel<0, false, false>, grid, dim3(256), 0, s, n, nat, v0, mask));
+      T3(launch_pdl(hybrid_kernel<1, false, false>, grid, dim3(256), 0, s, n, nat, v1, mask));
+    }
+  } else if (to_view) {
+    T3(launch_pdl(hybrid_kernel<0, true, true>, grid, dim3(256), 0, s, n, nat, v0, mask));
+    T3(launch_pdl(hybrid_kernel<1, true, true>, grid, dim3(256), 0, s, n, nat, v1, mask));
   } else {
-    T3(launch_pdl(hybrid_kernel<0, false>, grid, dim3(256), 0, s, n, nat, v0, mask));
-    T3(launch_pdl(hybrid_kernel<1, false>, grid, dim3(256), 0, s, n, nat, v1, mask));
+    T3(launch_pdl(hybrid_kernel<0, false, true>, grid, dim3(256), 0, s, n, nat, v0, mask));
+    T3(launch_pdl(hybrid_kernel<1, false, true>, grid, dim3(256), 0, s, n, nat, v1, mask));
   }
   return TMG_OK;
 }
@@ -495,8 +509,11 @@ int sweep3(tmg_cube* h, int l, double* u, const double* f, cudaStream_t s, bool 
         return cuda3(cudaGetLastError(), "wireframe stage");
     return TMG_OK;
   }
+  const tmg3::Fields3 F = use_views && hyb(h, l)
+                              ? tmg3::Fields3{{h->UI[l], h->UJ[l], u}, {h->FI[l], h->FJ[l], f}, 2}
+                              : tmg3::Fields3{{u, u, u}, {f, f, f}, 0};
   for (int red = 1; red >= 0; red--)
-    if (tmg3::hub_stage(h->hl[l], n, coefs(h, l), red, u, f, h->err, s))
+    if (tmg3::hub_stage(h->hl[l], n, coefs(h, l), red, F, h->err, s))
       return cuda3(cudaGetLastError(), "tweed stage");
   return TMG_OK;
 }
@@ -593,6 +610,9 @@ int tmg_cube_create_scheme(int n, const double* x, int scheme, tmg_cube** out) {
                           (int)kRestrictSmem3));
   tmg_cube* h = new tmg_cube();
   h->scheme = scheme;
+  // hybrid views from 257^3 (wireframe) / 513^3 (tweed) up: measured break-even
+  // against the conversions
+  h->hyb_min = scheme == 1 ? 256 : 512;
   if (const char* e = getenv("TMG_HYB_MIN")) h->hyb_min = atoi(e);  // A/B: a large value disables
   std::vector<double> xs(x, x + n + 1);
   while (true) {
@@ -644,7 +664,7 @@ int tmg_cube_create_scheme(int n, const double* x, int scheme, tmg_cube** out) {
     h->U.push_back(pu);
     h->F.push_back(pf);
     double* views[4] = {nullptr, nullptr, nullptr, nullptr};
-    if (scheme == 1 && m >= h->hyb_min)
+    if (m >= h->hyb_min)
       for (double*& v : views) {
         T3(cudaMalloc(&v, tot * sizeof(double)));
         T3(cudaMemset(v, 0, tot * sizeof(double)));

@@ -16,7 +16,9 @@ struct Coef3 {
 
 // Field views of the 3D block kernels (tmg3dw.cu): natural mode (hybrid = 0)
 // aliases the C-order arrays; hybrid mode adds i- and j-contiguous copies
-// (views 0, 1) next to the natural array (view 2), DESIGN.md §12.
+// (views 0, 1) next to the natural array (view 2); hybrid = 1:
+// a point belongs to the axis of its largest mirrored coordinate (3D
+// wireframe edges), 2: of its smallest (3D tweed legs).
 struct Fields3 {
   double* u[3];
   const double* f[3];
@@ -91,6 +93,8 @@ int hub_build_level(int n, const std::vector<HubB> blocks[2], HubLevel& L, std::
 void hub_free_level(HubLevel& L);
 int hub_stage(const HubLevel& L, int n, const Coef3& c, int red, double* u, const double* f,
               int* err, cudaStream_t s);
+int hub_stage(const HubLevel& L, int n, const Coef3& c, int red, const Fields3& F, int* err,
+              cudaStream_t s);
 
 int wire_build_level(int n, WLevel& L, std::string& err, int g0 = 0, int g1 = 1 << 30);
 void wire_free_level(WLevel& L);

@@ -83,21 +83,26 @@ __device__ __forceinline__ long str3(int lay, int n, int axis) {
   return axis == 0 ? n1 * n1 : (axis == 1 ? n1 : 1);
 }
 // owner view of a point in hybrid mode: the axis of the strictly largest
-// mirrored coordinate; -1 for ties and the boundary (valid everywhere)
-__device__ __forceinline__ int owner3(int n, int i, int j, int k) {
+// mirrored coordinate (3D wireframe edges, HYB = 1) or of the strictly
+// smallest (3D tweed legs, HYB = 2); -1 for ties and the boundary (valid in
+// every view)
+__device__ __forceinline__ int owner3(int n, int i, int j, int k, bool smallest) {
   if (i <= 0 || j <= 0 || k <= 0 || i >= n || j >= n || k >= n) return -1;
-  const int a = (int)mirror(i, n), b = (int)mirror(j, n), c = (int)mirror(k, n);
+  int a = (int)mirror(i, n), b = (int)mirror(j, n), c = (int)mirror(k, n);
+  if (smallest) { a = -a; b = -b; c = -c; }
   return (a > b && a > c) ? 0 : ((b > a && b > c) ? 1 : ((c > a && c > b) ? 2 : -1));
 }
+template <int HYB>
 __device__ __forceinline__ double u_at(const Fields3& F, int n, int i, int j, int k) {
-  if (!F.hybrid) return F.u[2][off3(2, n, i, j, k)];
-  const int o = owner3(n, i, j, k), v = o < 0 ? 2 : o;
+  if (!HYB) return F.u[2][off3(2, n, i, j, k)];
+  const int o = owner3(n, i, j, k, HYB == 2), v = o < 0 ? 2 : o;
   return F.u[v][off3(v, n, i, j, k)];
 }
 // a tie (or any point in natural mode): every view
+template <int HYB>
 __device__ __forceinline__ void u_put_all(const Fields3& F, int n, int i, int j, int k, double x) {
   F.u[2][off3(2, n, i, j, k)] = x;
-  if (F.hybrid) {
+  if (HYB) {
     F.u[0][off3(0, n, i, j, k)] = x;
     F.u[1][off3(1, n, i, j, k)] = x;
   }
@@ -183,7 +188,7 @@ struct EdgeG {
 
 // The cube API builds every axis from one coordinate array
 // (tmg_cube_create), so W = S = B and E = N = T: c.W / c.E serve every axis.
-template <int KIND, int NE>
+template <int KIND, int NE, int HYB>
 __device__ __forceinline__ EdgeG edge_geom(const Coef3& c, int n, const WBlk& B, int e,
                                            const Fields3& F) {
   int x, K0, K1, P0[3], P1[3];
@@ -198,7 +203,7 @@ __device__ __forceinline__ EdgeG edge_geom(const Coef3& c, int n, const WBlk& B,
   G.t2 = __ldg(c.W + p2);
   G.t3 = __ldg(c.E + p2);
   G.tsum = G.t0 + G.t1 + G.t2 + G.t3;
-  const int lay = F.hybrid ? x : 2;
+  const int lay = HYB ? x : 2;
   G.sx = str3(lay, n, x);
   G.so1 = str3(lay, n, o1);
   G.so2 = str3(lay, n, o2);
@@ -323,7 +328,7 @@ constexpr size_t wblock_smem() {
 // Blocks of one kind and class: whole blocks of NE * TE threads per CTA, TE
 // threads per edge.  `blocks`: Ring3 (rings), int shell (frames) or HubB
 // (3D tweed hub blocks).
-template <int KIND, int NE, int TE, int BDMAX, int Q>
+template <int KIND, int NE, int TE, int BDMAX, int Q, int HYB>
 __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1 : 2)
     wblock_kernel(int n, Coef3 c, const void* __restrict__ blocks, int nb, Fields3 F, int* err) {
   constexpr int NK = ncorners<KIND, NE>();
@@ -360,7 +365,7 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
     tlo[tix<Q>(x)] = __ldg(c.W + x);
     thi[tix<Q>(x)] = __ldg(c.E + x);
   }
-  const EdgeG G = edge_geom<KIND, NE>(c, n, B, ed, F);
+  const EdgeG G = edge_geom<KIND, NE, HYB>(c, n, B, ed, F);
   const int L = live && (KIND != kHub || ed < B.nleg) ? G.L : 0;  // unused hub legs: empty
   double* rr = sR + (g * NE + ed) * TE * Q;
   tmg::pdl_wait();  // the previous kernel's fields are complete from here on
@@ -393,7 +398,7 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
     int P[3];
     corner_pos<KIND, NE>(B, n, K, P);
     if (KIND == kHub && K > 0) {
-      sXc[g][K] = u_at(F, n, P[0], P[1], P[2]);  // a wall point: its Dirichlet value
+      sXc[g][K] = u_at<HYB>(F, n, P[0], P[1], P[2]);  // a wall point: its Dirichlet value
     } else {
       unsigned in = 0;  // in-block directions: bit 2a (toward -), 2a+1 (toward +)
       for (int e = 0; e < (KIND == kHub ? B.nleg : NE); e++) {
@@ -408,8 +413,8 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
         d -= lo + hi;
         const int i0 = P[0] - (a == 0), j0 = P[1] - (a == 1), k0 = P[2] - (a == 2);
         const int i1 = P[0] + (a == 0), j1 = P[1] + (a == 1), k1 = P[2] + (a == 2);
-        if (!(in & (1u << (2 * a)))) rk -= lo * u_at(F, n, i0, j0, k0);
-        if (!(in & (2u << (2 * a)))) rk -= hi * u_at(F, n, i1, j1, k1);
+        if (!(in & (1u << (2 * a)))) rk -= lo * u_at<HYB>(F, n, i0, j0, k0);
+        if (!(in & (2u << (2 * a)))) rk -= hi * u_at<HYB>(F, n, i1, j1, k1);
       }
       sKr[g][K] = rk;
       sKd[g][K] = d;
@@ -636,7 +641,7 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
   if (live && tid % SL < (KIND == kHub ? 1 : NK)) {  // hubs: the walls stay
     int P3[3];
     corner_pos<KIND, NE>(B, n, tid % SL, P3);
-    u_put_all(F, n, P3[0], P3[1], P3[2], sXc[g][tid % SL]);
+    u_put_all<HYB>(F, n, P3[0], P3[1], P3[2], sXc[g][tid % SL]);
   }
   // 5. finalise every chunk with both ends known, then scatter
   if (cnt > 0) {
@@ -657,6 +662,7 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
   if (bad) atomicOr(err, 1);
 }
 
+template <int HYB>
 __global__ void __launch_bounds__(128) wpoint_kernel(int n, Coef3 c, const int4* __restrict__ pts,
                                                      int np, Fields3 F, int* err) {
   tmg::pdl_trigger();
@@ -667,13 +673,13 @@ __global__ void __launch_bounds__(128) wpoint_kernel(int n, Coef3 c, const int4*
   const int i = P.x, j = P.y, k = P.z;
   const double d = -(__ldg(c.W + i) + __ldg(c.E + i) + __ldg(c.S + j) + __ldg(c.N + j) +
                      __ldg(c.B + k) + __ldg(c.T + k));
-  const double r = F.f[2][off3(2, n, i, j, k)] - __ldg(c.W + i) * u_at(F, n, i - 1, j, k) -
-                   __ldg(c.E + i) * u_at(F, n, i + 1, j, k) -
-                   __ldg(c.S + j) * u_at(F, n, i, j - 1, k) -
-                   __ldg(c.N + j) * u_at(F, n, i, j + 1, k) - __ldg(c.B + k) * u_at(F, n, i, j, k - 1) -
-                   __ldg(c.T + k) * u_at(F, n, i, j, k + 1);
+  const double r = F.f[2][off3(2, n, i, j, k)] - __ldg(c.W + i) * u_at<HYB>(F, n, i - 1, j, k) -
+                   __ldg(c.E + i) * u_at<HYB>(F, n, i + 1, j, k) -
+                   __ldg(c.S + j) * u_at<HYB>(F, n, i, j - 1, k) -
+                   __ldg(c.N + j) * u_at<HYB>(F, n, i, j + 1, k) - __ldg(c.B + k) * u_at<HYB>(F, n, i, j, k - 1) -
+                   __ldg(c.T + k) * u_at<HYB>(F, n, i, j, k + 1);
   if (wbad(d)) atomicOr(err, 1);
-  u_put_all(F, n, i, j, k, r / d);
+  u_put_all<HYB>(F, n, i, j, k, r / d);
 }
 
 // ring classes: TE = 1 .. 64 threads per side (edges of m - 1 <= TE kQW points)
@@ -693,33 +699,41 @@ int upload(const std::vector<T>& v, T** out, std::string& err) {
   return 0;
 }
 
-template <int KIND, int NE, int TE, int BDMAX, int Q>
+template <int KIND, int NE, int TE, int BDMAX, int Q, int HYB = 0>
 cudaError_t allow_smem() {
-  return cudaFuncSetAttribute(wblock_kernel<KIND, NE, TE, BDMAX, Q>,
+  if (HYB == 0 && KIND != kHub) {
+    const cudaError_t e = allow_smem<KIND, NE, TE, BDMAX, Q, 1>();
+    if (e != cudaSuccess) return e;
+  }
+  if (HYB == 0 && KIND == kHub) {
+    const cudaError_t e = allow_smem<KIND, NE, TE, BDMAX, Q, 2>();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaFuncSetAttribute(wblock_kernel<KIND, NE, TE, BDMAX, Q, HYB>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)wblock_smem<NE, TE, BDMAX, Q>());
 }
 
-template <int KIND, int NE, int TE, int BDMAX, int Q>
+template <int KIND, int NE, int TE, int BDMAX, int Q, int HYB>
 void launch_blocks(const void* blocks, int nb, int n, const Coef3& c, const Fields3& F, int* err,
                    cudaStream_t s) {
   if (!nb) return;
   constexpr int BD = wblock_bd<NE, TE, BDMAX>(), BPC = wblock_bpc<NE, TE, BDMAX>();
   TMG_COUNT(1);
-  tmg::launch_pdl(wblock_kernel<KIND, NE, TE, BDMAX, Q>, dim3((nb + BPC - 1) / BPC), dim3(BD),
+  tmg::launch_pdl(wblock_kernel<KIND, NE, TE, BDMAX, Q, HYB>, dim3((nb + BPC - 1) / BPC), dim3(BD),
                   wblock_smem<NE, TE, BDMAX, Q>(), s, n, c, blocks, nb, F, err);
 }
 
-template <int TE>
+template <int TE, int HYB>
 void launch_rings(const WLevel& L, int n, const Coef3& c, int red, int k, const Fields3& F, int* err,
                   cudaStream_t s) {
-  launch_blocks<kRing, 4, TE, ring_bd(TE), kRQ>(L.rings[red][k], L.nrings[red][k], n, c, F, err, s);
+  launch_blocks<kRing, 4, TE, ring_bd(TE), kRQ, HYB>(L.rings[red][k], L.nrings[red][k], n, c, F, err, s);
 }
 
-template <int TE>
+template <int TE, int HYB>
 void launch_frames(const WLevel& L, int n, const Coef3& c, const Fields3& F, int* err,
                    cudaStream_t s) {
-  launch_blocks<kFrame, 12, TE, 12 * TE, kQW>(L.frames, L.nframes, n, c, F, err, s);
+  launch_blocks<kFrame, 12, TE, 12 * TE, kQW, HYB>(L.frames, L.nframes, n, c, F, err, s);
 }
 
 // 3D tweed hub blocks: classes by legs (2, 3, 6) and threads per leg
@@ -742,17 +756,17 @@ void merge_small_classes(std::vector<T>* cls, int nc, int ne, const int* te) {
   }
 }
 
-template <int NL>
+template <int NL, int HYB>
 void launch_hubs(const HubLevel& L, int kind, int n, const Coef3& c, int red, const Fields3& F,
                  int* err, cudaStream_t s) {
   const HubB* const* b = L.blocks[red][kind];
   const int* nb = L.nblocks[red][kind];
-  launch_blocks<kHub, NL, 1, kRBD, kQW>(b[0], nb[0], n, c, F, err, s);
-  launch_blocks<kHub, NL, 2, kRBD, kQW>(b[1], nb[1], n, c, F, err, s);
-  launch_blocks<kHub, NL, 4, kRBD, kQW>(b[2], nb[2], n, c, F, err, s);
-  launch_blocks<kHub, NL, 8, kRBD, kQW>(b[3], nb[3], n, c, F, err, s);
-  launch_blocks<kHub, NL, 16, kRBD, kQW>(b[4], nb[4], n, c, F, err, s);
-  launch_blocks<kHub, NL, 32, kRBD, kQW>(b[5], nb[5], n, c, F, err, s);
+  launch_blocks<kHub, NL, 1, kRBD, kQW, HYB>(b[0], nb[0], n, c, F, err, s);
+  launch_blocks<kHub, NL, 2, kRBD, kQW, HYB>(b[1], nb[1], n, c, F, err, s);
+  launch_blocks<kHub, NL, 4, kRBD, kQW, HYB>(b[2], nb[2], n, c, F, err, s);
+  launch_blocks<kHub, NL, 8, kRBD, kQW, HYB>(b[3], nb[3], n, c, F, err, s);
+  launch_blocks<kHub, NL, 16, kRBD, kQW, HYB>(b[4], nb[4], n, c, F, err, s);
+  launch_blocks<kHub, NL, 32, kRBD, kQW, HYB>(b[5], nb[5], n, c, F, err, s);
 }
 
 template <int NL>
@@ -850,27 +864,34 @@ long wire_blocks(const WLevel& L, int red) {
   return nb;
 }
 
-int wire_stage(const WLevel& L, int n, const Coef3& c, int red, const Fields3& F, int* err,
-               cudaStream_t s) {
-  launch_rings<1>(L, n, c, red, 0, F, err, s);
-  launch_rings<2>(L, n, c, red, 1, F, err, s);
-  launch_rings<4>(L, n, c, red, 2, F, err, s);
-  launch_rings<8>(L, n, c, red, 3, F, err, s);
-  launch_rings<16>(L, n, c, red, 4, F, err, s);
-  launch_rings<32>(L, n, c, red, 5, F, err, s);
-  launch_rings<64>(L, n, c, red, 6, F, err, s);
-  if (kRQ < 16) launch_rings<128>(L, n, c, red, 7, F, err, s);
+template <int HYB>
+void wire_stage_t(const WLevel& L, int n, const Coef3& c, int red, const Fields3& F, int* err,
+                  cudaStream_t s) {
+  launch_rings<1, HYB>(L, n, c, red, 0, F, err, s);
+  launch_rings<2, HYB>(L, n, c, red, 1, F, err, s);
+  launch_rings<4, HYB>(L, n, c, red, 2, F, err, s);
+  launch_rings<8, HYB>(L, n, c, red, 3, F, err, s);
+  launch_rings<16, HYB>(L, n, c, red, 4, F, err, s);
+  launch_rings<32, HYB>(L, n, c, red, 5, F, err, s);
+  launch_rings<64, HYB>(L, n, c, red, 6, F, err, s);
+  if (kRQ < 16) launch_rings<128, HYB>(L, n, c, red, 7, F, err, s);
   if (red && L.nframes) {
     const int emax = n - 3;  // the outermost frame's edges
-    if (emax <= 4 * kQW) launch_frames<4>(L, n, c, F, err, s);
-    else if (emax <= 16 * kQW) launch_frames<16>(L, n, c, F, err, s);
-    else launch_frames<64>(L, n, c, F, err, s);
+    if (emax <= 4 * kQW) launch_frames<4, HYB>(L, n, c, F, err, s);
+    else if (emax <= 16 * kQW) launch_frames<16, HYB>(L, n, c, F, err, s);
+    else launch_frames<64, HYB>(L, n, c, F, err, s);
   }
   if (L.npoints[red]) {
     TMG_COUNT(1);
-    tmg::launch_pdl(wpoint_kernel, dim3((L.npoints[red] + 127) / 128), dim3(128), 0, s, n, c,
+    tmg::launch_pdl(wpoint_kernel<HYB>, dim3((L.npoints[red] + 127) / 128), dim3(128), 0, s, n, c,
                     L.points[red], L.npoints[red], F, err);
   }
+}
+
+int wire_stage(const WLevel& L, int n, const Coef3& c, int red, const Fields3& F, int* err,
+               cudaStream_t s) {
+  if (F.hybrid) wire_stage_t<1>(L, n, c, red, F, err, s);
+  else wire_stage_t<0>(L, n, c, red, F, err, s);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : 3;
 }
@@ -929,18 +950,29 @@ void hub_free_level(HubLevel& L) {
   L = HubLevel();
 }
 
-int hub_stage(const HubLevel& L, int n, const Coef3& c, int red, double* u, const double* f,
-              int* err, cudaStream_t s) {
-  const Fields3 F{{u, u, u}, {f, f, f}, 0};
-  launch_hubs<2>(L, 0, n, c, red, F, err, s);
-  launch_hubs<6>(L, 1, n, c, red, F, err, s);
+template <int HYB>
+void hub_stage_t(const HubLevel& L, int n, const Coef3& c, int red, const Fields3& F, int* err,
+                 cudaStream_t s) {
+  launch_hubs<2, HYB>(L, 0, n, c, red, F, err, s);
+  launch_hubs<6, HYB>(L, 1, n, c, red, F, err, s);
   if (L.npoints[red]) {
     TMG_COUNT(1);
-    tmg::launch_pdl(wpoint_kernel, dim3((L.npoints[red] + 127) / 128), dim3(128), 0, s, n, c,
+    tmg::launch_pdl(wpoint_kernel<HYB>, dim3((L.npoints[red] + 127) / 128), dim3(128), 0, s, n, c,
                     L.points[red], L.npoints[red], F, err);
   }
+}
+
+int hub_stage(const HubLevel& L, int n, const Coef3& c, int red, const Fields3& F, int* err,
+              cudaStream_t s) {
+  if (F.hybrid) hub_stage_t<2>(L, n, c, red, F, err, s);
+  else hub_stage_t<0>(L, n, c, red, F, err, s);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : 3;
+}
+
+int hub_stage(const HubLevel& L, int n, const Coef3& c, int red, double* u, const double* f,
+              int* err, cudaStream_t s) {
+  return hub_stage(L, n, c, red, Fields3{{u, u, u}, {f, f, f}, 0}, err, s);
 }
 
 }  // namespace tmg3

@@ -169,3 +169,23 @@ def test_config4_scale_sweep(cuda, orc):
     cube.sweep(h, u, f)
     o3.sweep(o3.assemble3(x.values, x.values, x.values), uo, f.cpu().numpy(), orc.max_threads())
     assert np.abs(u.cpu().numpy() - uo).max() <= 1e-10 * np.abs(uo).max()
+
+
+@pytest.mark.gpu
+def test_hybrid_vcycle_matches_oracle(cuda, orc, monkeypatch):
+    """3D tweed V-cycle on the hybrid layout (leg-axis views, forced down to
+    n = 4) against the oracle."""
+    from paper_2110_08389_b200 import cube, mgcycle
+    monkeypatch.setenv("TMG_HYB_MIN", "4")
+    o3 = _o3()
+    n = 32
+    x = grid.make_tanh_wall(n, 1.0, 3.0)
+    h = cube.CubeHierarchy(x)
+    H = o3.Hierarchy3(x.values)
+    f = cube.config4_rhs(n, device=False)
+    cfg = mgcycle.CycleConfig(smoother="tweed", nu1=2, nu2=2)
+    ug, uo = np.zeros_like(f), np.zeros_like(f)
+    for _ in range(3):
+        cube.v_cycle(h, cfg, ug, f)
+        o3.v_cycle(H, uo, f)
+        assert np.abs(ug - uo).max() <= 1e-10 * np.abs(uo).max()
