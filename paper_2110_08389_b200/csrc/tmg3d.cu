@@ -414,6 +414,7 @@ struct tmg_cube {
   // n >= hyb_min; null elsewhere
   std::vector<double*> UI, UJ, FI, FJ;
   int hyb_min = 256;                  // levels with n >= hyb_min get the views
+  bool nat_stale = false;             // level-0 natural u behind its views (lazy cycles)
   int* err = nullptr;
   unsigned long long* dmax = nullptr;
   int* h_err = nullptr;
@@ -496,6 +497,13 @@ int convert3(tmg_cube* h, int l, int which, bool to_view, cudaStream_t s) {
   return TMG_OK;
 }
 
+// the natural level-0 u of the session, current (after lazy cycles)
+int ensure_natural(tmg_cube* h, cudaStream_t s) {
+  if (!h->nat_stale) return TMG_OK;
+  h->nat_stale = false;
+  return convert3(h, 0, 0, false, s);
+}
+
 // one sweep of level l: on the caller's natural arrays (u, f), or on the
 // session's hybrid views when use_views
 int sweep3(tmg_cube* h, int l, double* u, const double* f, cudaStream_t s, bool use_views = false) {
@@ -537,7 +545,10 @@ dim3 grid_prolong(int nc) { return dim3((nc + 255) / 256, 2 * nc - 1, 2 * nc - 1
 // sweeps and in the natural array for the transfers; on return both forms of
 // u[l0] are current.  entry: the views of l0 are to be filled first (the
 // replicated tail of the sharded cycle; a session keeps them current).
-int cycle3(tmg_cube* h, int nu1, int nu2, cudaStream_t s, int l0 = 0, bool entry = false) {
+// lazy: leave the natural u[l0] stale at the end (the session's graph; the
+// next cycle converts after its pre-smoothing, readers call ensure_natural)
+int cycle3(tmg_cube* h, int nu1, int nu2, cudaStream_t s, int l0 = 0, bool entry = false,
+           bool lazy = false) {
   const int L = (int)h->n.size();
   if (entry && l0 < L - 1 && hyb(h, l0)) {
     int st = convert3(h, l0, 0, true, s);
@@ -549,7 +560,7 @@ int cycle3(tmg_cube* h, int nu1, int nu2, cudaStream_t s, int l0 = 0, bool entry
       int st = sweep3(h, l, h->U[l], h->F[l], s, true);
       if (st) return st;
     }
-    if (hyb(h, l) && nu1 > 0) {
+    if (hyb(h, l) && (nu1 > 0 || (lazy && l == l0))) {
       int st = convert3(h, l, 0, false, s);
       if (st) return st;
     }
@@ -582,7 +593,7 @@ int cycle3(tmg_cube* h, int nu1, int nu2, cudaStream_t s, int l0 = 0, bool entry
       int st = sweep3(h, l, h->U[l], h->F[l], s, true);
       if (st) return st;
     }
-    if (hyb(h, l) && nu2 > 0) {  // natural u current for the transfers / the caller
+    if (hyb(h, l) && nu2 > 0 && !(lazy && l == l0)) {  // natural u for the transfers / the caller
       int st = convert3(h, l, 0, false, s);
       if (st) return st;
     }
@@ -735,6 +746,7 @@ int tmg_cube_load(tmg_cube* h, const double* u, const double* f, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   T3(cudaMemcpyAsync(h->U[0], u, tot * sizeof(double), cudaMemcpyDeviceToDevice, s));
   T3(cudaMemcpyAsync(h->F[0], f, tot * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  h->nat_stale = false;
   if (hyb(h, 0)) {
     int st = convert3(h, 0, 0, true, s);
     if (!st) st = convert3(h, 0, 1, true, s);
@@ -745,6 +757,7 @@ int tmg_cube_load(tmg_cube* h, const double* u, const double* f, void* stream) {
 
 int tmg_cube_store(tmg_cube* h, double* u, void* stream) {
   if (!h) return fail3(TMG_BADARG, "null cube");
+  if (int st = ensure_natural(h, (cudaStream_t)stream)) return st;
   const size_t tot = (size_t)(h->n[0] + 1) * (h->n[0] + 1) * (h->n[0] + 1);
   T3(cudaMemcpyAsync(u, h->U[0], tot * sizeof(double), cudaMemcpyDeviceToDevice,
                      (cudaStream_t)stream));
@@ -764,7 +777,7 @@ int tmg_cube_cycles(tmg_cube* h, int nu1, int nu2, int reps, void* stream) {
     cudaGraph_t g;
     const long long counted = launch_counter();
     T3(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    int st = cycle3(h, nu1, nu2, cs);
+    int st = cycle3(h, nu1, nu2, cs, 0, false, true);
     cudaError_t e = cudaStreamEndCapture(cs, &g);
     launch_counter() = counted;
     cudaStreamDestroy(cs);
@@ -789,6 +802,7 @@ int tmg_cube_cycles(tmg_cube* h, int nu1, int nu2, int reps, void* stream) {
     T3(cudaGraphLaunch(h->graph, s));
     TMG_COUNT(h->graph_kernels);
   }
+  if (reps > 0 && hyb(h, 0)) h->nat_stale = true;
   return TMG_OK;
 }
 
@@ -798,6 +812,7 @@ int tmg_cube_cycles(tmg_cube* h, int nu1, int nu2, int reps, void* stream) {
 int tmg_cube_sweeps(tmg_cube* h, int reps, void* stream) {
   if (!h) return fail3(TMG_BADARG, "null cube");
   cudaStream_t s = (cudaStream_t)stream;
+  h->nat_stale = false;  // the views are current; natural follows below
   for (int r = 0; r < reps; r++) {
     int st = sweep3(h, 0, h->U[0], h->F[0], s, true);
     if (st) return st;
@@ -810,6 +825,7 @@ int tmg_cube_sweeps(tmg_cube* h, int reps, void* stream) {
 int tmg_cube_norm(tmg_cube* h, double* out_host, void* stream) {
   if (!h) return fail3(TMG_BADARG, "null cube");
   cudaStream_t s = (cudaStream_t)stream;
+  if (int st = ensure_natural(h, s)) return st;
   T3(cudaMemsetAsync(h->dmax, 0, sizeof(unsigned long long), s));
   TMG_COUNT(1);
   defect3_kernel<<<grid3(h->n[0]), 256, 0, s>>>(h->n[0], coefs(h, 0), h->U[0], h->F[0], nullptr,
@@ -925,6 +941,7 @@ long tmg_cube_group_offsets(int scheme, int n, int g0, int g1, long long* off, l
 int tmg_cube_sweep_part(tmg_cube* h, int level, int red, int g0, int g1, void* stream) {
   int st = cube_session_level(h, level, 0);
   if (st) return st;
+  if ((st = ensure_natural(h, (cudaStream_t)stream))) return st;
   if (h->scheme != 1)
     return fail3(TMG_BADARG, "only the 3D wireframe shards (config 5); 3D tweed runs on one GPU");
   const auto key = std::make_tuple(level, g0, g1);
@@ -946,6 +963,7 @@ int tmg_cube_sweep_part(tmg_cube* h, int level, int red, int g0, int g1, void* s
 int tmg_cube_restrict(tmg_cube* h, int level, void* stream) {
   int st = cube_session_level(h, level, 1);
   if (st) return st;
+  if ((st = ensure_natural(h, (cudaStream_t)stream))) return st;
   cudaStream_t s = (cudaStream_t)stream;
   TMG_COUNT(1);
   defect_restrict3_kernel<<<grid_restrict(h->n[level]), 256, kRestrictSmem3, s>>>(
@@ -960,6 +978,7 @@ int tmg_cube_restrict(tmg_cube* h, int level, void* stream) {
 int tmg_cube_prolong(tmg_cube* h, int level, void* stream) {
   int st = cube_session_level(h, level, 1);
   if (st) return st;
+  if ((st = ensure_natural(h, (cudaStream_t)stream))) return st;
   TMG_COUNT(1);
   prolong3v2_kernel<<<grid_prolong(h->n[level + 1]), 256, 0, (cudaStream_t)stream>>>(
       h->n[level + 1], h->U[level + 1], h->U[level]);
@@ -970,6 +989,7 @@ int tmg_cube_prolong(tmg_cube* h, int level, void* stream) {
 int tmg_cube_tail(tmg_cube* h, int level, int nu1, int nu2, void* stream) {
   int st = cube_session_level(h, level, 0);
   if (st) return st;
+  if ((st = ensure_natural(h, (cudaStream_t)stream))) return st;
   if (nu1 < 0 || nu2 < 0 || nu1 + nu2 < 1) return fail3(TMG_BADARG, "need nu1 + nu2 >= 1");
   return cycle3(h, nu1, nu2, (cudaStream_t)stream, level, true);
 }
@@ -980,6 +1000,7 @@ int tmg_cube_gather(tmg_cube* h, int level, int which, const long long* off, lon
                     void* stream) {
   int st = cube_session_level(h, level, 0);
   if (st || m <= 0) return st;
+  if ((st = ensure_natural(h, (cudaStream_t)stream))) return st;
   TMG_COUNT(1);
   cube_gather_kernel<<<(unsigned)((m + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       which ? h->F[level] : h->U[level], off, m, out);
@@ -990,6 +1011,7 @@ int tmg_cube_scatter(tmg_cube* h, int level, int which, const long long* off, lo
                      const double* in, void* stream) {
   int st = cube_session_level(h, level, 0);
   if (st || m <= 0) return st;
+  if ((st = ensure_natural(h, (cudaStream_t)stream))) return st;
   TMG_COUNT(1);
   cube_scatter_kernel<<<(unsigned)((m + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       which ? h->F[level] : h->U[level], off, m, in);
@@ -1002,6 +1024,7 @@ int tmg_cube_norm_part(tmg_cube* h, int g0, int g1, double* out_host, void* stre
   int st = cube_session_level(h, 0, 0);
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
+  if ((st = ensure_natural(h, s))) return st;
   T3(cudaMemsetAsync(h->dmax, 0, sizeof(unsigned long long), s));
   TMG_COUNT(1);
   defect3_kernel<<<grid3(h->n[0]), 256, 0, s>>>(h->n[0], coefs(h, 0), h->U[0], h->F[0], nullptr,
