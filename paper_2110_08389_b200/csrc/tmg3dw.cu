@@ -523,8 +523,11 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
     sEnd[g][ed][5] = -Q1;
   }
   __syncthreads();
-  // 4. the corner rows with the edge end points substituted
-  if (KIND == kHub && live && tid % SL == 0) {
+  // 4. the corner rows with the edge end points substituted.  Rings and hubs:
+  // every thread solves the small system itself (no serial section, no
+  // barrier); frames: one thread per frame, 8 x 8 with partial pivoting.
+  double xc[4] = {0.0, 0.0, 0.0, 0.0};  // ring corners / the hub (xc[0])
+  if (KIND == kHub && live) {
     // the branch row (m_legged_thomas's closing row, tridiag.py:84-125) with
     // every leg's end point next to it substituted; the walls are known
     double m = sKd[g][0], rhs = sKr[g][0];
@@ -544,9 +547,9 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
       }
     }
     bad |= wbad(m);
-    sXc[g][0] = rhs / m;
+    xc[0] = rhs / m;
   }
-  if (KIND == kRing && live && tid % SL == 0) {
+  if (KIND == kRing && live) {
     // 4 x 4 corner system in registers (static indices): the Schur
     // complement of the diagonally dominant ring, eliminated without pivoting
     double M[4][5];
@@ -561,10 +564,10 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
     for (int eg = 0; eg < 4; eg++) {
       const int K0 = eg == 0 ? 0 : (eg == 1 ? 1 : (eg == 2 ? 3 : 0));
       const int K1 = eg == 0 ? 1 : (eg == 1 ? 2 : (eg == 2 ? 2 : 3));
-      const int x0 = (K0 == 1 || K0 == 2) ? n - B.t : B.t;  // corner coordinates along the edge
-      const int x1 = (eg & 1) ? ((K1 >= 2) ? n - B.t : B.t) : ((K1 == 1 || K1 == 2) ? n - B.t : B.t);
-      const int y0 = (eg & 1) ? ((K0 >= 2) ? n - B.t : B.t) : x0;
-      const double c0 = __ldg(c.E + y0), c1 = __ldg(c.W + x1);
+      // the corners' coordinates along the edge (b for even edges, c for odd)
+      const int y0 = (eg & 1) ? ((K0 >= 2) ? n - B.t : B.t) : ((K0 == 1 || K0 == 2) ? n - B.t : B.t);
+      const int y1 = (eg & 1) ? ((K1 >= 2) ? n - B.t : B.t) : ((K1 == 1 || K1 == 2) ? n - B.t : B.t);
+      const double c0 = __ldg(c.E + y0), c1 = __ldg(c.W + y1);
       M[K0][K0] += c0 * sEnd[g][eg][1];
       M[K0][K1] += c0 * sEnd[g][eg][2];
       M[K0][4] -= c0 * sEnd[g][eg][0];
@@ -583,14 +586,12 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
         for (int v = col; v <= 4; v++) M[q][v] -= w * M[col][v];
       }
     }
-    double xr[4];
 #pragma unroll
     for (int q = 3; q >= 0; q--) {
       double sum = M[q][4];
 #pragma unroll
-      for (int v = q + 1; v < 4; v++) sum -= M[q][v] * xr[v];
-      xr[q] = sum / M[q][q];
-      sXc[g][q] = xr[q];
+      for (int v = q + 1; v < 4; v++) sum -= M[q][v] * xc[v];
+      xc[q] = sum / M[q][q];
     }
   }
   if (KIND == kFrame && live && tid % SL == 0) {
@@ -637,17 +638,22 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
       sXc[g][q] = sum / M[q][q];
     }
   }
-  __syncthreads();
+  if (KIND == kFrame) __syncthreads();  // the frame's corners from its solver thread
+  auto corner_val = [&](int K) {
+    if (KIND == kFrame) return sXc[g][K];
+    if (KIND == kHub) return K == 0 ? xc[0] : sXc[g][K];
+    return K == 0 ? xc[0] : (K == 1 ? xc[1] : (K == 2 ? xc[2] : xc[3]));
+  };
   if (live && tid % SL < (KIND == kHub ? 1 : NK)) {  // hubs: the walls stay
     int P3[3];
     corner_pos<KIND, NE>(B, n, tid % SL, P3);
-    u_put_all<HYB>(F, n, P3[0], P3[1], P3[2], sXc[g][tid % SL]);
+    u_put_all<HYB>(F, n, P3[0], P3[1], P3[2], corner_val(tid % SL));
   }
   // 5. finalise every chunk with both ends known, then scatter
   if (cnt > 0) {
     int x, K0, K1;
     edge_def<KIND, NE>(B, ed, x, K0, K1);
-    const double xa = sXc[g][K0], xb = sXc[g][K1];
+    const double xa = corner_val(K0), xb = corner_val(K1);
     const double XE = P - Q0 * xa - Q1 * xb;
     const double XL = lt == 0 ? xa : sD[tid - 1] - sH0[tid - 1] * xa - sH1[tid - 1] * xb;
     chunk_finalise<Q>(rr, p0, e, XL, XE, mu, amq);
