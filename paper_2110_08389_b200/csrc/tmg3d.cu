@@ -306,9 +306,10 @@ __device__ __forceinline__ int owner_h(int n, int i, int j, int k, bool smallest
 template <int V, bool TO_VIEW, bool SMALL>
 __global__ void __launch_bounds__(256) hybrid_kernel(int n, double* __restrict__ nat,
                                                      double* __restrict__ view, int mask) {
-  __shared__ double t[32][33];
+  constexpr int NF = 4;  // fixed-index planes per CTA: their tile loads are in flight together
+  __shared__ double t[NF][32][33];
   pdl_trigger();
-  const int kt = blockIdx.x * 32, fx = blockIdx.y, at = blockIdx.z * 32;  // fx: j (V = 0) or i (V = 1)
+  const int kt = blockIdx.x * 32, at = blockIdx.z * 32;
   const size_t n1 = (size_t)n + 1;
   const int lane = threadIdx.x & 31, row = threadIdx.x >> 5;
   // tile test on the mirrored coordinates (negated for SMALL, the 3D tweed):
@@ -321,15 +322,23 @@ __global__ void __launch_bounds__(256) hybrid_kernel(int n, double* __restrict__
   const int mk = SMALL ? -((kt <= n / 2 && n / 2 <= k1) ? n / 2
                                                         : max((int)mirror(kt, n), (int)mirror(k1, n)))
                        : min((int)mirror(kt, n), (int)mirror(k1, n));
-  const int mf = sg * (int)mirror(fx, n);
   const bool strict = !(TO_VIEW && mask == 1);
-  if (strict ? (ma <= mf || ma <= mk) : (ma < mf || ma < mk)) return;
+  bool any = false;
+  bool use[NF];
+#pragma unroll
+  for (int q = 0; q < NF; q++) {
+    const int fx = blockIdx.y * NF + q;
+    const int mf = sg * (int)mirror(min(fx, n), n);
+    use[q] = fx <= n && (strict ? (ma > mf && ma > mk) : (ma >= mf && ma >= mk));
+    any |= use[q];
+  }
+  if (!any) return;
   pdl_wait();
-  auto nat_off = [&](int a, int k) {
+  auto nat_off = [&](int fx, int a, int k) {
     return V == 0 ? ((size_t)a * n1 + fx) * n1 + k : ((size_t)fx * n1 + a) * n1 + k;
   };
-  auto view_off = [&](int a, int k) { return ((size_t)fx * n1 + k) * n1 + a; };
-  auto sel = [&](int a, int k) {
+  auto view_off = [&](int fx, int a, int k) { return ((size_t)fx * n1 + k) * n1 + a; };
+  auto sel = [&](int fx, int a, int k) {
     const int i = V == 0 ? a : fx, j = V == 0 ? fx : a;
     if (!strict) {
       const int mv = sg * (int)mirror(a, n), mo = max(sg * (int)mirror(fx, n), sg * (int)mirror(k, n));
@@ -337,25 +346,45 @@ __global__ void __launch_bounds__(256) hybrid_kernel(int n, double* __restrict__
     }
     return owner_h(n, i, j, k, SMALL) == V;
   };
-  if (TO_VIEW) {
-    for (int r = row; r < 32; r += 8) {
-      const int a = at + r, k = kt + lane;
-      if (a <= n && k <= n) t[r][lane] = nat[nat_off(a, k)];
+  double r[NF][4];
+#pragma unroll
+  for (int q = 0; q < NF; q++) {
+    const int fx = blockIdx.y * NF + q;
+#pragma unroll
+    for (int m = 0; m < 4; m++) {
+      const int rr = row + 8 * m;
+      if (TO_VIEW) {
+        const int a = at + rr, k = kt + lane;
+        r[q][m] = (use[q] && a <= n && k <= n) ? nat[nat_off(fx, a, k)] : 0.0;
+      } else {
+        const int k = kt + rr, a = at + lane;
+        r[q][m] = (use[q] && a <= n && k <= n) ? view[view_off(fx, a, k)] : 0.0;
+      }
     }
-    __syncthreads();
-    for (int r = row; r < 32; r += 8) {
-      const int k = kt + r, a = at + lane;
-      if (a <= n && k <= n && sel(a, k)) view[view_off(a, k)] = t[lane][r];
+  }
+#pragma unroll
+  for (int q = 0; q < NF; q++)
+#pragma unroll
+    for (int m = 0; m < 4; m++) {
+      const int rr = row + 8 * m;
+      if (TO_VIEW) t[q][rr][lane] = r[q][m];
+      else t[q][lane][rr] = r[q][m];
     }
-  } else {
-    for (int r = row; r < 32; r += 8) {
-      const int k = kt + r, a = at + lane;
-      if (a <= n && k <= n) t[lane][r] = view[view_off(a, k)];
-    }
-    __syncthreads();
-    for (int r = row; r < 32; r += 8) {
-      const int a = at + r, k = kt + lane;
-      if (a <= n && k <= n && sel(a, k)) nat[nat_off(a, k)] = t[r][lane];
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NF; q++) {
+    if (!use[q]) continue;
+    const int fx = blockIdx.y * NF + q;
+#pragma unroll
+    for (int m = 0; m < 4; m++) {
+      const int rr = row + 8 * m;
+      if (TO_VIEW) {
+        const int k = kt + rr, a = at + lane;
+        if (a <= n && k <= n && sel(fx, a, k)) view[view_off(fx, a, k)] = t[q][lane][rr];
+      } else {
+        const int a = at + rr, k = kt + lane;
+        if (a <= n && k <= n && sel(fx, a, k)) nat[nat_off(fx, a, k)] = t[q][rr][lane];
+      }
     }
   }
 }
@@ -473,7 +502,7 @@ bool hyb(const tmg_cube* h, int l) { return l < (int)h->UI.size() && h->UI[l]; }
 // hybrid <-> natural for level l: which = 0 u, 1 f
 int convert3(tmg_cube* h, int l, int which, bool to_view, cudaStream_t s) {
   const int n = h->n[l];
-  const dim3 grid((n + 32) / 32, n + 1, (n + 32) / 32);
+  const dim3 grid((n + 32) / 32, (n + 4) / 4, (n + 32) / 32);  // 4 fixed-index planes per CTA
   double* nat = which ? h->F[l] : h->U[l];
   double* v0 = which ? h->FI[l] : h->UI[l];
   double* v1 = which ? h->FJ[l] : h->UJ[l];
