@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) defect3_kernel(int n, Coef3 c, const doub
 // (defect3_kernel's arithmetic) into shared memory and folds them into the
 // coarse points in the oracle's order (orc3_restrict: a, b, e nested), while
 // u and f are read once (16 B per fine point, no defect field in HBM).
-constexpr int kRTJ = 8, kRTK = 32;                          // coarse tile
+constexpr int kRTJ = 8, kRTK = 31;                          // coarse tile (63 fine columns: 4 x 63 threads)
 constexpr int kRDJ = 2 * kRTJ + 1, kRDK = 2 * kRTK + 1;     // fine defects
 constexpr int kRUJ = kRDJ + 2, kRUK = kRDK + 2;             // u with halo
 
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(256, 3) defect_restrict3_kernel(int nf, Coef3 
   // per-thread element offsets within a plane (fixed for every plane): u
   // tile elements t = tid + 256 m, f / defect elements likewise; -1 = outside
   constexpr int PU = (kRU + 255) / 256, PD = (kRD + 255) / 256;
-  int uo[PU], fo[PD], so[PD];
+  int uo[PU], fo[PD];
 #pragma unroll
   for (int m = 0; m < PU; m++) {
     const int t = tid + 256 * m, r = t / kRUK, q = t - r * kRUK;
@@ -158,10 +158,14 @@ __global__ void __launch_bounds__(256, 3) defect_restrict3_kernel(int nf, Coef3 
   for (int m = 0; m < PD; m++) {
     const int t = tid + 256 * m, r = t / kRDK, q = t - r * kRDK;
     const int j = jd0 + r, k = kd0 + q;
-    const bool in = t < kRD && j < nf && k < nf;
-    fo[m] = in ? j * (nf + 1) + k : -1;
-    so[m] = t < kRD ? (r + 1) * kRUK + (q + 1) : 0;
+    fo[m] = (t < kRD && j < nf && k < nf) ? j * (nf + 1) + k : -1;
   }
+  // defect mapping: a thread per fine column q and a run of rows (a sliding
+  // window down the column: one new u load per row)
+  static_assert(4 * kRDK <= 256 && kRDJ == 17, "defect mapping");
+  const int dq = tid % kRDK, dg = tid / kRDK;
+  const int dr0 = dg == 0 ? 0 : 1 + 4 * dg, dr1 = dg == 0 ? 5 : 5 + 4 * dg;  // rows [dr0, dr1)
+  const bool dlive = dg < 4 && kd0 + dq < nf;
   const size_t plane = n1 * n1;
   auto issue_u = [&](int i) {  // plane i (0 .. nf) into slot i % 4
     double* dst = su + (i & 3) * kRU;
@@ -199,7 +203,7 @@ __global__ void __launch_bounds__(256, 3) defect_restrict3_kernel(int nf, Coef3 
   issue_f(2 * I0);
   cp_async_commit();
   const int tj = tid / kRTK, tk = tid % kRTK, J = J0 + tj, K = K0 + tk;
-  const bool own = J < nc && K < nc;
+  const bool own = tid < kRTJ * kRTK && J < nc && K < nc;
   double acc = 0.0;
   for (int i = 2 * I0 - 1; i <= 2 * I1 - 1; i++) {
     cp_async_wait1();  // u planes up to i + 1 and f plane i have landed
@@ -209,25 +213,35 @@ __global__ void __launch_bounds__(256, 3) defect_restrict3_kernel(int nf, Coef3 
     const double* up = su + ((i + 1) & 3) * kRU;
     const double* fc = sf + (i & 1) * kRD;
     const double Wi = __ldg(c.W + i), Ei = __ldg(c.E + i);
+    if (dlive) {
+      const double Bk = cB[dq], Tk = cT[dq];
+      int o = (dr0 + 1) * kRUK + (dq + 1);
+      double up_c = uc[o - kRUK], cur = uc[o];
 #pragma unroll
-    for (int m = 0; m < PD; m++) {
-      const int t = tid + 256 * m;
-      if (t >= kRD) continue;
-      double v = 0.0;
-      if (fo[m] >= 0) {
-        const int o = so[m], r = o / kRUK - 1, q = o - (r + 1) * kRUK - 1;
-        const double Sj = cS[r], Nj = cN[r], Bk = cB[q], Tk = cT[q];
-        const double cc = -(Wi + Ei + Sj + Nj + Bk + Tk);
-        double a = __dmul_rn(Wi, um[o]);
-        a = __dadd_rn(a, __dmul_rn(Ei, up[o]));
-        a = __dadd_rn(a, __dmul_rn(Sj, uc[o - kRUK]));
-        a = __dadd_rn(a, __dmul_rn(Nj, uc[o + kRUK]));
-        a = __dadd_rn(a, __dmul_rn(Bk, uc[o - 1]));
-        a = __dadd_rn(a, __dmul_rn(Tk, uc[o + 1]));
-        a = __dadd_rn(a, __dmul_rn(cc, uc[o]));
-        v = __dadd_rn(fc[t], -a);
+      for (int r = 0; r < 5; r++) {
+        const int rr = dr0 + r;
+        if (rr >= dr1) break;
+        const double nxt = uc[o + kRUK];
+        double v = 0.0;
+        if (jd0 + rr < nf) {
+          const double Sj = cS[rr], Nj = cN[rr];
+          const double cc = -(Wi + Ei + Sj + Nj + Bk + Tk);
+          double a = __dmul_rn(Wi, um[o]);
+          a = __dadd_rn(a, __dmul_rn(Ei, up[o]));
+          a = __dadd_rn(a, __dmul_rn(Sj, up_c));
+          a = __dadd_rn(a, __dmul_rn(Nj, nxt));
+          a = __dadd_rn(a, __dmul_rn(Bk, uc[o - 1]));
+          a = __dadd_rn(a, __dmul_rn(Tk, uc[o + 1]));
+          a = __dadd_rn(a, __dmul_rn(cc, cur));
+          v = __dadd_rn(fc[rr * kRDK + dq], -a);
+        }
+        sd[rr * kRDK + dq] = v;
+        up_c = cur;
+        cur = nxt;
+        o += kRUK;
       }
-      sd[t] = v;
+    } else if (dg < 4) {
+      for (int rr = dr0; rr < dr1; rr++) sd[rr * kRDK + dq] = 0.0;
     }
     __syncthreads();  // defects complete; u plane i-1 and f plane i are free
     if (i + 3 <= 2 * I1) issue_u(i + 3);
