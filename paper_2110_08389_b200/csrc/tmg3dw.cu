@@ -39,6 +39,12 @@
 namespace tmg3 {
 namespace {
 
+#ifndef TMG_WMINB
+#define TMG_WMINB 2
+#endif
+#ifndef TMG_SKEL
+#define TMG_SKEL 0
+#endif
 #ifndef TMG_WNB
 #define TMG_WNB 4
 #endif
@@ -329,7 +335,7 @@ constexpr size_t wblock_smem() {
 // threads per edge.  `blocks`: Ring3 (rings), int shell (frames) or HubB
 // (3D tweed hub blocks).
 template <int KIND, int NE, int TE, int BDMAX, int Q, int HYB>
-__global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1 : 2)
+__global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1 : TMG_WMINB)
     wblock_kernel(int n, Coef3 c, const void* __restrict__ blocks, int nb, Fields3 F, int* err) {
   constexpr int NK = ncorners<KIND, NE>();
   constexpr int SL = NE * TE;  // threads per block
@@ -421,6 +427,10 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
     }
   }
   __syncthreads();
+#if TMG_SKEL
+  bool bad = false;
+  if (KIND != kRing) {
+#endif
   // 2. chunk eliminations
   const EdgeCpl<Q> cpl{G, tlo, thi};
   const int p0 = lt * Q;
@@ -658,6 +668,9 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
     const double XL = lt == 0 ? xa : sD[tid - 1] - sH0[tid - 1] * xa - sH1[tid - 1] * xb;
     chunk_finalise<Q>(rr, p0, e, XL, XE, mu, amq);
   }
+#if TMG_SKEL
+  }
+#endif
   __syncthreads();
   tmg::pdl_trigger();  // the successor may launch while this CTA scatters
 #pragma unroll 4
