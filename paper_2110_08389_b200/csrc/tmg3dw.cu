@@ -429,6 +429,18 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
   __syncthreads();
 #if TMG_SKEL
   bool bad = false;
+#if TMG_SKEL == 2  // + three factor streams of 8 B per point (the factorised-solve estimate)
+  if (KIND == kRing && L > 0) {
+    double acc = 0.0;
+    const int p0s = lt * Q;
+    const double* src = G.f + G.o0 + 1;
+#pragma unroll
+    for (int k = 0; k < Q; k++)
+      if (p0s + k < L) acc += __ldg(src + p0s + k) + __ldg(src + ((p0s + k + 7) % L)) * 0.5 +
+                              __ldg(src + ((p0s + k + 13) % L)) * 0.25;
+    if (p0s < L) rr[rsw<Q>(p0s)] += acc * 1e-300;
+  }
+#endif
   if (KIND != kRing) {
 #endif
   // 2. chunk eliminations
