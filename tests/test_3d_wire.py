@@ -185,3 +185,53 @@ def test_hybrid_vcycle_matches_oracle(cuda, orc, monkeypatch, n):
     _, rep = cube.solve(h, cfg, f)
     _, repo = o3.solve(H, f)
     assert rep.cycles == repo.cycles and rep.converged == repo.converged
+
+
+@pytest.mark.gpu
+def test_cube_argument_errors(cuda):
+    """Shape, scheme and size errors map to ValueError (the C ABI's
+    TMG_BADARG), before any device work."""
+    from paper_2110_08389_b200 import cube, mgcycle
+    x = configs.sinh_centre(8, 1.0, 3.0)
+    with pytest.raises(ValueError):
+        cube.CubeHierarchy(configs.sinh_centre(7, 1.0, 3.0), scheme="wireframe")
+    with pytest.raises(ValueError):
+        cube.CubeHierarchy(x, scheme="checkerboard")
+    with pytest.raises(ValueError):  # rings longer than 64 threads x 16 points
+        cube.CubeHierarchy(np.linspace(0.0, 1.0, 1031), scheme="wireframe")
+    h = cube.CubeHierarchy(x, scheme="wireframe")
+    with pytest.raises(ValueError):
+        cube.sweep(h, np.zeros((8, 9, 9)), np.zeros((9, 9, 9)))
+    with pytest.raises(ValueError):
+        cube.v_cycle(h, mgcycle.CycleConfig(smoother="tweed"), np.zeros((9,) * 3), np.zeros((9,) * 3))
+
+
+@pytest.mark.gpu
+def test_sweeps_entry_matches_single_sweeps(cuda, orc):
+    """tmg_cube_sweeps (session sweeps on the hybrid views, forced here) equals
+    repeated natural sweeps of the same fields."""
+    import ctypes
+    import os
+    import torch
+    from paper_2110_08389_b200 import _lib, cube
+    n = 32
+    x = configs.sinh_centre(n, 1.0, 3.0)
+    os.environ["TMG_HYB_MIN"] = "4"
+    try:
+        h = cube.CubeHierarchy(x, scheme="wireframe")
+    finally:
+        del os.environ["TMG_HYB_MIN"]
+    rng = np.random.default_rng(3)
+    u0 = np.zeros((n + 1,) * 3)
+    u0[1:-1, 1:-1, 1:-1] = rng.standard_normal((n - 1,) * 3)
+    f = rng.standard_normal((n + 1,) * 3)
+    ud, fd = torch.from_numpy(u0).cuda(), torch.from_numpy(f).cuda()
+    L, s = _lib.lib(), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    cube._check(L.tmg_cube_load(h._h, ctypes.c_void_p(ud.data_ptr()), ctypes.c_void_p(fd.data_ptr()), s))
+    cube._check(L.tmg_cube_sweeps(h._h, 3, s))
+    out = torch.empty_like(ud)
+    cube._check(L.tmg_cube_store(h._h, ctypes.c_void_p(out.data_ptr()), s))
+    ref = u0.copy()
+    for _ in range(3):
+        cube.sweep(h, ref, f)
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
