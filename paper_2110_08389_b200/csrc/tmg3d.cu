@@ -268,32 +268,44 @@ __global__ void __launch_bounds__(256, 3) defect_restrict3_kernel(int nf, Coef3 
   }
 }
 
-// u += trilinear P uc on the fine interior: a thread per fine (i, j) and
-// coarse column K, writing fine k = 2K-1 and 2K; sums in orc3_prolong_add's
-// order (a, b, e nested), consecutive lanes on consecutive fine k pairs
+// u += trilinear P uc on the fine interior: a thread per fine i, coarse row
+// Jc and coarse column K, writing the 2 x 2 fine points j = 2Jc-1, 2Jc and
+// k = 2K-1, 2K from the 2 x 2 (x 2 in i) coarse values they share; sums in
+// orc3_prolong_add's order (a, b, e nested), lanes along K
 __global__ void __launch_bounds__(256) prolong3v2_kernel(int nc, const double* __restrict__ uc,
                                                          double* __restrict__ u) {
   pdl_trigger();
   pdl_wait();
   const int nf = 2 * nc;
   const int K = 1 + blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = 1 + blockIdx.y, i = 1 + blockIdx.z;
+  const int Jc = 1 + blockIdx.y, i = 1 + blockIdx.z;
   if (K > nc) return;
-  const int I = i / 2, J = j / 2, oi = i & 1, oj = j & 1;
+  const int I = i / 2, oi = i & 1;
   const size_t c1 = (size_t)nc + 1;
-  double ao = 0.0, ae = 0.0;
-  for (int a = 0; a <= oi; a++)
-    for (int b = 0; b <= oj; b++) {
-      const size_t o = ((size_t)(I + a) * c1 + (J + b)) * c1;
-      const double v0 = __ldg(uc + o + K - 1), v1 = __ldg(uc + o + K);
-      ao += v0;
-      ao += v1;
-      ae += v1;
-    }
-  const double wo = 1.0 / (double)((1 + oi) * (1 + oj) * 2), we = 1.0 / (double)((1 + oi) * (1 + oj));
-  const size_t of = ((size_t)i * (nf + 1) + j) * (nf + 1);
-  u[of + 2 * K - 1] += ao * wo;
-  if (2 * K < nf) u[of + 2 * K] += ae * we;
+  double oo = 0.0, oe = 0.0, eo = 0.0, ee = 0.0;  // (j odd / even, k odd / even)
+  for (int a = 0; a <= oi; a++) {
+    const size_t r0 = ((size_t)(I + a) * c1 + (Jc - 1)) * c1, r1 = r0 + c1;
+    const double v00 = __ldg(uc + r0 + K - 1), v01 = __ldg(uc + r0 + K);
+    const double v10 = __ldg(uc + r1 + K - 1), v11 = __ldg(uc + r1 + K);
+    oo += v00;
+    oo += v01;
+    oo += v10;
+    oo += v11;
+    oe += v01;
+    oe += v11;
+    eo += v10;
+    eo += v11;
+    ee += v11;
+  }
+  const double w1 = 1.0 / (double)(1 + oi);
+  const size_t n1 = (size_t)nf + 1;
+  const size_t ro = ((size_t)i * n1 + (2 * Jc - 1)) * n1, re = ro + n1;
+  u[ro + 2 * K - 1] += oo * (w1 / 4.0);
+  if (2 * K < nf) u[ro + 2 * K] += oe * (w1 / 2.0);
+  if (2 * Jc < nf) {
+    u[re + 2 * K - 1] += eo * (w1 / 2.0);
+    if (2 * K < nf) u[re + 2 * K] += ee * w1;
+  }
 }
 
 // ---- hybrid layout of the 3D wireframe V-cycle ------------
@@ -582,7 +594,7 @@ dim3 grid_restrict(int nf) {
   const int m = nf / 2 - 1, ti = restrict_ti(nf);  // interior coarse points per axis
   return dim3((m + kRTK - 1) / kRTK, (m + kRTJ - 1) / kRTJ, (m + ti - 1) / ti);
 }
-dim3 grid_prolong(int nc) { return dim3((nc + 255) / 256, 2 * nc - 1, 2 * nc - 1); }
+dim3 grid_prolong(int nc) { return dim3((nc + 255) / 256, nc, 2 * nc - 1); }
 
 // The V-cycle from level l0.  Hybrid levels keep u in the views during the
 // sweeps and in the natural array for the transfers; on return both forms of
