@@ -30,6 +30,7 @@
 // The solve is exact for the block (the reference's block Gauss-Seidel
 // step); only the elimination order differs from the circulant Thomas.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -778,7 +779,11 @@ template <class T>
 void merge_small_classes(std::vector<T>* cls, int nc, int ne, const int* te) {
   for (int q = 0; q + 1 < nc; q++) {
     const size_t per_cta = std::max(1, kRBD / (ne * te[q]));
-    if (cls[q].empty() || cls[q].size() >= 2 * 148 * per_cta) continue;
+    static const int waves = [] {
+      const char* e = getenv("TMG_MERGE_WAVES");  // A/B knob: launch waves below which a class folds
+      return e ? atoi(e) : 2;
+    }();
+    if (cls[q].empty() || cls[q].size() >= (size_t)waves * 148 * per_cta) continue;
     int nxt = q + 1;
     while (nxt + 1 < nc && cls[nxt].empty()) nxt++;
     if (cls[nxt].empty()) continue;  // the largest non-empty class stays
