@@ -946,8 +946,10 @@ int hub_build_level(int n, const std::vector<HubB> blocks[2], HubLevel& L, std::
     std::vector<HubB> cls[kHubKinds][kHubClasses];
     std::vector<int4> pts;
     for (const HubB& B : blocks[red]) {
-      if (B.len == 0) {  // a branch without legs: a point block
-        pts.push_back(make_int4(B.bi, B.bj, B.bk, 0));
+      if (B.len == 0) {  // a branch without legs: a point block, run as a hub with no legs
+        HubB P = B;        // in the 6-leg kernels (its row alone: one launch less per stage)
+        P.nleg = 0;
+        cls[1][0].push_back(P);
         continue;
       }
       if (B.nleg != 2 && B.nleg != 3 && B.nleg != 6) {
