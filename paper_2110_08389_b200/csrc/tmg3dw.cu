@@ -483,16 +483,17 @@ __global__ void __launch_bounds__(wblock_bd<NE, TE, BDMAX>(), KIND == kFrame ? 1
       A = 0.0;
     }
   }
-  // PCR over the edge's TE chunk ends: steps within a warp by shuffles
-  // (an edge of TE <= 32 threads is one aligned lane segment), the step
-  // across the two warps of a 64-thread edge through shared memory
+  // PCR over the edge's TE chunk ends: by shuffles when the edge is one
+  // aligned lane segment of a warp (TE <= 32), through shared memory when it
+  // spans two warps (TE = 64: a lane's partner at distance dd may sit in the
+  // other warp for every dd)
   constexpr int WS = TE < 32 ? TE : 32;
   constexpr unsigned FULL = 0xffffffffu;
 #pragma unroll
   for (int dd = 1; dd < TE; dd <<= 1) {
     double Am = 0, Bm = 1, Cm = 0, Dm = 0, Gm = 0, Hm = 0, Ap = 0, Bp = 1, Cp = 0, Dp = 0, Gp = 0,
            Hp = 0;
-    if (dd < 32) {
+    if (TE <= 32) {  // the edge is one lane segment of a warp
       const double a1 = __shfl_up_sync(FULL, A, dd, WS), b1 = __shfl_up_sync(FULL, Bv, dd, WS);
       const double c1 = __shfl_up_sync(FULL, Cc, dd, WS), d1 = __shfl_up_sync(FULL, D, dd, WS);
       const double g1 = __shfl_up_sync(FULL, H0, dd, WS), h1 = __shfl_up_sync(FULL, H1, dd, WS);
@@ -714,6 +715,14 @@ __global__ void __launch_bounds__(128) wpoint_kernel(int n, Coef3 c, const int4*
   u_put_all<HYB>(F, n, i, j, k, r / d);
 }
 
+// test knob: TMG_FORCE_TE=t runs rings and frames with at least t threads
+// per edge (small grids then exercise the wide classes, e.g. the two-warp
+// PCR of TE = 64)
+int force_te() {
+  const char* e = getenv("TMG_FORCE_TE");
+  return e ? atoi(e) : 0;
+}
+
 // ring classes: TE = 1 .. 64 threads per side (edges of m - 1 <= TE kQW points)
 constexpr int kTE[kRingClasses] = {1, 2, 4, 8, 16, 32, 64, 128};
 constexpr int ring_bd(int te) { return 4 * te > kRBD ? 4 * te : kRBD; }
@@ -830,6 +839,7 @@ int wire_build_level(int n, WLevel& L, std::string& err, int g0, int g1) {
   // the same face: order (a, xa, t).  On faces normal to k they are the
   // faces of shells s1 +- 1, s1 +- 2: order (a, t, xa).
   std::vector<Ring3> rg[2][kRingClasses];
+  const int fte = force_te();
   for (int a = 0; a < 3; a++)
     for (int outer = 1; outer < n; outer++)
       for (int inner = 1; inner < n; inner++) {
@@ -839,7 +849,7 @@ int wire_build_level(int n, WLevel& L, std::string& err, int g0, int g1) {
         if (s1 >= t || s1 < g0 || s1 >= g1) continue;  // the ring's sharding group is s1
         const int side = n - 2 * t - 1;  // points between two corners
         int cls = 0;
-        while (cls < kRingClasses - 1 && kTE[cls] * kRQ < side) cls++;
+        while (cls < kRingClasses - 1 && (kTE[cls] * kRQ < side || kTE[cls] < fte)) cls++;
         const int red = ((s1 + t) % 2) == 0;
         rg[red][cls].push_back(Ring3{(int16_t)a, (int16_t)t, xa});
       }
@@ -912,7 +922,7 @@ void wire_stage_t(const WLevel& L, int n, const Coef3& c, int red, const Fields3
   launch_rings<64, HYB>(L, n, c, red, 6, F, err, s);
   if (kRQ < 16) launch_rings<128, HYB>(L, n, c, red, 7, F, err, s);
   if (red && L.nframes) {
-    const int emax = n - 3;  // the outermost frame's edges
+    const int emax = std::max(n - 3, force_te() * kQW);  // the outermost frame's edges
     if (emax <= 4 * kQW) launch_frames<4, HYB>(L, n, c, F, err, s);
     else if (emax <= 16 * kQW) launch_frames<16, HYB>(L, n, c, F, err, s);
     else launch_frames<64, HYB>(L, n, c, F, err, s);

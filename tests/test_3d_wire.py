@@ -188,6 +188,38 @@ def test_hybrid_vcycle_matches_oracle(cuda, orc, monkeypatch, n):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("te", [32, 64])
+@pytest.mark.parametrize("hyb", ["4", "100000"])
+def test_wide_classes_match_oracle(cuda, orc, monkeypatch, te, hyb):
+    """Rings and frames forced into the wide launch classes (TE threads per
+    edge: 64 spans two warps, the PCR path of the 1025^3 cube) on a small
+    cube, natural and hybrid, against the oracle."""
+    from paper_2110_08389_b200 import cube, mgcycle
+    monkeypatch.setenv("TMG_FORCE_TE", str(te))
+    monkeypatch.setenv("TMG_HYB_MIN", hyb)
+    o3 = _o3()
+    n = 32
+    x = configs.sinh_centre(n, 1.0, 3.0)
+    h = cube.CubeHierarchy(x, scheme="wireframe")
+    rng = np.random.default_rng(9)
+    u = np.zeros((n + 1,) * 3)
+    u[1:-1, 1:-1, 1:-1] = rng.standard_normal((n - 1,) * 3)
+    f = rng.standard_normal((n + 1,) * 3)
+    ug, uo = u.copy(), u.copy()
+    cube.sweep(h, ug, f)
+    o3.sweep(o3.assemble3(x.values, x.values, x.values), uo, f, scheme="wireframe")
+    assert np.abs(ug - uo).max() <= 1e-12 * np.abs(uo).max()
+    H = o3.Hierarchy3(x.values, scheme="wireframe")
+    fc = cube.config5_rhs(n, device=False)
+    cfg = mgcycle.CycleConfig(smoother="wireframe", nu1=2, nu2=2)
+    ug, uo = np.zeros_like(fc), np.zeros_like(fc)
+    for _ in range(2):
+        cube.v_cycle(h, cfg, ug, fc)
+        o3.v_cycle(H, uo, fc)
+        assert np.abs(ug - uo).max() <= 1e-10 * np.abs(uo).max()
+
+
+@pytest.mark.gpu
 def test_cube_argument_errors(cuda):
     """Shape, scheme and size errors map to ValueError (the C ABI's
     TMG_BADARG), before any device work."""
@@ -235,3 +267,57 @@ def test_sweeps_entry_matches_single_sweeps(cuda, orc):
     for _ in range(3):
         cube.sweep(h, ref, f)
     assert np.abs(out.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.gpu
+def test_config5_full_size_properties(cuda):
+    """BASELINE config 5 at its full 1025^3 size, where the CPU oracle is too
+    slow to run in a test, through size-independent properties: the session's
+    hybrid-view sweep equals the natural-layout sweep (1e-12), one sweep is
+    affine in f (S(u, f1 + f2) - S(u, f1) = S(0, f2) - S(0, 0), S(0, 0) = 0 on
+    the homogeneous Dirichlet cube), and V(2,2) cycles reduce the defect at
+    the factor the bench reports (rho < 0.9)."""
+    import ctypes
+    import torch
+    from paper_2110_08389_b200 import _lib, cube
+    n = 1024
+    x = configs.sinh_centre(n, 1.0, 3.0)
+    h = cube.CubeHierarchy(x, scheme="wireframe")
+    L, s = _lib.lib(), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    f1 = cube.config5_rhs(n)
+    f2 = torch.roll(f1, shifts=(3, 5, 7), dims=(0, 1, 2)) * 0.5
+    f2[0], f2[-1], f2[:, 0], f2[:, -1], f2[:, :, 0], f2[:, :, -1] = 0, 0, 0, 0, 0, 0
+    u = f1 * 0.25
+    # hybrid session sweep vs natural sweep
+    cube._check(L.tmg_cube_load(h._h, P(u), P(f1), s))
+    cube._check(L.tmg_cube_sweeps(h._h, 1, s))
+    hyb = torch.empty_like(u)
+    cube._check(L.tmg_cube_store(h._h, P(hyb), s))
+    nat = u.clone()
+    cube._check(L.tmg_cube_sweep(h._h, P(nat), P(f1), s))
+    scale = nat.abs().max().item()
+    assert (hyb - nat).abs().max().item() <= 1e-12 * scale
+    del hyb
+    # affine in f
+    a = u.clone()
+    cube._check(L.tmg_cube_sweep(h._h, P(a), P(f1 + f2), s))
+    a -= nat
+    del nat
+    b = torch.zeros_like(u)
+    cube._check(L.tmg_cube_sweep(h._h, P(b), P(f2), s))
+    # a is a difference of O(scale) sweeps: rounding relative to their size
+    assert (a - b).abs().max().item() <= 1e-12 * scale
+    del a, b
+    # convergence of the hybrid V-cycle
+    z = torch.zeros_like(u)
+    cube._check(L.tmg_cube_load(h._h, P(z), P(f1), s))
+    out = ctypes.c_double()
+    cube._check(L.tmg_cube_norm(h._h, ctypes.byref(out), s))
+    norms = [out.value]
+    for _ in range(3):
+        cube._check(L.tmg_cube_cycles(h._h, 2, 2, 1, s))
+        cube._check(L.tmg_cube_norm(h._h, ctypes.byref(out), s))
+        norms.append(out.value)
+    ratios = [q / p for p, q in zip(norms, norms[1:])]
+    assert all(r < 0.9 for r in ratios), ratios
