@@ -952,6 +952,7 @@ int hub_build_level(int n, const std::vector<HubB> blocks[2], HubLevel& L, std::
     err = "3D tweed cubes above " + std::to_string(kMaxN) + " intervals are not supported";
     return 2;
   }
+  const int fte = force_te();
   for (int red = 0; red < 2; red++) {
     std::vector<HubB> cls[kHubKinds][kHubClasses];
     std::vector<int4> pts;
@@ -968,7 +969,7 @@ int hub_build_level(int n, const std::vector<HubB> blocks[2], HubLevel& L, std::
       }
       const int kind = B.nleg == 2 ? 0 : 1;
       int q = 0;
-      while (q < kHubClasses - 1 && kHubTE[q] * kQW < B.len) q++;
+      while (q < kHubClasses - 1 && (kHubTE[q] * kQW < B.len || kHubTE[q] < fte)) q++;
       cls[kind][q].push_back(B);
     }
     for (int k = 0; k < kHubKinds; k++) merge_small_classes(cls[k], kHubClasses, kHubLegs[k], kHubTE);

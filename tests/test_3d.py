@@ -189,3 +189,27 @@ def test_hybrid_vcycle_matches_oracle(cuda, orc, monkeypatch):
         cube.v_cycle(h, cfg, ug, f)
         o3.v_cycle(H, uo, f)
         assert np.abs(ug - uo).max() <= 1e-10 * np.abs(uo).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("te", [16, 32])
+def test_wide_hub_classes_match_oracle(cuda, orc, monkeypatch, te):
+    """3D tweed hub blocks forced into the wide launch classes (TE threads
+    per leg, as on the 1025^3 cube) on a small cube, natural and hybrid,
+    against the oracle."""
+    from paper_2110_08389_b200 import cube, mgcycle
+    monkeypatch.setenv("TMG_FORCE_TE", str(te))
+    o3 = _o3()
+    n = 32
+    x = grid.make_tanh_wall(n, 1.0, 3.0)
+    for hyb in ("4", "100000"):
+        monkeypatch.setenv("TMG_HYB_MIN", hyb)
+        h = cube.CubeHierarchy(x)
+        H = o3.Hierarchy3(x.values)
+        f = cube.config4_rhs(n, device=False)
+        cfg = mgcycle.CycleConfig(smoother="tweed", nu1=2, nu2=2)
+        ug, uo = np.zeros_like(f), np.zeros_like(f)
+        for _ in range(2):
+            cube.v_cycle(h, cfg, ug, f)
+            o3.v_cycle(H, uo, f)
+            assert np.abs(ug - uo).max() <= 1e-10 * np.abs(uo).max()
