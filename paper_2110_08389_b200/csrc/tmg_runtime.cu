@@ -3,6 +3,7 @@
 // driver (mgcycle.py:80-139) on the hybrid field layout, solver sessions and
 // CUDA-graph replay of whole cycles.
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -92,6 +93,15 @@ struct tmg_level {
   GridArgs grid() const { return GridArgs{nx, ny, W, E, S, N}; }
 };
 
+// State of the device-driven solve loop (mgcycle.py:128-138 on the GPU):
+// the check kernel after every cycle appends the defect norm and decides
+// whether the while-node runs another cycle.
+struct SolveDev {
+  double d0, tol;
+  int max_cycles, cycle, converged, err;
+  double norms[1];  // [solve_cap + 1]
+};
+
 struct tmg_hier {
   std::vector<tmg_level*> lv;
   int mode = -1;                // layout of the work fields (-1: not allocated)
@@ -101,6 +111,9 @@ struct tmg_hier {
   std::map<std::tuple<int, int, int, int>, std::pair<cudaGraphExec_t, int>> graphs;
   int last_kernels = 0;
   long long bytes = 0;
+  SolveDev* d_solve = nullptr;  // device-driven solve loop state (solve_graph)
+  int solve_cap = 0;            // cycles d_solve has room for
+  std::map<std::tuple<int, int, int, int>, std::pair<cudaGraphExec_t, int>> solve_graphs;
 };
 
 namespace {
@@ -322,6 +335,8 @@ int ensure_fields(tmg_hier* h, int mode) {
   h->blocks.clear();
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.first);
   h->graphs.clear();
+  for (auto& kv : h->solve_graphs) cudaGraphExecDestroy(kv.second.first);
+  h->solve_graphs.clear();
   h->bytes = 0;
   const int L = (int)h->lv.size();
   h->U.assign(L, FieldView{});
@@ -436,6 +451,8 @@ int session_store(tmg_hier* h, double* u, cudaStream_t s) {
   return e == cudaSuccess ? TMG_OK : cuda_fail(e, "layout conversion");
 }
 
+int session_norm_async(tmg_hier* h, cudaStream_t s);
+
 int session_cycles(tmg_hier* h, int kind, int full, int nu1, int nu2, int reps, cudaStream_t s) {
   if (!h->loaded) return fail(TMG_BADARG, "no solver session loaded");
   if (session_mode(kind) != h->mode)
@@ -450,7 +467,14 @@ int session_cycles(tmg_hier* h, int kind, int full, int nu1, int nu2, int reps, 
     cudaGraph_t g;
     const long long counted = launch_counter();  // captured launches do not run
     TMG_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    int st3 = vcycle_launches(h, kind, full, nu1, nu2, cs);
+    // full & 2: the solve loop's check (defect norm, pivot flags of every
+    // level) rides in the same graph, one launch and one sync per cycle
+    int st3 = vcycle_launches(h, kind, full & 1, nu1, nu2, cs);
+    if (!st3 && (full & 2)) {
+      st3 = session_norm_async(h, cs);
+      for (auto* lv : h->lv)
+        if (!st3) st3 = fetch_flags_async(lv, cs);
+    }
     cudaError_t e = cudaStreamEndCapture(cs, &g);
     launch_counter() = counted;
     cudaStreamDestroy(cs);
@@ -514,7 +538,10 @@ int guarded(Fn&& fn) {
 }  // namespace
 
 namespace tmg {
+thread_local bool g_pdl_off = false;  // set while capturing a body that may not use PDL
+
 bool pdl_enabled() {
+  if (g_pdl_off) return false;
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("TMG_PDL");
@@ -557,7 +584,7 @@ int tmg_level_create(int nx, int ny, const double* W, const double* E, const dou
     TMG_CUDA_TRY(cudaMemcpy(lv->E, E, bx, cudaMemcpyHostToDevice));
     TMG_CUDA_TRY(cudaMemcpy(lv->S, S, by, cudaMemcpyHostToDevice));
     TMG_CUDA_TRY(cudaMemcpy(lv->N, N, by, cudaMemcpyHostToDevice));
-    TMG_CUDA_TRY(cudaMalloc(&lv->d_err, sizeof(int) + sizeof(unsigned long long) * 2));
+    TMG_CUDA_TRY(cudaMalloc(&lv->d_err, sizeof(int) * 2 + sizeof(unsigned long long) * 2));
     lv->d_norm = reinterpret_cast<unsigned long long*>(lv->d_err + 2);
     TMG_CUDA_TRY(cudaMemset(lv->d_err, 0, sizeof(int)));
     TMG_CUDA_TRY(cudaMallocHost(&lv->h_err, sizeof(int) * 2 + sizeof(unsigned long long) * 2));
@@ -710,6 +737,8 @@ int tmg_hier_create(int nlevels, tmg_level* const* levels, tmg_hier** out) {
 int tmg_hier_destroy(tmg_hier* h) {
   if (!h) return TMG_OK;
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.first);
+  for (auto& kv : h->solve_graphs) cudaGraphExecDestroy(kv.second.first);
+  cudaFree(h->d_solve);
   for (double* p : h->blocks) cudaFree(p);
   delete h;
   return TMG_OK;
@@ -730,7 +759,7 @@ int tmg_session_cycles(tmg_hier* h, int kind, int full, int nu1, int nu2, int re
   int st = check_hier_args(h, kind, nu1, nu2);
   if (st) return st;
   return guarded(
-      [&] { return session_cycles(h, kind, full, nu1, nu2, reps, (cudaStream_t)stream); });
+      [&] { return session_cycles(h, kind, full ? 1 : 0, nu1, nu2, reps, (cudaStream_t)stream); });
 }
 
 int tmg_session_norm(tmg_hier* h, double* out_host, void* stream) {
@@ -771,7 +800,7 @@ int tmg_vcycle_graph(tmg_hier* h, int kind, int full, int nu1, int nu2, double* 
   return guarded([&]() -> int {
     cudaStream_t s = (cudaStream_t)stream;
     int st2 = session_load(h, kind, u, f, s);
-    if (!st2) st2 = session_cycles(h, kind, full, nu1, nu2, reps, s);
+    if (!st2) st2 = session_cycles(h, kind, full ? 1 : 0, nu1, nu2, reps, s);
     if (!st2) st2 = session_store(h, u, s);
     return st2;
   });
@@ -781,6 +810,138 @@ int tmg_vcycle(tmg_hier* h, int kind, int full, int nu1, int nu2, double* u, con
                void* stream) {
   return tmg_vcycle_graph(h, kind, full, nu1, nu2, u, f, 1, stream);
 }
+
+namespace {
+struct ErrPtrs {
+  int* p[32];
+  int n;
+};
+
+// after a cycle: record its defect norm, stop on convergence, a non-finite
+// norm, a vanishing pivot or max_cycles (the host loop's rule, same order)
+__global__ void solve_check_kernel(cudaGraphConditionalHandle hdl, SolveDev* sd,
+                                   unsigned long long* d_norm, ErrPtrs e) {
+  unsigned long long b = *d_norm;
+  *d_norm = 0ull;  // the next cycle's norm accumulates from zero
+  double dn;
+  memcpy(&dn, &b, sizeof(dn));
+  const int c = sd->cycle + 1;
+  sd->cycle = c;
+  sd->norms[c] = dn;
+  int err = 0;
+  for (int k = 0; k < e.n; k++) err |= *e.p[k];
+  sd->err = err;
+  bool stop = (err & 1) || c >= sd->max_cycles || !isfinite(dn);
+  if (!(err & 1) && isfinite(dn) && dn <= sd->tol * sd->d0) {
+    sd->converged = 1;
+    stop = true;
+  }
+  cudaGraphSetConditional(hdl, stop ? 0u : 1u);
+}
+
+// one graph per (kind, full, nu1, nu2): a while-node whose body is the
+// V-cycle, the defect norm and the check kernel -- no host round trip per
+// cycle.  Body kernels launch without PDL edges if the driver refuses them
+// inside a conditional body.
+int solve_graph(tmg_hier* h, int kind, int full, int nu1, int nu2, cudaGraphExec_t* out,
+                int* kernels_per_cycle) {
+  auto key = std::make_tuple(kind, full, nu1, nu2);
+  auto it = h->solve_graphs.find(key);
+  if (it != h->solve_graphs.end()) {
+    *out = it->second.first;
+    *kernels_per_cycle = it->second.second;
+    return TMG_OK;
+  }
+  int st = prepare(h, kind);
+  if (st) return st;
+  if (h->lv.size() > 32) return fail(TMG_BADARG, "too many levels for the solve graph");
+  ErrPtrs ep{};
+  ep.n = (int)h->lv.size();
+  for (int k = 0; k < ep.n; k++) ep.p[k] = h->lv[k]->d_err;
+  cudaError_t last = cudaSuccess;
+  for (int attempt = 0; attempt < 2; attempt++) {
+    cudaGraph_t g = nullptr;
+    TMG_CUDA_TRY(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle hdl;
+    cudaGraphExec_t ge = nullptr;
+    int kernels = 0;
+    cudaError_t e = cudaGraphConditionalHandleCreate(&hdl, g, 1, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = hdl;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    if (e == cudaSuccess) e = cudaGraphAddNode(&node, g, nullptr, 0, &cp);
+    if (e == cudaSuccess) {
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      cudaStream_t cs;
+      TMG_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      const long long counted = launch_counter();
+      g_pdl_off = attempt == 1;
+      e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
+                                        cudaStreamCaptureModeThreadLocal);
+      int st3 = TMG_OK;
+      if (e == cudaSuccess) {
+        st3 = vcycle_launches(h, kind, full, nu1, nu2, cs);
+        if (!st3) {
+          tmg_level* fine = h->lv[0];
+          cudaError_t e2 = launch_hdefect_norm(fine->grid(), h->U[0], h->F[0], fine->d_norm, cs);
+          if (e2 == cudaSuccess) {
+            solve_check_kernel<<<1, 1, 0, cs>>>(hdl, h->d_solve, fine->d_norm, ep);
+            e2 = cudaGetLastError();
+          }
+          if (e2 != cudaSuccess) st3 = cuda_fail(e2, "solve graph body");
+        }
+        cudaGraph_t captured = nullptr;
+        cudaError_t e3 = cudaStreamEndCapture(cs, &captured);
+        if (e == cudaSuccess) e = e3;
+      }
+      g_pdl_off = false;
+      launch_counter() = counted;
+      cudaStreamDestroy(cs);
+      if (st3) {
+        cudaGraphDestroy(g);
+        return st3;
+      }
+      if (e == cudaSuccess) {
+        size_t nn = 0;
+        e = cudaGraphGetNodes(body, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        if (e == cudaSuccess) e = cudaGraphGetNodes(body, nodes.data(), &nn);
+        for (size_t k = 0; e == cudaSuccess && k < nn; k++) {
+          cudaGraphNodeType t;
+          e = cudaGraphNodeGetType(nodes[k], &t);
+          kernels += (t == cudaGraphNodeTypeKernel);
+        }
+      }
+      if (e == cudaSuccess) e = cudaGraphInstantiate(&ge, g, 0);
+    }
+    cudaGraphDestroy(g);
+    if (e == cudaSuccess) {
+      h->solve_graphs.emplace(key, std::make_pair(ge, kernels));
+      *out = ge;
+      *kernels_per_cycle = kernels;
+      return TMG_OK;
+    }
+    cudaGetLastError();  // clear a refused capture before the retry
+    last = e;
+  }
+  return cuda_fail(last, "solve graph");
+}
+
+int ensure_solve_state(tmg_hier* h, int max_cycles) {
+  if (h->d_solve && h->solve_cap >= max_cycles) return TMG_OK;
+  for (auto& kv : h->solve_graphs) cudaGraphExecDestroy(kv.second.first);
+  h->solve_graphs.clear();  // the graphs bake the state's address
+  cudaFree(h->d_solve);
+  h->d_solve = nullptr;
+  const int cap = max_cycles > 64 ? max_cycles : 64;
+  TMG_CUDA_TRY(cudaMalloc(&h->d_solve, sizeof(SolveDev) + sizeof(double) * (size_t)cap));
+  h->solve_cap = cap;
+  return TMG_OK;
+}
+}  // namespace
 
 int tmg_solve(tmg_hier* h, int kind, int full, int nu1, int nu2, double tol, int max_cycles,
               double* u, const double* f, double* norms_out, int* cycles_out, int* converged_out,
@@ -802,20 +963,31 @@ int tmg_solve(tmg_hier* h, int kind, int full, int nu1, int nu2, double tol, int
       *converged_out = 1;
       return session_store(h, u, s);
     }
-    for (int cycle = 1; cycle <= max_cycles; cycle++) {  // mgcycle.py:128-138
-      st2 = session_cycles(h, kind, full, nu1, nu2, 1, s);
-      if (!st2) st2 = session_norm_async(h, s);
-      if (!st2) st2 = flags_all(h, s);
-      if (st2) return st2;
-      const double dn = bits_to_double(*h->lv[0]->h_norm);
-      norms_out[cycle] = dn;
-      *cycles_out = cycle;
-      if (!std::isfinite(dn)) break;
-      if (dn <= tol * d0) {
-        *converged_out = 1;
-        break;
-      }
-    }
+    if (max_cycles < 1) return session_store(h, u, s);
+    // mgcycle.py:128-138 on the device: one launch of the while-node graph
+    st2 = ensure_solve_state(h, max_cycles);
+    cudaGraphExec_t ge;
+    int per_cycle = 0;
+    if (!st2) st2 = solve_graph(h, kind, full ? 1 : 0, nu1, nu2, &ge, &per_cycle);
+    if (st2) return st2;
+    SolveDev hs = {};
+    hs.d0 = d0;
+    hs.tol = tol;
+    hs.max_cycles = max_cycles;
+    TMG_CUDA_TRY(cudaMemcpyAsync(h->d_solve, &hs, offsetof(SolveDev, norms), cudaMemcpyHostToDevice, s));
+    TMG_CUDA_TRY(cudaMemsetAsync(h->lv[0]->d_norm, 0, sizeof(unsigned long long), s));
+    TMG_CUDA_TRY(cudaGraphLaunch(ge, s));
+    TMG_CUDA_TRY(cudaMemcpyAsync(&hs, h->d_solve, offsetof(SolveDev, norms), cudaMemcpyDeviceToHost, s));
+    TMG_CUDA_TRY(cudaStreamSynchronize(s));
+    TMG_COUNT((long long)per_cycle * hs.cycle);
+    std::vector<double> nv((size_t)hs.cycle + 1);
+    TMG_CUDA_TRY(cudaMemcpy(nv.data(), h->d_solve->norms, sizeof(double) * nv.size(),
+                            cudaMemcpyDeviceToHost));
+    st2 = flags_all(h, s);  // raises on a vanishing pivot (and clears the flags)
+    if (st2) return st2;
+    for (int c = 1; c <= hs.cycle; c++) norms_out[c] = nv[(size_t)c];
+    *cycles_out = hs.cycle;
+    *converged_out = hs.converged;
     return session_store(h, u, s);
   });
 }

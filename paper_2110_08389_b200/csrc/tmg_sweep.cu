@@ -44,6 +44,10 @@ namespace cg = cooperative_groups;
 #define TMG_PDL_LATE 1  // 0: signal the dependent launch at entry instead of after the solve
 #endif
 
+#ifndef TMG_STAGE_ALONG
+#define TMG_STAGE_ALONG 1  // 0: read the along couplings per thread through L1 (measured slower)
+#endif
+
 #ifndef TMG_MINB8
 #define TMG_MINB8 TMG_MINB  // resident CTAs per SM targeted by the q <= 8 kernels
 #endif
@@ -175,9 +179,11 @@ __device__ int g_phase_n;
 #endif
 
 // Shared memory (doubles):
-//   R, PA, PC [T * Q] chunk-major point values: the right-hand side (later
-//                     rho, alpha, x) and the along couplings toward the
-//                     previous / next point; row t slot k lives at
+//   R [, PA, PC] [T * Q] chunk-major point values: the right-hand side
+//                     (later rho, alpha, x) and, when TMG_STAGE_ALONG, the
+//                     along couplings toward the previous / next point
+//                     (otherwise each thread reads them from the 1D
+//                     coefficient arrays through L1); row t slot k lives at
 //                     t*Q + (k ^ (t & (Q-1))) (XOR swizzle: conflict-free
 //                     for both the lane-along-chunk gather and the
 //                     lane-per-chunk elimination, no padding)
@@ -185,7 +191,7 @@ __device__ int g_phase_n;
 //   XH        [T]     hub values, slot = owner thread
 template <int Q>
 constexpr size_t sweep_smem() {
-  return sizeof(double) * (size_t)(3 * kThreads * Q + 6 * kThreads);
+  return sizeof(double) * (size_t)((TMG_STAGE_ALONG ? 3 : 1) * kThreads * Q + 6 * kThreads);
 }
 
 template <int Q>
@@ -193,15 +199,42 @@ __device__ __forceinline__ int sw(int t, int k) {
   return t * Q + (k ^ (t & (Q - 1)));
 }
 
+// Along couplings of a thread's chunk point k: toward the previous (a) and
+// the next (c) point.  Staged rows in shared memory, or the 1D coefficient
+// arrays (the same values: a chunk is one straight run, so point k's
+// couplings sit at a fixed element step from the first point's).
+template <int Q>
+struct AlongStaged {
+  const double* PA;
+  const double* PC;
+  int tid;
+  __device__ __forceinline__ double a(int k) const { return PA[sw<Q>(tid, k)]; }
+  __device__ __forceinline__ double c(int k) const { return PC[sw<Q>(tid, k)]; }
+};
+struct AlongL1 {
+  const double* __restrict__ pa;
+  const double* __restrict__ pc;
+  int da;
+  __device__ __forceinline__ double a(int k) const { return __ldg(pa + k * da); }
+  __device__ __forceinline__ double c(int k) const { return __ldg(pc + k * da); }
+};
+#if TMG_STAGE_ALONG
+template <int Q>
+using Along = AlongStaged<Q>;
+#else
+template <int Q>
+using Along = AlongL1;
+#endif
+
 // Phase B of one chunk: Thomas down sweep over the chunk interior (the
 // coupling to the previous chunk's end kept as the column lam) and an affine
 // back pass leaving x_k = alpha_k + beta_k * Xleft + gamma_k * X in (R, lam,
 // ivr).  NI > 0: compile-time interior count (full chunks, no predicates);
 // NI == 0: runtime count nI.  (ad, bd, gd) = the form of the last interior
 // point, (au, bu, gu) = that of the first.
-template <int Q, int NI>
-__device__ __forceinline__ void chunk_eliminate(int tid, int nI, double* R, const double* PA,
-                                                const double* PC, double csum, double a_first,
+template <int Q, int NI, class AL>
+__device__ __forceinline__ void chunk_eliminate(int tid, int nI, double* R, const AL& cpl,
+                                                double csum, double a_first,
                                                 double (&lam)[Q], double (&ivr)[Q], bool& bad,
                                                 double& ad, double& bd, double& gd, double& au,
                                                 double& bu, double& gu) {
@@ -211,7 +244,7 @@ __device__ __forceinline__ void chunk_eliminate(int tid, int nI, double* R, cons
   for (int k = 0; k < Q; k++) {
     if (k < n) {
       const int sl = sw<Q>(tid, k);
-      const double pav = PA[sl], pcv = PC[sl], rp = R[sl];
+      const double pav = cpl.a(k), pcv = cpl.c(k), rp = R[sl];
       const double bb = -(pav + pcv + csum);
       if (k == 0) {
         bp = bb;
@@ -245,7 +278,7 @@ __device__ __forceinline__ void chunk_eliminate(int tid, int nI, double* R, cons
         bd = be;
         gd = ga;
       } else {
-        const double cp = PC[sl];
+        const double cp = cpl.c(k);
         al = fma(-cp, al, R[sl]) * ivr[k];
         be = fma(-cp, be, lam[k]) * ivr[k];
         ga = -cp * ga * ivr[k];
@@ -268,9 +301,9 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
                                           int rank, double* smem) {
   constexpr int T = kThreads;
   double* R = smem;
-  double* PA = R + T * Q;
+  double* PA = R + T * Q;  // staged along couplings (TMG_STAGE_ALONG only)
   double* PC = PA + T * Q;
-  double* sA = PC + T * Q;
+  double* sA = TMG_STAGE_ALONG ? PC + T * Q : R + T * Q;
   double* sB = sA + T;
   double* sC = sB + T;
   double* sD = sC + T;
@@ -356,15 +389,19 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
         vf[b] = fb[o];
         vl[b] = ub[o - cs0];
         vh[b] = ub[o + cs0];
-        va[b] = __ldg(a.W + pa0 + p * da0);
-        vc[b] = __ldg(a.W + pc0 + p * da0);
+        if (TMG_STAGE_ALONG) {
+          va[b] = __ldg(a.W + pa0 + p * da0);
+          vc[b] = __ldg(a.W + pc0 + p * da0);
+        }
       }
 #pragma unroll
       for (int b = 0; b < BATCH; b++) {
         const int sl = sw<Q>(wbase + (m0 + b) * PER + csub, ksub);
         R[sl] = fma(-xh0, vh[b], fma(-xl0, vl[b], vf[b]));
-        PA[sl] = va[b];
-        PC[sl] = vc[b];
+        if (TMG_STAGE_ALONG) {
+          PA[sl] = va[b];
+          PC[sl] = vc[b];
+        }
       }
     }
   } else {
@@ -398,8 +435,10 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
           vf[b] = fb[o];
           vl[b] = ub[o - ri.z];
           vh[b] = ub[o + ri.z];
-          va[b] = __ldg(a.W + rj.x + ai);
-          vc[b] = __ldg(a.W + rj.y + ai);
+          if (TMG_STAGE_ALONG) {
+            va[b] = __ldg(a.W + rj.x + ai);
+            vc[b] = __ldg(a.W + rj.y + ai);
+          }
         }
       }
 #pragma unroll
@@ -407,8 +446,10 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
         const double2 rx = recX[wbase + (m0 + b) * PER + csub];
         if (slot[b] >= 0) {
           R[slot[b]] = fma(-rx.y, vh[b], fma(-rx.x, vl[b], vf[b]));
-          PA[slot[b]] = va[b];
-          PC[slot[b]] = vc[b];
+          if (TMG_STAGE_ALONG) {
+            PA[slot[b]] = va[b];
+            PC[slot[b]] = vc[b];
+          }
         }
       }
     }
@@ -460,6 +501,11 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
   double au = 0.0, bu = 0.0, gu = 1.0;  // x_s     = au + bu*Xleft + gu*X
   bool bad = false;
   const double csum = xlv + xhv;
+#if TMG_STAGE_ALONG
+  const Along<Q> cpl{PA, PC, tid};
+#else
+  const Along<Q> cpl{a.W + pa_rel, a.W + pc_rel, c.da};
+#endif
   double a_first = 0.0;
   if (c.n > 0) {
     int i0, j0;
@@ -469,8 +515,7 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
   if constexpr (Q > 1 && !(TMG_SKIP & 1)) {
     // full chunks (all but the last chunk of a leg) take the predicate-free path
     if (nI > 0)
-      chunk_eliminate<Q, 0>(tid, nI, R, PA, PC, csum, a_first, lam, ivr, bad, ad, bd, gd, au, bu,
-                            gu);
+      chunk_eliminate<Q, 0>(tid, nI, R, cpl, csum, a_first, lam, ivr, bad, ad, bd, gd, au, bu, gu);
   }
   TMG_T(2);
   // publish the first-point affine form for the left neighbour chunk
@@ -488,7 +533,7 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
     int ie, je;
     c.ij(nI, ie, je);
     const int sl = sw<Q>(tid, nI);
-    const double pav = PA[sl], pcv = PC[sl];
+    const double pav = cpl.a(nI), pcv = cpl.c(nI);
     const double ae = nI > 0 ? pav : a_first;
     const double ce = C.dir(c.dlast, ie, je);
     A = ae * bd;

@@ -8,6 +8,8 @@
 // the reference's order with explicit round-to-nearest intrinsics
 // (stencil.py:82-87, transfer.py:33-38, 51-53), bit-identical to the
 // natural-layout kernels of tmg_grid.cu.
+#include <cstdlib>
+
 #include "tmg_kernels.h"
 
 namespace tmg {
@@ -302,11 +304,292 @@ __global__ void __launch_bounds__(256) prolong2_kernel(int nx, int ny, FieldView
   }
 }
 
+// ---- marching residual kernels (large levels) -----------------------------
+// A warp owns 64 consecutive points along its buffer's contiguous ("lane")
+// axis, two per lane, and marches along the other ("march") axis keeping a
+// three-row window of u in registers: every u and f value is loaded once per
+// warp (coalesced, 512 B per row), the lane-axis neighbours come from the
+// adjacent lanes by shuffles and the window's edge columns from three extra
+// loads (lanes 0, 1 and 31).  No shared memory, no per-point index division:
+// the residual work is a handful of instructions per point, so the kernel
+// runs at the HBM rate where the tiled kernels above are issue-bound.
+// Mode 0: the warp's box lives in N (lanes along j), 1: in T (lanes along i),
+// 2: mixed ownership (lanes along j, every load through FieldView::at).
+
+template <int MODE>
+struct RowLoader {
+  const double* base;  // owner buffer (modes 0, 1)
+  FieldView v;         // mode 2
+  int ldr, nA, nM;     // row stride, last lane-axis / march-axis index (the ring)
+  __device__ __forceinline__ double ld(int m, int a) const {
+    if (a < 0 || a > nA || m < 0 || m > nM) return 0.0;
+    if constexpr (MODE == 2) return __ldg(v.at(m, a));
+    else return __ldg(base + (size_t)m * ldr + a);
+  }
+};
+
+template <int MODE>
+__device__ __forceinline__ RowLoader<MODE> row_loader(const FieldView& v) {
+  RowLoader<MODE> r;
+  r.v = v;
+  if constexpr (MODE == 1) {
+    r.base = v.t; r.ldr = v.nx + 1; r.nA = v.nx; r.nM = v.ny;
+  } else {
+    r.base = v.n; r.ldr = v.ny + 1; r.nA = v.ny; r.nM = v.nx;
+  }
+  return r;
+}
+
+// one row of a lane's window: lane-axis points a0, a0 + 1 and the lane's
+// extra column (lane 0: first - 1, lane 1: first - 2, lane 31: first + 64)
+struct Row3 {
+  double c0, c1, x;
+};
+
+template <int MODE>
+__device__ __forceinline__ Row3 load_row(const RowLoader<MODE>& L, int m, int a0, int ax) {
+  Row3 r;
+  r.c0 = L.ld(m, a0);
+  r.c1 = L.ld(m, a0 + 1);
+  r.x = ax >= -1 ? L.ld(m, ax) : 0.0;
+  return r;
+}
+
+// defect f - L u at one point in the reference's order (stencil.py:82-87):
+// (mm, mp) the march-axis neighbours, (am, ap) the lane-axis ones, (lm_lo,
+// lm_hi) the march-axis coefficients toward them, (la_lo, la_hi) the lane-axis
+// ones.  Mode 1 has i along the lane axis.
+template <int MODE>
+__device__ __forceinline__ double defect_pt(double c, double mm, double mp, double am, double ap,
+                                            double cm_lo, double cm_hi, double ca_lo, double ca_hi,
+                                            double fv) {
+  double Wi, Ei, Sj, Nj, im, ip, jm, jp;
+  if constexpr (MODE == 1) {
+    Wi = ca_lo; Ei = ca_hi; Sj = cm_lo; Nj = cm_hi; im = am; ip = ap; jm = mm; jp = mp;
+  } else {
+    Wi = cm_lo; Ei = cm_hi; Sj = ca_lo; Nj = ca_hi; im = mm; ip = mp; jm = am; jp = ap;
+  }
+  const double Cc = -__dadd_rn(__dadd_rn(__dadd_rn(Wi, Ei), Sj), Nj);
+  double acc = __dmul_rn(Wi, im);
+  acc = __dadd_rn(acc, __dmul_rn(Ei, ip));
+  acc = __dadd_rn(acc, __dmul_rn(Sj, jm));
+  acc = __dadd_rn(acc, __dmul_rn(Nj, jp));
+  return __dadd_rn(-__dadd_rn(acc, __dmul_rn(Cc, c)), fv);
+}
+
+// Defects of fine row m at the lane's points a0, a0 + 1 (d0, d1) and, on lane
+// 0, at a0 - 1 (dx).  (p, r, n) = u rows m - 1, m, m + 1.
+template <int MODE>
+__device__ __forceinline__ void defect_row(const Row3& p, const Row3& r, const Row3& n,
+                                           const Row3& f, double cm_lo, double cm_hi,
+                                           const double (&ca_lo)[3], const double (&ca_hi)[3],
+                                           int lane, double& d0, double& d1, double& dx) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const double up1 = __shfl_up_sync(FULL, r.c1, 1);   // u at a0 - 1 (lanes > 0)
+  const double dn0 = __shfl_down_sync(FULL, r.c0, 1); // u at a0 + 2 (lanes < 31)
+  const double x1 = __shfl_down_sync(FULL, r.x, 1);   // lane 0: u at a0 - 2 (lane 1's extra)
+  const double am0 = lane == 0 ? r.x : up1;
+  const double ap1 = lane == 31 ? r.x : dn0;
+  d0 = defect_pt<MODE>(r.c0, p.c0, n.c0, am0, r.c1, cm_lo, cm_hi, ca_lo[0], ca_hi[0], f.c0);
+  d1 = defect_pt<MODE>(r.c1, p.c1, n.c1, r.c0, ap1, cm_lo, cm_hi, ca_lo[1], ca_hi[1], f.c1);
+  dx = defect_pt<MODE>(r.x, p.x, n.x, x1, r.c0, cm_lo, cm_hi, ca_lo[2], ca_hi[2], f.x);
+}
+
+// Residual max-norm over a 128 x 128 fine box per CTA (warp: 64 lane-axis
+// points x 32 march steps).
+template <int MODE>
+__device__ __forceinline__ unsigned long long norm_march_warp(const GridArgs& g, const FieldView& U,
+                                                              const FieldView& F, int i0, int j0) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int A0 = (MODE == 1 ? i0 : j0) + 64 * (w & 1);
+  const int R0 = (MODE == 1 ? j0 : i0) + 32 * (w >> 1);
+  const int nA = MODE == 1 ? g.nx : g.ny, nM = MODE == 1 ? g.ny : g.nx;
+  const int Rend = min(R0 + 32, nM);
+  unsigned long long mx = 0ull;
+  if (R0 >= Rend || A0 >= nA) return mx;
+  const RowLoader<MODE> LU = row_loader<MODE>(U), LF = row_loader<MODE>(F);
+  const int a0 = A0 + 2 * lane;
+  const int ax = lane == 0 ? A0 - 1 : lane == 31 ? A0 + 64 : -2;
+  const double* alo = MODE == 1 ? g.W : g.S;
+  const double* ahi = MODE == 1 ? g.E : g.N;
+  const double* mlo = MODE == 1 ? g.S : g.W;
+  const double* mhi = MODE == 1 ? g.N : g.E;
+  double ca_lo[3], ca_hi[3];
+  {
+    const int cols[3] = {a0, a0 + 1, a0};
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      const int c = min(cols[k], nA);
+      ca_lo[k] = __ldg(alo + c);
+      ca_hi[k] = __ldg(ahi + c);
+    }
+  }
+  const bool v0 = a0 < nA, v1 = a0 + 1 < nA;  // interior lane-axis points
+  Row3 rp = load_row(LU, R0 - 1, a0, ax), rc = load_row(LU, R0, a0, ax);
+  Row3 rn = load_row(LU, R0 + 1, a0, ax), fr = load_row(LF, R0, a0, -2);
+  for (int m = R0; m < Rend; m++) {
+    Row3 nn, nf;
+    const bool more = m + 1 < Rend;
+    if (more) {
+      nn = load_row(LU, m + 2, a0, ax);
+      nf = load_row(LF, m + 1, a0, -2);
+    }
+    double d0, d1, dx;
+    defect_row<MODE>(rp, rc, rn, fr, __ldg(mlo + m), __ldg(mhi + m), ca_lo, ca_hi, lane, d0, d1,
+                     dx);
+    if (v0) {
+      const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(d0));
+      mx = b > mx ? b : mx;
+    }
+    if (v1) {
+      const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(d1));
+      mx = b > mx ? b : mx;
+    }
+    rp = rc; rc = rn;
+    if (more) { rn = nn; fr = nf; }
+  }
+  return mx;
+}
+
+__global__ void __launch_bounds__(256, 4) norm_march_kernel(GridArgs g, FieldView U, FieldView F,
+                                                         unsigned long long* dmax) {
+  const int i0 = 1 + 128 * blockIdx.y, j0 = 1 + 128 * blockIdx.x;
+  pdl_trigger();
+  const int own = box_owner(U, i0 - 1, j0 - 1, 130, 130);
+  pdl_wait();
+  unsigned long long m;
+  if (own == 1) m = norm_march_warp<1>(g, U, F, i0, j0);
+  else if (own == 0) m = norm_march_warp<0>(g, U, F, i0, j0);
+  else m = norm_march_warp<2>(g, U, F, i0, j0);
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, m, s);
+    m = o2 > m ? o2 : m;
+  }
+  __shared__ unsigned long long wm[8];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 1; k < 8; k++) m = wm[k] > m ? wm[k] : m;
+    if (m) atomicMax(dmax, m);
+  }
+}
+
+// Residual max-norm, strip variant: a thread owns SR consecutive points
+// along the march axis of one lane-axis column and issues every load of the
+// strip at once (SR + 2 centre-column values, 2 SR side values -- L1 hits of
+// the neighbouring lanes' lines -- and SR f values), then evaluates the SR
+// defects from registers.  A warp covers 32 lane-axis columns x SR steps;
+// a CTA 64 x (4 SR) points (same box for both orientations).
+#ifndef TMG_NORM_SR
+#define TMG_NORM_SR 8
+#endif
+template <int MODE>
+__device__ __forceinline__ unsigned long long norm_strip_warp(const GridArgs& g, const FieldView& U,
+                                                              const FieldView& F, int i0, int j0) {
+  constexpr int SR = TMG_NORM_SR;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int a = (MODE == 1 ? i0 : j0) + 32 * (w & 1) + lane;
+  const int R0 = (MODE == 1 ? j0 : i0) + SR * (w >> 1);
+  const int nA = MODE == 1 ? g.nx : g.ny, nM = MODE == 1 ? g.ny : g.nx;
+  const RowLoader<MODE> LU = row_loader<MODE>(U), LF = row_loader<MODE>(F);
+  double uc[SR + 2], ul[SR], uh[SR], fv[SR];
+#pragma unroll
+  for (int k = 0; k < SR + 2; k++) uc[k] = LU.ld(R0 - 1 + k, a);
+#pragma unroll
+  for (int k = 0; k < SR; k++) {
+    ul[k] = LU.ld(R0 + k, a - 1);
+    uh[k] = LU.ld(R0 + k, a + 1);
+    fv[k] = LF.ld(R0 + k, a);
+  }
+  const double* alo = MODE == 1 ? g.W : g.S;
+  const double* ahi = MODE == 1 ? g.E : g.N;
+  const double* mlo = MODE == 1 ? g.S : g.W;
+  const double* mhi = MODE == 1 ? g.N : g.E;
+  const int ac = min(a, nA);
+  const double ca_lo = __ldg(alo + ac), ca_hi = __ldg(ahi + ac);
+  unsigned long long mx = 0ull;
+  if (a >= nA) return mx;
+#pragma unroll
+  for (int k = 0; k < SR; k++) {
+    const int m = R0 + k;
+    if (m < nM) {
+      const double d = defect_pt<MODE>(uc[k + 1], uc[k], uc[k + 2], ul[k], uh[k], __ldg(mlo + m),
+                                       __ldg(mhi + m), ca_lo, ca_hi, fv[k]);
+      const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(d));
+      mx = b > mx ? b : mx;
+    }
+  }
+  return mx;
+}
+
+__global__ void __launch_bounds__(256) norm_strip_kernel(GridArgs g, FieldView U, FieldView F,
+                                                         unsigned long long* dmax) {
+  constexpr int BM = 4 * TMG_NORM_SR;  // march-axis extent of the CTA box (lane axis: 64)
+  // CTA box: 64 x 64 points, 64 / BM passes of the eight warps
+  const int i0 = 1 + 64 * blockIdx.y, j0 = 1 + 64 * blockIdx.x;
+  pdl_trigger();
+  const int own = box_owner(U, i0 - 1, j0 - 1, 66, 66);
+  pdl_wait();
+  unsigned long long m = 0ull;
+#pragma unroll 1
+  for (int pass = 0; pass < 64 / BM; pass++) {
+    unsigned long long p;
+    const int di = own == 1 ? 0 : pass * BM, dj = own == 1 ? pass * BM : 0;
+    if (own == 1) p = norm_strip_warp<1>(g, U, F, i0 + di, j0 + dj);
+    else if (own == 0) p = norm_strip_warp<0>(g, U, F, i0 + di, j0 + dj);
+    else p = norm_strip_warp<2>(g, U, F, i0 + di, j0 + dj);
+    m = p > m ? p : m;
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, m, s);
+    m = o2 > m ? o2 : m;
+  }
+  __shared__ unsigned long long wm[8];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 1; k < 8; k++) m = wm[k] > m ? wm[k] : m;
+    if (m) atomicMax(dmax, m);
+  }
+}
+
+// levels at least this large (fine points per axis) take the marching kernels
+int march_min() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("TMG_MARCH_MIN");  // A/B knob: a huge value disables
+    v = e ? std::atoi(e) : 4096;
+  }
+  return v;
+}
+
+int norm_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("TMG_NORM");  // A/B knob: 1 marching warps, else strips
+    v = e ? std::atoi(e) : 0;
+  }
+  return v;
+}
+
 }  // namespace
 
 cudaError_t launch_norm2(const GridArgs& g, const FieldView& U, const FieldView& F,
                          unsigned long long* dmax, cudaStream_t s, int scheme, int g0, int g1) {
   if (g.nx < 2 || g.ny < 2) return cudaSuccess;
+  if (g0 <= 0 && g.nx >= march_min() && g.ny >= march_min()) {
+    TMG_COUNT(1);
+    if (norm_variant() == 1) {
+      dim3 grid((g.ny - 1 + 127) / 128, (g.nx - 1 + 127) / 128);
+      return launch_pdl(norm_march_kernel, grid, dim3(256), 0, s, g, U, F, dmax);
+    }
+    dim3 grid((g.ny - 1 + 63) / 64, (g.nx - 1 + 63) / 64);
+    return launch_pdl(norm_strip_kernel, grid, dim3(256), 0, s, g, U, F, dmax);
+  }
   dim3 grid((g.ny - 1 + NT - 1) / NT, (g.nx - 1 + NT - 1) / NT);
   TMG_COUNT(1);
   return launch_pdl(norm2_kernel, grid, dim3(256), 0, s, g, U, F, dmax,

@@ -299,3 +299,25 @@ def test_legs_spanning_ctas(cuda, orc, monkeypatch, kind, n, q):
     uo = u0.copy()
     orc.sweep(kind, (st.W, st.E, st.S, st.N), uo, f, orc.max_threads())
     assert np.abs(ud.cpu().numpy() - uo).max() <= 1e-10 * np.abs(uo).max()
+
+
+@pytest.mark.gpu
+def test_device_solve_loop_edges(cuda, orc):
+    """The solve loop runs on the device (a while-node graph, tmg_runtime.cu
+    solve_graph): its stopping rule must be the host loop's (mgcycle.py:128-138)
+    for a cycle cap above the initial state capacity (64), a cap of 0 and 1,
+    and repeated solves through one cached graph with different tolerances."""
+    n = 32
+    x = grid.make_tanh_wall(n, 1.0, 2.0)
+    h = grid.build_hierarchy(x, x)
+    H = orc.Hierarchy(x.values, x.values)
+    f = mgcycle.random_rhs(n, n, 7)
+    for tol, cap in ((1e-300, 80), (1e-6, 50), (1e-300, 0), (1e-300, 1), (1e-10, 50)):
+        cfg = mgcycle.CycleConfig(smoother="zebra_alt", restriction="full", tol=tol,
+                                  max_cycles=cap)
+        u, rep = mgcycle.solve(h, cfg, f)
+        uo, repo = orc.solve(H, f, smoother="zebra_alt", restriction="full", tol=tol,
+                             max_cycles=cap)
+        assert rep.cycles == repo.cycles and rep.converged == repo.converged
+        assert len(rep.defect_norms) == rep.cycles + 1
+        assert _rel(u, uo) <= 1e-10
