@@ -724,6 +724,7 @@ def run_cube(args):
     solve = None
     if not args.no_solve and scheme == "tweed":
         cfg_s = mgcycle.CycleConfig(smoother="tweed", nu1=args.nu, nu2=args.nu, tol=1e-10)
+        cube.solve(h, cfg_s, f)  # warm (the solve loop's graph), as the 2D solve leg
         torch.cuda.synchronize()
         z0, z1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         z0.record(stream)

@@ -217,6 +217,12 @@ int tmg_cube_defect(tmg_cube* h, const double* u, const double* f, double* d, vo
 int tmg_cube_load(tmg_cube* h, const double* u, const double* f, void* stream);
 int tmg_cube_cycles(tmg_cube* h, int nu1, int nu2, int reps, void* stream);
 int tmg_cube_norm(tmg_cube* h, double* out_host, void* stream);
+/* mgcycle.py:128-138 in 3D on the device: V(nu1, nu2) cycles of the loaded
+ * session until max|f - Lu| <= tol * d0 (d0 from tmg_cube_norm), a non-finite
+ * defect, a vanishing pivot (TMG_SINGULAR) or max_cycles; one while-node
+ * graph launch, no host round trip per cycle.  norms_out[1..*cycles_out]. */
+int tmg_cube_solve_loop(tmg_cube* h, int nu1, int nu2, double d0, double tol, int max_cycles,
+                        double* norms_out, int* cycles_out, int* converged_out, void* stream);
 int tmg_cube_store(tmg_cube* h, double* u, void* stream);
 /* `reps` finest-level sweeps on the session (the smoother alone, on the
  * layout the V-cycle uses: i- / j-contiguous views for the 3D wireframe) */

@@ -78,6 +78,7 @@ def _declare(L):
         "tmg_cube_load": ([vp, vp, vp, vp], ip),
         "tmg_cube_cycles": ([vp, ip, ip, ip, vp], ip),
         "tmg_cube_norm": ([vp, pd, vp], ip),
+        "tmg_cube_solve_loop": ([vp, ip, ip, dp, dp, ip, pd, pi, pi, vp], ip),
         "tmg_cube_store": ([vp, vp, vp], ip),
         "tmg_cube_sweeps": ([vp, ip, vp], ip),
         "tmg_cube_group_count": ([ip, ip], ip),

@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <map>
 #include <tuple>
+#include <cstddef>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -56,8 +57,7 @@ __global__ void __launch_bounds__(256) defect3_kernel(int n, Coef3 c, const doub
   pdl_wait();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y, i = blockIdx.z;
-  if (k > n) return;
-  const size_t o = idx3(n, i, j, k);
+  const size_t o = idx3(n, i, j, k < n ? k : n);
   double v = 0.0;
   if (i > 0 && j > 0 && k > 0 && i < n && j < n && k < n) {
     const double cc = -(__ldg(c.W + i) + __ldg(c.E + i) + __ldg(c.S + j) + __ldg(c.N + j) +
@@ -71,8 +71,8 @@ __global__ void __launch_bounds__(256) defect3_kernel(int n, Coef3 c, const doub
     acc = __dadd_rn(acc, __dmul_rn(cc, u[o]));
     v = __dadd_rn(f[o], -acc);
   }
-  if (d) d[o] = v;
-  if (dmax) {
+  if (d && k <= n) d[o] = v;
+  if (dmax) {  // every lane takes part (lanes past the row carry v = 0)
     if (g0 > 0 || g1 < (1 << 30)) {
       const int grp = v != 0.0 ? cube_group(gscheme, n, i, j, k) : g0;
       if (grp < g0 || grp >= g1) v = 0.0;
@@ -83,7 +83,15 @@ __global__ void __launch_bounds__(256) defect3_kernel(int n, Coef3 c, const doub
       const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, bits, s);
       bits = o2 > bits ? o2 : bits;
     }
-    if ((threadIdx.x & 31) == 0 && bits) atomicMax(dmax, bits);
+    // one atomic per CTA (per-warp atomics on one address serialise in L2)
+    __shared__ unsigned long long wm[8];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = bits;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int w = 1; w < 8; w++) bits = wm[w] > bits ? wm[w] : bits;
+      if (bits) atomicMax(dmax, bits);
+    }
   }
 }
 
@@ -477,6 +485,11 @@ struct tmg_cube {
   cudaGraphExec_t graph = nullptr;
   int gnu1 = -1, gnu2 = -1;
   int graph_kernels = 0;
+  // device-driven solve loop (tmg_cube_solve_loop): state and while-node graph
+  tmg::SolveDev* d_solve = nullptr;
+  int solve_cap = 0;
+  cudaGraphExec_t solve_graph = nullptr;
+  int snu1 = -1, snu2 = -1, solve_kernels = 0;
 };
 
 namespace {
@@ -757,6 +770,8 @@ int tmg_cube_create_scheme(int n, const double* x, int scheme, tmg_cube** out) {
 int tmg_cube_destroy(tmg_cube* h) {
   if (!h) return TMG_OK;
   if (h->graph) cudaGraphExecDestroy(h->graph);
+  if (h->solve_graph) cudaGraphExecDestroy(h->solve_graph);
+  cudaFree(h->d_solve);
   for (double* p : h->coef) cudaFree(p);
   for (auto& w : h->wl) tmg3::wire_free_level(w);
   for (auto& kv : h->wparts) tmg3::wire_free_level(kv.second);
@@ -894,6 +909,72 @@ int tmg_cube_norm(tmg_cube* h, double* out_host, void* stream) {
   std::memcpy(&v, h->h_dmax, sizeof(v));
   *out_host = v;
   if (*h->h_err & 1) return fail3(TMG_SINGULAR, "zero pivot during 3D block elimination");
+  return TMG_OK;
+}
+
+// V(nu1, nu2) cycles on the loaded session until max |f - L u| <= tol * d0, a
+// non-finite defect, a vanishing pivot or max_cycles (mgcycle.py:128-138 in
+// 3D), run on the device as one while-node graph launch (V-cycle, defect
+// norm, check kernel per iteration).  norms_out[1 .. cycles] receive the
+// per-cycle defect norms; d0 is the caller's initial norm (tmg_cube_norm).
+int tmg_cube_solve_loop(tmg_cube* h, int nu1, int nu2, double d0, double tol, int max_cycles,
+                        double* norms_out, int* cycles_out, int* converged_out, void* stream) {
+  if (!h) return fail3(TMG_BADARG, "null cube");
+  if (nu1 < 0 || nu2 < 0 || nu1 + nu2 < 1) return fail3(TMG_BADARG, "need nu1 + nu2 >= 1");
+  cudaStream_t s = (cudaStream_t)stream;
+  *cycles_out = 0;
+  *converged_out = 0;
+  if (max_cycles < 1) return TMG_OK;
+  if (!h->d_solve || h->solve_cap < max_cycles) {
+    if (h->solve_graph) cudaGraphExecDestroy(h->solve_graph);  // it bakes the state's address
+    h->solve_graph = nullptr;
+    cudaFree(h->d_solve);
+    h->d_solve = nullptr;
+    const int cap = max_cycles > 64 ? max_cycles : 64;
+    T3(cudaMalloc(&h->d_solve, sizeof(tmg::SolveDev) + sizeof(double) * (size_t)cap));
+    h->solve_cap = cap;
+  }
+  if (int st = ensure_natural(h, s)) return st;
+  if (!h->solve_graph || h->snu1 != nu1 || h->snu2 != nu2) {
+    if (h->solve_graph) cudaGraphExecDestroy(h->solve_graph);
+    h->solve_graph = nullptr;
+    tmg::ErrPtrs ep{};
+    ep.n = 1;
+    ep.p[0] = h->err;
+    int st = tmg::build_while_graph(
+        [&](cudaStream_t cs, cudaGraphConditionalHandle hdl) -> int {
+          int st3 = cycle3(h, nu1, nu2, cs, 0, false, false);
+          if (st3) return st3;
+          TMG_COUNT(1);
+          defect3_kernel<<<grid3(h->n[0]), 256, 0, cs>>>(h->n[0], coefs(h, 0), h->U[0], h->F[0],
+                                                         nullptr, h->dmax);
+          cudaError_t e = cudaGetLastError();
+          if (e == cudaSuccess) e = tmg::launch_solve_check(cs, hdl, h->d_solve, h->dmax, ep);
+          return cuda3(e, "cube solve graph body");
+        },
+        &h->solve_graph, &h->solve_kernels);
+    if (st) return st;
+    h->snu1 = nu1;
+    h->snu2 = nu2;
+  }
+  tmg::SolveDev hs = {};
+  hs.d0 = d0;
+  hs.tol = tol;
+  hs.max_cycles = max_cycles;
+  T3(cudaMemcpyAsync(h->d_solve, &hs, offsetof(tmg::SolveDev, norms), cudaMemcpyHostToDevice, s));
+  T3(cudaMemsetAsync(h->dmax, 0, sizeof(unsigned long long), s));
+  T3(cudaGraphLaunch(h->solve_graph, s));
+  T3(cudaMemcpyAsync(&hs, h->d_solve, offsetof(tmg::SolveDev, norms), cudaMemcpyDeviceToHost, s));
+  T3(cudaMemcpyAsync(h->h_err, h->err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  T3(cudaMemsetAsync(h->err, 0, sizeof(int), s));
+  T3(cudaStreamSynchronize(s));
+  TMG_COUNT((long long)h->solve_kernels * hs.cycle);
+  if (*h->h_err & 1) return fail3(TMG_SINGULAR, "zero pivot during 3D block elimination");
+  if (hs.cycle > 0)
+    T3(cudaMemcpy(norms_out + 1, h->d_solve->norms + 1, sizeof(double) * (size_t)hs.cycle,
+                  cudaMemcpyDeviceToHost));
+  *cycles_out = hs.cycle;
+  *converged_out = hs.converged;
   return TMG_OK;
 }
 

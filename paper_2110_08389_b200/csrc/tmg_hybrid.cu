@@ -350,10 +350,15 @@ cudaError_t launch_scatter_points(const FieldView& V, const long long* enc, long
 }
 
 cudaError_t launch_hdefect_restrict(const GridArgs& g, int full, const FieldView& U,
-                                    const FieldView& F, const FieldView& FC, cudaStream_t s) {
+                                    const FieldView& F, const FieldView& FC, cudaStream_t s,
+                                    const FieldView* UC, bool* uc_zeroed) {
+  if (uc_zeroed) *uc_zeroed = false;
   const int nxc = g.nx / 2, nyc = g.ny / 2;
   if (nxc < 2 || nyc < 2) return cudaSuccess;
-  if (!transfer_v1()) return launch_restrict2(g, full, U, F, FC, s);
+  if (!transfer_v1()) {
+    if (uc_zeroed) *uc_zeroed = UC != nullptr;
+    return launch_restrict2(g, full, U, F, FC, s, UC);
+  }
   dim3 grid((nyc - 1 + CT - 1) / CT, (nxc - 1 + CT - 1) / CT);
   TMG_COUNT(1);
   hdefect_restrict_kernel<<<grid, 256, 0, s>>>(g, full, U, F, FC);

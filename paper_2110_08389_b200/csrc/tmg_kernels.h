@@ -2,6 +2,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <functional>
+
 #include "tmg_internal.h"
 #include "tmg_layout.h"
 #include "tmg_plan.h"
@@ -34,6 +36,24 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
+
+// Device-driven solve loops (mgcycle.py:128-138 on the GPU, tmg_runtime.cu):
+// a while-node graph whose body is one V-cycle, the defect norm and a check
+// kernel that appends the norm and decides whether another cycle runs.
+struct SolveDev {
+  double d0, tol;
+  int max_cycles, cycle, converged, err;
+  double norms[1];  // [capacity + 1]
+};
+struct ErrPtrs {  // pivot flags the check kernel ORs together
+  int* p[32];
+  int n;
+};
+cudaError_t launch_solve_check(cudaStream_t s, cudaGraphConditionalHandle hdl, SolveDev* sd,
+                               unsigned long long* d_norm, const ErrPtrs& e);
+// body(stream, handle) captures one iteration (ending with launch_solve_check)
+int build_while_graph(const std::function<int(cudaStream_t, cudaGraphConditionalHandle)>& body,
+                      cudaGraphExec_t* out, int* kernels_per_cycle);
 
 // Host-side count of the kernels this library has put on streams (graph
 // replays add their kernel nodes); tmg_kernel_launches() reads it.
@@ -118,7 +138,8 @@ cudaError_t launch_gather_points(const FieldView& V, const long long* enc, long 
 cudaError_t launch_scatter_points(const FieldView& V, const long long* enc, long n,
                                   const double* in, cudaStream_t s);
 cudaError_t launch_hdefect_restrict(const GridArgs& g, int full, const FieldView& U,
-                                    const FieldView& F, const FieldView& FC, cudaStream_t s);
+                                    const FieldView& F, const FieldView& FC, cudaStream_t s,
+                                    const FieldView* UC = nullptr, bool* uc_zeroed = nullptr);
 // u += P uc on the fine interior; (nx, ny) are the FINE dimensions
 cudaError_t launch_hprolong_correct(int nx, int ny, const FieldView& C, const FieldView& U,
                                     cudaStream_t s);
@@ -126,7 +147,7 @@ cudaError_t launch_hprolong_correct(int nx, int ny, const FieldView& C, const Fi
 cudaError_t launch_norm2(const GridArgs& g, const FieldView& U, const FieldView& F,
                          unsigned long long* dmax, cudaStream_t s, int scheme, int g0, int g1);
 cudaError_t launch_restrict2(const GridArgs& g, int full, const FieldView& U, const FieldView& F,
-                             const FieldView& FC, cudaStream_t s);
+                             const FieldView& FC, cudaStream_t s, const FieldView* UC = nullptr);
 cudaError_t launch_prolong2(int nx, int ny, const FieldView& C, const FieldView& U,
                             cudaStream_t s);
 bool transfer_v1();

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <string>
 #include <tuple>
@@ -91,15 +92,6 @@ struct tmg_level {
   long long bytes = 0;
 
   GridArgs grid() const { return GridArgs{nx, ny, W, E, S, N}; }
-};
-
-// State of the device-driven solve loop (mgcycle.py:128-138 on the GPU):
-// the check kernel after every cycle appends the defect norm and decides
-// whether the while-node runs another cycle.
-struct SolveDev {
-  double d0, tol;
-  int max_cycles, cycle, converged, err;
-  double norms[1];  // [solve_cap + 1]
 };
 
 struct tmg_hier {
@@ -381,10 +373,14 @@ int vcycle_launches(tmg_hier* h, int kind, int full, int nu1, int nu2, cudaStrea
       int st = sweep_kind(lv, kind, 3, h->U[l], h->F[l], s);
       if (st) return st;
     }
-    cudaError_t e = launch_hdefect_restrict(lv->grid(), full, h->U[l], h->F[l], h->F[l + 1], s);
+    bool zeroed = false;  // the restriction wrote the coarse zero guess itself
+    cudaError_t e = launch_hdefect_restrict(lv->grid(), full, h->U[l], h->F[l], h->F[l + 1], s,
+                                            &h->U[l + 1], &zeroed);
     if (e != cudaSuccess) return cuda_fail(e, "defect_restrict");
-    int st = zero_field(h->U[l + 1], s);
-    if (st) return st;
+    if (!zeroed) {
+      int st = zero_field(h->U[l + 1], s);
+      if (st) return st;
+    }
   }
   {  // coarsest level: direct solve (mgcycle.py:93-95)
     tmg_level* lc = h->lv[L - 1];
@@ -811,12 +807,9 @@ int tmg_vcycle(tmg_hier* h, int kind, int full, int nu1, int nu2, double* u, con
   return tmg_vcycle_graph(h, kind, full, nu1, nu2, u, f, 1, stream);
 }
 
-namespace {
-struct ErrPtrs {
-  int* p[32];
-  int n;
-};
+}  // extern "C"
 
+namespace {
 // after a cycle: record its defect norm, stop on convergence, a non-finite
 // norm, a vanishing pivot or max_cycles (the host loop's rule, same order)
 __global__ void solve_check_kernel(cudaGraphConditionalHandle hdl, SolveDev* sd,
@@ -838,26 +831,16 @@ __global__ void solve_check_kernel(cudaGraphConditionalHandle hdl, SolveDev* sd,
   }
   cudaGraphSetConditional(hdl, stop ? 0u : 1u);
 }
+}  // namespace
 
-// one graph per (kind, full, nu1, nu2): a while-node whose body is the
-// V-cycle, the defect norm and the check kernel -- no host round trip per
-// cycle.  Body kernels launch without PDL edges if the driver refuses them
-// inside a conditional body.
-int solve_graph(tmg_hier* h, int kind, int full, int nu1, int nu2, cudaGraphExec_t* out,
-                int* kernels_per_cycle) {
-  auto key = std::make_tuple(kind, full, nu1, nu2);
-  auto it = h->solve_graphs.find(key);
-  if (it != h->solve_graphs.end()) {
-    *out = it->second.first;
-    *kernels_per_cycle = it->second.second;
-    return TMG_OK;
-  }
-  int st = prepare(h, kind);
-  if (st) return st;
-  if (h->lv.size() > 32) return fail(TMG_BADARG, "too many levels for the solve graph");
-  ErrPtrs ep{};
-  ep.n = (int)h->lv.size();
-  for (int k = 0; k < ep.n; k++) ep.p[k] = h->lv[k]->d_err;
+cudaError_t tmg::launch_solve_check(cudaStream_t s, cudaGraphConditionalHandle hdl, SolveDev* sd,
+                               unsigned long long* d_norm, const ErrPtrs& e) {
+  solve_check_kernel<<<1, 1, 0, s>>>(hdl, sd, d_norm, e);
+  return cudaGetLastError();
+}
+
+int tmg::build_while_graph(const std::function<int(cudaStream_t, cudaGraphConditionalHandle)>& body,
+                      cudaGraphExec_t* out, int* kernels_per_cycle) {
   cudaError_t last = cudaSuccess;
   for (int attempt = 0; attempt < 2; attempt++) {
     cudaGraph_t g = nullptr;
@@ -874,25 +857,16 @@ int solve_graph(tmg_hier* h, int kind, int full, int nu1, int nu2, cudaGraphExec
     cudaGraphNode_t node;
     if (e == cudaSuccess) e = cudaGraphAddNode(&node, g, nullptr, 0, &cp);
     if (e == cudaSuccess) {
-      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      cudaGraph_t bg = cp.conditional.phGraph_out[0];
       cudaStream_t cs;
       TMG_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
       const long long counted = launch_counter();
       g_pdl_off = attempt == 1;
-      e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
+      e = cudaStreamBeginCaptureToGraph(cs, bg, nullptr, nullptr, 0,
                                         cudaStreamCaptureModeThreadLocal);
       int st3 = TMG_OK;
       if (e == cudaSuccess) {
-        st3 = vcycle_launches(h, kind, full, nu1, nu2, cs);
-        if (!st3) {
-          tmg_level* fine = h->lv[0];
-          cudaError_t e2 = launch_hdefect_norm(fine->grid(), h->U[0], h->F[0], fine->d_norm, cs);
-          if (e2 == cudaSuccess) {
-            solve_check_kernel<<<1, 1, 0, cs>>>(hdl, h->d_solve, fine->d_norm, ep);
-            e2 = cudaGetLastError();
-          }
-          if (e2 != cudaSuccess) st3 = cuda_fail(e2, "solve graph body");
-        }
+        st3 = body(cs, hdl);
         cudaGraph_t captured = nullptr;
         cudaError_t e3 = cudaStreamEndCapture(cs, &captured);
         if (e == cudaSuccess) e = e3;
@@ -906,9 +880,9 @@ int solve_graph(tmg_hier* h, int kind, int full, int nu1, int nu2, cudaGraphExec
       }
       if (e == cudaSuccess) {
         size_t nn = 0;
-        e = cudaGraphGetNodes(body, nullptr, &nn);
+        e = cudaGraphGetNodes(bg, nullptr, &nn);
         std::vector<cudaGraphNode_t> nodes(nn);
-        if (e == cudaSuccess) e = cudaGraphGetNodes(body, nodes.data(), &nn);
+        if (e == cudaSuccess) e = cudaGraphGetNodes(bg, nodes.data(), &nn);
         for (size_t k = 0; e == cudaSuccess && k < nn; k++) {
           cudaGraphNodeType t;
           e = cudaGraphNodeGetType(nodes[k], &t);
@@ -919,15 +893,50 @@ int solve_graph(tmg_hier* h, int kind, int full, int nu1, int nu2, cudaGraphExec
     }
     cudaGraphDestroy(g);
     if (e == cudaSuccess) {
-      h->solve_graphs.emplace(key, std::make_pair(ge, kernels));
       *out = ge;
       *kernels_per_cycle = kernels;
       return TMG_OK;
     }
-    cudaGetLastError();  // clear a refused capture before the retry
+    cudaGetLastError();  // clear a refused capture before the retry without PDL
     last = e;
   }
   return cuda_fail(last, "solve graph");
+}
+
+extern "C" {
+
+namespace {
+// one graph per (kind, full, nu1, nu2): a while-node whose body is the
+// V-cycle, the defect norm and the check kernel -- no host round trip per
+// cycle.
+int solve_graph(tmg_hier* h, int kind, int full, int nu1, int nu2, cudaGraphExec_t* out,
+                int* kernels_per_cycle) {
+  auto key = std::make_tuple(kind, full, nu1, nu2);
+  auto it = h->solve_graphs.find(key);
+  if (it != h->solve_graphs.end()) {
+    *out = it->second.first;
+    *kernels_per_cycle = it->second.second;
+    return TMG_OK;
+  }
+  int st = prepare(h, kind);
+  if (st) return st;
+  if (h->lv.size() > 32) return fail(TMG_BADARG, "too many levels for the solve graph");
+  ErrPtrs ep{};
+  ep.n = (int)h->lv.size();
+  for (int k = 0; k < ep.n; k++) ep.p[k] = h->lv[k]->d_err;
+  st = build_while_graph(
+      [&](cudaStream_t cs, cudaGraphConditionalHandle hdl) -> int {
+        int st3 = vcycle_launches(h, kind, full, nu1, nu2, cs);
+        if (st3) return st3;
+        tmg_level* fine = h->lv[0];
+        cudaError_t e2 = launch_hdefect_norm(fine->grid(), h->U[0], h->F[0], fine->d_norm, cs);
+        if (e2 == cudaSuccess) e2 = launch_solve_check(cs, hdl, h->d_solve, fine->d_norm, ep);
+        return e2 == cudaSuccess ? TMG_OK : cuda_fail(e2, "solve graph body");
+      },
+      out, kernels_per_cycle);
+  if (st) return st;
+  h->solve_graphs.emplace(key, std::make_pair(*out, *kernels_per_cycle));
+  return TMG_OK;
 }
 
 int ensure_solve_state(tmg_hier* h, int max_cycles) {

@@ -184,8 +184,12 @@ constexpr int RC = TMG_RC, RD = 2 * RC + 1, RU = 2 * RC + 3, RLU = RU + 1, RLD =
 constexpr size_t kRestrictSmem = sizeof(double) * (size_t)(RU * RLU + RD * RLD);
 constexpr int RPER = (RD * RD + 255) / 256;
 
+// zero_uc: also write the coarse level's zero initial guess (UC, same layout
+// as FC) at every coarse interior point (mgcycle.py:100, fused so that the
+// V-cycle needs no separate zeroing launch; the rings stay 0)
 __global__ void __launch_bounds__(256) restrict2_kernel(GridArgs g, int full, FieldView U,
-                                                        FieldView F, FieldView FC) {
+                                                        FieldView F, FieldView FC, FieldView UC,
+                                                        int zero_uc) {
   extern __shared__ double rsm[];
   double* su = rsm;
   double* sd = rsm + RU * RLU;
@@ -257,6 +261,11 @@ __global__ void __launch_bounds__(256) restrict2_kernel(GridArgs g, int full, Fi
     if (cown == 1) FC.t[FC.off_t(I, J)] = v;
     else if (cown == 0) FC.n[FC.off_n(I, J)] = v;
     else *FC.at(I, J) = v;
+    if (zero_uc) {
+      if (cown == 1) UC.t[UC.off_t(I, J)] = 0.0;
+      else if (cown == 0) UC.n[UC.off_n(I, J)] = 0.0;
+      else *UC.at(I, J) = 0.0;
+    }
   }
   }
 }
@@ -557,7 +566,7 @@ __global__ void __launch_bounds__(256) norm_strip_kernel(GridArgs g, FieldView U
   }
 }
 
-// levels at least this large (fine points per axis) take the marching kernels
+// levels at least this large (fine points per axis) take the strip / marching norm kernels
 int march_min() {
   static int v = -1;
   if (v < 0) {
@@ -597,7 +606,7 @@ cudaError_t launch_norm2(const GridArgs& g, const FieldView& U, const FieldView&
 }
 
 cudaError_t launch_restrict2(const GridArgs& g, int full, const FieldView& U, const FieldView& F,
-                             const FieldView& FC, cudaStream_t s) {
+                             const FieldView& FC, cudaStream_t s, const FieldView* UC) {
   const int nxc = g.nx / 2, nyc = g.ny / 2;
   if (nxc < 2 || nyc < 2) return cudaSuccess;
   dim3 grid((nyc - 1 + RC - 1) / RC, (nxc - 1 + RC - 1) / RC);
@@ -610,7 +619,8 @@ cudaError_t launch_restrict2(const GridArgs& g, int full, const FieldView& U, co
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_pdl(restrict2_kernel, grid, dim3(256), kRestrictSmem, s, g, full, U, F, FC);
+  return launch_pdl(restrict2_kernel, grid, dim3(256), kRestrictSmem, s, g, full, U, F, FC,
+                    UC ? *UC : FC, UC ? 1 : 0);
 }
 
 cudaError_t launch_prolong2(int nx, int ny, const FieldView& C, const FieldView& U,

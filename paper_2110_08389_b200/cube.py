@@ -148,18 +148,17 @@ def solve(h: CubeHierarchy, cfg: CycleConfig, f):
     if d0 == 0.0:
         rep.converged = True
     else:
-        for cyc in range(1, cfg.max_cycles + 1):
-            _check(L.tmg_cube_cycles(h._h, cfg.nu1, cfg.nu2, 1, s))
-            _check(L.tmg_cube_norm(h._h, ctypes.byref(out), s))
-            dn = out.value
-            rep.defect_norms.append(dn)
-            rep.relaxations.append(cyc * (cfg.nu1 + cfg.nu2))
-            rep.cycles = cyc
-            if not np.isfinite(dn):
-                break
-            if dn <= cfg.tol * d0:
-                rep.converged = True
-                break
+        # the cycle loop runs on the device (one while-node graph launch)
+        norms = np.zeros(max(cfg.max_cycles, 0) + 1)
+        cycles, conv = ctypes.c_int(), ctypes.c_int()
+        _check(L.tmg_cube_solve_loop(
+            h._h, cfg.nu1, cfg.nu2, float(d0), float(cfg.tol), int(cfg.max_cycles),
+            norms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(cycles),
+            ctypes.byref(conv), s))
+        rep.cycles = cycles.value
+        rep.defect_norms.extend(float(v) for v in norms[1:rep.cycles + 1])
+        rep.relaxations = [k * (cfg.nu1 + cfg.nu2) for k in range(1, rep.cycles + 1)]
+        rep.converged = bool(conv.value)
     _check(L.tmg_cube_store(h._h, _device.ptr(u), s))
     return _device.back(u, f), rep
 
