@@ -106,46 +106,84 @@ def _updates_per_cycle(h, nu):
     return nu * sum((lv.nx - 1) * (lv.ny - 1) for lv in h.levels)
 
 
-def _workload_desc(w):
-    return (f"{w.name}: {w.n + 1}^2 nodes fp64, "
-            + {"config1": "tanh wall c=3, f~U[-1,1) seed 0",
-               "config2": "sinh centre gamma=3, f~U[-1,1) seed 1",
-               "config3": "tanh wall gamma=4, 16 Gaussians seed 2"}[w.name]
-            + f", {w.smoother} V({w.nu1},{w.nu2}), full weighting, bilinear")
+_DESC = {
+    "config1": "tanh wall c=3, f = 2 Lcg64(0) - 1, tweed",
+    "config2": "sinh centre gamma=3, f = 2 Lcg64(1) - 1, wireframe",
+    "config3": "tanh wall gamma=4, 16 Gaussians (Lcg64(2)), tweed",
+    "config4": "tanh wall gamma=3 on all axes, f = 2 Lcg64(3) - 1, 3D tweed",
+    "config5": "sinh centre gamma=3 on all axes, f = 2 Lcg64(4) - 1, 3D wireframe",
+}
 
 
-def cpu_oracle_cycle(w, f, nthreads):
-    """One V-cycle of the workload through the CPU oracle; returns seconds."""
-    from oracle import oracle as orc
-    H = orc.Hierarchy(w.x.values, w.x.values)
-    u = np.zeros_like(f)
-    t0 = time.perf_counter()
-    orc.v_cycle(H, u, f, smoother=w.smoother, nu1=w.nu1, nu2=w.nu2, nthreads=nthreads)
-    return time.perf_counter() - t0, u
+def _config(args, world):
+    """The `config` object of the JSON line, identical in both arms (built
+    from the arguments only: the reference arm must not import the product
+    package)."""
+    from oracle import workloads as wl
+    n = args.n or wl.CONFIGS[args.config][0]
+    dim = 3 if args.config in ("config4", "config5") else 2
+    nodes = f"{n + 1}^{dim}"
+    nu = args.nu
+    upc = wl.updates_per_cycle(n, 2 * nu, dim)
+    levels, m = 1, n
+    while m % 2 == 0 and m // 2 >= 2:
+        levels, m = levels + 1, m // 2
+    fb = (n + 1) ** dim * 8
+    return {"workload": f"{args.config}: {nodes} nodes fp64, {_DESC[args.config]} "
+                        f"V({nu},{nu}), full weighting, {'trilinear' if dim == 3 else 'bilinear'}",
+            "levels": levels, "updates_per_cycle": upc,
+            "l2": "inputs larger than L2 (u, f = 2 x %.0f MB)" % (fb / 1e6),
+            "parallelism": f"{world} rank(s)"}
+
+
+def asymptotic_ratio(norms, floor=1e-7):
+    """Pre-floor asymptotic convergence factor: the reference's rule
+    (tests/test_acceptance.py:316-322, geometric mean of the cycle ratios,
+    first two skipped) with the floor set above the fp64 rounding plateau
+    (SURVEY.md 8(d)): ratios whose new relative defect is <= floor are cut."""
+    d = np.asarray(norms, dtype=float)
+    if len(d) < 2 or d[0] <= 0:
+        return None
+    d = d / d[0]
+    ratios = [d[k + 1] / d[k] for k in range(len(d) - 1) if d[k + 1] > floor]
+    use = ratios[2:] if len(ratios) > 3 else ratios
+    return float(np.exp(np.mean(np.log(use)))) if use else None
 
 
 def run_reference(args):
+    """The reference's CPU path (the oracle port, bit-identical to the
+    reference's kernels, all host threads) on the same workload.  Imports
+    only oracle/ -- never the product package."""
     world, rank, _ = _dist()
     if rank != 0:
         return
     from oracle import oracle as orc
-    from paper_2110_08389_b200 import configs, grid
-    w = configs.workload(args.config, n=args.n, nu=args.nu)
-    h = grid.build_hierarchy(w.x, w.x)
-    f = w.rhs()
+    from oracle import workloads as wl
+    n, x, smoother, rhs = wl.workload(args.config, args.n)
+    f = rhs()
     cores = orc.max_threads()
+    H = orc.Hierarchy(x, x)
+    nu = args.nu
+
+    def cycle():
+        u = np.zeros_like(f)
+        t0 = time.perf_counter()
+        orc.v_cycle(H, u, f, smoother=smoother, nu1=nu, nu2=nu, nthreads=cores)
+        return time.perf_counter() - t0
+
     for _ in range(args.warmup):
-        cpu_oracle_cycle(w, f, cores)
-    times = [cpu_oracle_cycle(w, f, cores)[0] for _ in range(args.steps)]
+        cycle()
+    times = [cycle() for _ in range(args.steps)]
     per = float(np.mean(times))
-    value = _updates_per_cycle(h, w.nu1 + w.nu2) / per
-    sample = f"one V({w.nu1},{w.nu2}) cycle of {args.config} per step, {cores} OpenMP threads"
+    conf = _config(args, world)
+    value = conf["updates_per_cycle"] / per
+    sample = f"one V({nu},{nu}) cycle of {args.config} per step, {cores} OpenMP threads"
     line = {
         "impl": "reference", "metric": "smoother grid-pt updates/s", "value": value,
         "unit": "grid-pt updates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": _workload_desc(w)},
+        "config": conf,
         "cpu_baseline": {"value": value, "unit": "grid-pt updates/s", "cores": cores,
                          "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "grid-pt updates/s", "h2d_bytes_per_step": 0,
@@ -252,12 +290,13 @@ def run_ours(args):
         _, rep = mgcycle.solve(h, cfg_s, fd_s)
         z1.record(stream)
         torch.cuda.synchronize()
-        r = rep.per_cycle_ratios
         solve = {"tol": tol_s, "max_cycles": max_s, "cycles": rep.cycles,
                  "converged": rep.converged,
                  "ms": max_over_ranks(z0.elapsed_time(z1)),
                  "final_rel_defect": rep.final_rel_defect,
-                 "mean_convergence_factor": float(np.exp(np.mean(np.log(r)))) if r else None}
+                 "asymptotic_ratio": asymptotic_ratio(rep.defect_norms),
+                 "asymptotic_rule": "geometric mean of cycle ratios, first 2 skipped, "
+                                    "relative defects <= 1e-7 cut (test_acceptance.py:316-322)"}
         _lib.check(L.tmg_session_load(state.native, kind, up, fp, sh))
 
     upc = _updates_per_cycle(h, w.nu1 + w.nu2)
@@ -366,10 +405,8 @@ def run_ours(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": _workload_desc(w), "levels": len(h.levels),
-                   "updates_per_cycle": upc, "vcycle_ms": ms_per_step,
-                   "l2": "inputs larger than L2 (u, f = 2 x %.0f MB)" % (field_bytes / 1e6),
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "config": _config(args, world),
+        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_unit": "GB per launch set",
                      "kernel": "block_sweep_kernel (one finest-level sweep, both colours)",
@@ -382,7 +419,12 @@ def run_ours(args):
         "kernels_per_cycle": kernels_per_cycle,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
-        secs, _ = cpu_oracle_cycle(w, f_host, 1)
+        from oracle import oracle as orc
+        H = orc.Hierarchy(w.x.values, w.x.values)
+        uo = np.zeros_like(f_host)
+        t0 = time.perf_counter()
+        orc.v_cycle(H, uo, f_host, smoother=w.smoother, nu1=w.nu1, nu2=w.nu2, nthreads=1)
+        secs = time.perf_counter() - t0
         line["cpu_baseline"] = {
             "value": upc / secs, "unit": "grid-pt updates/s", "cores": 1, "kind": "port",
             "sample": f"one V({w.nu1},{w.nu2}) cycle of the same workload, C oracle, 1 thread "
@@ -483,11 +525,9 @@ def run_sharded(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": _workload_desc(w), "levels": len(h.levels),
-                   "updates_per_cycle": upc, "vcycle_ms": t_ms / args.steps,
-                   "sharded_levels": solver.plan.nshard,
-                   "l2": "inputs larger than L2 (u, f = 2 x %.0f MB)" % (field_bytes / 1e6),
-                   "parallelism": f"sharded x{world}: group ranges, {backend} halo swaps"},
+        "config": _config(args, world),
+        "sharded_levels": solver.plan.nshard,
+        "parallelism": f"sharded x{world}: group ranges, {backend} halo swaps",
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None,
                      "kernel": "block_sweep_kernel (rank's finest-level share, both colours)",
@@ -586,11 +626,9 @@ def run_cube_sharded(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": _cube_desc(args, n), "levels": h.levels,
-                   "updates_per_cycle": upc, "vcycle_ms": t_ms / args.steps,
-                   "sharded_levels": solver.plan.nshard,
-                   "l2": "inputs larger than L2 (u, f = 2 x %.0f MB)" % (field_bytes / 1e6),
-                   "parallelism": f"sharded x{world}: shell ranges, {backend} halo swaps"},
+        "config": _config(args, world),
+        "sharded_levels": solver.plan.nshard,
+        "parallelism": f"sharded x{world}: shell ranges, {backend} halo swaps",
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None,
                      "kernel": "wblock_kernel (rank's finest-level shells, both colours)",
@@ -623,14 +661,6 @@ def _cube_workload(args):
 def _cube_rhs(args, n, device=True):
     from paper_2110_08389_b200 import cube
     return cube.config5_rhs(n, device) if args.config == "config5" else cube.config4_rhs(n, device)
-
-
-def _cube_desc(args, n):
-    if args.config == "config5":
-        return (f"config5: {n + 1}^3 nodes fp64, sinh centre gamma=3 on all axes, "
-                f"f = 2 Lcg64(4) - 1, 3D wireframe V(2,2), full weighting, trilinear")
-    return (f"config4: {n + 1}^3 nodes fp64, tanh wall gamma=3 on all axes, "
-            f"f = 2 Lcg64(3) - 1, 3D tweed V(2,2), full weighting, trilinear")
 
 
 def run_cube(args):
@@ -738,10 +768,8 @@ def run_cube(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": _cube_desc(args, n), "levels": h.levels, "updates_per_cycle": upc,
-                   "vcycle_ms": t_ms / args.steps,
-                   "l2": "inputs larger than L2 (u, f = 2 x %.0f MB)" % (fb / 1e6),
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "config": _config(args, world),
+        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
         "roofline": {"bound": "hbm", "achieved": alg / (sweep_ms * 1e-3) / 1e9, "peak": peak,
                      "unit": "GB/s", "frac": alg / (sweep_ms * 1e-3) / 1e9 / peak,
                      "traffic": None,
@@ -790,19 +818,21 @@ def run_cube(args):
 
 
 def run_cube_reference(args):
+    """Configs 4-5 through the 3D C oracle with all host threads; imports
+    only oracle/ (never the product package)."""
     world, rank, _ = _dist()
     if rank != 0:
         return
     from oracle import oracle as orc
     from oracle import oracle3d as o3
-    from paper_2110_08389_b200 import cube
-    n, x = _cube_workload(args)
-    scheme = _cube_scheme(args)
+    from oracle import workloads as wl
+    n, x, scheme, rhs = wl.workload(args.config, args.n)
     cores = orc.max_threads()
+    conf = _config(args, world)
     times = []
+    f = rhs()
     if n <= 256:  # one V-cycle of the workload per step
-        H = o3.Hierarchy3(x.values, scheme=scheme)
-        f = _cube_rhs(args, n, device=False)
+        H = o3.Hierarchy3(x, scheme=scheme)
         steps, warm = args.steps, args.warmup
         for k in range(warm + steps):
             u = np.zeros_like(f)
@@ -811,17 +841,10 @@ def run_cube_reference(args):
             if k >= warm:
                 times.append(time.perf_counter() - t0)
         per = float(np.mean(times))
-        pts, m = 0, n
-        while True:
-            pts += (m - 1) ** 3
-            if m % 2 or m // 2 < 2:
-                break
-            m //= 2
-        value = 2 * args.nu * pts / per
+        value = conf["updates_per_cycle"] / per
         sample = f"one V({args.nu},{args.nu}) cycle per step, 3D C oracle, {cores} OpenMP threads"
     else:  # bounded: one finest-level sweep of the full grid per step (<= 3 steps)
-        st = o3.assemble3(x.values, x.values, x.values)
-        f = _cube_rhs(args, n, device=False)
+        st = o3.assemble3(x, x, x)
         u = np.zeros_like(f)
         steps, warm = min(args.steps, 3), 1
         for k in range(warm + steps):
@@ -838,7 +861,7 @@ def run_cube_reference(args):
         "unit": "grid-pt updates/s", "n_gpus": world, "steps": steps,
         "warmup": warm, "ms_per_step": per * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": _cube_desc(args, n)},
+        "config": conf,
         "cpu_baseline": {"value": value, "unit": "grid-pt updates/s", "cores": cores,
                          "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "grid-pt updates/s", "h2d_bytes_per_step": 0,

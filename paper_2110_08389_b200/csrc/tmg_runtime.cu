@@ -463,8 +463,9 @@ int session_cycles(tmg_hier* h, int kind, int full, int nu1, int nu2, int reps, 
     cudaGraph_t g;
     const long long counted = launch_counter();  // captured launches do not run
     TMG_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    // full & 2: the solve loop's check (defect norm, pivot flags of every
-    // level) rides in the same graph, one launch and one sync per cycle
+    // full & 2: the host solve loop's check (defect norm, pivot flags of
+    // every level) rides in the same graph, one launch and one sync per cycle
+    // (tmg_solve's fallback when the while-node graph is unavailable)
     int st3 = vcycle_launches(h, kind, full & 1, nu1, nu2, cs);
     if (!st3 && (full & 2)) {
       st3 = session_norm_async(h, cs);
@@ -876,6 +877,13 @@ int tmg::build_while_graph(const std::function<int(cudaStream_t, cudaGraphCondit
       cudaStreamDestroy(cs);
       if (st3) {
         cudaGraphDestroy(g);
+        // a launch refused inside the capture (e.g. PDL in a conditional
+        // body): clear it and retry once without PDL
+        if (attempt == 0 && st3 == TMG_CUDA) {
+          cudaGetLastError();
+          last = cudaErrorNotSupported;
+          continue;
+        }
         return st3;
       }
       if (e == cudaSuccess) {
@@ -977,7 +985,32 @@ int tmg_solve(tmg_hier* h, int kind, int full, int nu1, int nu2, double tol, int
     st2 = ensure_solve_state(h, max_cycles);
     cudaGraphExec_t ge;
     int per_cycle = 0;
-    if (!st2) st2 = solve_graph(h, kind, full ? 1 : 0, nu1, nu2, &ge, &per_cycle);
+    const char* force_host = std::getenv("TMG_SOLVE_HOST");
+    if (!st2 && force_host && force_host[0] == '1') st2 = TMG_CUDA;
+    else if (!st2) st2 = solve_graph(h, kind, full ? 1 : 0, nu1, nu2, &ge, &per_cycle);
+    if (st2 == TMG_CUDA) {
+      // no conditional-node support (driver / capture refused): the same
+      // loop driven from the host, one graph launch and one sync per cycle
+      cudaGetLastError();
+      for (int c = 1; c <= max_cycles; c++) {
+        st2 = session_cycles(h, kind, (full ? 1 : 0) | 2, nu1, nu2, 1, s);
+        if (st2) return st2;
+        TMG_CUDA_TRY(cudaStreamSynchronize(s));
+        for (auto* lv : h->lv) {
+          st2 = check_fetched(lv);
+          if (st2) return st2;
+        }
+        const double dn = bits_to_double(*h->lv[0]->h_norm);
+        norms_out[c] = dn;
+        *cycles_out = c;
+        if (!std::isfinite(dn)) break;
+        if (dn <= tol * d0) {
+          *converged_out = 1;
+          break;
+        }
+      }
+      return session_store(h, u, s);
+    }
     if (st2) return st2;
     SolveDev hs = {};
     hs.d0 = d0;

@@ -143,6 +143,32 @@ def config_cases():
     return out
 
 
+# rows / columns sampled from the config-2 per-sweep iterates (the full
+# 1025^2 fields would be 8 MB each): two residues mod 16 on each axis, so both
+# colours of every smoother and both N/T owners of the hybrid layout appear
+C2_ROWS = np.array([i for i in range(1, 1024) if i % 16 in (1, 8)])
+C2_COLS = np.array([j for j in range(1, 1024) if j % 16 in (3, 10)])
+
+
+def config2_sweeps():
+    """Config 2 (1025^2 wireframe V(2,2)): the finest iterate after each of
+    the four finest-level sweeps of cycle 1, sampled on C2_ROWS x C2_COLS,
+    plus each full iterate's max |u| (the relative-error scale)."""
+    n = 1024
+    i = np.arange(n + 1)
+    v = 0.5 * (1.0 + np.sinh(3.0 * (2.0 * i / n - 1.0)) / np.sinh(3.0))
+    v[0], v[n] = 0.0, 1.0
+    x = grid.Coords1D(v)
+    f = np.zeros((n + 1, n + 1))
+    f[1:-1, 1:-1] = 2.0 * Lcg64(1).fill((n - 1, n - 1)) - 1.0
+    _, _, trace, _ = traced_solve(x, f, "wireframe", 2, 1e-300, 1, trace_cycles=1)
+    out = {"rows": C2_ROWS, "cols": C2_COLS}
+    for k, t in enumerate(trace):
+        out[f"sweep{k}"] = t[np.ix_(C2_ROWS, C2_COLS)]
+        out[f"sweep{k}_absmax"] = np.array(np.abs(t).max())
+    return out
+
+
 def frozen_grid():
     out = {}
     for kind, c in (("wall", 1.5), ("centre", 1.5), ("wall", 4.0)):
@@ -154,6 +180,9 @@ def frozen_grid():
 
 
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "config2_sweeps":
+        np.savez_compressed(os.path.join(HERE, "config2_sweeps.npz"), **config2_sweeps())
+        return
     np.savez_compressed(os.path.join(HERE, "small_sweeps.npz"), **small_cases())
     np.savez_compressed(os.path.join(HERE, "layouts.npz"), **layouts())
     np.savez_compressed(os.path.join(HERE, "grid.npz"), **frozen_grid())

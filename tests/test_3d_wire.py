@@ -164,6 +164,39 @@ def test_config5_scale_sweep(cuda, orc):
 
 
 @pytest.mark.gpu
+def test_config5_full_size_sweep_and_cycle(cuda, orc):
+    """BASELINE config 5 at its full 1025^3 size (the 64-thread-edge PCR
+    path and the 16-point chunks only occur here): one finest-level sweep on
+    the API layout and one V(2,2) cycle (hybrid views, every level) against
+    the oracle with all host threads, gate 1e-10."""
+    import gc
+
+    from paper_2110_08389_b200 import cube, mgcycle
+    o3 = _o3()
+    n = 1024
+    nthreads = orc.max_threads()
+    x = configs.sinh_centre(n, 1.0, 3.0)
+    h = cube.CubeHierarchy(x, scheme="wireframe")
+    f = cube.config5_rhs(n, device=False)
+    fd = cuda.from_numpy(f).cuda()
+    u = cuda.zeros_like(fd)
+    cube.sweep(h, u, fd)
+    uo = np.zeros_like(f)
+    o3.sweep(o3.assemble3(x.values, x.values, x.values), uo, f, nthreads, scheme="wireframe")
+    got = u.cpu().numpy()
+    assert np.abs(got - uo).max() <= 1e-10 * np.abs(uo).max()
+    del got, u
+    gc.collect()
+    ug = cuda.zeros_like(fd)
+    cube.v_cycle(h, mgcycle.CycleConfig(smoother="wireframe", nu1=2, nu2=2), ug, fd)
+    uo[...] = 0.0
+    H = o3.Hierarchy3(x.values, scheme="wireframe")
+    o3.v_cycle(H, uo, f, 2, 2, nthreads)
+    got = ug.cpu().numpy()
+    assert np.abs(got - uo).max() <= 1e-10 * np.abs(uo).max()
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("n", [16, 32])
 def test_hybrid_vcycle_matches_oracle(cuda, orc, monkeypatch, n):
     """The V-cycle on the hybrid layout (i- and j-contiguous views of every

@@ -124,3 +124,40 @@ def test_oracle_config2_solve_matches_golden(orc, cfgs):
     _, rep = orc.solve(H, f, smoother="wireframe", tol=1e-10, nthreads=orc.max_threads())
     assert rep.cycles == int(cfgs["config2_cycles"]) == 20
     assert np.array_equal(np.array(rep.defect_norms), cfgs["config2_norms"])
+
+
+def test_oracle_config2_cycle1_sweeps_match_golden(orc):
+    """Config 2's four finest-level iterates of cycle 1 (sampled rows/columns
+    of the reference's fields, tests/golden/config2_sweeps.npz): the oracle is
+    bit-identical to the reference there too."""
+    gold = np.load(os.path.join(GOLD, "config2_sweeps.npz"))
+    w = configs.workload("config2")
+    H = orc.Hierarchy(w.x.values, w.x.values)
+    trace = []
+    u = np.zeros((1025, 1025))
+    orc.v_cycle(H, u, w.rhs(), smoother="wireframe", trace=trace, nthreads=orc.max_threads())
+    assert len(trace) == 4
+    rows, cols = gold["rows"], gold["cols"]
+    for k, t in enumerate(trace):
+        assert np.array_equal(t[np.ix_(rows, cols)], gold[f"sweep{k}"])
+        assert np.abs(t).max() == gold[f"sweep{k}_absmax"]
+
+
+def test_oracle_workloads_match_package():
+    """oracle/workloads.py (the CPU reference arm's inputs, no product
+    import) produces the package's BASELINE inputs bit for bit."""
+    from oracle import workloads as wl
+    from paper_2110_08389_b200 import cube
+    for name, n in (("config1", None), ("config2", 64), ("config3", 256)):
+        w = configs.workload(name, n=n)
+        nn, x, smoother, rhs = wl.workload(name, n)
+        assert nn == w.n and smoother == w.smoother
+        assert np.array_equal(x, w.x.values)
+        assert np.array_equal(rhs(), w.rhs())
+    for name, fn in (("config4", cube.config4_rhs), ("config5", cube.config5_rhs)):
+        nn, x, _, rhs = wl.workload(name, 16)
+        assert np.array_equal(rhs(), fn(16, device=False))
+        want = (configs.sinh_centre(16, 1.0, 3.0) if name == "config5"
+                else grid.make_tanh_wall(16, 1.0, 3.0)).values
+        assert np.array_equal(x, want)
+    assert wl.updates_per_cycle(128, 4) == 4 * sum((m - 1) ** 2 for m in (128, 64, 32, 16, 8, 4, 2))
