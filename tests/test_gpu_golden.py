@@ -204,7 +204,7 @@ def test_config3_convergence_factors(cuda, orc, config3, nu):
     (test_acceptance.py:316-322: geometric mean of the cycle ratios, first two
     skipped) with the floor at 1e-7, above the fp64 rounding plateau
      -- over the first 8 cycles matches the oracle's over
-    the same cycles to 1e-3, and so do the first 8 ratios one by one."""
+    the same cycles to 1e-3, and so do the pre-floor ratios one by one."""
     w, f = config3
     h = grid.build_hierarchy(w.x, w.x)
     cfg = mgcycle.CycleConfig(smoother="tweed", nu1=nu, nu2=nu, tol=1e-300, max_cycles=20)
@@ -214,8 +214,16 @@ def test_config3_convergence_factors(cuda, orc, config3, nu):
     _, repo = orc.solve(H, f, smoother="tweed", nu1=nu, nu2=nu, tol=1e-300, max_cycles=8,
                         nthreads=orc.max_threads())
     assert rep.defect_norms[0] == repo.defect_norms[0]
-    for a, b in zip(rep.per_cycle_ratios[:8], repo.per_cycle_ratios):
-        assert abs(a - b) <= 1e-3
+    # ratios one by one while both relative defects stay above the floor
+    # (below it the fp64 rounding of the two summation orders dominates)
+    d0 = rep.defect_norms[0]
+    pre = 0
+    for k, (a, b) in enumerate(zip(rep.per_cycle_ratios[:8], repo.per_cycle_ratios)):
+        if min(rep.defect_norms[k + 1], repo.defect_norms[k + 1]) / d0 <= 1e-7:
+            break
+        assert abs(a - b) <= 1e-3, (k, a, b)
+        pre += 1
+    assert pre >= 3
     ag = _asymptotic_ratio(rep.defect_norms[:9], floor=1e-7)
     ao = _asymptotic_ratio(repo.defect_norms, floor=1e-7)
     assert abs(ag - ao) <= 1e-3, (ag, ao)
