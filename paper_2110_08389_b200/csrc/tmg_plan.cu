@@ -353,7 +353,38 @@ std::string build_plan(int scheme, int nx, int ny, int q, int mode, Plan& P) {
   Geometry g;
   std::string err = build_geometry(scheme, nx, ny, g);
   if (!err.empty()) return err;
-  return pack_plan(std::move(g), q, mode, P);
+  const bool legk = leg_plan_applies(scheme, nx, ny, mode) && !g_dry_run;
+  if (legk) {  // L-shells k in [k0, c) go to the leg kernel
+    const int k0 = leg_k0(), c = nx / 2;
+    Geometry out;
+    out.scheme = g.scheme;
+    out.nx = g.nx;
+    out.ny = g.ny;
+    for (const BlockD& B : g.blocks) {
+      int i = B.hi, j = B.hj;
+      if (i < 0) {
+        i = g.legs[B.leg0].i0;
+        j = g.legs[B.leg0].j0;
+      }
+      const int grp = point_group(g.scheme, g.nx, g.ny, i, j);
+      if (grp >= k0 && grp < c) continue;
+      BlockD nb = B;
+      nb.leg0 = (int32_t)out.legs.size();
+      for (int l = 0; l < B.nleg; l++) {
+        LegD L = g.legs[B.leg0 + l];
+        L.block = (int32_t)out.blocks.size();
+        out.legs.push_back(L);
+      }
+      out.blocks.push_back(nb);
+    }
+    g = std::move(out);
+  }
+  err = pack_plan(std::move(g), q, mode, P);
+  if (!err.empty() || !legk) return err;
+  P.lp = new LegPlan();
+  err = build_leg_plan(nx, *P.lp);
+  P.device_bytes += P.lp->device_bytes;
+  return err;
 }
 
 void filter_groups(Geometry& g, int g0, int g1) {
@@ -915,6 +946,11 @@ void free_plan(Plan& p) {
   cudaFree(p.d_blocks);
   p.d_legs = nullptr;
   p.d_blocks = nullptr;
+  if (p.lp) {
+    free_leg_plan(*p.lp);
+    delete p.lp;
+    p.lp = nullptr;
+  }
 }
 
 }  // namespace tmg

@@ -5,6 +5,7 @@
 
 #include "tmg_internal.h"
 #include "tmg_layout.h"
+#include "tmg_tweedleg.h"
 
 namespace tmg {
 
@@ -35,6 +36,9 @@ struct Plan {
   bool point_scheme = false;         // checkerboard: dedicated point kernel
   int g0 = 0, g1 = 0;                // group range of a partial plan (0, 0: all)
   size_t device_bytes = 0;
+  // tweed L-shells of square hybrid grids run on the TMA-fed leg kernel
+  // (tmg_tweedleg.cu); the generic classes then hold the remaining blocks
+  LegPlan* lp = nullptr;
 };
 
 std::string build_plan(int scheme, int nx, int ny, int q, int mode, Plan& p);

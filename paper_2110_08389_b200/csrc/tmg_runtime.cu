@@ -116,6 +116,9 @@ int get_plan(tmg_level* lv, int scheme, int mode, Plan** out) {
     if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");
     Plan* p = new Plan();
     std::string err = build_plan(scheme, lv->nx, lv->ny, default_q(lv->nx, lv->ny), mode, *p);
+    if (err.empty() && p->lp)
+      err = leg_plan_set_coefs(*p->lp, lv->hW.data(), lv->hE.data(), lv->hS.data(),
+                               lv->hN.data());
     if (!err.empty()) {
       free_plan(*p);
       delete p;
@@ -335,7 +338,8 @@ int ensure_fields(tmg_hier* h, int mode) {
   h->F.assign(L, FieldView{});
   for (int l = 0; l < L; l++) {
     const int nx = h->lv[l]->nx, ny = h->lv[l]->ny;
-    const size_t n = (size_t)(nx + 1) * (ny + 1);
+    // buffers start on 256-byte boundaries (bulk copies need 16-byte alignment)
+    const size_t n = ((size_t)(nx + 1) * (ny + 1) + 31) & ~(size_t)31;
     const int nbuf = mode == LM_NATURAL ? 2 : 4;
     double* p = nullptr;
     TMG_CUDA_TRY(cudaMalloc(&p, nbuf * n * sizeof(double)));

@@ -874,6 +874,7 @@ cudaError_t launch_colour(const Plan& P, int red, const SweepArgs& a, cudaStream
     }
     if (e != cudaSuccess) return e;
   }
+  if (P.lp) return launch_leg_colour(*P.lp, red, a, stream);
   return cudaSuccess;
 }
 

@@ -1,0 +1,946 @@
+// Tweed L-shell colour stage on sm_100a: a persistent, TMA-fed block solver
+// for the two-legged blocks of square tweed grids in the hybrid layout
+// (tmg_layout.h, LM_TWEED).  Same exact block Gauss-Seidel as
+// relax_legged (_ckernels.pyx:144-185) / m_legged_thomas (tridiag.py:84-125)
+// on the L-shell blocks of tweed_layout (layout.py:75-84): every leg of a
+// shell is one contiguous run of its owner buffer (x-legs in T, y-legs in N),
+// and its two cross-neighbour runs are the adjacent rows of the same buffer.
+//
+// Work split (host, build_leg_plan): blocks of shells k in [kLegK0, c) are
+// packed into items of <= 256 chunks of 17 points (a chunk per thread, legs
+// never split across CTAs); a block whose legs exceed 128 chunks each is
+// split over the two CTAs of a cluster (one leg each, the branch row
+// exchanged through DSMEM).  Clusters walk a static item schedule.
+//
+// Per item (one CTA):
+//   TMA     one thread issues cp.async.bulk copies of every leg's f run and
+//           its two u cross-neighbour runs into a shared stage (two stages:
+//           the next item streams in while this one is solved);
+//   chunk   per thread, in registers: frozen RHS r = f - cross couplings
+//           (_ckernels.pyx:34-39), Thomas down sweep and an affine back pass
+//           leaving x_k = alpha_k + beta_k X_left + gamma_k X (X = the chunk's
+//           last point); along couplings from a chunk-permuted coefficient
+//           copy (one coalesced 16-byte load per point, no staging);
+//   reduced the chunk ends of each leg form a tridiagonal system with the
+//           branch as a second right-hand side, solved by parallel cyclic
+//           reduction in shared memory;
+//   branch  one scalar row per block (m_legged_thomas's branch equation);
+//   store   finalize in registers, stage through shared memory, coalesced
+//           stores.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "tmg_kernels.h"
+#include "tmg_tweedleg.h"
+
+namespace cg = cooperative_groups;
+
+namespace tmg {
+
+namespace {
+
+constexpr int LQ = kLegQ;         // points per thread chunk (odd: conflict-free
+                                  // per-thread shared-memory rows)
+constexpr int LT = kLegThreads;   // threads per CTA
+constexpr int LCAP = LT * LQ;     // points per item
+
+__device__ __forceinline__ bool bad_pivot(double v) { return v > -1e-300 && v < 1e-300; }
+
+// the ~20-bit hardware reciprocal refined by two Newton steps (== 1.0 / x,
+// tmg_sweep.cu)
+__device__ __forceinline__ double drcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// Geometry of one leg of the L-shell block (k, quad) of an n x n grid
+// (layout.py:75-84; quad bit 0: the block's corner is at i = n-1, bit 1: at
+// j = n-1).  Leg 0 (x-leg) lives in T row bj, leg 1 (y-leg) in N row bi; both
+// run tip -> branch with point e at position p0 + dir * e of their row.
+struct LegGeo {
+  int m, dir, p0, row, orient, sx, sy, bi, bj;
+  __device__ __forceinline__ void set(int k, int quad, int leg, int n) {
+    sx = (quad & 1) ? -1 : 1;
+    sy = (quad & 2) ? -1 : 1;
+    const int x0 = sx > 0 ? 1 : n - 1, y0 = sy > 0 ? 1 : n - 1;
+    bi = x0 + sx * (k - 1);
+    bj = y0 + sy * (k - 1);
+    m = k - 1;
+    if (leg == 0) {
+      dir = sx;
+      p0 = x0;
+      row = bj;
+      orient = sx > 0 ? 0 : 1;
+    } else {
+      dir = sy;
+      p0 = y0;
+      row = bi;
+      orient = sy > 0 ? 2 : 3;
+    }
+  }
+};
+
+// issue an item's bulk loads (warp 0)
+__device__ __forceinline__ void issue_loads(const LegArgs& a, int item, double* stage,
+                                            uint64_t* bar) {
+  const int lane = threadIdx.x & 31;
+  const LegItem I = a.items[item];
+  if (lane == 0) mbar_expect_tx(bar, (unsigned)I.bytes);
+  __syncwarp();
+  for (int c = lane; c < I.ncopy; c += 32) {
+    const LegCopy cp = a.copies[I.copy0 + c];
+    const double* src = cp.src == 0 ? a.fn : cp.src == 1 ? a.ft : cp.src == 2 ? a.un : a.ut;
+    bulk_g2s(stage + cp.s, src + cp.g, (unsigned)cp.n * 8u, bar);
+  }
+}
+
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// One thread's chunk of 17 consecutive leg points: point k's f slot is
+// pF[DIR * k] (also the chunk's scratch: rho, then alpha, then the solution),
+// its u neighbours pL / pH[DIR * k], its couplings pc[32 * k] = (a, c) toward
+// the previous / next point and pd[32 * k] = -(a + c) (the along part of the
+// diagonal).  The tip chunk holds `pad` dummy points in front of the tip:
+// zero couplings, and the tip's own coupling toward them is zero too (its
+// Dirichlet neighbour is folded into f), so dummies are decoupled and only
+// touch the private gap the plan leaves before the tip's f slot.  Every chunk
+// is therefore full and the leg's last chunk ends on the leg's last point.
+// Leaves x_k = alpha_k + be_k * Xleft + ga_k * X (k < 16, X = point 16) with
+// alpha in the f slots.
+struct ChunkOut {
+  double ad, bd, gd;  // form of point 15
+  double au, bu, gu;  // form of point 0
+  double a_end, c_end, r_end;
+  int phi;            // smallest high word of |pivot| (vanishing-pivot check)
+};
+
+template <int DIR>
+__device__ __forceinline__ void chunk_forward(double* __restrict__ pF,
+                                              const double* __restrict__ pL,
+                                              const double* __restrict__ pH,
+                                              const double2* __restrict__ pc,
+                                              const double* __restrict__ pd, double clo,
+                                              double chi, bool first, int wallfix, double uwall,
+                                              double (&lam)[LQ - 1], double (&ivr)[LQ - 1],
+                                              ChunkOut& o) {
+  const double csum = clo + chi;
+  double ivp = 0.0, rho = 0.0, lm = 0.0, cprev = 0.0;
+  int phi = 0x7fffffff;
+#pragma unroll
+  for (int k = 0; k < LQ - 1; k++) {
+    const double r = fma(-chi, pH[DIR * k], fma(-clo, pL[DIR * k], pF[DIR * k]));
+    const double2 ac = __ldg(pc + 32 * k);
+    const double bb = __ldg(pd + 32 * k) - csum;
+    double bp;
+    if (k == 0) {
+      bp = bb;
+      rho = r;
+      lm = first ? 0.0 : -ac.x;
+    } else {
+      const double w = ac.x * ivp;
+      bp = fma(-w, cprev, bb);
+      rho = fma(-w, rho, r);
+      lm = -w * lm;
+    }
+    phi = min(phi, __double2hiint(bp) & 0x7fffffff);
+    ivp = drcp(bp);
+    pF[DIR * k] = rho;
+    lam[k] = lm;
+    ivr[k] = ivp;
+    cprev = ac.y;
+  }
+  constexpr int k = LQ - 1;  // the chunk-end row
+  double r;
+  if (!wallfix) {
+    r = fma(-chi, pH[DIR * k], fma(-clo, pL[DIR * k], pF[DIR * k]));
+  } else {  // x-leg's last point: its wall-side cross neighbour is an N-owned branch
+    const double ul = wallfix == 1 ? uwall : pL[DIR * k];
+    const double uh = wallfix == 1 ? pH[DIR * k] : uwall;
+    r = pF[DIR * k] - clo * ul - chi * uh;
+  }
+  const double2 ac = __ldg(pc + 32 * k);
+  o.a_end = ac.x;
+  o.c_end = ac.y;
+  o.r_end = r;
+  o.phi = phi;
+}
+
+// affine back pass: alpha into the f slots, beta into the thread's row of
+// the scratch (stride 17: conflict-free), gamma stays in registers
+template <int DIR>
+__device__ __forceinline__ void chunk_back(double* __restrict__ pF, double* __restrict__ sb,
+                                           const double2* __restrict__ pc,
+                                           const double (&lam)[LQ - 1], double (&ga)[LQ - 1],
+                                           ChunkOut& o) {
+  const double c15 = __ldg(pc + 32 * (LQ - 2)).y;
+  const double iv15 = ga[LQ - 2];
+  double A_ = pF[DIR * (LQ - 2)] * iv15;
+  double B_ = lam[LQ - 2] * iv15;
+  double G_ = -c15 * iv15;
+  o.ad = A_;
+  o.bd = B_;
+  o.gd = G_;
+  pF[DIR * (LQ - 2)] = A_;
+  sb[LQ - 2] = B_;
+  ga[LQ - 2] = G_;
+#pragma unroll
+  for (int k = LQ - 3; k >= 0; k--) {
+    const double cp = __ldg(pc + 32 * k).y, iv = ga[k];
+    A_ = fma(-cp, A_, pF[DIR * k]) * iv;
+    B_ = fma(-cp, B_, lam[k]) * iv;
+    G_ = -cp * G_ * iv;
+    pF[DIR * k] = A_;
+    sb[k] = B_;
+    ga[k] = G_;
+  }
+  o.au = A_;
+  o.bu = B_;
+  o.gu = G_;
+}
+
+template <int DIR>
+__device__ __forceinline__ void chunk_store(double* __restrict__ pF, const double* __restrict__ sb,
+                                            const double (&ga)[LQ - 1], double XL, double X) {
+#pragma unroll
+  for (int k = 0; k < LQ - 1; k++) pF[DIR * k] = fma(ga[k], X, fma(sb[k], XL, pF[DIR * k]));
+  pF[DIR * (LQ - 1)] = X;
+}
+
+}  // namespace
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
+    leg_sweep_kernel(LegArgs a) {
+  extern __shared__ __align__(128) double smem[];
+  double* F = smem;            // f, then the chunk scratch, then the new u
+  double* Ls = F + kLegArrF;   // u row on the low side
+  double* Hs = Ls + kLegArrU;  // u row on the high side
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Hs + kLegArrU);
+  double* xch = reinterpret_cast<double*>(bar + 1);  // [2 parities][P, Qh]
+  const int tid = threadIdx.x;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int n = a.n, ld = a.ld;
+
+  // every staged value a dummy point may read must be finite
+  for (int i = tid; i < kLegStage / 2; i += LT)
+    reinterpret_cast<double2*>(smem)[i] = make_double2(0, 0);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();  // the fields of the previous kernel are complete from here on
+
+  auto sched_at = [&](int s) -> int4 {
+    const int ci = cid + s * ncl;
+    return ci < a.nsched ? a.sched[ci] : make_int4(-2, -2, 0, 0);
+  };
+  int4 sc = sched_at(0);
+  if (tid < 32) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const int it = rank ? sc.y : sc.x;
+    if (it >= 0) issue_loads(a, it, smem, bar);
+  }
+  int nsplit = 0, phi = 0x7fffffff, ph = 0;
+  bool bad = false;
+  // phase clocks of a -DTMG_LEGK_TIMING build (make timing): setup, stage
+  // wait, forward, back, reduced system, branch, finalize, stores
+#ifdef TMG_LEGK_TIMING
+  long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tlast = clock64();
+  const bool timing = a.timing != nullptr && tid == 0;
+#define LEGK_MARK(i)                     \
+  do {                                   \
+    if (timing) {                        \
+      const long long tn = clock64();    \
+      tacc[i] += tn - tlast;             \
+      tlast = tn;                        \
+    }                                    \
+  } while (0)
+#else
+#define LEGK_MARK(i) \
+  do {               \
+  } while (0)
+#endif
+
+  for (int s = 0; sc.x != -2; s++) {
+    const int item = rank ? sc.y : sc.x;
+    const bool split = (sc.z & 1) != 0;
+    const int steps = (sc.z >> (rank ? 16 : 8)) & 0xff;
+    const int4 scn = sched_at(s + 1);
+
+    // ---- per-thread chunk setup (overlaps the wait for the staged rows) ----
+    uint16_t tm = 0xFFFF;
+    if (item >= 0) tm = a.tmap[(size_t)item * LT + tid];
+    const bool act = tm != 0xFFFF;
+    const int slot = tm >> 1, leg = tm & 1;
+    LegBlock B{};
+    if (act) B = a.blocks[a.items[item].blk0 + slot];
+    LegGeo g;
+    g.set(act ? B.k : 2, B.quad, leg, n);
+    const int m = g.m;
+    const int nch = (m + LQ - 1) / LQ;
+    const int pad = nch * LQ - m;
+    const int ch = act ? tid - (leg ? B.t0[1] : B.t0[0]) : 0;
+    const bool first = act && ch == 0, lastc = act && ch == nch - 1;
+    const int e0 = ch * LQ - pad;  // leg point of chunk point 0
+    double clo = 0.0, chi = 0.0;
+    if (act) {
+      clo = leg == 0 ? __ldg(a.S + g.bj) : __ldg(a.W + g.bi);
+      chi = leg == 0 ? __ldg(a.N + g.bj) : __ldg(a.E + g.bi);
+    }
+    const size_t cofs =
+        (size_t)(g.orient * LQ + pad) * a.cstride + (ch >> 5) * (32 * LQ) + (ch & 31);
+    const int bF = leg ? B.sb[1][0] : B.sb[0][0];
+    const int bL = leg ? B.sb[1][1] : B.sb[0][1];
+    const int bH = leg ? B.sb[1][2] : B.sb[0][2];
+    // branch row: frozen terms (the hub thread is the last chunk of leg 0, or
+    // of the CTA's own leg in a split block)
+    const bool hubthr = lastc && (leg == 0 || B.split == 2);
+    double hub_num = 0.0, den0 = 1.0, cx = 0.0, cy = 0.0;
+    if (hubthr) {
+      const int bi = g.bi, bj = g.bj;
+      const double Wi = __ldg(a.W + bi), Ei = __ldg(a.E + bi), Sj = __ldg(a.S + bj),
+                   Nj = __ldg(a.N + bj);
+      den0 = -(Wi + Ei + Sj + Nj);
+      cx = g.sx > 0 ? Wi : Ei;  // toward the x-leg end
+      cy = g.sy > 0 ? Sj : Nj;  // toward the y-leg end
+      const double ex = g.sx > 0 ? Ei : Wi, ey = g.sy > 0 ? Nj : Sj;
+      hub_num = a.fn[(size_t)bi * ld + bj] - ex * a.un[(size_t)(bi + g.sx) * ld + bj] -
+                ey * a.ut[(size_t)(bj + g.sy) * ld + bi];
+    }
+    double tipfold = 0.0, uwall = 0.0;
+    if (first) {  // Dirichlet neighbour of the tip (N buffer ring) times its coupling
+      const double ubd = leg == 0 ? a.un[(size_t)(g.p0 - g.sx) * ld + g.bj]
+                                  : a.un[(size_t)g.bi * ld + (g.p0 - g.sy)];
+      const int tp = g.p0;
+      const double at = leg == 0 ? (g.sx > 0 ? __ldg(a.W + tp) : __ldg(a.E + tp))
+                                 : (g.sy > 0 ? __ldg(a.S + tp) : __ldg(a.N + tp));
+      tipfold = at * ubd;
+    }
+    // x-leg's last point: true wall-side neighbour (1: the u-1 row, 2: the u+1 row)
+    const int wallfix = (lastc && leg == 0) ? (g.sy > 0 ? 1 : 2) : 0;
+    if (wallfix) uwall = a.un[(size_t)(g.p0 + g.sx * (m - 1)) * ld + (g.bj - g.sy)];
+
+    LEGK_MARK(0);
+    if (item >= 0) {
+      mbar_wait(bar, (unsigned)ph);
+      ph ^= 1;
+    }
+    LEGK_MARK(1);
+    double lam[LQ - 1], ga[LQ - 1];
+    ChunkOut co{0, 1, 0, 0, 0, 1, 0, 0, 0, 0x7fffffff};
+    double* pF = F + bF + g.dir * e0;
+    if (act) {
+      if (first) pF[g.dir * pad] -= tipfold;  // only this thread reads the tip's f
+      if (g.dir > 0)
+        chunk_forward<1>(pF, Ls + bL + e0, Hs + bH + e0, a.coef + cofs, a.diag + cofs, clo, chi,
+                         first, wallfix, uwall, lam, ga, co);
+      else
+        chunk_forward<-1>(pF, Ls + bL - e0, Hs + bH - e0, a.coef + cofs, a.diag + cofs, clo,
+                          chi, first, wallfix, uwall, lam, ga, co);
+    }
+    phi = min(phi, co.phi);
+    __syncthreads();  // every thread is done with the staged u rows
+    LEGK_MARK(2);
+    double* sb = Hs + tid * LQ;  // this thread's beta row
+    if (act) {
+      if (g.dir > 0)
+        chunk_back<1>(pF, sb, a.coef + cofs, lam, ga, co);
+      else
+        chunk_back<-1>(pF, sb, a.coef + cofs, lam, ga, co);
+    }
+
+    // ---- reduced system over the chunk ends (shared memory in Ls) ----------
+    double2* sFU = reinterpret_cast<double2*>(Ls);  // first-point forms (au, bu)
+    double* sGU = Ls + 2 * LT;                      // ... gu
+    // PCR rows, two buffers of 5 LT doubles: (A, C) pairs, (D, H) pairs, 1/B
+    auto rAC = [&](int b) { return reinterpret_cast<double2*>(Ls + (3 + 5 * b) * LT); };
+    auto rDH = [&](int b) { return reinterpret_cast<double2*>(Ls + (5 + 5 * b) * LT); };
+    auto rIB = [&](int b) { return Ls + (7 + 5 * b) * LT; };
+    double* sP = Ls + 13 * LT;  // X = P - Qh * x_branch
+    double* sQ = Ls + 14 * LT;
+    double* sX = Ls + 15 * LT;  // branch value per block slot
+    sFU[tid] = make_double2(co.au, co.bu);
+    sGU[tid] = co.gu;
+    __syncthreads();
+    LEGK_MARK(3);
+    double A = 0.0, Bv = 1.0, C = 0.0, D = 0.0, H = 0.0;
+    if (act) {
+      const double ae = co.a_end, ce = co.c_end;
+      const double bbe = __ldg(a.diag + cofs + 32 * (LQ - 1)) - (clo + chi);
+      A = first ? 0.0 : ae * co.bd;
+      Bv = fma(ae, co.gd, bbe);
+      D = fma(-ae, co.ad, co.r_end);
+      if (lastc) {
+        H = ce;  // the branch
+      } else {
+        const double2 fu = sFU[tid + 1];
+        Bv = fma(ce, fu.y, Bv);
+        C = ce * sGU[tid + 1];
+        D = fma(-ce, fu.x, D);
+      }
+    }
+    double iB = drcp(Bv);
+    // parallel cyclic reduction, double-buffered (one barrier per step).  A row
+    // whose partner at distance d lies outside the CTA has no coupling that far
+    // (legs never cross items), so the clamped partner only needs to be finite.
+    rAC(0)[tid] = make_double2(A, C);
+    rDH(0)[tid] = make_double2(D, H);
+    rIB(0)[tid] = iB;
+    __syncthreads();
+    for (int stp = 0; stp < steps; stp++) {
+      const int d = 1 << stp, src = stp & 1;
+      const int im = max(tid - d, 0), ip = min(tid + d, LT - 1);
+      const double2 acm = rAC(src)[im], dhm = rDH(src)[im];
+      const double2 acp = rAC(src)[ip], dhp = rDH(src)[ip];
+      const double k1 = A * rIB(src)[im], k2 = C * rIB(src)[ip];
+      A = -k1 * acm.x;
+      C = -k2 * acp.y;
+      Bv = fma(-k2, acp.x, fma(-k1, acm.y, Bv));
+      D = fma(-k2, dhp.x, fma(-k1, dhm.x, D));
+      H = fma(-k2, dhp.y, fma(-k1, dhm.y, H));
+      iB = drcp(Bv);
+      rAC(src ^ 1)[tid] = make_double2(A, C);
+      rDH(src ^ 1)[tid] = make_double2(D, H);
+      rIB(src ^ 1)[tid] = iB;
+      __syncthreads();
+    }
+    LEGK_MARK(4);
+    if (act) phi = min(phi, __double2hiint(Bv) & 0x7fffffff);
+    const double P = D * iB, Qh = H * iB;
+    sP[tid] = P;
+    sQ[tid] = Qh;
+    if (split) {
+      // the leg end of each CTA's half of a split block goes to the peer
+      const int par = nsplit & 1;
+      if (hubthr) {
+        xch[2 * par] = P;
+        xch[2 * par + 1] = Qh;
+      }
+      cluster_arrive();
+      cluster_wait();
+    } else {
+      __syncthreads();
+    }
+
+    // ---- branch rows ----------------------------------------------------------
+    if (hubthr) {
+      double px, qx, py, qy;
+      if (B.split) {
+        const int par = nsplit & 1;
+        const double* peer = cluster.map_shared_rank(xch, rank ^ 1);
+        const double pp = peer[2 * par], qp = peer[2 * par + 1];
+        if (leg == 0) { px = P; qx = Qh; py = pp; qy = qp; }
+        else { px = pp; qx = qp; py = P; qy = Qh; }
+      } else {
+        const int ty = B.t0[1] + nch - 1;
+        px = P;
+        qx = Qh;
+        py = sP[ty];
+        qy = sQ[ty];
+      }
+      const double den = den0 - cx * qx - cy * qy;
+      bad |= bad_pivot(den);
+      const double xb = (hub_num - cx * px - cy * py) / den;
+      sX[slot] = xb;
+      if (B.split != 2) a.un[(size_t)g.bi * ld + g.bj] = xb;
+    }
+    if (split) nsplit++;
+    __syncthreads();
+    LEGK_MARK(5);
+
+    // ---- finalize into the f slots ------------------------------------------
+    if (act) {
+      const double xb = sX[slot];
+      const double X = fma(-Qh, xb, P);
+      const double XL = first ? 0.0 : fma(-sQ[tid - 1], xb, sP[tid - 1]);
+      if (g.dir > 0)
+        chunk_store<1>(pF, sb, ga, XL, X);
+      else
+        chunk_store<-1>(pF, sb, ga, XL, X);
+    }
+    __syncthreads();
+    LEGK_MARK(6);
+
+    // ---- stores (bulk copies of the aligned leg interiors, single elements
+    // at the unaligned ends), then the next item's loads: warp 0 only ---------
+    if (tid < 32) {
+      if (item >= 0) {
+        const LegItem I = a.items[item];
+        for (int c = tid; c < I.nedge; c += 32) {
+          const LegCopy cp = a.copies[I.edge0 + c];
+          (cp.src == 3 ? a.ut : a.un)[cp.g] = F[cp.s];
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int c = tid; c < I.nstore; c += 32) {
+          const LegCopy cp = a.copies[I.store0 + c];
+          bulk_s2g((cp.src == 3 ? a.ut : a.un) + cp.g, F + cp.s, (unsigned)cp.n * 8u);
+        }
+        bulk_commit();
+      }
+      const int nx = rank ? scn.y : scn.x;
+      if (nx >= 0) {
+        bulk_wait_read();  // the stores have left shared memory
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_loads(a, nx, smem, bar);
+      }
+    }
+    LEGK_MARK(7);
+    sc = scn;
+  }
+#undef LEGK_MARK
+#ifdef TMG_LEGK_TIMING
+  if (timing)
+    for (int i = 0; i < 8; i++) a.timing[blockIdx.x * 8 + i] = tacc[i];
+#endif
+  if (tid < 32) bulk_wait_all();
+  bad |= phi < 0x01A56E1F;  // |pivot| < 1e-300 (high word of 1e-300)
+  if (bad) atomicOr(a.err, 1);
+  pdl_trigger();
+  // no CTA may exit while its peer can still read its exchange slots
+  cluster_arrive();
+  cluster_wait();
+}
+
+// ============================ host side =====================================
+
+namespace {
+
+struct HostBlock {
+  int k, quad, chunks;  // chunks per leg
+};
+
+inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+bool leg_plan_applies(int scheme, int nx, int ny, int mode) {
+  static int enabled = -1;
+  if (enabled < 0) {
+    const char* s = std::getenv("TMG_LEGK");
+    enabled = s ? std::atoi(s) != 0 : 1;
+  }
+  static int nmin = 0;
+  if (!nmin) {
+    const char* s = std::getenv("TMG_LEGK_NMIN");
+    nmin = s && std::atoi(s) > 0 ? std::atoi(s) : kLegNmin;
+  }
+  return enabled && scheme == SCHEME_TWEED && mode == LM_TWEED && nx == ny && nx >= nmin &&
+         nx % 2 == 0;
+}
+
+int leg_k0() {
+  static int k0 = 0;
+  if (!k0) {
+    const char* s = std::getenv("TMG_LEGK_K0");
+    k0 = s && std::atoi(s) >= 3 ? std::atoi(s) : kLegK0;
+  }
+  return k0;
+}
+
+// Blocks of one colour on an n x n grid handled by the leg kernel: shells
+// k in [k0, c) of that colour, the four quadrants (layout.py:75-84).
+static void colour_blocks(int n, int red, std::vector<HostBlock>& out) {
+  const int c = n / 2;  // (s + 1) / 2 with s = n - 1
+  for (int k = c - 1; k >= leg_k0(); k--) {
+    if (((k % 2) != 0) != (red != 0)) continue;  // layout.py:22-23
+    for (int q = 0; q < 4; q++) out.push_back(HostBlock{k, q, ceil_div(k - 1, LQ)});
+  }
+}
+
+std::string build_leg_plan(int n, LegPlan& P) {
+  P = LegPlan();
+  P.n = n;
+  const int ld = n + 1;
+  for (int red = 1; red >= 0; red--) {
+    LegColour& C = P.col[red];
+    std::vector<HostBlock> blocks;
+    colour_blocks(n, red, blocks);
+    std::vector<LegItem> items;
+    std::vector<LegBlock> iblocks;
+    std::vector<uint16_t> tmap;
+    std::vector<LegCopy> copies;
+    std::vector<int> item_chunks;
+
+    struct Open {
+      std::vector<std::pair<HostBlock, int>> members;  // block, split (0/1/2)
+      int chunks = 0;
+    };
+    auto emit = [&](const Open& o) -> int {
+      LegItem it{};
+      it.blk0 = (int32_t)iblocks.size();
+      it.nblk = (int16_t)o.members.size();
+      std::vector<uint16_t> map(LT, 0xFFFF);
+      std::vector<LegCopy> loads, stores, edges;
+      int t = 0, soff[3] = {kLegHead, kLegHead, kLegHead}, maxch = 1;
+      long bytes = 0;
+      for (size_t bi = 0; bi < o.members.size(); bi++) {
+        const HostBlock& hb = o.members[bi].first;
+        const int split = o.members[bi].second;
+        LegBlock lb{};
+        lb.k = (int16_t)hb.k;
+        lb.quad = (uint8_t)hb.quad;
+        lb.split = (uint8_t)split;
+        lb.t0[0] = lb.t0[1] = -1;
+        const int sx = (hb.quad & 1) ? -1 : 1, sy = (hb.quad & 2) ? -1 : 1;
+        const int x0 = sx > 0 ? 1 : n - 1, y0 = sy > 0 ? 1 : n - 1;
+        const int bi_ = x0 + sx * (hb.k - 1), bj_ = y0 + sy * (hb.k - 1), m = hb.k - 1;
+        for (int leg = 0; leg < 2; leg++) {
+          if ((split == 1 && leg == 1) || (split == 2 && leg == 0)) continue;
+          lb.t0[leg] = (int16_t)t;
+          for (int c = 0; c < hb.chunks; c++) map[t + c] = (uint16_t)((bi << 1) | leg);
+          t += hb.chunks;
+          maxch = std::max(maxch, hb.chunks);
+          const int dir = leg == 0 ? sx : sy, p0 = leg == 0 ? x0 : y0;
+          const int row = leg == 0 ? bj_ : bi_;
+          const int lo = std::min(p0, p0 + dir * (m - 1)), hi = std::max(p0, p0 + dir * (m - 1));
+          long gsF = 0;
+          int soffF = 0;
+          const int nchl = hb.chunks, padl = nchl * LQ - m;
+          for (int arr = 0; arr < 3; arr++) {
+            const long r = arr == 0 ? row : arr == 1 ? row - 1 : row + 1;
+            const long g0 = r * ld + lo, g1 = r * ld + hi + 1;  // [g0, g1)
+            const long gs = g0 & ~1L, ge = (g1 + 1) & ~1L;
+            const long gtip = r * ld + p0;
+            // the tip chunk's dummies write a private gap in front of the tip
+            // (before the run for ascending legs, after it for descending ones)
+            const int gap_lo = arr == 0 && dir > 0 ? std::max(0, padl - (int)(gtip - gs)) : 0;
+            const int gap_hi = arr == 0 && dir < 0 ? std::max(0, padl - (int)(ge - 1 - gtip)) : 0;
+            soff[arr] += (gap_lo + 1) & ~1;
+            LegCopy cp{};
+            cp.g = gs;
+            cp.s = (arr == 0 ? 0 : arr == 1 ? kLegArrF : kLegArrF + kLegArrU) + soff[arr];
+            cp.n = (int32_t)(ge - gs);
+            // sources: 0 f N, 1 f T, 2 u N, 3 u T
+            cp.src = (uint8_t)(arr == 0 ? (leg == 0 ? 1 : 0) : (leg == 0 ? 3 : 2));
+            loads.push_back(cp);
+            bytes += 8L * cp.n;
+            lb.sb[leg][arr] = (int16_t)(soff[arr] + (gtip - gs));
+            if (arr == 0) {
+              gsF = gs;
+              soffF = soff[arr];
+            }
+            soff[arr] += (int)(ge - gs) + ((gap_hi + 1) & ~1);
+            if (soff[arr] + kLegHead > (arr == 0 ? kLegArrF : kLegArrU)) return -1;
+          }
+          // the new values: bulk stores of the 16-byte aligned interior of the
+          // leg's run, single elements at unaligned ends
+          const long glo = (long)row * ld + lo, ghi = (long)row * ld + hi;
+          const long is = (glo + 1) & ~1L, ie = (ghi + 1) & ~1L;
+          const uint8_t dst = (uint8_t)(leg == 0 ? 3 : 2);
+          if (ie > is) {
+            LegCopy cp{};
+            cp.g = is;
+            cp.s = soffF + (int)(is - gsF);
+            cp.n = (int32_t)(ie - is);
+            cp.src = dst;
+            stores.push_back(cp);
+          }
+          for (long ge_ : {glo, ghi}) {
+            if (ge_ >= is && ge_ < ie) continue;
+            if (ge_ == ghi && ghi == glo && !edges.empty() && edges.back().g == ge_) continue;
+            LegCopy cp{};
+            cp.g = ge_;
+            cp.s = soffF + (int)(ge_ - gsF);
+            cp.n = 1;
+            cp.src = dst;
+            edges.push_back(cp);
+          }
+        }
+        iblocks.push_back(lb);
+      }
+      it.copy0 = (int32_t)copies.size();
+      it.ncopy = (int32_t)loads.size();
+      copies.insert(copies.end(), loads.begin(), loads.end());
+      it.store0 = (int32_t)copies.size();
+      it.nstore = (int32_t)stores.size();
+      copies.insert(copies.end(), stores.begin(), stores.end());
+      it.edge0 = (int32_t)copies.size();
+      it.nedge = (int32_t)edges.size();
+      copies.insert(copies.end(), edges.begin(), edges.end());
+      it.bytes = (int32_t)bytes;
+      int steps = 0;
+      while ((1 << steps) < maxch) steps++;
+      it.steps = (int16_t)steps;
+      items.push_back(it);
+      tmap.insert(tmap.end(), map.begin(), map.end());
+      item_chunks.push_back(t);
+      return (int)items.size() - 1;
+    };
+
+    // split blocks: one item per leg, scheduled on the two CTAs of a cluster
+    std::vector<int4> sched_split;
+    std::vector<Open> open;
+    for (const HostBlock& hb : blocks) {
+      if (hb.chunks > LT / 2) {
+        Open a_, b_;
+        a_.members.push_back({hb, 1});
+        a_.chunks = hb.chunks;
+        b_.members.push_back({hb, 2});
+        b_.chunks = hb.chunks;
+        const int ia = emit(a_), ib = emit(b_);
+        if (ia < 0 || ib < 0) return "leg plan: staging overflow";
+        sched_split.push_back(
+            make_int4(ia, ib, 1 | (items[ia].steps << 8) | (items[ib].steps << 16), hb.chunks));
+        continue;
+      }
+      // first fit (blocks arrive in decreasing size)
+      bool placed = false;
+      for (Open& o : open) {
+        if (o.chunks + 2 * hb.chunks <= LT && (int)o.members.size() < kLegMaxBlocks) {
+          o.members.push_back({hb, 0});
+          o.chunks += 2 * hb.chunks;
+          placed = true;
+          break;
+        }
+      }
+      if (!placed) {
+        Open o;
+        o.members.push_back({hb, 0});
+        o.chunks = 2 * hb.chunks;
+        open.push_back(o);
+      }
+    }
+    std::vector<std::pair<int, int>> whole;  // (chunks, item)
+    for (const Open& o : open) {
+      const int id = emit(o);
+      if (id < 0) return "leg plan: staging overflow";
+      whole.push_back({o.chunks, id});
+    }
+    std::sort(whole.begin(), whole.end(), [](auto& x, auto& y) { return x.first > y.first; });
+    std::vector<int4> sched = sched_split;
+    for (size_t i = 0; i < whole.size(); i += 2) {
+      const int ia = whole[i].second;
+      const int ib = i + 1 < whole.size() ? whole[i + 1].second : -1;
+      const int sb = ib >= 0 ? items[ib].steps : 0;
+      sched.push_back(make_int4(ia, ib, (items[ia].steps << 8) | (sb << 16), whole[i].first));
+    }
+    C.nsched = (int)sched.size();
+    C.nitems = (int)items.size();
+    C.points = 0;
+    for (const HostBlock& hb : blocks) C.points += 2L * (hb.k - 1) + 1;
+    std::string err;
+    auto up = [&](auto& v, auto*& d) {
+      using T = typename std::remove_reference<decltype(v)>::type::value_type;
+      if (v.empty()) return;
+      if (cudaMalloc(&d, v.size() * sizeof(T)) != cudaSuccess ||
+          cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess)
+        err = "leg plan upload failed";
+      P.device_bytes += v.size() * sizeof(T);
+    };
+    up(items, C.items);
+    up(iblocks, C.blocks);
+    up(tmap, C.tmap);
+    up(copies, C.copies);
+    up(sched, C.sched);
+    if (!err.empty()) return err;
+  }
+  return "";
+}
+
+std::string leg_plan_set_coefs(LegPlan& P, const double* W, const double* E, const double* S,
+                               const double* N) {
+  const int n = P.n;
+  const int mmax = n / 2 - 2;  // longest leg (shell c - 1)
+  const int nch = ceil_div(std::max(mmax, 1), LQ);
+  const int cstride = ceil_div(nch, 32) * 32 * LQ;
+  std::vector<double2> h((size_t)4 * LQ * cstride, make_double2(0.0, 0.0));
+  std::vector<double> hd((size_t)4 * LQ * cstride, -1.0);
+  for (int o = 0; o < 4; o++) {
+    for (int pad = 0; pad < LQ; pad++) {
+      const size_t base = (size_t)(o * LQ + pad) * cstride;
+      for (int ch = 0; ch < nch; ch++) {
+        for (int k = 0; k < LQ; k++) {
+          const int e = ch * LQ + k - pad;  // leg point (tip = 0)
+          if (e < 0 || e > n - 2) continue;  // dummies: no coupling
+          const int pos = (o % 2 == 0) ? 1 + e : n - 1 - e;
+          double av, cv;
+          switch (o) {
+            case 0: av = W[pos]; cv = E[pos]; break;
+            case 1: av = E[pos]; cv = W[pos]; break;
+            case 2: av = S[pos]; cv = N[pos]; break;
+            default: av = N[pos]; cv = S[pos]; break;
+          }
+          const size_t ix = base + (ch >> 5) * (32 * LQ) + k * 32 + (ch & 31);
+          // the tip's coupling toward the wall is folded into f (not eliminated)
+          h[ix] = make_double2(e == 0 ? 0.0 : av, cv);
+          hd[ix] = -(av + cv);
+        }
+      }
+    }
+  }
+  P.cstride = cstride;
+  if (cudaMalloc(&P.coef, h.size() * sizeof(double2)) != cudaSuccess ||
+      cudaMemcpy(P.coef, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice) !=
+          cudaSuccess ||
+      cudaMalloc(&P.diag, hd.size() * sizeof(double)) != cudaSuccess ||
+      cudaMemcpy(P.diag, hd.data(), hd.size() * sizeof(double), cudaMemcpyHostToDevice) !=
+          cudaSuccess)
+    return "leg plan coefficient upload failed";
+  P.device_bytes += h.size() * sizeof(double2) + hd.size() * sizeof(double);
+  return "";
+}
+
+void free_leg_plan(LegPlan& P) {
+  for (LegColour& C : P.col) {
+    cudaFree(C.items);
+    cudaFree(C.blocks);
+    cudaFree(C.tmap);
+    cudaFree(C.copies);
+    cudaFree(C.sched);
+    C = LegColour();
+  }
+  cudaFree(P.coef);
+  cudaFree(P.diag);
+  P.coef = nullptr;
+  P.diag = nullptr;
+}
+
+size_t leg_smem_bytes() { return sizeof(double) * kLegStage + sizeof(uint64_t) + 64; }
+
+cudaError_t init_leg_kernel() {
+  static cudaError_t done = cudaErrorNotReady;
+  if (done == cudaErrorNotReady)
+    done = cudaFuncSetAttribute(leg_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)leg_smem_bytes());
+  return done;
+}
+
+namespace {
+long long* g_leg_timing = nullptr;
+int g_leg_timing_ctas = 0;
+bool leg_timing_on() {
+  static int on = -1;
+  if (on < 0) {
+    const char* s = std::getenv("TMG_LEGK_TIMING");
+    on = s && std::atoi(s) != 0;
+  }
+  return on != 0;
+}
+}  // namespace
+
+cudaError_t launch_leg_colour(const LegPlan& P, int red, const SweepArgs& s, cudaStream_t stream) {
+  const LegColour& C = P.col[red ? 1 : 0];
+  if (C.nsched == 0) return cudaSuccess;
+  cudaError_t e = init_leg_kernel();
+  if (e != cudaSuccess) return e;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
+  }
+  LegArgs a{};
+  a.un = s.u;
+  a.ut = s.ut;
+  a.fn = s.f;
+  a.ft = s.ft;
+  a.W = s.W;
+  a.E = s.E;
+  a.S = s.S;
+  a.N = s.N;
+  a.coef = P.coef;
+  a.diag = P.diag;
+  a.cstride = P.cstride;
+  a.n = P.n;
+  a.ld = P.n + 1;
+  a.items = C.items;
+  a.blocks = C.blocks;
+  a.tmap = C.tmap;
+  a.copies = C.copies;
+  a.sched = C.sched;
+  a.nsched = C.nsched;
+  a.err = s.err;
+  const int ncl = std::max(1, std::min(sms, C.nsched));  // two CTAs per SM
+  a.timing = nullptr;
+  if (leg_timing_on()) {
+    if (!g_leg_timing) cudaMalloc(&g_leg_timing, sizeof(long long) * 8 * 2 * 1024);
+    a.timing = g_leg_timing;
+    g_leg_timing_ctas = 2 * ncl;
+  }
+  TMG_COUNT(1);
+  return launch_pdl(leg_sweep_kernel, dim3(2 * ncl), dim3(LT), leg_smem_bytes(), stream, a);
+}
+
+}  // namespace tmg
+
+// Average per-CTA clock cycles of the leg kernel's phases in its last launch
+// (TMG_LEGK_TIMING=1 only): setup, stage wait, forward, back, reduced system,
+// branch, finalize, stores.  Returns the number of CTAs averaged.
+extern "C" int tmg_debug_leg_phases(double* out8) {
+  for (int i = 0; i < 8; i++) out8[i] = 0.0;
+  if (!tmg::g_leg_timing || tmg::g_leg_timing_ctas == 0) return 0;
+  std::vector<long long> h(8 * (size_t)tmg::g_leg_timing_ctas);
+  if (cudaMemcpy(h.data(), tmg::g_leg_timing, h.size() * sizeof(long long),
+                 cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  for (size_t c = 0; c < (size_t)tmg::g_leg_timing_ctas; c++)
+    for (int i = 0; i < 8; i++) out8[i] += (double)h[c * 8 + i];
+  for (int i = 0; i < 8; i++) out8[i] /= tmg::g_leg_timing_ctas;
+  return tmg::g_leg_timing_ctas;
+}
