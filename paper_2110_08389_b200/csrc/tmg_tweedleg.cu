@@ -129,15 +129,17 @@ struct LegGeo {
   }
 };
 
-// issue an item's bulk loads (warp 0)
+// issue an item's bulk loads (warp 0).  part -1: everything; part 0: the
+// transaction bytes and the u rows; part 1: the f runs.
 __device__ __forceinline__ void issue_loads(const LegArgs& a, int item, double* stage,
-                                            uint64_t* bar) {
+                                            uint64_t* bar, int part = -1) {
   const int lane = threadIdx.x & 31;
   const LegItem I = a.items[item];
-  if (lane == 0) mbar_expect_tx(bar, (unsigned)I.bytes);
+  if (part <= 0 && lane == 0) mbar_expect_tx(bar, (unsigned)I.bytes);
   __syncwarp();
   for (int c = lane; c < I.ncopy; c += 32) {
     const LegCopy cp = a.copies[I.copy0 + c];
+    if (part >= 0 && (cp.s < kLegArrF) != (part == 1)) continue;
     const double* src = cp.src == 0 ? a.fn : cp.src == 1 ? a.ft : cp.src == 2 ? a.un : a.ut;
     bulk_g2s(stage + cp.s, src + cp.g, (unsigned)cp.n * 8u, bar);
   }
@@ -159,16 +161,20 @@ __device__ __forceinline__ void bulk_wait_all() {
 }
 
 // One thread's chunk of 17 consecutive leg points: point k's f slot is
-// pF[DIR * k] (also the chunk's scratch: rho, then alpha, then the solution),
-// its u neighbours pL / pH[DIR * k], its couplings pc[32 * k] = (a, c) toward
-// the previous / next point and pd[32 * k] = -(a + c) (the along part of the
-// diagonal).  The tip chunk holds `pad` dummy points in front of the tip:
-// zero couplings, and the tip's own coupling toward them is zero too (its
-// Dirichlet neighbour is folded into f), so dummies are decoupled and only
-// touch the private gap the plan leaves before the tip's f slot.  Every chunk
-// is therefore full and the leg's last chunk ends on the leg's last point.
-// Leaves x_k = alpha_k + be_k * Xleft + ga_k * X (k < 16, X = point 16) with
-// alpha in the f slots.
+// pF[DIR * k] (also the chunk's scratch: rho / p, then alpha, then the
+// solution), its u neighbours pL / pH[DIR * k] and its couplings
+// pc[32 * k] = (a, c) toward the previous / next point (the diagonal is
+// -(a + c + cross couplings)).  The tip chunk holds `pad` dummy points in
+// front of the tip with couplings (1e300, 0): their reciprocal pivots vanish,
+// so the tip is decoupled from them (its Dirichlet neighbour is folded into
+// f) and they only touch the private gap the plan leaves before the tip's f
+// slot.  Every chunk is therefore full and the leg's last chunk ends on the
+// leg's last point.
+//
+// The forward pass keeps, per interior point k, the pivot-scaled data
+// rho_k / p_k (f slot), lam_k / p_k and c_k / p_k (registers), so the back
+// pass needs no coefficient reload: x_k = alpha_k + be_k * Xleft + ga_k * X
+// (k < 16, X = point 16) with alpha in the f slots.
 struct ChunkOut {
   double ad, bd, gd;  // form of point 15
   double au, bu, gu;  // form of point 0
@@ -180,10 +186,9 @@ template <int DIR>
 __device__ __forceinline__ void chunk_forward(double* __restrict__ pF,
                                               const double* __restrict__ pL,
                                               const double* __restrict__ pH,
-                                              const double2* __restrict__ pc,
-                                              const double* __restrict__ pd, double clo,
+                                              const double2* __restrict__ pc, double clo,
                                               double chi, bool first, int wallfix, double uwall,
-                                              double (&lam)[LQ - 1], double (&ivr)[LQ - 1],
+                                              double (&lam)[LQ - 1], double (&cg_)[LQ - 1],
                                               ChunkOut& o) {
   const double csum = clo + chi;
   double ivp = 0.0, rho = 0.0, lm = 0.0, cprev = 0.0;
@@ -192,7 +197,7 @@ __device__ __forceinline__ void chunk_forward(double* __restrict__ pF,
   for (int k = 0; k < LQ - 1; k++) {
     const double r = fma(-chi, pH[DIR * k], fma(-clo, pL[DIR * k], pF[DIR * k]));
     const double2 ac = __ldg(pc + 32 * k);
-    const double bb = __ldg(pd + 32 * k) - csum;
+    const double bb = -(ac.x + ac.y + csum);
     double bp;
     if (k == 0) {
       bp = bb;
@@ -206,9 +211,9 @@ __device__ __forceinline__ void chunk_forward(double* __restrict__ pF,
     }
     phi = min(phi, __double2hiint(bp) & 0x7fffffff);
     ivp = drcp(bp);
-    pF[DIR * k] = rho;
-    lam[k] = lm;
-    ivr[k] = ivp;
+    pF[DIR * k] = rho * ivp;
+    lam[k] = lm * ivp;
+    cg_[k] = ac.y * ivp;
     cprev = ac.y;
   }
   constexpr int k = LQ - 1;  // the chunk-end row
@@ -228,29 +233,25 @@ __device__ __forceinline__ void chunk_forward(double* __restrict__ pF,
 }
 
 // affine back pass: alpha into the f slots, beta into the thread's row of
-// the scratch (stride 17: conflict-free), gamma stays in registers
+// the scratch (stride 17: conflict-free), gamma in place of c / p
 template <int DIR>
 __device__ __forceinline__ void chunk_back(double* __restrict__ pF, double* __restrict__ sb,
-                                           const double2* __restrict__ pc,
                                            const double (&lam)[LQ - 1], double (&ga)[LQ - 1],
                                            ChunkOut& o) {
-  const double c15 = __ldg(pc + 32 * (LQ - 2)).y;
-  const double iv15 = ga[LQ - 2];
-  double A_ = pF[DIR * (LQ - 2)] * iv15;
-  double B_ = lam[LQ - 2] * iv15;
-  double G_ = -c15 * iv15;
+  double A_ = pF[DIR * (LQ - 2)];
+  double B_ = lam[LQ - 2];
+  double G_ = -ga[LQ - 2];
   o.ad = A_;
   o.bd = B_;
   o.gd = G_;
-  pF[DIR * (LQ - 2)] = A_;
   sb[LQ - 2] = B_;
   ga[LQ - 2] = G_;
 #pragma unroll
   for (int k = LQ - 3; k >= 0; k--) {
-    const double cp = __ldg(pc + 32 * k).y, iv = ga[k];
-    A_ = fma(-cp, A_, pF[DIR * k]) * iv;
-    B_ = fma(-cp, B_, lam[k]) * iv;
-    G_ = -cp * G_ * iv;
+    const double g = ga[k];
+    A_ = fma(-g, A_, pF[DIR * k]);
+    B_ = fma(-g, B_, lam[k]);
+    G_ = -g * G_;
     pF[DIR * k] = A_;
     sb[k] = B_;
     ga[k] = G_;
@@ -299,6 +300,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     return ci < a.nsched ? a.sched[ci] : make_int4(-2, -2, 0, 0);
   };
   int4 sc = sched_at(0);
+#ifdef TMG_LEGK_PREFETCH
+  auto tm_of = [&](const int4& e) -> uint16_t {
+    const int it = rank ? e.y : e.x;
+    return it >= 0 ? a.tmap[(size_t)it * LT + tid] : (uint16_t)0xFFFF;
+  };
+  auto block_of = [&](const int4& e, uint16_t t) -> LegBlock {
+    LegBlock b{};
+    const int it = rank ? e.y : e.x;
+    if (it >= 0 && t != 0xFFFF) b = a.blocks[a.items[it].blk0 + (t >> 1)];
+    return b;
+  };
+  uint16_t tmC = tm_of(sc);
+  LegBlock BC = block_of(sc, tmC);
+#endif
   if (tid < 32) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     const int it = rank ? sc.y : sc.x;
@@ -311,7 +326,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
 #ifdef TMG_LEGK_TIMING
   long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tlast = clock64();
-  const bool timing = a.timing != nullptr && tid == 0;
+  const bool timing = a.timing != nullptr && (tid == 0 || tid == 96);
 #define LEGK_MARK(i)                     \
   do {                                   \
     if (timing) {                        \
@@ -333,12 +348,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     const int4 scn = sched_at(s + 1);
 
     // ---- per-thread chunk setup (overlaps the wait for the staged rows) ----
+#ifdef TMG_LEGK_PREFETCH
+    const uint16_t tm = tmC;
+    const bool act = tm != 0xFFFF;
+    const int slot = tm >> 1, leg = tm & 1;
+    const LegBlock B = BC;
+#else
     uint16_t tm = 0xFFFF;
     if (item >= 0) tm = a.tmap[(size_t)item * LT + tid];
     const bool act = tm != 0xFFFF;
     const int slot = tm >> 1, leg = tm & 1;
     LegBlock B{};
     if (act) B = a.blocks[a.items[item].blk0 + slot];
+#endif
     LegGeo g;
     g.set(act ? B.k : 2, B.quad, leg, n);
     const int m = g.m;
@@ -372,14 +394,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
       hub_num = a.fn[(size_t)bi * ld + bj] - ex * a.un[(size_t)(bi + g.sx) * ld + bj] -
                 ey * a.ut[(size_t)(bj + g.sy) * ld + bi];
     }
-    double tipfold = 0.0, uwall = 0.0;
-    if (first) {  // Dirichlet neighbour of the tip (N buffer ring) times its coupling
-      const double ubd = leg == 0 ? a.un[(size_t)(g.p0 - g.sx) * ld + g.bj]
-                                  : a.un[(size_t)g.bi * ld + (g.p0 - g.sy)];
+    double tip_u = 0.0, tip_a = 0.0, uwall = 0.0;
+    if (first) {  // Dirichlet neighbour of the tip (N buffer ring) and its coupling
+      tip_u = leg == 0 ? a.un[(size_t)(g.p0 - g.sx) * ld + g.bj]
+                       : a.un[(size_t)g.bi * ld + (g.p0 - g.sy)];
       const int tp = g.p0;
-      const double at = leg == 0 ? (g.sx > 0 ? __ldg(a.W + tp) : __ldg(a.E + tp))
-                                 : (g.sy > 0 ? __ldg(a.S + tp) : __ldg(a.N + tp));
-      tipfold = at * ubd;
+      tip_a = leg == 0 ? (g.sx > 0 ? __ldg(a.W + tp) : __ldg(a.E + tp))
+                       : (g.sy > 0 ? __ldg(a.S + tp) : __ldg(a.N + tp));
     }
     // x-leg's last point: true wall-side neighbour (1: the u-1 row, 2: the u+1 row)
     const int wallfix = (lastc && leg == 0) ? (g.sy > 0 ? 1 : 2) : 0;
@@ -395,23 +416,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     ChunkOut co{0, 1, 0, 0, 0, 1, 0, 0, 0, 0x7fffffff};
     double* pF = F + bF + g.dir * e0;
     if (act) {
-      if (first) pF[g.dir * pad] -= tipfold;  // only this thread reads the tip's f
+      if (first) pF[g.dir * pad] -= tip_a * tip_u;  // only this thread reads the tip's f
       if (g.dir > 0)
-        chunk_forward<1>(pF, Ls + bL + e0, Hs + bH + e0, a.coef + cofs, a.diag + cofs, clo, chi,
+        chunk_forward<1>(pF, Ls + bL + e0, Hs + bH + e0, a.coef + cofs, clo, chi,
                          first, wallfix, uwall, lam, ga, co);
       else
-        chunk_forward<-1>(pF, Ls + bL - e0, Hs + bH - e0, a.coef + cofs, a.diag + cofs, clo,
+        chunk_forward<-1>(pF, Ls + bL - e0, Hs + bH - e0, a.coef + cofs, clo,
                           chi, first, wallfix, uwall, lam, ga, co);
     }
     phi = min(phi, co.phi);
+#ifdef TMG_LEGK_PREFETCH
+    const uint16_t tmN = tm_of(scn);
+#endif
     __syncthreads();  // every thread is done with the staged u rows
     LEGK_MARK(2);
     double* sb = Hs + tid * LQ;  // this thread's beta row
     if (act) {
       if (g.dir > 0)
-        chunk_back<1>(pF, sb, a.coef + cofs, lam, ga, co);
+        chunk_back<1>(pF, sb, lam, ga, co);
       else
-        chunk_back<-1>(pF, sb, a.coef + cofs, lam, ga, co);
+        chunk_back<-1>(pF, sb, lam, ga, co);
     }
 
     // ---- reduced system over the chunk ends (shared memory in Ls) ----------
@@ -431,7 +455,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     double A = 0.0, Bv = 1.0, C = 0.0, D = 0.0, H = 0.0;
     if (act) {
       const double ae = co.a_end, ce = co.c_end;
-      const double bbe = __ldg(a.diag + cofs + 32 * (LQ - 1)) - (clo + chi);
+      const double bbe = -(ae + ce + clo + chi);
       A = first ? 0.0 : ae * co.bd;
       Bv = fma(ae, co.gd, bbe);
       D = fma(-ae, co.ad, co.r_end);
@@ -470,6 +494,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
       __syncthreads();
     }
     LEGK_MARK(4);
+#ifdef TMG_LEGK_PREFETCH
+    const LegBlock BN = block_of(scn, tmN);
+#endif
     if (act) phi = min(phi, __double2hiint(Bv) & 0x7fffffff);
     const double P = D * iB, Qh = H * iB;
     sP[tid] = P;
@@ -526,8 +553,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     __syncthreads();
     LEGK_MARK(6);
 
-    // ---- stores (bulk copies of the aligned leg interiors, single elements
-    // at the unaligned ends), then the next item's loads: warp 0 only ---------
+    // ---- stores and the next item's loads.  Default: warp 0 bulk-copies the
+    // aligned leg interiors (single elements at unaligned ends), waits until
+    // they have left shared memory and issues the next item's loads.
+    // TMG_LEGK_EARLYU: the next item's u rows go out before the stores (the u
+    // arrays are free).  TMG_LEGK_TSTORE: every thread stores, coalesced.
+    const int nx = rank ? scn.y : scn.x;
+#ifdef TMG_LEGK_EARLYU
+    if (tid < 32 && nx >= 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_loads(a, nx, smem, bar, 0);
+    }
+    constexpr int fpart = 1;
+#else
+    constexpr int fpart = -1;
+#endif
+#ifdef TMG_LEGK_TSTORE
+    if (item >= 0) {
+      const LegItem I = a.items[item];
+      const int nl = 2 * I.nblk;
+      const int w = tid >> 5, lane = tid & 31;
+      const bool wide = nl <= 2;  // one or two long legs: every thread walks each leg
+      for (int q = wide ? 0 : w; q < nl; q += wide ? 1 : LT / 32) {
+        const LegBlock Bq = a.blocks[I.blk0 + (q >> 1)];
+        const int lq = q & 1;
+        if ((lq ? Bq.t0[1] : Bq.t0[0]) < 0) continue;
+        LegGeo gq;
+        gq.set(Bq.k, Bq.quad, lq, n);
+        const int lo = min(gq.p0, gq.p0 + gq.dir * (gq.m - 1));
+        double* dst = (lq == 0 ? a.ut : a.un) + (size_t)gq.row * ld + lo;
+        const double* srcs = F + (lq ? Bq.sb[1][0] : Bq.sb[0][0]) + (lo - gq.p0);
+        for (int e = wide ? tid : lane; e < gq.m; e += wide ? LT : 32) dst[e] = srcs[e];
+      }
+    }
+    __syncthreads();  // the f array is free
+    if (tid < 32 && nx >= 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_loads(a, nx, smem, bar, fpart);
+    }
+#else
     if (tid < 32) {
       if (item >= 0) {
         const LegItem I = a.items[item];
@@ -542,20 +606,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
         }
         bulk_commit();
       }
-      const int nx = rank ? scn.y : scn.x;
       if (nx >= 0) {
         bulk_wait_read();  // the stores have left shared memory
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue_loads(a, nx, smem, bar);
+        issue_loads(a, nx, smem, bar, fpart);
       }
     }
+#endif
     LEGK_MARK(7);
     sc = scn;
+#ifdef TMG_LEGK_PREFETCH
+    tmC = tmN;
+    BC = BN;
+#endif
   }
 #undef LEGK_MARK
 #ifdef TMG_LEGK_TIMING
   if (timing)
-    for (int i = 0; i < 8; i++) a.timing[blockIdx.x * 8 + i] = tacc[i];
+    for (int i = 0; i < 8; i++) a.timing[(blockIdx.x + (tid ? gridDim.x : 0)) * 8 + i] = tacc[i];
 #endif
   if (tid < 32) bulk_wait_all();
   bad |= phi < 0x01A56E1F;  // |pivot| < 1e-300 (high word of 1e-300)
@@ -809,13 +877,18 @@ std::string leg_plan_set_coefs(LegPlan& P, const double* W, const double* E, con
   const int nch = ceil_div(std::max(mmax, 1), LQ);
   const int cstride = ceil_div(nch, 32) * 32 * LQ;
   std::vector<double2> h((size_t)4 * LQ * cstride, make_double2(0.0, 0.0));
-  std::vector<double> hd((size_t)4 * LQ * cstride, -1.0);
   for (int o = 0; o < 4; o++) {
     for (int pad = 0; pad < LQ; pad++) {
       const size_t base = (size_t)(o * LQ + pad) * cstride;
       for (int ch = 0; ch < nch; ch++) {
         for (int k = 0; k < LQ; k++) {
           const int e = ch * LQ + k - pad;  // leg point (tip = 0)
+          // dummies: a huge diagonal (1e300, so a vanishing reciprocal) and
+          // no coupling toward the next point decouple them from the tip
+          if (e < 0) {
+            h[base + (ch >> 5) * (32 * LQ) + k * 32 + (ch & 31)] = make_double2(1e300, 0.0);
+            continue;
+          }
           if (e < 0 || e > n - 2) continue;  // dummies: no coupling
           const int pos = (o % 2 == 0) ? 1 + e : n - 1 - e;
           double av, cv;
@@ -827,8 +900,7 @@ std::string leg_plan_set_coefs(LegPlan& P, const double* W, const double* E, con
           }
           const size_t ix = base + (ch >> 5) * (32 * LQ) + k * 32 + (ch & 31);
           // the tip's coupling toward the wall is folded into f (not eliminated)
-          h[ix] = make_double2(e == 0 ? 0.0 : av, cv);
-          hd[ix] = -(av + cv);
+          h[ix] = make_double2(av, cv);
         }
       }
     }
@@ -836,12 +908,9 @@ std::string leg_plan_set_coefs(LegPlan& P, const double* W, const double* E, con
   P.cstride = cstride;
   if (cudaMalloc(&P.coef, h.size() * sizeof(double2)) != cudaSuccess ||
       cudaMemcpy(P.coef, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice) !=
-          cudaSuccess ||
-      cudaMalloc(&P.diag, hd.size() * sizeof(double)) != cudaSuccess ||
-      cudaMemcpy(P.diag, hd.data(), hd.size() * sizeof(double), cudaMemcpyHostToDevice) !=
           cudaSuccess)
     return "leg plan coefficient upload failed";
-  P.device_bytes += h.size() * sizeof(double2) + hd.size() * sizeof(double);
+  P.device_bytes += h.size() * sizeof(double2);
   return "";
 }
 
@@ -855,9 +924,7 @@ void free_leg_plan(LegPlan& P) {
     C = LegColour();
   }
   cudaFree(P.coef);
-  cudaFree(P.diag);
   P.coef = nullptr;
-  P.diag = nullptr;
 }
 
 size_t leg_smem_bytes() { return sizeof(double) * kLegStage + sizeof(uint64_t) + 64; }
@@ -905,7 +972,6 @@ cudaError_t launch_leg_colour(const LegPlan& P, int red, const SweepArgs& s, cud
   a.S = s.S;
   a.N = s.N;
   a.coef = P.coef;
-  a.diag = P.diag;
   a.cstride = P.cstride;
   a.n = P.n;
   a.ld = P.n + 1;
@@ -919,7 +985,7 @@ cudaError_t launch_leg_colour(const LegPlan& P, int red, const SweepArgs& s, cud
   const int ncl = std::max(1, std::min(sms, C.nsched));  // two CTAs per SM
   a.timing = nullptr;
   if (leg_timing_on()) {
-    if (!g_leg_timing) cudaMalloc(&g_leg_timing, sizeof(long long) * 8 * 2 * 1024);
+    if (!g_leg_timing) cudaMalloc(&g_leg_timing, sizeof(long long) * 16 * 2 * 1024);
     a.timing = g_leg_timing;
     g_leg_timing_ctas = 2 * ncl;
   }
@@ -932,15 +998,23 @@ cudaError_t launch_leg_colour(const LegPlan& P, int red, const SweepArgs& s, cud
 // Average per-CTA clock cycles of the leg kernel's phases in its last launch
 // (TMG_LEGK_TIMING=1 only): setup, stage wait, forward, back, reduced system,
 // branch, finalize, stores.  Returns the number of CTAs averaged.
-extern "C" int tmg_debug_leg_phases(double* out8) {
-  for (int i = 0; i < 8; i++) out8[i] = 0.0;
+extern "C" int tmg_debug_leg_phases(double* out8 /* [16] */) {
+  for (int i = 0; i < 16; i++) out8[i] = 0.0;
   if (!tmg::g_leg_timing || tmg::g_leg_timing_ctas == 0) return 0;
   std::vector<long long> h(8 * (size_t)tmg::g_leg_timing_ctas);
   if (cudaMemcpy(h.data(), tmg::g_leg_timing, h.size() * sizeof(long long),
                  cudaMemcpyDeviceToHost) != cudaSuccess)
     return -1;
+  // out8[0..7]: thread 0 (warp 0, which also issues the bulk copies);
+  // out8[8..15]: thread 96
+  std::vector<long long> h2(8 * (size_t)tmg::g_leg_timing_ctas);
+  cudaMemcpy(h2.data(), tmg::g_leg_timing + 8 * (size_t)tmg::g_leg_timing_ctas,
+             h2.size() * sizeof(long long), cudaMemcpyDeviceToHost);
   for (size_t c = 0; c < (size_t)tmg::g_leg_timing_ctas; c++)
-    for (int i = 0; i < 8; i++) out8[i] += (double)h[c * 8 + i];
-  for (int i = 0; i < 8; i++) out8[i] /= tmg::g_leg_timing_ctas;
+    for (int i = 0; i < 8; i++) {
+      out8[i] += (double)h[c * 8 + i];
+      out8[8 + i] += (double)h2[c * 8 + i];
+    }
+  for (int i = 0; i < 16; i++) out8[i] /= tmg::g_leg_timing_ctas;
   return tmg::g_leg_timing_ctas;
 }

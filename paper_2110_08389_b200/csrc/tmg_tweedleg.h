@@ -11,7 +11,10 @@ struct SweepArgs;
 
 constexpr int kLegQ = 17;          // points per thread chunk
 constexpr int kLegThreads = 256;   // threads per CTA
-constexpr int kLegMaxBlocks = 16;  // blocks per item
+#ifndef TMG_LEGK_MAXB
+#define TMG_LEGK_MAXB 8
+#endif
+constexpr int kLegMaxBlocks = TMG_LEGK_MAXB;  // blocks per item
 // Staged arrays (doubles): 18 slots of headroom (dummy points in front of a
 // leg's tip read finite values there), the runs of the item's legs (<= 256
 // chunks of 17 points, <= 2 alignment elements per leg run), 18 slots of
@@ -60,7 +63,6 @@ struct LegPlan {
   int n = 0;
   // (a, c) along couplings, chunk-permuted: [orientation][tip pad 0..16][cstride]
   double2* coef = nullptr;
-  double* diag = nullptr;   // -(a + c), same layout
   int cstride = 0;
   LegColour col[2];         // [black, red]
   size_t device_bytes = 0;
@@ -76,7 +78,6 @@ struct LegArgs {
   const double* S;
   const double* N;
   const double2* coef;
-  const double* diag;
   int cstride;
   int n, ld;
   const LegItem* items;
