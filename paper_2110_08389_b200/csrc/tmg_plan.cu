@@ -325,9 +325,28 @@ long dump_members(const Geometry& g, int* oi, int* oj, int* oblk, int* oflags, l
 static thread_local bool g_dry_run = false;
 static thread_local long long g_stats[10];
 
+// Upload arena of the per-block shims (tmg_relax_*): while set, plan arrays
+// are carved from one grow-only device buffer and copied asynchronously on
+// its stream, so a shim call allocates nothing once the arena is warm.
+static thread_local UploadArena* g_arena = nullptr;
+void set_upload_arena(UploadArena* a) { g_arena = a; }
+
 template <class T>
 static T* upload(const std::vector<T>& v, size_t& bytes, std::string& err) {
   if (v.empty() || g_dry_run) return nullptr;
+  if (g_arena) {
+    const size_t nb = (v.size() * sizeof(T) + 255) & ~(size_t)255;
+    if (g_arena->used + nb > g_arena->cap) {
+      err = "shim arena too small";
+      return nullptr;
+    }
+    T* d = reinterpret_cast<T*>(g_arena->base + g_arena->used);
+    g_arena->used += nb;
+    cudaError_t e = cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice,
+                                    g_arena->stream);
+    if (e != cudaSuccess) err = cudaGetErrorString(e);
+    return d;
+  }
   T* d = nullptr;
   cudaError_t e = cudaMalloc(&d, v.size() * sizeof(T));
   if (e != cudaSuccess) { err = cudaGetErrorString(e); return nullptr; }
@@ -936,6 +955,12 @@ std::string add_explicit_block(Geometry& g, int kind, long n, const long long* i
 }
 
 void free_plan(Plan& p) {
+  if (p.arena) {  // arena-backed arrays are owned by the arena
+    p.classes.clear();
+    p.d_legs = nullptr;
+    p.d_blocks = nullptr;
+    return;
+  }
   for (auto& c : p.classes) {
     cudaFree(c.chunks);
     cudaFree(c.bins);

@@ -39,7 +39,17 @@ struct Plan {
   // tweed L-shells of square hybrid grids run on the TMA-fed leg kernel
   // (tmg_tweedleg.cu); the generic classes then hold the remaining blocks
   LegPlan* lp = nullptr;
+  bool arena = false;  // device arrays live in an UploadArena
 };
+
+// Grow-only device buffer the shims pack their one-block plans into.
+struct UploadArena {
+  char* base = nullptr;
+  size_t cap = 0, used = 0;
+  cudaStream_t stream = nullptr;
+};
+// Route pack_plan's uploads into `a` (nullptr: cudaMalloc per array).
+void set_upload_arena(UploadArena* a);
 
 std::string build_plan(int scheme, int nx, int ny, int q, int mode, Plan& p);
 // Plan restricted to the blocks of sharding groups [g0, g1) (point_group in

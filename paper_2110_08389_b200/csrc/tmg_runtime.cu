@@ -1200,46 +1200,105 @@ long tmg_layout_dump(int kind, int nx, int ny, int* oi, int* oj, int* oblk, int*
 // ---------------- per-block shims (test / plugin surface) -------------------
 namespace {
 
+// Index arrays may live in host or device memory: host indices (the
+// reference's numpy plans) are used in place, device ones are read back.
+bool host_pointer(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
+}
+
+// Per-thread shim workspace: the plan arena, the merged coefficient array
+// and the pivot flag, grown on demand and reused by every later call.
+struct ShimWork {
+  UploadArena arena;
+  double* cw = nullptr;
+  size_t cw_cap = 0;
+  int* d_err = nullptr;
+  int* h_err = nullptr;
+};
+thread_local ShimWork g_shim;
+
 int relax_explicit(int kind, long n, const int64_t* ii, const int64_t* jj, long m,
                    const int64_t* offs, long bi, long bj, int nx, int ny, const double* W,
                    const double* E, const double* S, const double* N, double* u, const double* f,
                    cudaStream_t s) {
   if (n < 1) return TMG_OK;
-  std::vector<long long> hi(n), hj(n), ho(m > 0 ? m + 1 : 1);
-  TMG_CUDA_TRY(cudaMemcpyAsync(hi.data(), ii, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
-  TMG_CUDA_TRY(cudaMemcpyAsync(hj.data(), jj, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
-  if (kind == 3)
-    TMG_CUDA_TRY(cudaMemcpyAsync(ho.data(), offs, sizeof(int64_t) * (m + 1),
-                                 cudaMemcpyDeviceToHost, s));
-  TMG_CUDA_TRY(cudaStreamSynchronize(s));
+  std::vector<long long> hi, hj, ho;
+  const long long* pi = reinterpret_cast<const long long*>(ii);
+  const long long* pj = reinterpret_cast<const long long*>(jj);
+  const long long* po = reinterpret_cast<const long long*>(offs);
+  if (!host_pointer(ii) || !host_pointer(jj) || (kind == 3 && !host_pointer(offs))) {
+    hi.resize(n);
+    hj.resize(n);
+    ho.resize(m > 0 ? m + 1 : 1);
+    TMG_CUDA_TRY(cudaMemcpyAsync(hi.data(), ii, sizeof(int64_t) * n, cudaMemcpyDefault, s));
+    TMG_CUDA_TRY(cudaMemcpyAsync(hj.data(), jj, sizeof(int64_t) * n, cudaMemcpyDefault, s));
+    if (kind == 3)
+      TMG_CUDA_TRY(cudaMemcpyAsync(ho.data(), offs, sizeof(int64_t) * (m + 1), cudaMemcpyDefault,
+                                   s));
+    TMG_CUDA_TRY(cudaStreamSynchronize(s));
+    pi = hi.data();
+    pj = hj.data();
+    po = ho.data();
+  }
   for (long k = 0; k < n; k++)
-    if (hi[k] < 1 || hi[k] >= nx || hj[k] < 1 || hj[k] >= ny)
+    if (pi[k] < 1 || pi[k] >= nx || pj[k] < 1 || pj[k] >= ny)
       return fail(TMG_BADARG, "block member outside the grid interior");
   Geometry g;
   g.nx = nx;
   g.ny = ny;
   g.scheme = -1;
-  std::string err = add_explicit_block(g, kind, n, hi.data(), hj.data(), m, ho.data(), bi, bj);
+  std::string err = add_explicit_block(g, kind, n, pi, pj, m, po, bi, bj);
   if (!err.empty()) return fail(TMG_BADARG, err);
   cudaError_t e = init_sweep_kernels();
   if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");
+  ShimWork& w = g_shim;
+  // arena: room for this block's plan (chunk records of 16 bytes, bins,
+  // hubs, legs) with slack; grown (the only allocation) when too small
+  const size_t need = (size_t)4096 + (size_t)(n / 2 + 64) * 64 * 4;
+  if (w.arena.cap < need) {
+    if (w.arena.base) {
+      TMG_CUDA_TRY(cudaStreamSynchronize(s));
+      cudaFree(w.arena.base);
+    }
+    w.arena.cap = std::max(need, (size_t)1 << 20);
+    TMG_CUDA_TRY(cudaMalloc(&w.arena.base, w.arena.cap));
+  }
+  const size_t bx = (size_t)nx + 1, by = (size_t)ny + 1;
+  if (w.cw_cap < 2 * bx + 2 * by) {
+    if (w.cw) {
+      TMG_CUDA_TRY(cudaStreamSynchronize(s));
+      cudaFree(w.cw);
+    }
+    w.cw_cap = std::max(2 * bx + 2 * by, (size_t)4096);
+    TMG_CUDA_TRY(cudaMalloc(&w.cw, sizeof(double) * w.cw_cap));
+  }
+  if (!w.d_err) {
+    TMG_CUDA_TRY(cudaMalloc(&w.d_err, sizeof(int)));
+    TMG_CUDA_TRY(cudaMallocHost(&w.h_err, sizeof(int)));
+  }
+  w.arena.used = 0;
+  w.arena.stream = s;
   Plan p;
+  set_upload_arena(&w.arena);
   err = pack_plan(std::move(g), kQmax, LM_NATURAL, p);
+  set_upload_arena(nullptr);
+  p.arena = true;
   if (!err.empty()) {
     free_plan(p);
     return fail(TMG_BADARG, err);
   }
   // the kernel addresses W, E, S, N as one allocation (tmg_kernels.h)
-  const size_t bx = (size_t)nx + 1, by = (size_t)ny + 1;
-  int* d_err = nullptr;
-  double* cw = nullptr;
-  TMG_CUDA_TRY(cudaMalloc(&d_err, sizeof(int)));
-  TMG_CUDA_TRY(cudaMalloc(&cw, sizeof(double) * (2 * bx + 2 * by)));
-  TMG_CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(int), s));
-  TMG_CUDA_TRY(cudaMemcpyAsync(cw, W, sizeof(double) * bx, cudaMemcpyDeviceToDevice, s));
-  TMG_CUDA_TRY(cudaMemcpyAsync(cw + bx, E, sizeof(double) * bx, cudaMemcpyDeviceToDevice, s));
-  TMG_CUDA_TRY(cudaMemcpyAsync(cw + 2 * bx, S, sizeof(double) * by, cudaMemcpyDeviceToDevice, s));
-  TMG_CUDA_TRY(cudaMemcpyAsync(cw + 2 * bx + by, N, sizeof(double) * by, cudaMemcpyDeviceToDevice, s));
+  double* cw = w.cw;
+  TMG_CUDA_TRY(cudaMemsetAsync(w.d_err, 0, sizeof(int), s));
+  TMG_CUDA_TRY(cudaMemcpyAsync(cw, W, sizeof(double) * bx, cudaMemcpyDefault, s));
+  TMG_CUDA_TRY(cudaMemcpyAsync(cw + bx, E, sizeof(double) * bx, cudaMemcpyDefault, s));
+  TMG_CUDA_TRY(cudaMemcpyAsync(cw + 2 * bx, S, sizeof(double) * by, cudaMemcpyDefault, s));
+  TMG_CUDA_TRY(cudaMemcpyAsync(cw + 2 * bx + by, N, sizeof(double) * by, cudaMemcpyDefault, s));
   SweepArgs a{};
   a.legs = p.d_legs;
   a.blocks = p.d_blocks;
@@ -1250,7 +1309,7 @@ int relax_explicit(int kind, long n, const int64_t* ii, const int64_t* jj, long 
   a.u = u;
   a.f = f;
   a.ld = ny + 1;
-  a.err = d_err;
+  a.err = w.d_err;
   a.ut = u;
   a.ft = f;
   a.ldt = nx + 1;
@@ -1258,14 +1317,13 @@ int relax_explicit(int kind, long n, const int64_t* ii, const int64_t* jj, long 
   a.nx = nx;
   a.ny = ny;
   e = launch_colour(p, 1, a, s);
-  int herr = 0;
-  if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, s);
+  // the reference raises SingularSystemError at once: one flag readback
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(w.h_err, w.d_err, sizeof(int), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  cudaFree(d_err);
-  cudaFree(cw);
   free_plan(p);
   if (e != cudaSuccess) return cuda_fail(e, "relax shim");
-  if (herr & 1) return fail(TMG_SINGULAR, "zero pivot");
+  if (*w.h_err & 1) return fail(TMG_SINGULAR, "zero pivot");
   return TMG_OK;
 }
 

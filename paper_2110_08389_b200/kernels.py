@@ -44,8 +44,27 @@ def set_backend(name: str) -> str:
     raise ValueError(f"unknown backend {name!r}")
 
 
+class _HostIdx:
+    """Host int64 index array handed to the shims in place (the library
+    reads host indices directly: no device copy, no read-back)."""
+
+    def __init__(self, a):
+        self.a = np.ascontiguousarray(a, dtype=np.int64)
+
+    def numel(self):
+        return self.a.size
+
+    def data_ptr(self):
+        return self.a.ctypes.data
+
+
+def _index(a):
+    return _HostIdx(a) if isinstance(a, (np.ndarray, list, tuple)) else \
+        _device.to_device(a, dtype=np.int64)
+
+
 def _common(ii, jj, W, E, S, N, u, f):
-    idx = [_device.to_device(a, dtype=np.int64) for a in (ii, jj)]
+    idx = [_index(a) for a in (ii, jj)]
     co = [_device.to_device(a) for a in (W, E, S, N)]
     ud, fd = _device.to_device(u), _device.to_device(f)
     nx, ny = ud.shape[0] - 1, ud.shape[1] - 1
@@ -85,7 +104,7 @@ def relax_legged(ii, jj, offs, bi, bj, W, E, S, N, u, f):
     """Exact solve of one m-legged block around branch (bi, bj)
     (_ckernels.pyx:144-185)."""
     (di, dj), co, ud, fd, nx, ny = _common(ii, jj, W, E, S, N, u, f)
-    do = _device.to_device(offs, dtype=np.int64)
+    do = _index(offs)
     _lib.check(_lib.lib().tmg_relax_legged(
         int(di.numel()), _device.ptr(di), _device.ptr(dj), int(do.numel()) - 1, _device.ptr(do),
         int(bi), int(bj), nx, ny, *[_device.ptr(c) for c in co], _device.ptr(ud),
