@@ -30,6 +30,24 @@
 
 namespace cg = cooperative_groups;
 
+// -DTMG_CHECK (make check): device bounds checks on the gathered / scattered
+// global offsets, the hub couplings and the DSMEM ranks (stand-in for
+// compute-sanitizer, which the GPU pool does not offer; profiles/r02_boundscheck.txt)
+#ifdef TMG_CHECK
+#define SWEEP_CHECK(cond, what)                                                              \
+  do {                                                                                       \
+    if (!(cond)) {                                                                           \
+      printf("block kernel check failed: %s (block %d thread %d)\n", what, (int)blockIdx.x, \
+             (int)threadIdx.x);                                                              \
+      __trap();                                                                              \
+    }                                                                                        \
+  } while (0)
+#else
+#define SWEEP_CHECK(cond, what) \
+  do {                          \
+  } while (0)
+#endif
+
 
 
 #ifndef TMG_SKIP
@@ -386,6 +404,7 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
       for (int b = 0; b < BATCH; b++) {
         const int p = 32 * (m0 + b) + lane;
         const int o = off0 + p * str0;
+        SWEEP_CHECK(o - cs0 >= 0 && o + cs0 < (a.nx + 1) * (a.ny + 1), "uniform gather offset");
         vf[b] = fb[o];
         vl[b] = ub[o - cs0];
         vh[b] = ub[o + cs0];
@@ -429,6 +448,8 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
         const double* ub = tb_s ? a.ut : u;
         const double* fb = tb_s ? a.ft : f;
         const int o = ri.x + ksub * ri.y;
+        SWEEP_CHECK(ksub >= (ri.w & 255) || (o - ri.z >= 0 && o + ri.z < (a.nx + 1) * (a.ny + 1)),
+                    "record gather offset");
         const int ai = ksub * rj.z;
         slot[b] = ksub < (ri.w & 255) ? sw<Q>(src, ksub) : -1;
         if (slot[b] >= 0) {
@@ -542,6 +563,7 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
     if (c.link & kLinkRightNext) {
       double an, bn, gn;
       if (CLUSTER && tid == T - 1) {  // the next chunk opens the next CTA
+        SWEEP_CHECK(rank + 1 < cs_size, "DSMEM rank");
         an = remote<CLUSTER>(sA, rank + 1)[0];
         bn = remote<CLUSTER>(sB, rank + 1)[0];
         gn = remote<CLUSTER>(sC, rank + 1)[0];
@@ -654,6 +676,9 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
     double num = hub_num, den = hub_den;
     for (int q = 0; q < hb.nadj; q++) {
       const int ta = hb.adj_t[q];
+      SWEEP_CHECK(ta >= 0 && ta < T * cs_size && hb.off >= 0 &&
+                      hb.off < (a.nx + 1) * (a.ny + 1),
+                  "hub coupling");
       const double cf = C.dir(hb.adj_d[q], hi, hj);
       num -= cf * remote<CLUSTER>(sD, ta / T)[ta % T];
       den -= cf * remote<CLUSTER>(sH, ta / T)[ta % T];

@@ -40,6 +40,26 @@
 
 namespace cg = cooperative_groups;
 
+// -DTMG_CHECK (make check): device-side bounds checks on every shared-memory
+// slot a chunk, a bulk copy or the reduced system touches, and on the global
+// offsets of the branch and boundary loads.  A failed check prints and traps
+// (the launch fails loudly).  compute-sanitizer is not available on the GPU
+// pool; this build is its stand-in (profiles/r02_boundscheck.txt).
+#ifdef TMG_CHECK
+#define LEGK_CHECK(cond, what)                                                             \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("leg kernel check failed: %s (block %d thread %d)\n", what, (int)blockIdx.x, \
+             (int)threadIdx.x);                                                            \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define LEGK_CHECK(cond, what) \
+  do {                         \
+  } while (0)
+#endif
+
 namespace tmg {
 
 namespace {
@@ -141,6 +161,13 @@ __device__ __forceinline__ void issue_loads(const LegArgs& a, int item, double* 
     const LegCopy cp = a.copies[I.copy0 + c];
     if (part >= 0 && (cp.s < kLegArrF) != (part == 1)) continue;
     const double* src = cp.src == 0 ? a.fn : cp.src == 1 ? a.ft : cp.src == 2 ? a.un : a.ut;
+    LEGK_CHECK(cp.s >= 0 && cp.n > 0 && cp.g >= 0 && (cp.s & 1) == 0 && (cp.g & 1) == 0 &&
+                   (cp.s < kLegArrF ? cp.s + cp.n <= kLegArrF
+                                    : cp.s + cp.n <= kLegArrF + 2 * kLegArrU &&
+                                          (cp.s >= kLegArrF + kLegArrU ||
+                                           cp.s + cp.n <= kLegArrF + kLegArrU)) &&
+                   cp.g + cp.n <= (long)a.ld * a.ld,
+               "bulk load range");
     bulk_g2s(stage + cp.s, src + cp.g, (unsigned)cp.n * 8u, bar);
   }
 }
@@ -415,6 +442,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     double lam[LQ - 1], ga[LQ - 1];
     ChunkOut co{0, 1, 0, 0, 0, 1, 0, 0, 0, 0x7fffffff};
     double* pF = F + bF + g.dir * e0;
+#ifdef TMG_CHECK
+    if (act) {  // every slot of the chunk (dummies included) inside its array
+      const int f0 = bF + g.dir * e0, f1 = f0 + g.dir * (LQ - 1);
+      const int l0 = bL + g.dir * e0, l1 = l0 + g.dir * (LQ - 1);
+      const int h0 = bH + g.dir * e0, h1 = h0 + g.dir * (LQ - 1);
+      LEGK_CHECK(min(f0, f1) >= 0 && max(f0, f1) < kLegArrF, "f slots");
+      LEGK_CHECK(min(l0, l1) >= 0 && max(l0, l1) < kLegArrU, "u-1 slots");
+      LEGK_CHECK(min(h0, h1) >= 0 && max(h0, h1) < kLegArrU, "u+1 slots");
+      LEGK_CHECK(pad >= 0 && pad < LQ && (!first || e0 == -pad), "tip padding");
+      LEGK_CHECK(ch >= 0 && ch < nch && tid - ch + nch <= LT, "chunk range");
+      LEGK_CHECK(cofs + 32 * (LQ - 1) < (size_t)4 * LQ * a.cstride, "coefficient index");
+      if (hubthr) {
+        LEGK_CHECK(B.split || tid + nch < LT, "branch partner");
+        LEGK_CHECK(g.bi > 0 && g.bi < n && g.bj > 0 && g.bj < n, "branch inside");
+      }
+    }
+#endif
     if (act) {
       if (first) pF[g.dir * pad] -= tip_a * tip_u;  // only this thread reads the tip's f
       if (g.dir > 0)
