@@ -373,7 +373,7 @@ std::string build_plan(int scheme, int nx, int ny, int q, int mode, Plan& P) {
   std::string err = build_geometry(scheme, nx, ny, g);
   if (!err.empty()) return err;
   const bool legk = leg_plan_applies(scheme, nx, ny, mode) && !g_dry_run;
-  if (legk) {  // L-shells k in [k0, c) go to the leg kernel
+  if (legk) {  // L-shells k in [k0, c) and the cross go to the leg kernel
     const int k0 = leg_k0(), c = nx / 2;
     Geometry out;
     out.scheme = g.scheme;
@@ -386,7 +386,7 @@ std::string build_plan(int scheme, int nx, int ny, int q, int mode, Plan& P) {
         j = g.legs[B.leg0].j0;
       }
       const int grp = point_group(g.scheme, g.nx, g.ny, i, j);
-      if (grp >= k0 && grp < c) continue;
+      if (grp >= k0 && grp <= c) continue;  // L-shells and the central cross
       BlockD nb = B;
       nb.leg0 = (int32_t)out.legs.size();
       for (int l = 0; l < B.nleg; l++) {

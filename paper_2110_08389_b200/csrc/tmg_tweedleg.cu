@@ -215,6 +215,7 @@ __device__ __forceinline__ void chunk_forward(double* __restrict__ pF,
                                               const double* __restrict__ pH,
                                               const double2* __restrict__ pc, double clo,
                                               double chi, bool first, int wallfix, double uwall,
+                                              double uwall2,
                                               double (&lam)[LQ - 1], double (&cg_)[LQ - 1],
                                               ChunkOut& o) {
   const double csum = clo + chi;
@@ -248,8 +249,9 @@ __device__ __forceinline__ void chunk_forward(double* __restrict__ pF,
   if (!wallfix) {
     r = fma(-chi, pH[DIR * k], fma(-clo, pL[DIR * k], pF[DIR * k]));
   } else {  // x-leg's last point: its wall-side cross neighbour is an N-owned branch
-    const double ul = wallfix == 1 ? uwall : pL[DIR * k];
-    const double uh = wallfix == 1 ? pH[DIR * k] : uwall;
+    // 1: the u-1 side, 2: the u+1 side, 3: both (the cross's x-legs)
+    const double ul = wallfix == 2 ? pL[DIR * k] : uwall;
+    const double uh = wallfix == 1 ? pH[DIR * k] : wallfix == 2 ? uwall : uwall2;
     r = pF[DIR * k] - clo * ul - chi * uh;
   }
   const double2 ac = __ldg(pc + 32 * k);
@@ -408,7 +410,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     const int bH = leg ? B.sb[1][2] : B.sb[0][2];
     // branch row: frozen terms (the hub thread is the last chunk of leg 0, or
     // of the CTA's own leg in a split block)
-    const bool hubthr = lastc && (leg == 0 || B.split == 2);
+    const bool hubthr = lastc && (leg == 0 || B.split >= 2);
+    const bool crossb = B.split >= 3;
     double hub_num = 0.0, den0 = 1.0, cx = 0.0, cy = 0.0;
     if (hubthr) {
       const int bi = g.bi, bj = g.bj;
@@ -418,8 +421,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
       cx = g.sx > 0 ? Wi : Ei;  // toward the x-leg end
       cy = g.sy > 0 ? Sj : Nj;  // toward the y-leg end
       const double ex = g.sx > 0 ? Ei : Wi, ey = g.sy > 0 ? Nj : Sj;
-      hub_num = a.fn[(size_t)bi * ld + bj] - ex * a.un[(size_t)(bi + g.sx) * ld + bj] -
-                ey * a.ut[(size_t)(bj + g.sy) * ld + bi];
+      hub_num = a.fn[(size_t)bi * ld + bj];
+      if (!crossb)  // the cross's branch has no frozen neighbour
+        hub_num = hub_num - ex * a.un[(size_t)(bi + g.sx) * ld + bj] -
+                  ey * a.ut[(size_t)(bj + g.sy) * ld + bi];
     }
     double tip_u = 0.0, tip_a = 0.0, uwall = 0.0;
     if (first) {  // Dirichlet neighbour of the tip (N buffer ring) and its coupling
@@ -430,8 +435,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
                        : (g.sy > 0 ? __ldg(a.S + tp) : __ldg(a.N + tp));
     }
     // x-leg's last point: true wall-side neighbour (1: the u-1 row, 2: the u+1 row)
-    const int wallfix = (lastc && leg == 0) ? (g.sy > 0 ? 1 : 2) : 0;
-    if (wallfix) uwall = a.un[(size_t)(g.p0 + g.sx * (m - 1)) * ld + (g.bj - g.sy)];
+    // (the cross's x-legs end between two N-owned branches: both sides)
+    const int wallfix = (lastc && leg == 0) ? (crossb ? 3 : g.sy > 0 ? 1 : 2) : 0;
+    double uwall2 = 0.0;
+    if (wallfix == 3) {
+      const size_t xl = (size_t)(g.p0 + g.sx * (m - 1)) * ld;
+      uwall = a.un[xl + g.bj - 1];
+      uwall2 = a.un[xl + g.bj + 1];
+    } else if (wallfix) {
+      uwall = a.un[(size_t)(g.p0 + g.sx * (m - 1)) * ld + (g.bj - g.sy)];
+    }
 
     LEGK_MARK(0);
     if (item >= 0) {
@@ -463,10 +476,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
       if (first) pF[g.dir * pad] -= tip_a * tip_u;  // only this thread reads the tip's f
       if (g.dir > 0)
         chunk_forward<1>(pF, Ls + bL + e0, Hs + bH + e0, a.coef + cofs, clo, chi,
-                         first, wallfix, uwall, lam, ga, co);
+                         first, wallfix, uwall, uwall2, lam, ga, co);
       else
         chunk_forward<-1>(pF, Ls + bL - e0, Hs + bH - e0, a.coef + cofs, clo,
-                          chi, first, wallfix, uwall, lam, ga, co);
+                          chi, first, wallfix, uwall, uwall2, lam, ga, co);
     }
     phi = min(phi, co.phi);
 #ifdef TMG_LEGK_PREFETCH
@@ -559,7 +572,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     }
 
     // ---- branch rows ----------------------------------------------------------
-    if (hubthr) {
+    if (hubthr && crossb) {
+      // central cross: the four leg ends meet through the global mailbox
+      // (every leg CTA runs in the first two cluster iterations, all resident)
+      const int sl = B.split - 3;
+      volatile double* mb = a.mail;
+      int* cnt = reinterpret_cast<int*>(a.mail + 8);
+      mb[2 * sl] = P;
+      mb[2 * sl + 1] = Qh;
+      __threadfence();
+      atomicAdd(cnt, 1);
+      while (atomicAdd(cnt, 0) < 4) __nanosleep(64);
+      __threadfence();
+      const int c = n / 2;
+      const double cf[4] = {__ldg(a.W + c), __ldg(a.E + c), __ldg(a.S + c), __ldg(a.N + c)};
+      double num = hub_num, den = den0;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        num -= cf[q] * mb[2 * q];
+        den -= cf[q] * mb[2 * q + 1];
+      }
+      bad |= bad_pivot(den);
+      const double xb = num / den;
+      sX[slot] = xb;
+      if (sl == 0) a.un[(size_t)c * ld + c] = xb;
+      if (atomicAdd(cnt + 1, 1) == 3) {  // the last reader rearms the mailbox
+        cnt[0] = 0;
+        cnt[1] = 0;
+        __threadfence();
+      }
+    } else if (hubthr) {
       double px, qx, py, qy;
       if (B.split) {
         const int par = nsplit & 1;
@@ -709,7 +751,7 @@ int leg_k0() {
   static int k0 = 0;
   if (!k0) {
     const char* s = std::getenv("TMG_LEGK_K0");
-    k0 = s && std::atoi(s) >= 3 ? std::atoi(s) : kLegK0;
+    k0 = s && std::atoi(s) >= 2 ? std::atoi(s) : kLegK0;
   }
   return k0;
 }
@@ -762,7 +804,11 @@ std::string build_leg_plan(int n, LegPlan& P) {
         const int x0 = sx > 0 ? 1 : n - 1, y0 = sy > 0 ? 1 : n - 1;
         const int bi_ = x0 + sx * (hb.k - 1), bj_ = y0 + sy * (hb.k - 1), m = hb.k - 1;
         for (int leg = 0; leg < 2; leg++) {
-          if ((split == 1 && leg == 1) || (split == 2 && leg == 0)) continue;
+          // split 1 / 2: the leg 0 / 1 half of a split block; 3..6: one leg of
+          // the central cross (W, E as x-legs of the LL / LR shell c, S, N as
+          // y-legs of the LL / UL shell c)
+          const int only = split == 1 ? 0 : split == 2 ? 1 : split >= 3 ? (split >= 5 ? 1 : 0) : -1;
+          if (only >= 0 && leg != only) continue;
           lb.t0[leg] = (int16_t)t;
           for (int c = 0; c < hb.chunks; c++) map[t + c] = (uint16_t)((bi << 1) | leg);
           t += hb.chunks;
@@ -812,9 +858,10 @@ std::string build_leg_plan(int n, LegPlan& P) {
             cp.src = dst;
             stores.push_back(cp);
           }
-          for (long ge_ : {glo, ghi}) {
+          for (int side = 0; side < 2; side++) {
+            const long ge_ = side ? ghi : glo;
             if (ge_ >= is && ge_ < ie) continue;
-            if (ge_ == ghi && ghi == glo && !edges.empty() && edges.back().g == ge_) continue;
+            if (side == 1 && ghi == glo) continue;  // a one-point leg has one edge
             LegCopy cp{};
             cp.g = ge_;
             cp.s = soffF + (int)(ge_ - gsF);
@@ -844,8 +891,28 @@ std::string build_leg_plan(int n, LegPlan& P) {
       return (int)items.size() - 1;
     };
 
-    // split blocks: one item per leg, scheduled on the two CTAs of a cluster
+    // the central cross (square grids, colour of shell c): four one-leg items
+    // run in the first two cluster iterations (all four CTAs co-resident;
+    // the branch row goes through a global mailbox)
     std::vector<int4> sched_split;
+    const int c = n / 2;
+    if (((c % 2) != 0) == (red != 0)) {
+      const int quads[4] = {0, 1, 0, 2};  // W: LL x-leg, E: LR x-leg, S: LL y-leg, N: UL y-leg
+      int ids[4];
+      for (int q = 0; q < 4; q++) {
+        Open o;
+        o.members.push_back({HostBlock{c, quads[q], ceil_div(c - 1, LQ)}, 3 + q});
+        o.chunks = ceil_div(c - 1, LQ);
+        ids[q] = emit(o);
+        if (ids[q] < 0) return "leg plan: staging overflow";
+      }
+      sched_split.push_back(make_int4(ids[0], ids[1], (items[ids[0]].steps << 8) |
+                                                          (items[ids[1]].steps << 16), 0));
+      sched_split.push_back(make_int4(ids[2], ids[3], (items[ids[2]].steps << 8) |
+                                                          (items[ids[3]].steps << 16), 0));
+      C.cross = 1;
+    }
+    // split blocks: one item per leg, scheduled on the two CTAs of a cluster
     std::vector<Open> open;
     for (const HostBlock& hb : blocks) {
       if (hb.chunks > LT / 2) {
@@ -907,6 +974,11 @@ std::string build_leg_plan(int n, LegPlan& P) {
     up(items, C.items);
     up(iblocks, C.blocks);
     up(tmap, C.tmap);
+    if (C.cross) {  // cross mailbox: 4 x (P, Qh), then two counters
+      if (cudaMalloc(&C.mail, 8 * sizeof(double) + 2 * sizeof(int)) != cudaSuccess ||
+          cudaMemset(C.mail, 0, 8 * sizeof(double) + 2 * sizeof(int)) != cudaSuccess)
+        err = "leg plan mailbox";
+    }
     up(copies, C.copies);
     up(sched, C.sched);
     if (!err.empty()) return err;
@@ -917,7 +989,7 @@ std::string build_leg_plan(int n, LegPlan& P) {
 std::string leg_plan_set_coefs(LegPlan& P, const double* W, const double* E, const double* S,
                                const double* N) {
   const int n = P.n;
-  const int mmax = n / 2 - 2;  // longest leg (shell c - 1)
+  const int mmax = n / 2 - 1;  // longest leg (a leg of the central cross)
   const int nch = ceil_div(std::max(mmax, 1), LQ);
   const int cstride = ceil_div(nch, 32) * 32 * LQ;
   std::vector<double2> h((size_t)4 * LQ * cstride, make_double2(0.0, 0.0));
@@ -964,6 +1036,7 @@ void free_leg_plan(LegPlan& P) {
     cudaFree(C.blocks);
     cudaFree(C.tmap);
     cudaFree(C.copies);
+    cudaFree(C.mail);
     cudaFree(C.sched);
     C = LegColour();
   }
@@ -1023,6 +1096,7 @@ cudaError_t launch_leg_colour(const LegPlan& P, int red, const SweepArgs& s, cud
   a.blocks = C.blocks;
   a.tmap = C.tmap;
   a.copies = C.copies;
+  a.mail = C.mail;
   a.sched = C.sched;
   a.nsched = C.nsched;
   a.err = s.err;

@@ -24,7 +24,7 @@ constexpr int kLegHead = 18;
 constexpr int kLegArrU = kLegHead + kLegThreads * kLegQ + 4 * kLegMaxBlocks + 18;
 constexpr int kLegArrF = kLegArrU + 2 * 16 * kLegMaxBlocks;
 constexpr int kLegStage = kLegArrF + 2 * kLegArrU;
-constexpr int kLegK0 = 48;     // smallest shell the kernel takes (smaller: generic plan)
+constexpr int kLegK0 = 2;      // smallest shell the kernel takes (the corners: generic plan)
 constexpr int kLegNmin = 512;  // smallest grid (n) the kernel runs on
 
 struct LegItem {  // one CTA's work of one cluster iteration
@@ -39,7 +39,8 @@ struct LegItem {  // one CTA's work of one cluster iteration
 struct LegBlock {
   int16_t k;       // shell (layout.py:75-84)
   uint8_t quad;    // bit 0: corner at i = n-1, bit 1: at j = n-1
-  uint8_t split;   // 0 whole block, 1 this CTA holds leg 0 only, 2 leg 1 only
+  uint8_t split;   // 0 whole block, 1 this CTA holds leg 0 only, 2 leg 1 only,
+                   // 3..6 one leg (W, E, S, N) of the central cross
   int16_t t0[2];   // thread of each leg's tip chunk (-1: on the peer CTA)
   int16_t sb[2][3];  // shared slot of each leg's tip element in the f / u-1 / u+1 arrays
 };
@@ -57,6 +58,8 @@ struct LegColour {
   LegCopy* copies = nullptr;  // loads, stores and edge stores of every item
   int4* sched = nullptr;     // cluster iteration: (item rank 0, item rank 1, split, load)
   int nsched = 0, nitems = 0;
+  int cross = 0;              // this colour holds the central cross
+  double* mail = nullptr;     // cross mailbox: 4 x (P, Qh), two counters
   long points = 0;
 };
 struct LegPlan {
@@ -88,6 +91,7 @@ struct LegArgs {
   int nsched;
   int* err;
   long long* timing;  // per-CTA phase clocks (TMG_LEGK_TIMING), or null
+  double* mail;       // cross mailbox (colour with the central cross), or null
 };
 
 // true if the L-shell kernel takes part of this plan's colour stages

@@ -67,8 +67,10 @@ def main(sizes):
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "default"
     if which == "small":  # run with TMG_LEGK_NMIN / TMG_LEGK_K0 lowered
-        main([(16, "wall", 2.0), (18, "wall", 2.0), (40, "wall", 3.0), (64, "centre", 1.5),
-              (100, "wall", 3.0), (130, "wall", 2.0), (256, "wall", 3.0), (600, "wall", 4.0)])
+        # 38, 72: cross legs whose tip chunk holds a single point (pad 16)
+        main([(16, "wall", 2.0), (18, "wall", 2.0), (38, "wall", 2.0), (40, "wall", 3.0),
+              (64, "centre", 1.5), (72, "wall", 3.0), (100, "wall", 3.0), (130, "wall", 2.0),
+              (256, "wall", 3.0), (600, "wall", 4.0)])
     elif which == "split":  # legs over 128 chunks: blocks split over a cluster
         main([(4400, "wall", 4.0), (4362, "wall", 3.0)])
     else:
