@@ -318,12 +318,13 @@ def run_ours(args):
     alg_bytes = 24.0 * n_int
     peak, peak_kind = _peak_hbm()
     achieved = alg_bytes / (sweep_ms * 1e-3) / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     try:  # DRAM bytes of one such sweep from the latest committed ncu capture
         with open(os.path.join(ROOT, "profiles", "latest_traffic.json")) as fh:
             tj = json.load(fh)
         if args.config == "config3" and args.n in (None, 8192):
             traffic = float(tj["bytes_per_sweep"]) / 1e9
+            traffic_src = tj.get("source")
     except Exception:
         traffic = None
 
@@ -409,7 +410,10 @@ def run_ours(args):
         "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_unit": "GB per launch set",
-                     "kernel": "block_sweep_kernel (one finest-level sweep, both colours)",
+                     "traffic_source": traffic_src,
+                     "kernel": ("leg_sweep_kernel (one finest-level sweep, both colours; the "
+                                "four corner points on block_sweep_kernel)" if kind == 4 else
+                                "block_sweep_kernel (one finest-level sweep, both colours)"),
                      "alg_bytes": alg_bytes, "ms": sweep_ms, "peak_kind": peak_kind},
         "sweep_updates_per_s": n_int / (sweep_ms * 1e-3),
         "solve": solve,
