@@ -151,6 +151,9 @@ int tmg_session_sweep_part(tmg_hier* h, int level, int kind, int red, int g0, in
                            void* stream);
 /* f[level+1] = R (f - L u)[level] and u[level+1] = 0 (mgcycle.py:98-100) */
 int tmg_session_restrict(tmg_hier* h, int level, int full, void* stream);
+/* copy one level's u (which = 0) or f (1) out of the session's layout into a
+ * C-order (nx+1) x (ny+1) device array (tests, diagnostics) */
+int tmg_session_read(tmg_hier* h, int level, int which, double* out, void* stream);
 /* u[level] += P u[level+1] (mgcycle.py:101-102) */
 int tmg_session_prolong(tmg_hier* h, int level, void* stream);
 /* the V-cycle from `level` down to the coarsest and back (replicated tail) */

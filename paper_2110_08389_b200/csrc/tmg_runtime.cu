@@ -1119,6 +1119,15 @@ int tmg_session_restrict(tmg_hier* h, int level, int full, void* stream) {
   return zero_field(h->U[level + 1], s);
 }
 
+int tmg_session_read(tmg_hier* h, int level, int which, double* out, void* stream) {
+  if (!h || !h->loaded) return fail(TMG_BADARG, "no solver session loaded");
+  if (level < 0 || level >= (int)h->lv.size() || (which != 0 && which != 1))
+    return fail(TMG_BADARG, "bad level or field");
+  const FieldView& v = which ? h->F[level] : h->U[level];
+  cudaError_t e = launch_from_hybrid(v, out, (cudaStream_t)stream);
+  return e == cudaSuccess ? TMG_OK : cuda_fail(e, "session read");
+}
+
 int tmg_session_prolong(tmg_hier* h, int level, void* stream) {
   int st = session_level(h, level, 1);
   if (st) return st;
