@@ -151,6 +151,12 @@ int tmg_session_sweep_part(tmg_hier* h, int level, int kind, int red, int g0, in
                            void* stream);
 /* f[level+1] = R (f - L u)[level] and u[level+1] = 0 (mgcycle.py:98-100) */
 int tmg_session_restrict(tmg_hier* h, int level, int full, void* stream);
+/* one rank's share of the two transfers (sharded V-cycle): the coarse points
+ * of sharding groups [cg0, cg1) of `kind` get f = R (f - L u) and u = 0; the
+ * fine points of groups [fg0, fg1) get u += P u[level+1] */
+int tmg_session_restrict_part(tmg_hier* h, int level, int full, int kind, int cg0, int cg1,
+                              void* stream);
+int tmg_session_prolong_part(tmg_hier* h, int level, int kind, int fg0, int fg1, void* stream);
 /* copy one level's u (which = 0) or f (1) out of the session's layout into a
  * C-order (nx+1) x (ny+1) device array (tests, diagnostics) */
 int tmg_session_read(tmg_hier* h, int level, int which, double* out, void* stream);

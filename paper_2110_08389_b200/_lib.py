@@ -97,6 +97,8 @@ def _declare(L):
         "tmg_session_sweep_part": ([vp, ip, ip, ip, ip, ip, vp], ip),
         "tmg_session_restrict": ([vp, ip, ip, vp], ip),
         "tmg_session_read": ([vp, ip, ip, vp, vp], ip),
+        "tmg_session_restrict_part": ([vp, ip, ip, ip, ip, ip, vp], ip),
+        "tmg_session_prolong_part": ([vp, ip, ip, ip, ip, vp], ip),
         "tmg_session_prolong": ([vp, ip, vp], ip),
         "tmg_session_tail": ([vp, ip, ip, ip, ip, ip, vp], ip),
         "tmg_session_gather": ([vp, ip, ip, vp, lp, vp, vp], ip),

@@ -146,10 +146,13 @@ cudaError_t launch_hprolong_correct(int nx, int ny, const FieldView& C, const Fi
 // second-generation versions (tmg_transfer.cu), used unless TMG_TRANSFER=v1
 cudaError_t launch_norm2(const GridArgs& g, const FieldView& U, const FieldView& F,
                          unsigned long long* dmax, cudaStream_t s, int scheme, int g0, int g1);
+// [cg0, cg1) / [fg0, fg1): only the coarse / fine points of those sharding
+// groups of `scheme` (one rank's share; g0 = 0: every point)
 cudaError_t launch_restrict2(const GridArgs& g, int full, const FieldView& U, const FieldView& F,
-                             const FieldView& FC, cudaStream_t s, const FieldView* UC = nullptr);
+                             const FieldView& FC, cudaStream_t s, const FieldView* UC = nullptr,
+                             int scheme = 0, int cg0 = 0, int cg1 = 0);
 cudaError_t launch_prolong2(int nx, int ny, const FieldView& C, const FieldView& U,
-                            cudaStream_t s);
+                            cudaStream_t s, int scheme = 0, int fg0 = 0, int fg1 = 0);
 bool transfer_v1();
 cudaError_t launch_to_hybrid(const FieldView& V, const double* nat, cudaStream_t s);
 cudaError_t launch_from_hybrid(const FieldView& V, double* nat, cudaStream_t s);

@@ -448,9 +448,41 @@ std::string build_plan_part(int scheme, int nx, int ny, int q, int mode, int g0,
   std::string err = build_geometry(scheme, nx, ny, g);
   if (!err.empty()) return err;
   filter_groups(g, g0, g1);
+  // a rank's L-shells and (if it owns group c) the cross on the leg kernel
+  const bool legk = leg_plan_applies(scheme, nx, ny, mode) && !g_dry_run;
+  const int k0 = leg_k0(), c = nx / 2;
+  const int ka = std::max(g0, k0), kb = std::min(g1 - 1, c);
+  if (legk && ka <= kb) {
+    Geometry out;
+    out.scheme = g.scheme;
+    out.nx = g.nx;
+    out.ny = g.ny;
+    for (const BlockD& B : g.blocks) {
+      int i = B.hi, j = B.hj;
+      if (i < 0) {
+        i = g.legs[B.leg0].i0;
+        j = g.legs[B.leg0].j0;
+      }
+      const int grp = point_group(g.scheme, g.nx, g.ny, i, j);
+      if (grp >= ka && grp <= kb) continue;
+      BlockD nb = B;
+      nb.leg0 = (int32_t)out.legs.size();
+      for (int l = 0; l < B.nleg; l++) {
+        LegD L = g.legs[B.leg0 + l];
+        L.block = (int32_t)out.blocks.size();
+        out.legs.push_back(L);
+      }
+      out.blocks.push_back(nb);
+    }
+    g = std::move(out);
+  }
   err = pack_plan(std::move(g), q, mode, P);
   P.g0 = g0;
   P.g1 = g1;
+  if (!err.empty() || !legk || ka > kb) return err;
+  P.lp = new LegPlan();
+  err = build_leg_plan(nx, *P.lp, ka, kb);
+  P.device_bytes += P.lp->device_bytes;
   return err;
 }
 

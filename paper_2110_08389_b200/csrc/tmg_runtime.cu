@@ -141,6 +141,9 @@ int get_part_plan(tmg_level* lv, int scheme, int mode, int g0, int g1, Plan** ou
     Plan* p = new Plan();
     std::string err =
         build_plan_part(scheme, lv->nx, lv->ny, default_q(lv->nx, lv->ny), mode, g0, g1, *p);
+    if (err.empty() && p->lp)
+      err = leg_plan_set_coefs(*p->lp, lv->hW.data(), lv->hE.data(), lv->hS.data(),
+                               lv->hN.data());
     if (!err.empty()) {
       free_plan(*p);
       delete p;
@@ -1117,6 +1120,29 @@ int tmg_session_restrict(tmg_hier* h, int level, int full, void* stream) {
                                           h->F[level + 1], s);
   if (e != cudaSuccess) return cuda_fail(e, "defect_restrict");
   return zero_field(h->U[level + 1], s);
+}
+
+int tmg_session_restrict_part(tmg_hier* h, int level, int full, int kind, int cg0, int cg1,
+                              void* stream) {
+  int st = session_level(h, level, 1);
+  if (st) return st;
+  if (!valid_kind(kind) || cg0 < 1 || cg1 <= cg0)
+    return fail(TMG_BADARG, "bad kind or coarse group range");
+  cudaError_t e = launch_restrict2(h->lv[level]->grid(), full, h->U[level], h->F[level],
+                                   h->F[level + 1], (cudaStream_t)stream, &h->U[level + 1], kind,
+                                   cg0, cg1);
+  return e == cudaSuccess ? TMG_OK : cuda_fail(e, "defect_restrict part");
+}
+
+int tmg_session_prolong_part(tmg_hier* h, int level, int kind, int fg0, int fg1, void* stream) {
+  int st = session_level(h, level, 1);
+  if (st) return st;
+  if (!valid_kind(kind) || fg0 < 1 || fg1 <= fg0)
+    return fail(TMG_BADARG, "bad kind or fine group range");
+  tmg_level* lv = h->lv[level];
+  cudaError_t e = launch_prolong2(lv->nx, lv->ny, h->U[level + 1], h->U[level],
+                                  (cudaStream_t)stream, kind, fg0, fg1);
+  return e == cudaSuccess ? TMG_OK : cuda_fail(e, "prolong_correct part");
 }
 
 int tmg_session_read(tmg_hier* h, int level, int which, double* out, void* stream) {

@@ -120,6 +120,36 @@ struct GroupSel2 {
   int scheme, g0, g1;
 };
 
+// (lo, hi) = the smallest / largest sharding group (tmg_layout.h point_group)
+// of the interior points of a box; a CTA whose box misses [g0, g1) skips
+__device__ __forceinline__ bool box_in_groups(const GroupSel2& s, int nx, int ny, int i0, int j0,
+                                              int ni, int nj) {
+  if (s.g0 <= 0) return true;
+  const int ia = max(i0, 1), ib = min(i0 + ni - 1, nx - 1);
+  const int ja = max(j0, 1), jb = min(j0 + nj - 1, ny - 1);
+  if (ia > ib || ja > jb) return false;
+  int lo, hi;
+  if (s.scheme == 1) {  // zebra_x: row j
+    lo = ja;
+    hi = jb;
+  } else if (s.scheme == 4 || s.scheme == 5) {
+    int ilo, ihi, jlo, jhi;
+    mirror_range2(ia, ib, nx, ilo, ihi);
+    mirror_range2(ja, jb, ny, jlo, jhi);
+    lo = s.scheme == 4 ? max(ilo, jlo) : min(ilo, jlo);
+    hi = s.scheme == 4 ? max(ihi, jhi) : min(ihi, jhi);
+  } else {  // zebra_y, checkerboard: column i
+    lo = ia;
+    hi = ib;
+  }
+  return hi >= s.g0 && lo < s.g1;
+}
+__device__ __forceinline__ bool in_groups(const GroupSel2& s, int nx, int ny, int i, int j) {
+  if (s.g0 <= 0) return true;
+  const int gp = point_group(s.scheme, nx, ny, i, j);
+  return gp >= s.g0 && gp < s.g1;
+}
+
 // ---- residual max-norm: 32 x 32 points per CTA, 4 per thread ----------------
 constexpr int NT = 32, NE = NT + 2, NLD = NE + 1;
 
@@ -189,7 +219,7 @@ constexpr int RPER = (RD * RD + 255) / 256;
 // V-cycle needs no separate zeroing launch; the rings stay 0)
 __global__ void __launch_bounds__(256) restrict2_kernel(GridArgs g, int full, FieldView U,
                                                         FieldView F, FieldView FC, FieldView UC,
-                                                        int zero_uc) {
+                                                        int zero_uc, GroupSel2 csel) {
   extern __shared__ double rsm[];
   double* su = rsm;
   double* sd = rsm + RU * RLU;
@@ -197,6 +227,11 @@ __global__ void __launch_bounds__(256) restrict2_kernel(GridArgs g, int full, Fi
   const int I0 = 1 + blockIdx.y * RC, J0 = 1 + blockIdx.x * RC;
   const int ui0 = 2 * I0 - 2, uj0 = 2 * J0 - 2;
   pdl_trigger();
+  // a partial restriction (one rank's coarse groups) skips tiles outside them
+  if (!box_in_groups(csel, nxc, nyc, I0, J0, RC, RC)) {
+    pdl_wait();
+    return;
+  }
   const int own = box_owner(U, ui0, uj0, RU, RU);
   pdl_wait();
   double fv[RPER];
@@ -242,7 +277,7 @@ __global__ void __launch_bounds__(256) restrict2_kernel(GridArgs g, int full, Fi
   const int p = cpt / RC, q = cpt - p * RC;
   const int ca = cown == 1 ? q : p, cb = cown == 1 ? p : q;  // I offset, J offset
   const int I = I0 + ca, J = J0 + cb;
-  if (I < nxc && J < nyc) {
+  if (I < nxc && J < nyc && in_groups(csel, nxc, nyc, I, J)) {
     const int a = 2 * ca + 1, b = 2 * cb + 1;  // fine (i, j) offsets in the defect tile
     const int o = own == 1 ? b * RLD + a : a * RLD + b;
     const int di = own == 1 ? 1 : RLD, dj = own == 1 ? RLD : 1;
@@ -273,9 +308,15 @@ __global__ void __launch_bounds__(256) restrict2_kernel(GridArgs g, int full, Fi
 // ---- fused prolongation + correction: 32 x 32 fine points per CTA --------
 constexpr int PC_E = NT / 2 + 1, PC_LD = PC_E + 1;
 
-__global__ void __launch_bounds__(256) prolong2_kernel(int nx, int ny, FieldView C, FieldView U) {
+__global__ void __launch_bounds__(256) prolong2_kernel(int nx, int ny, FieldView C, FieldView U,
+                                                       GroupSel2 fsel) {
   __shared__ double sc[PC_E * PC_LD];
   const int i0 = 1 + blockIdx.y * NT, j0 = 1 + blockIdx.x * NT;
+  if (!box_in_groups(fsel, nx, ny, i0, j0, NT, NT)) {  // outside a rank's groups
+    pdl_trigger();
+    pdl_wait();
+    return;
+  }
   const int own = box_owner(U, i0, j0, NT, NT);
   const int Ic0 = i0 >> 1, Jc0 = j0 >> 1;
   pdl_trigger();
@@ -296,7 +337,7 @@ __global__ void __launch_bounds__(256) prolong2_kernel(int nx, int ny, FieldView
 #pragma unroll
   for (int k = 0; k < 4; k++) {
     const int i = pi[k], j = pj[k];
-    if (i >= nx || j >= ny) continue;
+    if (i >= nx || j >= ny || !in_groups(fsel, nx, ny, i, j)) continue;
     const int I = i >> 1, J = j >> 1;
     const int o = (I - Ic0) * cI + (J - Jc0) * cJ;
     double pv;
@@ -606,7 +647,8 @@ cudaError_t launch_norm2(const GridArgs& g, const FieldView& U, const FieldView&
 }
 
 cudaError_t launch_restrict2(const GridArgs& g, int full, const FieldView& U, const FieldView& F,
-                             const FieldView& FC, cudaStream_t s, const FieldView* UC) {
+                             const FieldView& FC, cudaStream_t s, const FieldView* UC, int scheme,
+                             int cg0, int cg1) {
   const int nxc = g.nx / 2, nyc = g.ny / 2;
   if (nxc < 2 || nyc < 2) return cudaSuccess;
   dim3 grid((nyc - 1 + RC - 1) / RC, (nxc - 1 + RC - 1) / RC);
@@ -620,15 +662,16 @@ cudaError_t launch_restrict2(const GridArgs& g, int full, const FieldView& U, co
     attr = true;
   }
   return launch_pdl(restrict2_kernel, grid, dim3(256), kRestrictSmem, s, g, full, U, F, FC,
-                    UC ? *UC : FC, UC ? 1 : 0);
+                    UC ? *UC : FC, UC ? 1 : 0, GroupSel2{scheme, cg0, cg1});
 }
 
 cudaError_t launch_prolong2(int nx, int ny, const FieldView& C, const FieldView& U,
-                            cudaStream_t s) {
+                            cudaStream_t s, int scheme, int fg0, int fg1) {
   if (nx < 2 || ny < 2) return cudaSuccess;
   dim3 grid((ny - 1 + NT - 1) / NT, (nx - 1 + NT - 1) / NT);
   TMG_COUNT(1);
-  return launch_pdl(prolong2_kernel, grid, dim3(256), 0, s, nx, ny, C, U);
+  return launch_pdl(prolong2_kernel, grid, dim3(256), 0, s, nx, ny, C, U,
+                    GroupSel2{scheme, fg0, fg1});
 }
 
 }  // namespace tmg

@@ -710,6 +710,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
 #ifdef TMG_LEGK_TIMING
   if (timing)
     for (int i = 0; i < 8; i++) a.timing[(blockIdx.x + (tid ? gridDim.x : 0)) * 8 + i] = tacc[i];
+#ifdef TMG_LEGK_TIMING
+  if (a.timing && tid == 0) {  // SM of every CTA (cluster placement)
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    a.timing[16 * 1024 + blockIdx.x] = sm;
+  }
+#endif
 #endif
   if (tid < 32) bulk_wait_all();
   bad |= phi < 0x01A56E1F;  // |pivot| < 1e-300 (high word of 1e-300)
@@ -758,22 +765,22 @@ int leg_k0() {
 
 // Blocks of one colour on an n x n grid handled by the leg kernel: shells
 // k in [k0, c) of that colour, the four quadrants (layout.py:75-84).
-static void colour_blocks(int n, int red, std::vector<HostBlock>& out) {
+static void colour_blocks(int n, int red, int kmin, int kmax, std::vector<HostBlock>& out) {
   const int c = n / 2;  // (s + 1) / 2 with s = n - 1
-  for (int k = c - 1; k >= leg_k0(); k--) {
+  for (int k = std::min(c - 1, kmax); k >= std::max(leg_k0(), kmin); k--) {
     if (((k % 2) != 0) != (red != 0)) continue;  // layout.py:22-23
     for (int q = 0; q < 4; q++) out.push_back(HostBlock{k, q, ceil_div(k - 1, LQ)});
   }
 }
 
-std::string build_leg_plan(int n, LegPlan& P) {
+std::string build_leg_plan(int n, LegPlan& P, int kmin, int kmax) {
   P = LegPlan();
   P.n = n;
   const int ld = n + 1;
   for (int red = 1; red >= 0; red--) {
     LegColour& C = P.col[red];
     std::vector<HostBlock> blocks;
-    colour_blocks(n, red, blocks);
+    colour_blocks(n, red, kmin, kmax, blocks);
     std::vector<LegItem> items;
     std::vector<LegBlock> iblocks;
     std::vector<uint16_t> tmap;
@@ -896,7 +903,7 @@ std::string build_leg_plan(int n, LegPlan& P) {
     // the branch row goes through a global mailbox)
     std::vector<int4> sched_split;
     const int c = n / 2;
-    if (((c % 2) != 0) == (red != 0)) {
+    if (((c % 2) != 0) == (red != 0) && kmin <= c && c <= kmax) {
       const int quads[4] = {0, 1, 0, 2};  // W: LL x-leg, E: LR x-leg, S: LL y-leg, N: UL y-leg
       int ids[4];
       for (int q = 0; q < 4; q++) {
@@ -1116,6 +1123,16 @@ cudaError_t launch_leg_colour(const LegPlan& P, int red, const SweepArgs& s, cud
 // Average per-CTA clock cycles of the leg kernel's phases in its last launch
 // (TMG_LEGK_TIMING=1 only): setup, stage wait, forward, back, reduced system,
 // branch, finalize, stores.  Returns the number of CTAs averaged.
+// SM ids of the last timed launch's CTAs (TMG_LEGK_TIMING builds): returns the count
+extern "C" int tmg_debug_leg_smids(int* out, int cap) {
+  if (!tmg::g_leg_timing) return 0;
+  const int n = std::min(cap, tmg::g_leg_timing_ctas);
+  std::vector<long long> h(n);
+  cudaMemcpy(h.data(), tmg::g_leg_timing + 16 * 1024, n * sizeof(long long), cudaMemcpyDeviceToHost);
+  for (int i = 0; i < n; i++) out[i] = (int)h[i];
+  return n;
+}
+
 extern "C" int tmg_debug_leg_phases(double* out8 /* [16] */) {
   for (int i = 0; i < 16; i++) out8[i] = 0.0;
   if (!tmg::g_leg_timing || tmg::g_leg_timing_ctas == 0) return 0;

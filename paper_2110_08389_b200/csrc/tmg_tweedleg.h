@@ -97,7 +97,8 @@ struct LegArgs {
 // true if the L-shell kernel takes part of this plan's colour stages
 bool leg_plan_applies(int scheme, int nx, int ny, int mode);
 int leg_k0();
-std::string build_leg_plan(int n, LegPlan& P);
+// shells k in [kmin, kmax] (k = n/2: the central cross); default: all
+std::string build_leg_plan(int n, LegPlan& P, int kmin = 0, int kmax = 1 << 30);
 std::string leg_plan_set_coefs(LegPlan& P, const double* W, const double* E, const double* S,
                                const double* N);
 void free_leg_plan(LegPlan& P);

@@ -109,10 +109,10 @@ class NativeCubeShardOps:
     def sweep(self, level, red, g0, g1):
         _check(self.L.tmg_cube_sweep_part(self.h._h, level, int(red), g0, g1, self._s()))
 
-    def restrict(self, level):
+    def restrict(self, level, groups=None):  # whole level (groups: a rank's share)
         _check(self.L.tmg_cube_restrict(self.h._h, level, self._s()))
 
-    def prolong(self, level):
+    def prolong(self, level, groups=None):
         _check(self.L.tmg_cube_prolong(self.h._h, level, self._s()))
 
     def tail(self, level):

@@ -28,11 +28,11 @@ Per V-cycle level (mgcycle.py:89-104 with smoothers.py:139-150 split):
 
 * sweep: each colour stage runs on the rank's blocks, then the ranks swap
   ``HALO`` = 2 groups of u with each neighbour;
-* residual + restriction: computed on the whole local array; the coarse
-  points a rank owns only read fine defects within one group of its range,
-  which the width-2 u halo and width-2 f halo keep exact; the coarse f halo
-  is then swapped;
-* prolongation + correction, then a u halo swap;
+* residual + restriction: computed for the rank's coarse groups and their
+  halo only (tiles outside skip); the coarse points a rank owns only read
+  fine defects within one group of its range, which the width-2 u halo and
+  width-2 f halo keep exact; the coarse f halo is then swapped;
+* prolongation + correction on the rank's fine groups, then a u halo swap;
 * residual norm: max over the owned groups, then an all-reduce (MAX);
 * coarse levels: once a rank would own fewer than ``min_groups`` groups the
   ranks all-gather the coarse right-hand side and every rank runs the rest
@@ -296,11 +296,24 @@ class NativeShardOps:
         _lib.check(self.L.tmg_session_sweep_part(self.native, level, self.kid, int(red), g0, g1,
                                                  self._s()))
 
-    def restrict(self, level):
-        _lib.check(self.L.tmg_session_restrict(self.native, level, self.full, self._s()))
+    def restrict(self, level, groups=None):
+        """f[level+1] = R(f - Lu), u[level+1] = 0; groups = (g0, g1): only the
+        coarse points of those sharding groups (one rank's share + halo)."""
+        if groups is None:
+            _lib.check(self.L.tmg_session_restrict(self.native, level, self.full, self._s()))
+        else:
+            _lib.check(self.L.tmg_session_restrict_part(self.native, level, self.full, self.kid,
+                                                        int(groups[0]), int(groups[1]),
+                                                        self._s()))
 
-    def prolong(self, level):
-        _lib.check(self.L.tmg_session_prolong(self.native, level, self._s()))
+    def prolong(self, level, groups=None):
+        """u[level] += P u[level+1]; groups = (g0, g1): only those fine groups."""
+        if groups is None:
+            _lib.check(self.L.tmg_session_prolong(self.native, level, self._s()))
+        else:
+            _lib.check(self.L.tmg_session_prolong_part(self.native, level, self.kid,
+                                                       int(groups[0]), int(groups[1]),
+                                                       self._s()))
 
     def tail(self, level):
         _lib.check(self.L.tmg_session_tail(self.native, level, self.kid, self.full, self.nu1,
@@ -335,14 +348,27 @@ class ShardedSolver:
                                     sizes_fn=self.ops.group_sizes, min_groups=min_groups)
         r = self.comm.rank
         self.exchanges = 0
+        # per level: both sides' send / receive offsets concatenated, so that a
+        # swap is one gather kernel, the exchange and one scatter kernel; each
+        # side's message is a view of the joint buffer
         self._halo = []
         for lvl in range(self.plan.nshard):
-            sides = []
+            peers, sis, ris = [], [], []
             for peer, (s0, s1), (r0, r1) in self.plan.halo(lvl, r):
-                si, ri = self.ops.offsets(lvl, s0, s1), self.ops.offsets(lvl, r0, r1)
-                sides.append((peer, si, ri, self.ops.buffer(si.numel()),
-                              self.ops.buffer(ri.numel())))
-            self._halo.append(sides)
+                peers.append(peer)
+                sis.append(self.ops.offsets(lvl, s0, s1))
+                ris.append(self.ops.offsets(lvl, r0, r1))
+            if not peers:
+                self._halo.append(None)
+                continue
+            si, ri = torch.cat(sis), torch.cat(ris)
+            sb, rb = self.ops.buffer(si.numel()), self.ops.buffer(ri.numel())
+            pairs, so, ro = [], 0, 0
+            for peer, a, b in zip(peers, sis, ris):
+                pairs.append((peer, sb[so:so + a.numel()], rb[ro:ro + b.numel()]))
+                so += a.numel()
+                ro += b.numel()
+            self._halo.append((si, ri, sb, rb, pairs))
         self._gathers = {}
         if self.comm.world > 1:
             # a collective before the first batched send/recv of the group
@@ -351,11 +377,11 @@ class ShardedSolver:
 
     # -- plumbing ---------------------------------------------------------
     def _swap(self, level, which):
-        sides = self._halo[level]
-        for peer, si, ri, sb, rb in sides:
+        halo = self._halo[level]
+        if halo is not None:
+            si, ri, sb, rb, pairs = halo
             self.ops.gather(level, which, si, sb)
-        self.comm.exchange([(peer, sb, rb) for peer, si, ri, sb, rb in sides])
-        for peer, si, ri, sb, rb in sides:
+            self.comm.exchange(pairs)
             self.ops.scatter(level, which, ri, rb)
         self.exchanges += 1
 
@@ -388,13 +414,19 @@ class ShardedSolver:
             self.ops.tail(level)
             return
         self._smooth(level, self.cfg.nu1)
-        self.ops.restrict(level)
         if level + 1 < self.plan.nshard:
+            # the rank's coarse groups and their halo only: the owned points
+            # read fine defects inside the width-2 fine halo, the halo's f is
+            # swapped right after and its u must be the zero initial guess
+            g0, g1 = self.plan.own(level + 1, self.comm.rank)
+            G = self.plan.bounds[level + 1][-1] - 1
+            self.ops.restrict(level, (max(g0 - HALO, 1), min(g1 + HALO, G + 1)))
             self._swap(level + 1, 1)
-        else:
+        else:  # the replicated tail needs every coarse point (u = 0 everywhere)
+            self.ops.restrict(level)
             self._allgather_field(level + 1, 1)
         self._cycle(level + 1)
-        self.ops.prolong(level)
+        self.ops.prolong(level, self.plan.own(level, self.comm.rank))
         self._swap(level, 0)
         self._smooth(level, self.cfg.nu2)
 

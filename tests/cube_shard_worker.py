@@ -79,12 +79,12 @@ class OracleCubeShardOps:
     def sweep(self, level, red, g0, g1):
         self.o.sweep_part(self.st[level], self.U[level], self.F[level], red, g0, g1)
 
-    def restrict(self, level):
+    def restrict(self, level, groups=None):  # whole level (groups: a rank's share)
         d = self.o.defect(self.st[level], self.U[level], self.F[level])
         self.F[level + 1][...] = self.o.restrict(d)
         self.U[level + 1][...] = 0.0
 
-    def prolong(self, level):
+    def prolong(self, level, groups=None):
         self.o.prolong_add(self.U[level + 1], self.U[level])
 
     def tail(self, level):

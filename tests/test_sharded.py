@@ -165,7 +165,8 @@ def test_sharded_solve_oracle_ops(orc, tmp_path, kind, n, ny, world, restriction
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("kind,n,world", [("tweed", 256, 2), ("wireframe", 128, 2),
-                                          ("zebra_x", 64, 2), ("checkerboard", 64, 2)])
+                                          ("zebra_x", 64, 2), ("checkerboard", 64, 2),
+                                          ("tweed", 256, 4), ("wireframe", 256, 4)])
 def test_sharded_solve_native(orc, cuda, tmp_path, kind, n, world):
     """The product path sharded over ranks equals the single-domain oracle
     (per-sweep 1e-10 north-star tolerance on the final iterate; identical
@@ -181,18 +182,21 @@ def test_sharded_solve_native(orc, cuda, tmp_path, kind, n, world):
             assert abs(a - b) <= 1e-5 * b + 1e-11 * d0
         scale = np.abs(u_ref).max()
         assert np.abs(o["u"] - u_ref).max() <= 1e-10 * scale
-    assert np.array_equal(outs[0]["u"], outs[1]["u"])
+    for o in outs[1:]:
+        assert np.array_equal(outs[0]["u"], o["u"])
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("kind", sharded.SHARDABLE)
-def test_partial_sweeps_native(orc, cuda, kind):
+@pytest.mark.parametrize("kind,n", [(k, 64) for k in sharded.SHARDABLE] +
+                         [("tweed", 600), ("tweed", 1026)])
+def test_partial_sweeps_native(orc, cuda, kind, n):
     """Colour stages over group ranges on the device equal the oracle's
-    partial stages; the ranges together equal one full sweep."""
+    partial stages; the ranges together equal one full sweep.  At n >= 512
+    the tweed ranges run their L-shells (and, in the last range, the cross)
+    on the leg kernel."""
     import torch
 
     from paper_2110_08389_b200 import _device, _lib, grid, mgcycle
-    n = 64
     x, y = grid.make_coords("wall", n, 1.0, 3.0), grid.make_coords("wall", n, 2.0, 2.0)
     h = grid.build_hierarchy(x, y)
     st = h.finest.stencil
@@ -219,3 +223,72 @@ def test_partial_sweeps_native(orc, cuda, kind):
     assert np.array_equal(uo, ufull)
     assert np.abs(got - uo).max() <= 1e-12 * np.abs(uo).max()
     _lib.check(_lib.lib().tmg_session_check(ops.native, _device.stream_handle()))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", sharded.SHARDABLE)
+def test_partial_transfers_native(orc, cuda, kind):
+    """One rank's share of the transfers (tmg_session_restrict_part /
+    _prolong_part): restricting group range by group range, then prolonging
+    range by range, gives bit for bit the full-level transfers, and the
+    coarse u is zeroed exactly on the requested groups."""
+    import ctypes
+
+    import torch
+
+    from paper_2110_08389_b200 import _device, _lib, grid
+
+    n, m = 300, 260
+    x, y = grid.make_coords("wall", n, 1.0, 3.0), grid.make_coords("centre", m, 1.0, 1.5)
+    h = grid.build_hierarchy(x, y)
+    rng = np.random.default_rng(11)
+    u0 = rng.standard_normal((n + 1, m + 1))
+    f = rng.standard_normal((n + 1, m + 1))
+    L = _lib.lib()
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    kid = _lib.KIND_IDS[kind]
+    nc, mc = n // 2, m // 2
+
+    def run(parts):
+        ops = sharded.NativeShardOps(h, kind)
+        ops.load(_device.to_device(u0), _device.to_device(f))
+        fill = torch.full((nc + 1, mc + 1), 7.0, dtype=torch.float64, device="cuda")
+        if parts is None:
+            ops.restrict(0)
+        else:
+            for g in parts:
+                ops.restrict(0, g)
+        fc = torch.empty_like(fill)
+        uc = torch.empty_like(fill)
+        _lib.check(L.tmg_session_read(ops.native, 1, 1, P(fc), s))
+        _lib.check(L.tmg_session_read(ops.native, 1, 0, P(uc), s))
+        # a nonzero coarse correction, then the prolongation (tensors kept
+        # alive: the caching allocator would hand a freed block straight on)
+        enc = ops.offsets(1, 1, Gc + 1)
+        vals = torch.linspace(-1, 1, int(enc.numel()), dtype=torch.float64, device="cuda")
+        _lib.check(L.tmg_session_scatter(ops.native, 1, 0, P(enc), int(enc.numel()), P(vals), s))
+        if parts is None:
+            ops.prolong(0)
+        else:
+            for g in fparts:
+                ops.prolong(0, g)
+        out = torch.empty((n + 1, m + 1), dtype=torch.float64, device="cuda")
+        ops.store(out)
+        torch.cuda.synchronize()
+        return fc.cpu().numpy(), uc.cpu().numpy(), out.cpu().numpy()
+
+    Gc = sharded.group_count(kind, nc, mc)
+    G = sharded.group_count(kind, n, m)
+    cparts = [(1, Gc // 3), (Gc // 3, Gc // 2 + 1), (Gc // 2 + 1, Gc + 1)]
+    fparts = [(1, G // 4), (G // 4, G // 2), (G // 2, G + 1)]
+    fa, ua, oa = run(None)
+    fb, ub, ob = run(cparts)
+    assert np.array_equal(fa[1:-1, 1:-1], fb[1:-1, 1:-1])
+    assert not ub[1:-1, 1:-1].any()
+    assert np.array_equal(oa, ob)
+    # the coarse points outside a partial range keep their values
+    fc1, uc1, _ = run([cparts[0]])
+    gm = orc.group_map(kind, nc, mc)
+    inside = (gm >= cparts[0][0]) & (gm < cparts[0][1])
+    assert np.array_equal(fc1[inside], fa[inside])

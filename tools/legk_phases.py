@@ -24,3 +24,12 @@ for who, vals in (("thread0", list(out)[:8]), ("thread96", list(out)[8:])):
     tot = sum(vals)
     print(json.dumps({"who": who, "ctas": n, "cycles_per_cta": tot,
                       "share": {k: round(v / tot, 3) for k, v in zip(names, vals)}}))
+
+ids = (ctypes.c_int * 1024)()
+k = L.tmg_debug_leg_smids(ids, 1024)
+pairs = [(ids[2 * c], ids[2 * c + 1]) for c in range(k // 2)]
+same = sum(1 for a, b in pairs if a == b)
+from collections import Counter
+per_sm = Counter(ids[i] for i in range(k))
+print(json.dumps({"clusters": len(pairs), "pairs_on_one_sm": same,
+                  "ctas_per_sm": dict(Counter(per_sm.values()))}))
