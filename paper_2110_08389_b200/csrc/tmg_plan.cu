@@ -374,7 +374,8 @@ std::string build_plan(int scheme, int nx, int ny, int q, int mode, Plan& P) {
   if (!err.empty()) return err;
   const bool legk = leg_plan_applies(scheme, nx, ny, mode) && !g_dry_run;
   if (legk) {  // L-shells k in [k0, c) and the cross go to the leg kernel
-    const int k0 = leg_k0(), c = nx / 2;
+    // (with the default k0 = 2 the corner points go to it as well)
+    const int k0 = leg_k0() <= 2 ? 1 : leg_k0(), c = nx / 2;
     Geometry out;
     out.scheme = g.scheme;
     out.nx = g.nx;
@@ -450,7 +451,7 @@ std::string build_plan_part(int scheme, int nx, int ny, int q, int mode, int g0,
   filter_groups(g, g0, g1);
   // a rank's L-shells and (if it owns group c) the cross on the leg kernel
   const bool legk = leg_plan_applies(scheme, nx, ny, mode) && !g_dry_run;
-  const int k0 = leg_k0(), c = nx / 2;
+  const int k0 = leg_k0() <= 2 ? 1 : leg_k0(), c = nx / 2;  // 1: the corner points too
   const int ka = std::max(g0, k0), kb = std::min(g1 - 1, c);
   if (legk && ka <= kb) {
     Geometry out;

@@ -323,6 +323,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
   }
   __syncthreads();
   pdl_wait();  // the fields of the previous kernel are complete from here on
+  if (a.corners && blockIdx.x == 0 && tid < 4) {
+    // the four interior corner points: point blocks of the red stage
+    // (layout.py:72-74, relax_points _ckernels.pyx:42-51); their
+    // neighbours are boundary or black-shell points, frozen in this stage
+    const int i = (tid & 1) ? n - 1 : 1, j = (tid & 2) ? n - 1 : 1;
+    auto uat = [&](int ii, int jj) {
+      return owns_t(LM_TWEED, n, n, ii, jj) ? a.ut[(size_t)jj * ld + ii] : a.un[(size_t)ii * ld + jj];
+    };
+    const double Wi = __ldg(a.W + i), Ei = __ldg(a.E + i), Sj = __ldg(a.S + j),
+                 Nj = __ldg(a.N + j);
+    const double b = -(Wi + Ei + Sj + Nj);
+    const double r = a.fn[(size_t)i * ld + j] - Wi * uat(i - 1, j) - Ei * uat(i + 1, j) -
+                     Sj * uat(i, j - 1) - Nj * uat(i, j + 1);
+    if (bad_pivot(b)) atomicOr(a.err, 1);
+    a.un[(size_t)i * ld + j] = r / b;
+  }
 
   auto sched_at = [&](int s) -> int4 {
     const int ci = cid + s * ncl;
@@ -965,6 +981,7 @@ std::string build_leg_plan(int n, LegPlan& P, int kmin, int kmax) {
       const int sb = ib >= 0 ? items[ib].steps : 0;
       sched.push_back(make_int4(ia, ib, (items[ia].steps << 8) | (sb << 16), whole[i].first));
     }
+    C.corners = red && kmin <= 1;  // the four corner points (k = 1, red)
     C.nsched = (int)sched.size();
     C.nitems = (int)items.size();
     C.points = 0;
@@ -1076,7 +1093,7 @@ bool leg_timing_on() {
 
 cudaError_t launch_leg_colour(const LegPlan& P, int red, const SweepArgs& s, cudaStream_t stream) {
   const LegColour& C = P.col[red ? 1 : 0];
-  if (C.nsched == 0) return cudaSuccess;
+  if (C.nsched == 0 && !C.corners) return cudaSuccess;
   cudaError_t e = init_leg_kernel();
   if (e != cudaSuccess) return e;
   static int sms = 0;
@@ -1104,10 +1121,11 @@ cudaError_t launch_leg_colour(const LegPlan& P, int red, const SweepArgs& s, cud
   a.tmap = C.tmap;
   a.copies = C.copies;
   a.mail = C.mail;
+  a.corners = C.corners;
   a.sched = C.sched;
   a.nsched = C.nsched;
   a.err = s.err;
-  const int ncl = std::max(1, std::min(sms, C.nsched));  // two CTAs per SM
+  const int ncl = std::max(1, std::min(sms, C.nsched));  // two CTAs per SM (>= 1 for the corners)
   a.timing = nullptr;
   if (leg_timing_on()) {
     if (!g_leg_timing) cudaMalloc(&g_leg_timing, sizeof(long long) * 16 * 2 * 1024);

@@ -24,7 +24,7 @@ constexpr int kLegHead = 18;
 constexpr int kLegArrU = kLegHead + kLegThreads * kLegQ + 4 * kLegMaxBlocks + 18;
 constexpr int kLegArrF = kLegArrU + 2 * 16 * kLegMaxBlocks;
 constexpr int kLegStage = kLegArrF + 2 * kLegArrU;
-constexpr int kLegK0 = 2;      // smallest shell the kernel takes (the corners: generic plan)
+constexpr int kLegK0 = 2;      // smallest shell the kernel takes (at 2 it takes the corners too)
 constexpr int kLegNmin = 512;  // smallest grid (n) the kernel runs on
 
 struct LegItem {  // one CTA's work of one cluster iteration
@@ -59,6 +59,7 @@ struct LegColour {
   int4* sched = nullptr;     // cluster iteration: (item rank 0, item rank 1, split, load)
   int nsched = 0, nitems = 0;
   int cross = 0;              // this colour holds the central cross
+  int corners = 0;            // this colour (red) relaxes the four corner points
   double* mail = nullptr;     // cross mailbox: 4 x (P, Qh), two counters
   long points = 0;
 };
@@ -92,6 +93,7 @@ struct LegArgs {
   int* err;
   long long* timing;  // per-CTA phase clocks (TMG_LEGK_TIMING), or null
   double* mail;       // cross mailbox (colour with the central cross), or null
+  int corners;        // CTA 0 relaxes the four corner points first
 };
 
 // true if the L-shell kernel takes part of this plan's colour stages
