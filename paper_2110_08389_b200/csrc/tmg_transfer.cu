@@ -9,6 +9,7 @@
 // (stencil.py:82-87, transfer.py:33-38, 51-53), bit-identical to the
 // natural-layout kernels of tmg_grid.cu.
 #include <cstdlib>
+#include <string>
 
 #include "tmg_kernels.h"
 
@@ -303,6 +304,170 @@ __global__ void __launch_bounds__(256) restrict2_kernel(GridArgs g, int full, Fi
     }
   }
   }
+}
+
+// ---- fused residual + restriction, second layout: 15 x 15 coarse points per
+// CTA (31 x 31 fine defects, a 33 x 33 u box), warps along the tile's rows and
+// lanes along its columns in the owner buffer's orientation, so that every
+// index is a compile-time offset (restrict2_kernel spends most of its issue
+// slots on per-element index division).  Same arithmetic, bit for bit.
+constexpr int R3C = 15, R3D = 31, R3U = 33, R3LU = 34, R3LD = 32;
+
+// MODE 0: box inside the grid in the natural buffer (rows = i), 1: inside the
+// grid in the transposed buffer (rows = j), 2: anything else (rows = i, each
+// point read through its owner: grid edges, mixed-ownership boxes)
+template <int MODE>
+__device__ __forceinline__ void restrict3_body(const GridArgs& g, int full, const FieldView& U,
+                                               const FieldView& F, const FieldView& FC,
+                                               const FieldView& UC, int zero_uc,
+                                               const GroupSel2& csel, int own, int I0, int J0,
+                                               double* su, double* sd) {
+  constexpr bool T = MODE == 1, GEN = MODE == 2;
+  const int nxc = g.nx / 2, nyc = g.ny / 2;
+  const int ui0 = 2 * I0 - 2, uj0 = 2 * J0 - 2;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nA = T ? g.nx : g.ny, nM = T ? g.ny : g.nx;  // column / row axis extents
+  const int a0 = T ? ui0 : uj0, m0 = T ? uj0 : ui0;       // tile origin (column, row)
+  const double* colLo = T ? g.W : g.S;  // couplings along the column axis
+  const double* colHi = T ? g.E : g.N;
+  const double* rowLo = T ? g.S : g.W;  // along the row axis
+  const double* rowHi = T ? g.N : g.E;
+  // per-thread couplings: the defect column x = lane and rows y = w + 8q
+  const int xc = a0 + 1 + lane;
+  const bool colok = lane < R3D && (!GEN || xc < nA);
+  const double cLo = colok ? __ldg(colLo + xc) : 0.0;
+  const double cHi = colok ? __ldg(colHi + xc) : 0.0;
+  double rLo[4], rHi[4];
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const int y = w + 8 * q, mr = m0 + 1 + y;
+    const bool ok = (q < 3 || y < R3D) && (!GEN || mr < nM);
+    rLo[q] = ok ? __ldg(rowLo + mr) : 0.0;
+    rHi[q] = ok ? __ldg(rowHi + mr) : 0.0;
+  }
+  pdl_wait();
+  double fv[4], uv[5], ux[5];
+  if (!GEN) {
+    // the whole 33 x 33 box lies in [0, n] and every defect point is interior
+    const size_t ldr = (size_t)nA + 1, l8 = 8 * ldr;
+    const double* fp = (T ? F.t : F.n) + (m0 + 1 + w) * ldr + a0 + 1 + lane;
+    const double* up = (T ? U.t : U.n) + (m0 + w) * ldr + a0 + lane;
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+      fv[q] = ((q < 3 || w < 7) && lane < R3D) ? __ldg(fp + q * l8) : 0.0;
+#pragma unroll
+    for (int q = 0; q < 5; q++) {
+      const bool ok = q < 4 || w == 0;
+      uv[q] = ok ? __ldg(up + q * l8) : 0.0;
+      ux[q] = (ok && lane == 0) ? __ldg(up + q * l8 + 32) : 0.0;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int y = w + 8 * q, mr = m0 + 1 + y, ac = a0 + 1 + lane;
+      const bool in = y < R3D && lane < R3D && mr < nM && ac < nA;
+      fv[q] = in ? ld_view(F, own, mr, ac) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 5; q++) {
+      const int mr = m0 + w + 8 * q, ac = a0 + lane;
+      const bool y_in = w + 8 * q < R3U && mr <= nM;
+      uv[q] = (y_in && ac <= nA) ? ld_view(U, own, mr, ac) : 0.0;
+      ux[q] = (y_in && lane == 0 && a0 + 32 <= nA) ? ld_view(U, own, mr, a0 + 32) : 0.0;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 5; q++) {
+    if (q < 4 || w == 0) {
+      const int y = w + 8 * q;
+      su[y * R3LU + lane] = uv[q];
+      if (lane == 0) su[y * R3LU + 32] = ux[q];
+    }
+  }
+  __syncthreads();
+  // defects: (i, j) order of stencil.py:82-87 whatever the orientation
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const int y = w + 8 * q;
+    if ((q == 3 && y >= R3D) || lane >= R3D) continue;
+    double dv = 0.0;
+    if (!GEN || (m0 + 1 + y < nM && a0 + 1 + lane < nA)) {
+      const int o = (y + 1) * R3LU + (lane + 1);
+      const double c = su[o], uu = su[o - R3LU], dd = su[o + R3LU], ll = su[o - 1], rr = su[o + 1];
+      // i neighbours: rows in N, columns in T
+      const double im = T ? ll : uu, ip = T ? rr : dd, jm = T ? uu : ll, jp = T ? dd : rr;
+      const double Wi = T ? cLo : rLo[q], Ei = T ? cHi : rHi[q];
+      const double Sj = T ? rLo[q] : cLo, Nj = T ? rHi[q] : cHi;
+      const double Cc = -__dadd_rn(__dadd_rn(__dadd_rn(Wi, Ei), Sj), Nj);
+      double acc = __dmul_rn(Wi, im);
+      acc = __dadd_rn(acc, __dmul_rn(Ei, ip));
+      acc = __dadd_rn(acc, __dmul_rn(Sj, jm));
+      acc = __dadd_rn(acc, __dmul_rn(Nj, jp));
+      dv = __dadd_rn(-__dadd_rn(acc, __dmul_rn(Cc, c)), fv[q]);
+    }
+    sd[y * R3LD + lane] = dv;
+  }
+  __syncthreads();
+  // coarse points, lanes along the coarse owner's contiguous axis
+  const int cown = box_owner(FC, I0, J0, R3C, R3C);
+  const int cpt = threadIdx.x;
+  if (cpt >= R3C * R3C) return;
+  const int p = cpt / R3C, qq = cpt - p * R3C;
+  const int ca = cown == 1 ? qq : p, cb = cown == 1 ? p : qq;  // I offset, J offset
+  const int I = I0 + ca, J = J0 + cb;
+  if ((GEN && (I >= nxc || J >= nyc)) || !in_groups(csel, nxc, nyc, I, J)) return;
+  const int a = 2 * ca + 1, b = 2 * cb + 1;  // fine (i, j) offsets in the defect tile
+  const int o = T ? b * R3LD + a : a * R3LD + b;
+  constexpr int di = T ? 1 : R3LD, dj = T ? R3LD : 1;
+  const double ctr = sd[o];
+  const double edges = __dadd_rn(__dadd_rn(__dadd_rn(sd[o - di], sd[o + di]), sd[o - dj]),
+                                 sd[o + dj]);
+  double v;
+  if (!full) {
+    v = __dadd_rn(__dmul_rn(0.5, ctr), __dmul_rn(0.125, edges));
+  } else {
+    const double diags = __dadd_rn(
+        __dadd_rn(__dadd_rn(sd[o - di - dj], sd[o + di - dj]), sd[o - di + dj]), sd[o + di + dj]);
+    v = __dadd_rn(__dadd_rn(__dmul_rn(0.25, ctr), __dmul_rn(0.125, edges)),
+                  __dmul_rn(0.0625, diags));
+  }
+  if (cown == 1) FC.t[FC.off_t(I, J)] = v;
+  else if (cown == 0) FC.n[FC.off_n(I, J)] = v;
+  else *FC.at(I, J) = v;
+  if (zero_uc) {
+    if (cown == 1) UC.t[UC.off_t(I, J)] = 0.0;
+    else if (cown == 0) UC.n[UC.off_n(I, J)] = 0.0;
+    else *UC.at(I, J) = 0.0;
+  }
+}
+
+// ---- fused residual + restriction, second layout: 15 x 15 coarse points per
+// CTA (31 x 31 fine defects, a 33 x 33 u box), warps along the tile's rows and
+// lanes along its columns in the owner buffer's orientation, every index a
+// compile-time offset from one per-thread base (restrict2_kernel spends most
+// of its issue slots on per-element index division).  Same arithmetic, bit
+// for bit.
+__global__ void __launch_bounds__(256, 4) restrict3_kernel(GridArgs g, int full, FieldView U,
+                                                        FieldView F, FieldView FC, FieldView UC,
+                                                        int zero_uc, GroupSel2 csel) {
+  __shared__ double su[R3U * R3LU];
+  __shared__ double sd[R3D * R3LD];
+  const int nxc = g.nx / 2, nyc = g.ny / 2;
+  const int I0 = 1 + blockIdx.y * R3C, J0 = 1 + blockIdx.x * R3C;
+  pdl_trigger();
+  if (!box_in_groups(csel, nxc, nyc, I0, J0, R3C, R3C)) {
+    pdl_wait();
+    return;
+  }
+  const int ui0 = 2 * I0 - 2, uj0 = 2 * J0 - 2;
+  const int own = box_owner(U, ui0, uj0, R3U, R3U);
+  const bool inner = own >= 0 && ui0 + R3U - 1 <= g.nx && uj0 + R3U - 1 <= g.ny;
+  if (inner && own == 0)
+    restrict3_body<0>(g, full, U, F, FC, UC, zero_uc, csel, own, I0, J0, su, sd);
+  else if (inner)
+    restrict3_body<1>(g, full, U, F, FC, UC, zero_uc, csel, own, I0, J0, su, sd);
+  else
+    restrict3_body<2>(g, full, U, F, FC, UC, zero_uc, csel, own, I0, J0, su, sd);
 }
 
 // ---- fused prolongation + correction: 32 x 32 fine points per CTA --------
@@ -651,6 +816,17 @@ cudaError_t launch_restrict2(const GridArgs& g, int full, const FieldView& U, co
                              int cg0, int cg1) {
   const int nxc = g.nx / 2, nyc = g.ny / 2;
   if (nxc < 2 || nyc < 2) return cudaSuccess;
+  static int v2 = -1;
+  if (v2 < 0) {
+    const char* e = std::getenv("TMG_RESTRICT");
+    v2 = e && std::string(e) == "v2";
+  }
+  if (!v2) {  // restrict3_kernel (same arithmetic, 2D thread mapping)
+    dim3 grid3((nyc - 1 + R3C - 1) / R3C, (nxc - 1 + R3C - 1) / R3C);
+    TMG_COUNT(1);
+    return launch_pdl(restrict3_kernel, grid3, dim3(256), 0, s, g, full, U, F, FC,
+                      UC ? *UC : FC, UC ? 1 : 0, GroupSel2{scheme, cg0, cg1});
+  }
   dim3 grid((nyc - 1 + RC - 1) / RC, (nxc - 1 + RC - 1) / RC);
   TMG_COUNT(1);
   static bool attr = false;
