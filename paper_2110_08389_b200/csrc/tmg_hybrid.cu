@@ -13,6 +13,7 @@
 #include <cstring>
 
 #include "tmg_kernels.h"
+#include "tmg_transfer_dev.cuh"
 
 namespace tmg {
 
@@ -258,35 +259,14 @@ __global__ void __launch_bounds__(256) from_hybrid_kernel(FieldView V, double* _
 __global__ void hdense_rhs_kernel(GridArgs g, FieldView U, FieldView F, double* __restrict__ rhs) {
   pdl_trigger();
   pdl_wait();
-  const int mi = g.nx - 1, n = mi * (g.ny - 1);
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const int i = k % mi + 1, j = k / mi + 1;
-    const double bw = i == 1 ? *U.at(i - 1, j) : 0.0, be = i == g.nx - 1 ? *U.at(i + 1, j) : 0.0;
-    const double bs = j == 1 ? *U.at(i, j - 1) : 0.0, bn = j == g.ny - 1 ? *U.at(i, j + 1) : 0.0;
-    double acc = __dmul_rn(g.W[i], bw);
-    acc = __dadd_rn(acc, __dmul_rn(g.E[i], be));
-    acc = __dadd_rn(acc, __dmul_rn(g.S[j], bs));
-    acc = __dadd_rn(acc, __dmul_rn(g.N[j], bn));
-    rhs[k] = __dadd_rn(*F.at(i, j), -acc);
-  }
+  dense_rhs(g, U, F, rhs, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
 __global__ void hdense_apply_kernel(GridArgs g, const double* __restrict__ Ainv,
                                     const double* __restrict__ rhs, FieldView U) {
   pdl_trigger();
   pdl_wait();
-  const int mi = g.nx - 1, n = mi * (g.ny - 1);
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= n) return;
-  if (n == 1) {
-    if (lane == 0) *U.at(1, 1) = rhs[0] / Ainv[0];
-    return;
-  }
-  double acc = 0.0;
-  for (int c = lane; c < n; c += 32) acc += Ainv[(size_t)warp * n + c] * rhs[c];
-#pragma unroll
-  for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
-  if (lane == 0) *U.at(warp % mi + 1, warp / mi + 1) = acc;
+  dense_apply(g, Ainv, rhs, U, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31);
 }
 
 }  // namespace

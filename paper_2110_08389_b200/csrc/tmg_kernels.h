@@ -93,6 +93,42 @@ struct GridArgs {
   const double* N;
 };
 
+// Persistent coarse tail (tmg_sweep.cu tail_kernel): the levels of a V-cycle
+// below a size bound (mgcycle.py:89-104 from that level down and back up)
+// run as ONE cooperative launch executing a list of ops; a grid barrier
+// separates ops whose outputs feed the next (colour stages, transfers, the
+// direct solve), instead of one graph node per stage.
+enum TailOpType {
+  TAIL_SWEEP = 0,        // the bins of one launch class of a colour stage
+  TAIL_RESTRICT = 1,     // residual + restriction (+ zero coarse guess), 15 x 15 coarse tiles
+  TAIL_PROLONG = 2,      // prolongation + correction, 32 x 32 fine tiles
+  TAIL_DENSE_RHS = 3,    // coarsest level: right-hand side of the direct solve
+  TAIL_DENSE_APPLY = 4,  // coarsest level: u = Ainv rhs, one warp per row
+};
+struct TailOp {
+  int type;
+  int barrier;  // 1: grid barrier after this op
+  int q;        // sweep: points per thread chunk
+  int nitems;   // bins / tiles / rows
+  int gx;       // tiles along the fast grid axis (transfers)
+  int base;     // CTA rotation (ops sharing one barrier interval spread over the grid)
+  int full;     // restriction weighting
+  const ChunkD* chunks;
+  const BinD* bins;
+  const HubD* hubs;
+  SweepArgs sa;
+  GridArgs g;           // the (fine) level's grid
+  FieldView U, F;       // the level's u, f
+  FieldView CF, CU;     // restriction: coarse f, u; prolongation: CU = coarse u
+  const double* ainv;   // dense solve
+  double* work;
+};
+// Dynamic shared memory and kernel attributes of the tail kernel for chunk
+// sizes up to qmax; *max_ctas = co-resident CTAs (0: cannot run).
+cudaError_t tail_prepare(int qmax, size_t* smem, int* max_ctas);
+cudaError_t launch_tail(const TailOp* ops, int nops, int ctas, size_t smem, unsigned* bar,
+                        cudaStream_t s);
+
 // out = L u on the interior (0 on the boundary) if negate == 0, or
 // out = f - L u (defect) if f != nullptr.  stencil.py:76-96.
 cudaError_t launch_apply(const GridArgs& g, const double* u, const double* f, double* out,

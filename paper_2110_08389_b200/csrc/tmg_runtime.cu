@@ -106,6 +106,14 @@ struct tmg_hier {
   SolveDev* d_solve = nullptr;  // device-driven solve loop state (solve_graph)
   int solve_cap = 0;            // cycles d_solve has room for
   std::map<std::tuple<int, int, int, int>, std::pair<cudaGraphExec_t, int>> solve_graphs;
+  // persistent coarse-tail programs per (kind, full, nu1, nu2, first level)
+  struct TailProg {
+    TailOp* d_ops = nullptr;
+    int nops = 0, ctas = 0, level = 0;
+    size_t smem = 0;
+  };
+  std::map<std::tuple<int, int, int, int, int>, TailProg> tails;
+  unsigned* d_tail_bar = nullptr;  // grid barrier state of the tail kernel
 };
 
 namespace {
@@ -335,6 +343,8 @@ int ensure_fields(tmg_hier* h, int mode) {
   h->graphs.clear();
   for (auto& kv : h->solve_graphs) cudaGraphExecDestroy(kv.second.first);
   h->solve_graphs.clear();
+  for (auto& kv : h->tails) cudaFree(kv.second.d_ops);
+  h->tails.clear();
   h->bytes = 0;
   const int L = (int)h->lv.size();
   h->U.assign(L, FieldView{});
@@ -369,12 +379,173 @@ int zero_field(const FieldView& v, cudaStream_t s) {
   return TMG_OK;
 }
 
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
+// smoothing schemes one sweep of `kind` runs (sweep_kind)
+std::vector<int> sub_schemes(int kind) {
+  if (kind == TMG_ZEBRA_ALT) return {TMG_ZEBRA_X, TMG_ZEBRA_Y};
+  if (kind == TMG_TWEED_WIRE_ALT) return {TMG_TWEED, TMG_WIREFRAME};
+  return {kind};
+}
+
+// First level of the persistent coarse tail (lv.size(): none): the levels
+// from there down are at most TMG_TAIL_NMAX (default 1024) points per axis,
+// their colour stages are single-CTA block classes (no leg kernel, no
+// clusters, no point scheme), and each restricts onto a grid with interior.
+// Opt-in (TMG_TAIL=1): measured slower than one PDL graph node per stage
+// (coarse tail), kept as a bit-identical alternative.
+int tail_start(tmg_hier* h, int kind, int l0) {
+  const int L = (int)h->lv.size();
+  if (env_int("TMG_TAIL", 0) == 0 || transfer_v1() || L < 2) return L;
+  const int nmax = env_int("TMG_TAIL_NMAX", 1024);
+  int lt = L;
+  for (int l = L - 2; l >= l0; l--) {
+    tmg_level* lv = h->lv[l];
+    if (std::max(lv->nx, lv->ny) > nmax || lv->nx / 2 < 2 || lv->ny / 2 < 2) break;
+    bool ok = true;
+    for (int sc : sub_schemes(kind)) {
+      Plan* p = nullptr;
+      if (get_plan(lv, sc, h->mode, &p)) return L;
+      if (p->lp || p->point_scheme) ok = false;
+      for (const LaunchClass& c : p->classes)
+        if (c.nbins && (c.cs != 1 || c.xcta)) ok = false;
+    }
+    if (!ok) break;
+    lt = l;
+  }
+  return lt;
+}
+
+// Build (once, outside any stream capture) the op list of the tail entered
+// at level >= l0; vcycle_launches uses it when present.
+int prepare_tail(tmg_hier* h, int kind, int full, int nu1, int nu2, int l0) {
+  const int L = (int)h->lv.size();
+  const int lt = tail_start(h, kind, l0);
+  auto key = std::make_tuple(kind, full, nu1, nu2, l0);
+  if (lt >= L - 1 || h->tails.count(key)) return TMG_OK;
+  std::vector<TailOp> ops;
+  int maxitems = 1, qmax = 1;
+  auto sweeps = [&](int l) -> int {
+    tmg_level* lv = h->lv[l];
+    for (int sc : sub_schemes(kind)) {
+      Plan* p = nullptr;
+      int st = get_plan(lv, sc, h->mode, &p);
+      if (st) return st;
+      const SweepArgs a = sweep_args(lv, p, h->U[l], h->F[l]);
+      for (int red = 1; red >= 0; red--) {
+        int base = 0;
+        for (const LaunchClass& c : p->classes) {
+          if (c.red != red || c.nbins == 0) continue;
+          TailOp o{};
+          o.type = TAIL_SWEEP;
+          o.q = c.q;
+          o.nitems = c.nbins;
+          o.base = base;
+          o.chunks = c.chunks;
+          o.bins = c.bins;
+          o.hubs = c.hubs;
+          o.sa = a;
+          base += c.nbins;
+          qmax = std::max(qmax, c.q);
+          ops.push_back(o);
+        }
+        if (base) ops.back().barrier = 1;
+        maxitems = std::max(maxitems, base);
+      }
+    }
+    return TMG_OK;
+  };
+  for (int l = lt; l < L - 1; l++) {
+    for (int k = 0; k < nu1; k++) {
+      int st = sweeps(l);
+      if (st) return st;
+    }
+    tmg_level* lv = h->lv[l];
+    const int nxc = lv->nx / 2, nyc = lv->ny / 2;
+    TailOp o{};
+    o.type = TAIL_RESTRICT;
+    o.barrier = 1;
+    o.gx = (nyc - 1 + 14) / 15;
+    o.nitems = o.gx * ((nxc - 1 + 14) / 15);
+    o.full = full;
+    o.g = lv->grid();
+    o.U = h->U[l];
+    o.F = h->F[l];
+    o.CF = h->F[l + 1];
+    o.CU = h->U[l + 1];
+    ops.push_back(o);
+    maxitems = std::max(maxitems, o.nitems);
+  }
+  {
+    tmg_level* lc = h->lv[L - 1];
+    int st = factor_coarse(lc);
+    if (st) return st;
+    const int n = (lc->nx - 1) * (lc->ny - 1);
+    if (n > 0) {
+      TailOp o{};
+      o.type = TAIL_DENSE_RHS;
+      o.barrier = 1;
+      o.nitems = n;
+      o.g = lc->grid();
+      o.U = h->U[L - 1];
+      o.F = h->F[L - 1];
+      o.ainv = lc->d_ainv;
+      o.work = lc->d_work;
+      ops.push_back(o);
+      o.type = TAIL_DENSE_APPLY;
+      ops.push_back(o);
+      maxitems = std::max(maxitems, (n + kThreads / 32 - 1) / (kThreads / 32));
+    }
+  }
+  for (int l = L - 2; l >= lt; l--) {
+    tmg_level* lv = h->lv[l];
+    TailOp o{};
+    o.type = TAIL_PROLONG;
+    o.barrier = 1;
+    o.gx = (lv->ny - 1 + 31) / 32;
+    o.nitems = o.gx * ((lv->nx - 1 + 31) / 32);
+    o.g = lv->grid();
+    o.U = h->U[l];
+    o.CU = h->U[l + 1];
+    ops.push_back(o);
+    maxitems = std::max(maxitems, o.nitems);
+    for (int k = 0; k < nu2; k++) {
+      int st = sweeps(l);
+      if (st) return st;
+    }
+  }
+  ops.back().barrier = 0;  // the kernel's end orders the last op
+  tmg_hier::TailProg tp;
+  int max_ctas = 0;
+  TMG_CUDA_TRY(tail_prepare(qmax, &tp.smem, &max_ctas));
+  if (max_ctas < 1) return TMG_OK;  // cannot run: the per-stage path stays
+  tp.ctas = std::min(std::min(max_ctas, maxitems), std::max(1, env_int("TMG_TAIL_CTAS", 1 << 20)));
+  tp.nops = (int)ops.size();
+  tp.level = lt;
+  if (!h->d_tail_bar) {
+    TMG_CUDA_TRY(cudaMalloc(&h->d_tail_bar, 2 * sizeof(unsigned)));
+    TMG_CUDA_TRY(cudaMemset(h->d_tail_bar, 0, 2 * sizeof(unsigned)));
+  }
+  TMG_CUDA_TRY(cudaMalloc(&tp.d_ops, ops.size() * sizeof(TailOp)));
+  TMG_CUDA_TRY(cudaMemcpy(tp.d_ops, ops.data(), ops.size() * sizeof(TailOp),
+                          cudaMemcpyHostToDevice));
+  h->tails.emplace(key, tp);
+  return TMG_OK;
+}
+
 // one V-cycle on the hierarchy's work fields (mgcycle.py:89-104), entered at
 // level l0 (0: the whole cycle; > 0: the replicated tail of a sharded cycle)
 int vcycle_launches(tmg_hier* h, int kind, int full, int nu1, int nu2, cudaStream_t s,
                     int l0 = 0) {
   const int L = (int)h->lv.size();
-  for (int l = l0; l < L - 1; l++) {  // down: smooth, residual + restriction, zero guess
+  // levels >= lt run inside one persistent tail launch (prepare_tail)
+  auto tit = h->tails.find(std::make_tuple(kind, full, nu1, nu2, l0));
+  const tmg_hier::TailProg* tp = tit == h->tails.end() ? nullptr : &tit->second;
+  const int lt = tp ? tp->level : L - 1;
+  for (int l = l0; l < lt; l++) {  // down: smooth, residual + restriction, zero guess
     tmg_level* lv = h->lv[l];
     for (int k = 0; k < nu1; k++) {
       int st = sweep_kind(lv, kind, 3, h->U[l], h->F[l], s);
@@ -389,7 +560,10 @@ int vcycle_launches(tmg_hier* h, int kind, int full, int nu1, int nu2, cudaStrea
       if (st) return st;
     }
   }
-  {  // coarsest level: direct solve (mgcycle.py:93-95)
+  if (tp) {
+    cudaError_t e = launch_tail(tp->d_ops, tp->nops, tp->ctas, tp->smem, h->d_tail_bar, s);
+    if (e != cudaSuccess) return cuda_fail(e, "coarse tail");
+  } else {  // coarsest level: direct solve (mgcycle.py:93-95)
     tmg_level* lc = h->lv[L - 1];
     int st = factor_coarse(lc);
     if (st) return st;
@@ -397,7 +571,7 @@ int vcycle_launches(tmg_hier* h, int kind, int full, int nu1, int nu2, cudaStrea
                                         lc->d_work, s);
     if (e != cudaSuccess) return cuda_fail(e, "coarse solve");
   }
-  for (int l = L - 2; l >= l0; l--) {  // up: prolongation + correction, smooth
+  for (int l = lt - 1; l >= l0; l--) {  // up: prolongation + correction, smooth
     tmg_level* lv = h->lv[l];
     cudaError_t e = launch_hprolong_correct(lv->nx, lv->ny, h->U[l + 1], h->U[l], s);
     if (e != cudaSuccess) return cuda_fail(e, "prolong_correct");
@@ -464,6 +638,7 @@ int session_cycles(tmg_hier* h, int kind, int full, int nu1, int nu2, int reps, 
   auto it = h->graphs.find(key);
   if (it == h->graphs.end()) {
     int st = prepare(h, kind);
+    if (!st) st = prepare_tail(h, kind, full & 1, nu1, nu2, 0);
     if (st) return st;
     cudaStream_t cs;
     TMG_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -743,6 +918,8 @@ int tmg_hier_destroy(tmg_hier* h) {
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.first);
   for (auto& kv : h->solve_graphs) cudaGraphExecDestroy(kv.second.first);
   cudaFree(h->d_solve);
+  for (auto& kv : h->tails) cudaFree(kv.second.d_ops);
+  cudaFree(h->d_tail_bar);
   for (double* p : h->blocks) cudaFree(p);
   delete h;
   return TMG_OK;
@@ -934,6 +1111,7 @@ int solve_graph(tmg_hier* h, int kind, int full, int nu1, int nu2, cudaGraphExec
     return TMG_OK;
   }
   int st = prepare(h, kind);
+  if (!st) st = prepare_tail(h, kind, full, nu1, nu2, 0);
   if (st) return st;
   if (h->lv.size() > 32) return fail(TMG_BADARG, "too many levels for the solve graph");
   ErrPtrs ep{};
@@ -1171,6 +1349,7 @@ int tmg_session_tail(tmg_hier* h, int level, int kind, int full, int nu1, int nu
     return fail(TMG_BADARG, "smoother kind does not match the loaded session's layout");
   return guarded([&]() -> int {
     int st2 = prepare(h, kind);
+    if (!st2) st2 = prepare_tail(h, kind, full, nu1, nu2, level);
     return st2 ? st2 : vcycle_launches(h, kind, full, nu1, nu2, (cudaStream_t)stream, level);
   });
 }

@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "tmg_kernels.h"
+#include "tmg_transfer_dev.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -181,7 +182,7 @@ struct Chunk {
 }  // namespace
 
 #ifdef TMG_PHASE_TIMING
-__device__ long long g_phase_t[8][1 << 16];
+__device__ long long g_phase_t[12][1 << 16];
 __device__ int g_phase_n;
 #define TMG_T(slot)                                                        \
   do {                                                                     \
@@ -340,6 +341,7 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
   Chunk c;
   c.unpack(mine, C, ld, a.ldt);
   pdl_wait();  // the field data of the previous kernel are complete from here on
+  TMG_T(7);
   const FieldView U{u, a.ut, a.nx, a.ny, a.mode};
   const FieldView F{const_cast<double*>(f), const_cast<double*>(a.ft), a.nx, a.ny, a.mode};
   const BinD bd_ = bins[bin];
@@ -357,6 +359,7 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
     if (!(hb.mask & 8u)) hub_num -= __ldg(a.N + hj) * *U.at(hi, hj + 1);
     hub_den = -(__ldg(a.W + hi) + __ldg(a.E + hi) + __ldg(a.S + hj) + __ldg(a.N + hj));
   }
+  TMG_T(8);
   const double xlv = c.n > 0 ? __ldg(c.xl + c.cidx) : 0.0;
   const double xhv = c.n > 0 ? __ldg(c.xh + c.cidx) : 0.0;
   const int lane = tid & 31, wbase = tid & ~31;
@@ -477,6 +480,7 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
   }
   }  // record-driven gather
   __syncwarp();
+  TMG_T(9);
   if (!(TMG_SKIP & 16) && c.n > 0) {  // chunk ends: neighbours outside the block from the link directions
     const int alo = c.da > 0 ? (c.axis ? DS : DW) : (c.axis ? DN : DE);  // toward k-1
     const int ahi = alo ^ 1;                                             // toward k+1
@@ -757,6 +761,124 @@ block_sweep_kernel(SweepArgs a, const ChunkD* __restrict__ chunks, const BinD* _
   if constexpr (CLUSTER) cluster_wait();
 }
 
+// ---- persistent coarse tail ------------------------------------------------
+// Grid barrier of the cooperative tail launch: bar[0] counts arrivals,
+// bar[1] is the generation the last arrival bumps (both return to their
+// start state's form after every barrier, so graph replays reuse them).
+__device__ __forceinline__ void tail_barrier(unsigned* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned gen;
+    asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    if (old == nblocks - 1) {
+      asm volatile("st.relaxed.gpu.u32 [%0], 0;" ::"l"(bar) : "memory");
+      asm volatile("red.release.gpu.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
+    } else {
+      unsigned g2;
+      do {
+        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(g2) : "l"(bar + 1) : "memory");
+      } while (g2 == gen);
+    }
+  }
+  __syncthreads();
+}
+
+// (not inlined: each op body keeps its own register allocation)
+template <int Q>
+__device__ __noinline__ void tail_bins(const TailOp* __restrict__ opp, int b0, double* smem) {
+  const TailOp& op = *opp;
+  const SweepArgs sa = op.sa;
+  for (int b = b0; b < op.nitems; b += gridDim.x) {
+    sweep_bin<false, false, Q>(sa, op.chunks, op.bins, op.hubs, 1, b, 0, smem);
+    __syncthreads();  // the next bin's gather overwrites the staged rows
+  }
+}
+
+__device__ __noinline__ void tail_restrict(const TailOp* __restrict__ opp, int b0, double* smem) {
+  const TailOp& op = *opp;
+  for (int t = b0; t < op.nitems; t += gridDim.x) {
+    const int by = t / op.gx, bx = t - by * op.gx;
+    restrict3_tile(op.g, op.full, op.U, op.F, op.CF, op.CU, 1, GroupSel2{0, 0, 0}, 1 + by * R3C,
+                   1 + bx * R3C, smem, smem + R3U * R3LU);
+    __syncthreads();
+  }
+}
+
+__device__ __noinline__ void tail_prolong(const TailOp* __restrict__ opp, int b0, double* smem) {
+  const TailOp& op = *opp;
+  for (int t = b0; t < op.nitems; t += gridDim.x) {
+    const int by = t / op.gx, bx = t - by * op.gx;
+    prolong2_tile(op.g.nx, op.g.ny, op.CU, op.U, GroupSel2{0, 0, 0}, 1 + by * NT, 1 + bx * NT,
+                  smem);
+    __syncthreads();
+  }
+}
+
+#ifdef TMG_TAIL_TIMING
+__device__ unsigned long long g_tail_t[2][4096];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
+// One CTA per SM at most; every CTA walks the whole op list.
+__global__ void __launch_bounds__(kThreads, 1)
+tail_kernel(const TailOp* __restrict__ ops, int nops, unsigned* bar) {
+  extern __shared__ double smem[];
+  const int G = gridDim.x;
+  for (int k = 0; k < nops; k++) {
+    const TailOp& op = ops[k];
+    int b0 = ((int)blockIdx.x - op.base) % G;
+    if (b0 < 0) b0 += G;
+#ifdef TMG_TAIL_TIMING
+    if (blockIdx.x == 0 && threadIdx.x == 0 && k < 4096) g_tail_t[0][k] = gtimer();
+#endif
+    switch (op.type) {
+      case TAIL_SWEEP:
+        switch (op.q) {
+          case 16: tail_bins<16>(ops + k, b0, smem); break;
+          case 8: tail_bins<8>(ops + k, b0, smem); break;
+          case 4: tail_bins<4>(ops + k, b0, smem); break;
+          case 2: tail_bins<2>(ops + k, b0, smem); break;
+          default: tail_bins<1>(ops + k, b0, smem); break;
+        }
+        break;
+      case TAIL_RESTRICT: tail_restrict(ops + k, b0, smem); break;
+      case TAIL_PROLONG: tail_prolong(ops + k, b0, smem); break;
+      case TAIL_DENSE_RHS:
+        dense_rhs(op.g, op.U, op.F, op.work, b0 * kThreads + threadIdx.x, G * kThreads);
+        break;
+      case TAIL_DENSE_APPLY:
+        for (int w = b0 * (kThreads / 32) + (threadIdx.x >> 5); w < op.nitems;
+             w += G * (kThreads / 32))
+          dense_apply(op.g, op.ainv, op.work, op.U, w, threadIdx.x & 31);
+        break;
+      default: break;
+    }
+#ifdef TMG_TAIL_TIMING
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0 && k < 4096) g_tail_t[1][k] = gtimer();
+#endif
+    if (op.barrier) tail_barrier(bar, G);
+  }
+}
+
+extern "C" int tmg_debug_tail_times(unsigned long long* out, int n) {
+#ifdef TMG_TAIL_TIMING
+  if (n > 4096) n = 4096;
+  cudaMemcpyFromSymbol(out, g_tail_t, sizeof(unsigned long long) * 2 * 4096);
+  return n;
+#else
+  (void)out;
+  (void)n;
+  return 0;
+#endif
+}
+
 // Point Gauss-Seidel colour stage for checkerboard (smoothers.py:65-75,
 // _ckernels.pyx:42-51): red = (i + j) even.
 // Rows i in [i0, i0 + gridDim.y) (a partial plan covers its sharding groups).
@@ -848,6 +970,27 @@ cudaError_t launch_class(const LaunchClass& lc, const SweepArgs& a, cudaStream_t
 
 // Average per-CTA cycles between the phase marks of the last launches
 // (debug builds with -DTMG_PHASE_TIMING; zeros otherwise).
+// gather sub-phases: descriptor load + unpack + PDL wait, hub preload, main
+// gather, chunk-end fix (same builds)
+extern "C" int tmg_debug_gather_cycles(double* out4) {
+  for (int k = 0; k < 4; k++) out4[k] = 0.0;
+#ifdef TMG_PHASE_TIMING
+  int n = 0;
+  cudaMemcpyFromSymbol(&n, g_phase_n, sizeof(int));
+  if (n <= 0) return 0;
+  std::vector<long long> t(12 * (size_t)(1 << 16));
+  cudaMemcpyFromSymbol(t.data(), g_phase_t, t.size() * sizeof(long long));
+  const int from[4] = {0, 7, 8, 9}, to[4] = {7, 8, 9, 1};
+  for (int b = 0; b < n; b++)
+    for (int k = 0; k < 4; k++)
+      out4[k] += (double)(t[(size_t)to[k] * (1 << 16) + b] - t[(size_t)from[k] * (1 << 16) + b]);
+  for (int k = 0; k < 4; k++) out4[k] /= n;
+  return n;
+#else
+  return 0;
+#endif
+}
+
 extern "C" int tmg_debug_phase_cycles(double* out6) {
   for (int k = 0; k < 6; k++) out6[k] = 0.0;
 #ifdef TMG_PHASE_TIMING
@@ -877,6 +1020,41 @@ cudaError_t init_sweep_kernels() {
     if (done == cudaSuccess) done = set_attrs<1>();
   }
   return done;
+}
+
+cudaError_t tail_prepare(int qmax, size_t* smem, int* max_ctas) {
+  size_t sm = sizeof(double) * (size_t)(R3U * R3LU + R3D * R3LD);
+  const size_t sw = qmax >= 16 ? sweep_smem<16>() : qmax >= 8 ? sweep_smem<8>()
+                  : qmax >= 4 ? sweep_smem<4>() : qmax >= 2 ? sweep_smem<2>() : sweep_smem<1>();
+  sm = std::max(sm, sw);
+  *smem = sm;
+  *max_ctas = 0;
+  cudaError_t e = cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sm);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0, dev = 0, sms = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tail_kernel, kThreads, sm);
+  if (e == cudaSuccess) e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
+  *max_ctas = per_sm * sms;
+  return cudaSuccess;
+}
+
+cudaError_t launch_tail(const TailOp* ops, int nops, int ctas, size_t smem, unsigned* bar,
+                        cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (grid barriers)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TMG_COUNT(1);
+  return cudaLaunchKernelEx(&cfg, tail_kernel, ops, nops, bar);
 }
 
 cudaError_t launch_colour(const Plan& P, int red, const SweepArgs& a, cudaStream_t stream) {
