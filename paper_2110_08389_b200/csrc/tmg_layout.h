@@ -19,13 +19,15 @@ namespace tmg {
 
 enum LayoutMode : int { LM_NATURAL = 0, LM_TWEED = 1, LM_WIRE = 2, LM_XLINES = 3 };
 
+// Branch-free (bitwise & / |, no short circuit): the device code computes a
+// buffer address per point without control flow, so independent loads
+// through FieldView::at issue back to back.
 __host__ __device__ inline bool owns_t(int mode, int nx, int ny, int i, int j) {
-  if (mode == LM_NATURAL || i <= 0 || j <= 0 || i >= nx || j >= ny) return false;
   const int ip = i < nx - i ? i : nx - i;
   const int jp = j < ny - j ? j : ny - j;
-  if (mode == LM_TWEED) return ip < jp;
-  if (mode == LM_WIRE) return jp < ip;
-  return true;
+  const bool interior = (i > 0) & (j > 0) & (i < nx) & (j < ny);
+  return interior & (((mode == LM_TWEED) & (ip < jp)) | ((mode == LM_WIRE) & (jp < ip)) |
+                     (mode == LM_XLINES));
 }
 
 // layout a smoother kind runs fastest on

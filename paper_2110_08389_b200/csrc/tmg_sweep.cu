@@ -337,31 +337,116 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
 
   TMG_T(0);
   if (!TMG_PDL_LATE) pdl_trigger();
+  // static plan data and couplings first: under PDL these loads overlap the
+  // previous kernel, and none of them waits on another after the wait
   const ChunkD mine = chunks[((size_t)bin * cs_size + rank) * T + tid];
+  const BinD bd_ = bins[bin];
   Chunk c;
   c.unpack(mine, C, ld, a.ldt);
+  const bool has_hub = !(TMG_SKIP & 4) && c.own >= 0;
+  HubD hb0{};
+  double hW = 0.0, hE = 0.0, hS = 0.0, hN = 0.0;
+  if (has_hub) {
+    const HubD& hb = hb0;
+    hb0 = hubs[bd_.hub0 + c.own];
+    hW = __ldg(a.W + hb.i);
+    hE = __ldg(a.E + hb.i);
+    hS = __ldg(a.S + hb.j);
+    hN = __ldg(a.N + hb.j);
+  }
+
+  const double xlv = c.n > 0 ? __ldg(c.xl + c.cidx) : 0.0;
+  const double xhv = c.n > 0 ? __ldg(c.xh + c.cidx) : 0.0;
   pdl_wait();  // the field data of the previous kernel are complete from here on
   TMG_T(7);
   const FieldView U{u, a.ut, a.nx, a.ny, a.mode};
   const FieldView F{const_cast<double*>(f), const_cast<double*>(a.ft), a.nx, a.ny, a.mode};
-  const BinD bd_ = bins[bin];
   // frozen part of this thread's hub row (its out-of-block neighbours are
   // never written during this colour stage), loaded now so that the loads
   // overlap the gather instead of sitting on the hub step's critical path
+  // Every load below is unconditional (clamped to a valid point when unused)
+  // and masked through its coupling, so that all of them are in flight at
+  // once: under per-load branches they issued one round trip at a time.
   double hub_num = 0.0, hub_den = 1.0;
-  if (!(TMG_SKIP & 4) && c.own >= 0) {
-    const HubD hb = hubs[bd_.hub0 + c.own];
-    const int hi = hb.i, hj = hb.j;
-    hub_num = (hb.tbuf ? a.ft : f)[hb.off];
-    if (!(hb.mask & 1u)) hub_num -= __ldg(a.W + hi) * *U.at(hi - 1, hj);
-    if (!(hb.mask & 2u)) hub_num -= __ldg(a.E + hi) * *U.at(hi + 1, hj);
-    if (!(hb.mask & 4u)) hub_num -= __ldg(a.S + hj) * *U.at(hi, hj - 1);
-    if (!(hb.mask & 8u)) hub_num -= __ldg(a.N + hj) * *U.at(hi, hj + 1);
-    hub_den = -(__ldg(a.W + hi) + __ldg(a.E + hi) + __ldg(a.S + hj) + __ldg(a.N + hj));
+  {
+    const HubD& hb = hb0;
+    const int hi = has_hub ? hb.i : 1, hj = has_hub ? hb.j : 1;
+    const double* pf = has_hub ? (hb.tbuf ? a.ft : f) + hb.off : f;
+    const double h0 = *pf, h1 = *U.at(hi - 1, hj), h2 = *U.at(hi + 1, hj);
+    const double h3 = *U.at(hi, hj - 1), h4 = *U.at(hi, hj + 1);
+    if (has_hub) {
+      hub_num = h0;
+      hub_num -= ((hb.mask & 1u) ? 0.0 : hW) * h1;
+      hub_num -= ((hb.mask & 2u) ? 0.0 : hE) * h2;
+      hub_num -= ((hb.mask & 4u) ? 0.0 : hS) * h3;
+      hub_num -= ((hb.mask & 8u) ? 0.0 : hN) * h4;
+      hub_den = -(hW + hE + hS + hN);
+    }
   }
+  // chunk ends: neighbours outside the block from the link directions.  The
+  // gather's value is already exact for an end whose in-block neighbours are
+  // the two along neighbours and whose cross neighbours live in the chunk's
+  // buffer (most chunk ends); the others (leg tips, corners, points next to
+  // an ownership boundary) are recomputed here, their loads in flight with
+  // the gather's, and written over the gathered value after it.
+  // (small chunks, latency-bound levels: issued before the gather; q >= 8,
+  // throughput-bound levels: after it, keeping the gather's registers free)
+  double rend[2] = {0.0, 0.0};
+  bool fixe[2] = {false, false};
+  auto chunk_ends = [&]() {
+    const int alo = c.da > 0 ? (c.axis ? DS : DW) : (c.axis ? DN : DE);  // toward k-1
+    const int ahi = alo ^ 1;                                             // toward k+1
+    int ei[2], ej[2];
+    unsigned skip[2];
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+      const int k = e ? max(c.n - 1, 0) : 0;
+      const int dp = k == 0 ? c.dfirst : alo;
+      const int dn = k == c.n - 1 ? c.dlast : ahi;
+      int i, j;
+      c.ij(k, i, j);
+      const bool live = !(TMG_SKIP & 16) && c.n > 0 && (e == 0 || c.n > 1);
+      i = live ? i : 1;
+      j = live ? j : 1;
+      bool fix = dp != alo || dn != ahi;
+      if (a.mode != LM_NATURAL) {
+        const int i1 = c.axis ? i - 1 : i, j1 = c.axis ? j : j - 1;
+        const int i2 = c.axis ? i + 1 : i, j2 = c.axis ? j : j + 1;
+        fix |= (owns_t(a.mode, a.nx, a.ny, i1, j1) != (c.tb != 0)) & (i1 > 0) & (j1 > 0) |
+               (owns_t(a.mode, a.nx, a.ny, i2, j2) != (c.tb != 0)) & (i2 < a.nx) & (j2 < a.ny);
+      }
+      ei[e] = i;
+      ej[e] = j;
+      skip[e] = (dp < 4 ? 1u << dp : 0u) | (dn < 4 ? 1u << dn : 0u);
+      fixe[e] = live && fix;
+    }
+    // all loads of both ends first, then the arithmetic
+    double v[2][9];
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+      const int i = ei[e], j = ej[e];
+      v[e][0] = *F.at(i, j);
+      v[e][1] = *U.at(i - 1, j);
+      v[e][2] = *U.at(i + 1, j);
+      v[e][3] = *U.at(i, j - 1);
+      v[e][4] = *U.at(i, j + 1);
+      v[e][5] = __ldg(a.W + i);
+      v[e][6] = __ldg(a.E + i);
+      v[e][7] = __ldg(a.S + j);
+      v[e][8] = __ldg(a.N + j);
+    }
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+      double r = v[e][0];
+      r -= ((skip[e] & 1u) ? 0.0 : v[e][5]) * v[e][1];
+      r -= ((skip[e] & 2u) ? 0.0 : v[e][6]) * v[e][2];
+      r -= ((skip[e] & 4u) ? 0.0 : v[e][7]) * v[e][3];
+      r -= ((skip[e] & 8u) ? 0.0 : v[e][8]) * v[e][4];
+      rend[e] = r;
+    }
+  };
+  if constexpr (Q <= 4) chunk_ends();
   TMG_T(8);
-  const double xlv = c.n > 0 ? __ldg(c.xl + c.cidx) : 0.0;
-  const double xhv = c.n > 0 ? __ldg(c.xh + c.cidx) : 0.0;
   const int lane = tid & 31, wbase = tid & ~31;
   constexpr int PER = 32 / Q;  // chunks covered by one warp-wide pass
   constexpr int BATCH = Q < TMG_BATCH ? Q : TMG_BATCH;
@@ -481,38 +566,9 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
   }  // record-driven gather
   __syncwarp();
   TMG_T(9);
-  if (!(TMG_SKIP & 16) && c.n > 0) {  // chunk ends: neighbours outside the block from the link directions
-    const int alo = c.da > 0 ? (c.axis ? DS : DW) : (c.axis ? DN : DE);  // toward k-1
-    const int ahi = alo ^ 1;                                             // toward k+1
-#pragma unroll
-    for (int e = 0; e < 2; e++) {
-      const int k = e ? c.n - 1 : 0;
-      if (e && c.n == 1) break;
-      const int dp = k == 0 ? c.dfirst : alo;
-      const int dn = k == c.n - 1 ? c.dlast : ahi;
-      int i, j;
-      c.ij(k, i, j);
-      // The gather's value is already exact for an end whose in-block
-      // neighbours are the two along neighbours and whose cross neighbours
-      // live in the chunk's buffer (most chunk ends); recompute the others
-      // (leg tips, corners, points next to an ownership boundary).
-      bool fix = dp != alo || dn != ahi;
-      if (!fix && a.mode != LM_NATURAL) {
-        const int i1 = c.axis ? i - 1 : i, j1 = c.axis ? j : j - 1;
-        const int i2 = c.axis ? i + 1 : i, j2 = c.axis ? j : j + 1;
-        fix = owns_t(a.mode, a.nx, a.ny, i1, j1) != (c.tb != 0) && i1 > 0 && j1 > 0 ||
-              owns_t(a.mode, a.nx, a.ny, i2, j2) != (c.tb != 0) && i2 < a.nx && j2 < a.ny;
-      }
-      if (!fix) continue;
-      const unsigned skip = (dp < 4 ? 1u << dp : 0u) | (dn < 4 ? 1u << dn : 0u);
-      double r = *F.at(i, j);
-      if (!(skip & 1u)) r -= __ldg(a.W + i) * *U.at(i - 1, j);
-      if (!(skip & 2u)) r -= __ldg(a.E + i) * *U.at(i + 1, j);
-      if (!(skip & 4u)) r -= __ldg(a.S + j) * *U.at(i, j - 1);
-      if (!(skip & 8u)) r -= __ldg(a.N + j) * *U.at(i, j + 1);
-      R[sw<Q>(tid, k)] = r;
-    }
-  }
+  if constexpr (Q > 4) chunk_ends();
+  if (fixe[0]) R[sw<Q>(tid, 0)] = rend[0];
+  if (fixe[1]) R[sw<Q>(tid, c.n - 1)] = rend[1];
   __syncwarp();
   TMG_T(1);
 
@@ -673,17 +729,28 @@ __device__ __forceinline__ void sweep_bin(const SweepArgs& a, const ChunkD* __re
   bin_sync<CLUSTER>();
 
   // hub rows
-  if (!(TMG_SKIP & 4) && c.own >= 0) {
-    const HubD hb = hubs[bd_.hub0 + c.own];
-    const int hi = hb.i, hj = hb.j;
+  if (has_hub) {
+    // q >= 8: the descriptor again (L1) rather than 6 registers held throughout
+    const HubD hb = Q <= 4 ? hb0 : hubs[bd_.hub0 + c.own];
     const int o = hb.off;
     double num = hub_num, den = hub_den;
-    for (int q = 0; q < hb.nadj; q++) {
+    // couplings to the adjacent chunk ends, all four loads in flight at once
+    double hcf[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int d = hb.adj_d[q];
+      const double* p = d == DW ? a.W + hb.i : d == DE ? a.E + hb.i : d == DS ? a.S + hb.j
+                                                                              : a.N + hb.j;
+      hcf[q] = __ldg(p);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      if (q >= hb.nadj) break;
       const int ta = hb.adj_t[q];
       SWEEP_CHECK(ta >= 0 && ta < T * cs_size && hb.off >= 0 &&
                       hb.off < (a.nx + 1) * (a.ny + 1),
                   "hub coupling");
-      const double cf = C.dir(hb.adj_d[q], hi, hj);
+      const double cf = hcf[q];
       num -= cf * remote<CLUSTER>(sD, ta / T)[ta % T];
       den -= cf * remote<CLUSTER>(sH, ta / T)[ta % T];
     }
