@@ -209,11 +209,22 @@ struct ChunkOut {
   int phi;            // smallest high word of |pivot| (vanishing-pivot check)
 };
 
+#ifndef TMG_LEGK_CPRE
+#define TMG_LEGK_CPRE 0  // > 0: couplings of the chunk's first points loaded during the stage wait (measured slower: spills)
+#endif
+struct CoefSrc {
+  const double2* __restrict__ p;  // chunk-permuted table, point k at p[32 k]
+  double2 pre[TMG_LEGK_CPRE > 0 ? TMG_LEGK_CPRE : 1];
+};
+__device__ __forceinline__ double2 coef_at(const CoefSrc& c, int k) {
+  return k < TMG_LEGK_CPRE ? c.pre[k < TMG_LEGK_CPRE ? k : 0] : __ldg(c.p + 32 * k);
+}
+
 template <int DIR>
 __device__ __forceinline__ void chunk_forward(double* __restrict__ pF,
                                               const double* __restrict__ pL,
                                               const double* __restrict__ pH,
-                                              const double2* __restrict__ pc, double clo,
+                                              const CoefSrc& pc, double clo,
                                               double chi, bool first, int wallfix, double uwall,
                                               double uwall2,
                                               double (&lam)[LQ - 1], double (&cg_)[LQ - 1],
@@ -224,7 +235,7 @@ __device__ __forceinline__ void chunk_forward(double* __restrict__ pF,
 #pragma unroll
   for (int k = 0; k < LQ - 1; k++) {
     const double r = fma(-chi, pH[DIR * k], fma(-clo, pL[DIR * k], pF[DIR * k]));
-    const double2 ac = __ldg(pc + 32 * k);
+    const double2 ac = coef_at(pc, k);
     const double bb = -(ac.x + ac.y + csum);
     double bp;
     if (k == 0) {
@@ -254,7 +265,7 @@ __device__ __forceinline__ void chunk_forward(double* __restrict__ pF,
     const double uh = wallfix == 1 ? pH[DIR * k] : wallfix == 2 ? uwall : uwall2;
     r = pF[DIR * k] - clo * ul - chi * uh;
   }
-  const double2 ac = __ldg(pc + 32 * k);
+  const double2 ac = coef_at(pc, k);
   o.a_end = ac.x;
   o.c_end = ac.y;
   o.r_end = r;
@@ -462,6 +473,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
       uwall = a.un[(size_t)(g.p0 + g.sx * (m - 1)) * ld + (g.bj - g.sy)];
     }
 
+    CoefSrc cpre;  // first points' couplings in flight during the stage wait
+    cpre.p = a.coef + cofs;
+#pragma unroll
+    for (int k = 0; k < TMG_LEGK_CPRE; k++)
+      cpre.pre[k] = act ? __ldg(cpre.p + 32 * k) : make_double2(0.0, 0.0);
     LEGK_MARK(0);
     if (item >= 0) {
       mbar_wait(bar, (unsigned)ph);
@@ -491,10 +507,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     if (act) {
       if (first) pF[g.dir * pad] -= tip_a * tip_u;  // only this thread reads the tip's f
       if (g.dir > 0)
-        chunk_forward<1>(pF, Ls + bL + e0, Hs + bH + e0, a.coef + cofs, clo, chi,
+        chunk_forward<1>(pF, Ls + bL + e0, Hs + bH + e0, cpre, clo, chi,
                          first, wallfix, uwall, uwall2, lam, ga, co);
       else
-        chunk_forward<-1>(pF, Ls + bL - e0, Hs + bH - e0, a.coef + cofs, clo,
+        chunk_forward<-1>(pF, Ls + bL - e0, Hs + bH - e0, cpre, clo,
                           chi, first, wallfix, uwall, uwall2, lam, ga, co);
     }
     phi = min(phi, co.phi);
