@@ -301,6 +301,133 @@ __device__ __forceinline__ void chunk_back(double* __restrict__ pF, double* __re
   o.gu = G_;
 }
 
+// Twisted (two-ended) chunk elimination, TMG_LEGK_TWIST: the same exact
+// solve of the chunk's 16 interior rows as chunk_forward / chunk_back, but
+// eliminated from both ends at once so every thread runs two independent
+// 8-step chains (twice the ILP of the one-ended sweep, the forward / back
+// phases being latency-bound).  Top rows k = 0..7 go down as above
+// (f slot rho_k / p_k, lam_k = coefficient of X_left / p_k, ga_k = c_k / p_k);
+// bottom rows k = 15..8 go up (f slot sig_k / q_k, lam_k = coefficient of X
+// / q_k, ga_k = a_k / q_k).  Rows 7 and 8 meet in a 2 x 2 step scaled by
+// s = 1 / (1 - (a_8 / q_8)(c_7 / p_7)) (no determinant: the tip dummies'
+// 1e300 pivots cannot overflow it), then both halves back-substitute outward.
+template <int DIR>
+__device__ __forceinline__ void chunk_forward_tw(double* __restrict__ pF,
+                                                 const double* __restrict__ pL,
+                                                 const double* __restrict__ pH,
+                                                 const CoefSrc& pc, double clo, double chi,
+                                                 bool first, int wallfix, double uwall,
+                                                 double uwall2, double (&lam)[LQ - 1],
+                                                 double (&cg_)[LQ - 1], ChunkOut& o) {
+  constexpr int H = (LQ - 1) / 2;  // rows per half
+  const double csum = clo + chi;
+  double ivp = 0.0, rho = 0.0, lm = 0.0, cprev = 0.0;
+  double ivq = 0.0, sig = 0.0, mu = 0.0, anext = 0.0;
+  int phi = 0x7fffffff;
+#pragma unroll
+  for (int j = 0; j < H; j++) {
+    const int kt = j, kb = LQ - 2 - j;
+    const double2 act = coef_at(pc, kt);
+    const double2 acb = coef_at(pc, kb);
+    const double rt = fma(-chi, pH[DIR * kt], fma(-clo, pL[DIR * kt], pF[DIR * kt]));
+    const double rb = fma(-chi, pH[DIR * kb], fma(-clo, pL[DIR * kb], pF[DIR * kb]));
+    const double bbt = -(act.x + act.y + csum);
+    const double bbb = -(acb.x + acb.y + csum);
+    double bp, bq;
+    if (j == 0) {
+      bp = bbt;
+      rho = rt;
+      lm = first ? 0.0 : -act.x;
+      bq = bbb;
+      sig = rb;
+      mu = -acb.y;
+    } else {
+      const double w = act.x * ivp;
+      bp = fma(-w, cprev, bbt);
+      rho = fma(-w, rho, rt);
+      lm = -w * lm;
+      const double v = acb.y * ivq;
+      bq = fma(-v, anext, bbb);
+      sig = fma(-v, sig, rb);
+      mu = -v * mu;
+    }
+    phi = min(phi, min(__double2hiint(bp) & 0x7fffffff, __double2hiint(bq) & 0x7fffffff));
+    ivp = drcp(bp);
+    ivq = drcp(bq);
+    pF[DIR * kt] = rho * ivp;
+    lam[kt] = lm * ivp;
+    cg_[kt] = act.y * ivp;
+    cprev = act.y;
+    pF[DIR * kb] = sig * ivq;
+    lam[kb] = mu * ivq;
+    cg_[kb] = acb.x * ivq;
+    anext = acb.x;
+  }
+  constexpr int k = LQ - 1;  // the chunk-end row
+  double r;
+  if (!wallfix) {
+    r = fma(-chi, pH[DIR * k], fma(-clo, pL[DIR * k], pF[DIR * k]));
+  } else {
+    const double ul = wallfix == 2 ? pL[DIR * k] : uwall;
+    const double uh = wallfix == 1 ? pH[DIR * k] : wallfix == 2 ? uwall : uwall2;
+    r = pF[DIR * k] - clo * ul - chi * uh;
+  }
+  const double2 ac = coef_at(pc, k);
+  o.a_end = ac.x;
+  o.c_end = ac.y;
+  o.r_end = r;
+  o.phi = phi;
+}
+
+template <int DIR>
+__device__ __forceinline__ void chunk_back_tw(double* __restrict__ pF, double* __restrict__ sb,
+                                              const double (&lam)[LQ - 1], double (&ga)[LQ - 1],
+                                              ChunkOut& o) {
+  constexpr int H = (LQ - 1) / 2;
+  // rows H-1 and H: x_H = sig_H + mu_H X - ag_H x_{H-1},
+  //                 x_{H-1} = rho_{H-1} + lam_{H-1} XL - cg_{H-1} x_H
+  const double agm = ga[H], cgm = ga[H - 1];
+  const double den = fma(-agm, cgm, 1.0);
+  const double s = drcp(den);
+  o.phi = min(o.phi, __double2hiint(den) & 0x7fffffff);
+  const double rt = pF[DIR * (H - 1)];
+  const double Am = s * fma(-agm, rt, pF[DIR * H]);
+  const double Bm = -s * agm * lam[H - 1];
+  const double Gm = s * lam[H];
+  // top half (k = H-1 .. 0) and bottom half (k = H+1 .. LQ-2), interleaved
+  double At = Am, Bt = Bm, Gt = Gm, Ab = Am, Bb = Bm, Gb = Gm;
+#pragma unroll
+  for (int j = 0; j < H; j++) {
+    const int kt = H - 1 - j;
+    const double g = ga[kt];
+    At = fma(-g, At, pF[DIR * kt]);
+    Bt = fma(-g, Bt, lam[kt]);
+    Gt = -g * Gt;
+    pF[DIR * kt] = At;
+    sb[kt] = Bt;
+    ga[kt] = Gt;
+    if (j < H - 1) {
+      const int kb = H + 1 + j;
+      const double gb = ga[kb];
+      Ab = fma(-gb, Ab, pF[DIR * kb]);
+      Bb = -gb * Bb;
+      Gb = fma(-gb, Gb, lam[kb]);
+      pF[DIR * kb] = Ab;
+      sb[kb] = Bb;
+      ga[kb] = Gb;
+    }
+  }
+  pF[DIR * H] = Am;
+  sb[H] = Bm;
+  ga[H] = Gm;
+  o.au = At;
+  o.bu = Bt;
+  o.gu = Gt;
+  o.ad = Ab;
+  o.bd = Bb;
+  o.gd = Gb;
+}
+
 template <int DIR>
 __device__ __forceinline__ void chunk_store(double* __restrict__ pF, const double* __restrict__ sb,
                                             const double (&ga)[LQ - 1], double XL, double X) {
@@ -308,6 +435,17 @@ __device__ __forceinline__ void chunk_store(double* __restrict__ pF, const doubl
   for (int k = 0; k < LQ - 1; k++) pF[DIR * k] = fma(ga[k], X, fma(sb[k], XL, pF[DIR * k]));
   pF[DIR * (LQ - 1)] = X;
 }
+
+#ifndef TMG_LEGK_TWIST
+#define TMG_LEGK_TWIST 1  // 0: the one-ended chunk sweep
+#endif
+#if TMG_LEGK_TWIST
+#define LEGK_FWD chunk_forward_tw
+#define LEGK_BACK chunk_back_tw
+#else
+#define LEGK_FWD chunk_forward
+#define LEGK_BACK chunk_back
+#endif
 
 }  // namespace
 
@@ -507,13 +645,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     if (act) {
       if (first) pF[g.dir * pad] -= tip_a * tip_u;  // only this thread reads the tip's f
       if (g.dir > 0)
-        chunk_forward<1>(pF, Ls + bL + e0, Hs + bH + e0, cpre, clo, chi,
-                         first, wallfix, uwall, uwall2, lam, ga, co);
+        LEGK_FWD<1>(pF, Ls + bL + e0, Hs + bH + e0, cpre, clo, chi,
+                    first, wallfix, uwall, uwall2, lam, ga, co);
       else
-        chunk_forward<-1>(pF, Ls + bL - e0, Hs + bH - e0, cpre, clo,
-                          chi, first, wallfix, uwall, uwall2, lam, ga, co);
+        LEGK_FWD<-1>(pF, Ls + bL - e0, Hs + bH - e0, cpre, clo,
+                     chi, first, wallfix, uwall, uwall2, lam, ga, co);
     }
-    phi = min(phi, co.phi);
 #ifdef TMG_LEGK_PREFETCH
     const uint16_t tmN = tm_of(scn);
 #endif
@@ -522,10 +659,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     double* sb = Hs + tid * LQ;  // this thread's beta row
     if (act) {
       if (g.dir > 0)
-        chunk_back<1>(pF, sb, lam, ga, co);
+        LEGK_BACK<1>(pF, sb, lam, ga, co);
       else
-        chunk_back<-1>(pF, sb, lam, ga, co);
+        LEGK_BACK<-1>(pF, sb, lam, ga, co);
     }
+
+    phi = min(phi, co.phi);
 
     // ---- reduced system over the chunk ends (shared memory in Ls) ----------
     double2* sFU = reinterpret_cast<double2*>(Ls);  // first-point forms (au, bu)
