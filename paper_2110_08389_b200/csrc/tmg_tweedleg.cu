@@ -115,6 +115,29 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ unsigned mapa_u32(const void* p, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_v2(unsigned addr, double x, double y) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(x), "d"(y) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(unsigned addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void cluster_arrive() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
 }
@@ -436,6 +459,9 @@ __device__ __forceinline__ void chunk_store(double* __restrict__ pF, const doubl
   pF[DIR * (LQ - 1)] = X;
 }
 
+#ifndef TMG_LEGK_XMB
+#define TMG_LEGK_XMB 1  // 0: split pairs exchange through a full cluster barrier
+#endif
 #ifndef TMG_LEGK_TWIST
 #define TMG_LEGK_TWIST 1  // 0: the one-ended chunk sweep
 #endif
@@ -456,7 +482,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
   double* Ls = F + kLegArrF;   // u row on the low side
   double* Hs = Ls + kLegArrU;  // u row on the high side
   uint64_t* bar = reinterpret_cast<uint64_t*>(Hs + kLegArrU);
-  double* xch = reinterpret_cast<double*>(bar + 1);  // [2 parities][P, Qh]
+  uint64_t* xbar = bar + 1;  // split pairs: the peer's leg end has arrived
+  double* xch = reinterpret_cast<double*>(bar + 2);  // [2 parities][P, Qh]
   const int tid = threadIdx.x;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
@@ -468,9 +495,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     reinterpret_cast<double2*>(smem)[i] = make_double2(0, 0);
   if (tid == 0) {
     mbar_init(bar, 1);
+#if TMG_LEGK_XMB
+    mbar_init(xbar, 1);
+#endif
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+#if TMG_LEGK_XMB
+  cluster_arrive();  // the peer's exchange barrier is initialised before any remote arrive
+  cluster_wait();
+#else
   __syncthreads();
+#endif
   pdl_wait();  // the fields of the previous kernel are complete from here on
   if (a.corners && blockIdx.x == 0 && tid < 4) {
     // the four interior corner points: point blocks of the red stage
@@ -729,6 +764,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     const double P = D * iB, Qh = H * iB;
     sP[tid] = P;
     sQ[tid] = Qh;
+#if TMG_LEGK_XMB
+    if (split && hubthr) {
+      // the leg end of this CTA's half of a split block goes straight into the
+      // peer's exchange slot; the remote arrive (release, cluster scope)
+      // completes the peer's exchange-barrier phase
+      const int par = nsplit & 1;
+      st_cluster_v2(mapa_u32(xch + 2 * par, rank ^ 1), P, Qh);
+      mbar_arrive_remote(mapa_u32(xbar, rank ^ 1));
+    }
+    __syncthreads();
+#else
     if (split) {
       // the leg end of each CTA's half of a split block goes to the peer
       const int par = nsplit & 1;
@@ -741,6 +787,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     } else {
       __syncthreads();
     }
+#endif
 
     // ---- branch rows ----------------------------------------------------------
     if (hubthr && crossb) {
@@ -776,8 +823,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
       double px, qx, py, qy;
       if (B.split) {
         const int par = nsplit & 1;
+#if TMG_LEGK_XMB
+        mbar_wait_cluster(xbar, (unsigned)par);
+        const double pp = xch[2 * par], qp = xch[2 * par + 1];
+#else
         const double* peer = cluster.map_shared_rank(xch, rank ^ 1);
         const double pp = peer[2 * par], qp = peer[2 * par + 1];
+#endif
         if (leg == 0) { px = P; qx = Qh; py = pp; qy = qp; }
         else { px = pp; qx = qp; py = P; qy = Qh; }
       } else {
@@ -1223,7 +1275,7 @@ void free_leg_plan(LegPlan& P) {
   P.coef = nullptr;
 }
 
-size_t leg_smem_bytes() { return sizeof(double) * kLegStage + sizeof(uint64_t) + 64; }
+size_t leg_smem_bytes() { return sizeof(double) * kLegStage + 2 * sizeof(uint64_t) + 64; }
 
 cudaError_t init_leg_kernel() {
   static cudaError_t done = cudaErrorNotReady;
