@@ -195,6 +195,29 @@ __device__ __forceinline__ void issue_loads(const LegArgs& a, int item, double* 
   }
 }
 
+// the same from the item's descriptor blob in shared memory
+__device__ __forceinline__ void issue_loads_blob(const LegArgs& a, const unsigned char* blob,
+                                                 double* stage, uint64_t* bar) {
+  const int lane = threadIdx.x & 31;
+  const LegBlobHead* hd = reinterpret_cast<const LegBlobHead*>(blob);
+  const LegCopy* cps = reinterpret_cast<const LegCopy*>(blob + sizeof(LegBlobHead));
+  const int ncopy = hd->ncopy;
+  if (lane == 0) mbar_expect_tx(bar, (unsigned)hd->bytes);
+  __syncwarp();
+  for (int c = lane; c < ncopy; c += 32) {
+    const LegCopy cp = cps[c];
+    const double* src = cp.src == 0 ? a.fn : cp.src == 1 ? a.ft : cp.src == 2 ? a.un : a.ut;
+    LEGK_CHECK(cp.s >= 0 && cp.n > 0 && cp.g >= 0 && (cp.s & 1) == 0 && (cp.g & 1) == 0 &&
+                   (cp.s < kLegArrF ? cp.s + cp.n <= kLegArrF
+                                    : cp.s + cp.n <= kLegArrF + 2 * kLegArrU &&
+                                          (cp.s >= kLegArrF + kLegArrU ||
+                                           cp.s + cp.n <= kLegArrF + kLegArrU)) &&
+                   cp.g + cp.n <= (long)a.ld * a.ld,
+               "bulk load range");
+    bulk_g2s(stage + cp.s, src + cp.g, (unsigned)cp.n * 8u, bar);
+  }
+}
+
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
                "r"(smem_u32(src)), "r"(bytes)
@@ -232,16 +255,10 @@ struct ChunkOut {
   int phi;            // smallest high word of |pivot| (vanishing-pivot check)
 };
 
-#ifndef TMG_LEGK_CPRE
-#define TMG_LEGK_CPRE 0  // > 0: couplings of the chunk's first points loaded during the stage wait (measured slower: spills)
-#endif
 struct CoefSrc {
   const double2* __restrict__ p;  // chunk-permuted table, point k at p[32 k]
-  double2 pre[TMG_LEGK_CPRE > 0 ? TMG_LEGK_CPRE : 1];
 };
-__device__ __forceinline__ double2 coef_at(const CoefSrc& c, int k) {
-  return k < TMG_LEGK_CPRE ? c.pre[k < TMG_LEGK_CPRE ? k : 0] : __ldg(c.p + 32 * k);
-}
+__device__ __forceinline__ double2 coef_at(const CoefSrc& c, int k) { return __ldg(c.p + 32 * k); }
 
 template <int DIR>
 __device__ __forceinline__ void chunk_forward(double* __restrict__ pF,
@@ -484,6 +501,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
   uint64_t* bar = reinterpret_cast<uint64_t*>(Hs + kLegArrU);
   uint64_t* xbar = bar + 1;  // split pairs: the peer's leg end has arrived
   double* xch = reinterpret_cast<double*>(bar + 2);  // [2 parities][P, Qh]
+  uint64_t* bbar = reinterpret_cast<uint64_t*>(xch + 4);  // descriptor blob buffers 0, 1
+  unsigned char* blobs = reinterpret_cast<unsigned char*>(bbar + 2);
   const int tid = threadIdx.x;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
@@ -495,6 +514,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     reinterpret_cast<double2*>(smem)[i] = make_double2(0, 0);
   if (tid == 0) {
     mbar_init(bar, 1);
+    mbar_init(bbar, 1);
+    mbar_init(bbar + 1, 1);
 #if TMG_LEGK_XMB
     mbar_init(xbar, 1);
 #endif
@@ -528,25 +549,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     const int ci = cid + s * ncl;
     return ci < a.nsched ? a.sched[ci] : make_int4(-2, -2, 0, 0);
   };
+  // this rank's descriptor blob of cluster iteration s: (offset / 16, bytes)
+  auto blob_at = [&](int s) -> int2 {
+    const int ci = cid + s * ncl;
+    if (ci >= a.nsched) return make_int2(0, 0);
+    const int4 e = a.bsched[ci];
+    return rank ? make_int2(e.z, e.w) : make_int2(e.x, e.y);
+  };
+  // warp 0, lane 0: blob of iteration s into buffer s & 1
+  auto fetch_blob = [&](int2 bl, int s) {
+    if (bl.y > 0) {
+      uint64_t* bb = bbar + (s & 1);
+      mbar_expect_tx(bb, (unsigned)bl.y);
+      bulk_g2s(blobs + (s & 1) * kLegBlob, a.blob + (size_t)bl.x * 16, (unsigned)bl.y, bb);
+    }
+  };
   int4 sc = sched_at(0);
-#ifdef TMG_LEGK_PREFETCH
-  auto tm_of = [&](const int4& e) -> uint16_t {
-    const int it = rank ? e.y : e.x;
-    return it >= 0 ? a.tmap[(size_t)it * LT + tid] : (uint16_t)0xFFFF;
-  };
-  auto block_of = [&](const int4& e, uint16_t t) -> LegBlock {
-    LegBlock b{};
-    const int it = rank ? e.y : e.x;
-    if (it >= 0 && t != 0xFFFF) b = a.blocks[a.items[it].blk0 + (t >> 1)];
-    return b;
-  };
-  uint16_t tmC = tm_of(sc);
-  LegBlock BC = block_of(sc, tmC);
-#endif
+  unsigned bph = 0;  // parity of each blob buffer's next fill
   if (tid < 32) {
+    if (tid == 0) {
+      fetch_blob(blob_at(0), 0);
+      fetch_blob(blob_at(1), 1);
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     const int it = rank ? sc.y : sc.x;
-    if (it >= 0) issue_loads(a, it, smem, bar);
+    if (it >= 0) {
+      mbar_wait(bbar, 0);
+      issue_loads_blob(a, blobs, smem, bar);
+    }
   }
   int nsplit = 0, phi = 0x7fffffff, ph = 0;
   bool bad = false;
@@ -575,21 +605,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     const bool split = (sc.z & 1) != 0;
     const int steps = (sc.z >> (rank ? 16 : 8)) & 0xff;
     const int4 scn = sched_at(s + 1);
+    const unsigned char* blob = blobs + (s & 1) * kLegBlob;
 
     // ---- per-thread chunk setup (overlaps the wait for the staged rows) ----
-#ifdef TMG_LEGK_PREFETCH
-    const uint16_t tm = tmC;
-    const bool act = tm != 0xFFFF;
-    const int slot = tm >> 1, leg = tm & 1;
-    const LegBlock B = BC;
-#else
     uint16_t tm = 0xFFFF;
-    if (item >= 0) tm = a.tmap[(size_t)item * LT + tid];
+    LegBlock B{};
+    if (item >= 0) {
+      mbar_wait(bbar + (s & 1), (bph >> (s & 1)) & 1u);
+      bph ^= 1u << (s & 1);
+      const LegBlobHead* hd = reinterpret_cast<const LegBlobHead*>(blob);
+      tm = reinterpret_cast<const uint16_t*>(blob + hd->off_tmap)[tid];
+      if (tm != 0xFFFF) B = reinterpret_cast<const LegBlock*>(blob + hd->off_blocks)[tm >> 1];
+    }
     const bool act = tm != 0xFFFF;
     const int slot = tm >> 1, leg = tm & 1;
-    LegBlock B{};
-    if (act) B = a.blocks[a.items[item].blk0 + slot];
-#endif
     LegGeo g;
     g.set(act ? B.k : 2, B.quad, leg, n);
     const int m = g.m;
@@ -646,11 +675,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
       uwall = a.un[(size_t)(g.p0 + g.sx * (m - 1)) * ld + (g.bj - g.sy)];
     }
 
-    CoefSrc cpre;  // first points' couplings in flight during the stage wait
+    CoefSrc cpre;
     cpre.p = a.coef + cofs;
-#pragma unroll
-    for (int k = 0; k < TMG_LEGK_CPRE; k++)
-      cpre.pre[k] = act ? __ldg(cpre.p + 32 * k) : make_double2(0.0, 0.0);
     LEGK_MARK(0);
     if (item >= 0) {
       mbar_wait(bar, (unsigned)ph);
@@ -686,9 +712,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
         LEGK_FWD<-1>(pF, Ls + bL - e0, Hs + bH - e0, cpre, clo,
                      chi, first, wallfix, uwall, uwall2, lam, ga, co);
     }
-#ifdef TMG_LEGK_PREFETCH
-    const uint16_t tmN = tm_of(scn);
-#endif
     __syncthreads();  // every thread is done with the staged u rows
     LEGK_MARK(2);
     double* sb = Hs + tid * LQ;  // this thread's beta row
@@ -757,9 +780,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
       __syncthreads();
     }
     LEGK_MARK(4);
-#ifdef TMG_LEGK_PREFETCH
-    const LegBlock BN = block_of(scn, tmN);
-#endif
     if (act) phi = min(phi, __double2hiint(Bv) & 0x7fffffff);
     const double P = D * iB, Qh = H * iB;
     sP[tid] = P;
@@ -862,72 +882,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     __syncthreads();
     LEGK_MARK(6);
 
-    // ---- stores and the next item's loads.  Default: warp 0 bulk-copies the
-    // aligned leg interiors (single elements at unaligned ends), waits until
-    // they have left shared memory and issues the next item's loads.
-    // TMG_LEGK_EARLYU: the next item's u rows go out before the stores (the u
-    // arrays are free).  TMG_LEGK_TSTORE: every thread stores, coalesced.
+    // ---- stores and the next item's loads: warp 0 bulk-copies the aligned
+    // leg interiors (single elements at unaligned ends), waits until they have
+    // left shared memory, issues the next item's loads from its blob (fetched
+    // an item ago) and refills this item's blob buffer two items ahead.
     const int nx = rank ? scn.y : scn.x;
-#ifdef TMG_LEGK_EARLYU
-    if (tid < 32 && nx >= 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_loads(a, nx, smem, bar, 0);
-    }
-    constexpr int fpart = 1;
-#else
-    constexpr int fpart = -1;
-#endif
-#ifdef TMG_LEGK_TSTORE
-    if (item >= 0) {
-      const LegItem I = a.items[item];
-      const int nl = 2 * I.nblk;
-      const int w = tid >> 5, lane = tid & 31;
-      const bool wide = nl <= 2;  // one or two long legs: every thread walks each leg
-      for (int q = wide ? 0 : w; q < nl; q += wide ? 1 : LT / 32) {
-        const LegBlock Bq = a.blocks[I.blk0 + (q >> 1)];
-        const int lq = q & 1;
-        if ((lq ? Bq.t0[1] : Bq.t0[0]) < 0) continue;
-        LegGeo gq;
-        gq.set(Bq.k, Bq.quad, lq, n);
-        const int lo = min(gq.p0, gq.p0 + gq.dir * (gq.m - 1));
-        double* dst = (lq == 0 ? a.ut : a.un) + (size_t)gq.row * ld + lo;
-        const double* srcs = F + (lq ? Bq.sb[1][0] : Bq.sb[0][0]) + (lo - gq.p0);
-        for (int e = wide ? tid : lane; e < gq.m; e += wide ? LT : 32) dst[e] = srcs[e];
-      }
-    }
-    __syncthreads();  // the f array is free
-    if (tid < 32 && nx >= 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_loads(a, nx, smem, bar, fpart);
-    }
-#else
     if (tid < 32) {
       if (item >= 0) {
-        const LegItem I = a.items[item];
-        for (int c = tid; c < I.nedge; c += 32) {
-          const LegCopy cp = a.copies[I.edge0 + c];
+        const LegBlobHead* hd = reinterpret_cast<const LegBlobHead*>(blob);
+        const LegCopy* cps = reinterpret_cast<const LegCopy*>(blob + sizeof(LegBlobHead));
+        const int ncopy = hd->ncopy, nstore = hd->nstore, nedge = hd->nedge;
+        for (int c = tid; c < nedge; c += 32) {
+          const LegCopy cp = cps[ncopy + nstore + c];
           (cp.src == 3 ? a.ut : a.un)[cp.g] = F[cp.s];
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        for (int c = tid; c < I.nstore; c += 32) {
-          const LegCopy cp = a.copies[I.store0 + c];
+        for (int c = tid; c < nstore; c += 32) {
+          const LegCopy cp = cps[ncopy + c];
           bulk_s2g((cp.src == 3 ? a.ut : a.un) + cp.g, F + cp.s, (unsigned)cp.n * 8u);
         }
         bulk_commit();
       }
       if (nx >= 0) {
+        const int b1 = (s + 1) & 1;
+        mbar_wait(bbar + b1, (bph >> b1) & 1u);
         bulk_wait_read();  // the stores have left shared memory
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue_loads(a, nx, smem, bar, fpart);
+        issue_loads_blob(a, blobs + b1 * kLegBlob, smem, bar);
+      }
+      __syncwarp();  // every lane is done with this item's blob
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        fetch_blob(blob_at(s + 2), s + 2);  // its latency hides under the stage loads
       }
     }
-#endif
     LEGK_MARK(7);
     sc = scn;
-#ifdef TMG_LEGK_PREFETCH
-    tmC = tmN;
-    BC = BN;
-#endif
   }
 #undef LEGK_MARK
 #ifdef TMG_LEGK_TIMING
@@ -1009,6 +999,8 @@ std::string build_leg_plan(int n, LegPlan& P, int kmin, int kmax) {
     std::vector<uint16_t> tmap;
     std::vector<LegCopy> copies;
     std::vector<int> item_chunks;
+    std::vector<unsigned char> blob;   // descriptor blobs, 16-byte aligned
+    std::vector<int2> item_blob;       // (offset / 16, bytes) per item
 
     struct Open {
       std::vector<std::pair<HostBlock, int>> members;  // block, split (0/1/2)
@@ -1112,6 +1104,28 @@ std::string build_leg_plan(int n, LegPlan& P, int kmin, int kmax) {
       it.nedge = (int32_t)edges.size();
       copies.insert(copies.end(), edges.begin(), edges.end());
       it.bytes = (int32_t)bytes;
+      {  // the item's descriptor blob: header, copies, blocks, thread map
+        LegBlobHead hd{};
+        hd.nblk = it.nblk;
+        hd.ncopy = it.ncopy;
+        hd.nstore = it.nstore;
+        hd.nedge = it.nedge;
+        hd.bytes = it.bytes;
+        const int ncp = it.ncopy + it.nstore + it.nedge;
+        hd.off_blocks = (int32_t)(sizeof(LegBlobHead) + ncp * sizeof(LegCopy));
+        hd.off_tmap = hd.off_blocks + (int32_t)(o.members.size() * sizeof(LegBlock));
+        hd.off_tmap = (hd.off_tmap + 1) & ~1;
+        const int size = ((hd.off_tmap + LT * 2) + 15) & ~15;
+        if (size > kLegBlob) return -1;
+        std::vector<unsigned char> b(size, 0);
+        std::memcpy(b.data(), &hd, sizeof hd);
+        std::memcpy(b.data() + sizeof hd, copies.data() + it.copy0, ncp * sizeof(LegCopy));
+        std::memcpy(b.data() + hd.off_blocks, iblocks.data() + it.blk0,
+                    o.members.size() * sizeof(LegBlock));
+        std::memcpy(b.data() + hd.off_tmap, map.data(), LT * 2);
+        item_blob.push_back(make_int2((int)(blob.size() / 16), size));
+        blob.insert(blob.end(), b.begin(), b.end());
+      }
       int steps = 0;
       while ((1 << steps) < maxch) steps++;
       it.steps = (int16_t)steps;
@@ -1188,6 +1202,12 @@ std::string build_leg_plan(int n, LegPlan& P, int kmin, int kmax) {
       const int sb = ib >= 0 ? items[ib].steps : 0;
       sched.push_back(make_int4(ia, ib, (items[ia].steps << 8) | (sb << 16), whole[i].first));
     }
+    std::vector<int4> bsched;
+    for (const int4& e : sched) {
+      const int2 b0 = e.x >= 0 ? item_blob[e.x] : make_int2(0, 0);
+      const int2 b1 = e.y >= 0 ? item_blob[e.y] : make_int2(0, 0);
+      bsched.push_back(make_int4(b0.x, b0.y, b1.x, b1.y));
+    }
     C.corners = red && kmin <= 1;  // the four corner points (k = 1, red)
     C.nsched = (int)sched.size();
     C.nitems = (int)items.size();
@@ -1212,6 +1232,8 @@ std::string build_leg_plan(int n, LegPlan& P, int kmin, int kmax) {
     }
     up(copies, C.copies);
     up(sched, C.sched);
+    up(blob, C.blob);
+    up(bsched, C.bsched);
     if (!err.empty()) return err;
   }
   return "";
@@ -1269,13 +1291,19 @@ void free_leg_plan(LegPlan& P) {
     cudaFree(C.copies);
     cudaFree(C.mail);
     cudaFree(C.sched);
+    cudaFree(C.blob);
+    cudaFree(C.bsched);
     C = LegColour();
   }
   cudaFree(P.coef);
   P.coef = nullptr;
 }
 
-size_t leg_smem_bytes() { return sizeof(double) * kLegStage + 2 * sizeof(uint64_t) + 64; }
+size_t leg_smem_bytes() {
+  // stage, bar + xbar, xch (4 doubles), two blob barriers, two blob buffers
+  return sizeof(double) * kLegStage + 2 * sizeof(uint64_t) + 4 * sizeof(double) +
+         2 * sizeof(uint64_t) + 2 * kLegBlob;
+}
 
 cudaError_t init_leg_kernel() {
   static cudaError_t done = cudaErrorNotReady;
@@ -1330,6 +1358,8 @@ cudaError_t launch_leg_colour(const LegPlan& P, int red, const SweepArgs& s, cud
   a.mail = C.mail;
   a.corners = C.corners;
   a.sched = C.sched;
+  a.blob = C.blob;
+  a.bsched = C.bsched;
   a.nsched = C.nsched;
   a.err = s.err;
   const int ncl = std::max(1, std::min(sms, C.nsched));  // two CTAs per SM (>= 1 for the corners)

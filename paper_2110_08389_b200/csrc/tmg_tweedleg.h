@@ -51,12 +51,26 @@ struct LegCopy {  // one bulk copy between a field buffer and the shared stage
   uint8_t src;    // buffer: 0 f N, 1 f T, 2 u N, 3 u T
   uint8_t pad[7];
 };
+// Per-item descriptor blob (16-byte aligned, <= kLegBlob bytes): the header,
+// the item's LegCopy records (loads, stores, edge stores), its LegBlocks and
+// its thread map, bulk-copied into shared memory one item ahead so neither
+// the per-thread setup nor warp 0's store / load issue waits on L2.
+constexpr int kLegBlob = 3072;
+struct LegBlobHead {
+  int32_t nblk, ncopy, nstore, nedge;
+  int32_t bytes;       // staged bytes (mbarrier transaction count)
+  int32_t off_blocks;  // byte offsets in the blob
+  int32_t off_tmap;
+  int32_t pad;
+};
 struct LegColour {
   LegItem* items = nullptr;
   LegBlock* blocks = nullptr;
   uint16_t* tmap = nullptr;  // [item][thread]: (block slot << 1 | leg), 0xFFFF idle
   LegCopy* copies = nullptr;  // loads, stores and edge stores of every item
   int4* sched = nullptr;     // cluster iteration: (item rank 0, item rank 1, split, load)
+  unsigned char* blob = nullptr;  // descriptor blobs of every item
+  int4* bsched = nullptr;    // per cluster iteration: (blob offset / 16, bytes) of rank 0, rank 1
   int nsched = 0, nitems = 0;
   int cross = 0;              // this colour holds the central cross
   int corners = 0;            // this colour (red) relaxes the four corner points
@@ -89,6 +103,8 @@ struct LegArgs {
   const uint16_t* tmap;
   const LegCopy* copies;
   const int4* sched;
+  const unsigned char* blob;
+  const int4* bsched;
   int nsched;
   int* err;
   long long* timing;  // per-CTA phase clocks (TMG_LEGK_TIMING), or null
