@@ -60,6 +60,10 @@ namespace cg = cooperative_groups;
   } while (0)
 #endif
 
+#ifndef TMG_LEGK_SPLITISSUE
+#define TMG_LEGK_SPLITISSUE 1  // 0: warp 0 alone issues an item's stores and the next item's loads
+#endif
+
 namespace tmg {
 
 namespace {
@@ -172,40 +176,27 @@ struct LegGeo {
   }
 };
 
-// issue an item's bulk loads (warp 0).  part -1: everything; part 0: the
-// transaction bytes and the u rows; part 1: the f runs.
-__device__ __forceinline__ void issue_loads(const LegArgs& a, int item, double* stage,
-                                            uint64_t* bar, int part = -1) {
-  const int lane = threadIdx.x & 31;
-  const LegItem I = a.items[item];
-  if (part <= 0 && lane == 0) mbar_expect_tx(bar, (unsigned)I.bytes);
-  __syncwarp();
-  for (int c = lane; c < I.ncopy; c += 32) {
-    const LegCopy cp = a.copies[I.copy0 + c];
-    if (part >= 0 && (cp.s < kLegArrF) != (part == 1)) continue;
-    const double* src = cp.src == 0 ? a.fn : cp.src == 1 ? a.ft : cp.src == 2 ? a.un : a.ut;
-    LEGK_CHECK(cp.s >= 0 && cp.n > 0 && cp.g >= 0 && (cp.s & 1) == 0 && (cp.g & 1) == 0 &&
-                   (cp.s < kLegArrF ? cp.s + cp.n <= kLegArrF
-                                    : cp.s + cp.n <= kLegArrF + 2 * kLegArrU &&
-                                          (cp.s >= kLegArrF + kLegArrU ||
-                                           cp.s + cp.n <= kLegArrF + kLegArrU)) &&
-                   cp.g + cp.n <= (long)a.ld * a.ld,
-               "bulk load range");
-    bulk_g2s(stage + cp.s, src + cp.g, (unsigned)cp.n * 8u, bar);
-  }
-}
-
-// the same from the item's descriptor blob in shared memory
+// issue an item's bulk loads from its descriptor blob in shared memory (one
+// warp).  part -1: everything; 0: the u rows; 1: the f runs.  The stage
+// barrier counts one arrival per part (-1 arrives for both).
 __device__ __forceinline__ void issue_loads_blob(const LegArgs& a, const unsigned char* blob,
-                                                 double* stage, uint64_t* bar) {
+                                                 double* stage, uint64_t* bar, int part = -1) {
   const int lane = threadIdx.x & 31;
   const LegBlobHead* hd = reinterpret_cast<const LegBlobHead*>(blob);
   const LegCopy* cps = reinterpret_cast<const LegCopy*>(blob + sizeof(LegBlobHead));
   const int ncopy = hd->ncopy;
-  if (lane == 0) mbar_expect_tx(bar, (unsigned)hd->bytes);
+  if (lane == 0) {
+#if TMG_LEGK_SPLITISSUE
+    if (part != 1) mbar_expect_tx(bar, (unsigned)(hd->bytes - hd->bytes_f));
+    if (part != 0) mbar_expect_tx(bar, (unsigned)hd->bytes_f);
+#else
+    mbar_expect_tx(bar, (unsigned)hd->bytes);
+#endif
+  }
   __syncwarp();
   for (int c = lane; c < ncopy; c += 32) {
     const LegCopy cp = cps[c];
+    if (part >= 0 && (cp.s < kLegArrF) != (part == 1)) continue;
     const double* src = cp.src == 0 ? a.fn : cp.src == 1 ? a.ft : cp.src == 2 ? a.un : a.ut;
     LEGK_CHECK(cp.s >= 0 && cp.n > 0 && cp.g >= 0 && (cp.s & 1) == 0 && (cp.g & 1) == 0 &&
                    (cp.s < kLegArrF ? cp.s + cp.n <= kLegArrF
@@ -231,6 +222,28 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+#ifndef TMG_LEGK_L2PF
+#define TMG_LEGK_L2PF 1  // 1: warp 0 prefetches the next item's runs into L2 while this one is solved
+#endif
+#ifndef TMG_LEGK_STAGGER
+#define TMG_LEGK_STAGGER 0  // > 0: odd clusters start late by this many units of 1024 ns
+#endif
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+// warp 0: the bulk loads an item's blob lists, as L2 prefetches
+__device__ __forceinline__ void prefetch_loads_blob(const LegArgs& a, const unsigned char* blob) {
+  const int lane = threadIdx.x & 31;
+  const LegBlobHead* hd = reinterpret_cast<const LegBlobHead*>(blob);
+  const LegCopy* cps = reinterpret_cast<const LegCopy*>(blob + sizeof(LegBlobHead));
+  const int ncopy = hd->ncopy;
+  for (int c = lane; c < ncopy; c += 32) {
+    const LegCopy cp = cps[c];
+    const double* src = cp.src == 0 ? a.fn : cp.src == 1 ? a.ft : cp.src == 2 ? a.un : a.ut;
+    bulk_prefetch_l2(src + cp.g, (unsigned)cp.n * 8u);
+  }
 }
 
 // One thread's chunk of 17 consecutive leg points: point k's f slot is
@@ -513,7 +526,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
   for (int i = tid; i < kLegStage / 2; i += LT)
     reinterpret_cast<double2*>(smem)[i] = make_double2(0, 0);
   if (tid == 0) {
+#if TMG_LEGK_SPLITISSUE
+    mbar_init(bar, 2);  // the u rows and the f runs arrive separately
+#else
     mbar_init(bar, 1);
+#endif
     mbar_init(bbar, 1);
     mbar_init(bbar + 1, 1);
 #if TMG_LEGK_XMB
@@ -528,6 +545,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
   __syncthreads();
 #endif
   pdl_wait();  // the fields of the previous kernel are complete from here on
+#if TMG_LEGK_STAGGER
+  if ((blockIdx.x >> 1) & 1)
+    for (int i = 0; i < TMG_LEGK_STAGGER; i++) __nanosleep(1024);
+#endif
   if (a.corners && blockIdx.x == 0 && tid < 4) {
     // the four interior corner points: point blocks of the red stage
     // (layout.py:72-74, relax_points _ckernels.pyx:42-51); their
@@ -583,7 +604,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
   // phase clocks of a -DTMG_LEGK_TIMING build (make timing): setup, stage
   // wait, forward, back, reduced system, branch, finalize, stores
 #ifdef TMG_LEGK_TIMING
-  long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tacc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long tlast = clock64();
   const bool timing = a.timing != nullptr && (tid == 0 || tid == 96);
 #define LEGK_MARK(i)                     \
@@ -683,6 +704,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
       ph ^= 1;
     }
     LEGK_MARK(1);
+#if TMG_LEGK_L2PF
+    // the next item's runs start toward L2 now (its blob arrived an item ago);
+    // the stage loads issued after this item's stores then hit L2
+    if (tid < 32 && (rank ? scn.y : scn.x) >= 0) {
+      const int b1 = (s + 1) & 1;
+      mbar_wait(bbar + b1, (bph >> b1) & 1u);
+      prefetch_loads_blob(a, blobs + b1 * kLegBlob);
+    }
+#endif
     double lam[LQ - 1], ga[LQ - 1];
     ChunkOut co{0, 1, 0, 0, 0, 1, 0, 0, 0, 0x7fffffff};
     double* pF = F + bF + g.dir * e0;
@@ -887,6 +917,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     // left shared memory, issues the next item's loads from its blob (fetched
     // an item ago) and refills this item's blob buffer two items ahead.
     const int nx = rank ? scn.y : scn.x;
+#if TMG_LEGK_SPLITISSUE
+    // warp 1: the next item's u rows go out at once (Ls / Hs are free after
+    // the finalize barrier); warp 0: bulk stores first, the edge elements
+    // while they drain, then the next item's f runs into the freed f array
+    if (tid >= 32 && tid < 64 && nx >= 0) {
+      const int b1 = (s + 1) & 1;
+      mbar_wait(bbar + b1, (bph >> b1) & 1u);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_loads_blob(a, blobs + b1 * kLegBlob, smem, bar, 0);
+    }
+    if (tid < 32) {
+      if (item >= 0) {
+        const LegBlobHead* hd = reinterpret_cast<const LegBlobHead*>(blob);
+        const LegCopy* cps = reinterpret_cast<const LegCopy*>(blob + sizeof(LegBlobHead));
+        const int ncopy = hd->ncopy, nstore = hd->nstore, nedge = hd->nedge;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int c = tid; c < nstore; c += 32) {
+          const LegCopy cp = cps[ncopy + c];
+          bulk_s2g((cp.src == 3 ? a.ut : a.un) + cp.g, F + cp.s, (unsigned)cp.n * 8u);
+        }
+        bulk_commit();
+        for (int c = tid; c < nedge; c += 32) {
+          const LegCopy cp = cps[ncopy + nstore + c];
+          (cp.src == 3 ? a.ut : a.un)[cp.g] = F[cp.s];
+        }
+      }
+      LEGK_MARK(8);
+      if (nx >= 0) {
+        const int b1 = (s + 1) & 1;
+        mbar_wait(bbar + b1, (bph >> b1) & 1u);
+        LEGK_MARK(9);
+        bulk_wait_read();  // the stores have left shared memory
+        LEGK_MARK(10);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_loads_blob(a, blobs + b1 * kLegBlob, smem, bar, 1);
+      }
+      __syncwarp();  // every lane is done with this item's blob
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        fetch_blob(blob_at(s + 2), s + 2);  // its latency hides under the stage loads
+      }
+    }
+#else
     if (tid < 32) {
       if (item >= 0) {
         const LegBlobHead* hd = reinterpret_cast<const LegBlobHead*>(blob);
@@ -903,10 +976,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
         }
         bulk_commit();
       }
+      LEGK_MARK(8);
       if (nx >= 0) {
         const int b1 = (s + 1) & 1;
         mbar_wait(bbar + b1, (bph >> b1) & 1u);
+        LEGK_MARK(9);
         bulk_wait_read();  // the stores have left shared memory
+        LEGK_MARK(10);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue_loads_blob(a, blobs + b1 * kLegBlob, smem, bar);
       }
@@ -916,18 +992,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
         fetch_blob(blob_at(s + 2), s + 2);  // its latency hides under the stage loads
       }
     }
+#endif
     LEGK_MARK(7);
     sc = scn;
   }
 #undef LEGK_MARK
 #ifdef TMG_LEGK_TIMING
   if (timing)
-    for (int i = 0; i < 8; i++) a.timing[(blockIdx.x + (tid ? gridDim.x : 0)) * 8 + i] = tacc[i];
+    for (int i = 0; i < 12; i++) a.timing[(blockIdx.x + (tid ? gridDim.x : 0)) * 12 + i] = tacc[i];
 #ifdef TMG_LEGK_TIMING
   if (a.timing && tid == 0) {  // SM of every CTA (cluster placement)
     unsigned sm;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-    a.timing[16 * 1024 + blockIdx.x] = sm;
+    a.timing[24 * 1024 + blockIdx.x] = sm;
   }
 #endif
 #endif
@@ -1111,6 +1188,9 @@ std::string build_leg_plan(int n, LegPlan& P, int kmin, int kmax) {
         hd.nstore = it.nstore;
         hd.nedge = it.nedge;
         hd.bytes = it.bytes;
+        hd.bytes_f = 0;
+        for (const LegCopy& cp : loads)
+          if (cp.s < kLegArrF) hd.bytes_f += 8 * cp.n;
         const int ncp = it.ncopy + it.nstore + it.nedge;
         hd.off_blocks = (int32_t)(sizeof(LegBlobHead) + ncp * sizeof(LegCopy));
         hd.off_tmap = hd.off_blocks + (int32_t)(o.members.size() * sizeof(LegBlock));
@@ -1365,7 +1445,7 @@ cudaError_t launch_leg_colour(const LegPlan& P, int red, const SweepArgs& s, cud
   const int ncl = std::max(1, std::min(sms, C.nsched));  // two CTAs per SM (>= 1 for the corners)
   a.timing = nullptr;
   if (leg_timing_on()) {
-    if (!g_leg_timing) cudaMalloc(&g_leg_timing, sizeof(long long) * 16 * 2 * 1024);
+    if (!g_leg_timing) cudaMalloc(&g_leg_timing, sizeof(long long) * 26 * 1024);
     a.timing = g_leg_timing;
     g_leg_timing_ctas = 2 * ncl;
   }
@@ -1383,28 +1463,28 @@ extern "C" int tmg_debug_leg_smids(int* out, int cap) {
   if (!tmg::g_leg_timing) return 0;
   const int n = std::min(cap, tmg::g_leg_timing_ctas);
   std::vector<long long> h(n);
-  cudaMemcpy(h.data(), tmg::g_leg_timing + 16 * 1024, n * sizeof(long long), cudaMemcpyDeviceToHost);
+  cudaMemcpy(h.data(), tmg::g_leg_timing + 24 * 1024, n * sizeof(long long), cudaMemcpyDeviceToHost);
   for (int i = 0; i < n; i++) out[i] = (int)h[i];
   return n;
 }
 
-extern "C" int tmg_debug_leg_phases(double* out8 /* [16] */) {
-  for (int i = 0; i < 16; i++) out8[i] = 0.0;
+extern "C" int tmg_debug_leg_phases(double* out /* [24] */) {
+  for (int i = 0; i < 24; i++) out[i] = 0.0;
   if (!tmg::g_leg_timing || tmg::g_leg_timing_ctas == 0) return 0;
-  std::vector<long long> h(8 * (size_t)tmg::g_leg_timing_ctas);
+  const size_t nc = (size_t)tmg::g_leg_timing_ctas;
+  // out[0..11]: thread 0 (warp 0, which also issues the bulk copies);
+  // out[12..23]: thread 96.  Slots 0-7 as in the kernel's phase list, 8-10
+  // split warp 0's store phase: store issue, blob wait, wait for the stores'
+  // shared-memory reads (slot 7 keeps the load issue)
+  std::vector<long long> h(24 * nc);
   if (cudaMemcpy(h.data(), tmg::g_leg_timing, h.size() * sizeof(long long),
                  cudaMemcpyDeviceToHost) != cudaSuccess)
     return -1;
-  // out8[0..7]: thread 0 (warp 0, which also issues the bulk copies);
-  // out8[8..15]: thread 96
-  std::vector<long long> h2(8 * (size_t)tmg::g_leg_timing_ctas);
-  cudaMemcpy(h2.data(), tmg::g_leg_timing + 8 * (size_t)tmg::g_leg_timing_ctas,
-             h2.size() * sizeof(long long), cudaMemcpyDeviceToHost);
-  for (size_t c = 0; c < (size_t)tmg::g_leg_timing_ctas; c++)
-    for (int i = 0; i < 8; i++) {
-      out8[i] += (double)h[c * 8 + i];
-      out8[8 + i] += (double)h2[c * 8 + i];
+  for (size_t c = 0; c < nc; c++)
+    for (int i = 0; i < 12; i++) {
+      out[i] += (double)h[c * 12 + i];
+      out[12 + i] += (double)h[(nc + c) * 12 + i];
     }
-  for (int i = 0; i < 16; i++) out8[i] /= tmg::g_leg_timing_ctas;
+  for (int i = 0; i < 24; i++) out[i] /= (double)nc;
   return tmg::g_leg_timing_ctas;
 }

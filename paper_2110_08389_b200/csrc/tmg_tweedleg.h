@@ -61,7 +61,7 @@ struct LegBlobHead {
   int32_t bytes;       // staged bytes (mbarrier transaction count)
   int32_t off_blocks;  // byte offsets in the blob
   int32_t off_tmap;
-  int32_t pad;
+  int32_t bytes_f;     // the f runs' share of `bytes`
 };
 struct LegColour {
   LegItem* items = nullptr;

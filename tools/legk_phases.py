@@ -17,10 +17,11 @@ _lib.check(L.tmg_session_load(st.native, 4, ctypes.c_void_p(u.data_ptr()), ctype
 _lib.check(L.tmg_session_sweeps(st.native, 4, 2, s))
 torch.cuda.synchronize()
 # last launch = the black stage of the finest level's second sweep
-out = (ctypes.c_double * 16)()
+out = (ctypes.c_double * 24)()
 n = L.tmg_debug_leg_phases(out)
-names = ["setup", "wait", "forward", "back", "reduced", "branch", "finalize", "stores"]
-for who, vals in (("thread0", list(out)[:8]), ("thread96", list(out)[8:])):
+names = ["setup", "wait", "forward", "back", "reduced", "branch", "finalize", "loadissue",
+         "storeissue", "blobwait", "storeread", "-"]
+for who, vals in (("thread0", list(out)[:12]), ("thread96", list(out)[12:])):
     tot = sum(vals)
     print(json.dumps({"who": who, "ctas": n, "cycles_per_cta": tot,
                       "share": {k: round(v / tot, 3) for k, v in zip(names, vals)}}))
