@@ -704,15 +704,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
       ph ^= 1;
     }
     LEGK_MARK(1);
-#if TMG_LEGK_L2PF
-    // the next item's runs start toward L2 now (its blob arrived an item ago);
-    // the stage loads issued after this item's stores then hit L2
-    if (tid < 32 && (rank ? scn.y : scn.x) >= 0) {
-      const int b1 = (s + 1) & 1;
-      mbar_wait(bbar + b1, (bph >> b1) & 1u);
-      prefetch_loads_blob(a, blobs + b1 * kLegBlob);
-    }
-#endif
     double lam[LQ - 1], ga[LQ - 1];
     ChunkOut co{0, 1, 0, 0, 0, 1, 0, 0, 0, 0x7fffffff};
     double* pF = F + bF + g.dir * e0;
@@ -744,6 +735,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     }
     __syncthreads();  // every thread is done with the staged u rows
     LEGK_MARK(2);
+#if TMG_LEGK_L2PF
+    // the next item's runs start toward L2 now (its blob, requested at the end of
+    // the previous item, has arrived by the time the forward pass is done); the
+    // stage loads issued after this item's stores then hit L2
+    if (tid < 32 && (rank ? scn.y : scn.x) >= 0) {
+      const int b1 = (s + 1) & 1;
+      mbar_wait(bbar + b1, (bph >> b1) & 1u);
+      prefetch_loads_blob(a, blobs + b1 * kLegBlob);
+    }
+#endif
     double* sb = Hs + tid * LQ;  // this thread's beta row
     if (act) {
       if (g.dir > 0)
