@@ -489,6 +489,116 @@ __device__ __forceinline__ void chunk_store(double* __restrict__ pF, const doubl
   pF[DIR * (LQ - 1)] = X;
 }
 
+#ifndef TMG_LEGK_RED2
+#define TMG_LEGK_RED2 0  // 1: the reduced system solved by one warp in two levels (measured slower: 0.66 -> 0.77 ms)
+#endif
+// padded index of reduced row t: groups of eight rows start 9 slots apart, so
+// a lane walking its group and a warp walking consecutive rows are both free
+// of bank conflicts
+__device__ __forceinline__ int ridx(int t) { return t + (t >> 3); }
+
+// Two-level solve of an item's reduced system by one warp (TMG_LEGK_RED2).
+// The 256 chunk-end rows  A X[t-1] + B X[t] + C X[t+1] = D - H x_branch  form
+// one tridiagonal system (A = 0 / C = 0 at leg ends, idle rows are identity
+// rows), kept at padded slots.  Lane j eliminates rows 8j .. 8j+6 (Thomas
+// down sweep, then an affine back pass: X[r] = al + be X[8j-1] + ga X[8j+7],
+// two right-hand sides D and H), the 32 group-end rows are solved by cyclic
+// reduction on warp shuffles, and every lane back-substitutes its group.
+// Out: sP / sQ (padded), X[t] = sP[t] - sQ[t] x_branch.
+__device__ __forceinline__ void red2_solve(double2* __restrict__ rAC, double2* __restrict__ rDH,
+                                           const double* __restrict__ rB, double* __restrict__ sP,
+                                           double* __restrict__ sQ, int& phi) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int q0 = 9 * lane;
+  double cp, dp, hp, lp;
+  {
+    const double2 ac = rAC[q0], dh = rDH[q0];
+    const double b = rB[q0];
+    phi = min(phi, __double2hiint(b) & 0x7fffffff);
+    const double iv = drcp(b);
+    cp = ac.y * iv;
+    dp = dh.x * iv;
+    hp = dh.y * iv;
+    lp = -ac.x * iv;
+    rAC[q0] = make_double2(lp, cp);
+    rDH[q0] = make_double2(dp, hp);
+  }
+#pragma unroll 1
+  for (int r = 1; r < 7; r++) {
+    const double2 ac = rAC[q0 + r], dh = rDH[q0 + r];
+    const double w = ac.x;
+    const double pv = fma(-w, cp, rB[q0 + r]);
+    phi = min(phi, __double2hiint(pv) & 0x7fffffff);
+    const double iv = drcp(pv);
+    cp = ac.y * iv;
+    dp = fma(-w, dp, dh.x) * iv;
+    hp = fma(-w, hp, dh.y) * iv;
+    lp = (-w * lp) * iv;
+    if (r < 6) {
+      rAC[q0 + r] = make_double2(lp, cp);
+      rDH[q0 + r] = make_double2(dp, hp);
+    }
+  }
+  // X[8j+6] = ad + bd XL + gd X - hd x_branch; back pass to the group's first row
+  const double ad = dp, hd = hp, bd = lp, gd = -cp;
+  rAC[q0 + 6] = make_double2(bd, gd);
+  rDH[q0 + 6] = make_double2(ad, hd);
+  double al = ad, et = hd, be = bd, ga = gd;
+#pragma unroll 1
+  for (int r = 5; r >= 0; r--) {
+    const double2 lc = rAC[q0 + r], dh = rDH[q0 + r];
+    al = fma(-lc.y, al, dh.x);
+    et = fma(-lc.y, et, dh.y);
+    be = fma(-lc.y, be, lc.x);
+    ga = -lc.y * ga;
+    rAC[q0 + r] = make_double2(be, ga);
+    rDH[q0 + r] = make_double2(al, et);
+  }
+  // the group-end row, with the next group's first-row form
+  double A, Bv, C, D, H;
+  {
+    const double2 ac = rAC[q0 + 7], dh = rDH[q0 + 7];
+    const double aun = __shfl_down_sync(FULL, al, 1), etn = __shfl_down_sync(FULL, et, 1);
+    const double bun = __shfl_down_sync(FULL, be, 1), gun = __shfl_down_sync(FULL, ga, 1);
+    A = ac.x * bd;
+    Bv = fma(ac.y, bun, fma(ac.x, gd, rB[q0 + 7]));
+    C = ac.y * gun;  // row 255 ends a leg or is idle: C = 0 there
+    D = fma(-ac.y, aun, fma(-ac.x, ad, dh.x));
+    H = fma(-ac.y, etn, fma(-ac.x, hd, dh.y));
+  }
+  double iB = drcp(Bv);
+#pragma unroll 1
+  for (int d = 1; d < 32; d <<= 1) {
+    const double Am = __shfl_up_sync(FULL, A, d), Cm = __shfl_up_sync(FULL, C, d);
+    const double Dm = __shfl_up_sync(FULL, D, d), Hm = __shfl_up_sync(FULL, H, d);
+    const double im = __shfl_up_sync(FULL, iB, d);
+    const double Ap = __shfl_down_sync(FULL, A, d), Cq = __shfl_down_sync(FULL, C, d);
+    const double Dq = __shfl_down_sync(FULL, D, d), Hq = __shfl_down_sync(FULL, H, d);
+    const double ip = __shfl_down_sync(FULL, iB, d);
+    // rows closer than d to an end have no coupling that far (A or C is 0)
+    const double k1 = lane >= d ? A * im : 0.0, k2 = lane + d < 32 ? C * ip : 0.0;
+    A = -k1 * Am;
+    C = -k2 * Cq;
+    Bv = fma(-k2, Ap, fma(-k1, Cm, Bv));
+    D = fma(-k2, Dq, fma(-k1, Dm, D));
+    H = fma(-k2, Hq, fma(-k1, Hm, H));
+    iB = drcp(Bv);
+  }
+  phi = min(phi, __double2hiint(Bv) & 0x7fffffff);
+  const double P2 = D * iB, Q2 = H * iB;
+  double PL = __shfl_up_sync(FULL, P2, 1), QL = __shfl_up_sync(FULL, Q2, 1);
+  if (lane == 0) PL = QL = 0.0;  // row 0 starts a leg: its be is 0
+#pragma unroll 1
+  for (int r = 0; r < 7; r++) {
+    const double2 lc = rAC[q0 + r], dh = rDH[q0 + r];
+    sP[q0 + r] = fma(lc.y, P2, fma(lc.x, PL, dh.x));
+    sQ[q0 + r] = fma(lc.y, Q2, fma(lc.x, QL, dh.y));
+  }
+  sP[q0 + 7] = P2;
+  sQ[q0 + 7] = Q2;
+}
+
 #ifndef TMG_LEGK_XMB
 #define TMG_LEGK_XMB 1  // 0: split pairs exchange through a full cluster barrier
 #endif
@@ -785,6 +895,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
         D = fma(-ce, fu.x, D);
       }
     }
+#if TMG_LEGK_RED2
+#define LEGK_SP(t) sP2[ridx(t)]
+#define LEGK_SQ(t) sQ2[ridx(t)]
+    constexpr int LTP = LT + LT / 8;  // padded rows
+    double2* r2AC = reinterpret_cast<double2*>(Ls + 3 * LT);
+    double2* r2DH = r2AC + LTP;
+    double* r2B = reinterpret_cast<double*>(r2DH + LTP);
+    double* sP2 = r2B + LTP;
+    double* sQ2 = sP2 + LTP;
+    static_assert(3 * LT + 7 * LTP + LT <= kLegArrU, "reduced-system scratch");
+    const int rq = ridx(tid);
+    r2AC[rq] = make_double2(A, C);
+    r2DH[rq] = make_double2(D, H);
+    r2B[rq] = Bv;
+    __syncthreads();
+    if ((tid >> 5) == 2) red2_solve(r2AC, r2DH, r2B, sP2, sQ2, phi);
+    __syncthreads();
+    LEGK_MARK(4);
+    const double P = sP2[rq], Qh = sQ2[rq];
+#else
+#define LEGK_SP(t) sP[t]
+#define LEGK_SQ(t) sQ[t]
     double iB = drcp(Bv);
     // parallel cyclic reduction, double-buffered (one barrier per step).  A row
     // whose partner at distance d lies outside the CTA has no coupling that far
@@ -815,6 +947,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     const double P = D * iB, Qh = H * iB;
     sP[tid] = P;
     sQ[tid] = Qh;
+#endif
 #if TMG_LEGK_XMB
     if (split && hubthr) {
       // the leg end of this CTA's half of a split block goes straight into the
@@ -824,7 +957,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
       st_cluster_v2(mapa_u32(xch + 2 * par, rank ^ 1), P, Qh);
       mbar_arrive_remote(mapa_u32(xbar, rank ^ 1));
     }
+#if !TMG_LEGK_RED2
     __syncthreads();
+#endif
 #else
     if (split) {
       // the leg end of each CTA's half of a split block goes to the peer
@@ -887,8 +1022,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
         const int ty = B.t0[1] + nch - 1;
         px = P;
         qx = Qh;
-        py = sP[ty];
-        qy = sQ[ty];
+        py = LEGK_SP(ty);
+        qy = LEGK_SQ(ty);
       }
       const double den = den0 - cx * qx - cy * qy;
       bad |= bad_pivot(den);
@@ -904,7 +1039,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
     if (act) {
       const double xb = sX[slot];
       const double X = fma(-Qh, xb, P);
-      const double XL = first ? 0.0 : fma(-sQ[tid - 1], xb, sP[tid - 1]);
+      const double XL = first ? 0.0 : fma(-LEGK_SQ(tid - 1), xb, LEGK_SP(tid - 1));
       if (g.dir > 0)
         chunk_store<1>(pF, sb, ga, XL, X);
       else
