@@ -227,6 +227,9 @@ __device__ __forceinline__ void bulk_wait_all() {
 #ifndef TMG_LEGK_L2PF
 #define TMG_LEGK_L2PF 1  // 1: warp 0 prefetches the next item's runs into L2 while this one is solved
 #endif
+#ifndef TMG_LEGK_BLOBPF
+#define TMG_LEGK_BLOBPF 0  // 1: L2 prefetch of the CTA's descriptor blobs at kernel start (measured: no gain)
+#endif
 #ifndef TMG_LEGK_STAGGER
 #define TMG_LEGK_STAGGER 0  // > 0: odd clusters start late by this many units of 1024 ns
 #endif
@@ -653,6 +656,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LT, 2)
   cluster_wait();
 #else
   __syncthreads();
+#endif
+#if TMG_LEGK_BLOBPF
+  // this CTA's descriptor blobs (static plan data) start toward L2 while the
+  // previous kernel drains: the per-item blob fetches then hit L2
+  if (tid < 32) {
+    for (int s2 = tid;; s2 += 32) {
+      const int ci = cid + s2 * ncl;
+      if (ci >= a.nsched) break;
+      const int4 e = a.bsched[ci];
+      const int off = rank ? e.z : e.x, nb = rank ? e.w : e.y;
+      if (nb > 0) bulk_prefetch_l2(a.blob + (size_t)off * 16, (unsigned)nb);
+    }
+  }
 #endif
   pdl_wait();  // the fields of the previous kernel are complete from here on
 #if TMG_LEGK_STAGGER
@@ -1162,6 +1178,16 @@ struct HostBlock {
 };
 
 inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+// thread slots a leg of `chunks` chunks takes in an item (TMG_LEGK_WALIGN:
+// legs of a warp or more are padded to whole warps)
+inline int leg_slots(int chunks) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("TMG_LEGK_WALIGN");
+    on = e ? std::atoi(e) != 0 : 0;  // measured: 0.660 -> 0.670 ms (the padding costs more items)
+  }
+  return on && chunks >= 32 ? (chunks + 31) & ~31 : chunks;
+}
 
 }  // namespace
 
@@ -1244,6 +1270,10 @@ std::string build_leg_plan(int n, LegPlan& P, int kmin, int kmax) {
           // y-legs of the LL / UL shell c)
           const int only = split == 1 ? 0 : split == 2 ? 1 : split >= 3 ? (split >= 5 ? 1 : 0) : -1;
           if (only >= 0 && leg != only) continue;
+          // a leg of a warp or more starts on a warp boundary: no warp then
+          // holds chunks of two legs running in opposite directions (each
+          // direction is its own instantiation of the chunk passes)
+          if (leg_slots(33) == 64 && hb.chunks >= 32) t = (t + 31) & ~31;
           lb.t0[leg] = (int16_t)t;
           for (int c = 0; c < hb.chunks; c++) map[t + c] = (uint16_t)((bi << 1) | leg);
           t += hb.chunks;
@@ -1390,9 +1420,9 @@ std::string build_leg_plan(int n, LegPlan& P, int kmin, int kmax) {
       // first fit (blocks arrive in decreasing size)
       bool placed = false;
       for (Open& o : open) {
-        if (o.chunks + 2 * hb.chunks <= LT && (int)o.members.size() < kLegMaxBlocks) {
+        if (o.chunks + 2 * leg_slots(hb.chunks) <= LT && (int)o.members.size() < kLegMaxBlocks) {
           o.members.push_back({hb, 0});
-          o.chunks += 2 * hb.chunks;
+          o.chunks += 2 * leg_slots(hb.chunks);
           placed = true;
           break;
         }
@@ -1400,7 +1430,7 @@ std::string build_leg_plan(int n, LegPlan& P, int kmin, int kmax) {
       if (!placed) {
         Open o;
         o.members.push_back({hb, 0});
-        o.chunks = 2 * hb.chunks;
+        o.chunks = 2 * leg_slots(hb.chunks);
         open.push_back(o);
       }
     }
