@@ -268,6 +268,24 @@ int tmg_cube_scatter(tmg_cube* h, int level, int which, const long long* off, lo
 /* finest-level max |f - L u| over groups [g0, g1) + pivot flag; synchronizes */
 int tmg_cube_norm_part(tmg_cube* h, int g0, int g1, double* out_host, void* stream);
 
+/* ---- line-solver API (tweedmg.tridiag.thomas / circulant_thomas /
+ *      m_legged_thomas, tridiag.py:30-125): HOST arrays, one system per call,
+ *      solved on the device in the reference's operation order (results
+ *      bit-identical to the reference's numpy code); synchronizes.
+ *      TMG_SINGULAR on a vanishing pivot (tridiag.py:23-27), TMG_BADARG on
+ *      m < 3 (circulant) / fewer than 2 legs (tridiag.py:56-57, 100-101).
+ *      a, b, c, r, x: length m (thomas, circulant; wraparound entries a[0],
+ *      c[m-1] as in the reference).  legged: nleg legs packed back to back,
+ *      leg k at [offs[k], offs[k+1]) ordered tip -> branch, c at a leg's last
+ *      entry couples it to the branch, d[k] the branch row's coupling. */
+int tmg_thomas(long m, const double* a, const double* b, const double* c, const double* r,
+               double* x, void* stream);
+int tmg_circulant_thomas(long m, const double* a, const double* b, const double* c,
+                         const double* r, double* x, void* stream);
+int tmg_legged_thomas(long nleg, const long* offs, const double* a, const double* b,
+                      const double* c, const double* r, const double* d, double d_centre,
+                      double r_centre, double* x, double* x_branch, void* stream);
+
 /* ---- profiling aid: average per-CTA cycles between the phase marks of the
  *      block-solver kernel (gather, elimination, reduced solve, hub, finalize,
  *      scatter) over the last launch; non-zero only in builds made with

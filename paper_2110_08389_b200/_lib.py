@@ -111,6 +111,9 @@ def _declare(L):
         "tmg_relax_chain": ([lp, vp, vp, ip, ip, vp, vp, vp, vp, vp, vp, vp], ip),
         "tmg_relax_ring": ([lp, vp, vp, ip, ip, vp, vp, vp, vp, vp, vp, vp], ip),
         "tmg_relax_legged": ([lp, vp, vp, lp, vp, lp, lp, ip, ip, vp, vp, vp, vp, vp, vp, vp], ip),
+        "tmg_thomas": ([lp, vp, vp, vp, vp, vp, vp], ip),
+        "tmg_circulant_thomas": ([lp, vp, vp, vp, vp, vp, vp], ip),
+        "tmg_legged_thomas": ([lp, vp, vp, vp, vp, vp, vp, dp, dp, vp, vp, vp], ip),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -1581,4 +1581,212 @@ int tmg_relax_legged(long n, const int64_t* ii, const int64_t* jj, long m, const
   });
 }
 
+
+// ---- line-solver API (tridiag.py:30-125) ------------------------------------
+// The reference's three direct solvers on host arrays, executed on the device
+// in the reference's operation order (separate multiply / subtract / divide,
+// round to nearest: bit-identical to numpy).  One system per call: these are
+// the reference's specification functions, not a hot path.
+}  // extern "C"
+
+namespace {
+
+__device__ __forceinline__ bool tri_bad(double p) { return fabs(p) < 1e-300; }
+
+// forward elimination of one leg / chain (tridiag.py:35-38); returns false at
+// the first vanishing pivot among bb[0 .. m-2]
+__device__ bool tri_forward(long m, const double* a, const double* c, double* bb, double* rr,
+                            double* gg) {
+  for (long k = 1; k < m; k++) {
+    if (tri_bad(bb[k - 1])) return false;
+    const double w = __ddiv_rn(a[k], bb[k - 1]);
+    bb[k] = __dsub_rn(bb[k], __dmul_rn(w, c[k - 1]));
+    rr[k] = __dsub_rn(rr[k], __dmul_rn(w, rr[k - 1]));
+    if (gg) gg[k] = __dsub_rn(gg[k], __dmul_rn(w, gg[k - 1]));
+  }
+  return true;
+}
+
+__global__ void thomas_kernel(long m, const double* a, double* bb, const double* c, double* rr,
+                              double* x, int* err) {
+  if (!tri_forward(m, a, c, bb, rr, nullptr) || tri_bad(bb[m - 1])) {
+    *err = 1;
+    return;
+  }
+  x[m - 1] = __ddiv_rn(rr[m - 1], bb[m - 1]);
+  for (long k = m - 2; k >= 0; k--)
+    x[k] = __ddiv_rn(__dsub_rn(rr[k], __dmul_rn(c[k], x[k + 1])), bb[k]);
+}
+
+// tridiag.py:46-81; bb, rr hold copies of b, r (length m), gg / y / z scratch
+__global__ void circulant_kernel(long m, const double* a, const double* b, double* bb,
+                                 const double* c, const double* r, double* rr, double* gg,
+                                 double* y, double* z, double* x, int* err) {
+  const long mm = m - 1;
+  for (long k = 0; k < mm; k++) gg[k] = 0.0;
+  gg[0] = a[0];
+  gg[mm - 1] = __dadd_rn(gg[mm - 1], c[mm - 1]);
+  if (!tri_forward(mm, a, c, bb, rr, gg) || tri_bad(bb[mm - 1])) {
+    *err = 1;
+    return;
+  }
+  y[mm - 1] = __ddiv_rn(rr[mm - 1], bb[mm - 1]);
+  z[mm - 1] = __ddiv_rn(gg[mm - 1], bb[mm - 1]);
+  for (long k = mm - 2; k >= 0; k--) {
+    y[k] = __ddiv_rn(__dsub_rn(rr[k], __dmul_rn(c[k], y[k + 1])), bb[k]);
+    z[k] = __ddiv_rn(__dsub_rn(gg[k], __dmul_rn(c[k], z[k + 1])), bb[k]);
+  }
+  const double den = __dsub_rn(__dsub_rn(b[m - 1], __dmul_rn(c[m - 1], z[0])),
+                               __dmul_rn(a[m - 1], z[mm - 1]));
+  if (tri_bad(den)) {
+    *err = 1;
+    return;
+  }
+  const double xm = __ddiv_rn(__dsub_rn(__dsub_rn(r[m - 1], __dmul_rn(c[m - 1], y[0])),
+                                        __dmul_rn(a[m - 1], y[mm - 1])),
+                              den);
+  for (long k = 0; k < mm; k++) x[k] = __dsub_rn(y[k], __dmul_rn(z[k], xm));
+  x[m - 1] = xm;
+}
+
+// tridiag.py:84-125: a thread per leg eliminates tip -> branch, thread 0
+// closes the branch row in leg order, every thread substitutes back
+__global__ void legged_kernel(int nleg, const long* offs, const double* a, double* bb,
+                              const double* c, double* rr, const double* d, double d_centre,
+                              double r_centre, double* x, double* xb_out, int* err) {
+  __shared__ double xb;
+  __shared__ int bad;
+  const int t = threadIdx.x;
+  if (t == 0) bad = 0;
+  __syncthreads();
+  const long o = t < nleg ? offs[t] : 0, p = t < nleg ? offs[t + 1] - o : 0;
+  if (t < nleg && (!tri_forward(p, a + o, c + o, bb + o, rr + o, nullptr) || tri_bad(bb[o + p - 1])))
+    atomicExch(&bad, 1);
+  __syncthreads();
+  if (bad) {
+    if (t == 0) *err = 1;
+    return;
+  }
+  if (t == 0) {
+    double num = r_centre, den = d_centre;
+    for (int k = 0; k < nleg; k++) {
+      const long e = offs[k + 1] - 1;
+      num = __dsub_rn(num, __ddiv_rn(__dmul_rn(d[k], rr[e]), bb[e]));
+      den = __dsub_rn(den, __ddiv_rn(__dmul_rn(d[k], c[e]), bb[e]));
+    }
+    if (tri_bad(den)) {
+      *err = 1;
+      bad = 1;
+    } else {
+      xb = __ddiv_rn(num, den);
+      *xb_out = xb;
+    }
+  }
+  __syncthreads();
+  if (bad || t >= nleg) return;
+  x[o + p - 1] = __ddiv_rn(__dsub_rn(rr[o + p - 1], __dmul_rn(c[o + p - 1], xb)), bb[o + p - 1]);
+  for (long k = p - 2; k >= 0; k--)
+    x[o + k] = __ddiv_rn(__dsub_rn(rr[o + k], __dmul_rn(c[o + k], x[o + k + 1])), bb[o + k]);
+}
+
+// device scratch of one line-solver call: `nd` doubles, the flag after them
+struct TriScratch {
+  double* d = nullptr;
+  int* err = nullptr;
+  ~TriScratch() { cudaFree(d); }
+  cudaError_t init(size_t nd) {
+    cudaError_t e = cudaMalloc(&d, nd * sizeof(double) + sizeof(int));
+    if (e != cudaSuccess) return e;
+    err = reinterpret_cast<int*>(d + nd);
+    return cudaMemset(err, 0, sizeof(int));
+  }
+};
+
+int tri_finish(TriScratch& w, cudaStream_t st, double* x_host, const double* x_dev, long n,
+               double* extra_host, const double* extra_dev) {
+  int flag = 0;
+  TMG_CUDA_TRY(cudaGetLastError());
+  TMG_CUDA_TRY(cudaMemcpyAsync(&flag, w.err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  TMG_CUDA_TRY(cudaMemcpyAsync(x_host, x_dev, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (extra_host)
+    TMG_CUDA_TRY(cudaMemcpyAsync(extra_host, extra_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+  TMG_CUDA_TRY(cudaStreamSynchronize(st));
+  if (flag) return fail(TMG_SINGULAR, "zero pivot during tridiagonal elimination");
+  return TMG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tmg_thomas(long m, const double* a, const double* b, const double* c, const double* r,
+               double* x, void* stream) {
+  return guarded([&]() -> int {
+    if (m < 1 || !a || !b || !c || !r || !x) return fail(TMG_BADARG, "thomas: need m >= 1 and arrays");
+    cudaStream_t st = (cudaStream_t)stream;
+    TriScratch w;
+    TMG_CUDA_TRY(w.init(5 * (size_t)m));
+    const double* src[4] = {a, b, c, r};
+    for (int q = 0; q < 4; q++)
+      TMG_CUDA_TRY(cudaMemcpyAsync(w.d + q * m, src[q], m * sizeof(double), cudaMemcpyHostToDevice, st));
+    TMG_COUNT(1);
+    thomas_kernel<<<1, 1, 0, st>>>(m, w.d, w.d + m, w.d + 2 * m, w.d + 3 * m, w.d + 4 * m, w.err);
+    return tri_finish(w, st, x, w.d + 4 * m, m, nullptr, nullptr);
+  });
+}
+
+int tmg_circulant_thomas(long m, const double* a, const double* b, const double* c,
+                         const double* r, double* x, void* stream) {
+  return guarded([&]() -> int {
+    if (m < 3) return fail(TMG_BADARG, "circulant system needs m >= 3, got " + std::to_string(m));
+    if (!a || !b || !c || !r || !x) return fail(TMG_BADARG, "circulant_thomas: null array");
+    cudaStream_t st = (cudaStream_t)stream;
+    TriScratch w;
+    TMG_CUDA_TRY(w.init(10 * (size_t)m));
+    double* D = w.d;  // a, b, c, r, bb, rr, gg, y, z, x
+    const double* src[6] = {a, b, c, r, b, r};
+    for (int q = 0; q < 6; q++)
+      TMG_CUDA_TRY(cudaMemcpyAsync(D + q * m, src[q], m * sizeof(double), cudaMemcpyHostToDevice, st));
+    TMG_COUNT(1);
+    circulant_kernel<<<1, 1, 0, st>>>(m, D, D + m, D + 4 * m, D + 2 * m, D + 3 * m, D + 5 * m,
+                                      D + 6 * m, D + 7 * m, D + 8 * m, D + 9 * m, w.err);
+    return tri_finish(w, st, x, D + 9 * m, m, nullptr, nullptr);
+  });
+}
+
+int tmg_legged_thomas(long nleg, const long* offs, const double* a, const double* b,
+                      const double* c, const double* r, const double* d, double d_centre,
+                      double r_centre, double* x, double* x_branch, void* stream) {
+  return guarded([&]() -> int {
+    if (nleg < 2) return fail(TMG_BADARG, "need m >= 2 legs, got " + std::to_string(nleg));
+    if (nleg > 1024) return fail(TMG_BADARG, "legged_thomas: at most 1024 legs");
+    if (!offs || !a || !b || !c || !r || !d || !x || !x_branch)
+      return fail(TMG_BADARG, "legged_thomas: null array");
+    for (long k = 0; k < nleg; k++)
+      if (offs[k + 1] <= offs[k]) return fail(TMG_BADARG, "legged_thomas: empty leg");
+    const long n = offs[nleg] - offs[0];
+    if (offs[0] != 0) return fail(TMG_BADARG, "legged_thomas: offs[0] must be 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    TriScratch w;
+    // a, bb, c, rr, x (n each), d (nleg), x_branch, offs (as longs, 8-byte slots)
+    const size_t nd = 5 * (size_t)n + nleg + 1 + (nleg + 1);
+    TMG_CUDA_TRY(w.init(nd));
+    double* D = w.d;
+    const double* src[4] = {a, b, c, r};
+    for (int q = 0; q < 4; q++)
+      TMG_CUDA_TRY(cudaMemcpyAsync(D + q * n, src[q], n * sizeof(double), cudaMemcpyHostToDevice, st));
+    double* dd = D + 5 * n;
+    double* xb = dd + nleg;
+    long* doffs = reinterpret_cast<long*>(xb + 1);
+    static_assert(sizeof(long) == sizeof(double), "offsets share the scratch");
+    TMG_CUDA_TRY(cudaMemcpyAsync(dd, d, nleg * sizeof(double), cudaMemcpyHostToDevice, st));
+    TMG_CUDA_TRY(cudaMemcpyAsync(doffs, offs, (nleg + 1) * sizeof(long), cudaMemcpyHostToDevice, st));
+    TMG_COUNT(1);
+    const int threads = (int)((nleg + 31) / 32 * 32);
+    legged_kernel<<<1, threads, 0, st>>>((int)nleg, doffs, D, D + n, D + 2 * n, D + 3 * n, dd,
+                                         d_centre, r_centre, D + 4 * n, xb, w.err);
+    return tri_finish(w, st, x, D + 4 * n, n, x_branch, xb);
+  });
+}
+
 }  // extern "C"

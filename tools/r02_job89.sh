@@ -1,0 +1,6 @@
+# final verification of round 2: GPU suite, smoke, every bench line, V-cycle launch list
+mkdir -p gpurun_out
+timeout 1800 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/verify_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/verify_pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/verify_smoke.log 2>&1
+bash tools/r02_benchall.sh
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/r02_vcycle_launches.csv python tools/vcycle_once.py > gpurun_out/r02_vcycle_ncu.log 2>&1
