@@ -411,8 +411,8 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_unit": "GB per launch set",
                      "traffic_source": traffic_src,
-                     "kernel": ("leg_sweep_kernel (one finest-level sweep, both colours; the "
-                                "four corner points on block_sweep_kernel)" if kind == 4 else
+                     "kernel": ("leg_sweep_kernel (one finest-level sweep, both colours: "
+                                "L-shells, the central cross, the corner points)" if kind == 4 else
                                 "block_sweep_kernel (one finest-level sweep, both colours)"),
                      "alg_bytes": alg_bytes, "ms": sweep_ms, "peak_kind": peak_kind},
         "sweep_updates_per_s": n_int / (sweep_ms * 1e-3),
