@@ -15,6 +15,7 @@
 
 #include "../../include/tweedmg_b200.h"
 #include "tmg_kernels.h"
+#include "tmg_minitail.h"
 #include "tmg_plan.h"
 
 using namespace tmg;
@@ -111,6 +112,7 @@ struct tmg_hier {
     TailOp* d_ops = nullptr;
     int nops = 0, ctas = 0, level = 0;
     size_t smem = 0;
+    MiniTail* mini = nullptr;  // the shared-memory tail (tmg_minitail.cu) instead of an op list
   };
   std::map<std::tuple<int, int, int, int, int>, TailProg> tails;
   unsigned* d_tail_bar = nullptr;  // grid barrier state of the tail kernel
@@ -343,7 +345,13 @@ int ensure_fields(tmg_hier* h, int mode) {
   h->graphs.clear();
   for (auto& kv : h->solve_graphs) cudaGraphExecDestroy(kv.second.first);
   h->solve_graphs.clear();
-  for (auto& kv : h->tails) cudaFree(kv.second.d_ops);
+  for (auto& kv : h->tails) {
+    cudaFree(kv.second.d_ops);
+    if (kv.second.mini) {
+      free_mini_tail(*kv.second.mini);
+      delete kv.second.mini;
+    }
+  }
   h->tails.clear();
   h->bytes = 0;
   const int L = (int)h->lv.size();
@@ -421,7 +429,52 @@ int tail_start(tmg_hier* h, int kind, int l0) {
 
 // Build (once, outside any stream capture) the op list of the tail entered
 // at level >= l0; vcycle_launches uses it when present.
+// Shared-memory tail (tmg_minitail.cu, default on; TMG_MINI=0 turns it off):
+// the levels from the coarsest up whose axes have at most TMG_MINI_NMAX
+// (default 32) intervals and whose longest chain / ring / leg has at most
+// TMG_MINI_UNIT (default 32) points run as one single-CTA launch.
+int prepare_mini_tail(tmg_hier* h, int kind, int full, int nu1, int nu2, int l0) {
+  const int L = (int)h->lv.size();
+  auto key = std::make_tuple(kind, full, nu1, nu2, l0);
+  if (h->tails.count(key) || L < 2 || env_int("TMG_MINI", 1) == 0 || transfer_v1()) return TMG_OK;
+  const int nmax = env_int("TMG_MINI_NMAX", 32), umax = env_int("TMG_MINI_UNIT", 32);
+  const std::vector<int> schemes = sub_schemes(kind);
+  int lt = L;
+  for (int l = L - 1; l >= l0; l--) {
+    tmg_level* lv = h->lv[l];
+    if (std::max(lv->nx, lv->ny) > nmax) break;
+    if (l < L - 1) {
+      const int mu = mini_max_unit(schemes, lv->nx, lv->ny);
+      if (mu < 0 || mu > umax) break;
+    }
+    lt = l;
+  }
+  if (lt > L - 2) return TMG_OK;
+  int st = factor_coarse(h->lv[L - 1]);
+  if (st) return st;
+  std::vector<MiniLevelIn> in;
+  for (int l = lt; l < L; l++) {
+    tmg_level* lv = h->lv[l];
+    in.push_back(MiniLevelIn{lv->nx, lv->ny, lv->W, lv->E, lv->S, lv->N});
+  }
+  MiniTail* mt = new MiniTail();
+  const std::string err = build_mini_tail(in, schemes, *mt);
+  if (!err.empty()) {  // the per-stage path stays
+    delete mt;
+    return TMG_OK;
+  }
+  tmg_hier::TailProg tp;
+  tp.level = lt;
+  tp.mini = mt;
+  h->tails.emplace(key, tp);
+  return TMG_OK;
+}
+
 int prepare_tail(tmg_hier* h, int kind, int full, int nu1, int nu2, int l0) {
+  {
+    int st = prepare_mini_tail(h, kind, full, nu1, nu2, l0);
+    if (st) return st;
+  }
   const int L = (int)h->lv.size();
   const int lt = tail_start(h, kind, l0);
   auto key = std::make_tuple(kind, full, nu1, nu2, l0);
@@ -560,7 +613,11 @@ int vcycle_launches(tmg_hier* h, int kind, int full, int nu1, int nu2, cudaStrea
       if (st) return st;
     }
   }
-  if (tp) {
+  if (tp && tp->mini) {
+    cudaError_t e = launch_mini_tail(*tp->mini, h->U[lt], h->F[lt], h->lv[L - 1]->d_ainv, full & 1,
+                                     nu1, nu2, h->lv[lt]->d_err, s);
+    if (e != cudaSuccess) return cuda_fail(e, "shared-memory coarse tail");
+  } else if (tp) {
     cudaError_t e = launch_tail(tp->d_ops, tp->nops, tp->ctas, tp->smem, h->d_tail_bar, s);
     if (e != cudaSuccess) return cuda_fail(e, "coarse tail");
   } else {  // coarsest level: direct solve (mgcycle.py:93-95)
@@ -918,7 +975,13 @@ int tmg_hier_destroy(tmg_hier* h) {
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.first);
   for (auto& kv : h->solve_graphs) cudaGraphExecDestroy(kv.second.first);
   cudaFree(h->d_solve);
-  for (auto& kv : h->tails) cudaFree(kv.second.d_ops);
+  for (auto& kv : h->tails) {
+    cudaFree(kv.second.d_ops);
+    if (kv.second.mini) {
+      free_mini_tail(*kv.second.mini);
+      delete kv.second.mini;
+    }
+  }
   cudaFree(h->d_tail_bar);
   for (double* p : h->blocks) cudaFree(p);
   delete h;

@@ -19,6 +19,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _run(env):
     e = dict(os.environ)
+    e["TMG_MINI"] = "0"  # the shared-memory tail (tests/test_gpu_minitail.py) would take these levels first
     e.update(env)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "tail_worker.py")],
                        env=e, capture_output=True, text=True, timeout=900)
