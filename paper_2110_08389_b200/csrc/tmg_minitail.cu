@@ -3,20 +3,23 @@
 // back up) as ONE launch of one CTA.  u and f of every tail level, the 1D
 // coefficient arrays and the block plan live in shared memory; colour stages
 // and transfers are separated by __syncthreads instead of graph nodes (a
-// per-stage launch costs ~4 us at these sizes, a stage here well under 1 us
-// of shared-memory latency).
+// per-stage launch costs ~4 us at these sizes, a stage here 1-2 us of
+// dependent shared-memory and fp64 latency).
 //
-// Smoothing follows the reference's per-block kernels statement by statement
-// (relax_points / relax_chain / relax_ring / relax_legged,
-// _ckernels.pyx:42-185: frozen right-hand side, in-block couplings added
-// back in the reference's order by a thread per member; Thomas / circulant /
-// m-legged elimination by a thread per chain, ring or leg, multiplying by
-// reciprocal pivots where the reference divides: same algorithm, results
-// within rounding, gated at 1e-12 per sweep like the block kernels).
-// Residual, full / half weighting, bilinear prolongation + correction and the
-// coarsest-level solve use the arithmetic of tmg_transfer_dev.cuh
-// (stencil.py:82-87, transfer.py:33-38, 51-53, stencil.py:129-155).
+// Smoothing is the reference's per-block algorithm (relax_points / relax_chain /
+// relax_ring / relax_legged, _ckernels.pyx:42-185) in two phases per colour
+// stage: a thread per member builds its row (diagonal, along couplings, f
+// minus the couplings to neighbours outside its block), then a thread per
+// chain / ring / leg eliminates serially with register-carried reciprocal
+// pivots; the legs of a block sit in adjacent lanes and close their branch row
+// through warp shuffles, so a stage needs two barriers.  Results agree with
+// the reference within rounding (gated at 1e-12 per sweep like the block
+// kernels).  Residual, full / half weighting, bilinear prolongation +
+// correction and the coarsest-level solve use the arithmetic of
+// tmg_transfer_dev.cuh (stencil.py:82-87, transfer.py:33-38, 51-53,
+// stencil.py:129-155) and are bit-identical to the per-stage kernels.
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 
 #include "tmg_minitail.h"
@@ -26,29 +29,35 @@ namespace tmg {
 
 namespace {
 
-constexpr int MT = 256;  // threads of the tail CTA
+#ifndef TMG_MINI_THREADS
+#define TMG_MINI_THREADS 512
+#endif
+constexpr int MT = TMG_MINI_THREADS;  // threads of the tail CTA
 
-struct MiniUnit {   // a chain, a ring, a point or one leg of a legged block
+struct MiniUnit {   // a chain, a ring, or one leg of a legged block
   uint16_t m0, cnt;  // members [m0, m0 + cnt) of the stage's member arrays
-  uint8_t kind;      // 0 point, 1 chain, 2 leg, 3 ring
-  uint8_t leg;       // leg index in its block
-  uint16_t blk;      // legged block of the stage (kind 2)
-};
-struct MiniBlk {  // a legged block: branch point and its leg units
-  uint8_t bi, bj, nleg, pad;
-  uint16_t unit0, pad2;
+  uint8_t kind;      // 1 chain, 2 leg, 3 ring, 255 padding (a block's legs share a warp)
+  uint8_t leg;       // legs: leg index (low nibble), legs of the block (high nibble)
+  uint16_t mb;       // legs: the block's branch member
 };
 struct MiniStage {  // one colour of one sub-scheme on one level
-  int unit0, nunits, blk0, nblk, mem0, nmem;
+  int unit0, nunits, mem0, nmem;
 };
-// per-member flags (the build phase runs a thread per member)
-enum : uint8_t {
-  MF_PREV = 1,       // couples to the previous member of its unit
-  MF_NEXT = 2,       // ... to the next one
-  MF_RING_FIRST = 4, // first member of a ring: previous = the ring's last member
-  MF_RING_LAST = 8,  // last member of a ring: next = the ring's first member
-  MF_LEG_LAST = 16,  // innermost point of a leg: next = the block's branch
-  MF_POINT = 32      // a point block / a one-point chain: relax_points
+struct MiniMem {  // one member: its point, i * (ny + 1) + j and its flags
+  uint8_t i, j;
+  uint16_t p, fl, pad;
+};
+// Per-member flags (the build phase runs a thread per member).  Directions:
+// 0 none, 1 W (i-1), 2 E (i+1), 3 S (j-1), 4 N (j+1).
+enum : uint16_t {
+  MF_ADIR = 7,           // bits 0-2: toward the previous member of the unit (a ring's
+                         //           first member: toward its last one)
+  MF_CDIR = 7 << 3,      // bits 3-5: toward the next member (ring last -> first, a
+                         //           leg's innermost point -> the branch)
+  MF_POINT = 1 << 6,     // a point block / a one-point chain: relax_points
+  MF_RING_FIRST = 1 << 7,
+  MF_LEG_LAST = 1 << 8,
+  MF_BRANCH = 1 << 9     // the branch of a legged block (member of no unit)
 };
 struct MiniLevel {
   int nx, ny;
@@ -61,9 +70,9 @@ struct MiniLevel {
 struct MiniArgs {
   const unsigned char* blob;
   int blob_bytes;
-  int o_lev, o_stage, o_unit, o_blk, o_mi, o_mj, o_mu, o_mf;  // byte offsets in the blob
+  int o_lev, o_stage, o_unit, o_mem;  // byte offsets in the blob
   int nlev;
-  int off_scratch, maxmem, maxblk;  // doubles, after the blob copy
+  int off_scratch, maxmem;  // doubles, after the blob copy
   FieldView U0, F0;
   const double* ainv;
   int full, nu1, nu2;
@@ -135,49 +144,47 @@ __device__ bool eliminate(int m, const double* a, double* b, const double* c, do
 }
 
 struct Scratch {
-  double *a, *b, *c, *r, *g, *y, *z, *bx;
+  double *a, *b, *c, *r, *g, *y, *z;
 };
 
-// phase A1, a thread per member: its row of _chain_system (_ckernels.pyx:54-71)
+// Phase 1, a thread per member: its row of _chain_system (_ckernels.pyx:54-71)
 // with the ring closure (:114-117) or the branch coupling (:158-161) — the
-// diagonal, the frozen right-hand side with the in-block couplings added back
-// in the reference's order, the two along couplings
-__device__ void member_build(const Lv& L, int k, const MiniUnit* units, const MiniBlk* blks,
-                             const uint8_t* mi, const uint8_t* mj, const uint16_t* mu,
-                             const uint8_t* mf, const Scratch& S) {
-  const int i = mi[k], j = mj[k];
-  const uint8_t fl = mf[k];
-  double r = frozen(L, i, j);
-  const double b = diag(L, i, j);
+// diagonal, the two along couplings and the frozen right-hand side, i.e. f
+// minus the couplings to the neighbours OUTSIDE the unit (the reference
+// subtracts all four and adds the in-block ones back; here they are left out,
+// a difference of rounding only).  Every in-block neighbour is a grid
+// neighbour, so a direction code replaces the index lookups.  Points finish
+// here (relax_points); branches leave their frozen row for the legs' warp.
+// Reads the old u only; writes u only at points.
+__device__ __forceinline__ void member_build(const Lv& L, int k, const MiniMem* mem,
+                                             const Scratch& S) {
+  const MiniMem M = mem[k];
+  const int i = M.i, j = M.j, p = M.p;
+  const unsigned fl = M.fl;
+  const double Wi = L.W[i], Ei = L.E[i], Sj = L.S[j], Nj = L.N[j];
+  const double uw = L.u[p - L.ld], ue = L.u[p + L.ld], us = L.u[p - 1], un = L.u[p + 1];
+  const double fv = L.f[p], uc = L.u[p];
+  const int ad = fl & 7, cd = (fl >> 3) & 7;
+  // couplings that stay on the right-hand side: every direction but ad / cd
+  const double mW = (ad == 1 || cd == 1) ? 0.0 : Wi, mE = (ad == 2 || cd == 2) ? 0.0 : Ei;
+  const double mS = (ad == 3 || cd == 3) ? 0.0 : Sj, mN = (ad == 4 || cd == 4) ? 0.0 : Nj;
+  const double r = (fv - fma(mE, ue, mW * uw)) - fma(mN, un, mS * us);
+  const double b = -((Wi + Ei) + (Sj + Nj));
   if (fl & MF_POINT) {  // relax_points (_ckernels.pyx:42-51)
-    S.r[k] = __ddiv_rn(r, b);
+    L.u[p] = r * drcp(b);
     return;
   }
-  const MiniUnit un = units[mu[k]];
-  double av = 0.0, cv = 0.0;
-  if (fl & MF_RING_FIRST) {  // the chain's c term first, the closure's a term after
-    cv = coupling(L, i, j, mi[k + 1], mj[k + 1]);
-    r = __dadd_rn(r, __dmul_rn(cv, L.u[mi[k + 1] * L.ld + mj[k + 1]]));
-    const int e = un.m0 + un.cnt - 1;
-    av = coupling(L, i, j, mi[e], mj[e]);
-    r = __dadd_rn(r, __dmul_rn(av, L.u[mi[e] * L.ld + mj[e]]));
-  } else {
-    if (fl & MF_PREV) {
-      av = coupling(L, i, j, mi[k - 1], mj[k - 1]);
-      r = __dadd_rn(r, __dmul_rn(av, L.u[mi[k - 1] * L.ld + mj[k - 1]]));
-    }
-    if (fl & MF_NEXT) {
-      cv = coupling(L, i, j, mi[k + 1], mj[k + 1]);
-      r = __dadd_rn(r, __dmul_rn(cv, L.u[mi[k + 1] * L.ld + mj[k + 1]]));
-    } else if (fl & MF_RING_LAST) {
-      cv = coupling(L, i, j, mi[un.m0], mj[un.m0]);
-      r = __dadd_rn(r, __dmul_rn(cv, L.u[mi[un.m0] * L.ld + mj[un.m0]]));
-    } else if (fl & MF_LEG_LAST) {
-      const MiniBlk B = blks[un.blk];
-      cv = coupling(L, i, j, B.bi, B.bj);
-      r = __dadd_rn(r, __dmul_rn(cv, L.u[B.bi * L.ld + B.bj]));
-      S.g[un.m0] = coupling(L, B.bi, B.bj, i, j);  // d[k] of the branch row
-    }
+  if (fl & MF_BRANCH) {
+    S.r[k] = r;
+    S.b[k] = b;
+    return;
+  }
+  const double av = ad == 0 ? 0.0 : ad == 1 ? Wi : ad == 2 ? Ei : ad == 3 ? Sj : Nj;
+  const double cv = cd == 0 ? 0.0 : cd == 1 ? Wi : cd == 2 ? Ei : cd == 3 ? Sj : Nj;
+  if (fl & MF_LEG_LAST) {  // d[k]: the branch row's coupling toward this point
+    const double d = cd == 1 ? L.E[i - 1] : cd == 2 ? L.W[i + 1] : cd == 3 ? L.N[j - 1] : L.S[j + 1];
+    S.g[k] = d;
+    S.y[k] = d * uc;  // the branch's frozen row subtracted this (old) value: added back
   }
   S.a[k] = av;
   S.b[k] = b;
@@ -185,94 +192,109 @@ __device__ void member_build(const Lv& L, int k, const MiniUnit* units, const Mi
   S.r[k] = r;
 }
 
-// phase A2, a thread per unit: the serial eliminations
-__device__ void unit_solve(const MiniUnit& un, const Scratch& S, int* bad) {
+// Phase 2, a thread per unit (every thread of a warp calls it: the legs of a
+// block sit in adjacent lanes and meet through shuffles): the serial
+// elimination, the branch row, the back substitution, new values into u.
+__device__ __forceinline__ void unit_run(const Lv& L, bool active, const MiniUnit& un,
+                                         const MiniMem* smem_, const Scratch& S, int* bad) {
+  const unsigned FULL = 0xffffffffu;
+  const int kind = active ? un.kind : 255;
   const int m = un.cnt;
+  const MiniMem* mm_ = smem_ + un.m0;
   double *a = S.a + un.m0, *b = S.b + un.m0, *c = S.c + un.m0, *r = S.r + un.m0;
-  if (un.kind == 0 || (un.kind == 1 && m == 1)) return;
-  if (un.kind == 1) {  // relax_chain: _thomas_inplace (_ckernels.pyx:74-103)
+  double cn = 0.0, cdn = 0.0;
+  if (kind == 1) {  // relax_chain: _thomas_inplace (_ckernels.pyx:74-103)
     if (!eliminate(m, a, b, c, r, nullptr)) *bad = 1;
     double x = r[m - 1] * b[m - 1];
-    r[m - 1] = x;
+    L.u[mm_[m - 1].p] = x;
     for (int k = m - 2; k >= 0; k--) {
       x = fma(-c[k], x, r[k]) * b[k];
-      r[k] = x;
+      L.u[mm_[k].p] = x;
     }
-    return;
-  }
-  if (un.kind == 2) {  // one leg of relax_legged (_ckernels.pyx:163-168)
+  } else if (kind == 3) {  // relax_ring (_ckernels.pyx:118-141)
+    double *g = S.g + un.m0, *y = S.y + un.m0, *z = S.z + un.m0;
+    const int mm = m - 1;
+    const double bmm = b[mm];
+    for (int k = 0; k < mm; k++) g[k] = 0.0;
+    g[0] = a[0];
+    g[mm - 1] = g[mm - 1] + c[mm - 1];
+    if (!eliminate(mm, a, b, c, r, g)) *bad = 1;
+    double yv = r[mm - 1] * b[mm - 1], zv = g[mm - 1] * b[mm - 1];
+    y[mm - 1] = yv;
+    z[mm - 1] = zv;
+    for (int k = mm - 2; k >= 0; k--) {
+      yv = fma(-c[k], yv, r[k]) * b[k];
+      zv = fma(-c[k], zv, g[k]) * b[k];
+      y[k] = yv;
+      z[k] = zv;
+    }
+    const double den = bmm - c[mm] * z[0] - a[mm] * z[mm - 1];
+    if (badp(den)) *bad = 1;
+    const double xm = (r[mm] - c[mm] * y[0] - a[mm] * y[mm - 1]) * drcp(den);
+    for (int k = 0; k < mm; k++) L.u[mm_[k].p] = fma(-z[k], xm, y[k]);
+    L.u[mm_[mm].p] = xm;
+  } else if (kind == 2) {  // one leg of relax_legged (_ckernels.pyx:163-170)
     if (!eliminate(m, a, b, c, r, nullptr)) *bad = 1;
-    return;
+    const int e = m - 1;
+    const double dib = S.g[un.m0 + e] * b[e];  // b holds the reciprocal pivots
+    cn = fma(-dib, r[e], S.y[un.m0 + e]);
+    cdn = -dib * c[e];
   }
-  // relax_ring (_ckernels.pyx:118-141)
-  double *g = S.g + un.m0, *y = S.y + un.m0, *z = S.z + un.m0;
-  const int mm = m - 1;
-  const double bmm = b[mm];
-  for (int k = 0; k < mm; k++) g[k] = 0.0;
-  g[0] = a[0];
-  g[mm - 1] = g[mm - 1] + c[mm - 1];
-  if (!eliminate(mm, a, b, c, r, g)) *bad = 1;
-  double yv = r[mm - 1] * b[mm - 1], zv = g[mm - 1] * b[mm - 1];
-  y[mm - 1] = yv;
-  z[mm - 1] = zv;
-  for (int k = mm - 2; k >= 0; k--) {
-    yv = fma(-c[k], yv, r[k]) * b[k];
-    zv = fma(-c[k], zv, g[k]) * b[k];
-    y[k] = yv;
-    z[k] = zv;
+  // the branch row (_ckernels.pyx:171-175): leg 0 gathers its block's legs
+  const int leg = un.leg & 15, nleg = un.leg >> 4;
+  double num = cn, den = cdn;
+#pragma unroll
+  for (int sft = 1; sft < 4; sft++) {
+    const double vn = __shfl_down_sync(FULL, cn, sft), vd = __shfl_down_sync(FULL, cdn, sft);
+    if (kind == 2 && leg == 0 && sft < nleg) {
+      num += vn;
+      den += vd;
+    }
   }
-  const double den = bmm - c[mm] * z[0] - a[mm] * z[mm - 1];
-  if (badp(den)) {
-    *bad = 1;
-    return;
+  double xb = 0.0;
+  if (kind == 2 && leg == 0) {
+    num += S.r[un.mb];
+    den += S.b[un.mb];
+    if (badp(den)) *bad = 1;
+    xb = num * drcp(den);
+    L.u[smem_[un.mb].p] = xb;
   }
-  const double xm = (r[mm] - c[mm] * y[0] - a[mm] * y[mm - 1]) * drcp(den);
-  for (int k = 0; k < mm; k++) r[k] = fma(-z[k], xm, y[k]);
-  r[mm] = xm;
+  const int src = (threadIdx.x & 31) - (kind == 2 ? leg : 0);
+  xb = __shfl_sync(FULL, xb, src);
+  if (kind == 2) {  // back substitution (_ckernels.pyx:176-185)
+    double xk = fma(-c[m - 1], xb, r[m - 1]) * b[m - 1];
+    L.u[mm_[m - 1].p] = xk;
+    for (int t = m - 2; t >= 0; t--) {
+      xk = fma(-c[t], xk, r[t]) * b[t];
+      L.u[mm_[t].p] = xk;
+    }
+  }
 }
 
-// phase B: the branch row of a legged block, legs in order (_ckernels.pyx:156-173)
-__device__ void block_branch(const Lv& L, const MiniBlk& B, const MiniUnit* units,
-                             const uint8_t* smi, const uint8_t* smj, const Scratch& S, int blk,
-                             int* bad) {
-  double num = frozen(L, B.bi, B.bj);
-  double den = diag(L, B.bi, B.bj);
-  for (int k = 0; k < B.nleg; k++) {
-    const MiniUnit un = units[B.unit0 + k];
-    const int e = un.m0 + un.cnt - 1;
-    const double d = S.g[un.m0];
-    num = __dadd_rn(num, __dmul_rn(d, L.u[smi[e] * L.ld + smj[e]]));
-    const double dib = d * S.b[e];  // b holds the reciprocal pivots
-    num = fma(-dib, S.r[e], num);
-    den = fma(-dib, S.c[e], den);
-  }
-  if (badp(den)) {
-    *bad = 1;
-    den = 1.0;
-  }
-  S.bx[blk] = num * drcp(den);
-}
-
-// phase C: back substitution of a leg, new values into u (_ckernels.pyx:176-185)
-__device__ void leg_store(const Lv& L, const MiniUnit& un, const MiniBlk* blks,
-                          const uint8_t* smi, const uint8_t* smj, const Scratch& S) {
-  const int m = un.cnt;
-  const uint8_t *mi = smi + un.m0, *mj = smj + un.m0;
-  const double *b = S.b + un.m0, *c = S.c + un.m0, *r = S.r + un.m0;
-  const MiniBlk B = blks[un.blk];
-  const double xb = S.bx[un.blk];
-  if (un.leg == 0) L.u[B.bi * L.ld + B.bj] = xb;
-  double xk = fma(-c[m - 1], xb, r[m - 1]) * b[m - 1];
-  L.u[mi[m - 1] * L.ld + mj[m - 1]] = xk;
-  for (int t = m - 2; t >= 0; t--) {
-    xk = fma(-c[t], xk, r[t]) * b[t];
-    L.u[mi[t] * L.ld + mj[t]] = xk;
-  }
-}
+#ifdef TMG_MINI_TIMING
+#define MINI_MARK(i)                  \
+  do {                                \
+    if (tid == 0) {                   \
+      const long long tn = clock64(); \
+      tacc[i] += tn - tlast;          \
+      tlast = tn;                     \
+    }                                 \
+  } while (0)
+#else
+#define MINI_MARK(i) \
+  do {               \
+  } while (0)
+#endif
 
 __global__ void __launch_bounds__(MT) mini_tail_kernel(MiniArgs a) {
   extern __shared__ __align__(16) unsigned char msm[];
   const int tid = threadIdx.x;
+#ifdef TMG_MINI_TIMING
+  // thread 0's clocks: prologue, entry load, build, solve (slots 4, 5 unused),
+  // residual + restriction, coarse solve, prolongation, exit store
+  long long tacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long tlast = clock64();
+#endif
   // the plan blob (static) into shared memory while the predecessor drains
   for (int i = tid; i < a.blob_bytes / 16; i += MT)
     reinterpret_cast<int4*>(msm)[i] = __ldg(reinterpret_cast<const int4*>(a.blob) + i);
@@ -280,11 +302,7 @@ __global__ void __launch_bounds__(MT) mini_tail_kernel(MiniArgs a) {
   const MiniLevel* lev = reinterpret_cast<const MiniLevel*>(msm + a.o_lev);
   const MiniStage* stages = reinterpret_cast<const MiniStage*>(msm + a.o_stage);
   const MiniUnit* units = reinterpret_cast<const MiniUnit*>(msm + a.o_unit);
-  const MiniBlk* blks = reinterpret_cast<const MiniBlk*>(msm + a.o_blk);
-  const uint8_t* smi = msm + a.o_mi;
-  const uint8_t* smj = msm + a.o_mj;
-  const uint16_t* smu = reinterpret_cast<const uint16_t*>(msm + a.o_mu);
-  const uint8_t* smf = msm + a.o_mf;
+  const MiniMem* smem_all = reinterpret_cast<const MiniMem*>(msm + a.o_mem);
   double* dsm = reinterpret_cast<double*>(msm + a.blob_bytes);
   Scratch S;
   S.a = dsm + a.off_scratch;
@@ -294,7 +312,6 @@ __global__ void __launch_bounds__(MT) mini_tail_kernel(MiniArgs a) {
   S.g = S.r + a.maxmem;
   S.y = S.g + a.maxmem;
   S.z = S.y + a.maxmem;
-  S.bx = S.z + a.maxmem;
   __shared__ int s_bad;
   if (tid == 0) s_bad = 0;
   auto level = [&](int l) {
@@ -331,6 +348,7 @@ __global__ void __launch_bounds__(MT) mini_tail_kernel(MiniArgs a) {
       }
     }
   }
+  MINI_MARK(0);
   pdl_wait();  // the restriction above (or the caller's fields) is complete
   pdl_trigger();
   {
@@ -344,27 +362,22 @@ __global__ void __launch_bounds__(MT) mini_tail_kernel(MiniArgs a) {
     }
   }
   __syncthreads();
+  MINI_MARK(1);
 
   auto sweep = [&](const Lv& L, const MiniLevel& M) {
     for (int sidx = 0; sidx < M.nstage; sidx++) {
       const MiniStage st = stages[M.stage0 + sidx];
       const MiniUnit* un = units + st.unit0;
-      const MiniBlk* bl = blks + st.blk0;
-      const uint8_t *mi = smi + st.mem0, *mj = smj + st.mem0, *mf = smf + st.mem0;
-      const uint16_t* mu = smu + st.mem0;
-      for (int k = tid; k < st.nmem; k += MT) member_build(L, k, un, bl, mi, mj, mu, mf, S);
+      const MiniMem* mem = smem_all + st.mem0;
+      for (int k = tid; k < st.nmem; k += MT) member_build(L, k, mem, S);
       __syncthreads();
-      for (int q = tid; q < st.nunits; q += MT) unit_solve(un[q], S, &s_bad);
-      if (st.nblk) {
-        __syncthreads();
-        for (int q = tid; q < st.nblk; q += MT) block_branch(L, bl[q], un, mi, mj, S, q, &s_bad);
+      MINI_MARK(2);
+      for (int q0 = 0; q0 < st.nunits; q0 += MT) {  // whole warps: the legs meet by shuffles
+        const bool active = q0 + tid < st.nunits;
+        unit_run(L, active, un[active ? q0 + tid : 0], mem, S, &s_bad);
       }
       __syncthreads();
-      for (int k = tid; k < st.nmem; k += MT)
-        if (un[mu[k]].kind != 2) L.u[mi[k] * L.ld + mj[k]] = S.r[k];
-      for (int q = tid; q < st.nunits; q += MT)
-        if (un[q].kind == 2) leg_store(L, un[q], bl, mi, mj, S);
-      __syncthreads();
+      MINI_MARK(3);
     }
   };
 
@@ -414,6 +427,7 @@ __global__ void __launch_bounds__(MT) mini_tail_kernel(MiniArgs a) {
       }
     }
     __syncthreads();
+    MINI_MARK(6);
   }
 
   // ---- coarsest level: direct solve (mgcycle.py:93-95, tmg_transfer_dev.cuh) --
@@ -446,6 +460,7 @@ __global__ void __launch_bounds__(MT) mini_tail_kernel(MiniArgs a) {
       }
     }
     __syncthreads();
+    MINI_MARK(7);
   }
 
   // ---- up: prolongation + correction, smooth (mgcycle.py:101-103) ------------
@@ -468,6 +483,7 @@ __global__ void __launch_bounds__(MT) mini_tail_kernel(MiniArgs a) {
       L.u[p] = __dadd_rn(L.u[p], pv);
     }
     __syncthreads();
+    MINI_MARK(8);
     for (int k = 0; k < a.nu2; k++) sweep(L, lev[l]);
   }
 
@@ -481,6 +497,13 @@ __global__ void __launch_bounds__(MT) mini_tail_kernel(MiniArgs a) {
     }
   }
   if (tid == 0 && s_bad) atomicOr(a.err, 1);
+#ifdef TMG_MINI_TIMING
+  MINI_MARK(9);
+  if (tid == 0)
+    printf("mini tail cycles: prologue %lld entry %lld build %lld solve %lld branch %lld store %lld "
+           "restrict %lld coarse %lld prolong %lld exit %lld\n",
+           tacc[0], tacc[1], tacc[2], tacc[3], tacc[4], tacc[5], tacc[6], tacc[7], tacc[8], tacc[9]);
+#endif
 }
 
 }  // namespace
@@ -510,10 +533,14 @@ std::string build_mini_tail(const std::vector<MiniLevelIn>& lv, const std::vecto
   std::vector<MiniLevel> levs(nlev);
   std::vector<MiniStage> stages;
   std::vector<MiniUnit> units;
-  std::vector<MiniBlk> blks;
-  std::vector<uint8_t> mi, mj, mf;
-  std::vector<uint16_t> mu;
-  int maxmem = 1, maxblk = 1, maxfield = 1, off = 0;
+  std::vector<uint8_t> mi, mj;
+  std::vector<uint16_t> mf;
+  std::vector<MiniMem> mems;  // (i, j, flags) of mi / mj / mf with the level's row stride
+  int maxmem = 1, maxfield = 1, off = 0;
+  // direction of (pi, pj) seen from (i, j), _coupling's precedence (_ckernels.pyx:21-31)
+  auto dir = [](int i, int j, int pi, int pj) {
+    return pi == i - 1 ? 1 : pi == i + 1 ? 2 : pj == j - 1 ? 3 : 4;
+  };
   for (int l = 0; l < nlev; l++) {
     MiniLevel& M = levs[l];
     std::memset(&M, 0, sizeof M);
@@ -545,125 +572,123 @@ std::string build_mini_tail(const std::vector<MiniLevelIn>& lv, const std::vecto
       for (int red = 1; red >= 0; red--) {
         MiniStage st{};
         st.unit0 = (int)units.size();
-        st.blk0 = (int)blks.size();
         st.mem0 = (int)mi.size();
+        // members [s, e) of one unit; `to` = the point its last member couples
+        // to beyond the unit (ring: its first member, leg: the branch), or -1
+        auto push_members = [&](long s, long e, int ukind, long to) {
+          for (long t = s; t < e; t++) {
+            mi.push_back((uint8_t)oi[t]);
+            mj.push_back((uint8_t)oj[t]);
+            unsigned fl = 0;
+            if (ukind == 0 || (ukind == 1 && e - s == 1)) {
+              fl = MF_POINT;
+            } else {
+              if (t > s) fl |= dir(oi[t], oj[t], oi[t - 1], oj[t - 1]);
+              if (t + 1 < e) fl |= dir(oi[t], oj[t], oi[t + 1], oj[t + 1]) << 3;
+              if (ukind == 3 && t == s)
+                fl |= MF_RING_FIRST | dir(oi[t], oj[t], oi[e - 1], oj[e - 1]);
+              if (t + 1 == e && to >= 0) fl |= dir(oi[t], oj[t], oi[to], oj[to]) << 3;
+              if (ukind == 2 && t + 1 == e) fl |= MF_LEG_LAST;
+            }
+            mf.push_back((uint16_t)fl);
+          }
+        };
         long p = 0;
         while (p < n) {
           long q = p;
           while (q < n && ob[q] == ob[p]) q++;  // members [p, q) of one block
           if ((of[p] & 1) == red) {
             const int kind = (of[p] >> 4) & 3;
-            // members [s, e) of the unit about to be pushed, with their flags
-            auto push_members = [&](long s, long e, int ukind) {
-              const int uidx = (int)units.size() - st.unit0;
-              for (long t = s; t < e; t++) {
-                mi.push_back((uint8_t)oi[t]);
-                mj.push_back((uint8_t)oj[t]);
-                mu.push_back((uint16_t)uidx);
-                uint8_t fl = 0;
-                if (ukind == 0 || (ukind == 1 && e - s == 1)) {
-                  fl = MF_POINT;
-                } else {
-                  if (t > s) fl |= MF_PREV;
-                  if (t + 1 < e) fl |= MF_NEXT;
-                  if (ukind == 3 && t == s) fl |= MF_RING_FIRST;
-                  if (ukind == 3 && t + 1 == e) fl |= MF_RING_LAST;
-                  if (ukind == 2 && t + 1 == e) fl |= MF_LEG_LAST;
-                }
-                mf.push_back(fl);
-              }
-            };
             const int m0 = (int)mi.size() - st.mem0;
-            if (kind == 0 || kind == 1 || kind == 3) {
-              // point: its one member; line: the chain; ring: the traversal
-              // (closing point last, as the reference's member order)
+            if (kind == 0 || (kind == 1 && q - p == 1)) {
+              push_members(p, q, 0, -1);  // a point: finished by the build phase
+            } else if (kind == 1 || kind == 3) {
+              // line: the chain; ring: the traversal, closing point last
               MiniUnit u{};
               u.m0 = (uint16_t)m0;
               u.cnt = (uint16_t)(q - p);
-              u.kind = (uint8_t)(kind == 3 ? 3 : kind);
-              push_members(p, q, u.kind);
+              u.kind = (uint8_t)kind;
+              push_members(p, q, kind, kind == 3 ? p : -1);
               units.push_back(u);
             } else {  // legged: legs tip -> branch, the branch last
-              MiniBlk B{};
-              B.bi = (uint8_t)oi[q - 1];
-              B.bj = (uint8_t)oj[q - 1];
-              B.unit0 = (uint16_t)((int)units.size() - st.unit0);
-              const int blk = (int)blks.size() - st.blk0;
-              long s = p;
-              int nleg = 0;
-              while (s < q - 1) {
+              std::vector<std::pair<long, long>> legs;
+              for (long s = p; s < q - 1;) {
                 long e = s;
                 while (e < q - 1 && ((of[e] >> 1) & 7) == ((of[s] >> 1) & 7)) e++;
-                MiniUnit u{};
-                u.m0 = (uint16_t)((int)mi.size() - st.mem0);
-                u.cnt = (uint16_t)(e - s);
-                u.kind = 2;
-                u.leg = (uint8_t)nleg++;
-                u.blk = (uint16_t)blk;
-                push_members(s, e, 2);
-                units.push_back(u);
+                legs.push_back({s, e});
                 s = e;
               }
-              B.nleg = (uint8_t)nleg;
-              blks.push_back(B);
+              const int nleg = (int)legs.size();
+              if (nleg < 1 || nleg > 4) return "mini tail: unsupported leg count";
+              // a block's legs sit in adjacent lanes of one warp
+              while (((int)units.size() - st.unit0) % 32 + nleg > 32) {
+                MiniUnit pad{};
+                pad.kind = 255;
+                units.push_back(pad);
+              }
+              int total = 0;
+              for (auto& le : legs) total += (int)(le.second - le.first);
+              const int mb = m0 + total;  // the branch follows the legs' members
+              for (int k = 0; k < nleg; k++) {
+                MiniUnit u{};
+                u.m0 = (uint16_t)((int)mi.size() - st.mem0);
+                u.cnt = (uint16_t)(legs[k].second - legs[k].first);
+                u.kind = 2;
+                u.leg = (uint8_t)(k | (nleg << 4));
+                u.mb = (uint16_t)mb;
+                push_members(legs[k].first, legs[k].second, 2, q - 1);
+                units.push_back(u);
+              }
+              mi.push_back((uint8_t)oi[q - 1]);
+              mj.push_back((uint8_t)oj[q - 1]);
+              mf.push_back((uint16_t)MF_BRANCH);
             }
           }
           p = q;
         }
         st.nunits = (int)units.size() - st.unit0;
-        st.nblk = (int)blks.size() - st.blk0;
         st.nmem = (int)mi.size() - st.mem0;
+        for (size_t t = mems.size(); t < mi.size(); t++) {
+          MiniMem mm{};
+          mm.i = mi[t];
+          mm.j = mj[t];
+          mm.p = (uint16_t)(mi[t] * (M.ny + 1) + mj[t]);
+          mm.fl = mf[t];
+          mems.push_back(mm);
+        }
         if (st.nmem > 65535) return "mini tail stage too large";
         maxmem = std::max(maxmem, st.nmem);
-        maxblk = std::max(maxblk, st.nblk);
         stages.push_back(st);
       }
     }
     M.nstage = (int)stages.size() - M.stage0;
   }
   // scratch: seven member arrays (also the defect of a whole field and the
-  // coarse right-hand side) and the branch values
+  // coarse right-hand side)
   maxmem = std::max(maxmem, (maxfield + 6) / 7 + 1);
   maxmem = (maxmem + 1) & ~1;
   out.off_scratch = off;
   out.maxmem = maxmem;
-  out.maxblk = maxblk;
-  off += 7 * maxmem + maxblk + 2;
-  // the blob
+  off += 7 * maxmem + 2;
   auto align16 = [](size_t v) { return (v + 15) & ~(size_t)15; };
   std::vector<unsigned char> blob;
   auto put = [&](const void* p, size_t nb) {
     const size_t o = blob.size();
     blob.resize(align16(o + nb), 0);
     if (nb) std::memcpy(blob.data() + o, p, nb);
-    return o;
+    return (int)o;
   };
-  const size_t o_lev = put(levs.data(), levs.size() * sizeof(MiniLevel));
-  const size_t o_stage = put(stages.data(), stages.size() * sizeof(MiniStage));
-  const size_t o_unit = put(units.data(), units.size() * sizeof(MiniUnit));
-  const size_t o_blk = put(blks.data(), blks.size() * sizeof(MiniBlk));
-  const size_t o_mi = put(mi.data(), mi.size());
-  const size_t o_mj = put(mj.data(), mj.size());
-  const size_t o_mu = put(mu.data(), mu.size() * sizeof(uint16_t));
-  const size_t o_mf = put(mf.data(), mf.size());
-  out.o_mu = (int)o_mu;
-  out.o_mf = (int)o_mf;
+  out.o_lev = put(levs.data(), levs.size() * sizeof(MiniLevel));
+  out.o_stage = put(stages.data(), stages.size() * sizeof(MiniStage));
+  out.o_unit = put(units.data(), units.size() * sizeof(MiniUnit));
+  out.o_mem = put(mems.data(), mems.size() * sizeof(MiniMem));
+  out.blob_bytes = (int)blob.size();
   out.smem = blob.size() + (size_t)off * sizeof(double);
   if (out.smem > 200 * 1024) return "mini tail does not fit shared memory";
   if (cudaMalloc(&out.d_blob, blob.size()) != cudaSuccess ||
       cudaMemcpy(out.d_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice) != cudaSuccess)
     return "mini tail upload failed";
   out.nlev = nlev;
-  // offsets are kept as fake pointers relative to the blob
-  out.d_lev = reinterpret_cast<const void*>(o_lev);
-  out.d_stage = reinterpret_cast<const void*>(o_stage);
-  out.d_unit = reinterpret_cast<const void*>(o_unit);
-  out.d_blk = reinterpret_cast<const void*>(o_blk);
-  out.d_mi = reinterpret_cast<const unsigned char*>(o_mi);
-  out.d_mj = reinterpret_cast<const unsigned char*>(o_mj);
-  // blob size rides in maxblk's neighbour: store it in smem - scratch layout
-  out.maxblk = maxblk;
-  out.smem = blob.size() + (size_t)off * sizeof(double);
   return "";
 }
 
@@ -684,20 +709,14 @@ cudaError_t launch_mini_tail(const MiniTail& t, const FieldView& U0, const Field
   }
   MiniArgs a{};
   a.blob = static_cast<const unsigned char*>(t.d_blob);
-  a.o_lev = (int)reinterpret_cast<size_t>(t.d_lev);
-  a.o_stage = (int)reinterpret_cast<size_t>(t.d_stage);
-  a.o_unit = (int)reinterpret_cast<size_t>(t.d_unit);
-  a.o_blk = (int)reinterpret_cast<size_t>(t.d_blk);
-  a.o_mi = (int)reinterpret_cast<size_t>(t.d_mi);
-  a.o_mj = (int)reinterpret_cast<size_t>(t.d_mj);
-  a.o_mu = t.o_mu;
-  a.o_mf = t.o_mf;
+  a.blob_bytes = t.blob_bytes;
+  a.o_lev = t.o_lev;
+  a.o_stage = t.o_stage;
+  a.o_unit = t.o_unit;
+  a.o_mem = t.o_mem;
   a.nlev = t.nlev;
   a.off_scratch = t.off_scratch;
   a.maxmem = t.maxmem;
-  a.maxblk = t.maxblk;
-  const size_t doubles = (size_t)t.off_scratch + 7 * (size_t)t.maxmem + t.maxblk + 2;
-  a.blob_bytes = (int)(t.smem - doubles * sizeof(double));
   a.U0 = U0;
   a.F0 = F0;
   a.ainv = ainv;

@@ -21,15 +21,10 @@ struct MiniTail {
   void* d_blob = nullptr;  // every plan array, one allocation
   size_t smem = 0;         // dynamic shared memory of the launch
   int nlev = 0;
-  // device pointers into d_blob
-  const void* d_lev = nullptr;
-  const void* d_stage = nullptr;
-  const void* d_unit = nullptr;
-  const void* d_blk = nullptr;
-  const unsigned char* d_mi = nullptr;
-  const unsigned char* d_mj = nullptr;
-  int off_scratch = 0, maxmem = 0, maxblk = 0;
-  int o_mu = 0, o_mf = 0;  // blob offsets of the per-member unit index / flags
+  int blob_bytes = 0;
+  // byte offsets of the plan tables in the blob
+  int o_lev = 0, o_stage = 0, o_unit = 0, o_mem = 0;
+  int off_scratch = 0, maxmem = 0;  // doubles, after the blob's copy in shared memory
 };
 
 // largest smoothing block (members solved by one thread: a leg, a chain, a
