@@ -213,7 +213,10 @@ __global__ void __launch_bounds__(256) restrict2_kernel(GridArgs g, int full, Fi
 // compile-time offset from one per-thread base (restrict2_kernel spends most
 // of its issue slots on per-element index division).  Same arithmetic, bit
 // for bit.
-__global__ void __launch_bounds__(256, 4) restrict3_kernel(GridArgs g, int full, FieldView U,
+#ifndef TMG_RESTRICT_MINB
+#define TMG_RESTRICT_MINB 4
+#endif
+__global__ void __launch_bounds__(256, TMG_RESTRICT_MINB) restrict3_kernel(GridArgs g, int full, FieldView U,
                                                            FieldView F, FieldView FC,
                                                            FieldView UC, int zero_uc,
                                                            GroupSel2 csel) {
@@ -225,7 +228,11 @@ __global__ void __launch_bounds__(256, 4) restrict3_kernel(GridArgs g, int full,
 }
 
 // ---- fused prolongation + correction: 32 x 32 fine points per CTA --------
-__global__ void __launch_bounds__(256) prolong2_kernel(int nx, int ny, FieldView C, FieldView U,
+#ifndef TMG_PROLONG_MINB
+#define TMG_PROLONG_MINB 6  // resident CTAs per SM the register allocation aims at (40 registers:
+                            // 326 -> 254 us at 8193^2, the kernel is bound by loads in flight)
+#endif
+__global__ void __launch_bounds__(256, TMG_PROLONG_MINB) prolong2_kernel(int nx, int ny, FieldView C, FieldView U,
                                                        GroupSel2 fsel) {
   __shared__ double sc[PC_E * PC_LD];
   prolong2_tile(nx, ny, C, U, fsel, 1 + blockIdx.y * NT, 1 + blockIdx.x * NT, sc);

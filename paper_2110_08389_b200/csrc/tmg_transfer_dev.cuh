@@ -286,6 +286,43 @@ __device__ __forceinline__ void prolong2_tile(int nx, int ny, const FieldView& C
   pdl_trigger();
   const int cown = box_owner(C, Ic0, Jc0, PC_E, PC_E);
   pdl_wait();
+#ifndef TMG_PROLONG_FAST
+#define TMG_PROLONG_FAST 1  // 0: every tile takes the generic per-point path
+#endif
+  if (TMG_PROLONG_FAST && fsel.g0 <= 0 && own >= 0 && cown >= 0 && i0 + NT <= nx &&
+      j0 + NT <= ny) {
+    // Interior tile owned by one buffer, coarse box by one buffer (nearly every
+    // tile of a large level): one base pointer and a row stride, and — the tile
+    // origin being odd — a thread's four points (rows w, w + 8, ...) share
+    // their parity class and walk the coarse tile with a fixed step.  Same
+    // expressions as the generic path below (transfer.py:51-53, bit-identical).
+    const bool T = own == 1;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t ldr = T ? nx + 1 : ny + 1, l8 = 8 * ldr;
+    double* up = (T ? U.t : U.n) + ((T ? j0 : i0) + w) * ldr + (T ? i0 : j0) + lane;
+    double uv[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) uv[q] = up[q * l8];
+    load_box<PC_E, PC_LD>(C, cown, Ic0, Jc0, sc);
+    __syncthreads();
+    const int cI = cown == 1 ? 1 : PC_LD, cJ = cown == 1 ? PC_LD : 1;
+    const int di = T ? lane : w, dj = T ? w : lane;  // i - i0, j - j0 of the first point
+    const bool i_even = di & 1, j_even = dj & 1;      // i0, j0 are odd
+    int o = ((1 + di) >> 1) * cI + ((1 + dj) >> 1) * cJ;
+    const int step = 4 * (T ? cJ : cI);  // eight fine rows = four coarse rows
+#pragma unroll
+    for (int q = 0; q < 4; q++, o += step) {
+      double pv;
+      if (i_even && j_even) pv = sc[o];
+      else if (i_even) pv = __dmul_rn(0.5, __dadd_rn(sc[o], sc[o + cJ]));
+      else if (j_even) pv = __dmul_rn(0.5, __dadd_rn(sc[o], sc[o + cI]));
+      else
+        pv = __dmul_rn(0.25, __dadd_rn(__dadd_rn(__dadd_rn(sc[o], sc[o + cI]), sc[o + cJ]),
+                                       sc[o + cI + cJ]));
+      up[q * l8] = __dadd_rn(uv[q], pv);
+    }
+    return;
+  }
   double uv[4];
   int pi[4], pj[4];
 #pragma unroll

@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+J=j105
+for v in main rb3 rb5 rb6 main rb5; do
+  if [ $v = main ]; then L=paper_2110_08389_b200/libtmg_b200.so; else L=paper_2110_08389_b200/libtmg_b200_$v.so; fi
+  echo "== $v" >> gpurun_out/${J}_ab.log
+  TMG_LIB_PATH=$L timeout 300 python tools/transfer_time.py >> gpurun_out/${J}_ab.log 2>&1
+done
