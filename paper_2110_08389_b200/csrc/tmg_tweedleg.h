@@ -25,7 +25,7 @@ constexpr int kLegArrU = kLegHead + kLegThreads * kLegQ + 4 * kLegMaxBlocks + 18
 constexpr int kLegArrF = kLegArrU + 2 * 16 * kLegMaxBlocks;
 constexpr int kLegStage = kLegArrF + 2 * kLegArrU;
 constexpr int kLegK0 = 2;      // smallest shell the kernel takes (at 2 it takes the corners too)
-constexpr int kLegNmin = 512;  // smallest grid (n) the kernel runs on
+constexpr int kLegNmin = 1024;  // smallest grid (n) the kernel runs on (512: V-cycle +0.8 %)
 
 struct LegItem {  // one CTA's work of one cluster iteration
   int32_t blk0;   // first LegBlock

@@ -191,7 +191,7 @@ def test_sharded_solve_native(orc, cuda, tmp_path, kind, n, world):
                          [("tweed", 600), ("tweed", 1026)])
 def test_partial_sweeps_native(orc, cuda, kind, n):
     """Colour stages over group ranges on the device equal the oracle's
-    partial stages; the ranges together equal one full sweep.  At n >= 512
+    partial stages; the ranges together equal one full sweep.  At n >= 1024
     the tweed ranges run their L-shells (and, in the last range, the cross)
     on the leg kernel."""
     import torch
