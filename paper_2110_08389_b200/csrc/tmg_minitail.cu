@@ -25,6 +25,22 @@
 #include "tmg_minitail.h"
 #include "tmg_plan.h"
 
+// -DTMG_CHECK (make check): device-side bounds checks of every member, unit
+// and scratch index of the tail (the sanitizer stand-in)
+#ifdef TMG_CHECK
+#define MINI_CHECK(cond, what)                                                  \
+  do {                                                                          \
+    if (!(cond)) {                                                              \
+      printf("mini tail check failed: %s (thread %d)\n", what, (int)threadIdx.x); \
+      __trap();                                                                 \
+    }                                                                           \
+  } while (0)
+#else
+#define MINI_CHECK(cond, what) \
+  do {                         \
+  } while (0)
+#endif
+
 namespace tmg {
 
 namespace {
@@ -80,7 +96,7 @@ struct MiniArgs {
 };
 
 struct Lv {
-  int nx, ny, ld;
+  int nx, ny, ld, cap;  // cap: scratch entries per member array (TMG_CHECK)
   double *u, *f;
   const double *W, *E, *S, *N;
 };
@@ -161,6 +177,8 @@ __device__ __forceinline__ void member_build(const Lv& L, int k, const MiniMem* 
   const MiniMem M = mem[k];
   const int i = M.i, j = M.j, p = M.p;
   const unsigned fl = M.fl;
+  MINI_CHECK(k >= 0 && k < L.cap, "member scratch slot");
+  MINI_CHECK(i > 0 && j > 0 && i < L.nx && j < L.ny && p == i * L.ld + j, "member point");
   const double Wi = L.W[i], Ei = L.E[i], Sj = L.S[j], Nj = L.N[j];
   const double uw = L.u[p - L.ld], ue = L.u[p + L.ld], us = L.u[p - 1], un = L.u[p + 1];
   const double fv = L.f[p], uc = L.u[p];
@@ -201,6 +219,12 @@ __device__ __forceinline__ void unit_run(const Lv& L, bool active, const MiniUni
   const int kind = active ? un.kind : 255;
   const int m = un.cnt;
   const MiniMem* mm_ = smem_ + un.m0;
+  MINI_CHECK(!active || un.kind == 255 || (un.cnt >= 1 && un.m0 + un.cnt <= L.cap), "unit range");
+  MINI_CHECK(!active || un.kind != 2 ||
+                 (un.mb < L.cap && (smem_[un.mb].fl & MF_BRANCH) &&
+                  (int)(threadIdx.x & 31) - (un.leg & 15) >= 0 &&
+                  (int)(threadIdx.x & 31) - (un.leg & 15) + (un.leg >> 4) <= 32),
+             "leg block in one warp");
   double *a = S.a + un.m0, *b = S.b + un.m0, *c = S.c + un.m0, *r = S.r + un.m0;
   double cn = 0.0, cdn = 0.0;
   if (kind == 1) {  // relax_chain: _thomas_inplace (_ckernels.pyx:74-103)
@@ -320,6 +344,7 @@ __global__ void __launch_bounds__(MT) mini_tail_kernel(MiniArgs a) {
     L.nx = M.nx;
     L.ny = M.ny;
     L.ld = M.ny + 1;
+    L.cap = a.maxmem;
     L.u = dsm + M.off_u;
     L.f = dsm + M.off_f;
     L.W = dsm + M.off_w;

@@ -19,3 +19,7 @@ echo "== legk_worker small (NMIN=16, K0=3)" >> $O
 TMG_LEGK_NMIN=16 TMG_LEGK_K0=3 timeout 600 python tests/legk_worker.py small >> $O 2>&1; echo "rc=$?" >> $O
 echo "== pytest gpu parity / hybrid / golden / plans (checked library)" >> $O
 timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_hybrid.py tests/test_gpu_golden.py tests/test_gpu_plans.py -q -p no:cacheprovider >> $O 2>&1; echo "rc=$?" >> $O
+echo "== minitail_worker (shared-memory coarse tail, checked library)" >> $O
+timeout 900 python tests/minitail_worker.py >> $O 2>&1; echo "rc=$?" >> $O
+echo "== minitail_worker TMG_MINI_UNIT=128" >> $O
+TMG_MINI_UNIT=128 timeout 900 python tests/minitail_worker.py >> $O 2>&1; echo "rc=$?" >> $O
