@@ -137,19 +137,36 @@ __device__ __forceinline__ double drcp(double x) {
 // multiplies by the reciprocal where the reference divides (the divisions of
 // a dependent chain cost ~10x a multiply here); b[] is left holding the
 // RECIPROCAL pivots for the back substitution.
-__device__ bool eliminate(int m, const double* a, double* b, const double* c, double* r,
-                          double* g) {
+__device__ __forceinline__ bool eliminate(int m, const double* __restrict__ a,
+                                          double* __restrict__ b, const double* __restrict__ c,
+                                          double* __restrict__ r, double* __restrict__ g) {
   double bp = b[0], rp = r[0], gp = g ? g[0] : 0.0;
   bool ok = !badp(bp);
   double ib = drcp(bp);
   b[0] = ib;
+  // the next row's entries are loaded while this row's chain runs
+  double an = 0.0, cn = c[0], bn = 0.0, rn = 0.0, gn = 0.0;
+  if (m > 1) {
+    an = a[1];
+    bn = b[1];
+    rn = r[1];
+    if (g) gn = g[1];
+  }
   for (int k = 1; k < m; k++) {
-    const double w = a[k] * ib;
-    bp = fma(-w, c[k - 1], b[k]);
-    rp = fma(-w, rp, r[k]);
+    const double ak = an, ck = cn, bk = bn, rk = rn, gk = gn;
+    if (k + 1 < m) {
+      an = a[k + 1];
+      cn = c[k];
+      bn = b[k + 1];
+      rn = r[k + 1];
+      if (g) gn = g[k + 1];
+    }
+    const double w = ak * ib;
+    bp = fma(-w, ck, bk);
+    rp = fma(-w, rp, rk);
     r[k] = rp;
     if (g) {
-      gp = fma(-w, gp, g[k]);
+      gp = fma(-w, gp, gk);
       g[k] = gp;
     }
     ok &= !badp(bp);
@@ -288,9 +305,25 @@ __device__ __forceinline__ void unit_run(const Lv& L, bool active, const MiniUni
   if (kind == 2) {  // back substitution (_ckernels.pyx:176-185)
     double xk = fma(-c[m - 1], xb, r[m - 1]) * b[m - 1];
     L.u[mm_[m - 1].p] = xk;
+    double cn = 0.0, rn = 0.0, bn = 0.0;
+    int pn = 0;
+    if (m > 1) {
+      cn = c[m - 2];
+      rn = r[m - 2];
+      bn = b[m - 2];
+      pn = mm_[m - 2].p;
+    }
     for (int t = m - 2; t >= 0; t--) {
-      xk = fma(-c[t], xk, r[t]) * b[t];
-      L.u[mm_[t].p] = xk;
+      const double ct = cn, rt = rn, bt = bn;
+      const int pt = pn;
+      if (t > 0) {
+        cn = c[t - 1];
+        rn = r[t - 1];
+        bn = b[t - 1];
+        pn = mm_[t - 1].p;
+      }
+      xk = fma(-ct, xk, rt) * bt;
+      L.u[pt] = xk;
     }
   }
 }
@@ -320,6 +353,7 @@ __global__ void __launch_bounds__(MT) mini_tail_kernel(MiniArgs a) {
   long long tlast = clock64();
 #endif
   // the plan blob (static) into shared memory while the predecessor drains
+#pragma unroll 4
   for (int i = tid; i < a.blob_bytes / 16; i += MT)
     reinterpret_cast<int4*>(msm)[i] = __ldg(reinterpret_cast<const int4*>(a.blob) + i);
   __syncthreads();
@@ -353,37 +387,57 @@ __global__ void __launch_bounds__(MT) mini_tail_kernel(MiniArgs a) {
     L.N = L.S + M.ny + 1;
     return L;
   };
-  // coefficients of every level; zero fields below the first level
-  for (int l = 0; l < a.nlev; l++) {
+  // zero fields below the first level; the coefficients, a warp per level so
+  // that the levels' global-memory latencies overlap
+  for (int l = 1; l < a.nlev; l++) {
+    const MiniLevel& M = lev[l];
+    const int np = (M.nx + 1) * (M.ny + 1);
+    for (int p = tid; p < np; p += MT) {
+      dsm[M.off_u + p] = 0.0;
+      dsm[M.off_f + p] = 0.0;
+    }
+  }
+  for (int l = tid >> 5; l < a.nlev; l += MT / 32) {
     const MiniLevel& M = lev[l];
     double* w = dsm + M.off_w;
-    for (int i = tid; i <= M.nx; i += MT) {
-      w[i] = __ldg(M.W + i);
-      w[M.nx + 1 + i] = __ldg(M.E + i);
+    const int lane = tid & 31;
+    for (int i = lane; i <= M.nx; i += 32) {
+      const double wv = __ldg(M.W + i), ev = __ldg(M.E + i);
+      w[i] = wv;
+      w[M.nx + 1 + i] = ev;
     }
-    for (int j = tid; j <= M.ny; j += MT) {
-      w[2 * (M.nx + 1) + j] = __ldg(M.S + j);
-      w[2 * (M.nx + 1) + M.ny + 1 + j] = __ldg(M.N + j);
-    }
-    if (l > 0) {
-      const int np = (M.nx + 1) * (M.ny + 1);
-      for (int p = tid; p < np; p += MT) {
-        dsm[M.off_u + p] = 0.0;
-        dsm[M.off_f + p] = 0.0;
-      }
+    for (int j = lane; j <= M.ny; j += 32) {
+      const double sv = __ldg(M.S + j), nv = __ldg(M.N + j);
+      w[2 * (M.nx + 1) + j] = sv;
+      w[2 * (M.nx + 1) + M.ny + 1 + j] = nv;
     }
   }
   MINI_MARK(0);
   pdl_wait();  // the restriction above (or the caller's fields) is complete
   pdl_trigger();
-  {
+  {  // the first tail level's u and f: three rounds of loads in flight at once
     const Lv L = level(0);
     const int np = (L.nx + 1) * (L.ny + 1);
-    for (int p = tid; p < np; p += MT) {
-      const int i = p / L.ld, j = p - i * L.ld;
-      L.u[p] = *a.U0.at(i, j);
-      const bool interior = i > 0 && j > 0 && i < L.nx && j < L.ny;
-      L.f[p] = interior ? *a.F0.at(i, j) : 0.0;
+    for (int p0 = 0; p0 < np; p0 += 3 * MT) {
+      double uv[3], fv[3];
+#pragma unroll
+      for (int q = 0; q < 3; q++) {
+        const int p = p0 + q * MT + tid;
+        uv[q] = fv[q] = 0.0;
+        if (p < np) {
+          const int i = p / L.ld, j = p - i * L.ld;
+          uv[q] = *a.U0.at(i, j);
+          if (i > 0 && j > 0 && i < L.nx && j < L.ny) fv[q] = *a.F0.at(i, j);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 3; q++) {
+        const int p = p0 + q * MT + tid;
+        if (p < np) {
+          L.u[p] = uv[q];
+          L.f[p] = fv[q];
+        }
+      }
     }
   }
   __syncthreads();
