@@ -346,9 +346,9 @@ cudaError_t launch_hdefect_restrict(const GridArgs& g, int full, const FieldView
 }
 
 cudaError_t launch_hprolong_correct(int nx, int ny, const FieldView& C, const FieldView& U,
-                                    cudaStream_t s) {
+                                    cudaStream_t s, int skip_red) {
   if (nx < 2 || ny < 2) return cudaSuccess;
-  if (!transfer_v1()) return launch_prolong2(nx, ny, C, U, s);
+  if (!transfer_v1()) return launch_prolong2(nx, ny, C, U, s, 0, 0, 0, skip_red);
   dim3 grid((ny - 1 + TILE - 1) / TILE, (nx - 1 + TILE - 1) / TILE);
   TMG_COUNT(1);
   hprolong_correct_kernel<<<grid, 256, 0, s>>>(nx, ny, C, U);

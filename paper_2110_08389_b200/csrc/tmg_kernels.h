@@ -177,8 +177,10 @@ cudaError_t launch_hdefect_restrict(const GridArgs& g, int full, const FieldView
                                     const FieldView& F, const FieldView& FC, cudaStream_t s,
                                     const FieldView* UC = nullptr, bool* uc_zeroed = nullptr);
 // u += P uc on the fine interior; (nx, ny) are the FINE dimensions
+// skip_red: only the black points of the square tweed scheme (the caller's next
+// red stage overwrites the red ones without reading them; tmg_transfer_dev.cuh)
 cudaError_t launch_hprolong_correct(int nx, int ny, const FieldView& C, const FieldView& U,
-                                    cudaStream_t s);
+                                    cudaStream_t s, int skip_red = 0);
 // second-generation versions (tmg_transfer.cu), used unless TMG_TRANSFER=v1
 cudaError_t launch_norm2(const GridArgs& g, const FieldView& U, const FieldView& F,
                          unsigned long long* dmax, cudaStream_t s, int scheme, int g0, int g1);
@@ -188,7 +190,8 @@ cudaError_t launch_restrict2(const GridArgs& g, int full, const FieldView& U, co
                              const FieldView& FC, cudaStream_t s, const FieldView* UC = nullptr,
                              int scheme = 0, int cg0 = 0, int cg1 = 0);
 cudaError_t launch_prolong2(int nx, int ny, const FieldView& C, const FieldView& U,
-                            cudaStream_t s, int scheme = 0, int fg0 = 0, int fg1 = 0);
+                            cudaStream_t s, int scheme = 0, int fg0 = 0, int fg1 = 0,
+                            int skip_red = 0);
 bool transfer_v1();
 cudaError_t launch_to_hybrid(const FieldView& V, const double* nat, cudaStream_t s);
 cudaError_t launch_from_hybrid(const FieldView& V, double* nat, cudaStream_t s);

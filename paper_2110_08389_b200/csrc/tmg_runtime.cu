@@ -630,7 +630,16 @@ int vcycle_launches(tmg_hier* h, int kind, int full, int nu1, int nu2, cudaStrea
   }
   for (int l = lt - 1; l >= l0; l--) {  // up: prolongation + correction, smooth
     tmg_level* lv = h->lv[l];
-    cudaError_t e = launch_hprolong_correct(lv->nx, lv->ny, h->U[l + 1], h->U[l], s);
+    // the post-smoothing's first red stage overwrites the red points of a square
+    // tweed level unread: the correction goes to the black ones only
+    // (TMG_PROLONG_BLACK=0: everywhere).  Hybrid layout only: its sweeps are
+    // bit-identical with and without (tools/dbg_black.py); the natural-layout
+    // gather reads in-block values it cancels later, so it keeps the full
+    // correction.
+    static const int black_only = env_int("TMG_PROLONG_BLACK", 1);
+    const int skip_red = black_only && nu2 > 0 && kind == TMG_TWEED && h->mode == LM_TWEED &&
+                         lv->nx == lv->ny && lv->nx % 2 == 0 && lv->nx >= 4;
+    cudaError_t e = launch_hprolong_correct(lv->nx, lv->ny, h->U[l + 1], h->U[l], s, skip_red);
     if (e != cudaSuccess) return cuda_fail(e, "prolong_correct");
     for (int k = 0; k < nu2; k++) {
       int st = sweep_kind(lv, kind, 3, h->U[l], h->F[l], s);

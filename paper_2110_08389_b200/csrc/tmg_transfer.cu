@@ -233,9 +233,9 @@ __global__ void __launch_bounds__(256, TMG_RESTRICT_MINB) restrict3_kernel(GridA
                             // 326 -> 254 us at 8193^2, the kernel is bound by loads in flight)
 #endif
 __global__ void __launch_bounds__(256, TMG_PROLONG_MINB) prolong2_kernel(int nx, int ny, FieldView C, FieldView U,
-                                                       GroupSel2 fsel) {
+                                                       GroupSel2 fsel, int skip_red) {
   __shared__ double sc[PC_E * PC_LD];
-  prolong2_tile(nx, ny, C, U, fsel, 1 + blockIdx.y * NT, 1 + blockIdx.x * NT, sc);
+  prolong2_tile(nx, ny, C, U, fsel, 1 + blockIdx.y * NT, 1 + blockIdx.x * NT, sc, skip_red);
 }
 
 // ---- marching residual kernels (large levels) -----------------------------
@@ -561,12 +561,12 @@ cudaError_t launch_restrict2(const GridArgs& g, int full, const FieldView& U, co
 }
 
 cudaError_t launch_prolong2(int nx, int ny, const FieldView& C, const FieldView& U,
-                            cudaStream_t s, int scheme, int fg0, int fg1) {
+                            cudaStream_t s, int scheme, int fg0, int fg1, int skip_red) {
   if (nx < 2 || ny < 2) return cudaSuccess;
   dim3 grid((ny - 1 + NT - 1) / NT, (nx - 1 + NT - 1) / NT);
   TMG_COUNT(1);
   return launch_pdl(prolong2_kernel, grid, dim3(256), 0, s, nx, ny, C, U,
-                    GroupSel2{scheme, fg0, fg1});
+                    GroupSel2{scheme, fg0, fg1}, skip_red);
 }
 
 }  // namespace tmg

@@ -273,9 +273,15 @@ __device__ __forceinline__ void restrict3_tile(const GridArgs& g, int full, cons
 constexpr int PC_E = NT / 2 + 1, PC_LD = PC_E + 1;
 
 // One 32 x 32 fine tile at (i0, j0) of the fused prolongation + correction
+// skip_red: the caller smooths next with the square tweed scheme, whose red
+// stage overwrites every red point (shell index max(i', j') odd,
+// layout.py:22-23, 75-84) without reading its old value — block Gauss-Seidel
+// solves all unknowns of a block from their out-of-block neighbours
+// (_ckernels.pyx:34-39) and same-colour blocks never touch —
+// so only the black points need the correction: half the fine traffic.
 __device__ __forceinline__ void prolong2_tile(int nx, int ny, const FieldView& C,
                                               const FieldView& U, const GroupSel2& fsel, int i0,
-                                              int j0, double* sc) {
+                                              int j0, double* sc, int skip_red = 0) {
   if (!box_in_groups(fsel, nx, ny, i0, j0, NT, NT)) {  // outside a rank's groups
     pdl_trigger();
     pdl_wait();
@@ -290,7 +296,7 @@ __device__ __forceinline__ void prolong2_tile(int nx, int ny, const FieldView& C
 #define TMG_PROLONG_FAST 1  // 0: every tile takes the generic per-point path
 #endif
   if (TMG_PROLONG_FAST && fsel.g0 <= 0 && own >= 0 && cown >= 0 && i0 + NT <= nx &&
-      j0 + NT <= ny) {
+      j0 + NT <= ny && (!skip_red || U.mode == LM_TWEED)) {
     // Interior tile owned by one buffer, coarse box by one buffer (nearly every
     // tile of a large level): one base pointer and a row stride, and — the tile
     // origin being odd — a thread's four points (rows w, w + 8, ...) share
@@ -300,11 +306,19 @@ __device__ __forceinline__ void prolong2_tile(int nx, int ny, const FieldView& C
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t ldr = T ? nx + 1 : ny + 1, l8 = 8 * ldr;
     double* up = (T ? U.t : U.n) + ((T ? j0 : i0) + w) * ldr + (T ? i0 : j0) + lane;
-    double uv[4];
+    // the rows of a single-owner tile of the tweed layout are shell rows (T owns
+    // i' < j', N the rest): row m of the owner buffer is shell min(m, n - m),
+    // and a thread's rows w, w + 8, ... share its parity (n is even)
+    const int mrow = (T ? j0 : i0) + w;
+    const bool skip = skip_red && (min(mrow, (T ? ny : nx) - mrow) & 1);
+    double uv[4] = {0.0, 0.0, 0.0, 0.0};
+    if (!skip) {
 #pragma unroll
-    for (int q = 0; q < 4; q++) uv[q] = up[q * l8];
+      for (int q = 0; q < 4; q++) uv[q] = up[q * l8];
+    }
     load_box<PC_E, PC_LD>(C, cown, Ic0, Jc0, sc);
     __syncthreads();
+    if (skip) return;
     const int cI = cown == 1 ? 1 : PC_LD, cJ = cown == 1 ? PC_LD : 1;
     const int di = T ? lane : w, dj = T ? w : lane;  // i - i0, j - j0 of the first point
     const bool i_even = di & 1, j_even = dj & 1;      // i0, j0 are odd
@@ -339,6 +353,7 @@ __device__ __forceinline__ void prolong2_tile(int nx, int ny, const FieldView& C
   for (int k = 0; k < 4; k++) {
     const int i = pi[k], j = pj[k];
     if (i >= nx || j >= ny || !in_groups(fsel, nx, ny, i, j)) continue;
+    if (skip_red && (point_group(4, nx, ny, i, j) & 1)) continue;
     const int I = i >> 1, J = j >> 1;
     const int o = (I - Ic0) * cI + (J - Jc0) * cJ;
     double pv;
