@@ -18,7 +18,7 @@ from paper_2110_08389_b200 import grid, mgcycle  # noqa: E402
 from paper_2110_08389_b200.rng import Lcg64  # noqa: E402
 
 out = {}
-for n, nu1, nu2 in ((64, 2, 2), (256, 2, 2), (256, 1, 1), (256, 2, 0), (1024, 2, 2), (2050, 2, 1)):
+for n, nu1, nu2 in ((64, 2, 2), (256, 2, 2), (256, 1, 1), (256, 2, 0), (1024, 2, 2), (2048, 2, 1)):
     x = grid.make_coords("wall", n, 1.0, 3.0)
     h = grid.build_hierarchy(x, x)
     rng = Lcg64(n)
