@@ -238,6 +238,59 @@ __global__ void __launch_bounds__(256, TMG_PROLONG_MINB) prolong2_kernel(int nx,
   prolong2_tile(nx, ny, C, U, fsel, 1 + blockIdx.y * NT, 1 + blockIdx.x * NT, sc, skip_red);
 }
 
+// ---- black-only prolongation + correction of square tweed levels (hybrid
+// layout): 64 x 64 fine points per CTA.  In a single-owner tile the rows of
+// the owner buffer are shell rows, the black ones are the even rows, and a
+// thread takes four of them in two column blocks: eight loads in flight per
+// thread where the 32 x 32 kernel with half of its warps idle has four.
+// Black rows have an even index across the rows, so only the two interpolation
+// classes of transfer.py:51-53 with that index even occur.  Same expressions
+// as prolong2_tile (bit-identical); other tiles go through it, 32 x 32 at a
+// time.
+constexpr int PB_E = 33, PB_LD = 34;
+__global__ void __launch_bounds__(256, 4) prolong_black_kernel(int nx, int ny, FieldView C,
+                                                             FieldView U) {
+  __shared__ double sc[PB_E * PB_LD];
+  const int i0 = 1 + blockIdx.y * 64, j0 = 1 + blockIdx.x * 64;
+  const int own = box_owner(U, i0, j0, 64, 64);
+  const int Ic0 = i0 >> 1, Jc0 = j0 >> 1;
+  pdl_trigger();
+  const int cown = box_owner(C, Ic0, Jc0, PB_E, PB_E);
+  if (!(own >= 0 && cown >= 0 && i0 + 64 <= nx && j0 + 64 <= ny)) {
+    for (int q = 0; q < 4; q++) {  // prolong2_tile waits for the predecessor itself
+      prolong2_tile(nx, ny, C, U, GroupSel2{0, 0, 0}, i0 + 32 * (q >> 1), j0 + 32 * (q & 1), sc, 1);
+      __syncthreads();
+    }
+    return;
+  }
+  pdl_wait();
+  const bool T = own == 1;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t ldr = T ? nx + 1 : ny + 1, l16 = 16 * ldr;
+  // black rows of the tile: offsets 1, 3, ..., 63 from its (odd) first row
+  double* up = (T ? U.t : U.n) + ((T ? j0 : i0) + 1 + 2 * w) * ldr + (T ? i0 : j0) + lane;
+  double uv[4][2];
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    uv[q][0] = up[q * l16];
+    uv[q][1] = up[q * l16 + 32];
+  }
+  load_box<PB_E, PB_LD>(C, cown, Ic0, Jc0, sc);
+  __syncthreads();
+  const int cI = cown == 1 ? 1 : PB_LD, cJ = cown == 1 ? PB_LD : 1;
+  const int cR = T ? cJ : cI, cA = T ? cI : cJ;  // coarse strides across / along the rows
+  const bool a_even = lane & 1;                   // the column index (i0, j0 are odd)
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+#pragma unroll
+    for (int hb = 0; hb < 2; hb++) {
+      const int o = (1 + w + 8 * q) * cR + (((1 + lane) >> 1) + 16 * hb) * cA;
+      const double pv = a_even ? sc[o] : __dmul_rn(0.5, __dadd_rn(sc[o], sc[o + cA]));
+      up[q * l16 + 32 * hb] = __dadd_rn(uv[q][hb], pv);
+    }
+  }
+}
+
 // ---- marching residual kernels (large levels) -----------------------------
 // A warp owns 64 consecutive points along its buffer's contiguous ("lane")
 // axis, two per lane, and marches along the other ("march") axis keeping a
@@ -563,6 +616,15 @@ cudaError_t launch_restrict2(const GridArgs& g, int full, const FieldView& U, co
 cudaError_t launch_prolong2(int nx, int ny, const FieldView& C, const FieldView& U,
                             cudaStream_t s, int scheme, int fg0, int fg1, int skip_red) {
   if (nx < 2 || ny < 2) return cudaSuccess;
+  static const int black64 = [] {
+    const char* e = std::getenv("TMG_PROLONG_BLACK64");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (skip_red && fg0 <= 0 && black64 && U.mode == LM_TWEED && nx >= 128) {
+    dim3 grid64((ny - 1 + 63) / 64, (nx - 1 + 63) / 64);
+    TMG_COUNT(1);
+    return launch_pdl(prolong_black_kernel, grid64, dim3(256), 0, s, nx, ny, C, U);
+  }
   dim3 grid((ny - 1 + NT - 1) / NT, (nx - 1 + NT - 1) / NT);
   TMG_COUNT(1);
   return launch_pdl(prolong2_kernel, grid, dim3(256), 0, s, nx, ny, C, U,
