@@ -620,7 +620,9 @@ cudaError_t launch_prolong2(int nx, int ny, const FieldView& C, const FieldView&
     const char* e = std::getenv("TMG_PROLONG_BLACK64");
     return e ? std::atoi(e) : 1;
   }();
-  if (skip_red && fg0 <= 0 && black64 && U.mode == LM_TWEED && nx >= 128) {
+  // small levels keep the 32 x 32 kernel: most of their tiles straddle the
+  // owner diagonals and would take the four-sub-tile path (config 1: +5 %)
+  if (skip_red && fg0 <= 0 && black64 && U.mode == LM_TWEED && nx >= 512) {
     dim3 grid64((ny - 1 + 63) / 64, (nx - 1 + 63) / 64);
     TMG_COUNT(1);
     return launch_pdl(prolong_black_kernel, grid64, dim3(256), 0, s, nx, ny, C, U);
